@@ -1,0 +1,54 @@
+"""Seeded synthetic workloads (BASELINE.json configs 1-5) -- inputs only.
+
+This module holds the parameters and seeds of the five configurations and the
+parameter-sweep layout.  It contains none of the method's arithmetic: every
+population is generated *from these seeds* by each side's own counter-based
+generator (DESIGN.md "Contract" R1-R8).  Both the CUDA path's tests/bench and
+the oracle's callers read it; neither side imports the other.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+# C1: wealth transfer, N = 1,000, w0 = 1, Philox seed 42, 100 steps (BJ config 1)
+C1_WEALTH_SMALL = dict(kind="wealth", n=1_000, w0=1, amount=1, exclude_self=0, seed=42,
+                       steps=100)
+
+# C2: SIR on G(n, M), N = 1e5, mean degree 10, 1% initially infected,
+# beta = 0.05, gamma = 0.1, 200 steps, seed 7 (BJ config 2)
+C2_SIR = dict(kind="sir", n=100_000, mean_degree=10.0, beta=0.05, gamma=0.1, init_frac=0.01,
+              seed=7, steps=200)
+
+# C3: Boids, N = 1e5 in a 1000 x 1000 periodic box, R = 10, r_s = 2,
+# weights (0.01, 0.125, 0.05), vmax 2, dt 1, 100 steps, seed 3 (BJ config 3)
+C3_BOIDS = dict(kind="boids", n=100_000, L=1000.0, R=10.0, rs=2.0, wc=0.01, wa=0.125, ws=0.05,
+                vmax=2.0, dt=1.0, seed=3, steps=100)
+
+# C4: wealth at scale, N = 1e8, seed 11, 1000 steps, sharded over 1/2/4/8 GPUs (BJ config 4)
+C4_WEALTH_SCALE = dict(kind="wealth", n=100_000_000, w0=1, amount=1, exclude_self=0, seed=11,
+                       steps=1_000)
+
+# C5: 4096 SIR replicates, N = 1e4, mean degree 8, 64 betas in [0.01, 0.2] x 64 seeds,
+# gamma = 0.1, 300 steps (BJ config 5)
+C5_SWEEP = dict(kind="sweep", n=10_000, mean_degree=8.0, gamma=0.1, init_frac=0.01, n_beta=64,
+                n_seed=64, beta_lo=0.01, beta_hi=0.2, steps=300)
+
+CONFIGS = {"c1": C1_WEALTH_SMALL, "c2": C2_SIR, "c3": C3_BOIDS, "c4": C4_WEALTH_SCALE,
+           "c5": C5_SWEEP}
+
+
+def sweep_replicates(cfg=C5_SWEEP):
+    """Contract S6: replicate r = n_seed*b + q (beta-major); beta_b equals
+    numpy.linspace(lo, hi, n_beta)[b]; seed_r = r.  Returns (betas, seeds)."""
+    betas_grid = np.linspace(cfg["beta_lo"], cfg["beta_hi"], cfg["n_beta"])
+    betas = np.repeat(betas_grid, cfg["n_seed"]).astype(np.float64)
+    seeds = np.arange(cfg["n_beta"] * cfg["n_seed"], dtype=np.uint64)
+    return betas, seeds
+
+
+def sir_counts(cfg):
+    """G1/S1 integer sizes: M = round(N*kbar/2), K = round(init_frac*N) (round half up)."""
+    n = cfg["n"]
+    m = int(np.floor(n * cfg["mean_degree"] / 2.0 + 0.5))
+    k = int(np.floor(cfg["init_frac"] * n + 0.5))
+    return m, k
