@@ -1,0 +1,14 @@
+"""paper_2601_16292_b200 -- B200-native hot path of AMBER (arXiv 2601.16292).
+
+The per-step, population-wide synchronous update of columnar agent state,
+as hand-written sm_100a CUDA kernels behind the C ABI in include/amber.h
+(libamber.so).  This package is the thin Python binding over that ABI; it
+never imports oracle/ and has no CPU fallback.
+"""
+from . import capi
+from .capi import AmberError
+from .model import (Model, boids_params, make_runtime, nccl_unique_id, sir_params, sweep,
+                    wealth_params)
+
+__all__ = ["capi", "AmberError", "Model", "wealth_params", "sir_params", "boids_params", "sweep",
+           "make_runtime", "nccl_unique_id"]

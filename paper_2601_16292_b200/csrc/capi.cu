@@ -1,0 +1,257 @@
+// capi.cu -- the extern "C" boundary declared in include/amber.h.
+// Every entry point converts internal exceptions into AMBER_E_* codes and a
+// thread-local message; no C++ exception crosses the ABI.
+#include <new>
+
+#include "internal.cuh"
+
+extern "C" int amber_nccl_unique_id_impl(void* out, size_t out_bytes);
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f)
+{
+    try {
+        g_last_error.clear();
+        return f();
+    } catch (const amber::Error& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return AMBER_E_OOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return AMBER_E_INVALID_ARG;
+    } catch (...) {
+        g_last_error = "unknown internal error";
+        return AMBER_E_INVALID_ARG;
+    }
+}
+
+amber::Model* impl(amber_model* m)
+{
+    if (!m || !m->impl) amber::fail(AMBER_E_INVALID_ARG, "NULL model");
+    return m->impl;
+}
+
+void need(const void* p, const char* what)
+{
+    if (!p) amber::fail(AMBER_E_INVALID_ARG, std::string("NULL ") + what);
+}
+
+}  // namespace
+
+extern "C" {
+
+int amber_version(void) { return AMBER_ABI_VERSION; }
+
+const char* amber_last_error(void) { return g_last_error.c_str(); }
+
+int amber_model_create(amber_kind kind, int64_t n_agents, const void* params, size_t params_size, uint64_t seed,
+                       const amber_runtime* rt, amber_model** out)
+{
+    return guarded([&] {
+        need(out, "out");
+        *out = nullptr;
+        need(params, "params");
+        AMBER_REQUIRE(n_agents >= 1, "n_agents must be >= 1");
+        if (rt && rt->world > 1 && kind != AMBER_WEALTH)
+            amber::fail(AMBER_E_UNSUPPORTED, "only AMBER_WEALTH is sharded across ranks (others: replicas/amber_sweep)");
+        amber::Model* m = nullptr;
+        switch (kind) {
+            case AMBER_WEALTH:
+                AMBER_REQUIRE(params_size >= sizeof(amber_wealth_params), "params_size < sizeof(amber_wealth_params)");
+                m = amber::make_wealth(n_agents, *static_cast<const amber_wealth_params*>(params), seed, rt);
+                break;
+            case AMBER_SIR_GRAPH:
+                AMBER_REQUIRE(params_size >= sizeof(amber_sir_params), "params_size < sizeof(amber_sir_params)");
+                m = amber::make_sir(n_agents, *static_cast<const amber_sir_params*>(params), seed, rt);
+                break;
+            case AMBER_BOIDS:
+                AMBER_REQUIRE(params_size >= sizeof(amber_boids_params), "params_size < sizeof(amber_boids_params)");
+                m = amber::make_boids(n_agents, *static_cast<const amber_boids_params*>(params), seed, rt);
+                break;
+            default:
+                amber::fail(AMBER_E_UNKNOWN_KIND, "unknown amber_kind " + std::to_string(static_cast<int>(kind)));
+        }
+        *out = new amber_model{m};
+        return 0;
+    });
+}
+
+int amber_model_destroy(amber_model* m)
+{
+    return guarded([&] {
+        if (!m) return 0;
+        delete m->impl;
+        delete m;
+        return 0;
+    });
+}
+
+int amber_step(amber_model* m, int64_t n_steps)
+{
+    return guarded([&] {
+        impl(m)->step(n_steps);
+        return 0;
+    });
+}
+
+int amber_synchronize(amber_model* m)
+{
+    return guarded([&] {
+        impl(m)->synchronize();
+        return 0;
+    });
+}
+
+int amber_step_count(amber_model* m, int64_t* out)
+{
+    return guarded([&] {
+        need(out, "out");
+        *out = impl(m)->t;
+        return 0;
+    });
+}
+
+int amber_set_step(amber_model* m, int64_t step)
+{
+    return guarded([&] {
+        impl(m)->set_step(step);
+        return 0;
+    });
+}
+
+int amber_column_info(amber_model* m, const char* name, amber_dtype* dtype, int64_t* global_len, int64_t* local_off,
+                      int64_t* local_len)
+{
+    return guarded([&] {
+        need(name, "name");
+        if (!impl(m)->column_info(name, dtype, global_len, local_off, local_len))
+            amber::fail(AMBER_E_UNKNOWN_NAME, std::string("no column ") + name);
+        return 0;
+    });
+}
+
+int amber_read_column(amber_model* m, const char* name, void* dst, size_t dst_bytes, int dst_on_device)
+{
+    return guarded([&] {
+        need(name, "name");
+        need(dst, "dst");
+        impl(m)->read_column(name, dst, dst_bytes, dst_on_device != 0);
+        return 0;
+    });
+}
+
+int amber_write_column(amber_model* m, const char* name, const void* src, size_t src_bytes, int src_on_device)
+{
+    return guarded([&] {
+        need(name, "name");
+        need(src, "src");
+        impl(m)->write_column(name, src, src_bytes, src_on_device != 0);
+        return 0;
+    });
+}
+
+int amber_read_metrics(amber_model* m, const char* name, void* dst, size_t dst_bytes, int64_t* n_out)
+{
+    return guarded([&] {
+        need(name, "name");
+        need(dst, "dst");
+        impl(m)->read_metrics(name, dst, dst_bytes, n_out);
+        return 0;
+    });
+}
+
+int amber_reset_metrics(amber_model* m)
+{
+    return guarded([&] {
+        impl(m)->reset_metrics();
+        return 0;
+    });
+}
+
+int amber_digest(amber_model* m, const char* name, uint64_t* out)
+{
+    return guarded([&] {
+        need(name, "name");
+        need(out, "out");
+        *out = impl(m)->digest(name);
+        return 0;
+    });
+}
+
+int amber_set_option(amber_model* m, const char* key, int64_t value)
+{
+    return guarded([&] {
+        need(key, "key");
+        if (!impl(m)->set_option(key, value)) amber::fail(AMBER_E_UNKNOWN_NAME, std::string("no option ") + key);
+        return 0;
+    });
+}
+
+int amber_get_option(amber_model* m, const char* key, int64_t* value)
+{
+    return guarded([&] {
+        need(key, "key");
+        need(value, "value");
+        if (!impl(m)->get_option(key, value)) amber::fail(AMBER_E_UNKNOWN_NAME, std::string("no option ") + key);
+        return 0;
+    });
+}
+
+int amber_profile_enable(amber_model* m, int enable)
+{
+    return guarded([&] {
+        amber::Model* x = impl(m);
+        AMBER_CUDA(cudaStreamSynchronize(x->rt.stream));
+        x->prof.enable(enable != 0);
+        return 0;
+    });
+}
+
+int amber_profile_query(amber_model* m, int idx, char* name, size_t name_cap, int64_t* launches, double* total_ms)
+{
+    return guarded([&] {
+        need(launches, "launches");
+        need(total_ms, "total_ms");
+        std::string nm;
+        if (!impl(m)->prof.query(idx, &nm, launches, total_ms))
+            amber::fail(AMBER_E_INVALID_ARG, "profile index out of range");
+        if (name && name_cap) {
+            std::strncpy(name, nm.c_str(), name_cap - 1);
+            name[name_cap - 1] = 0;
+        }
+        return 0;
+    });
+}
+
+int amber_sweep(amber_kind kind, int64_t n_agents, const void* base_params, size_t params_size,
+                const amber_replicate* reps, int64_t n_reps, int64_t n_steps, const amber_runtime* rt,
+                double* out_final_r_frac, amber_sweep_stats* stats)
+{
+    return guarded([&] {
+        if (kind != AMBER_SIR_GRAPH) amber::fail(AMBER_E_UNKNOWN_KIND, "amber_sweep supports AMBER_SIR_GRAPH only");
+        need(base_params, "base_params");
+        AMBER_REQUIRE(params_size >= sizeof(amber_sir_params), "params_size < sizeof(amber_sir_params)");
+        AMBER_REQUIRE(n_reps >= 0 && n_steps >= 0 && n_agents >= 2, "bad sweep sizes");
+        if (n_reps) {
+            need(reps, "reps");
+            need(out_final_r_frac, "out_final_r_frac");
+        }
+        amber::run_sweep(n_agents, *static_cast<const amber_sir_params*>(base_params), reps, n_reps, n_steps, rt,
+                         out_final_r_frac, stats);
+        return 0;
+    });
+}
+
+int amber_nccl_unique_id(void* out, size_t out_bytes)
+{
+    return guarded([&] { return amber_nccl_unique_id_impl(out, out_bytes); });
+}
+
+}  // extern "C"

@@ -1,0 +1,210 @@
+// dist.cu -- multi-GPU plumbing over NCCL (NVLink 5 / NVSwitch).
+//
+// One process per GPU.  libnccl.so.2 is loaded at run time (dlopen) so the
+// library binds to the SAME NCCL the process's PyTorch uses (the binding sets
+// AMBER_NCCL_LIB to torch's bundled copy); the communicator is our own,
+// created from a unique id that rank 0 makes (amber_nccl_unique_id) and the
+// caller broadcasts (e.g. torch.distributed.broadcast_object_list).
+//
+// Wealth sharding: agents are split in contiguous id
+// ranges; each step the scatter kernel buckets cross-shard receivers per
+// destination rank, this file exchanges the bucket sizes (all-to-all of one
+// count per peer) and then the ids (grouped ncclSend/ncclRecv), and the
+// receive kernel adds them to the owner's counters.
+#include <dlfcn.h>
+
+#include <mutex>
+
+#include "internal.cuh"
+#include "nccl.h"
+
+namespace amber {
+
+namespace {
+
+struct NcclApi {
+    void* handle = nullptr;
+    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+    decltype(&ncclAllReduce) AllReduce = nullptr;
+    decltype(&ncclAllGather) AllGather = nullptr;
+    decltype(&ncclSend) Send = nullptr;
+    decltype(&ncclRecv) Recv = nullptr;
+    decltype(&ncclGroupStart) GroupStart = nullptr;
+    decltype(&ncclGroupEnd) GroupEnd = nullptr;
+    std::string error;
+};
+
+NcclApi& nccl()
+{
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* path = getenv("AMBER_NCCL_LIB");
+        api.handle = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!api.handle) {
+            api.error = std::string("dlopen NCCL failed: ") + dlerror();
+            return;
+        }
+#define AMBER_SYM(field, sym)                                                      \
+    api.field = reinterpret_cast<decltype(api.field)>(dlsym(api.handle, #sym));    \
+    if (!api.field) api.error = "NCCL symbol missing: " #sym;
+        AMBER_SYM(GetUniqueId, ncclGetUniqueId)
+        AMBER_SYM(CommInitRank, ncclCommInitRank)
+        AMBER_SYM(CommDestroy, ncclCommDestroy)
+        AMBER_SYM(GetErrorString, ncclGetErrorString)
+        AMBER_SYM(AllReduce, ncclAllReduce)
+        AMBER_SYM(AllGather, ncclAllGather)
+        AMBER_SYM(Send, ncclSend)
+        AMBER_SYM(Recv, ncclRecv)
+        AMBER_SYM(GroupStart, ncclGroupStart)
+        AMBER_SYM(GroupEnd, ncclGroupEnd)
+#undef AMBER_SYM
+    });
+    if (!api.error.empty()) fail(AMBER_E_NCCL, api.error);
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what)
+{
+    if (r != ncclSuccess) fail(AMBER_E_NCCL, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- communicator
+struct Comm {
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+};
+
+Comm* make_comm(const amber_runtime* r)
+{
+    AMBER_REQUIRE(r && r->world > 1 && r->nccl_unique_id, "world > 1 needs amber_runtime.nccl_unique_id");
+    NcclApi& api = nccl();
+    ncclUniqueId id;
+    std::memcpy(&id, r->nccl_unique_id, sizeof(id));
+    auto* c = new Comm;
+    c->rank = r->rank;
+    c->world = r->world;
+    AMBER_CUDA(cudaSetDevice(r->device));
+    ncclResult_t res = api.CommInitRank(&c->comm, r->world, id, r->rank);
+    if (res != ncclSuccess) {
+        delete c;
+        nccl_check(res, "ncclCommInitRank");
+    }
+    return c;
+}
+
+void destroy_comm(Comm* c)
+{
+    if (!c) return;
+    if (c->comm) nccl().CommDestroy(c->comm);
+    delete c;
+}
+
+void comm_allreduce_u64(Comm* c, cudaStream_t s, unsigned long long* d, size_t n)
+{
+    nccl_check(nccl().AllReduce(d, d, n, ncclUint64, ncclSum, c->comm, s), "ncclAllReduce");
+}
+
+void comm_allgather_f64(Comm* c, cudaStream_t s, const double* send, double* recv, size_t n_per_rank)
+{
+    nccl_check(nccl().AllGather(send, recv, n_per_rank, ncclFloat64, c->comm, s), "ncclAllGather");
+}
+
+// ---------------------------------------------------------------- wealth exchange
+struct WealthExchange {
+    Comm* comm = nullptr;
+    DevBuf<unsigned int> send_counts_copy, recv_counts;
+    std::vector<unsigned int> h_send, h_recv;
+    DevBuf<unsigned long long> flag;
+};
+
+WealthExchange* make_wealth_exchange_rt(Runtime& rt, const amber_runtime* r)
+{
+    auto* x = new WealthExchange;
+    x->comm = make_comm(r);
+    x->send_counts_copy.allocate(&rt, rt.world);
+    x->recv_counts.allocate(&rt, rt.world);
+    x->flag.allocate(&rt, 1);
+    x->h_send.assign(rt.world, 0);
+    x->h_recv.assign(rt.world, 0);
+    return x;
+}
+
+void destroy_wealth_exchange(WealthExchange* x)
+{
+    if (!x) return;
+    destroy_comm(x->comm);
+    x->send_counts_copy.reset();
+    x->recv_counts.reset();
+    x->flag.reset();
+    delete x;
+}
+
+// Ship bucketed receivers to their owner ranks.  d_recv_total receives the
+// number of ids written contiguously into d_recv_ids.
+void wealth_exchange_run(WealthExchange* x, Runtime& rt, const unsigned int* d_send_counts,
+                         const uint32_t* d_send_ids, uint64_t send_cap, uint32_t* d_recv_ids,
+                         unsigned long long* d_recv_total)
+{
+    NcclApi& api = nccl();
+    const int W = x->comm->world, me = x->comm->rank;
+    // 1) sizes: one count to each peer
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    for (int p = 0; p < W; ++p) {
+        nccl_check(api.Send(d_send_counts + p, 1, ncclUint32, p, x->comm->comm, rt.stream), "ncclSend(count)");
+        nccl_check(api.Recv(x->recv_counts.p + p, 1, ncclUint32, p, x->comm->comm, rt.stream), "ncclRecv(count)");
+    }
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+    AMBER_CUDA(cudaMemcpyAsync(x->h_send.data(), d_send_counts, W * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                               rt.stream));
+    AMBER_CUDA(cudaMemcpyAsync(x->h_recv.data(), x->recv_counts.p, W * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                               rt.stream));
+    AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    // 2) payload: grouped point-to-point, received contiguously in peer order
+    unsigned long long total = 0;
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    for (int p = 0; p < W; ++p) {
+        if (p == me) continue;
+        const unsigned long long ns = std::min<unsigned long long>(x->h_send[p], send_cap);
+        if (x->h_send[p] > send_cap) fail(AMBER_E_CUDA, "wealth exchange: send bucket overflow");
+        if (ns) nccl_check(api.Send(d_send_ids + p * send_cap, ns, ncclUint32, p, x->comm->comm, rt.stream), "ncclSend");
+        if (x->h_recv[p])
+            nccl_check(api.Recv(d_recv_ids + total, x->h_recv[p], ncclUint32, p, x->comm->comm, rt.stream), "ncclRecv");
+        total += x->h_recv[p];
+    }
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+    AMBER_CUDA(cudaMemcpyAsync(d_recv_total, &total, sizeof(total), cudaMemcpyHostToDevice, rt.stream));
+    AMBER_CUDA(cudaStreamSynchronize(rt.stream));  // `total` lives on this host stack frame
+}
+
+bool wealth_exchange_any(WealthExchange* x, Runtime& rt, bool local_flag)
+{
+    unsigned long long v = local_flag ? 1ull : 0ull;
+    AMBER_CUDA(cudaMemcpyAsync(x->flag.p, &v, 8, cudaMemcpyHostToDevice, rt.stream));
+    comm_allreduce_u64(x->comm, rt.stream, x->flag.p, 1);
+    AMBER_CUDA(cudaMemcpyAsync(&v, x->flag.p, 8, cudaMemcpyDeviceToHost, rt.stream));
+    AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    return v != 0;
+}
+
+void wealth_exchange_allreduce_u64(WealthExchange* x, Runtime& rt, unsigned long long* d_vals, int n)
+{
+    comm_allreduce_u64(x->comm, rt.stream, d_vals, static_cast<size_t>(n));
+}
+
+}  // namespace amber
+
+extern "C" int amber_nccl_unique_id_impl(void* out, size_t out_bytes)
+{
+    using namespace amber;
+    AMBER_REQUIRE(out && out_bytes >= sizeof(ncclUniqueId), "amber_nccl_unique_id needs a 128-byte buffer");
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out, &id, sizeof(id));
+    return 0;
+}

@@ -1,0 +1,238 @@
+// internal.cuh -- shared host/device infrastructure of libamber.so (product path).
+// Errors, runtime binding (device, stream, allocator hooks), RAII device
+// buffers, per-kernel CUDA-event profiler, the model interface, and small
+// device reduction helpers.  Nothing here is shared with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "amber.h"
+
+namespace amber {
+
+// ---------------------------------------------------------------- errors
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+#define AMBER_CUDA(call)                                                                   \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            ::amber::fail(e_ == cudaErrorMemoryAllocation ? AMBER_E_OOM : AMBER_E_CUDA,    \
+                          std::string(#call) + " -> " + cudaGetErrorString(e_) + " (" +   \
+                              __FILE__ + ":" + std::to_string(__LINE__) + ")");            \
+    } while (0)
+
+#define AMBER_REQUIRE(cond, msg)                                                  \
+    do {                                                                          \
+        if (!(cond)) ::amber::fail(AMBER_E_INVALID_ARG, std::string(msg));        \
+    } while (0)
+
+// Check the last launch (launch-config errors surface here, faults later).
+inline void check_launch(const char* what)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fail(AMBER_E_CUDA, std::string("launch ") + what + ": " + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------- runtime
+struct Runtime {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    amber_alloc_fn alloc = nullptr;
+    amber_free_fn release = nullptr;
+    void* ctx = nullptr;
+    int rank = 0, world = 1;
+    int num_sms = 148;
+
+    void init(const amber_runtime* rt);
+    void destroy();
+    void* alloc_bytes(size_t bytes);
+    void free_bytes(void* p, size_t bytes);
+};
+
+// RAII device buffer allocated through the runtime's allocator.
+template <class T>
+struct DevBuf {
+    Runtime* rt = nullptr;
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { reset(); }
+    void allocate(Runtime* r, size_t count)
+    {
+        reset();
+        rt = r;
+        n = count;
+        p = count ? static_cast<T*>(rt->alloc_bytes(count * sizeof(T))) : nullptr;
+    }
+    void reset()
+    {
+        if (p && rt) rt->free_bytes(p, n * sizeof(T));
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+    void zero_async(cudaStream_t s)
+    {
+        if (p) AMBER_CUDA(cudaMemsetAsync(p, 0, bytes(), s));
+    }
+};
+
+// ---------------------------------------------------------------- profiler
+// Records a CUDA event pair around every launch of a named kernel while
+// enabled (on the launching stream), so per-kernel device time can be read
+// back without an external profiler.
+struct Profiler {
+    bool on = false;
+    struct Kernel {
+        std::string name;
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    };
+    std::vector<Kernel> kernels;
+    std::vector<cudaEvent_t> pool;
+
+    cudaEvent_t get_event();
+    void clear();
+    void enable(bool v) { clear(); on = v; }
+    template <class F>
+    void launch(cudaStream_t s, const char* name, F&& f)
+    {
+        if (!on) {
+            f();
+            return;
+        }
+        cudaEvent_t a = get_event(), b = get_event();
+        AMBER_CUDA(cudaEventRecord(a, s));
+        f();
+        AMBER_CUDA(cudaEventRecord(b, s));
+        Kernel* k = nullptr;
+        for (auto& kk : kernels)
+            if (kk.name == name) k = &kk;
+        if (!k) {
+            kernels.push_back(Kernel{name, {}});
+            k = &kernels.back();
+        }
+        k->ev.emplace_back(a, b);
+    }
+    bool query(int idx, std::string* name, int64_t* launches, double* total_ms);
+    ~Profiler();
+};
+
+// ---------------------------------------------------------------- model base
+struct Model {
+    Runtime rt;
+    Profiler prof;
+    int64_t t = 0;  // step index of the current state
+    int64_t block = 0, grid = 0, persistent = 1, digest_on = 0, metrics_cap = 4096;
+
+    virtual ~Model() = default;
+    virtual void step(int64_t n) = 0;
+    virtual void synchronize() { AMBER_CUDA(cudaStreamSynchronize(rt.stream)); }
+    virtual bool column_info(const char* name, amber_dtype* dt, int64_t* glen, int64_t* off,
+                             int64_t* len) = 0;
+    virtual void read_column(const char* name, void* dst, size_t bytes, bool on_dev) = 0;
+    virtual void write_column(const char* name, const void* src, size_t bytes, bool on_dev) = 0;
+    virtual void read_metrics(const char* name, void* dst, size_t bytes, int64_t* n_out) = 0;
+    virtual void reset_metrics() = 0;
+    virtual uint64_t digest(const char* name) = 0;
+    virtual void set_step(int64_t s) = 0;
+    virtual bool set_option(const char* key, int64_t v);
+    virtual bool get_option(const char* key, int64_t* v);
+};
+
+// Factories (one per kind, defined in the kind's .cu file).
+Model* make_wealth(int64_t n, const amber_wealth_params& p, uint64_t seed, const amber_runtime* rt);
+Model* make_sir(int64_t n, const amber_sir_params& p, uint64_t seed, const amber_runtime* rt);
+Model* make_boids(int64_t n, const amber_boids_params& p, uint64_t seed, const amber_runtime* rt);
+void run_sweep(int64_t n, const amber_sir_params& base, const amber_replicate* reps,
+               int64_t n_reps, int64_t n_steps, const amber_runtime* rt, double* out,
+               amber_sweep_stats* stats);
+
+// Copy helper for column I/O (host or device endpoint), on the model stream.
+void copy_out(Runtime& rt, void* dst, const void* src, size_t bytes, bool dst_on_dev);
+void copy_in(Runtime& rt, void* dst, const void* src, size_t bytes, bool src_on_dev);
+
+// Metric read helper: copy the valid window of a device ring (oldest first).
+template <class T>
+void read_ring(Runtime& rt, const T* ring, int64_t cap, int64_t first, int64_t end, void* dst,
+               size_t bytes, int64_t* n_out);
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_sum_f64(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide sum of K 64-bit counters; thread 0 adds them atomically to out[k].
+// All threads of the block must call it.  blockDim.x must be a multiple of 32.
+template <int K>
+__device__ __forceinline__ void block_sum_atomic(unsigned long long (&v)[K],
+                                                 unsigned long long* const (&out)[K])
+{
+    __shared__ unsigned long long red[K][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        unsigned long long s = warp_sum_u64(v[k]);
+        if (lane == 0) red[k][wid] = s;
+    }
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            unsigned long long s = lane < nw ? red[k][lane] : 0ull;
+            s = warp_sum_u64(s);
+            if (lane == 0 && out[k] && s) atomicAdd(out[k], s);
+        }
+    }
+    __syncthreads();
+}
+
+// splitmix64 finaliser; D1 digest term for (id, 32-bit pattern).
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z)
+{
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ unsigned long long digest_term(unsigned long long id, uint32_t bits)
+{
+    return mix64((id << 32) ^ (unsigned long long)bits);
+}
+
+// Digest of a 32-bit or 8-bit column (generic reduction kernel launcher).
+uint64_t device_digest_u32(Runtime& rt, const uint32_t* col, int64_t n, int64_t id0);
+uint64_t device_digest_u8(Runtime& rt, const uint8_t* col, int64_t n, int64_t id0);
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace amber
+
+struct amber_model {
+    amber::Model* impl;
+};

@@ -1,0 +1,645 @@
+// wealth.cu -- wealth-transfer model (Sec. 5.1.1; W1-W3).
+//
+// One fused kernel per step.  Launch t:
+//   apply   step t  : w'_i = w_i - a*s_i + a*c_i,  c_i = counter i of step t (read + zeroed)
+//   scatter step t+1: s'_i = [w'_i >= a], r_i = Philox receiver, counter[r_i] += 1
+// so each step streams the int32 wealth column once in and once out (8 B per
+// agent) while the per-receiver counters of steps t and t+1 (packed 4-bit by
+// default: 2 x N/2 bytes) stay in L2 and take the scatter as L2 atomics.
+// A counter overflow is detected exactly (sum of decoded counters != number of
+// increments) and the affected step window is replayed with 32-bit counters
+// from a pinned copy of the window's first state (3 rotating wealth buffers).
+#include <algorithm>
+
+#include "internal.cuh"
+#include "philox.cuh"
+
+namespace amber {
+
+namespace {
+
+constexpr int kQPT = 4;                  // quads (4 agents) per thread per chunk
+constexpr int kChunkAgents = 4 * kQPT * 32;  // agents per warp chunk (512)
+
+struct Slot {  // per-step record (ring slot), all 64-bit for atomics
+    unsigned long long total, active, digest, sent, got;
+};
+
+struct WealthArgs {
+    PhiloxKey key;
+    const int32_t* w_in;
+    int32_t* w_out;
+    uint32_t* inc_cur;   // counters of the applied step (read + zeroed)
+    uint32_t* inc_next;  // counters of the scattered step (atomics)
+    int64_t nchunks;     // warp chunks (kChunkAgents agents each) of the padded shard
+    int64_t n_loc;       // real agents in this shard
+    unsigned long long lo;      // global id of local agent 0
+    unsigned long long n_glob;  // N
+    int32_t amount;
+    int32_t exclude_self;
+    uint32_t t_apply, t_scatter;
+    Slot* slot_apply;    // record of the applied step
+    Slot* slot_scatter;  // record receiving the scattered step's increment count
+    Slot* slot_zero;     // slot zeroed at kernel start (two steps ahead), may be null
+    // cross-shard receivers (REMOTE): bucket per destination rank
+    int world;
+    unsigned long long shard_size;
+    uint32_t* remote_ids;             // [world][remote_cap] global receiver ids
+    unsigned int* remote_count;       // [world]
+    unsigned long long remote_cap;
+};
+
+// ---- packed counters: 4 agents (a quad) own 4*B contiguous bits ----
+template <int B>
+__device__ __forceinline__ void load_quad_counts(const uint32_t* inc, int64_t q, uint32_t c[4])
+{
+    if constexpr (B == 2) {
+        const uint32_t v = reinterpret_cast<const uint8_t*>(inc)[q];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c[k] = (v >> (2 * k)) & 3u;
+    } else if constexpr (B == 4) {
+        const uint32_t v = reinterpret_cast<const uint16_t*>(inc)[q];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c[k] = (v >> (4 * k)) & 15u;
+    } else if constexpr (B == 8) {
+        const uint32_t v = inc[q];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c[k] = (v >> (8 * k)) & 255u;
+    } else if constexpr (B == 16) {
+        const uint2 v = reinterpret_cast<const uint2*>(inc)[q];
+        c[0] = v.x & 0xFFFFu; c[1] = v.x >> 16; c[2] = v.y & 0xFFFFu; c[3] = v.y >> 16;
+    } else {
+        const uint4 v = reinterpret_cast<const uint4*>(inc)[q];
+        c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w;
+    }
+}
+
+template <int B>
+__device__ __forceinline__ void zero_quad_counts(uint32_t* inc, int64_t q)
+{
+    if constexpr (B == 2) reinterpret_cast<uint8_t*>(inc)[q] = 0;
+    else if constexpr (B == 4) reinterpret_cast<uint16_t*>(inc)[q] = 0;
+    else if constexpr (B == 8) inc[q] = 0u;
+    else if constexpr (B == 16) reinterpret_cast<uint2*>(inc)[q] = make_uint2(0u, 0u);
+    else reinterpret_cast<uint4*>(inc)[q] = make_uint4(0u, 0u, 0u, 0u);
+}
+
+template <int B>
+__device__ __forceinline__ void add_count(uint32_t* inc, unsigned long long rl)
+{
+    if constexpr (B == 32) {
+        atomicAdd(inc + rl, 1u);
+    } else {
+        constexpr int per = 32 / B;
+        atomicAdd(inc + (rl / per), 1u << ((rl % per) * B));
+    }
+}
+
+__device__ __forceinline__ unsigned long long receiver(unsigned long long x, unsigned long long i,
+                                                       unsigned long long n, int exclude_self)
+{
+    const unsigned long long m = exclude_self ? n - 1 : n;
+    unsigned long long r = (m >> 32) ? mulhi64(x, m) : mulhi64_n32(x, static_cast<uint32_t>(m));
+    if (exclude_self) r += (r >= i);
+    return r;
+}
+
+// Warp-aggregated append of a cross-shard receiver into its destination bucket.
+// Must be reached by all 32 lanes (flag selects the participating ones).
+__device__ __forceinline__ void remote_append(const WealthArgs& a, bool flag, unsigned long long r)
+{
+    const unsigned mask = __ballot_sync(0xffffffffu, flag);
+    if (!flag) return;
+    unsigned long long d = r / a.shard_size;
+    const unsigned dest = static_cast<unsigned>(d < static_cast<unsigned long long>(a.world) ? d : a.world - 1);
+    const unsigned peers = __match_any_sync(mask, dest);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    const unsigned rank = __popc(peers & ((1u << lane) - 1u));
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(a.remote_count + dest, static_cast<unsigned>(__popc(peers)));
+    base = __shfl_sync(peers, base, leader);
+    const unsigned long long pos = base + rank;
+    if (pos < a.remote_cap) a.remote_ids[dest * a.remote_cap + pos] = static_cast<uint32_t>(r);
+}
+
+template <int B, bool APPLY, bool SCATTER, bool DIGEST, bool REMOTE>
+__global__ void __launch_bounds__(256) wealth_step_kernel(const WealthArgs a)
+{
+    if (a.slot_zero && blockIdx.x == 0 && threadIdx.x == 0) *a.slot_zero = Slot{0, 0, 0, 0, 0};
+
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    unsigned long long tot = 0, act = 0, sent = 0, got = 0, dig = 0;
+
+    for (int64_t chunk = warp; chunk < a.nchunks; chunk += nwarps) {
+        int4 w[kQPT];
+        uint32_t c[kQPT][4];
+#pragma unroll
+        for (int j = 0; j < kQPT; ++j) {
+            const int64_t q = (chunk * kQPT + j) * 32 + lane;
+            w[j] = __ldcs(reinterpret_cast<const int4*>(a.w_in) + q);  // streaming: evict-first
+            if constexpr (APPLY) load_quad_counts<B>(a.inc_cur, q, c[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < kQPT; ++j) {
+            const int64_t q = (chunk * kQPT + j) * 32 + lane;
+            int32_t v[4] = {w[j].x, w[j].y, w[j].z, w[j].w};
+            if constexpr (APPLY) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int32_t s = v[k] >= a.amount ? a.amount : 0;
+                    v[k] = v[k] - s + a.amount * static_cast<int32_t>(c[j][k]);
+                    got += c[j][k];
+                }
+                __stcs(reinterpret_cast<int4*>(a.w_out) + q, make_int4(v[0], v[1], v[2], v[3]));
+                zero_quad_counts<B>(a.inc_cur, q);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    tot += static_cast<unsigned long long>(static_cast<long long>(v[k]));
+                    act += v[k] > 0;
+                    if constexpr (DIGEST) {
+                        const int64_t loc = 4 * q + k;
+                        if (loc < a.n_loc)
+                            dig += digest_term(a.lo + static_cast<unsigned long long>(loc),
+                                               static_cast<uint32_t>(v[k]));
+                    }
+                }
+            }
+            if constexpr (SCATTER) {
+                const unsigned long long i0 = a.lo + 4ull * static_cast<unsigned long long>(q);
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const bool s0 = v[2 * p] >= a.amount, s1 = v[2 * p + 1] >= a.amount;
+                    uint4 x = make_uint4(0u, 0u, 0u, 0u);
+                    if (s0 || s1) x = stream_block(a.key, TAG_WEALTH_RECV, (i0 >> 1) + p, a.t_scatter);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const bool s = h ? s1 : s0;
+                        const unsigned long long i = i0 + 2 * p + h;
+                        const unsigned long long r = receiver(lane64_of(x, h), i, a.n_glob, a.exclude_self);
+                        const unsigned long long rl = r - a.lo;
+                        const bool local = s && rl < static_cast<unsigned long long>(a.n_loc);
+                        if (local) {
+                            add_count<B>(a.inc_next, rl);
+                            sent += 1;
+                        }
+                        if constexpr (REMOTE) remote_append(a, s && !local, r);
+                    }
+                }
+            }
+        }
+    }
+
+    unsigned long long vals[5] = {tot, act, dig, sent, got};
+    unsigned long long* const outs[5] = {
+        APPLY ? &a.slot_apply->total : nullptr, APPLY ? &a.slot_apply->active : nullptr,
+        (APPLY && DIGEST) ? &a.slot_apply->digest : nullptr, SCATTER ? &a.slot_scatter->sent : nullptr,
+        APPLY ? &a.slot_apply->got : nullptr};
+    block_sum_atomic<5>(vals, outs);
+}
+
+// Received cross-shard receivers -> local counters of the scattered step.
+template <int B>
+__global__ void wealth_recv_kernel(const uint32_t* __restrict__ ids, const unsigned long long* __restrict__ n_ids,
+                                   unsigned long long lo, uint32_t* inc, Slot* slot)
+{
+    const unsigned long long n = *n_ids;
+    unsigned long long cnt = 0;
+    for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < n;
+         k += (unsigned long long)gridDim.x * blockDim.x) {
+        add_count<B>(inc, static_cast<unsigned long long>(ids[k]) - lo);
+        cnt += 1;
+    }
+    unsigned long long vals[1] = {cnt};
+    unsigned long long* const outs[1] = {&slot->sent};
+    block_sum_atomic<1>(vals, outs);
+}
+
+__global__ void wealth_fill_kernel(int32_t* w, int64_t n_loc, int64_t n_pad, int32_t w0)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pad; i += (int64_t)gridDim.x * blockDim.x)
+        w[i] = i < n_loc ? w0 : 0;
+}
+
+__global__ void zero_slots_kernel(Slot* ring, int64_t cap, int64_t s0, int64_t count)
+{
+    for (int64_t k = threadIdx.x; k < count; k += blockDim.x) ring[(s0 + k) % cap] = Slot{0, 0, 0, 0, 0};
+}
+
+}  // namespace
+
+// Host side of the cross-shard exchange (defined in dist.cu).
+struct WealthExchange;
+WealthExchange* make_wealth_exchange_rt(Runtime& rt, const amber_runtime* r);
+void wealth_exchange_run(WealthExchange* x, Runtime& rt, const unsigned int* d_send_counts,
+                         const uint32_t* d_send_ids, uint64_t send_cap, uint32_t* d_recv_ids,
+                         unsigned long long* d_recv_total);
+bool wealth_exchange_any(WealthExchange* x, Runtime& rt, bool local_flag);
+void wealth_exchange_allreduce_u64(WealthExchange* x, Runtime& rt, unsigned long long* d_vals, int n);
+void destroy_wealth_exchange(WealthExchange* x);
+
+class WealthModel final : public Model {
+public:
+    int64_t n = 0, lo = 0, hi = 0, n_loc = 0, n_pad = 0, shard = 0;
+    amber_wealth_params p{};
+    uint64_t seed = 0;
+    PhiloxKey key{};
+    int B = 4;
+    DevBuf<int32_t> wb[3];
+    int cur = 0, pinned = -1;
+    DevBuf<uint32_t> inc[2], inc32[2];
+    bool pending = false;
+    int64_t win_start = -1;
+    DevBuf<Slot> ring;
+    int64_t m_first = 0, replays = 0;
+    // cross-shard exchange (world > 1)
+    WealthExchange* xch = nullptr;
+    DevBuf<uint32_t> send_ids, recv_ids;
+    DevBuf<unsigned int> send_counts;
+    DevBuf<unsigned long long> recv_total;
+    uint64_t send_cap = 0;
+
+    WealthModel(int64_t n_, const amber_wealth_params& p_, uint64_t seed_, const amber_runtime* r)
+    {
+        rt.init(r);
+        n = n_;
+        p = p_;
+        seed = seed_;
+        key = philox_key(seed);
+        if (p.counter_bits == 0) p.counter_bits = 4;
+        B = p.counter_bits;
+        AMBER_REQUIRE(B == 2 || B == 4 || B == 8 || B == 16 || B == 32, "counter_bits must be 0,2,4,8,16,32");
+        AMBER_REQUIRE(p.amount >= 1, "amount must be >= 1");
+        AMBER_REQUIRE(p.w0 >= 0, "w0 must be >= 0");
+        AMBER_REQUIRE(!p.exclude_self || n >= 2, "exclude_self needs n_agents >= 2");
+        AMBER_REQUIRE(static_cast<double>(n) * p.w0 < 2147483647.0 || n == 1,
+                      "n_agents * w0 must fit int32 wealth of a single agent");
+        AMBER_REQUIRE(rt.world == 1 || n < (1ll << 32), "sharded wealth needs n_agents < 2^32");
+        shard = ((ceil_div(n, rt.world) + 7) / 8) * 8;
+        lo = std::min<int64_t>(shard * rt.rank, n);
+        hi = std::min<int64_t>(shard * (rt.rank + 1), n);
+        n_loc = hi - lo;
+        n_pad = std::max<int64_t>(ceil_div(std::max<int64_t>(n_loc, 1), kChunkAgents) * kChunkAgents, kChunkAgents);
+        for (auto& b : wb) b.allocate(&rt, n_pad);
+        const int64_t inc_words = ceil_div(n_pad * B, 32) + 4;
+        for (auto& b : inc) {
+            b.allocate(&rt, inc_words);
+            b.zero_async(rt.stream);
+        }
+        ring.allocate(&rt, metrics_cap);
+        ring.zero_async(rt.stream);
+        for (auto& b : wb) b.zero_async(rt.stream);
+        wealth_fill_kernel<<<rt.num_sms * 4, 256, 0, rt.stream>>>(wb[0].p, n_loc, n_pad, p.w0);
+        check_launch("wealth_fill_kernel");
+        if (rt.world > 1) {
+            xch = make_wealth_exchange_rt(rt, r);
+            send_cap = static_cast<uint64_t>(std::max<int64_t>(n_loc, 1));
+            send_ids.allocate(&rt, send_cap * rt.world);
+            recv_ids.allocate(&rt, static_cast<size_t>(shard) * rt.world + 1);
+            send_counts.allocate(&rt, rt.world);
+            send_counts.zero_async(rt.stream);
+            recv_total.allocate(&rt, 1);
+        }
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    }
+
+    ~WealthModel() override
+    {
+        if (rt.stream) cudaStreamSynchronize(rt.stream);
+        if (xch) destroy_wealth_exchange(xch);
+        for (auto& b : wb) b.reset();
+        for (auto& b : inc) b.reset();
+        for (auto& b : inc32) b.reset();
+        ring.reset();
+        send_ids.reset();
+        recv_ids.reset();
+        send_counts.reset();
+        recv_total.reset();
+        rt.destroy();
+    }
+
+    int other(int a, int b) const
+    {
+        for (int k = 0; k < 3; ++k)
+            if (k != a && k != b) return k;
+        return -1;
+    }
+
+    Slot* slot(int64_t s) { return ring.p + (s % metrics_cap); }
+
+    template <int BB, bool APPLY, bool SCATTER, bool DIGEST, bool REMOTE>
+    void launch_inst(const WealthArgs& a)
+    {
+        auto kern = wealth_step_kernel<BB, APPLY, SCATTER, DIGEST, REMOTE>;
+        int threads = block ? static_cast<int>(block) : 256;
+        int g = static_cast<int>(grid);
+        if (!g) {
+            int per_sm = 0;
+            AMBER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
+            g = static_cast<int>(std::min<int64_t>(a.nchunks * 32 / threads + 1,
+                                                   static_cast<int64_t>(std::max(per_sm, 1)) * rt.num_sms));
+        }
+        const char* name = APPLY ? (SCATTER ? "wealth_step_fused" : "wealth_apply") : "wealth_scatter";
+        prof.launch(rt.stream, name, [&] { kern<<<g, threads, 0, rt.stream>>>(a); });
+        check_launch(name);
+    }
+
+    template <int BB>
+    void launch_b(const WealthArgs& a, bool apply, bool scatter, bool dig, bool remote)
+    {
+#define AMBER_W_DISPATCH(AP, SC)                                                         \
+    if (apply == AP && scatter == SC) {                                                  \
+        if (dig) {                                                                       \
+            if (remote) launch_inst<BB, AP, SC, true, true>(a);                          \
+            else launch_inst<BB, AP, SC, true, false>(a);                                \
+        } else {                                                                         \
+            if (remote) launch_inst<BB, AP, SC, false, true>(a);                         \
+            else launch_inst<BB, AP, SC, false, false>(a);                               \
+        }                                                                                \
+        return;                                                                          \
+    }
+        AMBER_W_DISPATCH(true, true)
+        AMBER_W_DISPATCH(false, true)
+        AMBER_W_DISPATCH(true, false)
+#undef AMBER_W_DISPATCH
+    }
+
+    // One launch: apply step ta (if apply) from wb[src] into wb[dst], scatter step ts (if scatter).
+    void launch(int bits, bool apply, bool scatter, int64_t ta, int64_t ts, int src, int dst)
+    {
+        DevBuf<uint32_t>* ib = bits == 32 ? inc32 : inc;
+        WealthArgs a{};
+        a.key = key;
+        a.w_in = wb[src].p;
+        a.w_out = apply ? wb[dst].p : nullptr;
+        a.inc_cur = apply ? ib[ta & 1].p : nullptr;
+        a.inc_next = scatter ? ib[ts & 1].p : nullptr;
+        a.nchunks = n_pad / kChunkAgents;
+        a.n_loc = n_loc;
+        a.lo = static_cast<unsigned long long>(lo);
+        a.n_glob = static_cast<unsigned long long>(n);
+        a.amount = p.amount;
+        a.exclude_self = p.exclude_self;
+        a.t_apply = static_cast<uint32_t>(ta);
+        a.t_scatter = static_cast<uint32_t>(ts);
+        a.slot_apply = apply ? slot(ta) : nullptr;
+        a.slot_scatter = scatter ? slot(ts) : nullptr;
+        a.slot_zero = (apply && scatter) ? slot(ta + 2) : nullptr;
+        const bool remote = rt.world > 1 && scatter;
+        if (remote) {
+            a.world = rt.world;
+            a.shard_size = static_cast<unsigned long long>(shard);
+            a.remote_ids = send_ids.p;
+            a.remote_count = send_counts.p;
+            a.remote_cap = send_cap;
+            send_counts.zero_async(rt.stream);
+        }
+        const bool dig = digest_on != 0;
+        switch (bits) {
+            case 2: launch_b<2>(a, apply, scatter, dig, remote); break;
+            case 4: launch_b<4>(a, apply, scatter, dig, remote); break;
+            case 8: launch_b<8>(a, apply, scatter, dig, remote); break;
+            case 16: launch_b<16>(a, apply, scatter, dig, remote); break;
+            default: launch_b<32>(a, apply, scatter, dig, remote); break;
+        }
+        if (remote) exchange(bits, ts);
+    }
+
+    // Cross-shard step: ship remote receivers to their owners, add them to the
+    // owners' counters of step ts.
+    void exchange(int bits, int64_t ts)
+    {
+        DevBuf<uint32_t>* ib = bits == 32 ? inc32 : inc;
+        wealth_exchange_run(xch, rt, send_counts.p, send_ids.p, send_cap, recv_ids.p, recv_total.p);
+        auto launch_recv = [&](auto kern) {
+            prof.launch(rt.stream, "wealth_recv_apply", [&] {
+                kern<<<rt.num_sms * 4, 256, 0, rt.stream>>>(recv_ids.p, recv_total.p,
+                                                          static_cast<unsigned long long>(lo), ib[ts & 1].p, slot(ts));
+            });
+            check_launch("wealth_recv_kernel");
+        };
+        switch (bits) {
+            case 2: launch_recv(wealth_recv_kernel<2>); break;
+            case 4: launch_recv(wealth_recv_kernel<4>); break;
+            case 8: launch_recv(wealth_recv_kernel<8>); break;
+            case 16: launch_recv(wealth_recv_kernel<16>); break;
+            default: launch_recv(wealth_recv_kernel<32>); break;
+        }
+    }
+
+    void zero_slots(int64_t s0, int64_t count)
+    {
+        zero_slots_kernel<<<1, 64, 0, rt.stream>>>(ring.p, metrics_cap, s0, count);
+        check_launch("zero_slots_kernel");
+    }
+
+    void step(int64_t nsteps) override
+    {
+        AMBER_REQUIRE(nsteps >= 0, "n_steps must be >= 0");
+        AMBER_REQUIRE(t + nsteps < (1ll << 32) - 2, "step index would exceed 2^32");
+        for (int64_t k = 0; k < nsteps; ++k) {
+            if (win_start >= 0 && t - win_start >= metrics_cap - 4) verify();
+            if (win_start < 0) {
+                win_start = t;
+                pinned = cur;
+            }
+            if (!pending) {
+                zero_slots(t, 2);
+                launch(B, false, true, t, t, cur, cur);
+            }
+            const int dst = other(cur, pinned == cur ? -1 : pinned);
+            launch(B, true, true, t, t + 1, cur, dst);
+            cur = dst;
+            ++t;
+            pending = true;
+        }
+    }
+
+    // Exact overflow check of the open window; replays it with 32-bit counters if needed.
+    void verify()
+    {
+        if (win_start < 0) {
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            return;
+        }
+        std::vector<Slot> h(metrics_cap);
+        AMBER_CUDA(cudaMemcpyAsync(h.data(), ring.p, metrics_cap * sizeof(Slot), cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        bool bad = false;
+        for (int64_t s = win_start; s < t; ++s) {
+            const Slot& x = h[s % metrics_cap];
+            if (x.sent != x.got) bad = true;
+        }
+        if (xch) bad = wealth_exchange_any(xch, rt, bad);
+        if (bad) replay(win_start, t);
+        win_start = -1;
+        pinned = -1;
+    }
+
+    void replay(int64_t s0, int64_t s1)
+    {
+        ++replays;
+        cur = pinned;
+        for (auto& b : inc) b.zero_async(rt.stream);
+        for (auto& b : inc32) {
+            if (!b.p) b.allocate(&rt, n_pad + 4);
+            b.zero_async(rt.stream);
+        }
+        ring.zero_async(rt.stream);
+        if (xch) send_counts.zero_async(rt.stream);
+        for (int64_t s = s0; s < s1; ++s) {
+            if (s == s0) launch(32, false, true, s, s, cur, cur);
+            const int dst = other(cur, -1);
+            launch(32, true, s + 1 < s1, s, s + 1, cur, dst);
+            cur = dst;
+        }
+        t = s1;
+        pending = false;
+        std::vector<Slot> h(metrics_cap);
+        AMBER_CUDA(cudaMemcpyAsync(h.data(), ring.p, metrics_cap * sizeof(Slot), cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        for (int64_t s = s0; s < s1; ++s)
+            if (h[s % metrics_cap].sent != h[s % metrics_cap].got)
+                fail(AMBER_E_CUDA, "wealth replay: increment count mismatch with 32-bit counters");
+        if (m_first < s0) m_first = s0;  // earlier records were cleared with the ring
+    }
+
+    void invalidate_pending()
+    {
+        if (pending) {
+            inc[t & 1].zero_async(rt.stream);
+            pending = false;
+        }
+    }
+
+    void synchronize() override { verify(); }
+
+    bool column_info(const char* name, amber_dtype* dt, int64_t* glen, int64_t* off, int64_t* len) override
+    {
+        if (std::string(name) != "wealth") return false;
+        if (dt) *dt = AMBER_I32;
+        if (glen) *glen = n;
+        if (off) *off = lo;
+        if (len) *len = n_loc;
+        return true;
+    }
+
+    void read_column(const char* name, void* dst, size_t bytes, bool on_dev) override
+    {
+        if (std::string(name) != "wealth") fail(AMBER_E_UNKNOWN_NAME, std::string("no column ") + name);
+        if (bytes < static_cast<size_t>(n_loc) * 4) fail(AMBER_E_BUFFER_TOO_SMALL, "dst too small for wealth slice");
+        verify();
+        copy_out(rt, dst, wb[cur].p, n_loc * 4, on_dev);
+    }
+
+    void write_column(const char* name, const void* src, size_t bytes, bool on_dev) override
+    {
+        if (std::string(name) != "wealth") fail(AMBER_E_UNKNOWN_NAME, std::string("no column ") + name);
+        if (bytes < static_cast<size_t>(n_loc) * 4) fail(AMBER_E_BUFFER_TOO_SMALL, "src smaller than wealth slice");
+        verify();
+        invalidate_pending();
+        copy_in(rt, wb[cur].p, src, n_loc * 4, on_dev);
+    }
+
+    void read_metrics(const char* name, void* dst, size_t bytes, int64_t* n_out) override
+    {
+        verify();
+        std::string k(name);
+        size_t off;
+        if (k == "total_wealth") off = offsetof(Slot, total);
+        else if (k == "active") off = offsetof(Slot, active);
+        else if (k == "digest" && digest_on) off = offsetof(Slot, digest);
+        else fail(AMBER_E_UNKNOWN_NAME, "no metric " + k + (k == "digest" ? " (set option digest=1)" : ""));
+        std::vector<Slot> h(metrics_cap);
+        AMBER_CUDA(cudaMemcpyAsync(h.data(), ring.p, metrics_cap * sizeof(Slot), cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        const int64_t first = std::max(m_first, t - metrics_cap + 3);
+        const int64_t cnt = std::max<int64_t>(t - first, 0);
+        if (bytes < static_cast<size_t>(cnt) * 8) fail(AMBER_E_BUFFER_TOO_SMALL, "metrics dst too small");
+        std::vector<unsigned long long> vals(cnt);
+        for (int64_t s = first; s < t; ++s)
+            std::memcpy(&vals[s - first], reinterpret_cast<const char*>(&h[s % metrics_cap]) + off, 8);
+        if (xch && cnt) {  // global values: sum over ranks
+            DevBuf<unsigned long long> d;
+            d.allocate(&rt, cnt);
+            AMBER_CUDA(cudaMemcpyAsync(d.p, vals.data(), cnt * 8, cudaMemcpyHostToDevice, rt.stream));
+            wealth_exchange_allreduce_u64(xch, rt, d.p, static_cast<int>(cnt));
+            AMBER_CUDA(cudaMemcpyAsync(vals.data(), d.p, cnt * 8, cudaMemcpyDeviceToHost, rt.stream));
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        }
+        std::memcpy(dst, vals.data(), cnt * 8);
+        if (n_out) *n_out = cnt;
+    }
+
+    void reset_metrics() override
+    {
+        verify();
+        m_first = t;
+    }
+
+    uint64_t digest(const char* name) override
+    {
+        if (std::string(name) != "wealth") fail(AMBER_E_UNKNOWN_NAME, std::string("no column ") + name);
+        verify();
+        uint64_t d = device_digest_u32(rt, reinterpret_cast<const uint32_t*>(wb[cur].p), n_loc, lo);
+        if (xch) {
+            DevBuf<unsigned long long> b;
+            b.allocate(&rt, 1);
+            AMBER_CUDA(cudaMemcpyAsync(b.p, &d, 8, cudaMemcpyHostToDevice, rt.stream));
+            wealth_exchange_allreduce_u64(xch, rt, b.p, 1);
+            AMBER_CUDA(cudaMemcpyAsync(&d, b.p, 8, cudaMemcpyDeviceToHost, rt.stream));
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        }
+        return d;
+    }
+
+    void set_step(int64_t s) override
+    {
+        AMBER_REQUIRE(s >= 0 && s < (1ll << 32) - 2, "step out of range");
+        verify();
+        invalidate_pending();
+        t = s;
+        m_first = s;
+    }
+
+    bool set_option(const char* key, int64_t v) override
+    {
+        std::string k(key);
+        if (k == "metrics_capacity") {
+            AMBER_REQUIRE(v >= 16, "metrics_capacity must be >= 16");
+            verify();
+            invalidate_pending();
+            metrics_cap = v;
+            ring.allocate(&rt, metrics_cap);
+            ring.zero_async(rt.stream);
+            m_first = t;
+            return true;
+        }
+        if (k == "digest" || k == "block" || k == "grid") verify();
+        return Model::set_option(key, v);
+    }
+
+    bool get_option(const char* key, int64_t* v) override
+    {
+        std::string k(key);
+        if (k == "replays") {
+            verify();
+            *v = replays;
+            return true;
+        }
+        if (k == "counter_bits") {
+            *v = B;
+            return true;
+        }
+        return Model::get_option(key, v);
+    }
+};
+
+Model* make_wealth(int64_t n, const amber_wealth_params& p, uint64_t seed, const amber_runtime* rt)
+{
+    return new WealthModel(n, p, seed, rt);
+}
+
+}  // namespace amber
