@@ -367,9 +367,9 @@ public:
     }
 
     // One launch: apply step ta (if apply) from wb[src] into wb[dst], scatter step ts (if scatter).
-    void launch(int bits, bool apply, bool scatter, int64_t ta, int64_t ts, int src, int dst)
+    void launch(int bits, bool exact, bool apply, bool scatter, int64_t ta, int64_t ts, int src, int dst)
     {
-        DevBuf<uint32_t>* ib = bits == 32 ? inc32 : inc;
+        DevBuf<uint32_t>* ib = exact ? inc32 : inc;
         WealthArgs a{};
         a.key = key;
         a.w_in = wb[src].p;
@@ -404,14 +404,14 @@ public:
             case 16: launch_b<16>(a, apply, scatter, dig, remote); break;
             default: launch_b<32>(a, apply, scatter, dig, remote); break;
         }
-        if (remote) exchange(bits, ts);
+        if (remote) exchange(bits, exact, ts);
     }
 
     // Cross-shard step: ship remote receivers to their owners, add them to the
     // owners' counters of step ts.
-    void exchange(int bits, int64_t ts)
+    void exchange(int bits, bool exact, int64_t ts)
     {
-        DevBuf<uint32_t>* ib = bits == 32 ? inc32 : inc;
+        DevBuf<uint32_t>* ib = exact ? inc32 : inc;
         wealth_exchange_run(xch, rt, send_counts.p, send_ids.p, send_cap, recv_ids.p, recv_total.p);
         auto launch_recv = [&](auto kern) {
             prof.launch(rt.stream, "wealth_recv_apply", [&] {
@@ -447,10 +447,10 @@ public:
             }
             if (!pending) {
                 zero_slots(t, 2);
-                launch(B, false, true, t, t, cur, cur);
+                launch(B, false, false, true, t, t, cur, cur);
             }
             const int dst = other(cur, pinned == cur ? -1 : pinned);
-            launch(B, true, true, t, t + 1, cur, dst);
+            launch(B, false, true, true, t, t + 1, cur, dst);
             cur = dst;
             ++t;
             pending = true;
@@ -490,9 +490,9 @@ public:
         ring.zero_async(rt.stream);
         if (xch) send_counts.zero_async(rt.stream);
         for (int64_t s = s0; s < s1; ++s) {
-            if (s == s0) launch(32, false, true, s, s, cur, cur);
+            if (s == s0) launch(32, true, false, true, s, s, cur, cur);
             const int dst = other(cur, -1);
-            launch(32, true, s + 1 < s1, s, s + 1, cur, dst);
+            launch(32, true, true, s + 1 < s1, s, s + 1, cur, dst);
             cur = dst;
         }
         t = s1;
@@ -617,6 +617,7 @@ public:
             m_first = t;
             return true;
         }
+        if (k == "block") AMBER_REQUIRE(v <= 256, "wealth kernels are built for <= 256 threads per block");
         if (k == "digest" || k == "block" || k == "grid") verify();
         return Model::set_option(key, v);
     }

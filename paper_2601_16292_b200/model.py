@@ -37,8 +37,11 @@ class TorchAllocator:
                 return None
 
         def _free(ptr, nbytes, stream, ctx):
-            if ptr:
-                torch.cuda.caching_allocator_delete(int(ptr))
+            try:
+                if ptr:
+                    torch.cuda.caching_allocator_delete(int(ptr))
+            except Exception:  # interpreter shutdown: torch already torn down
+                pass
 
         self.alloc = capi.ALLOC_FN(_alloc)
         self.free = capi.FREE_FN(_free)
@@ -50,9 +53,12 @@ def make_runtime(device=0, stream=None, torch_alloc=True, rank=0, world=1, uniqu
     rt.device = device
     keep = []
     if stream is None:
+        # a dedicated torch stream (not the legacy NULL stream, which the C ABI
+        # reads as "library-created stream"): callers time on model.stream
         import torch
-        stream = torch.cuda.current_stream(device).cuda_stream
-    rt.stream = C.c_void_p(int(stream)) if stream else None
+        stream = torch.cuda.Stream(device)
+    keep.append(stream)
+    rt.stream = C.c_void_p(int(getattr(stream, "cuda_stream", stream)))
     if torch_alloc:
         ta = TorchAllocator(device)
         rt.alloc, rt.free = ta.alloc, ta.free
@@ -84,6 +90,7 @@ class Model:
         self.kind = kind
         self.lib = capi.lib()
         self.rt = make_runtime(device, stream, torch_alloc, rank, world, unique_id)
+        self.stream = self.rt._keep[0]  # torch.cuda.Stream (or the caller's stream handle)
         self.params = params
         h = C.c_void_p()
         check(self.lib.amber_model_create(self.KINDS[kind], int(n_agents), C.byref(params),

@@ -61,7 +61,7 @@ def test_chunked_stepping_and_geometry_invariance(orc):
     b.step(13)
     b.step(17)
     c = make(n, seed)
-    c.set_option("block", 1024)
+    c.set_option("block", 128)
     c.step(30)
     for m in (a, b, c):
         assert np.array_equal(m.read_column("wealth"), ref)
