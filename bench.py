@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""bench.py -- agent-updates/s of the AMBER hot path on B200 (driver contract).
+
+Default workload (BASELINE.json config 4, the metric's "1/2/4/8 B200" config):
+wealth transfer, N = 1e8 agents, int32 wealth, Philox seed 11.  One "step" is
+one synchronous step of the whole population (one fused kernel launch on one
+GPU; plus the cross-shard exchange when sharded).  The state (400 MB) is
+larger than L2, so no L2 flush is needed between timed steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl amber|reference]
+                  [--workload c4|c1|c2|c3|c5] [--no-cpu-baseline]
+
+For N > 1 the driver launches it under torchrun (one rank per GPU over NCCL);
+agents are sharded by contiguous id ranges and the timed region is the max
+over ranks of the device time.  `--impl reference` times the CPU oracle (the
+reference arm for this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "agent-updates/sec per step (1/2/4/8 B200) and % of HBM roofline vs CPU oracle"
+UNIT = "agent-updates/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def host_info():
+    model = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.idx = device_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in out.strip().splitlines():
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ oracle
+def cpu_baseline_wealth(n_total, seed, budget_s=12.0):
+    """Oracle (as it stands, single-threaded C) on a bounded sample: a population
+    of n_s <= n_total agents stepped synchronously for as many steps as fit the
+    budget (at least 2).  Returns the cpu_baseline object."""
+    import numpy as np
+
+    import oracle
+    n_s = int(min(n_total, 10_000_000))
+    w = np.ones(n_s, np.int32)
+    t0 = time.perf_counter()
+    oracle.wealth_step(w, seed, 0)
+    one = time.perf_counter() - t0
+    steps = max(2, int(budget_s / max(one, 1e-6)))
+    t0 = time.perf_counter()
+    w2, _, _, _ = oracle.wealth_run(w, seed, 0, steps)
+    dt = time.perf_counter() - t0
+    return {"value": n_s * steps / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"wealth N={n_s:.0e} (of {n_total:.0e}) x {steps} steps, seed {seed}, "
+                      f"single thread, {dt:.1f}s"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed on the host cores (bounded sample)."""
+    import numpy as np
+
+    import oracle
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2601_16292_b200.workloads import C4_WEALTH_SCALE as cfg
+    oracle.build()
+    # size the per-step sample so warmup + steps stay within ~2-3 minutes
+    n_probe = 2_000_000
+    w = np.ones(n_probe, np.int32)
+    t0 = time.perf_counter()
+    oracle.wealth_step(w, cfg["seed"], 0)
+    per_agent = (time.perf_counter() - t0) / n_probe
+    budget = 150.0
+    n_s = int(max(100_000, min(cfg["n"], budget / (per_agent * max(args.steps + args.warmup, 1)))))
+    w = np.ones(n_s, np.int32)
+    for t in range(args.warmup):
+        w = oracle.wealth_step(w, cfg["seed"], t)
+    t0 = time.perf_counter()
+    w, _, _, _ = oracle.wealth_run(w, cfg["seed"], args.warmup, args.steps)
+    dt = time.perf_counter() - t0
+    v = n_s * args.steps / dt
+    model, ncpu = host_info()
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "C4 wealth transfer (BASELINE config 4)", "n_agents": cfg["n"],
+                       "sample_agents": n_s, "seed": cfg["seed"]},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"wealth N={n_s} x {args.steps} steps per timed region "
+                                       f"(of N={cfg['n']}); host {model}, {ncpu} cpus"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    return world, rank, local, pg
+
+
+def barrier_sync(pg, torch):
+    torch.cuda.synchronize()
+    if pg is not None:
+        pg.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(pg, torch, v):
+    if pg is None:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def bench_wealth(args):
+    import numpy as np
+    import torch
+
+    from paper_2601_16292_b200 import Model, nccl_unique_id, wealth_params
+    from paper_2601_16292_b200.workloads import C4_WEALTH_SCALE as cfg
+
+    world, rank, local, pg = dist_setup(args)
+    uid = None
+    if world > 1:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        pg.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    n = cfg["n"]
+    m = Model("wealth", n, wealth_params(w0=cfg["w0"], amount=cfg["amount"],
+                                         exclude_self=cfg["exclude_self"]), cfg["seed"],
+              device=local, rank=rank, world=world, unique_id=uid)
+    _, _, off, n_loc = m.column_info("wealth")
+    stream = m.stream
+    for _ in range(args.warmup):
+        m.step(1)
+    m.synchronize()
+    clocks = ClockSampler(local)
+    m.profile(True)
+    barrier_sync(pg, torch)
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        m.step(1)
+    ev1.record(stream)
+    m.synchronize()
+    barrier_sync(pg, torch)
+    cl = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(pg, torch, ms)
+    prof = m.profile_results()
+    m.profile(False)
+    tot = m.metrics("total_wealth")
+    assert (tot == n * cfg["w0"]).all(), "wealth not conserved"
+    launches = sum(c for _, c, _ in prof)
+    dom = max(prof, key=lambda r: r[2]) if prof else ("", 0, 0.0)
+    dom_avg_ms = dom[2] / max(dom[1], 1)
+    value = n * args.steps / (ms / 1e3)
+
+    # ---- end to end through the public API with host buffers -------------
+    # timed: H2D of the initial column from pinned host memory, K steps each
+    # followed by a D2H read of that step's observables, D2H of the final column
+    host_w = torch.full((n_loc,), cfg["w0"], dtype=torch.int32).pin_memory()
+    host_out = torch.empty((n_loc,), dtype=torch.int32).pin_memory()
+    m.set_step(0)
+    barrier_sync(pg, torch)
+    t0 = time.perf_counter()
+    m.write_column("wealth", host_w.numpy())
+    m.reset_metrics()
+    for _ in range(args.steps):
+        m.step(1)
+        m.metrics("active")
+    m.read_column("wealth", host_out.numpy())
+    barrier_sync(pg, torch)
+    e2e_s = max_over_ranks(pg, torch, time.perf_counter() - t0)
+    e2e = {"value": n * args.steps / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": int(n_loc * 4 / args.steps),
+           "d2h_bytes_per_step": int(n_loc * 4 / args.steps + 8 * min(args.steps, 4096))}
+
+    hbm, kind = peaks()
+    alg_bytes = 8.0 * n_loc  # wealth column read + written once per step
+    achieved = alg_bytes / (dom_avg_ms / 1e3) / 1e9 if dom_avg_ms > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "wealth_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    if rank == 0:
+        model, ncpu = host_info()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (seeded Philox population, BASELINE config 4)",
+            "config": {"workload": "C4 wealth transfer (BASELINE config 4)", "n_agents": n,
+                       "seed": cfg["seed"], "parallelism": f"id-sharded x{world}",
+                       "counter_bits": m.get_option("counter_bits"),
+                       "l2": "state (400 MB int32 column) larger than L2; no flush"},
+            "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": hbm,
+                         "peak_kind": kind, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
+                         "avg_launch_ms": dom_avg_ms,
+                         "share_of_step": dom[2] / ms if ms > 0 else None},
+            "kernels": [{"name": a, "launches": b, "total_ms": c} for a, b, c in prof],
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "clocks": cl,
+            "host": {"cpu": model, "cpus": ncpu},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_wealth(n, cfg["seed"])
+        print(json.dumps(line), flush=True)
+    m.close()
+    if pg is not None:
+        pg.destroy_process_group()
+    return 0
+
+
+def bench_small(args):
+    """Extra single-GPU measurements of the other configs (not the driver line)."""
+    import numpy as np
+    import torch
+
+    from paper_2601_16292_b200 import Model, boids_params, sir_params, sweep, wealth_params
+    from paper_2601_16292_b200 import workloads as W
+
+    out = {}
+    w = args.workload
+    if w == "c1":
+        c = W.C1_WEALTH_SMALL
+        m = Model("wealth", c["n"], wealth_params(), c["seed"])
+        k = c["steps"]
+    elif w == "c2":
+        c = W.C2_SIR
+        m = Model("sir", c["n"], sir_params(c["mean_degree"], c["beta"], c["gamma"], c["init_frac"]),
+                  c["seed"])
+        k = c["steps"]
+    elif w == "c3":
+        c = W.C3_BOIDS
+        m = Model("boids", c["n"], boids_params(*[c[x] for x in ("L", "R", "rs", "wc", "wa", "ws",
+                                                                   "vmax", "dt")]), c["seed"])
+        k = c["steps"]
+    elif w == "c5":
+        c = W.C5_SWEEP
+        betas, seeds = W.sweep_replicates(c)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res, st = sweep(c["n"], sir_params(c["mean_degree"], 0.0, c["gamma"], c["init_frac"]), betas,
+                        seeds, c["steps"], with_stats=True)
+        wall = time.perf_counter() - t0
+        upd = c["n"] * c["steps"] * len(betas)
+        print(json.dumps({"workload": "c5", "agent_updates": upd, "step_ms": st["step_ms"],
+                          "build_ms": st["build_ms"], "wall_s": wall,
+                          "value": upd / (st["step_ms"] / 1e3), "unit": UNIT,
+                          "active_updates": st["active_updates"]}))
+        return 0
+    else:
+        raise SystemExit(f"unknown workload {w}")
+    m.step(1)
+    m.synchronize()
+    m.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(m.stream)
+    m.step(k)
+    e1.record(m.stream)
+    m.synchronize()
+    ms = e0.elapsed_time(e1)
+    print(json.dumps({"workload": w, "n": c["n"], "steps": k, "ms": ms, "ms_per_step": ms / k,
+                      "value": c["n"] * k / (ms / 1e3), "unit": UNIT,
+                      "kernels": m.profile_results()}))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="amber", choices=["amber", "reference"])
+    ap.add_argument("--workload", default="c4")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.workload != "c4":
+        return bench_small(args)
+    return bench_wealth(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

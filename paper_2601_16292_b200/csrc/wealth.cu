@@ -10,6 +10,7 @@
 // increments) and the affected step window is replayed with 32-bit counters
 // from a pinned copy of the window's first state (3 rotating wealth buffers).
 #include <algorithm>
+#include <type_traits>
 
 #include "internal.cuh"
 #include "philox.cuh"
@@ -84,22 +85,38 @@ __device__ __forceinline__ void zero_quad_counts(uint32_t* inc, int64_t q)
     else reinterpret_cast<uint4*>(inc)[q] = make_uint4(0u, 0u, 0u, 0u);
 }
 
-template <int B>
-__device__ __forceinline__ void add_count(uint32_t* inc, unsigned long long rl)
+// L2 eviction-priority policies: keep the counters resident, stream the column.
+__device__ __forceinline__ unsigned long long policy_evict_last()
+{
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ void red_add_hint(uint32_t* addr, uint32_t v, unsigned long long pol)
+{
+    asm volatile("red.global.add.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(addr), "r"(v), "l"(pol) : "memory");
+}
+
+template <int B, class Id>
+__device__ __forceinline__ void add_count(uint32_t* inc, Id rl, unsigned long long pol)
 {
     if constexpr (B == 32) {
-        atomicAdd(inc + rl, 1u);
+        red_add_hint(inc + rl, 1u, pol);
     } else {
-        constexpr int per = 32 / B;
-        atomicAdd(inc + (rl / per), 1u << ((rl % per) * B));
+        constexpr Id per = 32 / B;
+        red_add_hint(inc + (rl / per), 1u << (static_cast<uint32_t>(rl % per) * B), pol);
     }
 }
 
+// R6/W2 receiver; `m` = N (or N-1 when excluding self), precomputed on the host.
+template <bool FAST32>
 __device__ __forceinline__ unsigned long long receiver(unsigned long long x, unsigned long long i,
-                                                       unsigned long long n, int exclude_self)
+                                                       unsigned long long m, int exclude_self)
 {
-    const unsigned long long m = exclude_self ? n - 1 : n;
-    unsigned long long r = (m >> 32) ? mulhi64(x, m) : mulhi64_n32(x, static_cast<uint32_t>(m));
+    unsigned long long r;
+    if constexpr (FAST32) r = mulhi64_n32(x, static_cast<uint32_t>(m));
+    else r = mulhi64(x, m);
     if (exclude_self) r += (r >= i);
     return r;
 }
@@ -123,28 +140,40 @@ __device__ __forceinline__ void remote_append(const WealthArgs& a, bool flag, un
     if (pos < a.remote_cap) a.remote_ids[dest * a.remote_cap + pos] = static_cast<uint32_t>(r);
 }
 
-template <int B, bool APPLY, bool SCATTER, bool DIGEST, bool REMOTE>
+// One launch of the step pipeline.  Thread layout: a warp owns a chunk of
+// kQPT*32 quads (4 agents each); lane l takes quads chunk*kQPT*32 + j*32 + l,
+// so every global load/store instruction of the warp is a contiguous 512-byte
+// (w) or 64-byte (4-bit counters) segment.  FAST32: all ids < 2^32 (32-bit
+// index arithmetic); REMOTE: receivers outside this shard are bucketed for
+// the exchange instead of counted locally.
+template <int B, bool APPLY, bool SCATTER, bool DIGEST, bool REMOTE, bool FAST32>
 __global__ void __launch_bounds__(256) wealth_step_kernel(const WealthArgs a)
 {
+    using Id = typename std::conditional<FAST32, uint32_t, unsigned long long>::type;
     if (a.slot_zero && blockIdx.x == 0 && threadIdx.x == 0) *a.slot_zero = Slot{0, 0, 0, 0, 0};
 
     const int lane = threadIdx.x & 31;
     const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    unsigned long long tot = 0, act = 0, sent = 0, got = 0, dig = 0;
+    const unsigned long long pol = policy_evict_last();
+    const Id lo = static_cast<Id>(a.lo), n_loc = static_cast<Id>(a.n_loc);
+    const unsigned long long m = a.n_glob - (a.exclude_self ? 1 : 0);
+    unsigned long long tot = 0, dig = 0;
+    uint32_t act = 0, sent = 0, got = 0;
 
     for (int64_t chunk = warp; chunk < a.nchunks; chunk += nwarps) {
         int4 w[kQPT];
         uint32_t c[kQPT][4];
 #pragma unroll
         for (int j = 0; j < kQPT; ++j) {
-            const int64_t q = (chunk * kQPT + j) * 32 + lane;
+            const Id q = static_cast<Id>((chunk * kQPT + j) * 32 + lane);
             w[j] = __ldcs(reinterpret_cast<const int4*>(a.w_in) + q);  // streaming: evict-first
             if constexpr (APPLY) load_quad_counts<B>(a.inc_cur, q, c[j]);
         }
+        int32_t tsum = 0;
 #pragma unroll
         for (int j = 0; j < kQPT; ++j) {
-            const int64_t q = (chunk * kQPT + j) * 32 + lane;
+            const Id q = static_cast<Id>((chunk * kQPT + j) * 32 + lane);
             int32_t v[4] = {w[j].x, w[j].y, w[j].z, w[j].w};
             if constexpr (APPLY) {
 #pragma unroll
@@ -157,39 +186,38 @@ __global__ void __launch_bounds__(256) wealth_step_kernel(const WealthArgs a)
                 zero_quad_counts<B>(a.inc_cur, q);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    tot += static_cast<unsigned long long>(static_cast<long long>(v[k]));
+                    tsum += v[k];
                     act += v[k] > 0;
                     if constexpr (DIGEST) {
-                        const int64_t loc = 4 * q + k;
-                        if (loc < a.n_loc)
+                        const Id loc = 4 * q + k;
+                        if (loc < n_loc)
                             dig += digest_term(a.lo + static_cast<unsigned long long>(loc),
                                                static_cast<uint32_t>(v[k]));
                     }
                 }
             }
             if constexpr (SCATTER) {
-                const unsigned long long i0 = a.lo + 4ull * static_cast<unsigned long long>(q);
+                const Id i0 = lo + 4 * q;  // even: shards start at multiples of 8
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
-                    const bool s0 = v[2 * p] >= a.amount, s1 = v[2 * p + 1] >= a.amount;
-                    uint4 x = make_uint4(0u, 0u, 0u, 0u);
-                    if (s0 || s1) x = stream_block(a.key, TAG_WEALTH_RECV, (i0 >> 1) + p, a.t_scatter);
+                    const uint4 x = stream_block(a.key, TAG_WEALTH_RECV, (i0 >> 1) + p, a.t_scatter);
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const bool s = h ? s1 : s0;
-                        const unsigned long long i = i0 + 2 * p + h;
-                        const unsigned long long r = receiver(lane64_of(x, h), i, a.n_glob, a.exclude_self);
-                        const unsigned long long rl = r - a.lo;
-                        const bool local = s && rl < static_cast<unsigned long long>(a.n_loc);
-                        if (local) {
-                            add_count<B>(a.inc_next, rl);
-                            sent += 1;
-                        }
+                        const bool s = v[2 * p + h] >= a.amount;
+                        const Id i = i0 + 2 * p + h;
+                        const Id r = static_cast<Id>(receiver<FAST32>(lane64_of(x, h), i, m, a.exclude_self));
+                        const Id rl = r - lo;
+                        bool local = s;
+                        if constexpr (REMOTE) local = s && rl < n_loc;
+                        if (local) add_count<B>(a.inc_next, rl, pol);
+                        sent += local;
                         if constexpr (REMOTE) remote_append(a, s && !local, r);
                     }
                 }
             }
         }
+        // per-chunk partial in 32 bits (at most 16 agents' wealth), then widen
+        tot += static_cast<unsigned long long>(static_cast<long long>(tsum));
     }
 
     unsigned long long vals[5] = {tot, act, dig, sent, got};
@@ -209,7 +237,7 @@ __global__ void wealth_recv_kernel(const uint32_t* __restrict__ ids, const unsig
     unsigned long long cnt = 0;
     for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < n;
          k += (unsigned long long)gridDim.x * blockDim.x) {
-        add_count<B>(inc, static_cast<unsigned long long>(ids[k]) - lo);
+        add_count<B>(inc, static_cast<unsigned long long>(ids[k]) - lo, policy_evict_last());
         cnt += 1;
     }
     unsigned long long vals[1] = {cnt};
@@ -247,6 +275,7 @@ public:
     uint64_t seed = 0;
     PhiloxKey key{};
     int B = 4;
+    bool fast32 = true;  // every id and padded index < 2^32 (32-bit index arithmetic)
     DevBuf<int32_t> wb[3];
     int cur = 0, pinned = -1;
     DevBuf<uint32_t> inc[2], inc32[2];
@@ -282,6 +311,8 @@ public:
         hi = std::min<int64_t>(shard * (rt.rank + 1), n);
         n_loc = hi - lo;
         n_pad = std::max<int64_t>(ceil_div(std::max<int64_t>(n_loc, 1), kChunkAgents) * kChunkAgents, kChunkAgents);
+        fast32 = n < (1ll << 32) - 1 && lo + n_pad < (1ll << 32);
+        AMBER_REQUIRE(fast32 || rt.world == 1, "sharded wealth needs ids < 2^32");
         for (auto& b : wb) b.allocate(&rt, n_pad);
         const int64_t inc_words = ceil_div(n_pad * B, 32) + 4;
         for (auto& b : inc) {
@@ -332,7 +363,9 @@ public:
     template <int BB, bool APPLY, bool SCATTER, bool DIGEST, bool REMOTE>
     void launch_inst(const WealthArgs& a)
     {
-        auto kern = wealth_step_kernel<BB, APPLY, SCATTER, DIGEST, REMOTE>;
+        constexpr bool kFast = true;
+        auto kern = fast32 ? wealth_step_kernel<BB, APPLY, SCATTER, DIGEST, REMOTE, kFast>
+                           : wealth_step_kernel<BB, APPLY, SCATTER, DIGEST, REMOTE, REMOTE>;
         int threads = block ? static_cast<int>(block) : 256;
         int g = static_cast<int>(grid);
         if (!g) {
