@@ -1,0 +1,507 @@
+// boids.cu -- flocking in a periodic 2-D box (BASELINE config 3; continuous
+// wrapped space per PAPER.md Sec. 4.1; B1-B8).
+//
+// Per step (all on the model stream):
+//   1. bin     : cell of every agent (uniform grid, cell side >= R with margin)
+//                -> per-cell counts (atomics)
+//   2. scan    : exclusive scan of the counts -> cell_start (one CTA)
+//   3. scatter : counting-sort placement; gathers (x, y, vx, vy) into a
+//                cell-sorted float4 array and carries the agent ids along
+//   4. step    : one thread per sorted agent scans the 3x3 cell stencil
+//                (contiguous ranges of the sorted array, L1-resident), sums
+//                neighbour terms in int64 fixed point (exact, so independent
+//                of traversal order), applies the rules and writes the next
+//                state in sorted order (coalesced).
+// The columns therefore live in "current order" with an id array; reads and
+// writes of the id-ordered columns go through an un-permute / permute kernel.
+// Float contract B7: every float/double op below is an explicit _rn intrinsic
+// (no FMA contraction, IEEE division and square root), so the step equals the
+// oracle's bit for bit.
+#include <algorithm>
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+#include "philox.cuh"
+
+namespace amber {
+
+namespace {
+
+constexpr float kFix = 16777216.0f;  // 2^24 (B3)
+
+struct BoidsArgs {
+    float L, R, rs, wc, wa, ws, vmax, dt;
+    int nc;       // cells per side
+    float inv_cs; // nc / L
+};
+
+__device__ __forceinline__ int cell_coord(float x, const BoidsArgs& a)
+{
+    int c = static_cast<int>(__fmul_rn(x, a.inv_cs));
+    return c < 0 ? 0 : (c >= a.nc ? a.nc - 1 : c);
+}
+
+// B1: initial positions and rejection-sampled unit velocities (id order).
+__global__ void boids_init_kernel(PhiloxKey key, int64_t n, float L, float4* st, int32_t* ids)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        // R4: 32-bit lanes 2i, 2i+1 of tag BOIDS_POS = words (2i%4, 2i%4+1) of block i/2
+        const uint4 w = stream_block(key, TAG_BOIDS_POS, static_cast<unsigned long long>(i) >> 1, 0u);
+        const uint32_t ux = (i & 1) ? w.z : w.x, uy = (i & 1) ? w.w : w.y;
+        const float x = __fmul_rn(L, u01(ux)), y = __fmul_rn(L, u01(uy));
+        float vx = 0.f, vy = 0.f;
+        for (uint32_t attempt = 0;; ++attempt) {
+            const uint4 v = philox(make_uint4(static_cast<uint32_t>(i), static_cast<uint32_t>(static_cast<unsigned long long>(i) >> 32),
+                                              attempt, TAG_BOIDS_VEL),
+                                   key);
+            const float a = __fsub_rn(__fmul_rn(2.0f, u01(v.x)), 1.0f);
+            const float b = __fsub_rn(__fmul_rn(2.0f, u01(v.y)), 1.0f);
+            const float s2 = __fadd_rn(__fmul_rn(a, a), __fmul_rn(b, b));
+            if (s2 > 0.0f && s2 <= 1.0f) {
+                const float s = __fsqrt_rn(s2);
+                vx = __fdiv_rn(a, s);
+                vy = __fdiv_rn(b, s);
+                break;
+            }
+        }
+        st[i] = make_float4(x, y, vx, vy);
+        ids[i] = static_cast<int32_t>(i);
+    }
+}
+
+__global__ void boids_count_kernel(const float4* __restrict__ st, int64_t n, BoidsArgs a, int* __restrict__ cnt,
+                                   int* __restrict__ cell_of)
+{
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const float4 s = st[p];
+        const int c = cell_coord(s.y, a) * a.nc + cell_coord(s.x, a);
+        cell_of[p] = c;
+        atomicAdd(cnt + c, 1);
+    }
+}
+
+// Exclusive scan of the cell counts by one CTA (ncell is at most a few 1e4);
+// also zeroes the counts for the next step.
+__global__ void __launch_bounds__(1024) boids_scan_kernel(int* cnt, int* start, int* cursor, int ncell)
+{
+    using Scan = cub::BlockScan<int, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < ncell; base += 1024) {
+        const int c = base + threadIdx.x;
+        const int v = c < ncell ? cnt[c] : 0;
+        int ex, agg;
+        Scan(tmp).ExclusiveSum(v, ex, agg);
+        if (c < ncell) {
+            start[c] = carry + ex;
+            cursor[c] = carry + ex;
+            cnt[c] = 0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) start[ncell] = carry;
+}
+
+__global__ void boids_scatter_kernel(const float4* __restrict__ st, const int32_t* __restrict__ ids, int64_t n,
+                                     const int* __restrict__ cell_of, int* __restrict__ cursor, float4* __restrict__ sorted,
+                                     int32_t* __restrict__ sorted_ids)
+{
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const int q = atomicAdd(cursor + cell_of[p], 1);
+        sorted[q] = st[p];
+        sorted_ids[q] = ids[p];
+    }
+}
+
+struct Acc {
+    long long n, sdx, sdy, svx, svy, ssx, ssy;
+};
+
+__device__ __forceinline__ long long q24(float f) { return __float2ll_rn(__fmul_rn(f, kFix)); }
+
+__device__ __forceinline__ float min_image(float d, float L, float halfL)
+{
+    if (d > halfL) return __fsub_rn(d, L);
+    if (d < -halfL) return __fadd_rn(d, L);
+    return d;
+}
+
+struct BoidsSlot {
+    double mean_speed, polar_x, polar_y;
+    unsigned long long digest;
+};
+
+// B2-B6 for every agent (sorted order in, sorted order out).
+__global__ void __launch_bounds__(256) boids_step_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ sids,
+                                                         const int* __restrict__ start, int64_t n, BoidsArgs a,
+                                                         float4* __restrict__ out, int32_t* __restrict__ out_ids,
+                                                         BoidsSlot* slot, int digest)
+{
+    const float L = a.L, halfL = __fmul_rn(0.5f, a.L), R2 = __fmul_rn(a.R, a.R), rs2 = __fmul_rn(a.rs, a.rs);
+    double sp_sum = 0.0, ux_sum = 0.0, uy_sum = 0.0;
+    unsigned long long dig = 0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const float4 me = sorted[p];
+        const int cx = cell_coord(me.x, a), cy = cell_coord(me.y, a);
+        Acc acc{0, 0, 0, 0, 0, 0, 0};
+        const int span = a.nc >= 3 ? 1 : 0;  // nc == 1: the single cell is visited once
+#pragma unroll 1
+        for (int dyc = -span; dyc <= span; ++dyc) {
+            int yy = cy + dyc;
+            yy = yy < 0 ? yy + a.nc : (yy >= a.nc ? yy - a.nc : yy);
+#pragma unroll 1
+            for (int dxc = -span; dxc <= span; ++dxc) {
+                int xx = cx + dxc;
+                xx = xx < 0 ? xx + a.nc : (xx >= a.nc ? xx - a.nc : xx);
+                const int c = yy * a.nc + xx;
+                const int b = start[c], e = start[c + 1];
+                for (int q = b; q < e; ++q) {
+                    if (q == p) continue;
+                    const float4 o = sorted[q];
+                    const float dx = min_image(__fsub_rn(o.x, me.x), L, halfL);
+                    const float dy = min_image(__fsub_rn(o.y, me.y), L, halfL);
+                    const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+                    if (d2 <= R2) {
+                        const long long qx = q24(dx), qy = q24(dy);
+                        acc.n += 1;
+                        acc.sdx += qx;
+                        acc.sdy += qy;
+                        acc.svx += q24(o.z);
+                        acc.svy += q24(o.w);
+                        if (d2 <= rs2) {
+                            acc.ssx += qx;
+                            acc.ssy += qy;
+                        }
+                    }
+                }
+            }
+        }
+        float ux = me.z, uy = me.w;
+        if (acc.n > 0) {
+            const double nd = static_cast<double>(acc.n);
+            const double fix = 16777216.0;
+            const float cohx = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.sdx), fix), nd));
+            const float cohy = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.sdy), fix), nd));
+            const float avx = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.svx), fix), nd));
+            const float avy = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.svy), fix), nd));
+            const float sepx = __double2float_rn(__ddiv_rn(static_cast<double>(acc.ssx), fix));
+            const float sepy = __double2float_rn(__ddiv_rn(static_cast<double>(acc.ssy), fix));
+            ux = __fsub_rn(__fadd_rn(__fadd_rn(me.z, __fmul_rn(a.wc, cohx)), __fmul_rn(a.wa, __fsub_rn(avx, me.z))),
+                           __fmul_rn(a.ws, sepx));
+            uy = __fsub_rn(__fadd_rn(__fadd_rn(me.w, __fmul_rn(a.wc, cohy)), __fmul_rn(a.wa, __fsub_rn(avy, me.w))),
+                           __fmul_rn(a.ws, sepy));
+        }
+        const float s2 = __fadd_rn(__fmul_rn(ux, ux), __fmul_rn(uy, uy));
+        if (s2 > __fmul_rn(a.vmax, a.vmax)) {
+            const float f = __fdiv_rn(a.vmax, __fsqrt_rn(s2));
+            ux = __fmul_rn(ux, f);
+            uy = __fmul_rn(uy, f);
+        }
+        float x = __fadd_rn(me.x, __fmul_rn(ux, a.dt));
+        float y = __fadd_rn(me.y, __fmul_rn(uy, a.dt));
+        if (x < 0.0f) x = __fadd_rn(x, L);
+        if (x >= L) x = __fsub_rn(x, L);
+        if (y < 0.0f) y = __fadd_rn(y, L);
+        if (y >= L) y = __fsub_rn(y, L);
+        out[p] = make_float4(x, y, ux, uy);
+        const int32_t id = sids[p];
+        out_ids[p] = id;
+        // observables (B8), in double
+        const double dvx = static_cast<double>(ux), dvy = static_cast<double>(uy);
+        const double sp = __dsqrt_rn(__dadd_rn(__dmul_rn(dvx, dvx), __dmul_rn(dvy, dvy)));
+        sp_sum += sp;
+        if (sp > 0.0) {
+            ux_sum += __ddiv_rn(dvx, sp);
+            uy_sum += __ddiv_rn(dvy, sp);
+        }
+        if (digest) dig += digest_term(static_cast<unsigned long long>(id), __float_as_uint(x));
+    }
+    // block reduction of the observables
+    __shared__ double red[3][32];
+    __shared__ unsigned long long dred[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    sp_sum = warp_sum_f64(sp_sum);
+    ux_sum = warp_sum_f64(ux_sum);
+    uy_sum = warp_sum_f64(uy_sum);
+    dig = warp_sum_u64(dig);
+    if (lane == 0) {
+        red[0][wid] = sp_sum;
+        red[1][wid] = ux_sum;
+        red[2][wid] = uy_sum;
+        dred[wid] = dig;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        double s0 = lane < nw ? red[0][lane] : 0.0, s1 = lane < nw ? red[1][lane] : 0.0, s2v = lane < nw ? red[2][lane] : 0.0;
+        unsigned long long d = lane < nw ? dred[lane] : 0ull;
+        s0 = warp_sum_f64(s0);
+        s1 = warp_sum_f64(s1);
+        s2v = warp_sum_f64(s2v);
+        d = warp_sum_u64(d);
+        if (lane == 0) {
+            atomicAdd(&slot->mean_speed, s0);
+            atomicAdd(&slot->polar_x, s1);
+            atomicAdd(&slot->polar_y, s2v);
+            if (digest) atomicAdd(&slot->digest, d);
+        }
+    }
+}
+
+// Un-permute: column k of the state (0 x, 1 y, 2 vx, 3 vy) into id order.
+__global__ void boids_gather_column(const float4* __restrict__ st, const int32_t* __restrict__ ids, int64_t n, int k,
+                                    float* __restrict__ out)
+{
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const float4 s = st[p];
+        out[ids[p]] = k == 0 ? s.x : (k == 1 ? s.y : (k == 2 ? s.z : s.w));
+    }
+}
+
+__global__ void boids_put_column(float4* __restrict__ st, const int32_t* __restrict__ ids, int64_t n, int k,
+                                 const float* __restrict__ in)
+{
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const float v = in[ids[p]];
+        float4 s = st[p];
+        if (k == 0) s.x = v;
+        else if (k == 1) s.y = v;
+        else if (k == 2) s.z = v;
+        else s.w = v;
+        st[p] = s;
+    }
+}
+
+__global__ void boids_zero_slots(BoidsSlot* ring, int64_t cap, int64_t s0, int64_t count)
+{
+    for (int64_t k = threadIdx.x; k < count && k < cap; k += blockDim.x) ring[(s0 + k) % cap] = BoidsSlot{0.0, 0.0, 0.0, 0ull};
+}
+
+}  // namespace
+
+class BoidsModel final : public Model {
+public:
+    int64_t n = 0;
+    amber_boids_params p{};
+    uint64_t seed = 0;
+    BoidsArgs ba{};
+    DevBuf<float4> st, sorted;
+    DevBuf<int32_t> ids, sids;
+    DevBuf<int> cnt, start, cursor, cell_of;
+    DevBuf<float> col_tmp;
+    DevBuf<BoidsSlot> ring;
+    int64_t m_first = 0;
+    int ncell = 0;
+
+    BoidsModel(int64_t n_, const amber_boids_params& p_, uint64_t seed_, const amber_runtime* r)
+    {
+        rt.init(r);
+        n = n_;
+        p = p_;
+        seed = seed_;
+        AMBER_REQUIRE(n >= 1 && n < (1ll << 31), "Boids needs 1 <= n_agents < 2^31");
+        AMBER_REQUIRE(p.L > 0 && p.R > 0 && p.rs >= 0 && p.rs <= p.R && p.vmax > 0 && p.dt >= 0,
+                      "Boids params out of range (need L, R, vmax > 0, 0 <= rs <= R, dt >= 0)");
+        AMBER_REQUIRE(p.R < 0.5f * p.L && p.vmax * p.dt < 0.5f * p.L, "Boids needs R < L/2 and vmax*dt < L/2");
+        ba = BoidsArgs{p.L, p.R, p.rs, p.wc, p.wa, p.ws, p.vmax, p.dt, 0, 0.f};
+        // Cells of side >= R*(1+1e-3): float rounding of the cell index can then
+        // never hide a neighbour outside the 3x3 stencil.  The stencil needs >= 3
+        // distinct cells per side; boxes with fewer use one cell holding every
+        // agent (each agent then scans all others, i.e. the brute-force definition).
+        double nc = std::floor(static_cast<double>(p.L) / (static_cast<double>(p.R) * 1.001));
+        nc = std::min(nc, 4096.0);
+        ba.nc = static_cast<int>(nc >= 3 ? nc : 1);
+        ba.inv_cs = static_cast<float>(ba.nc / static_cast<double>(p.L));
+        ncell = ba.nc * ba.nc;
+        st.allocate(&rt, n);
+        sorted.allocate(&rt, n);
+        ids.allocate(&rt, n);
+        sids.allocate(&rt, n);
+        cnt.allocate(&rt, ncell + 1);
+        cnt.zero_async(rt.stream);
+        start.allocate(&rt, ncell + 1);
+        cursor.allocate(&rt, ncell + 1);
+        cell_of.allocate(&rt, n);
+        ring.allocate(&rt, metrics_cap);
+        ring.zero_async(rt.stream);
+        boids_init_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(philox_key(seed), n, p.L, st.p, ids.p);
+        check_launch("boids_init_kernel");
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    }
+
+    ~BoidsModel() override
+    {
+        if (rt.stream) cudaStreamSynchronize(rt.stream);
+        st.reset(); sorted.reset(); ids.reset(); sids.reset(); cnt.reset(); start.reset(); cursor.reset();
+        cell_of.reset(); col_tmp.reset(); ring.reset();
+        rt.destroy();
+    }
+
+    int grid_for(int threads) const
+    {
+        if (grid) return static_cast<int>(grid);
+        return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), rt.num_sms * 16)));
+    }
+
+    void step(int64_t nsteps) override
+    {
+        AMBER_REQUIRE(nsteps >= 0, "n_steps must be >= 0");
+        const int threads = block ? static_cast<int>(std::min<int64_t>(block, 256)) : 256;
+        for (int64_t k = 0; k < nsteps; ++k) {
+            boids_zero_slots<<<1, 32, 0, rt.stream>>>(ring.p, metrics_cap, t, 1);
+            check_launch("boids_zero_slots");
+            if (ba.nc == 1) {
+                // degenerate small box: one cell holding every agent (the stencil
+                // visits it once); count = n, start = {0, n}
+                const int h[2] = {0, static_cast<int>(n)};
+                AMBER_CUDA(cudaMemcpyAsync(start.p, h, sizeof(h), cudaMemcpyHostToDevice, rt.stream));
+                AMBER_CUDA(cudaMemcpyAsync(sorted.p, st.p, n * sizeof(float4), cudaMemcpyDeviceToDevice, rt.stream));
+                AMBER_CUDA(cudaMemcpyAsync(sids.p, ids.p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, rt.stream));
+            } else {
+                prof.launch(rt.stream, "boids_bin", [&] {
+                    boids_count_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(st.p, n, ba, cnt.p, cell_of.p);
+                });
+                check_launch("boids_count_kernel");
+                prof.launch(rt.stream, "boids_scan", [&] {
+                    boids_scan_kernel<<<1, 1024, 0, rt.stream>>>(cnt.p, start.p, cursor.p, ncell);
+                });
+                check_launch("boids_scan_kernel");
+                prof.launch(rt.stream, "boids_scatter", [&] {
+                    boids_scatter_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(st.p, ids.p, n, cell_of.p,
+                                                                                       cursor.p, sorted.p, sids.p);
+                });
+                check_launch("boids_scatter_kernel");
+            }
+            const BoidsArgs a = ba;
+            prof.launch(rt.stream, "boids_step", [&] {
+                boids_step_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a, st.p,
+                                                                                ids.p, ring.p + (t % metrics_cap),
+                                                                                digest_on ? 1 : 0);
+            });
+            check_launch("boids_step_kernel");
+            ++t;
+        }
+    }
+
+    int col_index(const std::string& k) const
+    {
+        if (k == "pos_x") return 0;
+        if (k == "pos_y") return 1;
+        if (k == "vel_x") return 2;
+        if (k == "vel_y") return 3;
+        return -1;
+    }
+
+    bool column_info(const char* name, amber_dtype* dt, int64_t* glen, int64_t* off, int64_t* len) override
+    {
+        if (col_index(name) < 0) return false;
+        if (dt) *dt = AMBER_F32;
+        if (glen) *glen = n;
+        if (off) *off = 0;
+        if (len) *len = n;
+        return true;
+    }
+
+    void read_column(const char* name, void* dst, size_t bytes, bool on_dev) override
+    {
+        const int k = col_index(name);
+        if (k < 0) fail(AMBER_E_UNKNOWN_NAME, std::string("no column ") + name);
+        if (bytes < static_cast<size_t>(n) * 4) fail(AMBER_E_BUFFER_TOO_SMALL, "dst too small");
+        if (!col_tmp.p) col_tmp.allocate(&rt, n);
+        boids_gather_column<<<grid_for(256), 256, 0, rt.stream>>>(st.p, ids.p, n, k, col_tmp.p);
+        check_launch("boids_gather_column");
+        copy_out(rt, dst, col_tmp.p, n * 4, on_dev);
+    }
+
+    void write_column(const char* name, const void* src, size_t bytes, bool on_dev) override
+    {
+        const int k = col_index(name);
+        if (k < 0) fail(AMBER_E_UNKNOWN_NAME, std::string("no column ") + name);
+        if (bytes < static_cast<size_t>(n) * 4) fail(AMBER_E_BUFFER_TOO_SMALL, "src too small");
+        if (!col_tmp.p) col_tmp.allocate(&rt, n);
+        copy_in(rt, col_tmp.p, src, n * 4, on_dev);
+        boids_put_column<<<grid_for(256), 256, 0, rt.stream>>>(st.p, ids.p, n, k, col_tmp.p);
+        check_launch("boids_put_column");
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    }
+
+    void read_metrics(const char* name, void* dst, size_t bytes, int64_t* n_out) override
+    {
+        std::string k(name);
+        if (k != "mean_speed" && k != "polarisation" && !(k == "digest" && digest_on))
+            fail(AMBER_E_UNKNOWN_NAME, "no metric " + k);
+        std::vector<BoidsSlot> h(metrics_cap);
+        AMBER_CUDA(cudaMemcpyAsync(h.data(), ring.p, metrics_cap * sizeof(BoidsSlot), cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        const int64_t first = std::max(m_first, t - metrics_cap + 1);
+        const int64_t cnt_ = std::max<int64_t>(t - first, 0);
+        if (bytes < static_cast<size_t>(cnt_) * 8) fail(AMBER_E_BUFFER_TOO_SMALL, "metrics dst too small");
+        for (int64_t s = first; s < t; ++s) {
+            const BoidsSlot& x = h[s % metrics_cap];
+            if (k == "mean_speed") static_cast<double*>(dst)[s - first] = x.mean_speed / static_cast<double>(n);
+            else if (k == "polarisation")
+                static_cast<double*>(dst)[s - first] = std::sqrt(x.polar_x * x.polar_x + x.polar_y * x.polar_y) / static_cast<double>(n);
+            else static_cast<unsigned long long*>(dst)[s - first] = x.digest;
+        }
+        if (n_out) *n_out = cnt_;
+    }
+
+    void reset_metrics() override
+    {
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        m_first = t;
+    }
+
+    uint64_t digest(const char* name) override
+    {
+        const int k = col_index(name);
+        if (k < 0) fail(AMBER_E_UNKNOWN_NAME, std::string("no column ") + name);
+        if (!col_tmp.p) col_tmp.allocate(&rt, n);
+        boids_gather_column<<<grid_for(256), 256, 0, rt.stream>>>(st.p, ids.p, n, k, col_tmp.p);
+        check_launch("boids_gather_column");
+        return device_digest_u32(rt, reinterpret_cast<const uint32_t*>(col_tmp.p), n, 0);
+    }
+
+    void set_step(int64_t s) override
+    {
+        AMBER_REQUIRE(s >= 0, "step out of range");
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        t = s;
+        m_first = s;
+    }
+
+    bool set_option(const char* key, int64_t v) override
+    {
+        std::string k(key);
+        if (k == "metrics_capacity") {
+            AMBER_REQUIRE(v >= 16, "metrics_capacity must be >= 16");
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            metrics_cap = v;
+            ring.allocate(&rt, metrics_cap);
+            ring.zero_async(rt.stream);
+            m_first = t;
+            return true;
+        }
+        if (k == "block") AMBER_REQUIRE(v <= 256, "Boids kernels are built for <= 256 threads per block");
+        return Model::set_option(key, v);
+    }
+
+    bool get_option(const char* key, int64_t* v) override
+    {
+        if (std::string(key) == "cells_per_side") {
+            *v = ba.nc;
+            return true;
+        }
+        return Model::get_option(key, v);
+    }
+};
+
+Model* make_boids(int64_t n, const amber_boids_params& p, uint64_t seed, const amber_runtime* rt)
+{
+    return new BoidsModel(n, p, seed, rt);
+}
+
+}  // namespace amber

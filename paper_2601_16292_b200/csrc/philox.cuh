@@ -27,7 +27,7 @@ struct PhiloxKey {
 };
 
 // R2: key = (lo32(seed), hi32(seed)); round r uses key + r*(W0, W1).
-inline PhiloxKey philox_key(uint64_t seed)
+__host__ __device__ inline PhiloxKey philox_key(uint64_t seed)
 {
     PhiloxKey k;
     uint32_t a = static_cast<uint32_t>(seed), b = static_cast<uint32_t>(seed >> 32);
@@ -39,6 +39,8 @@ inline PhiloxKey philox_key(uint64_t seed)
     }
     return k;
 }
+
+__device__ __forceinline__ PhiloxKey philox_key_dev(uint64_t seed) { return philox_key(seed); }
 
 // R1: the block function.
 __device__ __forceinline__ uint4 philox(uint4 c, const PhiloxKey& K)

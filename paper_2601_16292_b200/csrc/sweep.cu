@@ -1,0 +1,289 @@
+// sweep.cu -- batched SIR replicate sweep (Sec. 4.2
+// "configurable replication counts", Sec. 4.4 line 191 ParallelRunner;
+// BASELINE config 5; S5-S6).
+//
+// All replicates' graphs and initial states are built on the device in one
+// batch (sir.cu builders).  The stepping kernel is persistent: a CTA takes
+// the next replicate from a work queue (ordered by beta, largest first, so the
+// longest epidemics start first), stages its CSR (row offsets as u32, column
+// ids as u16 when n <= 65536) and both state buffers in shared memory, runs
+// all steps there with one __syncthreads per step, and stops early once no
+// agent is infected (later steps cannot change the state: S needs an I
+// neighbour and only I agents move).  Final R / n goes to out[r].
+#include <algorithm>
+#include <numeric>
+
+#include "graph.cuh"
+#include "internal.cuh"
+#include "philox.cuh"
+
+namespace amber {
+
+struct Comm;
+Comm* make_comm(const amber_runtime* r);
+void destroy_comm(Comm* c);
+void comm_allgather_f64(Comm* c, cudaStream_t s, const double* send, double* recv, size_t n_per_rank);
+void comm_allreduce_u64(Comm* c, cudaStream_t s, unsigned long long* d, size_t n);
+
+namespace {
+
+constexpr uint8_t kS = 0, kI = 1, kR = 2;
+
+struct SweepArgs {
+    const int32_t* row_ptr;  // R*n + 1 (global offsets)
+    const int32_t* col;      // replicate-local ids
+    const uint8_t* state0;   // R * n_pad
+    const unsigned long long* seeds;
+    const unsigned long long* t_beta;  // per replicate
+    const int* order;        // processing order
+    unsigned long long t_gamma;
+    int64_t R, n, n_pad, steps;
+    int* next;               // work-queue counter
+    double* out;             // final R fraction per replicate
+    unsigned long long* active_updates;
+    int col_smem;            // 1: stage col as u16 in shared memory
+    int64_t col_cap;         // u16 entries reserved in shared memory
+};
+
+template <bool COL_SMEM>
+__global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t* rp = reinterpret_cast<uint32_t*>(smem);                  // n + 1
+    uint16_t* cs = reinterpret_cast<uint16_t*>(rp + ((a.n + 4) & ~3ll));  // col_cap (COL_SMEM)
+    uint8_t* xs = reinterpret_cast<uint8_t*>(cs + (COL_SMEM ? ((a.col_cap + 7) & ~7ll) : 0));
+    uint8_t* st[2] = {xs, xs + a.n_pad};
+    __shared__ int rep_s;
+    __shared__ int cnt_s[2];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int64_t nq = a.n_pad / 4;
+
+    for (;;) {
+        if (tid == 0) rep_s = atomicAdd(a.next, 1);
+        __syncthreads();
+        const int slot = rep_s;
+        __syncthreads();
+        if (slot >= a.R) break;
+        const int r = a.order[slot];
+        const int32_t base = a.row_ptr[static_cast<int64_t>(r) * a.n];
+        const int32_t* gcol = a.col + base;
+        for (int64_t v = tid; v <= a.n; v += nt) rp[v] = static_cast<uint32_t>(a.row_ptr[r * a.n + v] - base);
+        __syncthreads();
+        if constexpr (COL_SMEM) {
+            const uint32_t na = rp[a.n];
+            for (uint32_t p = tid; p < na; p += nt) cs[p] = static_cast<uint16_t>(gcol[p]);
+        }
+        const uchar4* s0 = reinterpret_cast<const uchar4*>(a.state0 + static_cast<int64_t>(r) * a.n_pad);
+        for (int64_t q = tid; q < nq; q += nt) reinterpret_cast<uchar4*>(st[0])[q] = s0[q];
+        if (tid == 0) cnt_s[0] = cnt_s[1] = 0;
+        __syncthreads();
+        const PhiloxKey key = philox_key(a.seeds[r]);
+        const unsigned long long tb = a.t_beta[r];
+        int cur = 0;
+        int64_t executed = a.steps;
+        for (int64_t t = 0; t < a.steps; ++t) {
+            const uint8_t* x = st[cur];
+            uint8_t* y = st[cur ^ 1];
+            int n_inf = 0;
+            for (int64_t q = tid; q < nq; q += nt) {
+                const uchar4 v = reinterpret_cast<const uchar4*>(x)[q];
+                const uint8_t in[4] = {v.x, v.y, v.z, v.w};
+                uint8_t o[4];
+                uint4 rec = make_uint4(0u, 0u, 0u, 0u);
+                if (in[0] == kI || in[1] == kI || in[2] == kI || in[3] == kI)
+                    rec = stream_block(key, TAG_SIR_REC, static_cast<unsigned long long>(q), static_cast<uint32_t>(t));
+                const uint32_t rw[4] = {rec.x, rec.y, rec.z, rec.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t i = static_cast<uint32_t>(4 * q + k);
+                    o[k] = in[k];
+                    if (in[k] == kS) {
+                        bool inf = false;
+                        const uint32_t b = rp[i], e = rp[i + 1];
+                        for (uint32_t p = b; p < e && !inf; ++p) {
+                            const uint32_t j = COL_SMEM ? static_cast<uint32_t>(cs[p]) : static_cast<uint32_t>(gcol[p]);
+                            if (x[j] == kI) {
+                                const uint4 w = philox(make_uint4(min(i, j), max(i, j), static_cast<uint32_t>(t), TAG_SIR_TX), key);
+                                inf = static_cast<unsigned long long>(w.x) < tb;
+                            }
+                        }
+                        if (inf) o[k] = kI;
+                    } else if (in[k] == kI) {
+                        if (static_cast<unsigned long long>(rw[k]) < a.t_gamma) o[k] = kR;
+                    }
+                    n_inf += (o[k] == kI);
+                }
+                reinterpret_cast<uchar4*>(y)[q] = make_uchar4(o[0], o[1], o[2], o[3]);
+            }
+            n_inf = __reduce_add_sync(0xffffffffu, n_inf);
+            if ((tid & 31) == 0 && n_inf) atomicAdd(&cnt_s[t & 1], n_inf);
+            __syncthreads();
+            const int total_inf = cnt_s[t & 1];
+            if (tid == 0) cnt_s[(t + 1) & 1] = 0;
+            cur ^= 1;
+            __syncthreads();
+            if (total_inf == 0) {
+                executed = t + 1;
+                break;
+            }
+        }
+        // final R count
+        int n_rec = 0;
+        for (int64_t i = tid; i < a.n; i += nt) n_rec += (st[cur][i] == kR);
+        n_rec = __reduce_add_sync(0xffffffffu, n_rec);
+        if (tid == 0) cnt_s[0] = 0;
+        __syncthreads();
+        if ((tid & 31) == 0 && n_rec) atomicAdd(&cnt_s[0], n_rec);
+        __syncthreads();
+        if (tid == 0) {
+            a.out[r] = static_cast<double>(cnt_s[0]) / static_cast<double>(a.n);
+            atomicAdd(a.active_updates, static_cast<unsigned long long>(executed) * a.n);
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+void run_sweep(int64_t n, const amber_sir_params& base, const amber_replicate* reps, int64_t n_reps, int64_t n_steps,
+               const amber_runtime* r, double* out, amber_sweep_stats* stats)
+{
+    Runtime rt;
+    rt.init(r);
+    struct Guard {
+        Runtime& rt;
+        ~Guard() { rt.destroy(); }
+    } guard{rt};
+    AMBER_REQUIRE(n >= 2 && n < (1ll << 31), "sweep needs 2 <= n_agents < 2^31");
+    AMBER_REQUIRE(base.gamma >= 0 && base.gamma <= 1 && base.init_frac >= 0 && base.init_frac <= 1 &&
+                      base.mean_degree >= 0,
+                  "sweep params out of range");
+    const int W = rt.world, me = rt.rank;
+    const int64_t per = ceil_div(std::max<int64_t>(n_reps, 1), W);
+    const int64_t r0 = std::min<int64_t>(per * me, n_reps), r1 = std::min<int64_t>(per * (me + 1), n_reps);
+    const int64_t R = r1 - r0;
+    const int64_t m = static_cast<int64_t>(std::floor(static_cast<double>(n) * base.mean_degree / 2.0 + 0.5));
+    const int64_t k_inf = static_cast<int64_t>(std::floor(base.init_frac * static_cast<double>(n) + 0.5));
+    const int64_t n_pad = ceil_div(n, 16) * 16;
+    std::vector<double> local(std::max<int64_t>(per, 1), 0.0);
+    double build_ms = 0, step_ms = 0;
+    unsigned long long active = 0;
+    cudaEvent_t e0, e1, e2;
+    AMBER_CUDA(cudaEventCreate(&e0));
+    AMBER_CUDA(cudaEventCreate(&e1));
+    AMBER_CUDA(cudaEventCreate(&e2));
+    // batches bound the setup memory (sort buffers) for very large sweeps
+    const int64_t batch_cap = std::max<int64_t>(1, std::min<int64_t>(R, ((1ll << 31) - 1) / std::max<int64_t>(2 * m, 1)));
+    for (int64_t b0 = 0; b0 < R; b0 += batch_cap) {
+        const int64_t B = std::min(batch_cap, R - b0);
+        std::vector<unsigned long long> seeds(B), tb(B);
+        std::vector<std::pair<double, int>> ord(B);
+        for (int64_t k = 0; k < B; ++k) {
+            const amber_replicate& rep = reps[r0 + b0 + k];
+            AMBER_REQUIRE(rep.beta >= 0 && rep.beta <= 1, "replicate beta out of [0,1]");
+            seeds[k] = rep.seed;
+            tb[k] = bernoulli_threshold_host(rep.beta);
+            ord[k] = {-rep.beta, static_cast<int>(k)};
+        }
+        std::stable_sort(ord.begin(), ord.end());
+        std::vector<int> order(B);
+        for (int64_t k = 0; k < B; ++k) order[k] = ord[k].second;
+        AMBER_CUDA(cudaEventRecord(e0, rt.stream));
+        Graphs g;
+        build_graphs(rt, seeds, n, m, g);
+        DevBuf<uint8_t> st0;
+        st0.allocate(&rt, B * n_pad);
+        build_init_state(rt, seeds, n, n_pad, k_inf, st0.p);
+        DevBuf<unsigned long long> d_seeds, d_tb, d_active;
+        DevBuf<int> d_order, d_next;
+        DevBuf<double> d_out;
+        d_seeds.allocate(&rt, B);
+        d_tb.allocate(&rt, B);
+        d_order.allocate(&rt, B);
+        d_next.allocate(&rt, 1);
+        d_out.allocate(&rt, B);
+        d_active.allocate(&rt, 1);
+        AMBER_CUDA(cudaMemcpyAsync(d_seeds.p, seeds.data(), B * 8, cudaMemcpyHostToDevice, rt.stream));
+        AMBER_CUDA(cudaMemcpyAsync(d_tb.p, tb.data(), B * 8, cudaMemcpyHostToDevice, rt.stream));
+        AMBER_CUDA(cudaMemcpyAsync(d_order.p, order.data(), B * sizeof(int), cudaMemcpyHostToDevice, rt.stream));
+        d_next.zero_async(rt.stream);
+        d_active.zero_async(rt.stream);
+        // max arcs of any replicate in the batch (for the shared-memory column stage)
+        std::vector<int32_t> h_rp(B * n + 1);
+        AMBER_CUDA(cudaMemcpyAsync(h_rp.data(), g.row_ptr.p, (B * n + 1) * 4, cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        int64_t max_arcs = 0;
+        for (int64_t k = 0; k < B; ++k) max_arcs = std::max<int64_t>(max_arcs, h_rp[(k + 1) * n] - h_rp[k * n]);
+        AMBER_CUDA(cudaEventRecord(e1, rt.stream));
+        SweepArgs a{};
+        a.row_ptr = g.row_ptr.p;
+        a.col = g.col.p;
+        a.state0 = st0.p;
+        a.seeds = d_seeds.p;
+        a.t_beta = d_tb.p;
+        a.order = d_order.p;
+        a.t_gamma = bernoulli_threshold_host(base.gamma);
+        a.R = B;
+        a.n = n;
+        a.n_pad = n_pad;
+        a.steps = n_steps;
+        a.next = d_next.p;
+        a.out = d_out.p;
+        a.active_updates = d_active.p;
+        int smem_max = 0;
+        AMBER_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, rt.device));
+        const size_t rp_bytes = ((n + 4) & ~3ll) * 4, st_bytes = 2 * n_pad;
+        const size_t col_bytes = ((max_arcs + 7) & ~7ll) * 2;
+        const bool col_smem = n <= 65536 && rp_bytes + col_bytes + st_bytes + 64 <= static_cast<size_t>(smem_max);
+        a.col_smem = col_smem;
+        a.col_cap = col_smem ? max_arcs : 0;
+        size_t smem = rp_bytes + (col_smem ? col_bytes : 0) + st_bytes;
+        AMBER_REQUIRE(smem + 64 <= static_cast<size_t>(smem_max), "sweep: replicate state does not fit shared memory");
+        auto kern = col_smem ? sir_sweep_kernel<true> : sir_sweep_kernel<false>;
+        AMBER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        int per_sm = 0;
+        AMBER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1024, smem));
+        const int blocks = static_cast<int>(std::min<int64_t>(std::max(per_sm, 1) * rt.num_sms, B));
+        if (B > 0) {
+            kern<<<blocks, 1024, smem, rt.stream>>>(a);
+            check_launch("sir_sweep_kernel");
+        }
+        AMBER_CUDA(cudaEventRecord(e2, rt.stream));
+        AMBER_CUDA(cudaMemcpyAsync(local.data() + b0, d_out.p, B * 8, cudaMemcpyDeviceToHost, rt.stream));
+        unsigned long long act = 0;
+        AMBER_CUDA(cudaMemcpyAsync(&act, d_active.p, 8, cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        float f1 = 0, f2 = 0;
+        AMBER_CUDA(cudaEventElapsedTime(&f1, e0, e1));
+        AMBER_CUDA(cudaEventElapsedTime(&f2, e1, e2));
+        build_ms += f1;
+        step_ms += f2;
+        active += act;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    if (W > 1) {
+        Comm* c = make_comm(r);
+        DevBuf<double> d_loc, d_all;
+        d_loc.allocate(&rt, per);
+        d_all.allocate(&rt, per * W);
+        AMBER_CUDA(cudaMemcpyAsync(d_loc.p, local.data(), per * 8, cudaMemcpyHostToDevice, rt.stream));
+        comm_allgather_f64(c, rt.stream, d_loc.p, d_all.p, per);
+        std::vector<double> all(per * W);
+        AMBER_CUDA(cudaMemcpyAsync(all.data(), d_all.p, per * W * 8, cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        destroy_comm(c);
+        for (int64_t k = 0; k < n_reps; ++k) out[k] = all[k];  // rank g's block starts at g*per
+    } else {
+        for (int64_t k = 0; k < n_reps; ++k) out[k] = local[k];
+    }
+    if (stats) {
+        stats->build_ms = build_ms;
+        stats->step_ms = step_ms;
+        stats->agent_updates = n * n_steps * R;
+        stats->active_updates = static_cast<int64_t>(active);
+    }
+}
+
+}  // namespace amber

@@ -1,0 +1,142 @@
+"""GPU parity: SIR on G(n, M) (C2) and the replicate sweep (C5) vs the oracle, bit-exact."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from paper_2601_16292_b200 import Model, sir_params, sweep
+from paper_2601_16292_b200.workloads import C2_SIR, C5_SWEEP, sir_counts, sweep_replicates
+
+
+def make(cfg, **kw):
+    p = sir_params(cfg["mean_degree"], cfg["beta"], cfg["gamma"], cfg["init_frac"])
+    return Model("sir", cfg["n"], p, cfg["seed"], **kw)
+
+
+@pytest.mark.parametrize("n,kbar,seed", [(2, 1.0, 1), (50, 4.0, 3), (1000, 10.0, 7), (100_000, 10.0, 7)])
+def test_graph_and_initial_state(orc, n, kbar, seed):
+    cfg = dict(n=n, mean_degree=kbar, beta=0.05, gamma=0.1, init_frac=0.01, seed=seed)
+    m = make(cfg)
+    m_draws, k = sir_counts(cfg)
+    rp, col, mu = orc.er_graph(n, m_draws, seed)
+    assert np.array_equal(m.read_column("row_ptr"), rp)
+    assert np.array_equal(m.read_column("col_idx"), col)
+    assert m.get_option("edges") == mu
+    assert np.array_equal(m.read_column("state"), orc.sir_init(n, k, seed))
+
+
+@pytest.mark.parametrize("persistent", [0, 1])
+def test_c2_every_step_bit_exact(orc, persistent):
+    cfg = C2_SIR
+    m = make(cfg)
+    m.set_option("persistent", persistent)
+    m.set_option("digest", 1)
+    rp = m.read_column("row_ptr")
+    col = m.read_column("col_idx")
+    st = orc.sir_init(cfg["n"], sir_counts(cfg)[1], cfg["seed"])
+    st_ref, counts, dig = orc.sir_run(rp, col, st, cfg["seed"], cfg["beta"], cfg["gamma"], 0,
+                                      cfg["steps"], digests=True)
+    if persistent:
+        m.step(cfg["steps"])
+    else:
+        x = st.copy()
+        for t in range(cfg["steps"]):
+            m.step(1)
+            x = orc.sir_step(rp, col, x, cfg["seed"], t, cfg["beta"], cfg["gamma"])
+            if t % 20 == 0:
+                assert np.array_equal(m.read_column("state"), x), f"step {t}"
+    assert np.array_equal(m.read_column("state"), st_ref)
+    for k, name in enumerate("SIR"):
+        assert np.array_equal(m.metrics(name), counts[:, k]), name
+    assert np.array_equal(m.metrics("digest"), dig.astype(np.uint64))
+    assert m.digest("state") == orc.digest(st_ref)
+
+
+@pytest.mark.parametrize("beta,gamma", [(0.0, 0.3), (1.0, 0.0), (1.0, 1.0), (0.3, 1.0)])
+def test_special_cases(orc, beta, gamma):
+    cfg = dict(n=3000, mean_degree=5.0, beta=beta, gamma=gamma, init_frac=0.003, seed=21)
+    m = make(cfg)
+    m.step(12)
+    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
+    st = orc.sir_init(3000, 9, 21)
+    ref, _, _ = orc.sir_run(rp, col, st, 21, beta, gamma, 0, 12)
+    assert np.array_equal(m.read_column("state"), ref)
+
+
+def test_geometry_and_chunking_invariance(orc):
+    cfg = dict(C2_SIR, n=20_000, steps=40)
+    a = make(cfg)
+    a.step(40)
+    b = make(cfg)
+    b.set_option("persistent", 0)
+    b.set_option("block", 64)
+    b.step(17)
+    b.step(23)
+    c = make(cfg)
+    c.set_option("grid", 5)
+    c.step(40)
+    ref = a.read_column("state")
+    assert np.array_equal(b.read_column("state"), ref)
+    assert np.array_equal(c.read_column("state"), ref)
+
+
+def test_checkpoint_resume_state():
+    cfg = dict(C2_SIR, n=20_000)
+    full = make(cfg)
+    full.step(60)
+    a = make(cfg)
+    a.step(30)
+    saved = a.read_column("state")
+    b = make(cfg)
+    b.write_column("state", saved)
+    b.set_step(30)
+    b.step(30)
+    assert np.array_equal(b.read_column("state"), full.read_column("state"))
+
+
+def test_sweep_subset_bit_exact(orc):
+    c = C5_SWEEP
+    betas, seeds = sweep_replicates(c)
+    pick = np.arange(0, 4096, 61)  # 68 replicates spanning all betas
+    got = sweep(c["n"], sir_params(c["mean_degree"], 0.0, c["gamma"], c["init_frac"]), betas[pick],
+                seeds[pick], c["steps"])
+    want = orc.sir_sweep(c["n"], c["mean_degree"], c["gamma"], c["init_frac"], betas[pick],
+                         seeds[pick], c["steps"])
+    assert np.array_equal(got, want)
+
+
+def test_sweep_full_c5_sampled(orc):
+    # the full 4096-replicate batch in the bench configuration; 96 sampled replicates
+    c = C5_SWEEP
+    betas, seeds = sweep_replicates(c)
+    got, st = sweep(c["n"], sir_params(c["mean_degree"], 0.0, c["gamma"], c["init_frac"]), betas,
+                    seeds, c["steps"], with_stats=True)
+    rng = np.random.default_rng(0)
+    pick = np.sort(rng.choice(4096, 96, replace=False))
+    want = orc.sir_sweep(c["n"], c["mean_degree"], c["gamma"], c["init_frac"], betas[pick],
+                         seeds[pick], c["steps"])
+    assert np.array_equal(got[pick], want)
+    assert st["agent_updates"] == 4096 * 10_000 * 300
+    assert 0 < st["active_updates"] <= st["agent_updates"]
+    # final size rises with beta (sanity)
+    per_beta = got.reshape(64, 64).mean(axis=1)
+    assert per_beta[-1] > 0.95 and per_beta[0] < 0.3
+
+
+def test_sweep_global_graph_path(orc):
+    # n large enough that the CSR cannot be staged in shared memory (global-memory path)
+    n, kbar, g, f = 30_000, 8.0, 0.1, 0.001
+    betas = np.array([0.02, 0.05, 0.1, 0.2])
+    seeds = np.array([5, 6, 7, 8], dtype=np.uint64)
+    got = sweep(n, sir_params(kbar, 0.0, g, f), betas, seeds, 120)
+    want = orc.sir_sweep(n, kbar, g, f, betas, seeds, 120)
+    assert np.array_equal(got, want)
+
+
+def test_sweep_edge_cases(orc):
+    n = 500
+    got = sweep(n, sir_params(6.0, 0.0, 0.1, 0.0), [0.5, 1.0], [1, 2], 50)
+    assert (got == 0).all()  # nobody infected initially
+    got = sweep(n, sir_params(6.0, 0.0, 1.0, 0.02), [0.0], [3], 5)
+    assert got[0] == 10 / n  # gamma = 1, beta = 0: exactly the initial infected recover
+    assert sweep(n, sir_params(6.0, 0.0, 0.1, 0.02), [], [], 5).size == 0
