@@ -107,9 +107,11 @@ typedef struct {
     int32_t w0;           /* initial wealth of every agent (>= 0) */
     int32_t amount;       /* units given per step by each sender (>= 1) */
     int32_t exclude_self; /* 0: receiver uniform over all N (BJ config 1); 1: over N-1 others */
-    int32_t counter_bits; /* per-receiver counter width in {0(default=4),2,4,8,16,32};
-                             narrower counters stay L2-resident; an overflow is detected
-                             exactly and the step window is replayed with 32-bit counters */
+    int32_t counter_bits; /* scatter of the transfers: {0 (default = 4), 2, 4, 8, 16, 32} =
+                             per-receiver counter width for L2 atomics (narrow counters stay
+                             L2-resident; an overflow is detected exactly and the step window
+                             is replayed with 32-bit counters); -1 = range-partitioned
+                             counting sort through shared memory (single GPU, N <= 2^28) */
 } amber_wealth_params;
 
 /* SIR on G(n, M) (Sec. 5.1.1, Listing 2;

@@ -14,6 +14,7 @@
 
 #include "internal.cuh"
 #include "philox.cuh"
+#include "wealth.cuh"
 
 namespace amber {
 
@@ -22,9 +23,7 @@ namespace {
 constexpr int kQPT = 4;                  // quads (4 agents) per thread per chunk
 constexpr int kChunkAgents = 4 * kQPT * 32;  // agents per warp chunk (512)
 
-struct Slot {  // per-step record (ring slot), all 64-bit for atomics
-    unsigned long long total, active, digest, sent, got;
-};
+using Slot = WealthSlot;
 
 struct WealthArgs {
     PhiloxKey key;
@@ -283,6 +282,11 @@ public:
     int64_t win_start = -1;
     DevBuf<Slot> ring;
     int64_t m_first = 0, replays = 0;
+    // range-partitioned scatter (default on one GPU, wealth_bins.cu)
+    bool bins = false;
+    bool slot_ready = false;  // slot(t) is zero and the bins work queues are reset
+    BinPlan plan;
+    BinBuffers bb;
     // cross-shard exchange (world > 1)
     WealthExchange* xch = nullptr;
     DevBuf<uint32_t> send_ids, recv_ids;
@@ -297,7 +301,10 @@ public:
         p = p_;
         seed = seed_;
         key = philox_key(seed);
-        if (p.counter_bits == 0) p.counter_bits = 4;
+        // counter_bits -1: range-partitioned scatter (wealth_bins.cu, single GPU);
+        // 0: default = 4-bit packed counters with L2 atomics (measured faster)
+        const bool want_bins = p.counter_bits == -1 && (r == nullptr || r->world <= 1);
+        if (p.counter_bits <= 0) p.counter_bits = 4;
         B = p.counter_bits;
         AMBER_REQUIRE(B == 2 || B == 4 || B == 8 || B == 16 || B == 32, "counter_bits must be 0,2,4,8,16,32");
         AMBER_REQUIRE(p.amount >= 1, "amount must be >= 1");
@@ -311,13 +318,24 @@ public:
         hi = std::min<int64_t>(shard * (rt.rank + 1), n);
         n_loc = hi - lo;
         n_pad = std::max<int64_t>(ceil_div(std::max<int64_t>(n_loc, 1), kChunkAgents) * kChunkAgents, kChunkAgents);
+        if (want_bins) {
+            const int64_t np = ceil_div(std::max<int64_t>(n_loc, 1), kBinRange) * kBinRange;
+            if (bins_plan(rt, n, lo, np, plan)) {
+                bins = true;
+                n_pad = np;
+            }
+        }
         fast32 = n < (1ll << 32) - 1 && lo + n_pad < (1ll << 32);
         AMBER_REQUIRE(fast32 || rt.world == 1, "sharded wealth needs ids < 2^32");
         for (auto& b : wb) b.allocate(&rt, n_pad);
-        const int64_t inc_words = ceil_div(n_pad * B, 32) + 4;
-        for (auto& b : inc) {
-            b.allocate(&rt, inc_words);
-            b.zero_async(rt.stream);
+        if (bins) {
+            bins_allocate(rt, plan, bb);
+        } else {
+            const int64_t inc_words = ceil_div(n_pad * B, 32) + 4;
+            for (auto& b : inc) {
+                b.allocate(&rt, inc_words);
+                b.zero_async(rt.stream);
+            }
         }
         ring.allocate(&rt, metrics_cap);
         ring.zero_async(rt.stream);
@@ -343,6 +361,9 @@ public:
         for (auto& b : wb) b.reset();
         for (auto& b : inc) b.reset();
         for (auto& b : inc32) b.reset();
+        for (auto& b : bb.data) b.reset();
+        for (auto& b : bb.cnt) b.reset();
+        bb.queue.reset();
         ring.reset();
         send_ids.reset();
         recv_ids.reset();
@@ -472,6 +493,27 @@ public:
     {
         AMBER_REQUIRE(nsteps >= 0, "n_steps must be >= 0");
         AMBER_REQUIRE(t + nsteps < (1ll << 32) - 2, "step index would exceed 2^32");
+        if (bins) {
+            WealthStepCfg c{key, n_loc, n_pad, static_cast<unsigned long long>(lo), static_cast<unsigned long long>(n),
+                            p.amount, p.exclude_self, digest_on ? 1 : 0};
+            for (int64_t k = 0; k < nsteps; ++k) {
+                if (win_start >= 0 && t - win_start >= metrics_cap - 4) verify();
+                if (win_start < 0) {
+                    win_start = t;
+                    pinned = cur;
+                }
+                if (!slot_ready) {
+                    zero_slots(t, 1);
+                    bb.queue.zero_async(rt.stream);
+                }
+                const int dst = other(cur, pinned == cur ? -1 : pinned);
+                bins_step(rt, prof, plan, bb, c, static_cast<uint32_t>(t), wb[cur].p, wb[dst].p, slot(t), slot(t + 1));
+                slot_ready = true;
+                cur = dst;
+                ++t;
+            }
+            return;
+        }
         for (int64_t k = 0; k < nsteps; ++k) {
             if (win_start >= 0 && t - win_start >= metrics_cap - 4) verify();
             if (win_start < 0) {
@@ -514,6 +556,8 @@ public:
     void replay(int64_t s0, int64_t s1)
     {
         ++replays;
+        slot_ready = false;
+        for (auto& b : bb.cnt) b.zero_async(rt.stream);
         cur = pinned;
         for (auto& b : inc) b.zero_async(rt.stream);
         for (auto& b : inc32) {
@@ -541,6 +585,7 @@ public:
 
     void invalidate_pending()
     {
+        slot_ready = false;
         if (pending) {
             inc[t & 1].zero_async(rt.stream);
             pending = false;
@@ -650,6 +695,15 @@ public:
             m_first = t;
             return true;
         }
+        if (k == "bin_capacity") {  // test hook: shrink the per-range bins to force the exact replay
+            AMBER_REQUIRE(bins, "bin_capacity applies to the range-partitioned scatter only");
+            AMBER_REQUIRE(v >= 8 && v <= 0x7fffffff, "bin_capacity must be >= 8");
+            verify();
+            invalidate_pending();
+            plan.cap = static_cast<uint32_t>((v + 7) & ~7ll);
+            bins_allocate(rt, plan, bb);
+            return true;
+        }
         if (k == "block") AMBER_REQUIRE(v <= 256, "wealth kernels are built for <= 256 threads per block");
         if (k == "digest" || k == "block" || k == "grid") verify();
         return Model::set_option(key, v);
@@ -665,6 +719,10 @@ public:
         }
         if (k == "counter_bits") {
             *v = B;
+            return true;
+        }
+        if (k == "scatter") {  // 0: range-partitioned bins, 1: packed-counter atomics
+            *v = bins ? 0 : 1;
             return true;
         }
         return Model::get_option(key, v);

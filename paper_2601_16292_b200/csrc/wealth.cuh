@@ -1,0 +1,51 @@
+// wealth.cuh -- pieces of the wealth model shared by its two scatter
+// implementations (wealth.cu: packed-counter L2 atomics, also the exact replay
+// path; wealth_bins.cu: range-partitioned scatter, the default on one GPU).
+#pragma once
+
+#include "internal.cuh"
+#include "philox.cuh"
+
+namespace amber {
+
+// Per-step record (ring slot); all 64-bit for atomics.
+struct WealthSlot {
+    unsigned long long total, active, digest, sent, got;
+};
+
+// Range-partitioned scatter: receivers are bucketed by 2^16-agent range.
+constexpr int kBinShift = 16;
+constexpr int64_t kBinRange = 1ll << kBinShift;
+
+struct BinPlan {
+    int K = 0;                  // global ranges (bins) = ceil(N / 2^16)
+    int k0 = 0, k_loc = 0;      // this rank's first range and range count
+    uint32_t cap = 0;           // entry capacity per bin
+    int tile = 0;               // agents per production tile (shared-memory staging)
+    size_t prod_smem = 0, apply_smem = 0;
+    int prod_grid = 0, apply_grid = 0, apply_threads = 512;
+};
+
+struct BinBuffers {
+    DevBuf<uint16_t> data[2];   // [parity][K][cap] receiver offsets within the range
+    DevBuf<uint32_t> cnt[2];    // [parity][K] entries produced (cursor)
+    DevBuf<int> queue;          // [2] work-queue counters (production tiles, apply ranges)
+};
+
+// Plan + allocate; returns false if the range count does not fit the shared-memory staging.
+bool bins_plan(Runtime& rt, int64_t n, int64_t lo, int64_t n_pad, BinPlan& plan);
+void bins_allocate(Runtime& rt, const BinPlan& plan, BinBuffers& b);
+
+struct WealthStepCfg {
+    PhiloxKey key;
+    int64_t n_loc, n_pad;
+    unsigned long long lo, n_glob;
+    int32_t amount, exclude_self;
+    int digest;
+};
+
+// Step t: produce (bucket step t's receivers from w) then apply (w -> w_out).
+void bins_step(Runtime& rt, Profiler& prof, const BinPlan& plan, BinBuffers& b, const WealthStepCfg& c,
+               uint32_t t, const int32_t* w, int32_t* w_out, WealthSlot* slot_t, WealthSlot* slot_next);
+
+}  // namespace amber

@@ -49,6 +49,31 @@ def test_counter_widths_and_ragged_sizes(orc, bits, n):
         assert m.get_option("replays") > 0
 
 
+def test_range_partitioned_scatter_replays_exactly(orc):
+    n, seed = 300_000, 5
+    m = make(n, seed, bits=-1)
+    assert m.get_option("scatter") == 0
+    m.set_option("bin_capacity", 64)  # far below ~3e4 entries per range: every step overflows
+    m.step(6)
+    w, tot, _, _ = orc.wealth_run(np.full(n, 1, np.int32), seed, 0, 6)
+    assert np.array_equal(m.read_column("wealth"), w)
+    assert m.get_option("replays") >= 1
+    assert np.array_equal(m.metrics("total_wealth"), tot)
+    m.step(4)  # back on the fast path after the replay
+    w = orc.wealth_run(w, seed, 6, 4)[0]
+    assert np.array_equal(m.read_column("wealth"), w)
+
+
+def test_atomic_and_binned_scatter_agree(orc):
+    n, seed = 200_003, 8
+    a = make(n, seed, bits=-1)
+    b = make(n, seed)
+    assert a.get_option("scatter") == 0 and b.get_option("scatter") == 1
+    a.step(20)
+    b.step(20)
+    assert np.array_equal(a.read_column("wealth"), b.read_column("wealth"))
+
+
 def test_chunked_stepping_and_geometry_invariance(orc):
     n, seed = 40_000, 77
     ref = orc.wealth_run(np.full(n, 1, np.int32), seed, 0, 30)[0]
