@@ -17,8 +17,9 @@ from concurrent.futures import ThreadPoolExecutor
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OUT = os.path.join(PKG, "libamber.so")
-BUILD = os.path.join(PKG, "build")
+OUT = os.environ.get("AMBER_BUILD_OUT") or os.path.join(PKG, "libamber.so")
+BUILD = os.environ.get("AMBER_BUILD_DIR") or os.path.join(PKG, "build")
+EXTRA = os.environ.get("AMBER_NVCC_EXTRA", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -36,7 +37,7 @@ def nccl_include() -> str:
 def _flags(src: str) -> list[str]:
     f = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", nccl_include(),
-         "--expt-relaxed-constexpr"] + ARCH
+         "--expt-relaxed-constexpr"] + ARCH + EXTRA
     if os.path.basename(src) == "boids.cu":
         f += ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"]
     return f

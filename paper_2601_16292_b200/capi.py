@@ -12,7 +12,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libamber.so")
+LIB_PATH = os.environ.get("AMBER_LIB_PATH") or os.path.join(PKG, "libamber.so")
 
 AMBER_WEALTH, AMBER_SIR_GRAPH, AMBER_BOIDS = 0, 1, 2
 AMBER_I32, AMBER_U8, AMBER_F32, AMBER_I64, AMBER_F64, AMBER_U64 = range(6)

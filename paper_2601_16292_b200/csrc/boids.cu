@@ -28,6 +28,7 @@ namespace amber {
 namespace {
 
 constexpr float kFix = 16777216.0f;  // 2^24 (B3)
+constexpr int kTileCap = 3072;        // staged halo agents per tile (48 KB)
 
 struct BoidsArgs {
     float L, R, rs, wc, wa, ws, vmax, dt;
@@ -80,30 +81,27 @@ __global__ void boids_count_kernel(const float4* __restrict__ st, int64_t n, Boi
     }
 }
 
-// Exclusive scan of the cell counts by one CTA (ncell is at most a few 1e4);
-// also zeroes the counts for the next step.
+// Exclusive scan of the cell counts by one CTA: each thread owns a contiguous
+// run of cells (sequential sum), one block-wide scan of the run totals, then a
+// sequential write-back.  Also zeroes the counts for the next step.
 __global__ void __launch_bounds__(1024) boids_scan_kernel(int* cnt, int* start, int* cursor, int ncell)
 {
     using Scan = cub::BlockScan<int, 1024>;
     __shared__ typename Scan::TempStorage tmp;
-    __shared__ int carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int base = 0; base < ncell; base += 1024) {
-        const int c = base + threadIdx.x;
-        const int v = c < ncell ? cnt[c] : 0;
-        int ex, agg;
-        Scan(tmp).ExclusiveSum(v, ex, agg);
-        if (c < ncell) {
-            start[c] = carry + ex;
-            cursor[c] = carry + ex;
-            cnt[c] = 0;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) carry += agg;
-        __syncthreads();
+    const int per = (ncell + 1023) / 1024;
+    const int c0 = threadIdx.x * per;
+    int sum = 0;
+    for (int c = c0; c < c0 + per && c < ncell; ++c) sum += cnt[c];
+    int ex, agg;
+    Scan(tmp).ExclusiveSum(sum, ex, agg);
+    for (int c = c0; c < c0 + per && c < ncell; ++c) {
+        const int v = cnt[c];
+        start[c] = ex;
+        cursor[c] = ex;
+        cnt[c] = 0;
+        ex += v;
     }
-    if (threadIdx.x == 0) start[ncell] = carry;
+    if (threadIdx.x == 0) start[ncell] = agg;
 }
 
 __global__ void boids_scatter_kernel(const float4* __restrict__ st, const int32_t* __restrict__ ids, int64_t n,
@@ -251,6 +249,195 @@ __global__ void __launch_bounds__(256) boids_step_kernel(const float4* __restric
     }
 }
 
+// ---------------------------------------------------------------- tiled step
+// CTA per tile of kT x kT cells.  The (kT+2)^2 halo cells' agents are staged
+// in shared memory (float4 each, contiguous cell runs of the sorted array);
+// each thread then handles inner agents and scans their 3x3 stencil from
+// shared memory.  Tiles whose halo exceeds the staging capacity (dense
+// flocks) read the candidates from global memory instead.  Identical
+// arithmetic to boids_step_kernel (B2-B6), so identical results.
+constexpr int kT = 4, kW = kT + 2, kHalo = kW * kW;
+
+__device__ __forceinline__ void boid_accumulate(const float4 o, const float4 me, float L, float halfL, float R2,
+                                                float rs2, Acc& acc)
+{
+    const float dx = min_image(__fsub_rn(o.x, me.x), L, halfL);
+    const float dy = min_image(__fsub_rn(o.y, me.y), L, halfL);
+    const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+    if (d2 <= R2) {
+        const long long qx = q24(dx), qy = q24(dy);
+        acc.n += 1;
+        acc.sdx += qx;
+        acc.sdy += qy;
+        acc.svx += q24(o.z);
+        acc.svy += q24(o.w);
+        if (d2 <= rs2) {
+            acc.ssx += qx;
+            acc.ssy += qy;
+        }
+    }
+}
+
+__device__ __forceinline__ float4 boid_update(const float4 me, const Acc& acc, const BoidsArgs& a)
+{
+    const float L = a.L;
+    float ux = me.z, uy = me.w;
+    if (acc.n > 0) {
+        const double nd = static_cast<double>(acc.n);
+        const double fix = 16777216.0;
+        const float cohx = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.sdx), fix), nd));
+        const float cohy = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.sdy), fix), nd));
+        const float avx = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.svx), fix), nd));
+        const float avy = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.svy), fix), nd));
+        const float sepx = __double2float_rn(__ddiv_rn(static_cast<double>(acc.ssx), fix));
+        const float sepy = __double2float_rn(__ddiv_rn(static_cast<double>(acc.ssy), fix));
+        ux = __fsub_rn(__fadd_rn(__fadd_rn(me.z, __fmul_rn(a.wc, cohx)), __fmul_rn(a.wa, __fsub_rn(avx, me.z))),
+                       __fmul_rn(a.ws, sepx));
+        uy = __fsub_rn(__fadd_rn(__fadd_rn(me.w, __fmul_rn(a.wc, cohy)), __fmul_rn(a.wa, __fsub_rn(avy, me.w))),
+                       __fmul_rn(a.ws, sepy));
+    }
+    const float s2 = __fadd_rn(__fmul_rn(ux, ux), __fmul_rn(uy, uy));
+    if (s2 > __fmul_rn(a.vmax, a.vmax)) {
+        const float f = __fdiv_rn(a.vmax, __fsqrt_rn(s2));
+        ux = __fmul_rn(ux, f);
+        uy = __fmul_rn(uy, f);
+    }
+    float x = __fadd_rn(me.x, __fmul_rn(ux, a.dt));
+    float y = __fadd_rn(me.y, __fmul_rn(uy, a.dt));
+    if (x < 0.0f) x = __fadd_rn(x, L);
+    if (x >= L) x = __fsub_rn(x, L);
+    if (y < 0.0f) y = __fadd_rn(y, L);
+    if (y >= L) y = __fsub_rn(y, L);
+    return make_float4(x, y, ux, uy);
+}
+
+__global__ void __launch_bounds__(256) boids_tile_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ sids,
+                                                         const int* __restrict__ start, BoidsArgs a, int tiles_per_side,
+                                                         int cap, float4* __restrict__ out, int32_t* __restrict__ out_ids,
+                                                         BoidsSlot* slot, int digest)
+{
+    extern __shared__ __align__(16) float4 sa[];
+    __shared__ int hstart[kHalo + 1], hglob[kHalo], hcnt[kHalo];
+    __shared__ int istart[kT * kT + 1], ihalo[kT * kT];
+    const int tid = threadIdx.x;
+    const int tx0 = (blockIdx.x % tiles_per_side) * kT, ty0 = (blockIdx.x / tiles_per_side) * kT;
+    const int nc = a.nc;
+    if (tid < kHalo) {
+        const int hx = tid % kW, hy = tid / kW;
+        int cx = tx0 + hx - 1, cy = ty0 + hy - 1;
+        cx = cx < 0 ? cx + nc : (cx >= nc ? cx - nc : cx);
+        cy = cy < 0 ? cy + nc : (cy >= nc ? cy - nc : cy);
+        const int c = cy * nc + cx;
+        hglob[tid] = start[c];
+        hcnt[tid] = start[c + 1] - start[c];
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int acc = 0;
+        for (int h = 0; h < kHalo; ++h) {
+            hstart[h] = acc;
+            acc += hcnt[h];
+        }
+        hstart[kHalo] = acc;
+        int ia = 0, j = 0;
+        for (int iy = 1; iy <= kT; ++iy)
+            for (int ix = 1; ix <= kT; ++ix) {
+                const bool real = tx0 + ix - 1 < nc && ty0 + iy - 1 < nc;
+                const int h = iy * kW + ix;
+                istart[j] = ia;
+                ihalo[j] = h;
+                ia += real ? hcnt[h] : 0;
+                ++j;
+            }
+        istart[kT * kT] = ia;
+    }
+    __syncthreads();
+    const int total = hstart[kHalo];
+    const bool staged = total <= cap;
+    if (staged) {
+        for (int k = tid; k < total; k += blockDim.x) {
+            int lo = 0, hi = kHalo - 1;  // halo cell of staged entry k
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (hstart[mid] <= k) lo = mid;
+                else hi = mid - 1;
+            }
+            sa[k] = sorted[hglob[lo] + (k - hstart[lo])];
+        }
+    }
+    __syncthreads();
+    const float L = a.L, halfL = __fmul_rn(0.5f, a.L), R2 = __fmul_rn(a.R, a.R), rs2 = __fmul_rn(a.rs, a.rs);
+    const float4* base = staged ? sa : sorted;
+    double sp_sum = 0.0, ux_sum = 0.0, uy_sum = 0.0;
+    unsigned long long dig = 0;
+    const int n_inner = istart[kT * kT];
+    for (int k = tid; k < n_inner; k += blockDim.x) {
+        int lo = 0, hi = kT * kT - 1;  // inner cell of inner agent k
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (istart[mid] <= k) lo = mid;
+            else hi = mid - 1;
+        }
+        const int h = ihalo[lo];
+        const int off = k - istart[lo];
+        const int p = hglob[h] + off;                          // global sorted index
+        const int me_i = staged ? hstart[h] + off : p;         // index in `base`
+        const float4 me = base[me_i];
+        Acc acc{0, 0, 0, 0, 0, 0, 0};
+        const int hx = h % kW, hy = h / kW;
+#pragma unroll 1
+        for (int dyc = -1; dyc <= 1; ++dyc)
+#pragma unroll 1
+            for (int dxc = -1; dxc <= 1; ++dxc) {
+                const int h2 = (hy + dyc) * kW + hx + dxc;
+                const int b = staged ? hstart[h2] : hglob[h2];
+                const int e = b + hcnt[h2];
+                for (int q = b; q < e; ++q)
+                    if (q != me_i) boid_accumulate(base[q], me, L, halfL, R2, rs2, acc);
+            }
+        const float4 nx = boid_update(me, acc, a);
+        out[p] = nx;
+        const int32_t id = sids[p];
+        out_ids[p] = id;
+        const double dvx = static_cast<double>(nx.z), dvy = static_cast<double>(nx.w);
+        const double sp = __dsqrt_rn(__dadd_rn(__dmul_rn(dvx, dvx), __dmul_rn(dvy, dvy)));
+        sp_sum += sp;
+        if (sp > 0.0) {
+            ux_sum += __ddiv_rn(dvx, sp);
+            uy_sum += __ddiv_rn(dvy, sp);
+        }
+        if (digest) dig += digest_term(static_cast<unsigned long long>(id), __float_as_uint(nx.x));
+    }
+    __shared__ double red[3][8];
+    __shared__ unsigned long long dred[8];
+    const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    sp_sum = warp_sum_f64(sp_sum);
+    ux_sum = warp_sum_f64(ux_sum);
+    uy_sum = warp_sum_f64(uy_sum);
+    dig = warp_sum_u64(dig);
+    if (lane == 0) {
+        red[0][wid] = sp_sum;
+        red[1][wid] = ux_sum;
+        red[2][wid] = uy_sum;
+        dred[wid] = dig;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double s0 = 0, s1 = 0, s2v = 0;
+        unsigned long long d = 0;
+        for (int w = 0; w < nw; ++w) {
+            s0 += red[0][w];
+            s1 += red[1][w];
+            s2v += red[2][w];
+            d += dred[w];
+        }
+        atomicAdd(&slot->mean_speed, s0);
+        atomicAdd(&slot->polar_x, s1);
+        atomicAdd(&slot->polar_y, s2v);
+        if (digest) atomicAdd(&slot->digest, d);
+    }
+}
+
 // Un-permute: column k of the state (0 x, 1 y, 2 vx, 3 vy) into id order.
 __global__ void boids_gather_column(const float4* __restrict__ st, const int32_t* __restrict__ ids, int64_t n, int k,
                                     float* __restrict__ out)
@@ -327,6 +514,8 @@ public:
         cell_of.allocate(&rt, n);
         ring.allocate(&rt, metrics_cap);
         ring.zero_async(rt.stream);
+        AMBER_CUDA(cudaFuncSetAttribute(boids_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kTileCap * sizeof(float4))));
         boids_init_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(philox_key(seed), n, p.L, st.p, ids.p);
         check_launch("boids_init_kernel");
         AMBER_CUDA(cudaStreamSynchronize(rt.stream));
@@ -376,12 +565,23 @@ public:
                 check_launch("boids_scatter_kernel");
             }
             const BoidsArgs a = ba;
-            prof.launch(rt.stream, "boids_step", [&] {
-                boids_step_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a, st.p,
-                                                                                ids.p, ring.p + (t % metrics_cap),
-                                                                                digest_on ? 1 : 0);
-            });
-            check_launch("boids_step_kernel");
+            if (ba.nc >= 3 && persistent) {
+                const int tps = (ba.nc + kT - 1) / kT;
+                prof.launch(rt.stream, "boids_step", [&] {
+                    boids_tile_kernel<<<tps * tps, 256, kTileCap * sizeof(float4), rt.stream>>>(
+                        sorted.p, sids.p, start.p, a, tps, kTileCap, st.p, ids.p, ring.p + (t % metrics_cap),
+                        digest_on ? 1 : 0);
+                });
+                check_launch("boids_tile_kernel");
+            } else {
+                prof.launch(rt.stream, "boids_step", [&] {
+                    boids_step_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a,
+                                                                                    st.p, ids.p,
+                                                                                    ring.p + (t % metrics_cap),
+                                                                                    digest_on ? 1 : 0);
+                });
+                check_launch("boids_step_kernel");
+            }
             ++t;
         }
     }

@@ -272,54 +272,79 @@ struct SirStepArgs {
     int digest;
 };
 
-// S2 for one agent s in state S: pull over its row, early exit on the first
-// transmitting edge (S3: the draw is keyed on the unordered pair, so the
-// result equals the OR over all S-I edges).
-__device__ __forceinline__ bool pull_infect(const SirStepArgs& a, const uint8_t* __restrict__ x, uint32_t s, uint32_t t)
-{
-    const int32_t b = a.row_ptr[s], e = a.row_ptr[s + 1];
-    for (int32_t p = b; p < e; ++p) {
-        const uint32_t j = static_cast<uint32_t>(__ldg(a.col + p));
-        if (x[j] == kI) {
-            const uint32_t lo = min(s, j), hi = max(s, j);
-            const uint4 w = philox(make_uint4(lo, hi, t, TAG_SIR_TX), a.key);
-            if (static_cast<unsigned long long>(w.x) < a.t_beta) return true;
-        }
-    }
-    return false;
-}
-
-// One step over all quads (grid-stride); accumulates S/I/R/digest of the new state.
+// One step, warp-cooperative pull.  A warp owns 32 consecutive agents
+// (lane = agent).  Their CSR rows are contiguous, so the warp walks the
+// concatenated arc range 32 arcs at a time (coalesced col loads, 32 independent
+// neighbour-state gathers in flight); each lane finds the owner of its arc by a
+// 5-step shuffle search over the row starts, draws the pair-keyed Bernoulli
+// (S3) for S-owner / I-neighbour arcs, and ORs a hit into the owner's bit of a
+// per-warp mask.  Owners already infected skip further draws (early exit is
+// legal because the result is the OR over all S-I edges).
 __device__ __forceinline__ void sir_step_body(const SirStepArgs& a, const uint8_t* __restrict__ x, uint8_t* __restrict__ y,
-                                              uint32_t t, unsigned long long (&cnt)[4])
+                                              uint32_t t, unsigned long long (&cnt)[4], uint32_t* wmask)
 {
-    const int64_t nq = a.n_pad / 4;
-    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nq; g += (int64_t)gridDim.x * blockDim.x) {
-        const uchar4 v = reinterpret_cast<const uchar4*>(x)[g];
-        uint8_t in[4] = {v.x, v.y, v.z, v.w}, out[4];
-        uint4 rec = make_uint4(0u, 0u, 0u, 0u);
-        if (in[0] == kI || in[1] == kI || in[2] == kI || in[3] == kI)
-            rec = stream_block(a.key, TAG_SIR_REC, static_cast<unsigned long long>(g), t);  // R4: block i/4
-        const uint32_t rw[4] = {rec.x, rec.y, rec.z, rec.w};
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int32_t arcs_end = a.row_ptr[a.n];
+    for (int64_t a0 = gw * 32; a0 < a.n_pad; a0 += nw * 32) {
+        const int64_t i = a0 + lane;
+        const bool real = i < a.n;
+        const uint8_t st = x[i];
+        const int32_t rb = real ? a.row_ptr[i] : arcs_end;
+        const int32_t we = __shfl_sync(0xffffffffu, real ? a.row_ptr[i + 1] : arcs_end, 31);
+        const int32_t wb = __shfl_sync(0xffffffffu, rb, 0);
+        const bool is_s = st == kS;
+        const unsigned s_lanes = __ballot_sync(0xffffffffu, is_s);
+        if (lane == 0) *wmask = 0u;
+        __syncwarp();
+        if (s_lanes) {
+            for (int32_t e0 = wb; e0 < we; e0 += 32) {
+                const int32_t e = e0 + lane;
+                // owner = largest lane L with rb_L <= e (rows are contiguous)
+                int L = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t i = static_cast<uint32_t>(4 * g + k);
-            uint8_t o = in[k];
-            if (in[k] == kS) o = pull_infect(a, x, i, t) ? kI : kS;
-            else if (in[k] == kI) o = (static_cast<unsigned long long>(rw[k]) < a.t_gamma) ? kR : kI;
-            out[k] = o;
-            if (o < 3) cnt[o] += 1;
-            if (a.digest && o < 3) cnt[3] += digest_term(i, o);
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int cand = L + step;
+                    const int32_t rbc = __shfl_sync(0xffffffffu, rb, cand & 31);
+                    if (cand < 32 && rbc <= e) L = cand;
+                }
+                const unsigned done = *wmask;
+                if (e < we && ((s_lanes >> L) & 1u) && !((done >> L) & 1u)) {
+                    const uint32_t j = static_cast<uint32_t>(__ldg(a.col + e));
+                    if (x[j] == kI) {
+                        const uint32_t s = static_cast<uint32_t>(a0 + L);
+                        const uint4 w = philox(make_uint4(min(s, j), max(s, j), t, TAG_SIR_TX), a.key);
+                        if (static_cast<unsigned long long>(w.x) < a.t_beta) atomicOr(wmask, 1u << L);
+                    }
+                }
+                __syncwarp();
+            }
         }
-        reinterpret_cast<uchar4*>(y)[g] = make_uchar4(out[0], out[1], out[2], out[3]);
+        uint8_t o = st;
+        if (is_s) {
+            if ((*wmask >> lane) & 1u) o = kI;
+        } else if (st == kI) {
+            const uint4 rec = stream_block(a.key, TAG_SIR_REC, static_cast<unsigned long long>(i >> 2), t);  // R4
+            const uint32_t k = static_cast<uint32_t>(i & 3);
+            const uint32_t d = k == 0 ? rec.x : (k == 1 ? rec.y : (k == 2 ? rec.z : rec.w));
+            if (static_cast<unsigned long long>(d) < a.t_gamma) o = kR;
+        }
+        y[i] = o;
+        if (real) {
+            cnt[o] += 1;
+            if (a.digest) cnt[3] += digest_term(static_cast<unsigned long long>(i), o);
+        }
+        __syncwarp();
     }
 }
 
 __global__ void __launch_bounds__(256) sir_step_kernel(const SirStepArgs a)
 {
+    __shared__ uint32_t wmask[8];
     const uint32_t t = a.t0;
     unsigned long long cnt[4] = {0, 0, 0, 0};
-    sir_step_body(a, a.x[a.cur], a.x[a.cur ^ 1], t, cnt);
+    sir_step_body(a, a.x[a.cur], a.x[a.cur ^ 1], t, cnt, &wmask[threadIdx.x >> 5]);
     SirSlot* sl = a.ring + (t % a.ring_cap);
     unsigned long long* const outs[4] = {&sl->S, &sl->I, &sl->R, a.digest ? &sl->digest : nullptr};
     block_sum_atomic<4>(cnt, outs);
@@ -329,11 +354,12 @@ __global__ void __launch_bounds__(256) sir_step_kernel(const SirStepArgs a)
 __global__ void __launch_bounds__(256) sir_persistent_kernel(const SirStepArgs a)
 {
     cg::grid_group grid = cg::this_grid();
+    __shared__ uint32_t wmask[8];
     int cur = a.cur;
     for (int64_t k = 0; k < a.n_steps; ++k) {
         const uint32_t t = a.t0 + static_cast<uint32_t>(k);
         unsigned long long cnt[4] = {0, 0, 0, 0};
-        sir_step_body(a, a.x[cur], a.x[cur ^ 1], t, cnt);
+        sir_step_body(a, a.x[cur], a.x[cur ^ 1], t, cnt, &wmask[threadIdx.x >> 5]);
         SirSlot* sl = a.ring + (t % a.ring_cap);
         unsigned long long* const outs[4] = {&sl->S, &sl->I, &sl->R, a.digest ? &sl->digest : nullptr};
         block_sum_atomic<4>(cnt, outs);
@@ -375,7 +401,7 @@ public:
                       "SIR params out of range");
         m_draws = static_cast<int64_t>(std::floor(static_cast<double>(n) * p.mean_degree / 2.0 + 0.5));
         k_inf = static_cast<int64_t>(std::floor(p.init_frac * static_cast<double>(n) + 0.5));
-        n_pad = ceil_div(n, 16) * 16;
+        n_pad = ceil_div(n, 32) * 32;
         std::vector<unsigned long long> seeds{seed};
         build_graphs(rt, seeds, n, m_draws, g);
         for (auto& b : x) b.allocate(&rt, n_pad);
@@ -430,7 +456,7 @@ public:
                 int per_sm = 0;
                 AMBER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sir_persistent_kernel, threads, 0));
                 int blocks = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(per_sm) * rt.num_sms,
-                                                                ceil_div(n_pad / 4, threads)));
+                                                                ceil_div(n_pad, threads)));
                 if (grid) blocks = static_cast<int>(std::min<int64_t>(grid, static_cast<int64_t>(per_sm) * rt.num_sms));
                 blocks = std::max(blocks, 1);
                 SirStepArgs a = args(chunk);
@@ -445,7 +471,7 @@ public:
             } else {
                 for (int64_t k = 0; k < chunk; ++k) {
                     SirStepArgs a = args(1);
-                    int blocks = static_cast<int>(ceil_div(n_pad / 4, threads));
+                    int blocks = static_cast<int>(ceil_div(n_pad, threads));
                     if (grid) blocks = static_cast<int>(grid);
                     prof.launch(rt.stream, "sir_step", [&] { sir_step_kernel<<<blocks, threads, 0, rt.stream>>>(a); });
                     check_launch("sir_step_kernel");

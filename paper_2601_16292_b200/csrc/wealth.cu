@@ -20,7 +20,16 @@ namespace amber {
 
 namespace {
 
-constexpr int kQPT = 4;                  // quads (4 agents) per thread per chunk
+#ifndef AMBER_WEALTH_QPT
+#define AMBER_WEALTH_QPT 8
+#endif
+#ifndef AMBER_WEALTH_MINB
+#define AMBER_WEALTH_MINB 1
+#endif
+#ifndef AMBER_WEALTH_HINT
+#define AMBER_WEALTH_HINT 1
+#endif
+constexpr int kQPT = AMBER_WEALTH_QPT;   // quads (4 agents) per thread per chunk
 constexpr int kChunkAgents = 4 * kQPT * 32;  // agents per warp chunk (512)
 
 using Slot = WealthSlot;
@@ -94,7 +103,12 @@ __device__ __forceinline__ unsigned long long policy_evict_last()
 
 __device__ __forceinline__ void red_add_hint(uint32_t* addr, uint32_t v, unsigned long long pol)
 {
+#if AMBER_WEALTH_HINT
     asm volatile("red.global.add.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(addr), "r"(v), "l"(pol) : "memory");
+#else
+    (void)pol;
+    atomicAdd(addr, v);
+#endif
 }
 
 template <int B, class Id>
@@ -146,7 +160,7 @@ __device__ __forceinline__ void remote_append(const WealthArgs& a, bool flag, un
 // index arithmetic); REMOTE: receivers outside this shard are bucketed for
 // the exchange instead of counted locally.
 template <int B, bool APPLY, bool SCATTER, bool DIGEST, bool REMOTE, bool FAST32>
-__global__ void __launch_bounds__(256) wealth_step_kernel(const WealthArgs a)
+__global__ void __launch_bounds__(256, AMBER_WEALTH_MINB) wealth_step_kernel(const WealthArgs a)
 {
     using Id = typename std::conditional<FAST32, uint32_t, unsigned long long>::type;
     if (a.slot_zero && blockIdx.x == 0 && threadIdx.x == 0) *a.slot_zero = Slot{0, 0, 0, 0, 0};
@@ -225,6 +239,82 @@ __global__ void __launch_bounds__(256) wealth_step_kernel(const WealthArgs a)
         (APPLY && DIGEST) ? &a.slot_apply->digest : nullptr, SCATTER ? &a.slot_scatter->sent : nullptr,
         APPLY ? &a.slot_apply->got : nullptr};
     block_sum_atomic<5>(vals, outs);
+}
+
+
+// Small populations (C1): every step of a call in ONE single-CTA launch.  The
+// wealth column and exact 32-bit receiver counters live in shared memory, so
+// a step costs two __syncthreads instead of a kernel launch, and no counter
+// can overflow (sent == got by construction).
+constexpr int kSmallMax = 16384;  // agents (64 KB column + 64 KB counters)
+
+struct SmallArgs {
+    PhiloxKey key;
+    const int32_t* w_in;
+    int32_t* w_out;
+    int64_t n;                 // agents (single GPU)
+    int32_t amount, exclude_self;
+    uint32_t t0;
+    int64_t steps;
+    Slot* ring;
+    int64_t ring_cap;
+    int digest;
+};
+
+__global__ void __launch_bounds__(1024, 1) wealth_small_kernel(const SmallArgs a)
+{
+    extern __shared__ __align__(16) int32_t sw[];
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(sw + kSmallMax);
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const uint32_t n = static_cast<uint32_t>(a.n);
+    const unsigned long long m = a.n - (a.exclude_self ? 1 : 0);
+    for (uint32_t i = tid; i < n; i += nt) {
+        sw[i] = a.w_in[i];
+        cnt[i] = 0u;
+    }
+    __syncthreads();
+    for (int64_t k = 0; k < a.steps; ++k) {
+        const uint32_t t = a.t0 + static_cast<uint32_t>(k);
+        // scatter: one Philox block per pair of agents (R4)
+        unsigned long long sent = 0;
+        for (uint32_t p = tid; 2 * p < n; p += nt) {
+            const uint32_t i0 = 2 * p;
+            const bool s0 = sw[i0] >= a.amount, s1 = (i0 + 1 < n) && sw[i0 + 1] >= a.amount;
+            if (s0 || s1) {
+                const uint4 x = stream_block(a.key, TAG_WEALTH_RECV, p, t);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (h ? s1 : s0) {
+                        unsigned long long r = mulhi64(lane64_of(x, h), m);
+                        if (a.exclude_self) r += (r >= i0 + h);
+                        atomicAdd(cnt + r, 1u);
+                        ++sent;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // apply + observables
+        unsigned long long tot = 0, act = 0, got = 0, dig = 0;
+        for (uint32_t i = tid; i < n; i += nt) {
+            const uint32_t c = cnt[i];
+            cnt[i] = 0u;
+            int32_t v = sw[i];
+            v = v - (v >= a.amount ? a.amount : 0) + a.amount * static_cast<int32_t>(c);
+            sw[i] = v;
+            tot += static_cast<unsigned long long>(static_cast<long long>(v));
+            act += v > 0;
+            got += c;
+            if (a.digest) dig += digest_term(i, static_cast<uint32_t>(v));
+        }
+        Slot* sl = a.ring + (t % a.ring_cap);
+        if (tid == 0) *sl = Slot{0, 0, 0, 0, 0};
+        __syncthreads();
+        unsigned long long vals[5] = {tot, act, dig, sent, got};
+        unsigned long long* const outs[5] = {&sl->total, &sl->active, a.digest ? &sl->digest : nullptr, &sl->sent, &sl->got};
+        block_sum_atomic<5>(vals, outs);
+    }
+    for (uint32_t i = tid; i < n; i += nt) a.w_out[i] = sw[i];
 }
 
 // Received cross-shard receivers -> local counters of the scattered step.
@@ -489,10 +579,36 @@ public:
         check_launch("zero_slots_kernel");
     }
 
+    bool small_path() const { return rt.world == 1 && n <= kSmallMax && !bins && persistent; }
+
     void step(int64_t nsteps) override
     {
         AMBER_REQUIRE(nsteps >= 0, "n_steps must be >= 0");
         AMBER_REQUIRE(t + nsteps < (1ll << 32) - 2, "step index would exceed 2^32");
+        if (small_path() && nsteps > 0) {
+            // no pending scatter across calls on this path; flush any from the large path
+            verify();
+            invalidate_pending();
+            int64_t done = 0;
+            while (done < nsteps) {
+                const int64_t chunk = std::min<int64_t>(nsteps - done, metrics_cap - 4);
+                SmallArgs a{key, wb[cur].p, wb[other(cur, -1)].p, n, p.amount, p.exclude_self,
+                            static_cast<uint32_t>(t), chunk, ring.p, metrics_cap, digest_on ? 1 : 0};
+                const size_t smem = static_cast<size_t>(kSmallMax) * 8;
+                AMBER_CUDA(cudaFuncSetAttribute(wealth_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                static_cast<int>(smem)));
+                int threads = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(32, ceil_div(n, 32) * 32)));
+                if (block) threads = static_cast<int>(block);
+                prof.launch(rt.stream, "wealth_small_persistent", [&] {
+                    wealth_small_kernel<<<1, threads, smem, rt.stream>>>(a);
+                });
+                check_launch("wealth_small_kernel");
+                cur = other(cur, -1);
+                t += chunk;
+                done += chunk;
+            }
+            return;
+        }
         if (bins) {
             WealthStepCfg c{key, n_loc, n_pad, static_cast<unsigned long long>(lo), static_cast<unsigned long long>(n),
                             p.amount, p.exclude_self, digest_on ? 1 : 0};

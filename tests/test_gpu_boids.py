@@ -79,6 +79,20 @@ def test_c3_hundred_steps_ensemble(orc):
     assert match == 1.0
 
 
+def test_dense_flock_tile_overflow_path(orc):
+    # strong cohesion packs agents into few cells: tiles exceed the shared-memory
+    # staging and take the global-memory path; results must still be exact
+    cfg = dict(C3_BOIDS, n=6000, L=100.0, R=10.0, rs=0.5, wc=0.5, wa=0.5, ws=0.0, vmax=2.0, seed=9)
+    m = make(cfg)
+    st = state(m)
+    P = oparams(orc, cfg)
+    m.step(40)
+    for _ in range(40):
+        st = orc.boids_step(st, P)
+    for a, b in zip(state(m), st):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
 @pytest.mark.parametrize("kw", [dict(L=15.0, R=7.0, rs=2.0), dict(L=64.0, R=7.5, rs=3.0),
                                 dict(L=200.0, R=10.0, wa=1.0, wc=0.3, ws=0.4, vmax=0.5)])
 def test_small_boxes_and_params(orc, kw):
@@ -98,6 +112,7 @@ def test_geometry_invariance_and_io(orc):
     a = make(cfg)
     a.step(10)
     b = make(cfg)
+    b.set_option("persistent", 0)  # per-agent global-memory kernel instead of the tiled one
     b.set_option("block", 64)
     b.set_option("grid", 7)
     b.step(4)

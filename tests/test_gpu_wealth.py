@@ -40,6 +40,7 @@ def test_c1_every_step_bit_exact(orc):
 def test_counter_widths_and_ragged_sizes(orc, bits, n):
     # 2-bit counters overflow often: exercises the exact detection + replay path
     m = make(n, 1234, bits=bits)
+    m.set_option("persistent", 0)  # the multi-CTA counter path (small N would use one CTA)
     m.step(60)
     w, tot, act, _ = orc.wealth_run(np.full(n, 1, np.int32), 1234, 0, 60)
     assert np.array_equal(m.read_column("wealth"), w)
@@ -72,6 +73,20 @@ def test_atomic_and_binned_scatter_agree(orc):
     a.step(20)
     b.step(20)
     assert np.array_equal(a.read_column("wealth"), b.read_column("wealth"))
+
+
+@pytest.mark.parametrize("n", [1, 2, 1000, 16384])
+def test_small_single_cta_path_equals_counter_path(orc, n):
+    a = make(n, 42)  # n <= 16384: one CTA runs all steps in shared memory
+    b = make(n, 42)
+    b.set_option("persistent", 0)
+    a.step(37)
+    a.step(63)
+    b.step(100)
+    w = orc.wealth_run(np.full(n, 1, np.int32), 42, 0, 100)[0]
+    assert np.array_equal(a.read_column("wealth"), w)
+    assert np.array_equal(b.read_column("wealth"), w)
+    assert np.array_equal(a.metrics("active"), b.metrics("active"))
 
 
 def test_chunked_stepping_and_geometry_invariance(orc):
