@@ -482,6 +482,7 @@ public:
     DevBuf<BoidsSlot> ring;
     int64_t m_first = 0;
     int ncell = 0;
+    int64_t tiled = 0;  // 1: shared-memory tiled stencil kernel (slower once flocks cluster)
 
     BoidsModel(int64_t n_, const amber_boids_params& p_, uint64_t seed_, const amber_runtime* r)
     {
@@ -565,7 +566,7 @@ public:
                 check_launch("boids_scatter_kernel");
             }
             const BoidsArgs a = ba;
-            if (ba.nc >= 3 && persistent) {
+            if (ba.nc >= 3 && tiled) {
                 const int tps = (ba.nc + kT - 1) / kT;
                 prof.launch(rt.stream, "boids_step", [&] {
                     boids_tile_kernel<<<tps * tps, 256, kTileCap * sizeof(float4), rt.stream>>>(
@@ -686,6 +687,10 @@ public:
             return true;
         }
         if (k == "block") AMBER_REQUIRE(v <= 256, "Boids kernels are built for <= 256 threads per block");
+        if (k == "tiled") {
+            tiled = v ? 1 : 0;
+            return true;
+        }
         return Model::set_option(key, v);
     }
 
@@ -693,6 +698,10 @@ public:
     {
         if (std::string(key) == "cells_per_side") {
             *v = ba.nc;
+            return true;
+        }
+        if (std::string(key) == "tiled") {
+            *v = tiled;
             return true;
         }
         return Model::get_option(key, v);

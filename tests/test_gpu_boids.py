@@ -84,6 +84,7 @@ def test_dense_flock_tile_overflow_path(orc):
     # staging and take the global-memory path; results must still be exact
     cfg = dict(C3_BOIDS, n=6000, L=100.0, R=10.0, rs=0.5, wc=0.5, wa=0.5, ws=0.0, vmax=2.0, seed=9)
     m = make(cfg)
+    m.set_option("tiled", 1)
     st = state(m)
     P = oparams(orc, cfg)
     m.step(40)
@@ -112,7 +113,7 @@ def test_geometry_invariance_and_io(orc):
     a = make(cfg)
     a.step(10)
     b = make(cfg)
-    b.set_option("persistent", 0)  # per-agent global-memory kernel instead of the tiled one
+    b.set_option("tiled", 1)  # shared-memory tiled stencil kernel instead of the per-agent one
     b.set_option("block", 64)
     b.set_option("grid", 7)
     b.step(4)
