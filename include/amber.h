@@ -261,6 +261,17 @@ int amber_sweep(amber_kind kind, int64_t n_agents, const void* base_params, size
 
 /* ------------------------------------------------------------ multi-GPU */
 
+/* Host-only (no device needed): the contiguous agent range [*lo, *hi) that rank
+ * `rank` of `world` owns in a sharded wealth model of n_agents:
+ * shard size = ceil(n/world) rounded up to a multiple of 8 agents, so the
+ * two-agent Philox blocks (contract R4) never straddle shards; trailing ranks
+ * may be shorter or empty.  Errors: INVALID_ARG. */
+int amber_shard_range(int64_t n_agents, int world, int rank, int64_t* lo, int64_t* hi);
+
+/* Host-only: the replicates [*r0, *r1) that rank `rank` of `world` runs in
+ * amber_sweep (blocks of ceil(n_reps/world)).  Errors: INVALID_ARG. */
+int amber_sweep_range(int64_t n_reps, int world, int rank, int64_t* r0, int64_t* r1);
+
 /* Write a fresh 128-byte NCCL unique id into out (host, out_bytes >= 128).
  * Call on rank 0 and broadcast it (e.g. with torch.distributed).
  * Errors: NCCL (libnccl.so.2 not loadable: set AMBER_NCCL_LIB to its path). */

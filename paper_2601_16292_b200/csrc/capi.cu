@@ -249,6 +249,28 @@ int amber_sweep(amber_kind kind, int64_t n_agents, const void* base_params, size
     });
 }
 
+int amber_shard_range(int64_t n_agents, int world, int rank, int64_t* lo, int64_t* hi)
+{
+    return guarded([&] {
+        need(lo, "lo");
+        need(hi, "hi");
+        AMBER_REQUIRE(n_agents >= 1 && world >= 1 && rank >= 0 && rank < world, "bad shard request");
+        amber::shard_range(n_agents, world, rank, lo, hi);
+        return 0;
+    });
+}
+
+int amber_sweep_range(int64_t n_reps, int world, int rank, int64_t* r0, int64_t* r1)
+{
+    return guarded([&] {
+        need(r0, "r0");
+        need(r1, "r1");
+        AMBER_REQUIRE(n_reps >= 0 && world >= 1 && rank >= 0 && rank < world, "bad sweep-range request");
+        amber::sweep_range(n_reps, world, rank, r0, r1);
+        return 0;
+    });
+}
+
 int amber_nccl_unique_id(void* out, size_t out_bytes)
 {
     return guarded([&] { return amber_nccl_unique_id_impl(out, out_bytes); });

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -230,6 +231,22 @@ uint64_t device_digest_u32(Runtime& rt, const uint32_t* col, int64_t n, int64_t 
 uint64_t device_digest_u8(Runtime& rt, const uint8_t* col, int64_t n, int64_t id0);
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Multi-GPU partitions (host logic).  Wealth: contiguous id
+// ranges of ceil(n/world) rounded up to 8 agents.  Sweep: replicate blocks.
+inline void shard_range(int64_t n, int world, int rank, int64_t* lo, int64_t* hi)
+{
+    const int64_t shard = ((ceil_div(n, world) + 7) / 8) * 8;
+    *lo = std::min<int64_t>(shard * rank, n);
+    *hi = std::min<int64_t>(shard * (rank + 1), n);
+}
+
+inline void sweep_range(int64_t n_reps, int world, int rank, int64_t* r0, int64_t* r1)
+{
+    const int64_t per = ceil_div(std::max<int64_t>(n_reps, 1), world);
+    *r0 = std::min<int64_t>(per * rank, n_reps);
+    *r1 = std::min<int64_t>(per * (rank + 1), n_reps);
+}
 
 }  // namespace amber
 

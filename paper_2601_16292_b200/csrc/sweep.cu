@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
     uint8_t* xs = reinterpret_cast<uint8_t*>(cs + (COL_SMEM ? ((a.col_cap + 7) & ~7ll) : 0));
     uint8_t* st[2] = {xs, xs + a.n_pad};
     __shared__ int rep_s;
-    __shared__ int cnt_s[2];
+    __shared__ int cnt_s[2][2];  // [parity][I, S]
     const int tid = threadIdx.x, nt = blockDim.x;
     const int64_t nq = a.n_pad / 4;
 
@@ -75,68 +75,125 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
         }
         const uchar4* s0 = reinterpret_cast<const uchar4*>(a.state0 + static_cast<int64_t>(r) * a.n_pad);
         for (int64_t q = tid; q < nq; q += nt) reinterpret_cast<uchar4*>(st[0])[q] = s0[q];
-        if (tid == 0) cnt_s[0] = cnt_s[1] = 0;
+        if (tid == 0) cnt_s[0][0] = cnt_s[0][1] = cnt_s[1][0] = cnt_s[1][1] = 0;
         __syncthreads();
         const PhiloxKey key = philox_key(a.seeds[r]);
         const unsigned long long tb = a.t_beta[r];
         int cur = 0;
         int64_t executed = a.steps;
+        // initial S / I counts (direction choice of the first step)
+        {
+            int ni = 0, ns = 0;
+            for (int64_t i = tid; i < a.n; i += nt) {
+                ni += st[0][i] == kI;
+                ns += st[0][i] == kS;
+            }
+            ni = __reduce_add_sync(0xffffffffu, ni);
+            ns = __reduce_add_sync(0xffffffffu, ns);
+            if ((tid & 31) == 0) {
+                atomicAdd(&cnt_s[0][0], ni);
+                atomicAdd(&cnt_s[0][1], ns);
+            }
+            __syncthreads();
+        }
         for (int64_t t = 0; t < a.steps; ++t) {
             const uint8_t* x = st[cur];
             uint8_t* y = st[cur ^ 1];
-            int n_inf = 0;
-            for (int64_t q = tid; q < nq; q += nt) {
-                const uchar4 v = reinterpret_cast<const uchar4*>(x)[q];
-                const uint8_t in[4] = {v.x, v.y, v.z, v.w};
-                uint8_t o[4];
-                uint4 rec = make_uint4(0u, 0u, 0u, 0u);
-                if (in[0] == kI || in[1] == kI || in[2] == kI || in[3] == kI)
-                    rec = stream_block(key, TAG_SIR_REC, static_cast<unsigned long long>(q), static_cast<uint32_t>(t));
-                const uint32_t rw[4] = {rec.x, rec.y, rec.z, rec.w};
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t i = static_cast<uint32_t>(4 * q + k);
-                    o[k] = in[k];
-                    if (in[k] == kS) {
-                        bool inf = false;
-                        const uint32_t b = rp[i], e = rp[i + 1];
-                        for (uint32_t p = b; p < e && !inf; ++p) {
-                            const uint32_t j = COL_SMEM ? static_cast<uint32_t>(cs[p]) : static_cast<uint32_t>(gcol[p]);
-                            if (x[j] == kI) {
-                                const uint4 w = philox(make_uint4(min(i, j), max(i, j), static_cast<uint32_t>(t), TAG_SIR_TX), key);
-                                inf = static_cast<unsigned long long>(w.x) < tb;
-                            }
-                        }
-                        if (inf) o[k] = kI;
-                    } else if (in[k] == kI) {
-                        if (static_cast<unsigned long long>(rw[k]) < a.t_gamma) o[k] = kR;
-                    }
-                    n_inf += (o[k] == kI);
-                }
-                reinterpret_cast<uchar4*>(y)[q] = make_uchar4(o[0], o[1], o[2], o[3]);
-            }
-            n_inf = __reduce_add_sync(0xffffffffu, n_inf);
-            if ((tid & 31) == 0 && n_inf) atomicAdd(&cnt_s[t & 1], n_inf);
-            __syncthreads();
-            const int total_inf = cnt_s[t & 1];
-            if (tid == 0) cnt_s[(t + 1) & 1] = 0;
-            cur ^= 1;
-            __syncthreads();
-            if (total_inf == 0) {
-                executed = t + 1;
+            const int par = static_cast<int>(t & 1);
+            const int prev_inf = cnt_s[par][0], prev_sus = cnt_s[par][1];
+            if (prev_inf == 0) {  // no infected agent: nothing can change any more
+                executed = t;
                 break;
             }
+            int n_inf = 0, n_sus = 0;
+            if (prev_inf < prev_sus) {
+                // push: recoveries + copy, then each infected agent tries its susceptible
+                // neighbours (S3: the pair-keyed draw makes this identical to pull)
+                for (int64_t q = tid; q < nq; q += nt) {
+                    const uchar4 v = reinterpret_cast<const uchar4*>(x)[q];
+                    uint8_t o[4] = {v.x, v.y, v.z, v.w};
+                    if (o[0] == kI || o[1] == kI || o[2] == kI || o[3] == kI) {
+                        const uint4 rec = stream_block(key, TAG_SIR_REC, static_cast<unsigned long long>(q), static_cast<uint32_t>(t));
+                        const uint32_t rw[4] = {rec.x, rec.y, rec.z, rec.w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (o[k] == kI && static_cast<unsigned long long>(rw[k]) < a.t_gamma) o[k] = kR;
+                    }
+                    reinterpret_cast<uchar4*>(y)[q] = make_uchar4(o[0], o[1], o[2], o[3]);
+                }
+                __syncthreads();
+                for (int64_t i = tid; i < a.n; i += nt) {
+                    if (x[i] != kI) continue;
+                    const uint32_t b = rp[i], e = rp[i + 1];
+                    for (uint32_t p = b; p < e; ++p) {
+                        const uint32_t j = COL_SMEM ? static_cast<uint32_t>(cs[p]) : static_cast<uint32_t>(gcol[p]);
+                        if (x[j] == kS && y[j] == kS) {
+                            const uint32_t ii = static_cast<uint32_t>(i);
+                            const uint4 w = philox(make_uint4(min(ii, j), max(ii, j), static_cast<uint32_t>(t), TAG_SIR_TX), key);
+                            if (static_cast<unsigned long long>(w.x) < tb) y[j] = kI;
+                        }
+                    }
+                }
+                __syncthreads();
+                for (int64_t i = tid; i < a.n; i += nt) {
+                    n_inf += y[i] == kI;
+                    n_sus += y[i] == kS;
+                }
+            } else {
+                // pull: each susceptible scans its row, early exit on the first transmitting edge
+                for (int64_t q = tid; q < nq; q += nt) {
+                    const uchar4 v = reinterpret_cast<const uchar4*>(x)[q];
+                    const uint8_t in[4] = {v.x, v.y, v.z, v.w};
+                    uint8_t o[4];
+                    uint4 rec = make_uint4(0u, 0u, 0u, 0u);
+                    if (in[0] == kI || in[1] == kI || in[2] == kI || in[3] == kI)
+                        rec = stream_block(key, TAG_SIR_REC, static_cast<unsigned long long>(q), static_cast<uint32_t>(t));
+                    const uint32_t rw[4] = {rec.x, rec.y, rec.z, rec.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t i = static_cast<uint32_t>(4 * q + k);
+                        o[k] = in[k];
+                        if (in[k] == kS) {
+                            bool inf = false;
+                            const uint32_t b = rp[i], e = rp[i + 1];
+                            for (uint32_t p = b; p < e && !inf; ++p) {
+                                const uint32_t j = COL_SMEM ? static_cast<uint32_t>(cs[p]) : static_cast<uint32_t>(gcol[p]);
+                                if (x[j] == kI) {
+                                    const uint4 w = philox(make_uint4(min(i, j), max(i, j), static_cast<uint32_t>(t), TAG_SIR_TX), key);
+                                    inf = static_cast<unsigned long long>(w.x) < tb;
+                                }
+                            }
+                            if (inf) o[k] = kI;
+                        } else if (in[k] == kI) {
+                            if (static_cast<unsigned long long>(rw[k]) < a.t_gamma) o[k] = kR;
+                        }
+                        n_inf += (o[k] == kI);
+                        n_sus += (o[k] == kS);
+                    }
+                    reinterpret_cast<uchar4*>(y)[q] = make_uchar4(o[0], o[1], o[2], o[3]);
+                }
+            }
+            n_inf = __reduce_add_sync(0xffffffffu, n_inf);
+            n_sus = __reduce_add_sync(0xffffffffu, n_sus);
+            if ((tid & 31) == 0) {
+                if (n_inf) atomicAdd(&cnt_s[par ^ 1][0], n_inf);
+                if (n_sus) atomicAdd(&cnt_s[par ^ 1][1], n_sus);
+            }
+            __syncthreads();
+            if (tid == 0) cnt_s[par][0] = cnt_s[par][1] = 0;
+            cur ^= 1;
+            __syncthreads();
         }
         // final R count
         int n_rec = 0;
         for (int64_t i = tid; i < a.n; i += nt) n_rec += (st[cur][i] == kR);
         n_rec = __reduce_add_sync(0xffffffffu, n_rec);
-        if (tid == 0) cnt_s[0] = 0;
+        if (tid == 0) cnt_s[0][0] = 0;
         __syncthreads();
-        if ((tid & 31) == 0 && n_rec) atomicAdd(&cnt_s[0], n_rec);
+        if ((tid & 31) == 0 && n_rec) atomicAdd(&cnt_s[0][0], n_rec);
         __syncthreads();
         if (tid == 0) {
-            a.out[r] = static_cast<double>(cnt_s[0]) / static_cast<double>(a.n);
+            a.out[r] = static_cast<double>(cnt_s[0][0]) / static_cast<double>(a.n);
             atomicAdd(a.active_updates, static_cast<unsigned long long>(executed) * a.n);
         }
         __syncthreads();
@@ -160,7 +217,8 @@ void run_sweep(int64_t n, const amber_sir_params& base, const amber_replicate* r
                   "sweep params out of range");
     const int W = rt.world, me = rt.rank;
     const int64_t per = ceil_div(std::max<int64_t>(n_reps, 1), W);
-    const int64_t r0 = std::min<int64_t>(per * me, n_reps), r1 = std::min<int64_t>(per * (me + 1), n_reps);
+    int64_t r0, r1;
+    sweep_range(n_reps, W, me, &r0, &r1);
     const int64_t R = r1 - r0;
     const int64_t m = static_cast<int64_t>(std::floor(static_cast<double>(n) * base.mean_degree / 2.0 + 0.5));
     const int64_t k_inf = static_cast<int64_t>(std::floor(base.init_frac * static_cast<double>(n) + 0.5));

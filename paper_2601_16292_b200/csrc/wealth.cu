@@ -404,8 +404,7 @@ public:
                       "n_agents * w0 must fit int32 wealth of a single agent");
         AMBER_REQUIRE(rt.world == 1 || n < (1ll << 32), "sharded wealth needs n_agents < 2^32");
         shard = ((ceil_div(n, rt.world) + 7) / 8) * 8;
-        lo = std::min<int64_t>(shard * rt.rank, n);
-        hi = std::min<int64_t>(shard * (rt.rank + 1), n);
+        shard_range(n, rt.world, rt.rank, &lo, &hi);
         n_loc = hi - lo;
         n_pad = std::max<int64_t>(ceil_div(std::max<int64_t>(n_loc, 1), kChunkAgents) * kChunkAgents, kChunkAgents);
         if (want_bins) {

@@ -74,6 +74,20 @@ def make_runtime(device=0, stream=None, torch_alloc=True, rank=0, world=1, uniqu
     return rt
 
 
+def shard_range(n_agents: int, world: int, rank: int):
+    """amber_shard_range: this rank's agent range [lo, hi) (host logic, no GPU)."""
+    lo, hi = C.c_int64(), C.c_int64()
+    check(capi.lib().amber_shard_range(int(n_agents), int(world), int(rank), C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+def sweep_range(n_reps: int, world: int, rank: int):
+    """amber_sweep_range: the replicates [r0, r1) this rank runs (host logic, no GPU)."""
+    r0, r1 = C.c_int64(), C.c_int64()
+    check(capi.lib().amber_sweep_range(int(n_reps), int(world), int(rank), C.byref(r0), C.byref(r1)))
+    return r0.value, r1.value
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(capi.lib().amber_nccl_unique_id(buf, 128))

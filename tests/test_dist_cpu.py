@@ -1,0 +1,149 @@
+"""Multi-process (world_size 2 and 4, gloo on CPU) checks of the N>1 host logic.
+
+The GPU data path (NCCL exchange inside libamber.so) cannot run here; these
+tests cover what the ranks must agree on before any kernel runs:
+  * the partition rules the library exposes (amber_shard_range / amber_sweep_range)
+    tile [0, N) / [0, R) exactly, with shard boundaries on 8-agent multiples
+    (R4: two-agent Philox blocks never straddle ranks);
+  * the NCCL unique-id rendezvous used by bench.py (rank 0 creates, all ranks
+    receive the same 128 bytes through torch.distributed);
+  * bench.py's max-over-ranks timing reduction;
+  * the sharded wealth step: receivers bucketed by owner rank (owner = r / shard
+    size, as in the kernel), exchanged with all_to_all, applied by the owner,
+    equal the unsharded oracle step bit for bit.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, fn, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, fn(rank, world)))
+    except Exception as e:  # surface failures to the parent
+        q.put((rank, f"ERROR {type(e).__name__}: {e}"))
+    finally:
+        dist.destroy_process_group()
+
+
+def run_world(world, fn):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fn, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for r, v in out.items():
+        assert not (isinstance(v, str) and v.startswith("ERROR")), v
+    return [out[r] for r in range(world)]
+
+
+def _partitions(rank, world):
+    from paper_2601_16292_b200 import shard_range, sweep_range
+    res = {}
+    for n in (1, 7, 1000, 100_003, 100_000_000):
+        lo, hi = shard_range(n, world, rank)
+        t = torch.tensor([lo, hi], dtype=torch.int64)
+        g = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(g, t)
+        res[n] = [tuple(x.tolist()) for x in g]
+    for R in (0, 5, 4096):
+        r0, r1 = sweep_range(R, world, rank)
+        t = torch.tensor([r0, r1], dtype=torch.int64)
+        g = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(g, t)
+        res[("sweep", R)] = [tuple(x.tolist()) for x in g]
+    return res
+
+
+def _uid(rank, world):
+    from paper_2601_16292_b200 import nccl_unique_id
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def _maxtime(rank, world):
+    import bench
+    return bench.max_over_ranks(dist, torch, float(rank + 1) * 1.5, device="cpu")
+
+
+def _sharded_wealth(rank, world):
+    import oracle
+    from paper_2601_16292_b200 import shard_range
+    n, seed, steps = 1003, 17, 6
+    lo, hi = shard_range(n, world, rank)
+    shard = ((-(-n // world) + 7) // 8) * 8
+    w = np.ones(n, np.int32)[lo:hi].copy()
+    for t in range(steps):
+        send = [[] for _ in range(world)]
+        inc = np.zeros(hi - lo, np.int64)
+        for k, i in enumerate(range(lo, hi)):
+            if w[k] >= 1:
+                r = oracle.wealth_receiver(seed, n, i, t)
+                d = min(r // shard, world - 1)
+                if d == rank:
+                    inc[r - lo] += 1
+                else:
+                    send[d].append(r)
+        counts = torch.tensor([len(s) for s in send], dtype=torch.int64)
+        rc = torch.zeros(world, dtype=torch.int64)
+        dist.all_to_all_single(rc, counts)
+        out = torch.tensor(sum(send, []), dtype=torch.int64)
+        inp = torch.zeros(int(rc.sum()), dtype=torch.int64)
+        dist.all_to_all_single(inp, out, rc.tolist(), counts.tolist())
+        for r in inp.tolist():
+            inc[r - lo] += 1
+        w = (w - (w >= 1) + inc).astype(np.int32)
+    g = [None] * world
+    dist.all_gather_object(g, (lo, w.tolist()))
+    return g
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_partitions_tile_exactly(world):
+    res = run_world(world, _partitions)[0]
+    for key, parts in res.items():
+        total = key[1] if isinstance(key, tuple) else key
+        cur = 0
+        for lo, hi in parts:
+            assert lo == min(cur, total) and lo <= hi
+            if not isinstance(key, tuple) and hi < total:
+                assert hi % 8 == 0
+            cur = hi
+        assert cur == total
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_nccl_unique_id_rendezvous(world):
+    ids = run_world(world, _uid)
+    assert len(ids[0]) == 128 and all(x == ids[0] for x in ids)
+
+
+def test_max_over_ranks():
+    assert run_world(2, _maxtime) == [3.0, 3.0]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_wealth_step_equals_oracle(world, orc):
+    parts = run_world(world, _sharded_wealth)[0]
+    w = np.concatenate([np.array(x, np.int32) for _, x in sorted(parts)])
+    ref = orc.wealth_run(np.ones(1003, np.int32), 17, 0, 6)[0]
+    assert np.array_equal(w, ref)
