@@ -30,6 +30,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "agent-updates/sec per step (1/2/4/8 B200) and % of HBM roofline vs CPU oracle"
 UNIT = "agent-updates/s"
+# random 32-bit L2 atomics, any target set that fits L2 (measured on this pool's B200,
+# tools/red_ceiling.cu -> profiles/r01_red_ceiling.txt): the scatter's binding roof
+RED_CEILING = 1.85e11
 
 
 def peaks():
@@ -234,6 +237,10 @@ def bench_wealth(args):
     m.profile(False)
     tot = m.metrics("total_wealth")
     assert (tot == n * cfg["w0"]).all(), "wealth not conserved"
+    # scatter REDs issued in the timed region = senders of each timed step =
+    # agents with w >= amount in the state the step starts from
+    act = m.metrics("active")
+    reds = float(act[-args.steps - 1:-1].sum()) if len(act) > args.steps else float(act[:-1].sum())
     launches = sum(c for _, c, _ in prof)
     dom = max(prof, key=lambda r: r[2]) if prof else ("", 0, 0.0)
     dom_avg_ms = dom[2] / max(dom[1], 1)
@@ -282,6 +289,13 @@ def bench_wealth(args):
                          "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                          "avg_launch_ms": dom_avg_ms,
                          "share_of_step": dom[2] / ms if ms > 0 else None},
+            "l2_atomic_roof": {
+                "bound": "l2_atomics", "kernel": dom[0],
+                "achieved_reds_per_s": reds / (ms / 1e3) if ms > 0 else None,
+                "peak_reds_per_s": RED_CEILING, "peak_kind": "measured (tools/red_ceiling.cu, "
+                "profiles/r01_red_ceiling.txt)",
+                "frac": (reds / (ms / 1e3)) / RED_CEILING if ms > 0 else None,
+                "reds_per_step": reds / args.steps},
             "kernels": [{"name": a, "launches": b, "total_ms": c} for a, b, c in prof],
             "gpu_launches": launches,
             "e2e": e2e,
