@@ -277,6 +277,13 @@ int amber_sweep_range(int64_t n_reps, int world, int rank, int64_t* r0, int64_t*
  * Errors: NCCL (libnccl.so.2 not loadable: set AMBER_NCCL_LIB to its path). */
 int amber_nccl_unique_id(void* out, size_t out_bytes);
 
+/* Write a 128-byte id for an in-process LOOPBACK group (testing/emulation):
+ * `world` models created with this id (rank 0..world-1) on one device form a
+ * sharded model whose exchanges are host barriers + device-to-device copies
+ * instead of NCCL.  Each rank's calls must come from its own host thread
+ * (collective calls block until every rank has made them).  Errors: INVALID_ARG. */
+int amber_loopback_id(void* out, size_t out_bytes);
+
 #ifdef __cplusplus
 }
 #endif

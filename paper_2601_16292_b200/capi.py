@@ -27,7 +27,7 @@ SYMBOLS = ["amber_version", "amber_last_error", "amber_model_create", "amber_mod
            "amber_column_info", "amber_read_column", "amber_write_column", "amber_read_metrics",
            "amber_reset_metrics", "amber_digest", "amber_set_option", "amber_get_option",
            "amber_profile_enable", "amber_profile_query", "amber_sweep", "amber_shard_range",
-           "amber_sweep_range", "amber_nccl_unique_id"]
+           "amber_sweep_range", "amber_nccl_unique_id", "amber_loopback_id"]
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -118,6 +118,7 @@ def load():
         "amber_shard_range": (C.c_int, [C.c_int64, C.c_int, C.c_int, i64p, i64p]),
         "amber_sweep_range": (C.c_int, [C.c_int64, C.c_int, C.c_int, i64p, i64p]),
         "amber_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_size_t]),
+        "amber_loopback_id": (C.c_int, [C.c_void_p, C.c_size_t]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -6,6 +6,7 @@
 #include "internal.cuh"
 
 extern "C" int amber_nccl_unique_id_impl(void* out, size_t out_bytes);
+extern "C" int amber_loopback_id_impl(void* out, size_t out_bytes);
 
 namespace {
 
@@ -269,6 +270,11 @@ int amber_sweep_range(int64_t n_reps, int world, int rank, int64_t* r0, int64_t*
         amber::sweep_range(n_reps, world, rank, r0, r1);
         return 0;
     });
+}
+
+int amber_loopback_id(void* out, size_t out_bytes)
+{
+    return guarded([&] { return amber_loopback_id_impl(out, out_bytes); });
 }
 
 int amber_nccl_unique_id(void* out, size_t out_bytes)

@@ -13,6 +13,10 @@
 // receive kernel adds them to the owner's counters.
 #include <dlfcn.h>
 
+#include <atomic>
+#include <condition_variable>
+#include <map>
+#include <memory>
 #include <mutex>
 
 #include "internal.cuh"
@@ -115,9 +119,79 @@ void comm_allgather_f64(Comm* c, cudaStream_t s, const double* send, double* rec
     nccl_check(nccl().AllGather(send, recv, n_per_rank, ncclFloat64, c->comm, s), "ncclAllGather");
 }
 
+// ---------------------------------------------------------------- loopback transport
+// In-process stand-in for NCCL: `world` virtual shards of one model on ONE
+// device, each driven from its own host thread.  Exchanges are host barriers
+// plus device-to-device copies; no kernel ever waits on another, so it is safe
+// on a single GPU.  Used by the tests to run the sharded algorithm end to end.
+static const char kLoopbackMagic[8] = {'A', 'M', 'B', 'E', 'R', 'L', 'B', 0};
+
+struct LoopbackHub {
+    int world = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long long generation = 0;
+    std::vector<std::vector<unsigned>> counts;       // [rank][peer]
+    std::vector<const uint32_t*> send_ids;           // [rank]
+    std::vector<uint64_t> send_cap;                  // [rank]
+    std::vector<std::vector<unsigned long long>> vals;  // [rank][k]
+
+    explicit LoopbackHub(int w) : world(w), counts(w), send_ids(w, nullptr), send_cap(w, 0), vals(w) {}
+
+    void barrier()
+    {
+        std::unique_lock<std::mutex> lk(mu);
+        const long long gen = generation;
+        if (++arrived == world) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return generation != gen; });
+        }
+    }
+};
+
+std::shared_ptr<LoopbackHub> loopback_hub(const char* id, int world)
+{
+    static std::mutex reg_mu;
+    static std::map<std::string, std::weak_ptr<LoopbackHub>> reg;
+    std::lock_guard<std::mutex> g(reg_mu);
+    std::string key(id, 128);
+    auto it = reg.find(key);
+    if (it != reg.end())
+        if (auto h = it->second.lock()) {
+            AMBER_REQUIRE(h->world == world, "loopback group world size mismatch");
+            return h;
+        }
+    auto h = std::make_shared<LoopbackHub>(world);
+    reg[key] = h;
+    return h;
+}
+
+// Loopback all-gather of equal-size double blocks (sweep results); false if
+// `r` does not name a loopback group.
+bool loopback_allgather_f64(const amber_runtime* r, const std::vector<double>& mine, std::vector<double>& all)
+{
+    if (!r || !r->nccl_unique_id || std::memcmp(r->nccl_unique_id, kLoopbackMagic, sizeof(kLoopbackMagic)) != 0)
+        return false;
+    auto hub = loopback_hub(static_cast<const char*>(r->nccl_unique_id), r->world);
+    std::vector<unsigned long long> bits(mine.size());
+    std::memcpy(bits.data(), mine.data(), mine.size() * 8);
+    hub->vals[r->rank] = bits;
+    hub->barrier();
+    all.assign(mine.size() * r->world, 0.0);
+    for (int p = 0; p < r->world; ++p) std::memcpy(all.data() + p * mine.size(), hub->vals[p].data(), mine.size() * 8);
+    hub->barrier();
+    return true;
+}
+
 // ---------------------------------------------------------------- wealth exchange
 struct WealthExchange {
-    Comm* comm = nullptr;
+    Comm* comm = nullptr;                 // NCCL transport
+    std::shared_ptr<LoopbackHub> hub;     // or the loopback transport
+    int rank = 0, world = 1;
     DevBuf<unsigned int> send_counts_copy, recv_counts;
     std::vector<unsigned int> h_send, h_recv;
     DevBuf<unsigned long long> flag;
@@ -126,7 +200,14 @@ struct WealthExchange {
 WealthExchange* make_wealth_exchange_rt(Runtime& rt, const amber_runtime* r)
 {
     auto* x = new WealthExchange;
-    x->comm = make_comm(r);
+    x->rank = rt.rank;
+    x->world = rt.world;
+    AMBER_REQUIRE(r && r->nccl_unique_id, "world > 1 needs amber_runtime.nccl_unique_id");
+    if (std::memcmp(r->nccl_unique_id, kLoopbackMagic, sizeof(kLoopbackMagic)) == 0) {
+        x->hub = loopback_hub(static_cast<const char*>(r->nccl_unique_id), rt.world);
+    } else {
+        x->comm = make_comm(r);
+    }
     x->send_counts_copy.allocate(&rt, rt.world);
     x->recv_counts.allocate(&rt, rt.world);
     x->flag.allocate(&rt, 1);
@@ -138,7 +219,8 @@ WealthExchange* make_wealth_exchange_rt(Runtime& rt, const amber_runtime* r)
 void destroy_wealth_exchange(WealthExchange* x)
 {
     if (!x) return;
-    destroy_comm(x->comm);
+    if (x->comm) destroy_comm(x->comm);
+    x->hub.reset();
     x->send_counts_copy.reset();
     x->recv_counts.reset();
     x->flag.reset();
@@ -151,6 +233,31 @@ void wealth_exchange_run(WealthExchange* x, Runtime& rt, const unsigned int* d_s
                          const uint32_t* d_send_ids, uint64_t send_cap, uint32_t* d_recv_ids,
                          unsigned long long* d_recv_total)
 {
+    if (x->hub) {  // loopback: post, barrier, pull the peers' buckets addressed to me, barrier
+        LoopbackHub& h = *x->hub;
+        const int W = x->world, me = x->rank;
+        AMBER_CUDA(cudaMemcpyAsync(x->h_send.data(), d_send_counts, W * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                   rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));  // send buckets complete
+        h.counts[me].assign(x->h_send.begin(), x->h_send.end());
+        h.send_ids[me] = d_send_ids;
+        h.send_cap[me] = send_cap;
+        h.barrier();
+        unsigned long long total = 0;
+        for (int p = 0; p < W; ++p) {
+            if (p == me) continue;
+            const unsigned long long c = h.counts[p][me];
+            if (c > h.send_cap[p]) fail(AMBER_E_CUDA, "wealth exchange: send bucket overflow");
+            if (c)
+                AMBER_CUDA(cudaMemcpyAsync(d_recv_ids + total, h.send_ids[p] + static_cast<uint64_t>(me) * h.send_cap[p],
+                                           c * sizeof(uint32_t), cudaMemcpyDeviceToDevice, rt.stream));
+            total += c;
+        }
+        AMBER_CUDA(cudaMemcpyAsync(d_recv_total, &total, sizeof(total), cudaMemcpyHostToDevice, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        h.barrier();  // peers may now reuse their send buckets
+        return;
+    }
     NcclApi& api = nccl();
     const int W = x->comm->world, me = x->comm->rank;
     // 1) sizes: one count to each peer
@@ -182,8 +289,22 @@ void wealth_exchange_run(WealthExchange* x, Runtime& rt, const unsigned int* d_s
     AMBER_CUDA(cudaStreamSynchronize(rt.stream));  // `total` lives on this host stack frame
 }
 
+// loopback all-reduce (sum) of n host values
+static std::vector<unsigned long long> loopback_sum(WealthExchange* x, const std::vector<unsigned long long>& mine)
+{
+    LoopbackHub& h = *x->hub;
+    h.vals[x->rank] = mine;
+    h.barrier();
+    std::vector<unsigned long long> out(mine.size(), 0ull);
+    for (int p = 0; p < x->world; ++p)
+        for (size_t k = 0; k < out.size(); ++k) out[k] += h.vals[p][k];
+    h.barrier();
+    return out;
+}
+
 bool wealth_exchange_any(WealthExchange* x, Runtime& rt, bool local_flag)
 {
+    if (x->hub) return loopback_sum(x, {local_flag ? 1ull : 0ull})[0] != 0;
     unsigned long long v = local_flag ? 1ull : 0ull;
     AMBER_CUDA(cudaMemcpyAsync(x->flag.p, &v, 8, cudaMemcpyHostToDevice, rt.stream));
     comm_allreduce_u64(x->comm, rt.stream, x->flag.p, 1);
@@ -194,10 +315,32 @@ bool wealth_exchange_any(WealthExchange* x, Runtime& rt, bool local_flag)
 
 void wealth_exchange_allreduce_u64(WealthExchange* x, Runtime& rt, unsigned long long* d_vals, int n)
 {
+    if (x->hub) {
+        std::vector<unsigned long long> h(n);
+        AMBER_CUDA(cudaMemcpyAsync(h.data(), d_vals, n * 8, cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        h = loopback_sum(x, h);
+        AMBER_CUDA(cudaMemcpyAsync(d_vals, h.data(), n * 8, cudaMemcpyHostToDevice, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        return;
+    }
     comm_allreduce_u64(x->comm, rt.stream, d_vals, static_cast<size_t>(n));
 }
 
 }  // namespace amber
+
+extern "C" int amber_loopback_id_impl(void* out, size_t out_bytes)
+{
+    using namespace amber;
+    AMBER_REQUIRE(out && out_bytes >= 128, "amber_loopback_id needs a 128-byte buffer");
+    static std::atomic<unsigned long long> counter{1};
+    char id[128] = {0};
+    std::memcpy(id, kLoopbackMagic, sizeof(kLoopbackMagic));
+    const unsigned long long k = counter.fetch_add(1);
+    std::memcpy(id + 8, &k, sizeof(k));
+    std::memcpy(out, id, 128);
+    return 0;
+}
 
 extern "C" int amber_nccl_unique_id_impl(void* out, size_t out_bytes)
 {

@@ -88,6 +88,13 @@ def sweep_range(n_reps: int, world: int, rank: int):
     return r0.value, r1.value
 
 
+def loopback_id() -> bytes:
+    """amber_loopback_id: id of an in-process loopback group (virtual shards on one GPU)."""
+    buf = C.create_string_buffer(128)
+    check(capi.lib().amber_loopback_id(buf, 128))
+    return buf.raw
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(capi.lib().amber_nccl_unique_id(buf, 128))
