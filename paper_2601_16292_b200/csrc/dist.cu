@@ -86,15 +86,16 @@ struct Comm {
 
 Comm* make_comm(const amber_runtime* r)
 {
-    AMBER_REQUIRE(r && r->world > 1 && r->nccl_unique_id, "world > 1 needs amber_runtime.nccl_unique_id");
+    AMBER_REQUIRE(r && r->nccl_unique_id, "a communicator needs amber_runtime.nccl_unique_id");
+    const int world = r->world > 1 ? r->world : 1;
     NcclApi& api = nccl();
     ncclUniqueId id;
     std::memcpy(&id, r->nccl_unique_id, sizeof(id));
     auto* c = new Comm;
     c->rank = r->rank;
-    c->world = r->world;
+    c->world = world;
     AMBER_CUDA(cudaSetDevice(r->device));
-    ncclResult_t res = api.CommInitRank(&c->comm, r->world, id, r->rank);
+    ncclResult_t res = api.CommInitRank(&c->comm, world, id, r->rank);
     if (res != ncclSuccess) {
         delete c;
         nccl_check(res, "ncclCommInitRank");

@@ -393,7 +393,8 @@ public:
         key = philox_key(seed);
         // counter_bits -1: range-partitioned scatter (wealth_bins.cu, single GPU);
         // 0: default = 4-bit packed counters with L2 atomics (measured faster)
-        const bool want_bins = p.counter_bits == -1 && (r == nullptr || r->world <= 1);
+        const bool want_bins = p.counter_bits == -1 && (r == nullptr || r->world <= 1) &&
+                               !(getenv("AMBER_TEST_FORCE_EXCHANGE") && r && r->nccl_unique_id);
         if (p.counter_bits <= 0) p.counter_bits = 4;
         B = p.counter_bits;
         AMBER_REQUIRE(B == 2 || B == 4 || B == 8 || B == 16 || B == 32, "counter_bits must be 0,2,4,8,16,32");
@@ -431,7 +432,11 @@ public:
         for (auto& b : wb) b.zero_async(rt.stream);
         wealth_fill_kernel<<<rt.num_sms * 4, 256, 0, rt.stream>>>(wb[0].p, n_loc, n_pad, p.w0);
         check_launch("wealth_fill_kernel");
-        if (rt.world > 1) {
+        // AMBER_TEST_FORCE_EXCHANGE=1 with a unique id builds the exchange even for
+        // world == 1 (a one-rank NCCL communicator): exercises the NCCL plumbing on one GPU
+        const char* force = getenv("AMBER_TEST_FORCE_EXCHANGE");
+        const bool force_x = force && force[0] == '1' && r && r->nccl_unique_id && rt.world == 1;
+        if (rt.world > 1 || force_x) {
             xch = make_wealth_exchange_rt(rt, r);
             send_cap = static_cast<uint64_t>(std::max<int64_t>(n_loc, 1));
             send_ids.allocate(&rt, send_cap * rt.world);
@@ -530,7 +535,7 @@ public:
         a.slot_apply = apply ? slot(ta) : nullptr;
         a.slot_scatter = scatter ? slot(ts) : nullptr;
         a.slot_zero = (apply && scatter) ? slot(ta + 2) : nullptr;
-        const bool remote = rt.world > 1 && scatter;
+        const bool remote = xch != nullptr && scatter;
         if (remote) {
             a.world = rt.world;
             a.shard_size = static_cast<unsigned long long>(shard);
@@ -578,7 +583,7 @@ public:
         check_launch("zero_slots_kernel");
     }
 
-    bool small_path() const { return rt.world == 1 && n <= kSmallMax && !bins && persistent; }
+    bool small_path() const { return rt.world == 1 && !xch && n <= kSmallMax && !bins && persistent; }
 
     void step(int64_t nsteps) override
     {

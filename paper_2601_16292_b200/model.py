@@ -64,7 +64,7 @@ def make_runtime(device=0, stream=None, torch_alloc=True, rank=0, world=1, uniqu
         rt.alloc, rt.free = ta.alloc, ta.free
         keep.append(ta)
     rt.rank, rt.world = rank, world
-    if world > 1:
+    if world > 1 or unique_id is not None:
         if unique_id is None or len(unique_id) < 128:
             raise ValueError("world > 1 needs the 128-byte NCCL unique id")
         buf = C.create_string_buffer(bytes(unique_id), 128)

@@ -94,3 +94,19 @@ def test_split_sweep_equals_single(orc):
         assert np.array_equal(o, single)
     want = orc.sir_sweep(c["n"], c["mean_degree"], c["gamma"], c["init_frac"], betas[pick], seeds[pick], 120)
     assert np.array_equal(single, want)
+
+
+def test_nccl_plumbing_single_rank(orc, monkeypatch):
+    # one-rank NCCL communicator from amber_nccl_unique_id: dlopen of torch's NCCL,
+    # ncclCommInitRank, grouped ncclSend/ncclRecv of the bucket counts, ncclAllReduce
+    # of the overflow flag and of the metrics -- the NCCL calls the multi-GPU run makes
+    from paper_2601_16292_b200 import nccl_unique_id
+    monkeypatch.setenv("AMBER_TEST_FORCE_EXCHANGE", "1")
+    n, seed = 70_001, 12
+    m = Model("wealth", n, wealth_params(counter_bits=2), seed, unique_id=nccl_unique_id())
+    m.step(15)
+    ref, tot, _, _ = orc.wealth_run(np.ones(n, np.int32), seed, 0, 15)
+    assert np.array_equal(m.read_column("wealth"), ref)
+    assert np.array_equal(m.metrics("total_wealth"), tot)
+    assert m.digest("wealth") == orc.digest(ref)
+    assert m.get_option("replays") > 0
