@@ -351,6 +351,56 @@ __global__ void __launch_bounds__(256) sir_step_kernel(const SirStepArgs a)
 }
 
 // All n_steps steps in one cooperative launch (grid barrier between steps).
+// Push step (direction-optimizing, persistent kernel only).  x = state t,
+// y = the other ping-pong buffer, which holds state t-1 because the previous
+// step of this launch wrote it.  Every agent that is S at t was S at t-1, so y
+// already reads S there; only I/R agents and newly infected agents change.
+// All updates of y are 32-bit atomics on the byte's word (exact new-infection
+// count from the returned old value; duplicates from several infected
+// neighbours are harmless).  Result identical to pull by S3.
+__device__ __forceinline__ void sir_push_body(const SirStepArgs& a, const uint8_t* __restrict__ x, uint8_t* y, uint32_t t,
+                                              long long (&d)[3])
+{
+    uint32_t* yw = reinterpret_cast<uint32_t*>(y);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t st = x[i];
+        if (st == kS || st == kPad) continue;
+        const uint32_t sh = static_cast<uint32_t>(i & 3) * 8;
+        const uint8_t old = y[i];  // state t-1 of agent i: nobody else writes this byte in this step
+        uint8_t nw = kR;
+        if (st == kI) {
+            const uint4 rec = stream_block(a.key, TAG_SIR_REC, static_cast<unsigned long long>(i >> 2), t);
+            const uint32_t k = static_cast<uint32_t>(i & 3);
+            const uint32_t dr = k == 0 ? rec.x : (k == 1 ? rec.y : (k == 2 ? rec.z : rec.w));
+            nw = (static_cast<unsigned long long>(dr) < a.t_gamma) ? kR : kI;
+            if (nw == kR) {
+                d[1] -= 1;
+                d[2] += 1;
+            }
+            const int32_t b = a.row_ptr[i], e = a.row_ptr[i + 1];
+            const uint32_t ii = static_cast<uint32_t>(i);
+            for (int32_t p = b; p < e; ++p) {
+                const uint32_t j = static_cast<uint32_t>(__ldg(a.col + p));
+                if (x[j] != kS) continue;
+                const uint4 w = philox(make_uint4(min(ii, j), max(ii, j), t, TAG_SIR_TX), a.key);
+                if (static_cast<unsigned long long>(w.x) < a.t_beta) {
+                    const uint32_t sj = (j & 3u) * 8u;
+                    const uint32_t prev = atomicOr(yw + (j >> 2), 1u << sj);
+                    if (((prev >> sj) & 0xFFu) == kS) {
+                        d[0] -= 1;
+                        d[1] += 1;
+                    }
+                }
+            }
+        }
+        if (nw != old) atomicAdd(yw + (i >> 2), static_cast<uint32_t>(nw - old) << sh);
+    }
+}
+
+// All n_steps steps in one cooperative launch (grid barrier between steps).
+// Step k > 0 pushes from the infected agents when they are fewer than the
+// susceptible ones (counts of the previous step, read from its ring slot after
+// the barrier, so every block takes the same decision); otherwise it pulls.
 __global__ void __launch_bounds__(256) sir_persistent_kernel(const SirStepArgs a)
 {
     cg::grid_group grid = cg::this_grid();
@@ -358,11 +408,34 @@ __global__ void __launch_bounds__(256) sir_persistent_kernel(const SirStepArgs a
     int cur = a.cur;
     for (int64_t k = 0; k < a.n_steps; ++k) {
         const uint32_t t = a.t0 + static_cast<uint32_t>(k);
-        unsigned long long cnt[4] = {0, 0, 0, 0};
-        sir_step_body(a, a.x[cur], a.x[cur ^ 1], t, cnt, &wmask[threadIdx.x >> 5]);
         SirSlot* sl = a.ring + (t % a.ring_cap);
-        unsigned long long* const outs[4] = {&sl->S, &sl->I, &sl->R, a.digest ? &sl->digest : nullptr};
-        block_sum_atomic<4>(cnt, outs);
+        bool push = false;
+        unsigned long long prev_s = 0, prev_i = 0, prev_r = 0;
+        if (k > 0 && !a.digest) {
+            const SirSlot* pv = a.ring + ((t - 1) % a.ring_cap);
+            prev_s = pv->S;
+            prev_i = pv->I;
+            prev_r = pv->R;
+            push = prev_i < prev_s;
+        }
+        if (push) {
+            long long d[3] = {0, 0, 0};
+            sir_push_body(a, a.x[cur], a.x[cur ^ 1], t, d);
+            unsigned long long v[3] = {static_cast<unsigned long long>(d[0]), static_cast<unsigned long long>(d[1]),
+                                       static_cast<unsigned long long>(d[2])};
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                v[0] += prev_s;
+                v[1] += prev_i;
+                v[2] += prev_r;
+            }
+            unsigned long long* const outs[3] = {&sl->S, &sl->I, &sl->R};
+            block_sum_atomic<3>(v, outs);
+        } else {
+            unsigned long long cnt[4] = {0, 0, 0, 0};
+            sir_step_body(a, a.x[cur], a.x[cur ^ 1], t, cnt, &wmask[threadIdx.x >> 5]);
+            unsigned long long* const outs[4] = {&sl->S, &sl->I, &sl->R, a.digest ? &sl->digest : nullptr};
+            block_sum_atomic<4>(cnt, outs);
+        }
         cur ^= 1;
         grid.sync();
     }
@@ -455,7 +528,9 @@ public:
             if (persistent && chunk > 1) {
                 int per_sm = 0;
                 AMBER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sir_persistent_kernel, threads, 0));
-                int blocks = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(per_sm) * rt.num_sms,
+                // latency-bound: many resident warps help, but the grid barrier
+                // cost grows with the block count; 3 blocks/SM measured best (C2)
+                int blocks = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(std::min(per_sm, 3)) * rt.num_sms,
                                                                 ceil_div(n_pad, threads)));
                 if (grid) blocks = static_cast<int>(std::min<int64_t>(grid, static_cast<int64_t>(per_sm) * rt.num_sms));
                 blocks = std::max(blocks, 1);
