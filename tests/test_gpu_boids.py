@@ -121,6 +121,17 @@ def test_geometry_invariance_and_io(orc):
     for x, y in zip(state(a), state(b)):
         assert np.array_equal(x, y)
     # write/read round trip through the permuted internal order
+    e = make(cfg)
+    e.set_option("fused", 1)  # one cooperative launch for all phases and steps
+    e.step(10)
+    for x, y in zip(state(a), state(e)):
+        assert np.array_equal(x, y)
+    for lanes in (1, 4, 16):
+        d = make(cfg)
+        d.set_option("lanes", lanes)
+        d.step(10)
+        for x, y in zip(state(a), state(d)):
+            assert np.array_equal(x, y)
     c = make(cfg)
     c.step(3)
     s = state(c)
