@@ -1,0 +1,118 @@
+#!/usr/bin/env python
+"""Measure every BASELINE config on one B200 through the public API, with the
+CPU oracle timed beside it (single thread, bounded samples), and write one JSON
+object per config to stdout (collected into profiles/rNN_all_configs.jsonl).
+
+GPU timing: CUDA events on the model stream around amber_step(K) after a
+warm-up call; per-kernel device time from the library's event profiler.
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402  (tests/bench-only dependency: the CPU baseline)
+from paper_2601_16292_b200 import Model, boids_params, sir_params, sweep, wealth_params  # noqa: E402
+from paper_2601_16292_b200 import workloads as W  # noqa: E402
+
+HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+
+
+def timed(m, k):
+    m.step(2)
+    m.synchronize()
+    m.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(m.stream)
+    m.step(k)
+    e1.record(m.stream)
+    m.synchronize()
+    ms = e0.elapsed_time(e1)
+    prof = m.profile_results()
+    m.profile(False)
+    return ms, prof
+
+
+def cpu_rate(fn, units):
+    t0 = time.perf_counter()
+    fn()
+    return units / (time.perf_counter() - t0)
+
+
+def main():
+    out = []
+    # C1
+    c = W.C1_WEALTH_SMALL
+    m = Model("wealth", c["n"], wealth_params(), c["seed"])
+    ms, prof = timed(m, c["steps"])
+    cpu = cpu_rate(lambda: oracle.wealth_run(np.ones(c["n"], np.int32), c["seed"], 0, c["steps"]),
+                   c["n"] * c["steps"])
+    out.append(dict(config="C1 wealth N=1e3 x100", us_per_step=ms / c["steps"] * 1e3,
+                    agent_updates_per_s=c["n"] * c["steps"] / ms * 1e3, kernels=prof,
+                    bound="launch/latency (single-CTA, all steps one launch)", cpu_oracle_per_s=cpu))
+    m.close()
+    # C2
+    c = W.C2_SIR
+    m = Model("sir", c["n"], sir_params(c["mean_degree"], c["beta"], c["gamma"], c["init_frac"]), c["seed"])
+    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
+    m.close()
+    m = Model("sir", c["n"], sir_params(c["mean_degree"], c["beta"], c["gamma"], c["init_frac"]), c["seed"])
+    ms, prof = timed(m, c["steps"])
+    _, k_inf = W.sir_counts(c)
+    st = oracle.sir_init(c["n"], k_inf, c["seed"])
+    cpu = cpu_rate(lambda: oracle.sir_run(rp, col, st, c["seed"], c["beta"], c["gamma"], 0, c["steps"]),
+                   c["n"] * c["steps"])
+    out.append(dict(config="C2 SIR G(1e5,5e5) x200", us_per_step=ms / c["steps"] * 1e3,
+                    agent_updates_per_s=c["n"] * c["steps"] / ms * 1e3, kernels=prof,
+                    bound="latency (L2-resident 4.6 MB; grid barrier per step)", cpu_oracle_per_s=cpu))
+    m.close()
+    # C3
+    c = W.C3_BOIDS
+    bp = boids_params(*[c[k] for k in ("L", "R", "rs", "wc", "wa", "ws", "vmax", "dt")])
+    m = Model("boids", c["n"], bp, c["seed"])
+    ms, prof = timed(m, c["steps"])
+    P = oracle.boids_params(**{k: c[k] for k in ("L", "R", "rs", "wc", "wa", "ws", "vmax", "dt")})
+    s0 = oracle.boids_init(c["n"], c["L"], c["seed"])
+    cpu = cpu_rate(lambda: oracle.boids_run(s0, P, 3), c["n"] * 3)
+    out.append(dict(config="C3 Boids N=1e5 x100", us_per_step=ms / c["steps"] * 1e3,
+                    agent_updates_per_s=c["n"] * c["steps"] / ms * 1e3, kernels=prof,
+                    bound="issue/latency (fp32+int64 stencil, L1-resident)",
+                    cpu_oracle_per_s=cpu, cpu_sample="first 3 steps (sparse phase; later steps denser)"))
+    m.close()
+    # C4 (short run; the driver line is bench.py)
+    c = W.C4_WEALTH_SCALE
+    m = Model("wealth", c["n"], wealth_params(), c["seed"])
+    ms, prof = timed(m, 200)
+    dom = max(prof, key=lambda r: r[2])
+    avg = dom[2] / dom[1]
+    out.append(dict(config="C4 wealth N=1e8 x200 (of 1000)", us_per_step=ms / 200 * 1e3,
+                    agent_updates_per_s=c["n"] * 200 / ms * 1e3, kernels=prof,
+                    hbm_frac=8 * c["n"] / (avg / 1e3) / 1e9 / HBM,
+                    bound="L2 atomics (random REDs, profiles/r01_red_ceiling.txt)"))
+    m.close()
+    # C5
+    c = W.C5_SWEEP
+    betas, seeds = W.sweep_replicates(c)
+    res, stt = sweep(c["n"], sir_params(c["mean_degree"], 0.0, c["gamma"], c["init_frac"]), betas, seeds,
+                     c["steps"], with_stats=True)
+    pick = np.arange(0, 4096, 256)
+    cpu = cpu_rate(lambda: oracle.sir_sweep(c["n"], c["mean_degree"], c["gamma"], c["init_frac"], betas[pick],
+                                            seeds[pick], c["steps"]), c["n"] * c["steps"] * len(pick))
+    out.append(dict(config="C5 sweep 4096 x N=1e4 x300", step_ms=stt["step_ms"], build_ms=stt["build_ms"],
+                    agent_updates_per_s=stt["agent_updates"] / stt["step_ms"] * 1e3,
+                    active_updates_per_s=stt["active_updates"] / stt["step_ms"] * 1e3,
+                    bound="shared-memory latency (graphs smem-resident, early exit)",
+                    cpu_oracle_per_s=cpu, cpu_sample="16 replicates spanning all betas (nominal updates)"))
+    for o in out:
+        print(json.dumps(o), flush=True)
+
+
+if __name__ == "__main__":
+    main()
