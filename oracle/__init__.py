@@ -31,6 +31,8 @@ TAG_SIR_INIT = 0x12
 TAG_GRAPH = 0x13
 TAG_BOIDS_POS = 0x20
 TAG_BOIDS_VEL = 0x21
+TAG_WALK_POS = 0x30
+TAG_WALK_VEL = 0x31
 S, I, R = 0, 1, 2
 
 
@@ -98,6 +100,11 @@ def lib():
             "orc_boids_run": (C.c_int, [C.c_int64, C.POINTER(BoidsParams), C.c_int64] + [f32p] * 4
                               + [f64p, f64p]),
             "orc_boids_step_brute_f64": (None, [C.c_int64, C.POINTER(BoidsParams)] + [f64p] * 8),
+            "orc_walk_init": (None, [C.c_int64, C.c_float, C.c_uint64, f32p, f32p]),
+            "orc_walk_step": (None, [C.c_int64, C.c_float, C.c_float, C.c_uint64, C.c_uint32, f32p, f32p,
+                                     f32p, f32p]),
+            "orc_walk_run": (C.c_int, [C.c_int64, C.c_float, C.c_float, C.c_uint64, C.c_uint32,
+                                       C.c_int64, f32p, f32p, f32p, f32p, f64p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -317,3 +324,28 @@ def boids_step_f64(state, P):
     lib().orc_boids_step_brute_f64(arrs[0].size, C.byref(P),
                                    *[_p(a, C.c_double) for a in (*arrs, *outs)])
     return tuple(outs)
+
+
+# ------------------------------------------------------------ Random Walk (K)
+def walk_init(n, L, seed):
+    px, py = np.zeros(n, np.float32), np.zeros(n, np.float32)
+    lib().orc_walk_init(n, L, seed, _p(px, C.c_float), _p(py, C.c_float))
+    return px, py
+
+
+def walk_step(px, py, L, vmax, seed, t):
+    px, py = _f32(px), _f32(py)
+    ox, oy = np.empty_like(px), np.empty_like(py)
+    lib().orc_walk_step(px.size, L, vmax, seed, t, _p(px, C.c_float), _p(py, C.c_float),
+                        _p(ox, C.c_float), _p(oy, C.c_float))
+    return ox, oy
+
+
+def walk_run(px, py, L, vmax, seed, t0, steps, origin=None):
+    """Returns (px, py, mean_displacement[steps]) ; origin defaults to the input positions."""
+    px, py = _f32(px).copy(), _f32(py).copy()
+    ox, oy = (px.copy(), py.copy()) if origin is None else (_f32(origin[0]), _f32(origin[1]))
+    md = np.zeros(max(steps, 1), np.float64)
+    _check(lib().orc_walk_run(px.size, L, vmax, seed, t0, steps, _p(px, C.c_float), _p(py, C.c_float),
+                              _p(ox, C.c_float), _p(oy, C.c_float), _p(md, C.c_double)))
+    return px, py, md[:steps]

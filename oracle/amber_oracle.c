@@ -689,3 +689,65 @@ void orc_boids_step_brute_f64(int64_t n, const orc_boids_params* P, const double
         opx[i] = x; opy[i] = y; ovx[i] = ux; ovy[i] = uy;
     }
 }
+
+/* ======================================================================== */
+/* Random Walk (Sec. 5.1.1: "agents move in continuous 2D */
+/* space according to random velocity vectors with boundary handling";      */
+/* Sec. 5.3: "vector additions ... boundary handling applied as    */
+/* vectorized clipping").  Contract items K1-K3.                */
+/* ======================================================================== */
+
+/* K1: positions uniform in [0, L)^2 from 32-bit lanes 2i, 2i+1 of tag 0x30. */
+void orc_walk_init(int64_t n, float L, uint64_t seed, float* px, float* py)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        px[i] = L * orc_u01(orc_lane32(seed, ORC_TAG_WALK_POS, 2 * (uint64_t)i, 0));
+        py[i] = L * orc_u01(orc_lane32(seed, ORC_TAG_WALK_POS, 2 * (uint64_t)i + 1, 0));
+    }
+}
+
+/* K2/K3: v = (2u - 1) * vmax per component (u from lanes 2i, 2i+1 of tag 0x31
+ * at step t); p' = clip(p + v) into [0, L - ulp] (the largest float below L:
+ * the half-open box of SPEC's bounded space). */
+void orc_walk_step(int64_t n, float L, float vmax, uint64_t seed, uint32_t t, const float* px, const float* py,
+                   float* opx, float* opy)
+{
+    const float hi = nextafterf(L, 0.0f);
+    for (int64_t i = 0; i < n; ++i) {
+        float vx = (2.0f * orc_u01(orc_lane32(seed, ORC_TAG_WALK_VEL, 2 * (uint64_t)i, t)) - 1.0f) * vmax;
+        float vy = (2.0f * orc_u01(orc_lane32(seed, ORC_TAG_WALK_VEL, 2 * (uint64_t)i + 1, t)) - 1.0f) * vmax;
+        float x = px[i] + vx, y = py[i] + vy;
+        if (x < 0.0f) x = 0.0f;
+        if (x > hi) x = hi;
+        if (y < 0.0f) y = 0.0f;
+        if (y > hi) y = hi;
+        opx[i] = x;
+        opy[i] = y;
+    }
+}
+
+/* Runs `steps` steps in place; records the mean displacement from the origin
+ * positions (ox, oy) after each step (SPEC run_walk metric), in double. */
+int orc_walk_run(int64_t n, float L, float vmax, uint64_t seed, uint32_t t0, int64_t steps, float* px, float* py,
+                 const float* ox, const float* oy, double* mean_disp_out)
+{
+    size_t bytes = (size_t)(n > 0 ? n : 1) * sizeof(float);
+    float* tx = (float*)malloc(bytes);
+    float* ty = (float*)malloc(bytes);
+    if (!tx || !ty) { free(tx); free(ty); return ORC_E_OOM; }
+    for (int64_t k = 0; k < steps; ++k) {
+        orc_walk_step(n, L, vmax, seed, t0 + (uint32_t)k, px, py, tx, ty);
+        memcpy(px, tx, (size_t)n * sizeof(float));
+        memcpy(py, ty, (size_t)n * sizeof(float));
+        if (mean_disp_out) {
+            double s = 0.0;
+            for (int64_t i = 0; i < n; ++i) {
+                double dx = (double)px[i] - (double)ox[i], dy = (double)py[i] - (double)oy[i];
+                s += sqrt(dx * dx + dy * dy);
+            }
+            mean_disp_out[k] = n > 0 ? s / (double)n : 0.0;
+        }
+    }
+    free(tx); free(ty);
+    return 0;
+}

@@ -19,7 +19,9 @@ enum {
     ORC_TAG_SIR_INIT = 0x12,
     ORC_TAG_GRAPH = 0x13,
     ORC_TAG_BOIDS_POS = 0x20,
-    ORC_TAG_BOIDS_VEL = 0x21
+    ORC_TAG_BOIDS_VEL = 0x21,
+    ORC_TAG_WALK_POS = 0x30,
+    ORC_TAG_WALK_VEL = 0x31
 };
 
 enum { ORC_S = 0, ORC_I = 1, ORC_R = 2 };
@@ -82,6 +84,12 @@ int orc_boids_run(int64_t n, const orc_boids_params* P, int64_t steps, float* px
 void orc_boids_step_brute_f64(int64_t n, const orc_boids_params* P, const double* px,
                               const double* py, const double* vx, const double* vy, double* opx,
                               double* opy, double* ovx, double* ovy);
+
+void orc_walk_init(int64_t n, float L, uint64_t seed, float* px, float* py);
+void orc_walk_step(int64_t n, float L, float vmax, uint64_t seed, uint32_t t, const float* px, const float* py,
+                   float* opx, float* opy);
+int orc_walk_run(int64_t n, float L, float vmax, uint64_t seed, uint32_t t0, int64_t steps, float* px, float* py,
+                 const float* ox, const float* oy, double* mean_disp_out);
 
 #ifdef __cplusplus
 }
