@@ -316,11 +316,34 @@ def bench_small(args):
     import numpy as np
     import torch
 
-    from paper_2601_16292_b200 import Model, boids_params, sir_params, sweep, wealth_params
+    from paper_2601_16292_b200 import Model, boids_params, sir_params, sweep, walk_params, wealth_params
     from paper_2601_16292_b200 import workloads as W
 
     out = {}
     w = args.workload
+    if w in ("walk", "walk_scale"):
+        c = W.CONFIGS[w]
+        m = Model("walk", c["n"], walk_params(c["L"], c["vmax"]), c["seed"])
+        k = c["steps"]
+        m.step(2)
+        m.synchronize()
+        m.profile(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(m.stream)
+        m.step(k)
+        e1.record(m.stream)
+        m.synchronize()
+        ms = e0.elapsed_time(e1)
+        prof = m.profile_results()
+        avg = prof[0][2] / prof[0][1]
+        hbm, kind = peaks()
+        ach = 24.0 * c["n"] / (avg / 1e3) / 1e9
+        print(json.dumps({"workload": w, "n": c["n"], "steps": k, "ms_per_step": ms / k,
+                          "value": c["n"] * k / (ms / 1e3), "unit": UNIT,
+                          "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                                       "frac": ach / hbm, "alg_bytes_per_agent": 24},
+                          "kernels": prof}))
+        return 0
     if w == "c1":
         c = W.C1_WEALTH_SMALL
         m = Model("wealth", c["n"], wealth_params(), c["seed"])

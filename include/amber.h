@@ -52,7 +52,8 @@ typedef struct amber_model amber_model; /* opaque, library-owned */
 typedef enum {
     AMBER_WEALTH = 0,    /* wealth transfer; column "wealth" (int32)            */
     AMBER_SIR_GRAPH = 1, /* SIR on an Erdos-Renyi CSR graph; column "state" (u8) */
-    AMBER_BOIDS = 2      /* flocking; columns pos_x, pos_y, vel_x, vel_y (f32)  */
+    AMBER_BOIDS = 2,     /* flocking; columns pos_x, pos_y, vel_x, vel_y (f32)  */
+    AMBER_WALK = 3       /* random walk; columns pos_x, pos_y, origin_x, origin_y (f32) */
 } amber_kind;
 
 typedef enum {
@@ -134,6 +135,16 @@ typedef struct {
 typedef struct {
     float L, R, rs, wc, wa, ws, vmax, dt;
 } amber_boids_params;
+
+/* Random Walk (Sec. 5.1.1, Sec. 5.3; DESIGN.md
+ * K1-K3).  Positions uniform in [0, L)^2 (32-bit lanes 2i, 2i+1 of tag 0x30);
+ * step t: v = (2u - 1) * vmax per component from lanes 2i, 2i+1 of tag 0x31,
+ * p' = clip(p + v) into [0, largest float below L] (float32, no FMA).
+ * Metric "mean_displacement" = mean |p - origin| (per step, double sum). */
+typedef struct {
+    float L;    /* box side (> 0) */
+    float vmax; /* max speed per component (>= 0) */
+} amber_walk_params;
 
 /* One replicate of a sweep (Sec. 4.2). */
 typedef struct {

@@ -160,6 +160,7 @@ struct Model {
 Model* make_wealth(int64_t n, const amber_wealth_params& p, uint64_t seed, const amber_runtime* rt);
 Model* make_sir(int64_t n, const amber_sir_params& p, uint64_t seed, const amber_runtime* rt);
 Model* make_boids(int64_t n, const amber_boids_params& p, uint64_t seed, const amber_runtime* rt);
+Model* make_walk(int64_t n, const amber_walk_params& p, uint64_t seed, const amber_runtime* rt);
 void run_sweep(int64_t n, const amber_sir_params& base, const amber_replicate* reps,
                int64_t n_reps, int64_t n_steps, const amber_runtime* rt, double* out,
                amber_sweep_stats* stats);

@@ -17,7 +17,8 @@ from .capi import check
 _NP = {capi.AMBER_I32: np.int32, capi.AMBER_U8: np.uint8, capi.AMBER_F32: np.float32,
        capi.AMBER_I64: np.int64, capi.AMBER_F64: np.float64, capi.AMBER_U64: np.uint64}
 _METRIC_DT = {"total_wealth": np.int64, "active": np.int64, "digest": np.uint64, "S": np.int64,
-              "I": np.int64, "R": np.int64, "mean_speed": np.float64, "polarisation": np.float64}
+              "I": np.int64, "R": np.int64, "mean_speed": np.float64, "polarisation": np.float64,
+              "mean_displacement": np.float64}
 
 
 class TorchAllocator:
@@ -104,7 +105,8 @@ def nccl_unique_id() -> bytes:
 class Model:
     """One agent population on one GPU (or one shard of it when world > 1)."""
 
-    KINDS = {"wealth": capi.AMBER_WEALTH, "sir": capi.AMBER_SIR_GRAPH, "boids": capi.AMBER_BOIDS}
+    KINDS = {"wealth": capi.AMBER_WEALTH, "sir": capi.AMBER_SIR_GRAPH, "boids": capi.AMBER_BOIDS,
+             "walk": capi.AMBER_WALK}
 
     def __init__(self, kind: str, n_agents: int, params, seed: int, *, device=0, stream=None,
                  torch_alloc=True, rank=0, world=1, unique_id=None):
@@ -238,6 +240,10 @@ def sir_params(mean_degree=10.0, beta=0.05, gamma=0.1, init_frac=0.01):
 
 def boids_params(L=1000.0, R=10.0, rs=2.0, wc=0.01, wa=0.125, ws=0.05, vmax=2.0, dt=1.0):
     return capi.amber_boids_params(L, R, rs, wc, wa, ws, vmax, dt)
+
+
+def walk_params(L=100.0, vmax=1.0):
+    return capi.amber_walk_params(L, vmax)
 
 
 def sweep(n_agents, params, betas, seeds, n_steps, *, device=0, stream=None, torch_alloc=True,

@@ -33,8 +33,13 @@ C4_WEALTH_SCALE = dict(kind="wealth", n=100_000_000, w0=1, amount=1, exclude_sel
 C5_SWEEP = dict(kind="sweep", n=10_000, mean_degree=8.0, gamma=0.1, init_frac=0.01, n_beta=64,
                 n_seed=64, beta_lo=0.01, beta_hi=0.2, steps=300)
 
+# NEXT-2: the paper's Random Walk benchmark at the paper's size
+# (N = 10,000, 100 steps; Sec. 5.1.2 l.209) and at N = 1e8 (HBM-bound)
+WALK_PAPER = dict(kind="walk", n=10_000, L=100.0, vmax=1.0, seed=3, steps=100)
+WALK_SCALE = dict(kind="walk", n=100_000_000, L=10_000.0, vmax=1.0, seed=3, steps=100)
+
 CONFIGS = {"c1": C1_WEALTH_SMALL, "c2": C2_SIR, "c3": C3_BOIDS, "c4": C4_WEALTH_SCALE,
-           "c5": C5_SWEEP}
+           "c5": C5_SWEEP, "walk": WALK_PAPER, "walk_scale": WALK_SCALE}
 
 
 def sweep_replicates(cfg=C5_SWEEP):
