@@ -1,2 +1,3 @@
-timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
-python tools/measure_all.py > gpurun_out/all_configs.jsonl 2> gpurun_out/all_configs.err; cat gpurun_out/all_configs.jsonl | cut -c1-300
+timeout 600 python -m pytest tests/test_gpu_walk.py tests/test_capi.py -x -q 2>&1 | tail -3
+python bench.py --workload walk 2>&1 | tail -1
+python bench.py --workload walk_scale 2>&1 | tail -1
