@@ -33,6 +33,7 @@ TAG_BOIDS_POS = 0x20
 TAG_BOIDS_VEL = 0x21
 TAG_WALK_POS = 0x30
 TAG_WALK_VEL = 0x31
+TAG_SIRS_POS, TAG_SIRS_TX, TAG_SIRS_INIT, TAG_SIRS_REC = 0x40, 0x41, 0x42, 0x43
 S, I, R = 0, 1, 2
 
 
@@ -100,6 +101,12 @@ def lib():
             "orc_boids_run": (C.c_int, [C.c_int64, C.POINTER(BoidsParams), C.c_int64] + [f32p] * 4
                               + [f64p, f64p]),
             "orc_boids_step_brute_f64": (None, [C.c_int64, C.POINTER(BoidsParams)] + [f64p] * 8),
+            "orc_sirs_init": (C.c_int, [C.c_int64, C.c_float, C.c_int64, C.c_uint64, f32p, f32p, u8p]),
+            "orc_sirs_contacts": (C.c_int64, [C.c_int64, f32p, f32p, C.c_float, i32p, i32p, C.c_int64]),
+            "orc_sirs_step": (None, [C.c_int64, i32p, i32p, C.c_uint64, C.c_uint32, C.c_uint64,
+                                     C.c_uint64, u8p, u8p]),
+            "orc_sirs_run": (C.c_int, [C.c_int64, i32p, i32p, C.c_uint64, C.c_double, C.c_double,
+                                       C.c_uint32, C.c_int64, u8p, i64p]),
             "orc_walk_init": (None, [C.c_int64, C.c_float, C.c_uint64, f32p, f32p]),
             "orc_walk_step": (None, [C.c_int64, C.c_float, C.c_float, C.c_uint64, C.c_uint32, f32p, f32p,
                                      f32p, f32p]),
@@ -349,3 +356,42 @@ def walk_run(px, py, L, vmax, seed, t0, steps, origin=None):
     _check(lib().orc_walk_run(px.size, L, vmax, seed, t0, steps, _p(px, C.c_float), _p(py, C.c_float),
                               _p(ox, C.c_float), _p(oy, C.c_float), _p(md, C.c_double)))
     return px, py, md[:steps]
+
+
+# ------------------------------------------------- SIR in continuous space (C)
+def sirs_init(n, L, k, seed):
+    px, py = np.zeros(n, np.float32), np.zeros(n, np.float32)
+    st = np.zeros(n, np.uint8)
+    _check(lib().orc_sirs_init(n, L, k, seed, _p(px, C.c_float), _p(py, C.c_float), _p(st, C.c_uint8)))
+    return px, py, st
+
+
+def sirs_contacts(px, py, r, cap=None):
+    px, py = _f32(px), _f32(py)
+    n = px.size
+    cap = cap or max(64 * n, 1)
+    rp = np.zeros(n + 1, np.int32)
+    col = np.zeros(cap, np.int32)
+    a = _check(int(lib().orc_sirs_contacts(n, _p(px, C.c_float), _p(py, C.c_float), r, _p(rp, C.c_int32),
+                                           _p(col, C.c_int32), cap)))
+    return rp, col[:a].copy()
+
+
+def sirs_step(rp, col, st, seed, t, p_inf, p_rec):
+    rp = np.ascontiguousarray(rp, np.int32)
+    col = np.ascontiguousarray(col if len(col) else np.zeros(1, np.int32), np.int32)
+    st = np.ascontiguousarray(st, np.uint8)
+    out = np.empty_like(st)
+    lib().orc_sirs_step(st.size, _p(rp, C.c_int32), _p(col, C.c_int32), seed, t, bernoulli_threshold(p_inf),
+                        bernoulli_threshold(p_rec), _p(st, C.c_uint8), _p(out, C.c_uint8))
+    return out
+
+
+def sirs_run(rp, col, st, seed, p_inf, p_rec, t0, steps):
+    rp = np.ascontiguousarray(rp, np.int32)
+    col = np.ascontiguousarray(col if len(col) else np.zeros(1, np.int32), np.int32)
+    st = np.ascontiguousarray(st, np.uint8).copy()
+    counts = np.zeros((max(steps, 1), 3), np.int64)
+    _check(lib().orc_sirs_run(st.size, _p(rp, C.c_int32), _p(col, C.c_int32), seed, p_inf, p_rec, t0, steps,
+                              _p(st, C.c_uint8), _p(counts, C.c_int64)))
+    return st, counts[:steps]

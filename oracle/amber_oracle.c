@@ -751,3 +751,97 @@ int orc_walk_run(int64_t n, float L, float vmax, uint64_t seed, uint32_t t0, int
     free(tx); free(ty);
     return 0;
 }
+
+/* ======================================================================== */
+/* SIR in continuous space -- the paper's SIR benchmark (PAPER.md Sec.      */
+/* 5.1.1 line 203: "agents in continuous 2D space ... based on contact with */
+/* infected neighbors within a fixed radius"; Listing 2: one  */
+/* draw per susceptible with >= 1 infected neighbour).  Items C1-C4.        */
+/* ======================================================================== */
+
+/* C1: static positions uniform in [0, L)^2 (lanes 2i, 2i+1 of tag 0x40) and
+ * the K agents with the smallest (lane64(0x42, i, 0), i) infected (as S1). */
+int orc_sirs_init(int64_t n, float L, int64_t k, uint64_t seed, float* px, float* py, uint8_t* state)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        px[i] = L * orc_u01(orc_lane32(seed, ORC_TAG_SIRS_POS, 2 * (uint64_t)i, 0));
+        py[i] = L * orc_u01(orc_lane32(seed, ORC_TAG_SIRS_POS, 2 * (uint64_t)i + 1, 0));
+    }
+    if (n < 1 || k < 0 || k > n) return ORC_E_INVALID;
+    key_id* ki = (key_id*)malloc((size_t)n * sizeof(key_id));
+    if (!ki) return ORC_E_OOM;
+    for (int64_t i = 0; i < n; ++i) {
+        ki[i].key = orc_lane64(seed, ORC_TAG_SIRS_INIT, (uint64_t)i, 0);
+        ki[i].id = i;
+    }
+    qsort(ki, (size_t)n, sizeof(key_id), cmp_key_id);
+    for (int64_t i = 0; i < n; ++i) state[i] = ORC_S;
+    for (int64_t j = 0; j < k; ++j) state[ki[j].id] = ORC_I;
+    free(ki);
+    return 0;
+}
+
+/* C2: contact lists by brute force: j != i with dx*dx + dy*dy <= r*r (float,
+ * bounded box, no wrap; boundary inclusive as SPEC neighbors_within), rows
+ * ascending.  Returns the number of arcs (or < 0; ORC_E_INVALID if > cap). */
+int64_t orc_sirs_contacts(int64_t n, const float* px, const float* py, float r, int32_t* row_ptr, int32_t* col,
+                          int64_t cap)
+{
+    const float r2 = r * r;
+    int64_t a = 0;
+    row_ptr[0] = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        for (int64_t j = 0; j < n; ++j) {
+            if (j == i) continue;
+            float dx = px[j] - px[i], dy = py[j] - py[i];
+            if (dx * dx + dy * dy <= r2) {
+                if (a >= cap) return ORC_E_INVALID;
+                col[a++] = (int32_t)j;
+            }
+        }
+        row_ptr[i + 1] = (int32_t)a;
+    }
+    return a;
+}
+
+/* C3: one synchronous step: a susceptible with at least one infected contact
+ * takes ONE draw, lane32(0x41, i, t) < T(p_infect) (Listing 2); an infected
+ * agent recovers iff lane32(0x43, i, t) < T(p_recover); R stays R. */
+void orc_sirs_step(int64_t n, const int32_t* row_ptr, const int32_t* col, uint64_t seed, uint32_t t,
+                   uint64_t t_inf, uint64_t t_rec, const uint8_t* x, uint8_t* x_next)
+{
+    for (int64_t s = 0; s < n; ++s) {
+        if (x[s] == ORC_S) {
+            int exposed = 0;
+            for (int32_t p = row_ptr[s]; p < row_ptr[s + 1]; ++p)
+                if (x[col[p]] == ORC_I) { exposed = 1; break; }
+            int inf = exposed && (uint64_t)orc_lane32(seed, ORC_TAG_SIRS_TX, (uint64_t)s, t) < t_inf;
+            x_next[s] = inf ? ORC_I : ORC_S;
+        } else if (x[s] == ORC_I) {
+            x_next[s] = ((uint64_t)orc_lane32(seed, ORC_TAG_SIRS_REC, (uint64_t)s, t) < t_rec) ? ORC_R : ORC_I;
+        } else {
+            x_next[s] = ORC_R;
+        }
+    }
+}
+
+int orc_sirs_run(int64_t n, const int32_t* row_ptr, const int32_t* col, uint64_t seed, double p_inf,
+                 double p_rec, uint32_t t0, int64_t steps, uint8_t* state, int64_t* counts_out)
+{
+    uint8_t* tmp = (uint8_t*)malloc((size_t)(n > 0 ? n : 1));
+    if (!tmp) return ORC_E_OOM;
+    uint64_t ti = orc_bernoulli_threshold(p_inf), tr = orc_bernoulli_threshold(p_rec);
+    for (int64_t k = 0; k < steps; ++k) {
+        orc_sirs_step(n, row_ptr, col, seed, t0 + (uint32_t)k, ti, tr, state, tmp);
+        memcpy(state, tmp, (size_t)n);
+        if (counts_out) {
+            int64_t cc[3] = {0, 0, 0};
+            for (int64_t i = 0; i < n; ++i) cc[state[i]] += 1;
+            counts_out[3 * k] = cc[0];
+            counts_out[3 * k + 1] = cc[1];
+            counts_out[3 * k + 2] = cc[2];
+        }
+    }
+    free(tmp);
+    return 0;
+}

@@ -21,7 +21,11 @@ enum {
     ORC_TAG_BOIDS_POS = 0x20,
     ORC_TAG_BOIDS_VEL = 0x21,
     ORC_TAG_WALK_POS = 0x30,
-    ORC_TAG_WALK_VEL = 0x31
+    ORC_TAG_WALK_VEL = 0x31,
+    ORC_TAG_SIRS_POS = 0x40,
+    ORC_TAG_SIRS_TX = 0x41,
+    ORC_TAG_SIRS_INIT = 0x42,
+    ORC_TAG_SIRS_REC = 0x43
 };
 
 enum { ORC_S = 0, ORC_I = 1, ORC_R = 2 };
@@ -90,6 +94,14 @@ void orc_walk_step(int64_t n, float L, float vmax, uint64_t seed, uint32_t t, co
                    float* opx, float* opy);
 int orc_walk_run(int64_t n, float L, float vmax, uint64_t seed, uint32_t t0, int64_t steps, float* px, float* py,
                  const float* ox, const float* oy, double* mean_disp_out);
+
+int orc_sirs_init(int64_t n, float L, int64_t k, uint64_t seed, float* px, float* py, uint8_t* state);
+int64_t orc_sirs_contacts(int64_t n, const float* px, const float* py, float r, int32_t* row_ptr, int32_t* col,
+                          int64_t cap);
+void orc_sirs_step(int64_t n, const int32_t* row_ptr, const int32_t* col, uint64_t seed, uint32_t t,
+                   uint64_t t_inf, uint64_t t_rec, const uint8_t* x, uint8_t* x_next);
+int orc_sirs_run(int64_t n, const int32_t* row_ptr, const int32_t* col, uint64_t seed, double p_inf,
+                 double p_rec, uint32_t t0, int64_t steps, uint8_t* state, int64_t* counts_out);
 
 #ifdef __cplusplus
 }
