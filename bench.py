@@ -344,7 +344,13 @@ def bench_small(args):
                                        "frac": ach / hbm, "alg_bytes_per_agent": 24},
                           "kernels": prof}))
         return 0
-    if w == "c1":
+    if w in ("sirs", "sirs_scale"):
+        c = W.CONFIGS[w]
+        from paper_2601_16292_b200 import sir_space_params
+        m = Model("sir_space", c["n"], sir_space_params(c["L"], c["r"], c["p_infect"], c["p_recover"],
+                                                        c["init_frac"]), c["seed"])
+        k = c["steps"]
+    elif w == "c1":
         c = W.C1_WEALTH_SMALL
         m = Model("wealth", c["n"], wealth_params(), c["seed"])
         k = c["steps"]

@@ -53,7 +53,8 @@ typedef enum {
     AMBER_WEALTH = 0,    /* wealth transfer; column "wealth" (int32)            */
     AMBER_SIR_GRAPH = 1, /* SIR on an Erdos-Renyi CSR graph; column "state" (u8) */
     AMBER_BOIDS = 2,     /* flocking; columns pos_x, pos_y, vel_x, vel_y (f32)  */
-    AMBER_WALK = 3       /* random walk; columns pos_x, pos_y, origin_x, origin_y (f32) */
+    AMBER_WALK = 3,      /* random walk; columns pos_x, pos_y, origin_x, origin_y (f32) */
+    AMBER_SIR_SPACE = 4  /* SIR in continuous space; columns state (u8), pos_x, pos_y (f32) */
 } amber_kind;
 
 typedef enum {
@@ -145,6 +146,22 @@ typedef struct {
     float L;    /* box side (> 0) */
     float vmax; /* max speed per component (>= 0) */
 } amber_walk_params;
+
+/* SIR in continuous space -- the paper's SIR benchmark (Sec. 5.1.1
+ * line 203, Listing 2; C1-C4).  Static positions
+ * uniform in [0, L)^2 (lanes 2i, 2i+1 of tag 0x40); contacts: j != i with
+ * dx*dx + dy*dy <= r*r (float, bounded box, inclusive), built once; initial
+ * infected: the round(init_frac*N) smallest lane64(0x42, i) keys.  Step t: a
+ * susceptible with >= 1 infected contact becomes I iff lane32(0x41, i, t) <
+ * ceil(p_infect*2^32) (ONE draw, Listing 2); infected recover iff
+ * lane32(0x43, i, t) < ceil(p_recover*2^32). */
+typedef struct {
+    float L;          /* box side (> 0) */
+    float r;          /* contact radius (> 0) */
+    double p_infect;  /* per exposed susceptible per step, in [0, 1] */
+    double p_recover; /* per infected per step, in [0, 1] */
+    double init_frac; /* fraction initially infected, in [0, 1] */
+} amber_sir_space_params;
 
 /* One replicate of a sweep (Sec. 4.2). */
 typedef struct {

@@ -8,7 +8,7 @@ never imports oracle/ and has no CPU fallback.
 from . import capi
 from .capi import AmberError
 from .model import (Model, boids_params, loopback_id, make_runtime, nccl_unique_id, shard_range, sir_params,
-                    sweep, sweep_range, walk_params, wealth_params)
+                    sweep, sweep_range, sir_space_params, walk_params, wealth_params)
 
 __all__ = ["capi", "AmberError", "Model", "wealth_params", "sir_params", "boids_params", "sweep",
-           "make_runtime", "nccl_unique_id", "shard_range", "sweep_range", "loopback_id", "walk_params"]
+           "make_runtime", "nccl_unique_id", "shard_range", "sweep_range", "loopback_id", "walk_params", "sir_space_params"]

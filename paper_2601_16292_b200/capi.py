@@ -14,7 +14,7 @@ import os
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AMBER_LIB_PATH") or os.path.join(PKG, "libamber.so")
 
-AMBER_WEALTH, AMBER_SIR_GRAPH, AMBER_BOIDS, AMBER_WALK = 0, 1, 2, 3
+AMBER_WEALTH, AMBER_SIR_GRAPH, AMBER_BOIDS, AMBER_WALK, AMBER_SIR_SPACE = 0, 1, 2, 3, 4
 AMBER_I32, AMBER_U8, AMBER_F32, AMBER_I64, AMBER_F64, AMBER_U64 = range(6)
 AMBER_OK = 0
 ERRORS = {-1: "AMBER_E_INVALID_ARG", -2: "AMBER_E_UNKNOWN_KIND", -3: "AMBER_E_UNKNOWN_NAME",
@@ -55,6 +55,11 @@ class amber_boids_params(C.Structure):
 
 class amber_walk_params(C.Structure):
     _fields_ = [("L", C.c_float), ("vmax", C.c_float)]
+
+
+class amber_sir_space_params(C.Structure):
+    _fields_ = [("L", C.c_float), ("r", C.c_float), ("p_infect", C.c_double),
+                ("p_recover", C.c_double), ("init_frac", C.c_double)]
 
 
 class amber_replicate(C.Structure):

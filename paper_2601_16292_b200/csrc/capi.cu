@@ -76,6 +76,11 @@ int amber_model_create(amber_kind kind, int64_t n_agents, const void* params, si
                 AMBER_REQUIRE(params_size >= sizeof(amber_boids_params), "params_size < sizeof(amber_boids_params)");
                 m = amber::make_boids(n_agents, *static_cast<const amber_boids_params*>(params), seed, rt);
                 break;
+            case AMBER_SIR_SPACE:
+                AMBER_REQUIRE(params_size >= sizeof(amber_sir_space_params),
+                              "params_size < sizeof(amber_sir_space_params)");
+                m = amber::make_sir_space(n_agents, *static_cast<const amber_sir_space_params*>(params), seed, rt);
+                break;
             case AMBER_WALK:
                 AMBER_REQUIRE(params_size >= sizeof(amber_walk_params), "params_size < sizeof(amber_walk_params)");
                 m = amber::make_walk(n_agents, *static_cast<const amber_walk_params*>(params), seed, rt);

@@ -21,6 +21,6 @@ void build_graphs(Runtime& rt, const std::vector<unsigned long long>& seeds, int
 
 // S1: initial states (row stride n_pad; padding entries = 3) for every seed.
 void build_init_state(Runtime& rt, const std::vector<unsigned long long>& seeds, int64_t n, int64_t n_pad,
-                      int64_t k_inf, uint8_t* state);
+                      int64_t k_inf, uint8_t* state, uint32_t tag = 0x12u);
 
 }  // namespace amber

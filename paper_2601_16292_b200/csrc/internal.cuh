@@ -161,6 +161,7 @@ Model* make_wealth(int64_t n, const amber_wealth_params& p, uint64_t seed, const
 Model* make_sir(int64_t n, const amber_sir_params& p, uint64_t seed, const amber_runtime* rt);
 Model* make_boids(int64_t n, const amber_boids_params& p, uint64_t seed, const amber_runtime* rt);
 Model* make_walk(int64_t n, const amber_walk_params& p, uint64_t seed, const amber_runtime* rt);
+Model* make_sir_space(int64_t n, const amber_sir_space_params& p, uint64_t seed, const amber_runtime* rt);
 void run_sweep(int64_t n, const amber_sir_params& base, const amber_replicate* reps,
                int64_t n_reps, int64_t n_steps, const amber_runtime* rt, double* out,
                amber_sweep_stats* stats);

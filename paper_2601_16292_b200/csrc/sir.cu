@@ -110,13 +110,13 @@ __global__ void count_valid_kernel(const unsigned long long* arcs, int64_t total
 
 // S1: init keys (64-bit lane of SIR_INIT, step 0) and ids per replicate.
 __global__ void init_keys_kernel(const unsigned long long* seeds, int64_t R, int64_t n, unsigned long long* keys,
-                                 int32_t* ids)
+                                 int32_t* ids, uint32_t tag)
 {
     const int64_t total = R * n;
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = k / n, i = k - r * n;
         const PhiloxKey K = philox_key_dev(seeds[r]);
-        const uint4 w = stream_block(K, TAG_SIR_INIT, static_cast<unsigned long long>(i / 2), 0u);
+        const uint4 w = stream_block(K, tag, static_cast<unsigned long long>(i / 2), 0u);
         keys[k] = lane64_of(w, static_cast<unsigned>(i & 1));
         ids[k] = static_cast<int32_t>(i);
     }
@@ -213,7 +213,7 @@ void build_graphs(Runtime& rt, const std::vector<unsigned long long>& seeds, int
 
 // S1: initial state for R replicates (row stride n_pad, padding = kPad).
 void build_init_state(Runtime& rt, const std::vector<unsigned long long>& seeds, int64_t n, int64_t n_pad,
-                      int64_t k_inf, uint8_t* state)
+                      int64_t k_inf, uint8_t* state, uint32_t tag)
 {
     const int64_t R = static_cast<int64_t>(seeds.size());
     cudaStream_t s = rt.stream;
@@ -227,7 +227,7 @@ void build_init_state(Runtime& rt, const std::vector<unsigned long long>& seeds,
     ids.allocate(&rt, R * n);
     ids2.allocate(&rt, R * n);
     const int grid = rt.num_sms * 8;
-    init_keys_kernel<<<grid, 256, 0, s>>>(d_seeds.p, R, n, keys.p, ids.p);
+    init_keys_kernel<<<grid, 256, 0, s>>>(d_seeds.p, R, n, keys.p, ids.p, tag);
     check_launch("init_keys_kernel");
     std::vector<int> h_off(R + 1);
     for (int64_t r = 0; r <= R; ++r) h_off[r] = static_cast<int>(r * n);

@@ -1,0 +1,402 @@
+// sirs.cu -- SIR in continuous space, the paper's SIR benchmark (PAPER.md
+// Sec. 5.1.1: "agents in continuous 2D space ... transition between
+// Susceptible, Infected, and Recovered states based on contact with infected
+// neighbors within a fixed radius"; Listing 2: one draw per
+// susceptible with >= 1 infected neighbour; C1-C4).
+//
+// Positions are static, so the contact graph is built ONCE at creation:
+// uniform-grid binning (cell side >= r*1.001, bounded box: the stencil is
+// clipped at the walls, not wrapped), a per-agent neighbour count over the
+// 3x3 stencil, an exclusive scan, and a per-agent fill + row sort (the
+// paper's SpatialIndex radius query, done as a grid instead of a KD-tree).
+// Each step is then a pure CSR update in one cooperative launch per call
+// (grid barrier per step): a susceptible checks its contacts for any I and
+// takes ONE Philox draw; infected agents take a recovery draw.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cub/cub.cuh>
+
+#include "graph.cuh"
+#include "internal.cuh"
+#include "philox.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace amber {
+
+namespace {
+
+constexpr uint8_t kS = 0, kI = 1, kR = 2;
+constexpr uint32_t TAG_SIRS_POS = 0x40u, TAG_SIRS_TX = 0x41u, TAG_SIRS_INIT = 0x42u, TAG_SIRS_REC = 0x43u;
+
+struct Grid2 {
+    int nc;
+    float inv_cs;
+};
+
+__device__ __forceinline__ int cc(float x, const Grid2& g)
+{
+    int c = static_cast<int>(__fmul_rn(x, g.inv_cs));
+    return c < 0 ? 0 : (c >= g.nc ? g.nc - 1 : c);
+}
+
+__global__ void sirs_pos_kernel(PhiloxKey key, int64_t n, float L, float* px, float* py)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 w = stream_block(key, TAG_SIRS_POS, static_cast<unsigned long long>(i) >> 1, 0u);
+        px[i] = __fmul_rn(L, u01((i & 1) ? w.z : w.x));
+        py[i] = __fmul_rn(L, u01((i & 1) ? w.w : w.y));
+    }
+}
+
+__global__ void sirs_cell_kernel(const float* px, const float* py, int64_t n, Grid2 g, int* cell, int* cnt)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = cc(py[i], g) * g.nc + cc(px[i], g);
+        cell[i] = c;
+        atomicAdd(cnt + c, 1);
+    }
+}
+
+__global__ void sirs_place_kernel(const float* px, const float* py, int64_t n, const int* cell, int* cursor,
+                                  float2* sp, int32_t* sid)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int q = atomicAdd(cursor + cell[i], 1);
+        sp[q] = make_float2(px[i], py[i]);
+        sid[q] = static_cast<int32_t>(i);
+    }
+}
+
+// C2: for agent i (id order) count (pass 0) or write (pass 1) its contacts.
+template <bool FILL>
+__global__ void sirs_contacts_kernel(const float* px, const float* py, int64_t n, Grid2 g, float r2,
+                                     const int* start, const float2* sp, const int32_t* sid, int* deg,
+                                     const int32_t* row_ptr, int32_t* col)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float xi = px[i], yi = py[i];
+        const int cx = cc(xi, g), cy = cc(yi, g);
+        const int span = g.nc >= 3 ? 1 : 0;
+        int k = 0;
+        const int32_t base = FILL ? row_ptr[i] : 0;
+        for (int dy = -span; dy <= span; ++dy) {
+            const int yy = cy + dy;
+            if (yy < 0 || yy >= g.nc) continue;
+            for (int dx = -span; dx <= span; ++dx) {
+                const int xx = cx + dx;
+                if (xx < 0 || xx >= g.nc) continue;
+                const int c = yy * g.nc + xx;
+                for (int q = start[c]; q < start[c + 1]; ++q) {
+                    const int32_t j = sid[q];
+                    if (j == static_cast<int32_t>(i)) continue;
+                    const float ddx = __fsub_rn(sp[q].x, xi), ddy = __fsub_rn(sp[q].y, yi);
+                    if (__fadd_rn(__fmul_rn(ddx, ddx), __fmul_rn(ddy, ddy)) <= r2) {
+                        if (FILL) col[base + k] = j;
+                        ++k;
+                    }
+                }
+            }
+        }
+        if (!FILL) {
+            deg[i] = k;
+        } else {  // ascending row (insertion sort; rows are ~ rho*pi*r^2 long)
+            for (int a = 1; a < k; ++a) {
+                const int32_t v = col[base + a];
+                int b = a - 1;
+                while (b >= 0 && col[base + b] > v) {
+                    col[base + b + 1] = col[base + b];
+                    --b;
+                }
+                col[base + b + 1] = v;
+            }
+        }
+    }
+}
+
+struct SirsSlot {
+    unsigned long long S, I, R, digest;
+};
+
+struct SirsArgs {
+    PhiloxKey key;
+    const int32_t* row_ptr;
+    const int32_t* col;
+    uint8_t* x[2];
+    int64_t n;
+    unsigned long long t_inf, t_rec;
+    uint32_t t0;
+    int64_t steps;
+    int cur;
+    SirsSlot* ring;
+    int64_t ring_cap;
+    int digest;
+};
+
+__device__ __forceinline__ uint32_t lane32_word(const uint4& w, uint32_t k)
+{
+    return k == 0 ? w.x : (k == 1 ? w.y : (k == 2 ? w.z : w.w));
+}
+
+__global__ void __launch_bounds__(256) sirs_persistent_kernel(const SirsArgs a)
+{
+    cg::grid_group grid = cg::this_grid();
+    int cur = a.cur;
+    for (int64_t k = 0; k < a.steps; ++k) {
+        const uint32_t t = a.t0 + static_cast<uint32_t>(k);
+        const uint8_t* x = a.x[cur];
+        uint8_t* y = a.x[cur ^ 1];
+        unsigned long long cnt[4] = {0, 0, 0, 0};
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+            const uint8_t st = x[i];
+            uint8_t o = st;
+            if (st == kS) {
+                bool exposed = false;
+                for (int32_t p = a.row_ptr[i]; p < a.row_ptr[i + 1] && !exposed; ++p) exposed = x[a.col[p]] == kI;
+                if (exposed) {
+                    const uint4 w = stream_block(a.key, TAG_SIRS_TX, static_cast<unsigned long long>(i) >> 2, t);
+                    if (static_cast<unsigned long long>(lane32_word(w, static_cast<uint32_t>(i & 3))) < a.t_inf) o = kI;
+                }
+            } else if (st == kI) {
+                const uint4 w = stream_block(a.key, TAG_SIRS_REC, static_cast<unsigned long long>(i) >> 2, t);
+                if (static_cast<unsigned long long>(lane32_word(w, static_cast<uint32_t>(i & 3))) < a.t_rec) o = kR;
+            }
+            y[i] = o;
+            cnt[o] += 1;
+            if (a.digest) cnt[3] += digest_term(static_cast<unsigned long long>(i), o);
+        }
+        SirsSlot* sl = a.ring + (t % a.ring_cap);
+        unsigned long long* const outs[4] = {&sl->S, &sl->I, &sl->R, a.digest ? &sl->digest : nullptr};
+        block_sum_atomic<4>(cnt, outs);
+        cur ^= 1;
+        grid.sync();
+    }
+}
+
+__global__ void sirs_zero_slots(SirsSlot* ring, int64_t cap, int64_t s0, int64_t count)
+{
+    for (int64_t k = threadIdx.x; k < count && k < cap; k += blockDim.x) ring[(s0 + k) % cap] = SirsSlot{0, 0, 0, 0};
+}
+
+}  // namespace
+
+class SirSpaceModel final : public Model {
+public:
+    int64_t n = 0, arcs = 0, k_inf = 0;
+    amber_sir_space_params p{};
+    PhiloxKey key{};
+    DevBuf<float> px, py;
+    DevBuf<int32_t> row_ptr, col;
+    DevBuf<uint8_t> x[2];
+    int cur = 0;
+    DevBuf<SirsSlot> ring;
+    int64_t m_first = 0;
+
+    SirSpaceModel(int64_t n_, const amber_sir_space_params& p_, uint64_t seed, const amber_runtime* r)
+    {
+        rt.init(r);
+        n = n_;
+        p = p_;
+        AMBER_REQUIRE(n >= 1 && n < (1ll << 31), "SIR-space needs 1 <= n_agents < 2^31");
+        AMBER_REQUIRE(p.L > 0 && p.r > 0 && p.p_infect >= 0 && p.p_infect <= 1 && p.p_recover >= 0 &&
+                          p.p_recover <= 1 && p.init_frac >= 0 && p.init_frac <= 1,
+                      "SIR-space params out of range");
+        key = philox_key(seed);
+        k_inf = static_cast<int64_t>(std::floor(p.init_frac * static_cast<double>(n) + 0.5));
+        cudaStream_t s = rt.stream;
+        const int gsz = rt.num_sms * 8;
+        px.allocate(&rt, n);
+        py.allocate(&rt, n);
+        sirs_pos_kernel<<<gsz, 256, 0, s>>>(key, n, p.L, px.p, py.p);
+        check_launch("sirs_pos_kernel");
+        for (auto& b : x) b.allocate(&rt, n + 16);
+        std::vector<unsigned long long> seeds{seed};
+        build_init_state(rt, seeds, n, n, k_inf, x[0].p, TAG_SIRS_INIT);
+        // contact graph, once
+        Grid2 g{};
+        double ncd = std::floor(static_cast<double>(p.L) / (static_cast<double>(p.r) * 1.001));
+        ncd = std::min(ncd, 4096.0);
+        g.nc = static_cast<int>(ncd >= 3 ? ncd : 1);
+        g.inv_cs = static_cast<float>(g.nc / static_cast<double>(p.L));
+        const int ncell = g.nc * g.nc;
+        DevBuf<int> cell, cnt, start, cursor, deg;
+        DevBuf<float2> sp;
+        DevBuf<int32_t> sid;
+        cell.allocate(&rt, n);
+        cnt.allocate(&rt, ncell + 1);
+        cnt.zero_async(s);
+        start.allocate(&rt, ncell + 1);
+        cursor.allocate(&rt, ncell + 1);
+        sp.allocate(&rt, n);
+        sid.allocate(&rt, n);
+        deg.allocate(&rt, n + 1);
+        deg.zero_async(s);
+        sirs_cell_kernel<<<gsz, 256, 0, s>>>(px.p, py.p, n, g, cell.p, cnt.p);
+        check_launch("sirs_cell_kernel");
+        scan(cnt.p, start.p, ncell + 1);
+        AMBER_CUDA(cudaMemcpyAsync(cursor.p, start.p, (ncell + 1) * sizeof(int), cudaMemcpyDeviceToDevice, s));
+        sirs_place_kernel<<<gsz, 256, 0, s>>>(px.p, py.p, n, cell.p, cursor.p, sp.p, sid.p);
+        check_launch("sirs_place_kernel");
+        const float r2 = p.r * p.r;
+        sirs_contacts_kernel<false><<<gsz, 256, 0, s>>>(px.p, py.p, n, g, r2, start.p, sp.p, sid.p, deg.p, nullptr,
+                                                        nullptr);
+        check_launch("sirs_contacts_kernel<count>");
+        row_ptr.allocate(&rt, n + 1);
+        scan(deg.p, row_ptr.p, n + 1);
+        int32_t total = 0;
+        AMBER_CUDA(cudaMemcpyAsync(&total, row_ptr.p + n, 4, cudaMemcpyDeviceToHost, s));
+        AMBER_CUDA(cudaStreamSynchronize(s));
+        arcs = total;
+        col.allocate(&rt, std::max<int64_t>(arcs, 1));
+        sirs_contacts_kernel<true><<<gsz, 256, 0, s>>>(px.p, py.p, n, g, r2, start.p, sp.p, sid.p, nullptr,
+                                                       row_ptr.p, col.p);
+        check_launch("sirs_contacts_kernel<fill>");
+        ring.allocate(&rt, metrics_cap);
+        ring.zero_async(s);
+        AMBER_CUDA(cudaStreamSynchronize(s));
+    }
+
+    void scan(const int* in, int* out, int64_t count)
+    {
+        size_t tmp = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, count, rt.stream);
+        DevBuf<char> t;
+        t.allocate(&rt, tmp + 16);
+        AMBER_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, count, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    }
+
+    ~SirSpaceModel() override
+    {
+        if (rt.stream) cudaStreamSynchronize(rt.stream);
+        px.reset(); py.reset(); row_ptr.reset(); col.reset();
+        for (auto& b : x) b.reset();
+        ring.reset();
+        rt.destroy();
+    }
+
+    void step(int64_t nsteps) override
+    {
+        AMBER_REQUIRE(nsteps >= 0 && t + nsteps < (1ll << 32), "bad n_steps");
+        int64_t done = 0;
+        while (done < nsteps) {
+            const int64_t chunk = std::min<int64_t>(nsteps - done, metrics_cap);
+            sirs_zero_slots<<<1, 256, 0, rt.stream>>>(ring.p, metrics_cap, t, chunk);
+            check_launch("sirs_zero_slots");
+            int per_sm = 0;
+            AMBER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sirs_persistent_kernel, 256, 0));
+            int blocks = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(std::min(per_sm, 3)) * rt.num_sms,
+                                                            std::max<int64_t>(1, ceil_div(n, 256))));
+            if (grid) blocks = static_cast<int>(std::min<int64_t>(grid, static_cast<int64_t>(per_sm) * rt.num_sms));
+            SirsArgs a{key, row_ptr.p, col.p, {x[0].p, x[1].p}, n, bernoulli_threshold_host(p.p_infect),
+                       bernoulli_threshold_host(p.p_recover), static_cast<uint32_t>(t), chunk, cur, ring.p,
+                       metrics_cap, digest_on ? 1 : 0};
+            void* kargs[] = {&a};
+            prof.launch(rt.stream, "sirs_persistent", [&] {
+                AMBER_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sirs_persistent_kernel), blocks, 256,
+                                                       kargs, 0, rt.stream));
+            });
+            check_launch("sirs_persistent_kernel");
+            t += chunk;
+            if (chunk & 1) cur ^= 1;
+            done += chunk;
+        }
+    }
+
+    bool column_info(const char* name, amber_dtype* dt, int64_t* glen, int64_t* off, int64_t* len) override
+    {
+        std::string k(name);
+        amber_dtype d;
+        int64_t L;
+        if (k == "state") { d = AMBER_U8; L = n; }
+        else if (k == "pos_x" || k == "pos_y") { d = AMBER_F32; L = n; }
+        else if (k == "row_ptr") { d = AMBER_I32; L = n + 1; }
+        else if (k == "col_idx") { d = AMBER_I32; L = arcs; }
+        else return false;
+        if (dt) *dt = d;
+        if (glen) *glen = L;
+        if (off) *off = 0;
+        if (len) *len = L;
+        return true;
+    }
+
+    void read_column(const char* name, void* dst, size_t bytes, bool on_dev) override
+    {
+        std::string k(name);
+        const void* src;
+        size_t nb;
+        if (k == "state") { src = x[cur].p; nb = n; }
+        else if (k == "pos_x") { src = px.p; nb = n * 4; }
+        else if (k == "pos_y") { src = py.p; nb = n * 4; }
+        else if (k == "row_ptr") { src = row_ptr.p; nb = (n + 1) * 4; }
+        else if (k == "col_idx") { src = col.p; nb = arcs * 4; }
+        else fail(AMBER_E_UNKNOWN_NAME, "no column " + k);
+        if (bytes < nb) fail(AMBER_E_BUFFER_TOO_SMALL, "dst too small for column " + k);
+        copy_out(rt, dst, src, nb, on_dev);
+    }
+
+    void write_column(const char* name, const void* src, size_t bytes, bool on_dev) override
+    {
+        std::string k(name);
+        if (k != "state") fail(AMBER_E_INVALID_ARG, "only the state column is writable (positions are static)");
+        if (bytes < static_cast<size_t>(n)) fail(AMBER_E_BUFFER_TOO_SMALL, "src smaller than state column");
+        copy_in(rt, x[cur].p, src, n, on_dev);
+    }
+
+    void read_metrics(const char* name, void* dst, size_t bytes, int64_t* n_out) override
+    {
+        std::string k(name);
+        size_t off;
+        if (k == "S") off = offsetof(SirsSlot, S);
+        else if (k == "I") off = offsetof(SirsSlot, I);
+        else if (k == "R") off = offsetof(SirsSlot, R);
+        else if (k == "digest" && digest_on) off = offsetof(SirsSlot, digest);
+        else fail(AMBER_E_UNKNOWN_NAME, "no metric " + k);
+        std::vector<SirsSlot> h(metrics_cap);
+        AMBER_CUDA(cudaMemcpyAsync(h.data(), ring.p, metrics_cap * sizeof(SirsSlot), cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        const int64_t first = std::max(m_first, t - metrics_cap);
+        const int64_t cnt = std::max<int64_t>(t - first, 0);
+        if (bytes < static_cast<size_t>(cnt) * 8) fail(AMBER_E_BUFFER_TOO_SMALL, "metrics dst too small");
+        for (int64_t s = first; s < t; ++s)
+            std::memcpy(static_cast<char*>(dst) + (s - first) * 8, reinterpret_cast<const char*>(&h[s % metrics_cap]) + off, 8);
+        if (n_out) *n_out = cnt;
+    }
+
+    void reset_metrics() override
+    {
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        m_first = t;
+    }
+
+    uint64_t digest(const char* name) override
+    {
+        if (std::string(name) != "state") fail(AMBER_E_UNKNOWN_NAME, std::string("no column ") + name);
+        return device_digest_u8(rt, x[cur].p, n, 0);
+    }
+
+    void set_step(int64_t s) override
+    {
+        AMBER_REQUIRE(s >= 0 && s < (1ll << 32), "step out of range");
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        t = s;
+        m_first = s;
+    }
+
+    bool get_option(const char* key_, int64_t* v) override
+    {
+        if (std::string(key_) == "edges") {
+            *v = arcs / 2;
+            return true;
+        }
+        return Model::get_option(key_, v);
+    }
+};
+
+Model* make_sir_space(int64_t n, const amber_sir_space_params& p, uint64_t seed, const amber_runtime* rt)
+{
+    return new SirSpaceModel(n, p, seed, rt);
+}
+
+}  // namespace amber

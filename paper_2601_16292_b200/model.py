@@ -106,7 +106,7 @@ class Model:
     """One agent population on one GPU (or one shard of it when world > 1)."""
 
     KINDS = {"wealth": capi.AMBER_WEALTH, "sir": capi.AMBER_SIR_GRAPH, "boids": capi.AMBER_BOIDS,
-             "walk": capi.AMBER_WALK}
+             "walk": capi.AMBER_WALK, "sir_space": capi.AMBER_SIR_SPACE}
 
     def __init__(self, kind: str, n_agents: int, params, seed: int, *, device=0, stream=None,
                  torch_alloc=True, rank=0, world=1, unique_id=None):
@@ -240,6 +240,10 @@ def sir_params(mean_degree=10.0, beta=0.05, gamma=0.1, init_frac=0.01):
 
 def boids_params(L=1000.0, R=10.0, rs=2.0, wc=0.01, wa=0.125, ws=0.05, vmax=2.0, dt=1.0):
     return capi.amber_boids_params(L, R, rs, wc, wa, ws, vmax, dt)
+
+
+def sir_space_params(L=100.0, r=2.0, p_infect=0.1, p_recover=0.05, init_frac=0.01):
+    return capi.amber_sir_space_params(L, r, p_infect, p_recover, init_frac)
 
 
 def walk_params(L=100.0, vmax=1.0):

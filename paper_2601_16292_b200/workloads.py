@@ -38,8 +38,17 @@ C5_SWEEP = dict(kind="sweep", n=10_000, mean_degree=8.0, gamma=0.1, init_frac=0.
 WALK_PAPER = dict(kind="walk", n=10_000, L=100.0, vmax=1.0, seed=3, steps=100)
 WALK_SCALE = dict(kind="walk", n=100_000_000, L=10_000.0, vmax=1.0, seed=3, steps=100)
 
+# NEXT-1: the paper's SIR benchmark in continuous space at the paper's
+# size (N = 10,000, 100 steps) with SPEC's parameters (L = 100, r = 2,
+# p_infect 0.1, p_recover 0.05, 1% infected), and at N = 1e7 with the same density
+SIRS_PAPER = dict(kind="sir_space", n=10_000, L=100.0, r=2.0, p_infect=0.1, p_recover=0.05,
+                  init_frac=0.01, seed=7, steps=100)
+SIRS_SCALE = dict(kind="sir_space", n=10_000_000, L=3162.2776, r=2.0, p_infect=0.1, p_recover=0.05,
+                  init_frac=0.01, seed=7, steps=100)
+
 CONFIGS = {"c1": C1_WEALTH_SMALL, "c2": C2_SIR, "c3": C3_BOIDS, "c4": C4_WEALTH_SCALE,
-           "c5": C5_SWEEP, "walk": WALK_PAPER, "walk_scale": WALK_SCALE}
+           "c5": C5_SWEEP, "walk": WALK_PAPER, "walk_scale": WALK_SCALE,
+           "sirs": SIRS_PAPER, "sirs_scale": SIRS_SCALE}
 
 
 def sweep_replicates(cfg=C5_SWEEP):
