@@ -305,6 +305,92 @@ int amber_sweep_range(int64_t n_reps, int world, int rank, int64_t* r0, int64_t*
  * Errors: NCCL (libnccl.so.2 not loadable: set AMBER_NCCL_LIB to its path). */
 int amber_nccl_unique_id(void* out, size_t out_bytes);
 
+/* ------------------------------------------------- generic Population (NEXT-4) */
+/* The paper's general columnar API (Sec. 3.1.2 lines 85-96 and
+ * Listing 1 "population.data.with_columns((pl.col('wealth') + 10))", Sec. 3.3
+ * line 155 "columnar updates for all or filtered agents ... BatchUpdateContext
+ * ... applying all changes atomically", Sec. 6.2 line 284 dynamic populations)
+ * on the device: typed columns (one row per agent), an alive mask, stable
+ * agent ids (never reused), population-wide updates and aggregates given as
+ * postfix expression programs evaluated per row by one kernel. */
+typedef struct amber_population amber_population; /* opaque, library-owned */
+
+typedef struct {
+    const char* name;  /* column name (copied) */
+    amber_dtype dtype; /* AMBER_I32, AMBER_I64, AMBER_F32, AMBER_F64 or AMBER_U8 */
+} amber_column_spec;
+
+/* Expression instruction (postfix / stack machine, evaluated in double per
+ * row; results are stored with C conversion semantics: truncation toward zero
+ * for integer columns).  arg = column index for AMBER_OP_COL, tag for
+ * AMBER_OP_RAND; value = the constant for AMBER_OP_CONST. */
+typedef enum {
+    AMBER_OP_CONST = 0, AMBER_OP_COL = 1, AMBER_OP_ID = 2, AMBER_OP_STEP = 3,
+    AMBER_OP_ADD = 10, AMBER_OP_SUB, AMBER_OP_MUL, AMBER_OP_DIV, AMBER_OP_MIN, AMBER_OP_MAX,
+    AMBER_OP_NEG = 20, AMBER_OP_ABS, AMBER_OP_FLOOR, AMBER_OP_SQRT,
+    AMBER_OP_LT = 30, AMBER_OP_LE, AMBER_OP_GT, AMBER_OP_GE, AMBER_OP_EQ, AMBER_OP_NE,
+    AMBER_OP_AND = 40, AMBER_OP_OR, AMBER_OP_NOT,
+    AMBER_OP_SELECT = 50, /* c a b -> c != 0 ? a : b */
+    AMBER_OP_RAND = 60    /* uniform [0,1): (lane32(tag=arg, agent id, step) >> 8) * 2^-24 */
+} amber_op;
+
+typedef struct {
+    int32_t op;
+    int32_t arg;
+    double value;
+} amber_instr;
+
+typedef enum { AMBER_AGG_SUM = 0, AMBER_AGG_MEAN = 1, AMBER_AGG_MIN = 2, AMBER_AGG_MAX = 3, AMBER_AGG_COUNT = 4 } amber_agg;
+
+/* Create an empty population (0 agents) with n_cols typed columns and room for
+ * `capacity` rows (grows on demand).  seed keys AMBER_OP_RAND draws.
+ * Errors: INVALID_ARG (duplicate/empty names, bad dtype, n_cols < 1). */
+int amber_population_create(const amber_column_spec* cols, int n_cols, int64_t capacity, uint64_t seed,
+                            const amber_runtime* rt, amber_population** out);
+int amber_population_destroy(amber_population* p);
+
+/* Append n live agents; their ids are next_id .. next_id+n-1 (*first_id).
+ * defaults: n_cols host doubles (initial value per column) or NULL (zeros). */
+int amber_population_add_agents(amber_population* p, int64_t n, const double* defaults, int64_t* first_id);
+
+/* Mark agents dead (host id list).  Errors: INVALID_ARG (unknown or dead id;
+ * then nothing is removed). */
+int amber_population_remove_agents(amber_population* p, const int64_t* ids, int64_t n);
+
+/* Drop dead rows, keeping row order (stream compaction on the device). */
+int amber_population_compact(amber_population* p);
+
+/* *live = live agents, *rows = rows in use (live + dead before compaction). */
+int amber_population_size(amber_population* p, int64_t* live, int64_t* rows);
+
+/* Synchronous population-wide update: for every live row where `where`
+ * evaluates != 0 (n_where == 0: every live row), target = expr(row), all rows
+ * reading the pre-update snapshot (SPEC update_column / update_where).
+ * *n_updated (may be NULL) = rows updated.  Errors: UNKNOWN_NAME, INVALID_ARG
+ * (bad program: stack underflow/overflow, unknown op, column index). */
+int amber_population_update(amber_population* p, const char* target, const amber_instr* expr, int n_expr,
+                            const amber_instr* where, int n_where, int64_t* n_updated);
+
+/* Reduce expr over live rows where `where` holds (double result on the host;
+ * COUNT counts the rows, SUM of an empty set is 0).  Errors: INVALID_ARG for
+ * MEAN/MIN/MAX of an empty set (SPEC aggregate). */
+int amber_population_aggregate(amber_population* p, int agg, const amber_instr* expr, int n_expr,
+                               const amber_instr* where, int n_where, double* out);
+
+/* Column of the LIVE agents in row order (host or device dst); "id" (I64) is
+ * the implicit agent-id column.  Errors: UNKNOWN_NAME, BUFFER_TOO_SMALL. */
+int amber_population_read_column(amber_population* p, const char* name, void* dst, size_t dst_bytes,
+                                 int dst_on_device);
+
+/* Atomic batch of individual writes (BatchUpdateContext): values[k] goes to
+ * column `name` of agent ids[k] (host arrays).  Every id is validated first;
+ * on any error nothing is written.  Duplicate ids: the last write wins. */
+int amber_population_batch_set(amber_population* p, const char* name, const int64_t* ids,
+                               const double* values, int64_t n);
+
+/* Step counter read by AMBER_OP_STEP / AMBER_OP_RAND (advance it per model step). */
+int amber_population_set_step(amber_population* p, int64_t step);
+
 /* Write a 128-byte id for an in-process LOOPBACK group (testing/emulation):
  * `world` models created with this id (rank 0..world-1) on one device form a
  * sharded model whose exchanges are host barriers + device-to-device copies

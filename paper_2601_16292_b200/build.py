@@ -38,7 +38,7 @@ def _flags(src: str) -> list[str]:
     f = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", nccl_include(),
          "--expt-relaxed-constexpr"] + ARCH + EXTRA
-    if os.path.basename(src) == "boids.cu":
+    if os.path.basename(src) in ("boids.cu", "population.cu"):
         f += ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"]
     return f
 

@@ -27,7 +27,11 @@ SYMBOLS = ["amber_version", "amber_last_error", "amber_model_create", "amber_mod
            "amber_column_info", "amber_read_column", "amber_write_column", "amber_read_metrics",
            "amber_reset_metrics", "amber_digest", "amber_set_option", "amber_get_option",
            "amber_profile_enable", "amber_profile_query", "amber_sweep", "amber_shard_range",
-           "amber_sweep_range", "amber_nccl_unique_id", "amber_loopback_id"]
+           "amber_sweep_range", "amber_nccl_unique_id", "amber_loopback_id",
+           "amber_population_create", "amber_population_destroy", "amber_population_add_agents",
+           "amber_population_remove_agents", "amber_population_compact", "amber_population_size",
+           "amber_population_update", "amber_population_aggregate", "amber_population_read_column",
+           "amber_population_batch_set", "amber_population_set_step"]
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -69,6 +73,14 @@ class amber_replicate(C.Structure):
 class amber_sweep_stats(C.Structure):
     _fields_ = [("build_ms", C.c_double), ("step_ms", C.c_double),
                 ("agent_updates", C.c_int64), ("active_updates", C.c_int64)]
+
+
+class amber_column_spec(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("dtype", C.c_int)]
+
+
+class amber_instr(C.Structure):
+    _fields_ = [("op", C.c_int32), ("arg", C.c_int32), ("value", C.c_double)]
 
 
 class AmberError(RuntimeError):
@@ -128,6 +140,20 @@ def load():
         "amber_sweep_range": (C.c_int, [C.c_int64, C.c_int, C.c_int, i64p, i64p]),
         "amber_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_size_t]),
         "amber_loopback_id": (C.c_int, [C.c_void_p, C.c_size_t]),
+        "amber_population_create": (C.c_int, [P(amber_column_spec), C.c_int, C.c_int64, C.c_uint64,
+                                              P(amber_runtime), P(C.c_void_p)]),
+        "amber_population_destroy": (C.c_int, [C.c_void_p]),
+        "amber_population_add_agents": (C.c_int, [C.c_void_p, C.c_int64, P(C.c_double), i64p]),
+        "amber_population_remove_agents": (C.c_int, [C.c_void_p, i64p, C.c_int64]),
+        "amber_population_compact": (C.c_int, [C.c_void_p]),
+        "amber_population_size": (C.c_int, [C.c_void_p, i64p, i64p]),
+        "amber_population_update": (C.c_int, [C.c_void_p, C.c_char_p, P(amber_instr), C.c_int,
+                                              P(amber_instr), C.c_int, i64p]),
+        "amber_population_aggregate": (C.c_int, [C.c_void_p, C.c_int, P(amber_instr), C.c_int,
+                                                 P(amber_instr), C.c_int, P(C.c_double)]),
+        "amber_population_read_column": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t, C.c_int]),
+        "amber_population_batch_set": (C.c_int, [C.c_void_p, C.c_char_p, i64p, P(C.c_double), C.c_int64]),
+        "amber_population_set_step": (C.c_int, [C.c_void_p, C.c_int64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

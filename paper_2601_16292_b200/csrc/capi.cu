@@ -281,6 +281,119 @@ int amber_sweep_range(int64_t n_reps, int world, int rank, int64_t* r0, int64_t*
     });
 }
 
+static amber::Population* pimpl(amber_population* p)
+{
+    if (!p || !p->impl) amber::fail(AMBER_E_INVALID_ARG, "NULL population");
+    return p->impl;
+}
+
+int amber_population_create(const amber_column_spec* cols, int n_cols, int64_t capacity, uint64_t seed,
+                            const amber_runtime* rt, amber_population** out)
+{
+    return guarded([&] {
+        need(out, "out");
+        *out = nullptr;
+        need(cols, "cols");
+        *out = new amber_population{amber::make_population(cols, n_cols, capacity, seed, rt)};
+        return 0;
+    });
+}
+
+int amber_population_destroy(amber_population* p)
+{
+    return guarded([&] {
+        if (!p) return 0;
+        amber::destroy_population(p->impl);
+        delete p;
+        return 0;
+    });
+}
+
+int amber_population_add_agents(amber_population* p, int64_t n, const double* defaults, int64_t* first_id)
+{
+    return guarded([&] {
+        const int64_t f = amber::population_add(pimpl(p), n, defaults);
+        if (first_id) *first_id = f;
+        return 0;
+    });
+}
+
+int amber_population_remove_agents(amber_population* p, const int64_t* ids, int64_t n)
+{
+    return guarded([&] {
+        AMBER_REQUIRE(n >= 0 && (n == 0 || ids), "bad id list");
+        amber::population_remove(pimpl(p), ids, n);
+        return 0;
+    });
+}
+
+int amber_population_compact(amber_population* p)
+{
+    return guarded([&] {
+        amber::population_compact(pimpl(p));
+        return 0;
+    });
+}
+
+int amber_population_size(amber_population* p, int64_t* live, int64_t* rows)
+{
+    return guarded([&] {
+        amber::population_size(pimpl(p), live, rows);
+        return 0;
+    });
+}
+
+int amber_population_update(amber_population* p, const char* target, const amber_instr* expr, int n_expr,
+                            const amber_instr* where, int n_where, int64_t* n_updated)
+{
+    return guarded([&] {
+        need(target, "target");
+        const int64_t k = amber::population_update(pimpl(p), target, expr, n_expr, where, n_where);
+        if (n_updated) *n_updated = k;
+        return 0;
+    });
+}
+
+int amber_population_aggregate(amber_population* p, int agg, const amber_instr* expr, int n_expr,
+                               const amber_instr* where, int n_where, double* out)
+{
+    return guarded([&] {
+        need(out, "out");
+        *out = amber::population_aggregate(pimpl(p), agg, expr, n_expr, where, n_where);
+        return 0;
+    });
+}
+
+int amber_population_read_column(amber_population* p, const char* name, void* dst, size_t dst_bytes,
+                                 int dst_on_device)
+{
+    return guarded([&] {
+        need(name, "name");
+        need(dst, "dst");
+        amber::population_read(pimpl(p), name, dst, dst_bytes, dst_on_device != 0);
+        return 0;
+    });
+}
+
+int amber_population_batch_set(amber_population* p, const char* name, const int64_t* ids, const double* values,
+                               int64_t n)
+{
+    return guarded([&] {
+        need(name, "name");
+        AMBER_REQUIRE(n >= 0 && (n == 0 || (ids && values)), "bad batch");
+        amber::population_batch_set(pimpl(p), name, ids, values, n);
+        return 0;
+    });
+}
+
+int amber_population_set_step(amber_population* p, int64_t step)
+{
+    return guarded([&] {
+        amber::population_set_step(pimpl(p), step);
+        return 0;
+    });
+}
+
 int amber_loopback_id(void* out, size_t out_bytes)
 {
     return guarded([&] { return amber_loopback_id_impl(out, out_bytes); });

@@ -166,6 +166,20 @@ void run_sweep(int64_t n, const amber_sir_params& base, const amber_replicate* r
                int64_t n_reps, int64_t n_steps, const amber_runtime* rt, double* out,
                amber_sweep_stats* stats);
 
+// Generic Population (population.cu).
+struct Population;
+Population* make_population(const amber_column_spec* cols, int n, int64_t cap, uint64_t seed, const amber_runtime* rt);
+void destroy_population(Population* p);
+int64_t population_add(Population* p, int64_t n, const double* defaults);
+void population_remove(Population* p, const int64_t* ids, int64_t n);
+void population_compact(Population* p);
+void population_size(Population* p, int64_t* live, int64_t* rows);
+int64_t population_update(Population* p, const char* target, const amber_instr* e, int ne, const amber_instr* w, int nw);
+double population_aggregate(Population* p, int agg, const amber_instr* e, int ne, const amber_instr* w, int nw);
+void population_read(Population* p, const char* name, void* dst, size_t bytes, bool on_dev);
+void population_batch_set(Population* p, const char* name, const int64_t* ids, const double* vals, int64_t n);
+void population_set_step(Population* p, int64_t s);
+
 // Copy helper for column I/O (host or device endpoint), on the model stream.
 void copy_out(Runtime& rt, void* dst, const void* src, size_t bytes, bool dst_on_dev);
 void copy_in(Runtime& rt, void* dst, const void* src, size_t bytes, bool src_on_dev);
@@ -254,4 +268,8 @@ inline void sweep_range(int64_t n_reps, int world, int rank, int64_t* r0, int64_
 
 struct amber_model {
     amber::Model* impl;
+};
+
+struct amber_population {
+    amber::Population* impl;
 };

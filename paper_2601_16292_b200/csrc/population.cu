@@ -1,0 +1,594 @@
+// population.cu -- generic device Population: the paper's
+// columnar API (Sec. 3.1.2 lines 85-96, Listing 1; Sec. 3.3;
+// Sec. 6.2) with SPEC's semantics (columnar-core module): typed
+// columns, tombstone alive mask, stable never-reused ids (rows stay sorted by
+// id, so id -> row is a binary search), order-preserving compaction, and
+// population-wide updates / aggregates given as postfix expression programs
+// that one kernel evaluates per row (a tiny vectorised expression engine:
+// Listing 1's `wealth + 10` is [COL wealth][CONST 10][ADD]).
+#include <algorithm>
+#include <cmath>
+#include <cub/cub.cuh>
+#include <map>
+
+#include "internal.cuh"
+#include "philox.cuh"
+
+namespace amber {
+
+namespace {
+
+constexpr int kMaxProg = 64, kMaxStack = 16, kMaxCols = 32;
+
+struct Prog {
+    int n;
+    amber_instr ins[kMaxProg];
+};
+
+struct ColView {
+    void* p;
+    int dtype;
+};
+
+struct Cols {
+    ColView c[kMaxCols];
+    int n;
+};
+
+__device__ __forceinline__ double load_col(const ColView& c, int64_t row)
+{
+    switch (c.dtype) {
+        case AMBER_I32: return static_cast<double>(static_cast<const int32_t*>(c.p)[row]);
+        case AMBER_I64: return static_cast<double>(static_cast<const int64_t*>(c.p)[row]);
+        case AMBER_F32: return static_cast<double>(static_cast<const float*>(c.p)[row]);
+        case AMBER_F64: return static_cast<const double*>(c.p)[row];
+        default: return static_cast<double>(static_cast<const uint8_t*>(c.p)[row]);
+    }
+}
+
+__device__ __forceinline__ void store_col(const ColView& c, int64_t row, double v)
+{
+    switch (c.dtype) {
+        case AMBER_I32: static_cast<int32_t*>(c.p)[row] = static_cast<int32_t>(v); break;
+        case AMBER_I64: static_cast<int64_t*>(c.p)[row] = static_cast<int64_t>(v); break;
+        case AMBER_F32: static_cast<float*>(c.p)[row] = static_cast<float>(v); break;
+        case AMBER_F64: static_cast<double*>(c.p)[row] = v; break;
+        default: static_cast<uint8_t*>(c.p)[row] = static_cast<uint8_t>(v); break;
+    }
+}
+
+__device__ double eval(const Prog& P, const Cols& C, int64_t row, int64_t id, uint32_t step, const PhiloxKey& key)
+{
+    double st[kMaxStack];
+    int sp = 0;
+    for (int k = 0; k < P.n; ++k) {
+        const amber_instr in = P.ins[k];
+        switch (in.op) {
+            case AMBER_OP_CONST: st[sp++] = in.value; break;
+            case AMBER_OP_COL: st[sp++] = load_col(C.c[in.arg], row); break;
+            case AMBER_OP_ID: st[sp++] = static_cast<double>(id); break;
+            case AMBER_OP_STEP: st[sp++] = static_cast<double>(step); break;
+            case AMBER_OP_RAND: {
+                const uint4 w = stream_block(key, static_cast<uint32_t>(in.arg), static_cast<unsigned long long>(id) >> 2,
+                                             step);
+                const uint32_t q = static_cast<uint32_t>(id & 3);
+                st[sp++] = static_cast<double>(u01(q == 0 ? w.x : (q == 1 ? w.y : (q == 2 ? w.z : w.w))));
+                break;
+            }
+            case AMBER_OP_NEG: st[sp - 1] = -st[sp - 1]; break;
+            case AMBER_OP_ABS: st[sp - 1] = fabs(st[sp - 1]); break;
+            case AMBER_OP_FLOOR: st[sp - 1] = floor(st[sp - 1]); break;
+            case AMBER_OP_SQRT: st[sp - 1] = sqrt(st[sp - 1]); break;
+            case AMBER_OP_NOT: st[sp - 1] = st[sp - 1] == 0.0 ? 1.0 : 0.0; break;
+            case AMBER_OP_SELECT: {
+                const double b = st[--sp], a = st[--sp], c = st[--sp];
+                st[sp++] = c != 0.0 ? a : b;
+                break;
+            }
+            default: {
+                const double b = st[--sp], a = st[--sp];
+                double r = 0.0;
+                switch (in.op) {
+                    case AMBER_OP_ADD: r = a + b; break;
+                    case AMBER_OP_SUB: r = a - b; break;
+                    case AMBER_OP_MUL: r = a * b; break;
+                    case AMBER_OP_DIV: r = a / b; break;
+                    case AMBER_OP_MIN: r = fmin(a, b); break;
+                    case AMBER_OP_MAX: r = fmax(a, b); break;
+                    case AMBER_OP_LT: r = a < b; break;
+                    case AMBER_OP_LE: r = a <= b; break;
+                    case AMBER_OP_GT: r = a > b; break;
+                    case AMBER_OP_GE: r = a >= b; break;
+                    case AMBER_OP_EQ: r = a == b; break;
+                    case AMBER_OP_NE: r = a != b; break;
+                    case AMBER_OP_AND: r = (a != 0.0) && (b != 0.0); break;
+                    case AMBER_OP_OR: r = (a != 0.0) || (b != 0.0); break;
+                    default: break;
+                }
+                st[sp++] = r;
+            }
+        }
+    }
+    return st[0];
+}
+
+__global__ void pop_update_kernel(Prog expr, Prog where, Cols C, int target, const int64_t* __restrict__ ids,
+                                  const uint8_t* __restrict__ alive, int64_t rows, uint32_t step, PhiloxKey key,
+                                  unsigned long long* n_updated)
+{
+    unsigned long long cnt = 0;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        if (!alive[r]) continue;
+        const int64_t id = ids[r];
+        if (where.n && eval(where, C, r, id, step, key) == 0.0) continue;
+        const double v = eval(expr, C, r, id, step, key);  // all reads of row r happen before its write
+        store_col(C.c[target], r, v);
+        ++cnt;
+    }
+    unsigned long long vals[1] = {cnt};
+    unsigned long long* const outs[1] = {n_updated};
+    block_sum_atomic<1>(vals, outs);
+}
+
+// Per-block partials (sum, min, max, count), reduced on the host in block order.
+__global__ void pop_aggregate_kernel(Prog expr, Prog where, Cols C, const int64_t* __restrict__ ids,
+                                     const uint8_t* __restrict__ alive, int64_t rows, uint32_t step, PhiloxKey key,
+                                     double* partial)
+{
+    double s = 0.0, mn = INFINITY, mx = -INFINITY, c = 0.0;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        if (!alive[r]) continue;
+        const int64_t id = ids[r];
+        if (where.n && eval(where, C, r, id, step, key) == 0.0) continue;
+        const double v = expr.n ? eval(expr, C, r, id, step, key) : 0.0;
+        s += v;
+        mn = fmin(mn, v);
+        mx = fmax(mx, v);
+        c += 1.0;
+    }
+    __shared__ double red[4][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    if (lane == 0) {
+        red[0][wid] = s;
+        red[1][wid] = mn;
+        red[2][wid] = mx;
+        red[3][wid] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double S = 0, MN = INFINITY, MX = -INFINITY, CC = 0;
+        for (int w = 0; w < nw; ++w) {
+            S += red[0][w];
+            MN = fmin(MN, red[1][w]);
+            MX = fmax(MX, red[2][w]);
+            CC += red[3][w];
+        }
+        partial[4 * blockIdx.x + 0] = S;
+        partial[4 * blockIdx.x + 1] = MN;
+        partial[4 * blockIdx.x + 2] = MX;
+        partial[4 * blockIdx.x + 3] = CC;
+    }
+}
+
+__global__ void pop_fill_kernel(ColView c, int64_t r0, int64_t r1, double v)
+{
+    for (int64_t r = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < r1; r += (int64_t)gridDim.x * blockDim.x)
+        store_col(c, r, v);
+}
+
+__global__ void pop_new_rows_kernel(int64_t* ids, uint8_t* alive, int64_t r0, int64_t r1, int64_t id0)
+{
+    for (int64_t r = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < r1; r += (int64_t)gridDim.x * blockDim.x) {
+        ids[r] = id0 + (r - r0);
+        alive[r] = 1;
+    }
+}
+
+// rows are sorted by id: binary search; row index or -1 (unknown) / -2 (dead)
+__global__ void pop_find_kernel(const int64_t* __restrict__ ids, const uint8_t* __restrict__ alive, int64_t rows,
+                                const int64_t* __restrict__ q, int64_t n, int64_t* __restrict__ row_out, int* bad)
+{
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = rows - 1, found = -1;
+        while (lo <= hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (ids[mid] == q[k]) {
+                found = mid;
+                break;
+            }
+            if (ids[mid] < q[k]) lo = mid + 1;
+            else hi = mid - 1;
+        }
+        if (found >= 0 && !alive[found]) found = -2;
+        row_out[k] = found;
+        if (found < 0) atomicExch(bad, 1);
+    }
+}
+
+__global__ void pop_kill_kernel(uint8_t* alive, const int64_t* rows, int64_t n, int* dup)
+{
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        alive[rows[k]] = 0;
+}
+
+__global__ void pop_scatter_kernel(ColView c, const int64_t* rows, const double* vals, int64_t n)
+{
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        store_col(c, rows[k], vals[k]);
+}
+
+size_t dtype_size(int dt)
+{
+    switch (dt) {
+        case AMBER_I32: case AMBER_F32: return 4;
+        case AMBER_I64: case AMBER_F64: return 8;
+        case AMBER_U8: return 1;
+        default: fail(AMBER_E_INVALID_ARG, "population columns must be I32, I64, F32, F64 or U8");
+    }
+}
+
+}  // namespace
+
+struct Population {
+    Runtime rt;
+    PhiloxKey key{};
+    struct Column {
+        std::string name;
+        int dtype;
+        DevBuf<char> data;
+    };
+    std::vector<std::unique_ptr<Column>> cols;
+    DevBuf<int64_t> ids;
+    DevBuf<uint8_t> alive;
+    int64_t cap = 0, rows = 0, live = 0, next_id = 0, step = 0;
+
+    Population(const amber_column_spec* specs, int n, int64_t capacity, uint64_t seed, const amber_runtime* r)
+    {
+        rt.init(r);
+        key = philox_key(seed);
+        AMBER_REQUIRE(n >= 1 && n <= kMaxCols, "population needs 1..32 columns");
+        for (int k = 0; k < n; ++k) {
+            AMBER_REQUIRE(specs[k].name && *specs[k].name, "empty column name");
+            std::string nm(specs[k].name);
+            AMBER_REQUIRE(nm != "id", "column name 'id' is reserved");
+            for (auto& c : cols) AMBER_REQUIRE(c->name != nm, "duplicate column name " + nm);
+            dtype_size(specs[k].dtype);
+            auto c = std::make_unique<Column>();
+            c->name = nm;
+            c->dtype = specs[k].dtype;
+            cols.push_back(std::move(c));
+        }
+        reserve(std::max<int64_t>(capacity, 16));
+    }
+
+    ~Population()
+    {
+        if (rt.stream) cudaStreamSynchronize(rt.stream);
+        cols.clear();
+        ids.reset();
+        alive.reset();
+        rt.destroy();
+    }
+
+    Cols views() const
+    {
+        Cols C{};
+        C.n = static_cast<int>(cols.size());
+        for (int k = 0; k < C.n; ++k) C.c[k] = ColView{cols[k]->data.p, cols[k]->dtype};
+        return C;
+    }
+
+    int col_index(const std::string& nm) const
+    {
+        for (size_t k = 0; k < cols.size(); ++k)
+            if (cols[k]->name == nm) return static_cast<int>(k);
+        return -1;
+    }
+
+    void reserve(int64_t want)
+    {
+        if (want <= cap) return;
+        const int64_t nc = std::max<int64_t>(want, cap * 2);
+        auto grow = [&](DevBuf<char>& b, size_t esz) {
+            DevBuf<char> nb;
+            nb.allocate(&rt, nc * esz);
+            if (rows) AMBER_CUDA(cudaMemcpyAsync(nb.p, b.p, rows * esz, cudaMemcpyDeviceToDevice, rt.stream));
+            std::swap(b.p, nb.p);
+            std::swap(b.n, nb.n);
+            b.rt = &rt;
+        };
+        for (auto& c : cols) grow(c->data, dtype_size(c->dtype));
+        DevBuf<int64_t> ni;
+        ni.allocate(&rt, nc);
+        DevBuf<uint8_t> na;
+        na.allocate(&rt, nc);
+        if (rows) {
+            AMBER_CUDA(cudaMemcpyAsync(ni.p, ids.p, rows * 8, cudaMemcpyDeviceToDevice, rt.stream));
+            AMBER_CUDA(cudaMemcpyAsync(na.p, alive.p, rows, cudaMemcpyDeviceToDevice, rt.stream));
+        }
+        std::swap(ids.p, ni.p);
+        std::swap(ids.n, ni.n);
+        ids.rt = &rt;
+        std::swap(alive.p, na.p);
+        std::swap(alive.n, na.n);
+        alive.rt = &rt;
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        cap = nc;
+    }
+
+    int grid_for(int64_t n) const
+    {
+        return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), rt.num_sms * 8)));
+    }
+
+    int64_t add(int64_t n, const double* defaults)
+    {
+        AMBER_REQUIRE(n >= 0, "add_agents needs n >= 0");
+        reserve(rows + n);
+        const int64_t first = next_id;
+        if (n) {
+            for (size_t k = 0; k < cols.size(); ++k) {
+                pop_fill_kernel<<<grid_for(n), 256, 0, rt.stream>>>(ColView{cols[k]->data.p, cols[k]->dtype}, rows,
+                                                                    rows + n, defaults ? defaults[k] : 0.0);
+                check_launch("pop_fill_kernel");
+            }
+            pop_new_rows_kernel<<<grid_for(n), 256, 0, rt.stream>>>(ids.p, alive.p, rows, rows + n, next_id);
+            check_launch("pop_new_rows_kernel");
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        }
+        rows += n;
+        live += n;
+        next_id += n;
+        return first;
+    }
+
+    // validated id -> row lookup on the device (throws if any id is unknown/dead)
+    void find_rows(const int64_t* h_ids, int64_t n, DevBuf<int64_t>& d_rows)
+    {
+        DevBuf<int64_t> q;
+        DevBuf<int> bad;
+        q.allocate(&rt, n);
+        d_rows.allocate(&rt, n);
+        bad.allocate(&rt, 1);
+        bad.zero_async(rt.stream);
+        AMBER_CUDA(cudaMemcpyAsync(q.p, h_ids, n * 8, cudaMemcpyHostToDevice, rt.stream));
+        pop_find_kernel<<<grid_for(n), 256, 0, rt.stream>>>(ids.p, alive.p, rows, q.p, n, d_rows.p, bad.p);
+        check_launch("pop_find_kernel");
+        int hb = 0;
+        AMBER_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        if (hb) fail(AMBER_E_INVALID_ARG, "unknown or dead agent id");
+    }
+
+    void remove(const int64_t* h_ids, int64_t n)
+    {
+        if (!n) return;
+        std::vector<int64_t> u(h_ids, h_ids + n);
+        std::sort(u.begin(), u.end());
+        AMBER_REQUIRE(std::adjacent_find(u.begin(), u.end()) == u.end(), "duplicate id in remove_agents");
+        DevBuf<int64_t> d_rows;
+        find_rows(u.data(), n, d_rows);
+        pop_kill_kernel<<<grid_for(n), 256, 0, rt.stream>>>(alive.p, d_rows.p, n, nullptr);
+        check_launch("pop_kill_kernel");
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        live -= n;
+    }
+
+    void compact()
+    {
+        if (live == rows) return;
+        DevBuf<int> n_sel;
+        n_sel.allocate(&rt, 1);
+        auto select = [&](void* data, size_t esz) {
+            DevBuf<char> out;
+            out.allocate(&rt, std::max<int64_t>(cap, 1) * esz);
+            size_t tmp = 0;
+            // flagged selection of fixed-size records via 1/2/4/8-byte element types
+            auto run = [&](auto* in, auto* o) {
+                cub::DeviceSelect::Flagged(nullptr, tmp, in, alive.p, o, n_sel.p, rows, rt.stream);
+                DevBuf<char> t;
+                t.allocate(&rt, tmp + 16);
+                AMBER_CUDA(cub::DeviceSelect::Flagged(t.p, tmp, in, alive.p, o, n_sel.p, rows, rt.stream));
+                AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            };
+            if (esz == 1) run(static_cast<uint8_t*>(data), reinterpret_cast<uint8_t*>(out.p));
+            else if (esz == 4) run(static_cast<uint32_t*>(data), reinterpret_cast<uint32_t*>(out.p));
+            else run(static_cast<unsigned long long*>(data), reinterpret_cast<unsigned long long*>(out.p));
+            AMBER_CUDA(cudaMemcpyAsync(data, out.p, live * esz, cudaMemcpyDeviceToDevice, rt.stream));
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        };
+        for (auto& c : cols) select(c->data.p, dtype_size(c->dtype));
+        select(ids.p, 8);
+        AMBER_CUDA(cudaMemsetAsync(alive.p, 1, live, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rows = live;
+    }
+
+    Prog prog(const amber_instr* ins, int n, bool allow_empty) const
+    {
+        Prog P{};
+        AMBER_REQUIRE(n >= 0 && n <= kMaxProg, "expression longer than 64 instructions");
+        AMBER_REQUIRE(allow_empty || n > 0, "empty expression");
+        AMBER_REQUIRE(n == 0 || ins, "NULL expression");
+        int depth = 0;
+        for (int k = 0; k < n; ++k) {
+            const int op = ins[k].op;
+            int pop = 0, push = 1;
+            if (op == AMBER_OP_CONST || op == AMBER_OP_ID || op == AMBER_OP_STEP || op == AMBER_OP_RAND) {
+                pop = 0;
+            } else if (op == AMBER_OP_COL) {
+                AMBER_REQUIRE(ins[k].arg >= 0 && ins[k].arg < static_cast<int>(cols.size()), "column index out of range");
+            } else if (op >= AMBER_OP_NEG && op <= AMBER_OP_SQRT) {
+                pop = 1;
+            } else if (op == AMBER_OP_NOT) {
+                pop = 1;
+            } else if ((op >= AMBER_OP_ADD && op <= AMBER_OP_MAX) || (op >= AMBER_OP_LT && op <= AMBER_OP_NE) ||
+                       op == AMBER_OP_AND || op == AMBER_OP_OR) {
+                pop = 2;
+            } else if (op == AMBER_OP_SELECT) {
+                pop = 3;
+            } else {
+                fail(AMBER_E_INVALID_ARG, "unknown expression op " + std::to_string(op));
+            }
+            AMBER_REQUIRE(depth >= pop, "expression stack underflow");
+            depth += push - pop;
+            AMBER_REQUIRE(depth <= kMaxStack, "expression stack deeper than 16");
+            P.ins[k] = ins[k];
+        }
+        AMBER_REQUIRE(n == 0 || depth == 1, "expression must leave exactly one value");
+        P.n = n;
+        return P;
+    }
+
+    int64_t update(const std::string& target, const amber_instr* e, int ne, const amber_instr* w, int nw)
+    {
+        const int tgt = col_index(target);
+        if (tgt < 0) fail(AMBER_E_UNKNOWN_NAME, "no column " + target);
+        const Prog pe = prog(e, ne, false), pw = prog(w, nw, true);
+        DevBuf<unsigned long long> cnt;
+        cnt.allocate(&rt, 1);
+        cnt.zero_async(rt.stream);
+        if (rows) {
+            pop_update_kernel<<<grid_for(rows), 256, 0, rt.stream>>>(pe, pw, views(), tgt, ids.p, alive.p, rows,
+                                                                     static_cast<uint32_t>(step), key, cnt.p);
+            check_launch("pop_update_kernel");
+        }
+        unsigned long long h = 0;
+        AMBER_CUDA(cudaMemcpyAsync(&h, cnt.p, 8, cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        return static_cast<int64_t>(h);
+    }
+
+    double aggregate(int agg, const amber_instr* e, int ne, const amber_instr* w, int nw)
+    {
+        AMBER_REQUIRE(agg >= AMBER_AGG_SUM && agg <= AMBER_AGG_COUNT, "unknown aggregate");
+        const Prog pe = prog(e, ne, agg == AMBER_AGG_COUNT), pw = prog(w, nw, true);
+        const int g = grid_for(std::max<int64_t>(rows, 1));
+        DevBuf<double> part;
+        part.allocate(&rt, 4 * g);
+        std::vector<double> h(4 * g, 0.0);
+        if (rows) {
+            pop_aggregate_kernel<<<g, 256, 0, rt.stream>>>(pe, pw, views(), ids.p, alive.p, rows,
+                                                           static_cast<uint32_t>(step), key, part.p);
+            check_launch("pop_aggregate_kernel");
+            AMBER_CUDA(cudaMemcpyAsync(h.data(), part.p, h.size() * 8, cudaMemcpyDeviceToHost, rt.stream));
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        } else {
+            for (int b = 0; b < g; ++b) {
+                h[4 * b + 1] = INFINITY;
+                h[4 * b + 2] = -INFINITY;
+            }
+        }
+        double S = 0, MN = INFINITY, MX = -INFINITY, CC = 0;
+        for (int b = 0; b < g; ++b) {
+            S += h[4 * b];
+            MN = std::fmin(MN, h[4 * b + 1]);
+            MX = std::fmax(MX, h[4 * b + 2]);
+            CC += h[4 * b + 3];
+        }
+        if (agg == AMBER_AGG_COUNT) return CC;
+        if (agg == AMBER_AGG_SUM) return S;
+        AMBER_REQUIRE(CC > 0, "mean/min/max of an empty selection");
+        if (agg == AMBER_AGG_MEAN) return S / CC;
+        return agg == AMBER_AGG_MIN ? MN : MX;
+    }
+
+    void read(const std::string& nm, void* dst, size_t bytes, bool on_dev)
+    {
+        void* data;
+        size_t esz;
+        if (nm == "id") {
+            data = ids.p;
+            esz = 8;
+        } else {
+            const int k = col_index(nm);
+            if (k < 0) fail(AMBER_E_UNKNOWN_NAME, "no column " + nm);
+            data = cols[k]->data.p;
+            esz = dtype_size(cols[k]->dtype);
+        }
+        if (bytes < static_cast<size_t>(live) * esz) fail(AMBER_E_BUFFER_TOO_SMALL, "dst too small for column " + nm);
+        if (!live) return;
+        DevBuf<char> out;
+        out.allocate(&rt, live * esz);
+        DevBuf<int> n_sel;
+        n_sel.allocate(&rt, 1);
+        size_t tmp = 0;
+        auto run = [&](auto* in, auto* o) {
+            cub::DeviceSelect::Flagged(nullptr, tmp, in, alive.p, o, n_sel.p, rows, rt.stream);
+            DevBuf<char> t;
+            t.allocate(&rt, tmp + 16);
+            AMBER_CUDA(cub::DeviceSelect::Flagged(t.p, tmp, in, alive.p, o, n_sel.p, rows, rt.stream));
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        };
+        if (esz == 1) run(static_cast<uint8_t*>(data), reinterpret_cast<uint8_t*>(out.p));
+        else if (esz == 4) run(static_cast<uint32_t*>(data), reinterpret_cast<uint32_t*>(out.p));
+        else run(static_cast<unsigned long long*>(data), reinterpret_cast<unsigned long long*>(out.p));
+        copy_out(rt, dst, out.p, live * esz, on_dev);
+    }
+
+    void batch_set(const std::string& nm, const int64_t* h_ids, const double* vals, int64_t n)
+    {
+        const int k = col_index(nm);
+        if (k < 0) fail(AMBER_E_UNKNOWN_NAME, "no column " + nm);
+        if (!n) return;
+        // last staged write wins: keep the last occurrence of every id
+        std::map<int64_t, double> last;
+        for (int64_t i = 0; i < n; ++i) last[h_ids[i]] = vals[i];
+        std::vector<int64_t> u;
+        std::vector<double> v;
+        for (auto& kv : last) {
+            u.push_back(kv.first);
+            v.push_back(kv.second);
+        }
+        DevBuf<int64_t> d_rows;
+        find_rows(u.data(), static_cast<int64_t>(u.size()), d_rows);  // validates all before writing
+        DevBuf<double> d_vals;
+        d_vals.allocate(&rt, v.size());
+        AMBER_CUDA(cudaMemcpyAsync(d_vals.p, v.data(), v.size() * 8, cudaMemcpyHostToDevice, rt.stream));
+        pop_scatter_kernel<<<grid_for(v.size()), 256, 0, rt.stream>>>(ColView{cols[k]->data.p, cols[k]->dtype}, d_rows.p,
+                                                                      d_vals.p, static_cast<int64_t>(v.size()));
+        check_launch("pop_scatter_kernel");
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    }
+};
+
+Population* make_population(const amber_column_spec* cols, int n, int64_t cap, uint64_t seed, const amber_runtime* rt)
+{
+    return new Population(cols, n, cap, seed, rt);
+}
+void destroy_population(Population* p) { delete p; }
+int64_t population_add(Population* p, int64_t n, const double* d) { return p->add(n, d); }
+void population_remove(Population* p, const int64_t* ids, int64_t n) { p->remove(ids, n); }
+void population_compact(Population* p) { p->compact(); }
+void population_size(Population* p, int64_t* live, int64_t* rows)
+{
+    if (live) *live = p->live;
+    if (rows) *rows = p->rows;
+}
+int64_t population_update(Population* p, const char* t, const amber_instr* e, int ne, const amber_instr* w, int nw)
+{
+    return p->update(t, e, ne, w, nw);
+}
+double population_aggregate(Population* p, int agg, const amber_instr* e, int ne, const amber_instr* w, int nw)
+{
+    return p->aggregate(agg, e, ne, w, nw);
+}
+void population_read(Population* p, const char* nm, void* dst, size_t bytes, bool on_dev) { p->read(nm, dst, bytes, on_dev); }
+void population_batch_set(Population* p, const char* nm, const int64_t* ids, const double* v, int64_t n)
+{
+    p->batch_set(nm, ids, v, n);
+}
+void population_set_step(Population* p, int64_t s)
+{
+    AMBER_REQUIRE(s >= 0 && s < (1ll << 32), "step out of range");
+    p->step = s;
+}
+
+}  // namespace amber
