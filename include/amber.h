@@ -320,9 +320,9 @@ typedef struct {
     amber_dtype dtype; /* AMBER_I32, AMBER_I64, AMBER_F32, AMBER_F64 or AMBER_U8 */
 } amber_column_spec;
 
-/* Expression instruction (postfix / stack machine, evaluated in double per
- * row; results are stored with C conversion semantics: truncation toward zero
- * for integer columns).  arg = column index for AMBER_OP_COL, tag for
+/* Expression instruction (postfix / stack machine of at most 64 instructions
+ * and stack depth 8, evaluated in double per row; results are stored with C
+ * conversion semantics: truncation toward zero for integer columns).  arg = column index for AMBER_OP_COL, tag for
  * AMBER_OP_RAND; value = the constant for AMBER_OP_CONST. */
 typedef enum {
     AMBER_OP_CONST = 0, AMBER_OP_COL = 1, AMBER_OP_ID = 2, AMBER_OP_STEP = 3,
@@ -366,7 +366,8 @@ int amber_population_size(amber_population* p, int64_t* live, int64_t* rows);
 /* Synchronous population-wide update: for every live row where `where`
  * evaluates != 0 (n_where == 0: every live row), target = expr(row), all rows
  * reading the pre-update snapshot (SPEC update_column / update_where).
- * *n_updated (may be NULL) = rows updated.  Errors: UNKNOWN_NAME, INVALID_ARG
+ * *n_updated = rows updated (synchronising); n_updated == NULL makes the call
+ * fully asynchronous on the population's stream (amber_population_synchronize).  Errors: UNKNOWN_NAME, INVALID_ARG
  * (bad program: stack underflow/overflow, unknown op, column index). */
 int amber_population_update(amber_population* p, const char* target, const amber_instr* expr, int n_expr,
                             const amber_instr* where, int n_where, int64_t* n_updated);
@@ -387,6 +388,9 @@ int amber_population_read_column(amber_population* p, const char* name, void* ds
  * on any error nothing is written.  Duplicate ids: the last write wins. */
 int amber_population_batch_set(amber_population* p, const char* name, const int64_t* ids,
                                const double* values, int64_t n);
+
+/* Wait for all work enqueued on the population's stream. */
+int amber_population_synchronize(amber_population* p);
 
 /* Step counter read by AMBER_OP_STEP / AMBER_OP_RAND (advance it per model step). */
 int amber_population_set_step(amber_population* p, int64_t step);

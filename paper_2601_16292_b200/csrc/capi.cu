@@ -348,7 +348,7 @@ int amber_population_update(amber_population* p, const char* target, const amber
 {
     return guarded([&] {
         need(target, "target");
-        const int64_t k = amber::population_update(pimpl(p), target, expr, n_expr, where, n_where);
+        const int64_t k = amber::population_update(pimpl(p), target, expr, n_expr, where, n_where, n_updated != nullptr);
         if (n_updated) *n_updated = k;
         return 0;
     });
@@ -382,6 +382,14 @@ int amber_population_batch_set(amber_population* p, const char* name, const int6
         need(name, "name");
         AMBER_REQUIRE(n >= 0 && (n == 0 || (ids && values)), "bad batch");
         amber::population_batch_set(pimpl(p), name, ids, values, n);
+        return 0;
+    });
+}
+
+int amber_population_synchronize(amber_population* p)
+{
+    return guarded([&] {
+        amber::population_synchronize(pimpl(p));
         return 0;
     });
 }

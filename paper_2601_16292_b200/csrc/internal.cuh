@@ -174,7 +174,9 @@ int64_t population_add(Population* p, int64_t n, const double* defaults);
 void population_remove(Population* p, const int64_t* ids, int64_t n);
 void population_compact(Population* p);
 void population_size(Population* p, int64_t* live, int64_t* rows);
-int64_t population_update(Population* p, const char* target, const amber_instr* e, int ne, const amber_instr* w, int nw);
+int64_t population_update(Population* p, const char* target, const amber_instr* e, int ne, const amber_instr* w, int nw,
+                          bool want_count);
+void population_synchronize(Population* p);
 double population_aggregate(Population* p, int agg, const amber_instr* e, int ne, const amber_instr* w, int nw);
 void population_read(Population* p, const char* name, void* dst, size_t bytes, bool on_dev);
 void population_batch_set(Population* p, const char* name, const int64_t* ids, const double* vals, int64_t n);

@@ -18,10 +18,13 @@ namespace amber {
 
 namespace {
 
-constexpr int kMaxProg = 64, kMaxStack = 16, kMaxCols = 32;
+constexpr int kMaxProg = 64, kMaxStack = 8, kMaxCols = 32;
+constexpr int kThreads = 256, kRPT = 4, kTile = kThreads * kRPT;   // rows per tile
+constexpr size_t kStackBytes = kMaxStack * kTile * sizeof(double);   // 64 KB per block
 
 struct Prog {
     int n;
+    int uses_id;  // program reads the agent id (ID / RAND): load the id column
     amber_instr ins[kMaxProg];
 };
 
@@ -57,73 +60,143 @@ __device__ __forceinline__ void store_col(const ColView& c, int64_t row, double 
     }
 }
 
-__device__ double eval(const Prog& P, const Cols& C, int64_t row, int64_t id, uint32_t step, const PhiloxKey& key)
+// Columnar stack machine: every instruction is applied to a whole tile of
+// kTile rows before the next one (as a column engine would), so the dispatch
+// is amortised over the tile.  Thread tid owns rows tid, tid+256, ... of the
+// tile (coalesced column loads) and only ever touches its own rows' stack
+// slots, so no barrier is needed between instructions.  stk[slot*kTile + j].
+__device__ void eval_tile(const Prog& P, const Cols& C, int64_t row0, int64_t rows, const int64_t* __restrict__ ids,
+                          uint32_t step, const PhiloxKey& key, double* stk)
 {
-    double st[kMaxStack];
+    const int tid = threadIdx.x;
     int sp = 0;
     for (int k = 0; k < P.n; ++k) {
         const amber_instr in = P.ins[k];
         switch (in.op) {
-            case AMBER_OP_CONST: st[sp++] = in.value; break;
-            case AMBER_OP_COL: st[sp++] = load_col(C.c[in.arg], row); break;
-            case AMBER_OP_ID: st[sp++] = static_cast<double>(id); break;
-            case AMBER_OP_STEP: st[sp++] = static_cast<double>(step); break;
-            case AMBER_OP_RAND: {
-                const uint4 w = stream_block(key, static_cast<uint32_t>(in.arg), static_cast<unsigned long long>(id) >> 2,
-                                             step);
-                const uint32_t q = static_cast<uint32_t>(id & 3);
-                st[sp++] = static_cast<double>(u01(q == 0 ? w.x : (q == 1 ? w.y : (q == 2 ? w.z : w.w))));
+            case AMBER_OP_CONST:
+#pragma unroll
+                for (int m = 0; m < kRPT; ++m) stk[sp * kTile + m * kThreads + tid] = in.value;
+                ++sp;
                 break;
-            }
-            case AMBER_OP_NEG: st[sp - 1] = -st[sp - 1]; break;
-            case AMBER_OP_ABS: st[sp - 1] = fabs(st[sp - 1]); break;
-            case AMBER_OP_FLOOR: st[sp - 1] = floor(st[sp - 1]); break;
-            case AMBER_OP_SQRT: st[sp - 1] = sqrt(st[sp - 1]); break;
-            case AMBER_OP_NOT: st[sp - 1] = st[sp - 1] == 0.0 ? 1.0 : 0.0; break;
-            case AMBER_OP_SELECT: {
-                const double b = st[--sp], a = st[--sp], c = st[--sp];
-                st[sp++] = c != 0.0 ? a : b;
-                break;
-            }
-            default: {
-                const double b = st[--sp], a = st[--sp];
-                double r = 0.0;
-                switch (in.op) {
-                    case AMBER_OP_ADD: r = a + b; break;
-                    case AMBER_OP_SUB: r = a - b; break;
-                    case AMBER_OP_MUL: r = a * b; break;
-                    case AMBER_OP_DIV: r = a / b; break;
-                    case AMBER_OP_MIN: r = fmin(a, b); break;
-                    case AMBER_OP_MAX: r = fmax(a, b); break;
-                    case AMBER_OP_LT: r = a < b; break;
-                    case AMBER_OP_LE: r = a <= b; break;
-                    case AMBER_OP_GT: r = a > b; break;
-                    case AMBER_OP_GE: r = a >= b; break;
-                    case AMBER_OP_EQ: r = a == b; break;
-                    case AMBER_OP_NE: r = a != b; break;
-                    case AMBER_OP_AND: r = (a != 0.0) && (b != 0.0); break;
-                    case AMBER_OP_OR: r = (a != 0.0) || (b != 0.0); break;
-                    default: break;
+            case AMBER_OP_COL: {
+                double v[kRPT];
+#pragma unroll
+                for (int m = 0; m < kRPT; ++m) {
+                    const int64_t r = row0 + m * kThreads + tid;
+                    v[m] = r < rows ? load_col(C.c[in.arg], r) : 0.0;
                 }
-                st[sp++] = r;
+#pragma unroll
+                for (int m = 0; m < kRPT; ++m) stk[sp * kTile + m * kThreads + tid] = v[m];
+                ++sp;
+                break;
             }
+            case AMBER_OP_ID:
+            case AMBER_OP_RAND:
+#pragma unroll
+                for (int m = 0; m < kRPT; ++m) {
+                    const int64_t r = row0 + m * kThreads + tid;
+                    const int64_t id = r < rows ? ids[r] : 0;
+                    double v = static_cast<double>(id);
+                    if (in.op == AMBER_OP_RAND) {
+                        const uint4 w = stream_block(key, static_cast<uint32_t>(in.arg),
+                                                     static_cast<unsigned long long>(id) >> 2, step);
+                        const uint32_t q = static_cast<uint32_t>(id & 3);
+                        v = static_cast<double>(u01(q == 0 ? w.x : (q == 1 ? w.y : (q == 2 ? w.z : w.w))));
+                    }
+                    stk[sp * kTile + m * kThreads + tid] = v;
+                }
+                ++sp;
+                break;
+            case AMBER_OP_STEP:
+#pragma unroll
+                for (int m = 0; m < kRPT; ++m) stk[sp * kTile + m * kThreads + tid] = static_cast<double>(step);
+                ++sp;
+                break;
+            case AMBER_OP_NEG:
+            case AMBER_OP_ABS:
+            case AMBER_OP_FLOOR:
+            case AMBER_OP_SQRT:
+            case AMBER_OP_NOT:
+#pragma unroll
+                for (int m = 0; m < kRPT; ++m) {
+                    double& a = stk[(sp - 1) * kTile + m * kThreads + tid];
+                    switch (in.op) {
+                        case AMBER_OP_NEG: a = -a; break;
+                        case AMBER_OP_ABS: a = fabs(a); break;
+                        case AMBER_OP_FLOOR: a = floor(a); break;
+                        case AMBER_OP_SQRT: a = sqrt(a); break;
+                        default: a = a == 0.0 ? 1.0 : 0.0; break;
+                    }
+                }
+                break;
+            case AMBER_OP_SELECT:
+#pragma unroll
+                for (int m = 0; m < kRPT; ++m) {
+                    const int j = m * kThreads + tid;
+                    const double b = stk[(sp - 1) * kTile + j], a = stk[(sp - 2) * kTile + j],
+                                 c = stk[(sp - 3) * kTile + j];
+                    stk[(sp - 3) * kTile + j] = c != 0.0 ? a : b;
+                }
+                sp -= 2;
+                break;
+            default:
+#pragma unroll
+                for (int m = 0; m < kRPT; ++m) {
+                    const int j = m * kThreads + tid;
+                    const double b = stk[(sp - 1) * kTile + j], a = stk[(sp - 2) * kTile + j];
+                    double r = 0.0;
+                    switch (in.op) {
+                        case AMBER_OP_ADD: r = a + b; break;
+                        case AMBER_OP_SUB: r = a - b; break;
+                        case AMBER_OP_MUL: r = a * b; break;
+                        case AMBER_OP_DIV: r = a / b; break;
+                        case AMBER_OP_MIN: r = fmin(a, b); break;
+                        case AMBER_OP_MAX: r = fmax(a, b); break;
+                        case AMBER_OP_LT: r = a < b; break;
+                        case AMBER_OP_LE: r = a <= b; break;
+                        case AMBER_OP_GT: r = a > b; break;
+                        case AMBER_OP_GE: r = a >= b; break;
+                        case AMBER_OP_EQ: r = a == b; break;
+                        case AMBER_OP_NE: r = a != b; break;
+                        case AMBER_OP_AND: r = (a != 0.0) && (b != 0.0); break;
+                        case AMBER_OP_OR: r = (a != 0.0) || (b != 0.0); break;
+                        default: break;
+                    }
+                    stk[(sp - 2) * kTile + j] = r;
+                }
+                --sp;
         }
     }
-    return st[0];
 }
 
-__global__ void pop_update_kernel(Prog expr, Prog where, Cols C, int target, const int64_t* __restrict__ ids,
-                                  const uint8_t* __restrict__ alive, int64_t rows, uint32_t step, PhiloxKey key,
-                                  unsigned long long* n_updated)
+__global__ void __launch_bounds__(kThreads) pop_update_kernel(Prog expr, Prog where, Cols C, int target,
+                                                              const int64_t* __restrict__ ids,
+                                                              const uint8_t* __restrict__ alive, int64_t rows,
+                                                              uint32_t step, PhiloxKey key,
+                                                              unsigned long long* n_updated)
 {
+    extern __shared__ double stk[];
     unsigned long long cnt = 0;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
-        if (!alive[r]) continue;
-        const int64_t id = ids[r];
-        if (where.n && eval(where, C, r, id, step, key) == 0.0) continue;
-        const double v = eval(expr, C, r, id, step, key);  // all reads of row r happen before its write
-        store_col(C.c[target], r, v);
-        ++cnt;
+    const int tid = threadIdx.x;
+    for (int64_t row0 = static_cast<int64_t>(blockIdx.x) * kTile; row0 < rows; row0 += static_cast<int64_t>(gridDim.x) * kTile) {
+        bool sel[kRPT];
+#pragma unroll
+        for (int m = 0; m < kRPT; ++m) {
+            const int64_t r = row0 + m * kThreads + tid;
+            sel[m] = r < rows && alive[r];
+        }
+        if (where.n) {
+            eval_tile(where, C, row0, rows, ids, step, key, stk);
+#pragma unroll
+            for (int m = 0; m < kRPT; ++m) sel[m] = sel[m] && stk[m * kThreads + tid] != 0.0;
+        }
+        eval_tile(expr, C, row0, rows, ids, step, key, stk);  // all reads of a row happen before its write
+#pragma unroll
+        for (int m = 0; m < kRPT; ++m)
+            if (sel[m]) {
+                store_col(C.c[target], row0 + m * kThreads + tid, stk[m * kThreads + tid]);
+                ++cnt;
+            }
     }
     unsigned long long vals[1] = {cnt};
     unsigned long long* const outs[1] = {n_updated};
@@ -131,23 +204,39 @@ __global__ void pop_update_kernel(Prog expr, Prog where, Cols C, int target, con
 }
 
 // Per-block partials (sum, min, max, count), reduced on the host in block order.
-__global__ void pop_aggregate_kernel(Prog expr, Prog where, Cols C, const int64_t* __restrict__ ids,
-                                     const uint8_t* __restrict__ alive, int64_t rows, uint32_t step, PhiloxKey key,
-                                     double* partial)
+__global__ void __launch_bounds__(kThreads) pop_aggregate_kernel(Prog expr, Prog where, Cols C,
+                                                                 const int64_t* __restrict__ ids,
+                                                                 const uint8_t* __restrict__ alive, int64_t rows,
+                                                                 uint32_t step, PhiloxKey key, double* partial)
 {
+    extern __shared__ double stk[];
     double s = 0.0, mn = INFINITY, mx = -INFINITY, c = 0.0;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
-        if (!alive[r]) continue;
-        const int64_t id = ids[r];
-        if (where.n && eval(where, C, r, id, step, key) == 0.0) continue;
-        const double v = expr.n ? eval(expr, C, r, id, step, key) : 0.0;
-        s += v;
-        mn = fmin(mn, v);
-        mx = fmax(mx, v);
-        c += 1.0;
+    const int tid = threadIdx.x;
+    for (int64_t row0 = static_cast<int64_t>(blockIdx.x) * kTile; row0 < rows; row0 += static_cast<int64_t>(gridDim.x) * kTile) {
+        bool sel[kRPT];
+#pragma unroll
+        for (int m = 0; m < kRPT; ++m) {
+            const int64_t r = row0 + m * kThreads + tid;
+            sel[m] = r < rows && alive[r];
+        }
+        if (where.n) {
+            eval_tile(where, C, row0, rows, ids, step, key, stk);
+#pragma unroll
+            for (int m = 0; m < kRPT; ++m) sel[m] = sel[m] && stk[m * kThreads + tid] != 0.0;
+        }
+        if (expr.n) eval_tile(expr, C, row0, rows, ids, step, key, stk);
+#pragma unroll
+        for (int m = 0; m < kRPT; ++m)
+            if (sel[m]) {
+                const double v = expr.n ? stk[m * kThreads + tid] : 0.0;
+                s += v;
+                mn = fmin(mn, v);
+                mx = fmax(mx, v);
+                c += 1.0;
+            }
     }
     __shared__ double red[4][32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -162,7 +251,7 @@ __global__ void pop_aggregate_kernel(Prog expr, Prog where, Cols C, const int64_
         red[3][wid] = c;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
         double S = 0, MN = INFINITY, MX = -INFINITY, CC = 0;
         for (int w = 0; w < nw; ++w) {
             S += red[0][w];
@@ -175,6 +264,169 @@ __global__ void pop_aggregate_kernel(Prog expr, Prog where, Cols C, const int64_
         partial[4 * blockIdx.x + 2] = MX;
         partial[4 * blockIdx.x + 3] = CC;
     }
+}
+
+// Fast path for the most common update shape (Listing 1):
+// target = col[a] OP (constant | col[b]), no filter.  8 rows per thread with
+// every load issued before the first use (memory-level parallelism); same
+// double arithmetic and store conversion as the interpreter.
+constexpr int kBinRows = 8;
+
+__global__ void __launch_bounds__(256) pop_binop_kernel(ColView tgt, ColView a, ColView b, int b_is_const, double k,
+                                                        int op, const uint8_t* __restrict__ alive, int64_t rows,
+                                                        unsigned long long* n_updated)
+{
+    unsigned long long cnt = 0;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * kBinRows; base < rows;
+         base += stride * kBinRows) {
+        double va[kBinRows], vb[kBinRows];
+        bool live[kBinRows];
+#pragma unroll
+        for (int m = 0; m < kBinRows; ++m) {
+            const int64_t r = base + static_cast<int64_t>(m) * blockDim.x + threadIdx.x;
+            live[m] = r < rows && alive[r];
+            va[m] = r < rows ? load_col(a, r) : 0.0;
+            vb[m] = b_is_const ? k : (r < rows ? load_col(b, r) : 0.0);
+        }
+#pragma unroll
+        for (int m = 0; m < kBinRows; ++m) {
+            if (!live[m]) continue;
+            const double x = va[m], y = vb[m];
+            double v;
+            switch (op) {
+                case AMBER_OP_ADD: v = x + y; break;
+                case AMBER_OP_SUB: v = x - y; break;
+                case AMBER_OP_MUL: v = x * y; break;
+                case AMBER_OP_DIV: v = x / y; break;
+                case AMBER_OP_MIN: v = fmin(x, y); break;
+                default: v = fmax(x, y); break;
+            }
+            store_col(tgt, base + static_cast<int64_t>(m) * blockDim.x + threadIdx.x, v);
+            ++cnt;
+        }
+    }
+    unsigned long long vals[1] = {cnt};
+    unsigned long long* const outs[1] = {n_updated};
+    block_sum_atomic<1>(vals, outs);
+}
+
+// Same fast path when target and operand columns share one element type:
+// typed loads (no per-element dtype dispatch), all 8 rows' loads in flight.
+template <class T>
+__global__ void __launch_bounds__(256) pop_binop_typed_kernel(T* __restrict__ tgt, const T* __restrict__ a,
+                                                              const T* __restrict__ b, int b_is_const, double k, int op,
+                                                              const uint8_t* __restrict__ alive, int64_t rows,
+                                                              unsigned long long* n_updated)
+{
+    unsigned long long cnt = 0;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * kBinRows; base < rows;
+         base += stride * kBinRows) {
+        T va[kBinRows], vb[kBinRows];
+        uint8_t live[kBinRows];
+#pragma unroll
+        for (int m = 0; m < kBinRows; ++m) {
+            const int64_t r = base + static_cast<int64_t>(m) * blockDim.x + threadIdx.x;
+            const bool in = r < rows;
+            live[m] = in ? alive[r] : 0;
+            va[m] = in ? a[r] : T(0);
+            vb[m] = (!b_is_const && in) ? b[r] : T(0);
+        }
+#pragma unroll
+        for (int m = 0; m < kBinRows; ++m) {
+            if (!live[m]) continue;
+            const double x = static_cast<double>(va[m]), y = b_is_const ? k : static_cast<double>(vb[m]);
+            double v;
+            switch (op) {
+                case AMBER_OP_ADD: v = x + y; break;
+                case AMBER_OP_SUB: v = x - y; break;
+                case AMBER_OP_MUL: v = x * y; break;
+                case AMBER_OP_DIV: v = x / y; break;
+                case AMBER_OP_MIN: v = fmin(x, y); break;
+                default: v = fmax(x, y); break;
+            }
+            tgt[base + static_cast<int64_t>(m) * blockDim.x + threadIdx.x] = static_cast<T>(v);
+            ++cnt;
+        }
+    }
+    unsigned long long vals[1] = {cnt};
+    unsigned long long* const outs[1] = {n_updated};
+    block_sum_atomic<1>(vals, outs);
+}
+
+// 4-byte columns: thread g owns rows [8g, 8g+8) -> two 128-bit loads per
+// operand column, one 64-bit load of the alive mask, two 128-bit stores.
+template <class T>
+__device__ __forceinline__ double binop(int op, double x, double y)
+{
+    switch (op) {
+        case AMBER_OP_ADD: return x + y;
+        case AMBER_OP_SUB: return x - y;
+        case AMBER_OP_MUL: return x * y;
+        case AMBER_OP_DIV: return x / y;
+        case AMBER_OP_MIN: return fmin(x, y);
+        default: return fmax(x, y);
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) pop_binop_vec4_kernel(T* __restrict__ tgt, const T* __restrict__ a,
+                                                             const T* __restrict__ b, int b_is_const, double k, int op,
+                                                             const uint8_t* __restrict__ alive, int64_t rows,
+                                                             unsigned long long* n_updated)
+{
+    static_assert(sizeof(T) == 4, "4-byte element types only");
+    unsigned long long cnt = 0;
+    const int64_t groups = rows / 8;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+        const uint2 lv = __ldcs(reinterpret_cast<const uint2*>(alive) + g);
+        const uint4 a0 = __ldcs(reinterpret_cast<const uint4*>(a) + 2 * g);
+        const uint4 a1 = __ldcs(reinterpret_cast<const uint4*>(a) + 2 * g + 1);
+        uint4 b0 = make_uint4(0u, 0u, 0u, 0u), b1 = b0;
+        if (!b_is_const) {
+            b0 = __ldcs(reinterpret_cast<const uint4*>(b) + 2 * g);
+            b1 = __ldcs(reinterpret_cast<const uint4*>(b) + 2 * g + 1);
+        }
+        uint4 o0 = a0, o1 = a1;
+        if (lv.x == 0x01010101u && lv.y == 0x01010101u) {  // all eight rows live (the common case)
+            const uint32_t ai[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const uint32_t bi[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            uint32_t oi[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                T x, y;
+                memcpy(&x, &ai[m], 4);
+                memcpy(&y, &bi[m], 4);
+                const T v = static_cast<T>(binop<T>(op, static_cast<double>(x), b_is_const ? k : static_cast<double>(y)));
+                memcpy(&oi[m], &v, 4);
+            }
+            o0 = make_uint4(oi[0], oi[1], oi[2], oi[3]);
+            o1 = make_uint4(oi[4], oi[5], oi[6], oi[7]);
+            __stcs(reinterpret_cast<uint4*>(tgt) + 2 * g, o0);
+            __stcs(reinterpret_cast<uint4*>(tgt) + 2 * g + 1, o1);
+            cnt += 8;
+        } else {
+            for (int m = 0; m < 8; ++m) {
+                const int64_t r = 8 * g + m;
+                if (!alive[r]) continue;
+                const double y = b_is_const ? k : static_cast<double>(b[r]);
+                tgt[r] = static_cast<T>(binop<T>(op, static_cast<double>(a[r]), y));
+                ++cnt;
+            }
+        }
+    }
+    if (blockIdx.x == 0) {  // tail rows
+        for (int64_t r = groups * 8 + threadIdx.x; r < rows; r += blockDim.x) {
+            if (!alive[r]) continue;
+            const double y = b_is_const ? k : static_cast<double>(b[r]);
+            tgt[r] = static_cast<T>(binop<T>(op, static_cast<double>(a[r]), y));
+            ++cnt;
+        }
+    }
+    unsigned long long vals[1] = {cnt};
+    unsigned long long* const outs[1] = {n_updated};
+    block_sum_atomic<1>(vals, outs);
 }
 
 __global__ void pop_fill_kernel(ColView c, int64_t r0, int64_t r1, double v)
@@ -266,12 +518,17 @@ struct Population {
             cols.push_back(std::move(c));
         }
         reserve(std::max<int64_t>(capacity, 16));
+        AMBER_CUDA(cudaFuncSetAttribute(pop_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kStackBytes)));
+        AMBER_CUDA(cudaFuncSetAttribute(pop_aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kStackBytes)));
     }
 
     ~Population()
     {
         if (rt.stream) cudaStreamSynchronize(rt.stream);
         cols.clear();
+        cnt.reset();
         ids.reset();
         alive.reset();
         rt.destroy();
@@ -321,6 +578,12 @@ struct Population {
         alive.rt = &rt;
         AMBER_CUDA(cudaStreamSynchronize(rt.stream));
         cap = nc;
+    }
+
+    int tiles_grid() const
+    {
+        return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(rows, 1), kTile),
+                                                                        rt.num_sms * 3)));
     }
 
     int grid_for(int64_t n) const
@@ -423,6 +686,7 @@ struct Population {
             int pop = 0, push = 1;
             if (op == AMBER_OP_CONST || op == AMBER_OP_ID || op == AMBER_OP_STEP || op == AMBER_OP_RAND) {
                 pop = 0;
+                if (op == AMBER_OP_ID || op == AMBER_OP_RAND) P.uses_id = 1;
             } else if (op == AMBER_OP_COL) {
                 AMBER_REQUIRE(ins[k].arg >= 0 && ins[k].arg < static_cast<int>(cols.size()), "column index out of range");
             } else if (op >= AMBER_OP_NEG && op <= AMBER_OP_SQRT) {
@@ -439,7 +703,7 @@ struct Population {
             }
             AMBER_REQUIRE(depth >= pop, "expression stack underflow");
             depth += push - pop;
-            AMBER_REQUIRE(depth <= kMaxStack, "expression stack deeper than 16");
+            AMBER_REQUIRE(depth <= kMaxStack, "expression stack deeper than 8");
             P.ins[k] = ins[k];
         }
         AMBER_REQUIRE(n == 0 || depth == 1, "expression must leave exactly one value");
@@ -447,19 +711,67 @@ struct Population {
         return P;
     }
 
-    int64_t update(const std::string& target, const amber_instr* e, int ne, const amber_instr* w, int nw)
+    DevBuf<unsigned long long> cnt;  // persistent update counter (one per population)
+
+    int64_t update(const std::string& target, const amber_instr* e, int ne, const amber_instr* w, int nw, bool want_count)
     {
         const int tgt = col_index(target);
         if (tgt < 0) fail(AMBER_E_UNKNOWN_NAME, "no column " + target);
         const Prog pe = prog(e, ne, false), pw = prog(w, nw, true);
-        DevBuf<unsigned long long> cnt;
-        cnt.allocate(&rt, 1);
-        cnt.zero_async(rt.stream);
-        if (rows) {
-            pop_update_kernel<<<grid_for(rows), 256, 0, rt.stream>>>(pe, pw, views(), tgt, ids.p, alive.p, rows,
-                                                                     static_cast<uint32_t>(step), key, cnt.p);
+        if (!cnt.p) cnt.allocate(&rt, 1);
+        unsigned long long* cnt_p = want_count ? cnt.p : nullptr;
+        if (want_count) cnt.zero_async(rt.stream);
+        const bool fast = pw.n == 0 && pe.n == 3 && pe.ins[0].op == AMBER_OP_COL &&
+                          (pe.ins[1].op == AMBER_OP_CONST || pe.ins[1].op == AMBER_OP_COL) &&
+                          pe.ins[2].op >= AMBER_OP_ADD && pe.ins[2].op <= AMBER_OP_MAX;
+        const Cols C = views();
+        const int bcol = (fast && pe.ins[1].op == AMBER_OP_COL) ? pe.ins[1].arg : -1;
+        const bool same_type = fast && C.c[pe.ins[0].arg].dtype == C.c[tgt].dtype &&
+                               (bcol < 0 || C.c[bcol].dtype == C.c[tgt].dtype);
+        const int gfast = static_cast<int>(std::max<int64_t>(
+            1, std::min<int64_t>(ceil_div(std::max<int64_t>(rows, 1), 256 * kBinRows), rt.num_sms * 8)));
+        if (rows && same_type) {
+            const int isc = bcol < 0;
+            const double kk = pe.ins[1].value;
+            const int op = pe.ins[2].op;
+            void* tp = C.c[tgt].p;
+            const void* ap = C.c[pe.ins[0].arg].p;
+            const void* bp = bcol >= 0 ? C.c[bcol].p : ap;
+            auto go4 = [&](auto tag) {
+                using T = decltype(tag);
+                const int g4 = static_cast<int>(std::max<int64_t>(
+                    1, std::min<int64_t>(ceil_div(std::max<int64_t>(rows / 8, 1), 256), rt.num_sms * 8)));
+                pop_binop_vec4_kernel<T><<<g4, 256, 0, rt.stream>>>(static_cast<T*>(tp), static_cast<const T*>(ap),
+                                                                    static_cast<const T*>(bp), isc, kk, op, alive.p,
+                                                                    rows, cnt_p);
+            };
+            auto go = [&](auto tag) {
+                using T = decltype(tag);
+                pop_binop_typed_kernel<T><<<gfast, 256, 0, rt.stream>>>(static_cast<T*>(tp), static_cast<const T*>(ap),
+                                                                         static_cast<const T*>(bp), isc, kk, op, alive.p,
+                                                                         rows, cnt_p);
+            };
+            switch (C.c[tgt].dtype) {
+                case AMBER_I32: go4(int32_t{}); break;
+                case AMBER_I64: go(int64_t{}); break;
+                case AMBER_F32: go4(float{}); break;
+                case AMBER_F64: go(double{}); break;
+                default: go(uint8_t{}); break;
+            }
+            check_launch("pop_binop_typed_kernel");
+        } else if (rows && fast) {
+            const int g = gfast;
+            pop_binop_kernel<<<g, 256, 0, rt.stream>>>(C.c[tgt], C.c[pe.ins[0].arg],
+                                                       C.c[pe.ins[1].op == AMBER_OP_COL ? pe.ins[1].arg : 0],
+                                                       pe.ins[1].op == AMBER_OP_CONST, pe.ins[1].value, pe.ins[2].op,
+                                                       alive.p, rows, cnt_p);
+            check_launch("pop_binop_kernel");
+        } else if (rows) {
+            pop_update_kernel<<<tiles_grid(), kThreads, kStackBytes, rt.stream>>>(pe, pw, views(), tgt, ids.p, alive.p, rows,
+                                                                     static_cast<uint32_t>(step), key, cnt_p);
             check_launch("pop_update_kernel");
         }
+        if (!want_count) return -1;  // asynchronous: nothing to wait for
         unsigned long long h = 0;
         AMBER_CUDA(cudaMemcpyAsync(&h, cnt.p, 8, cudaMemcpyDeviceToHost, rt.stream));
         AMBER_CUDA(cudaStreamSynchronize(rt.stream));
@@ -470,12 +782,12 @@ struct Population {
     {
         AMBER_REQUIRE(agg >= AMBER_AGG_SUM && agg <= AMBER_AGG_COUNT, "unknown aggregate");
         const Prog pe = prog(e, ne, agg == AMBER_AGG_COUNT), pw = prog(w, nw, true);
-        const int g = grid_for(std::max<int64_t>(rows, 1));
+        const int g = tiles_grid();
         DevBuf<double> part;
         part.allocate(&rt, 4 * g);
         std::vector<double> h(4 * g, 0.0);
         if (rows) {
-            pop_aggregate_kernel<<<g, 256, 0, rt.stream>>>(pe, pw, views(), ids.p, alive.p, rows,
+            pop_aggregate_kernel<<<g, kThreads, kStackBytes, rt.stream>>>(pe, pw, views(), ids.p, alive.p, rows,
                                                            static_cast<uint32_t>(step), key, part.p);
             check_launch("pop_aggregate_kernel");
             AMBER_CUDA(cudaMemcpyAsync(h.data(), part.p, h.size() * 8, cudaMemcpyDeviceToHost, rt.stream));
@@ -572,10 +884,12 @@ void population_size(Population* p, int64_t* live, int64_t* rows)
     if (live) *live = p->live;
     if (rows) *rows = p->rows;
 }
-int64_t population_update(Population* p, const char* t, const amber_instr* e, int ne, const amber_instr* w, int nw)
+int64_t population_update(Population* p, const char* t, const amber_instr* e, int ne, const amber_instr* w, int nw,
+                          bool want_count)
 {
-    return p->update(t, e, ne, w, nw);
+    return p->update(t, e, ne, w, nw, want_count);
 }
+void population_synchronize(Population* p) { AMBER_CUDA(cudaStreamSynchronize(p->rt.stream)); }
 double population_aggregate(Population* p, int agg, const amber_instr* e, int ne, const amber_instr* w, int nw)
 {
     return p->aggregate(agg, e, ne, w, nw);

@@ -106,6 +106,7 @@ class Population:
             specs[i].name = k
             specs[i].dtype = DTYPES[d]
         self.rt = make_runtime(device, stream, torch_alloc)
+        self.stream = self.rt._keep[0]
         h = C.c_void_p()
         check(self.lib.amber_population_create(specs, len(self.names), int(capacity), int(seed),
                                                C.byref(self.rt), C.byref(h)))
@@ -154,12 +155,17 @@ class Population:
             arr[i].value = float(val)
         return arr, len(e.prog)
 
-    def update(self, target: str, expr, where=None) -> int:
+    def update(self, target: str, expr, where=None, count: bool = True):
+        """Returns the number of rows updated; count=False enqueues asynchronously (None)."""
         pe, ne = self._compile(expr)
         pw, nw = self._compile(where)
         k = C.c_int64()
-        check(self.lib.amber_population_update(self.h, target.encode(), pe, ne, pw, nw, C.byref(k)))
-        return k.value
+        check(self.lib.amber_population_update(self.h, target.encode(), pe, ne, pw, nw,
+                                               C.byref(k) if count else None))
+        return k.value if count else None
+
+    def synchronize(self):
+        check(self.lib.amber_population_synchronize(self.h))
 
     def aggregate(self, kind: str, expr=None, where=None) -> float:
         pe, ne = self._compile(expr)

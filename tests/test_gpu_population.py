@@ -93,14 +93,40 @@ def test_random_programs_match_reference(seed):
         for k in SCHEMA:
             assert np.array_equal(p.column(k), r.column(k), equal_nan=True), (it, k)
         for kind in ("sum", "min", "max", "count"):
+            try:
+                h = r.aggregate(kind, col("y").prog, (col("a") > 0).prog)
+            except ValueError:  # empty selection: the device must refuse too
+                with pytest.raises(Exception):
+                    p.aggregate(kind, col("y"), where=col("a") > 0)
+                continue
             g = p.aggregate(kind, col("y"), where=col("a") > 0)
-            h = r.aggregate(kind, col("y").prog, (col("a") > 0).prog)
             assert g == pytest.approx(h, rel=1e-12, abs=1e-9)
     if seed % 2:
         p.compact()
         r.compact()
         assert np.array_equal(p.column("id"), r.column("id"))
         assert np.array_equal(p.column("y"), r.column("y"))
+
+
+@pytest.mark.parametrize("op", ["+", "-", "*", "/", "min", "max"])
+def test_fast_binop_path_matches_reference(op):
+    # [COL a][CONST k | COL b][op] with no filter takes the specialised kernel
+    rng = np.random.default_rng(3)
+    n = 20_011
+    p, r = Population(SCHEMA), PopulationRef(SCHEMA)
+    p.add_agents(n)
+    r.add_agents(n)
+    for k, v in {"x": rng.normal(size=n), "y": rng.normal(size=n) + 3, "a": rng.integers(-9, 9, n)}.items():
+        p.batch_set(k, np.arange(n), v)
+        r.batch_set(k, np.arange(n), v)
+    dead = rng.choice(n, 999, replace=False)
+    p.remove_agents(dead)
+    r.remove_agents(dead.tolist())
+    f = {"+": lambda a, b: a + b, "-": lambda a, b: a - b, "*": lambda a, b: a * b, "/": lambda a, b: a / b,
+         "min": lambda a, b: a.min(b), "max": lambda a, b: a.max(b)}[op]
+    for tgt, e in (("x", f(col("x"), 2.5)), ("y", f(col("y"), col("x"))), ("a", f(col("a"), 3.0))):
+        assert p.update(tgt, e) == r.update(tgt, e.prog)
+        assert np.array_equal(p.column(tgt), r.column(tgt))
 
 
 def test_rand_is_counter_based(orc):
