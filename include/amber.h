@@ -113,7 +113,9 @@ typedef struct {
                              per-receiver counter width for L2 atomics (narrow counters stay
                              L2-resident; an overflow is detected exactly and the step window
                              is replayed with 32-bit counters); -1 = range-partitioned
-                             counting sort through shared memory (single GPU, N <= 2^28) */
+                             counting sort through shared memory (single GPU, N <= 2^28);
+                             -2 = fused range-binned step (single GPU, 1024..4096 ranges of
+                             2^16 agents; otherwise falls back to 4-bit counters) */
 } amber_wealth_params;
 
 /* SIR on G(n, M) (Sec. 5.1.1, Listing 2;

@@ -377,6 +377,11 @@ public:
     bool slot_ready = false;  // slot(t) is zero and the bins work queues are reset
     BinPlan plan;
     BinBuffers bb;
+    // fused range-binned step (wealth_fb.cu)
+    bool fb = false;
+    FbPlan fplan;
+    FbBuffers fbb;
+    int fb_launches = 0;
     // cross-shard exchange (world > 1)
     WealthExchange* xch = nullptr;
     DevBuf<uint32_t> send_ids, recv_ids;
@@ -395,9 +400,10 @@ public:
         // 0: default = 4-bit packed counters with L2 atomics (measured faster)
         const bool want_bins = p.counter_bits == -1 && (r == nullptr || r->world <= 1) &&
                                !(getenv("AMBER_TEST_FORCE_EXCHANGE") && r && r->nccl_unique_id);
+        const bool want_fb = p.counter_bits == -2 && (r == nullptr || r->world <= 1);
         if (p.counter_bits <= 0) p.counter_bits = 4;
         B = p.counter_bits;
-        AMBER_REQUIRE(B == 2 || B == 4 || B == 8 || B == 16 || B == 32, "counter_bits must be 0,2,4,8,16,32");
+        AMBER_REQUIRE(B == 2 || B == 4 || B == 8 || B == 16 || B == 32, "counter_bits must be -2,-1,0,2,4,8,16,32");
         AMBER_REQUIRE(p.amount >= 1, "amount must be >= 1");
         AMBER_REQUIRE(p.w0 >= 0, "w0 must be >= 0");
         AMBER_REQUIRE(!p.exclude_self || n >= 2, "exclude_self needs n_agents >= 2");
@@ -415,10 +421,19 @@ public:
                 n_pad = np;
             }
         }
+        if (want_fb) {
+            const int64_t np = ceil_div(std::max<int64_t>(n_loc, 1), kBinRange) * kBinRange;
+            if (fb_plan(rt, n, lo, np, fplan)) {
+                fb = true;
+                n_pad = np;
+            }
+        }
         fast32 = n < (1ll << 32) - 1 && lo + n_pad < (1ll << 32);
         AMBER_REQUIRE(fast32 || rt.world == 1, "sharded wealth needs ids < 2^32");
         for (auto& b : wb) b.allocate(&rt, n_pad);
-        if (bins) {
+        if (fb) {
+            fb_allocate(rt, fplan, fbb);
+        } else if (bins) {
             bins_allocate(rt, plan, bb);
         } else {
             const int64_t inc_words = ceil_div(n_pad * B, 32) + 4;
@@ -458,6 +473,10 @@ public:
         for (auto& b : bb.data) b.reset();
         for (auto& b : bb.cnt) b.reset();
         bb.queue.reset();
+        for (auto& b : fbb.data) b.reset();
+        for (auto& b : fbb.lo) b.reset();
+        for (auto& b : fbb.hi) b.reset();
+        fbb.queue.reset();
         ring.reset();
         send_ids.reset();
         recv_ids.reset();
@@ -583,7 +602,7 @@ public:
         check_launch("zero_slots_kernel");
     }
 
-    bool small_path() const { return rt.world == 1 && !xch && n <= kSmallMax && !bins && persistent; }
+    bool small_path() const { return rt.world == 1 && !xch && n <= kSmallMax && !bins && !fb && persistent; }
 
     void step(int64_t nsteps) override
     {
@@ -610,6 +629,29 @@ public:
                 cur = other(cur, -1);
                 t += chunk;
                 done += chunk;
+            }
+            return;
+        }
+        if (fb) {
+            WealthStepCfg c{key, n_loc, n_pad, static_cast<unsigned long long>(lo), static_cast<unsigned long long>(n),
+                            p.amount, p.exclude_self, digest_on ? 1 : 0};
+            for (int64_t k = 0; k < nsteps; ++k) {
+                if (win_start >= 0 && t - win_start >= metrics_cap - 4) verify();
+                if (win_start < 0) {
+                    win_start = t;
+                    pinned = cur;
+                }
+                if (!pending) {
+                    zero_slots(t, 2);
+                    fb_launch(rt, prof, fplan, fbb, c, false, static_cast<uint32_t>(t), static_cast<uint32_t>(t),
+                              wb[cur].p, nullptr, nullptr, slot(t), nullptr, fb_launches++);
+                }
+                const int dst = other(cur, pinned == cur ? -1 : pinned);
+                fb_launch(rt, prof, fplan, fbb, c, true, static_cast<uint32_t>(t), static_cast<uint32_t>(t + 1), wb[cur].p,
+                          wb[dst].p, slot(t), slot(t + 1), slot(t + 2), fb_launches++);
+                cur = dst;
+                ++t;
+                pending = true;
             }
             return;
         }
@@ -673,10 +715,20 @@ public:
         pinned = -1;
     }
 
+    void reset_fb()
+    {
+        if (!fb) return;
+        for (auto& b : fbb.lo) b.zero_async(rt.stream);
+        for (auto& b : fbb.hi) b.zero_async(rt.stream);
+        fbb.queue.zero_async(rt.stream);
+        fb_launches = 0;
+    }
+
     void replay(int64_t s0, int64_t s1)
     {
         ++replays;
         slot_ready = false;
+        reset_fb();
         for (auto& b : bb.cnt) b.zero_async(rt.stream);
         cur = pinned;
         for (auto& b : inc) b.zero_async(rt.stream);
@@ -707,7 +759,8 @@ public:
     {
         slot_ready = false;
         if (pending) {
-            inc[t & 1].zero_async(rt.stream);
+            if (fb) reset_fb();
+            else if (inc[t & 1].p) inc[t & 1].zero_async(rt.stream);
             pending = false;
         }
     }
@@ -815,6 +868,16 @@ public:
             m_first = t;
             return true;
         }
+        if (k == "bin_capacity" && fb) {  // test hook: shrink the bins to force drops and the exact replay
+            AMBER_REQUIRE(v >= 8 && v <= 0x7fffffff, "bin_capacity must be >= 8");
+            verify();
+            invalidate_pending();
+            fplan.cap_lo = static_cast<uint32_t>(v) & ~7u;
+            fplan.cap_hi = static_cast<uint32_t>(std::min<int64_t>(v, 8192));
+            fb_allocate(rt, fplan, fbb);
+            fb_launches = 0;
+            return true;
+        }
         if (k == "bin_capacity") {  // test hook: shrink the per-range bins to force the exact replay
             AMBER_REQUIRE(bins, "bin_capacity applies to the range-partitioned scatter only");
             AMBER_REQUIRE(v >= 8 && v <= 0x7fffffff, "bin_capacity must be >= 8");
@@ -841,8 +904,8 @@ public:
             *v = B;
             return true;
         }
-        if (k == "scatter") {  // 0: range-partitioned bins, 1: packed-counter atomics
-            *v = bins ? 0 : 1;
+        if (k == "scatter") {  // 0: range-partitioned bins, 1: packed-counter atomics, 2: fused binned
+            *v = fb ? 2 : (bins ? 0 : 1);
             return true;
         }
         return Model::get_option(key, v);

@@ -48,4 +48,26 @@ struct WealthStepCfg {
 void bins_step(Runtime& rt, Profiler& prof, const BinPlan& plan, BinBuffers& b, const WealthStepCfg& c,
                uint32_t t, const int32_t* w, int32_t* w_out, WealthSlot* slot_t, WealthSlot* slot_next);
 
+// Fused range-binned step (wealth_fb.cu): bins written as 16-byte chunks from
+// per-CTA shared-memory write-combining buffers, consumed by a per-range
+// shared-memory histogram in the next launch.
+struct FbPlan {
+    int K = 0, k0 = 0, k_loc = 0, S = 0, grid = 0;
+    uint32_t cap_lo = 0, cap_hi = 0;
+    size_t smem_apply = 0, smem_prod = 0;
+};
+
+struct FbBuffers {
+    DevBuf<uint16_t> data[2];  // [parity][K][cap_lo + cap_hi]
+    DevBuf<uint32_t> lo[2];    // full-chunk entries per range
+    DevBuf<uint32_t> hi[2];    // tail entries per range
+    DevBuf<int> queue;         // [2] work-queue counters, alternated by launch
+};
+
+bool fb_plan(Runtime& rt, int64_t n, int64_t lo, int64_t n_pad, FbPlan& plan);
+void fb_allocate(Runtime& rt, const FbPlan& plan, FbBuffers& b);
+void fb_launch(Runtime& rt, Profiler& prof, const FbPlan& plan, FbBuffers& b, const WealthStepCfg& c, bool apply,
+               uint32_t t_apply, uint32_t t_prod, const int32_t* w_in, int32_t* w_out, WealthSlot* slot_apply,
+               WealthSlot* slot_prod, WealthSlot* slot_zero, int launch_parity);
+
 }  // namespace amber

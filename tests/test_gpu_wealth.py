@@ -65,6 +65,29 @@ def test_range_partitioned_scatter_replays_exactly(orc):
     assert np.array_equal(m.read_column("wealth"), w)
 
 
+def test_fused_binned_scatter_bit_exact(orc):
+    # needs >= 1024 ranges of 2^16 agents (smaller populations fall back to the counters)
+    n, seed = 70_000_003, 19
+    m = make(n, seed, bits=-2)
+    assert m.get_option("scatter") == 2
+    m.step(1)
+    m.step(1)
+    w, tot, act, _ = orc.wealth_run(np.full(n, 1, np.int32), seed, 0, 2)
+    assert np.array_equal(m.read_column("wealth"), w)
+    assert np.array_equal(m.metrics("total_wealth"), tot) and np.array_equal(m.metrics("active"), act)
+    assert m.get_option("replays") == 0
+
+
+def test_fused_binned_overflow_replays_exactly(orc):
+    n, seed = 70_000_000, 4
+    m = make(n, seed, bits=-2)
+    m.set_option("bin_capacity", 4096)
+    m.step(2)
+    w = orc.wealth_run(np.full(n, 1, np.int32), seed, 0, 2)[0]
+    assert np.array_equal(m.read_column("wealth"), w)
+    assert m.get_option("replays") >= 1
+
+
 def test_atomic_and_binned_scatter_agree(orc):
     n, seed = 200_003, 8
     a = make(n, seed, bits=-1)
