@@ -211,7 +211,8 @@ def bench_wealth(args):
         uid = obj[0]
     n = cfg["n"]
     m = Model("wealth", n, wealth_params(w0=cfg["w0"], amount=cfg["amount"],
-                                         exclude_self=cfg["exclude_self"]), cfg["seed"],
+                                         exclude_self=cfg["exclude_self"],
+                                         counter_bits=args.counter_bits), cfg["seed"],
               device=local, rank=rank, world=world, unique_id=uid)
     _, _, off, n_loc = m.column_info("wealth")
     stream = m.stream
@@ -267,12 +268,16 @@ def bench_wealth(args):
            "d2h_bytes_per_step": int(n_loc * 4 / args.steps + 8 * min(args.steps, 4096))}
 
     hbm, kind = peaks()
-    alg_bytes = 8.0 * n_loc  # wealth column read + written once per step
+    # algorithmic bytes of the method per step: the
+    # column read + written once (8 B/agent) plus one 4-byte increment read and
+    # written per transfer (8 B/transfer; transfers = senders, from `active`)
+    transfers = reds / args.steps
+    alg_bytes = 8.0 * n_loc + 8.0 * transfers
     achieved = alg_bytes / (dom_avg_ms / 1e3) / 1e9 if dom_avg_ms > 0 else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "wealth_traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch", {}).get(dom[0])
     if rank == 0:
         model, ncpu = host_info()
         line = {
@@ -287,21 +292,27 @@ def bench_wealth(args):
             "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": hbm,
                          "peak_kind": kind, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
+                         "alg_bytes_rule": "8 B/agent + 8 B/transfer",
+                         "transfers_per_step": transfers,
                          "avg_launch_ms": dom_avg_ms,
                          "share_of_step": dom[2] / ms if ms > 0 else None},
-            "l2_atomic_roof": {
-                "bound": "l2_atomics", "kernel": dom[0],
-                "achieved_reds_per_s": reds / (ms / 1e3) if ms > 0 else None,
-                "peak_reds_per_s": RED_CEILING, "peak_kind": "measured (tools/red_ceiling.cu, "
-                "profiles/r01_red_ceiling.txt)",
-                "frac": (reds / (ms / 1e3)) / RED_CEILING if ms > 0 else None,
-                "reds_per_step": reds / args.steps},
+            "scatter": {0: "range-partitioned bins", 1: "packed-counter L2 atomics", 2: "fused binned",
+                        3: "segmented bins (shared-memory histograms, no L2 atomics)"}.get(
+                m.get_option("scatter")),
             "kernels": [{"name": a, "launches": b, "total_ms": c} for a, b, c in prof],
             "gpu_launches": launches,
             "e2e": e2e,
             "clocks": cl,
             "host": {"cpu": model, "cpus": ncpu},
         }
+        if m.get_option("scatter") == 1:  # packed counters: one L2 RED per transfer
+            line["l2_atomic_roof"] = {
+                "bound": "l2_atomics", "kernel": dom[0],
+                "achieved_reds_per_s": reds / (ms / 1e3) if ms > 0 else None,
+                "peak_reds_per_s": RED_CEILING, "peak_kind": "measured (tools/red_ceiling.cu, "
+                "profiles/r01_red_ceiling.txt)",
+                "frac": (reds / (ms / 1e3)) / RED_CEILING if ms > 0 else None,
+                "reds_per_step": reds / args.steps}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_wealth(n, cfg["seed"])
         print(json.dumps(line), flush=True)
@@ -429,6 +440,8 @@ def main():
     ap.add_argument("--impl", default="amber", choices=["amber", "reference"])
     ap.add_argument("--workload", default="c4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--counter-bits", type=int, default=0,
+                    help="wealth scatter (amber_wealth_params.counter_bits); 0 = library default")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

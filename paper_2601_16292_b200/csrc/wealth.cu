@@ -382,6 +382,10 @@ public:
     FbPlan fplan;
     FbBuffers fbb;
     int fb_launches = 0;
+    // segmented-bin step (wealth_seg.cu)
+    bool seg = false;
+    SegPlan splan;
+    SegBuffers sgb;
     // cross-shard exchange (world > 1)
     WealthExchange* xch = nullptr;
     DevBuf<uint32_t> send_ids, recv_ids;
@@ -401,9 +405,10 @@ public:
         const bool want_bins = p.counter_bits == -1 && (r == nullptr || r->world <= 1) &&
                                !(getenv("AMBER_TEST_FORCE_EXCHANGE") && r && r->nccl_unique_id);
         const bool want_fb = p.counter_bits == -2 && (r == nullptr || r->world <= 1);
+        const bool want_seg = p.counter_bits == -3 && (r == nullptr || r->world <= 1);
         if (p.counter_bits <= 0) p.counter_bits = 4;
         B = p.counter_bits;
-        AMBER_REQUIRE(B == 2 || B == 4 || B == 8 || B == 16 || B == 32, "counter_bits must be -2,-1,0,2,4,8,16,32");
+        AMBER_REQUIRE(B == 2 || B == 4 || B == 8 || B == 16 || B == 32, "counter_bits must be -3,-2,-1,0,2,4,8,16,32");
         AMBER_REQUIRE(p.amount >= 1, "amount must be >= 1");
         AMBER_REQUIRE(p.w0 >= 0, "w0 must be >= 0");
         AMBER_REQUIRE(!p.exclude_self || n >= 2, "exclude_self needs n_agents >= 2");
@@ -428,10 +433,16 @@ public:
                 n_pad = np;
             }
         }
+        if (want_seg && seg_plan(rt, n, n_loc, splan)) {
+            seg = true;
+            n_pad = splan.R * splan.K;
+        }
         fast32 = n < (1ll << 32) - 1 && lo + n_pad < (1ll << 32);
         AMBER_REQUIRE(fast32 || rt.world == 1, "sharded wealth needs ids < 2^32");
         for (auto& b : wb) b.allocate(&rt, n_pad);
-        if (fb) {
+        if (seg) {
+            seg_allocate(rt, splan, sgb);
+        } else if (fb) {
             fb_allocate(rt, fplan, fbb);
         } else if (bins) {
             bins_allocate(rt, plan, bb);
@@ -477,6 +488,9 @@ public:
         for (auto& b : fbb.lo) b.reset();
         for (auto& b : fbb.hi) b.reset();
         fbb.queue.reset();
+        for (auto* v : {&sgb.data[0], &sgb.data[1], &sgb.cnt[0], &sgb.cnt[1], &sgb.tail[0], &sgb.tail[1],
+                        &sgb.tcnt[0], &sgb.tcnt[1]})
+            v->reset();
         ring.reset();
         send_ids.reset();
         recv_ids.reset();
@@ -602,7 +616,7 @@ public:
         check_launch("zero_slots_kernel");
     }
 
-    bool small_path() const { return rt.world == 1 && !xch && n <= kSmallMax && !bins && !fb && persistent; }
+    bool small_path() const { return rt.world == 1 && !xch && n <= kSmallMax && !bins && !fb && !seg && persistent; }
 
     void step(int64_t nsteps) override
     {
@@ -629,6 +643,29 @@ public:
                 cur = other(cur, -1);
                 t += chunk;
                 done += chunk;
+            }
+            return;
+        }
+        if (seg) {
+            WealthStepCfg c{key, n_loc, n_pad, static_cast<unsigned long long>(lo), static_cast<unsigned long long>(n),
+                            p.amount, p.exclude_self, digest_on ? 1 : 0};
+            for (int64_t k = 0; k < nsteps; ++k) {
+                if (win_start >= 0 && t - win_start >= metrics_cap - 4) verify();
+                if (win_start < 0) {
+                    win_start = t;
+                    pinned = cur;
+                }
+                if (!pending) {
+                    zero_slots(t, 2);
+                    seg_launch(rt, prof, splan, sgb, c, false, static_cast<uint32_t>(t), static_cast<uint32_t>(t),
+                               wb[cur].p, nullptr, nullptr, slot(t), nullptr);
+                }
+                const int dst = other(cur, pinned == cur ? -1 : pinned);
+                seg_launch(rt, prof, splan, sgb, c, true, static_cast<uint32_t>(t), static_cast<uint32_t>(t + 1),
+                           wb[cur].p, wb[dst].p, slot(t), slot(t + 1), slot(t + 2));
+                cur = dst;
+                ++t;
+                pending = true;
             }
             return;
         }
@@ -717,6 +754,7 @@ public:
 
     void reset_fb()
     {
+        if (seg) seg_reset(rt, sgb);
         if (!fb) return;
         for (auto& b : fbb.lo) b.zero_async(rt.stream);
         for (auto& b : fbb.hi) b.zero_async(rt.stream);
@@ -759,7 +797,7 @@ public:
     {
         slot_ready = false;
         if (pending) {
-            if (fb) reset_fb();
+            if (fb || seg) reset_fb();
             else if (inc[t & 1].p) inc[t & 1].zero_async(rt.stream);
             pending = false;
         }
@@ -868,6 +906,15 @@ public:
             m_first = t;
             return true;
         }
+        if (k == "bin_capacity" && seg) {  // test hook: shrink the segments to force drops and the exact replay
+            AMBER_REQUIRE(v >= 4 && v <= 0x7fffffff, "bin_capacity must be >= 4");
+            verify();
+            invalidate_pending();
+            splan.cap = static_cast<uint32_t>(v) & ~3u;
+            splan.tcap = static_cast<uint32_t>(std::min<int64_t>(v, 4096));
+            seg_allocate(rt, splan, sgb);
+            return true;
+        }
         if (k == "bin_capacity" && fb) {  // test hook: shrink the bins to force drops and the exact replay
             AMBER_REQUIRE(v >= 8 && v <= 0x7fffffff, "bin_capacity must be >= 8");
             verify();
@@ -904,8 +951,8 @@ public:
             *v = B;
             return true;
         }
-        if (k == "scatter") {  // 0: range-partitioned bins, 1: packed-counter atomics, 2: fused binned
-            *v = fb ? 2 : (bins ? 0 : 1);
+        if (k == "scatter") {  // 0: range-partitioned bins, 1: packed-counter atomics, 2: fused binned, 3: segmented bins
+            *v = seg ? 3 : (fb ? 2 : (bins ? 0 : 1));
             return true;
         }
         return Model::get_option(key, v);

@@ -64,6 +64,38 @@ struct FbBuffers {
     DevBuf<int> queue;         // [2] work-queue counters, alternated by launch
 };
 
+// Segmented-bin step (wealth_seg.cu): ranges of R agents (R a multiple of
+// 8192, <= 344064, about two ranges per SM), a 4-bit shared-memory histogram
+// per range, and per-(destination, producer) bin segments written from a
+// per-chunk shared-memory staging area, so no global atomic per transfer.
+struct SegPlan {
+    int64_t R = 0;              // agents per range
+    int K = 0;                  // ranges (= bins)
+    int S = 0;                  // staging slots per destination per chunk
+    int NT = 1024;              // threads per CTA (1024: one CTA per SM; 512: two)
+    int grid = 0;               // persistent CTAs
+    uint32_t cap = 0;           // entries per (destination, producer) segment
+    uint32_t tcap = 0;          // overflow ("tail") entries per destination
+    unsigned long long magic = 0;  // d = umulhi(r, magic) >> msh == r / R for r < 2^31
+    int msh = 0;
+    size_t smem = 0;
+};
+
+struct SegBuffers {
+    DevBuf<uint32_t> data[2];   // [parity][K dest][K producer][cap]
+    DevBuf<uint32_t> cnt[2];    // [parity][K dest][K producer] entries produced
+    DevBuf<uint32_t> tail[2];   // [parity][K dest][tcap]
+    DevBuf<uint32_t> tcnt[2];   // [parity][K dest]
+};
+
+bool seg_plan(Runtime& rt, int64_t n, int64_t n_loc, SegPlan& plan);
+void seg_allocate(Runtime& rt, const SegPlan& plan, SegBuffers& b);
+void seg_reset(Runtime& rt, SegBuffers& b);
+// apply == false: produce step t_prod's bins from w_in only ("prime").
+void seg_launch(Runtime& rt, Profiler& prof, const SegPlan& plan, SegBuffers& b, const WealthStepCfg& c, bool apply,
+                uint32_t t_apply, uint32_t t_prod, const int32_t* w_in, int32_t* w_out, WealthSlot* slot_apply,
+                WealthSlot* slot_prod, WealthSlot* slot_zero);
+
 bool fb_plan(Runtime& rt, int64_t n, int64_t lo, int64_t n_pad, FbPlan& plan);
 void fb_allocate(Runtime& rt, const FbPlan& plan, FbBuffers& b);
 void fb_launch(Runtime& rt, Profiler& prof, const FbPlan& plan, FbBuffers& b, const WealthStepCfg& c, bool apply,

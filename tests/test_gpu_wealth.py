@@ -202,3 +202,55 @@ def test_errors_are_reported():
         m.read_column("nope")
     with pytest.raises(AmberError):
         m.read_column("wealth", np.zeros(3, np.int32))
+
+
+@pytest.mark.parametrize("n,steps", [(40_000, 25), (5_000_003, 6)])
+def test_segmented_bins_bit_exact(orc, n, steps):
+    # wealth_seg.cu: per-(destination, producer) bin segments + 4-bit shared-memory histograms
+    m = make(n, 31, bits=-3)
+    assert m.get_option("scatter") == 3
+    m.set_option("digest", 1)
+    m.step(1)
+    m.step(steps - 1)
+    w, tot, act, dig = orc.wealth_run(np.full(n, 1, np.int32), 31, 0, steps, digests=True)
+    assert np.array_equal(m.read_column("wealth"), w)
+    assert np.array_equal(m.metrics("total_wealth"), tot) and np.array_equal(m.metrics("active"), act)
+    assert np.array_equal(m.metrics("digest"), dig.astype(np.uint64))
+    assert m.get_option("replays") == 0
+
+
+@pytest.mark.parametrize("kw", [dict(exclude_self=1), dict(w0=3, amount=2)])
+def test_segmented_bins_variants(orc, kw):
+    n, seed = 1_000_001, 12
+    m = make(n, seed, bits=-3, **kw)
+    assert m.get_option("scatter") == 3
+    m.step(5)
+    w0 = kw.get("w0", 1)
+    w = orc.wealth_run(np.full(n, w0, np.int32), seed, 0, 5, amount=kw.get("amount", 1),
+                       exclude_self=kw.get("exclude_self", 0))[0]
+    assert np.array_equal(m.read_column("wealth"), w)
+    assert m.get_option("replays") == 0
+
+
+def test_segmented_bins_overflow_replays_exactly(orc):
+    n, seed = 2_000_000, 6
+    m = make(n, seed, bits=-3)
+    m.set_option("bin_capacity", 8)  # segments and tails far too small: entries dropped every step
+    m.step(3)
+    w = orc.wealth_run(np.full(n, 1, np.int32), seed, 0, 3)[0]
+    assert np.array_equal(m.read_column("wealth"), w)
+    assert m.get_option("replays") >= 1
+    m.step(2)
+    w = orc.wealth_run(w, seed, 3, 2)[0]
+    assert np.array_equal(m.read_column("wealth"), w)
+
+
+def test_segmented_bins_full_size_first_steps(orc):
+    # BASELINE config 4 size (N = 1e8) in the launch configuration bench.py times
+    cfg = C4_WEALTH_SCALE
+    m = make(cfg["n"], cfg["seed"], bits=-3)
+    assert m.get_option("scatter") == 3
+    m.step(2)
+    w = orc.wealth_run(np.full(cfg["n"], 1, np.int32), cfg["seed"], 0, 2)[0]
+    assert np.array_equal(m.read_column("wealth"), w)
+    assert m.get_option("replays") == 0
