@@ -23,6 +23,10 @@ import os
 import statistics
 import subprocess
 import sys
+
+# load every kernel at context creation: lazy module loading inside a timed
+# region would be counted as step time
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))

@@ -262,177 +262,329 @@ struct SirStepArgs {
     const int32_t* row_ptr;  // n + 1 (replicate-local offsets)
     const int32_t* col;
     uint8_t* x[2];           // ping-pong state (n_pad, padding = kPad)
+    uint32_t* ib[2];         // ping-pong I bitmaps (n_pad / 32 words): bit i = [x_i == I]
+    uint32_t* sb[2];         // ping-pong S bitmaps
     int64_t n, n_pad;
     unsigned long long t_beta, t_gamma;
     uint32_t t0;             // first step index
     int64_t n_steps;         // steps in this launch (persistent) or 1
-    int cur;                 // index of the buffer holding the state at t0
+    int cur;                 // index of the buffers holding the state at t0
+    int prev_ok;             // ring slot t0 - 1 holds the counts of the state at t0
     SirSlot* ring;
     int64_t ring_cap;
     int digest;
+    uint32_t* queue;         // persistent launch: [2 parities][2 phases][kRegions] chunk counters
+    int grab;                // chunks per queue grab
 };
 
-// One step, warp-cooperative pull.  A warp owns 32 consecutive agents
-// (lane = agent).  Their CSR rows are contiguous, so the warp walks the
-// concatenated arc range 32 arcs at a time (coalesced col loads, 32 independent
-// neighbour-state gathers in flight); each lane finds the owner of its arc by a
-// 5-step shuffle search over the row starts, draws the pair-keyed Bernoulli
-// (S3) for S-owner / I-neighbour arcs, and ORs a hit into the owner's bit of a
-// per-warp mask.  Owners already infected skip further draws (early exit is
-// legal because the result is the OR over all S-I edges).
-__device__ __forceinline__ void sir_step_body(const SirStepArgs& a, const uint8_t* __restrict__ x, uint8_t* __restrict__ y,
-                                              uint32_t t, unsigned long long (&cnt)[4], uint32_t* wmask)
+constexpr int kRegions = 16;
+
+// Warp chunks (32 agents each) of the padded population.  Persistent launch
+// (queue != nullptr): dynamic -- the chunk range is split into kRegions
+// contiguous regions, warp w draws batches of `grab` chunks from region
+// w % kRegions with one atomic (per-region counters, so the atomics spread);
+// the pull and push walks cost very different amounts per chunk, and static
+// striding left most warps waiting at the step barrier (r01 ncu: 43% of stall
+// samples).  Per-step launch: one chunk per warp, the block scheduler balances.
+template <class F>
+__device__ __forceinline__ void for_chunks(const SirStepArgs& a, uint32_t* q, F&& f)
 {
     const int lane = threadIdx.x & 31;
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    const int32_t arcs_end = a.row_ptr[a.n];
-    for (int64_t a0 = gw * 32; a0 < a.n_pad; a0 += nw * 32) {
-        const int64_t i = a0 + lane;
-        const bool real = i < a.n;
-        const uint8_t st = x[i];
-        const int32_t rb = real ? a.row_ptr[i] : arcs_end;
-        const int32_t we = __shfl_sync(0xffffffffu, real ? a.row_ptr[i + 1] : arcs_end, 31);
-        const int32_t wb = __shfl_sync(0xffffffffu, rb, 0);
-        const bool is_s = st == kS;
-        const unsigned s_lanes = __ballot_sync(0xffffffffu, is_s);
-        if (lane == 0) *wmask = 0u;
-        __syncwarp();
-        if (s_lanes) {
-            for (int32_t e0 = wb; e0 < we; e0 += 32) {
-                const int32_t e = e0 + lane;
-                // owner = largest lane L with rb_L <= e (rows are contiguous)
-                int L = 0;
+    const int64_t nchunks = a.n_pad >> 5;
+    if (!q || nw < kRegions) {
+        for (int64_t c = gw; c < nchunks; c += nw) f(c << 5);
+        return;
+    }
+    const int r = static_cast<int>(gw % kRegions);
+    const int64_t lo = nchunks * r / kRegions, hi = nchunks * (r + 1) / kRegions;
+    for (;;) {
+        uint32_t c0 = 0;
+        if (lane == 0) c0 = atomicAdd(q + r, static_cast<uint32_t>(a.grab));
+        c0 = __shfl_sync(0xffffffffu, c0, 0);
+        if (lo + c0 >= hi) break;
+        const int64_t e = lo + c0 + a.grab < hi ? lo + c0 + a.grab : hi;
+        for (int64_t c = lo + c0; c < e; ++c) f(c << 5);
+    }
+}
+
+__device__ __forceinline__ uint32_t* queue_of(const SirStepArgs& a, uint32_t t, int phase)
+{
+    return a.queue ? a.queue + ((t & 1u) * 2 + phase) * kRegions : nullptr;
+}
+
+// Plain (coherent) load: the bitmaps are rewritten by earlier steps of the same
+// persistent launch, so the read-only (.nc) path must not be used.
+// The lookups are random over the whole bitmap (12.5 MB at N = 1e8), so they
+// carry an L2 evict_last hint, and the streamed CSR columns an evict-first one,
+// to keep the bitmaps L2-resident.
+__device__ __forceinline__ bool bit_of(const uint32_t* bits, uint32_t j)
+{
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    uint32_t w;
+    asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(w) : "l"(bits + (j >> 5)), "l"(pol));
+    return (w >> (j & 31u)) & 1u;
+}
+
+__device__ __forceinline__ bool recovers(const SirStepArgs& a, int64_t i, uint32_t t)
+{
+    const uint4 rec = stream_block(a.key, TAG_SIR_REC, static_cast<unsigned long long>(i >> 2), t);  // R4
+    const uint32_t k = static_cast<uint32_t>(i & 3);
+    const uint32_t d = k == 0 ? rec.x : (k == 1 ? rec.y : (k == 2 ? rec.z : rec.w));
+    return static_cast<unsigned long long>(d) < a.t_gamma;
+}
+
+// Warp-cooperative walk over the concatenated CSR rows of the lanes in `own`
+// (lane L owns row [rb_L, re_L)).  Position q of the concatenation -> owner
+// lane by a 5-step shuffle search over the inclusive prefix of the row
+// lengths.  kU batches of 32 arcs are in flight per iteration: all their
+// column loads are issued, then all the neighbour tests, so each warp keeps
+// kU x 32 independent gathers outstanding (the walk is latency-bound on the
+// col -> bitmap chain at large N).  test(j, e, owner) returns true for an arc
+// that sets the owner's bit; owners whose bit is set skip their remaining arcs
+// (early exit).  Returns the mask of owners with a set bit.  All 32 lanes call it.
+template <int kU, class T>
+__device__ __forceinline__ uint32_t walk_rows(const int32_t* __restrict__ col, uint32_t own, int32_t rb, int32_t re,
+                                              T&& test)
+{
+    const int lane = threadIdx.x & 31;
+    const int32_t len = ((own >> lane) & 1u) ? re - rb : 0;
+    int32_t incl = len;
 #pragma unroll
-                for (int step = 16; step > 0; step >>= 1) {
-                    const int cand = L + step;
-                    const int32_t rbc = __shfl_sync(0xffffffffu, rb, cand & 31);
-                    if (cand < 32 && rbc <= e) L = cand;
-                }
-                const unsigned done = *wmask;
-                if (e < we && ((s_lanes >> L) & 1u) && !((done >> L) & 1u)) {
-                    const uint32_t j = static_cast<uint32_t>(__ldg(a.col + e));
-                    if (x[j] == kI) {
-                        const uint32_t s = static_cast<uint32_t>(a0 + L);
-                        const uint4 w = philox(make_uint4(min(s, j), max(s, j), t, TAG_SIR_TX), a.key);
-                        if (static_cast<unsigned long long>(w.x) < a.t_beta) atomicOr(wmask, 1u << L);
-                    }
-                }
-                __syncwarp();
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const int32_t start = rb - (incl - len);  // arc index of concatenation position q is start_L + q
+    uint32_t hit = 0;
+    for (int32_t q0 = 0; q0 < total; q0 += 32 * kU) {
+        int Ls[kU];
+        int32_t es[kU];
+        bool live[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int32_t q = q0 + 32 * u + lane;
+            int L = 0;  // number of lanes with incl <= q = the owner of position q
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+                const int32_t v = __shfl_sync(0xffffffffu, incl, (L + st - 1) & 31);
+                if (v <= q) L += st;
             }
+            L &= 31;
+            Ls[u] = L;
+            es[u] = __shfl_sync(0xffffffffu, start, L) + q;
+            live[u] = q < total && !((hit >> L) & 1u);
         }
-        uint8_t o = st;
-        if (is_s) {
-            if ((*wmask >> lane) & 1u) o = kI;
-        } else if (st == kI) {
-            const uint4 rec = stream_block(a.key, TAG_SIR_REC, static_cast<unsigned long long>(i >> 2), t);  // R4
-            const uint32_t k = static_cast<uint32_t>(i & 3);
-            const uint32_t d = k == 0 ? rec.x : (k == 1 ? rec.y : (k == 2 ? rec.z : rec.w));
-            if (static_cast<unsigned long long>(d) < a.t_gamma) o = kR;
-        }
-        y[i] = o;
-        if (real) {
-            cnt[o] += 1;
+        uint32_t js[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) js[u] = live[u] ? static_cast<uint32_t>(__ldcs(col + es[u])) : 0u;
+        uint32_t add = 0;
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (live[u] && test(js[u], es[u], Ls[u])) add |= 1u << Ls[u];
+        hit |= __reduce_or_sync(0xffffffffu, add);
+        if ((hit & own) == own) break;  // every owner decided
+    }
+    return hit;
+}
+
+// Pull step for the 32 agents of warp chunk a0 (lane = agent): susceptible
+// owners walk their rows; an arc transmits iff the neighbour is I (bitmap,
+// L2-resident) and the pair-keyed Bernoulli (S3) fires.  Writes the next state
+// and the next bitmaps; returns the new state of the lane's agent.
+__device__ __forceinline__ uint8_t sir_pull_chunk(const SirStepArgs& a, int64_t a0, const uint8_t* __restrict__ x,
+                                                  uint8_t* __restrict__ y, const uint32_t* __restrict__ ib,
+                                                  uint32_t* __restrict__ ib_next, uint32_t* __restrict__ sb_next,
+                                                  uint32_t t)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t i = a0 + lane;
+    const bool real = i < a.n;
+    const uint8_t st = x[i];
+    const bool is_s = st == kS;
+    const uint32_t s_mask = __ballot_sync(0xffffffffu, is_s);
+    uint32_t hit = 0;
+    if (s_mask) {
+        const int32_t rb = real ? a.row_ptr[i] : 0, re = real ? a.row_ptr[i + 1] : 0;
+        hit = walk_rows<4>(a.col, s_mask, rb, re, [&](uint32_t j, int32_t, int L) {
+            if (!bit_of(ib, j)) return false;
+            const uint32_t s = static_cast<uint32_t>(a0 + L);
+            const uint4 w = philox(make_uint4(min(s, j), max(s, j), t, TAG_SIR_TX), a.key);
+            return static_cast<unsigned long long>(w.x) < a.t_beta;
+        });
+    }
+    uint8_t o = st;
+    if (is_s) {
+        if ((hit >> lane) & 1u) o = kI;
+    } else if (st == kI) {
+        if (recovers(a, i, t)) o = kR;
+    }
+    y[i] = o;
+    const uint32_t ibw = __ballot_sync(0xffffffffu, o == kI), sbw = __ballot_sync(0xffffffffu, o == kS);
+    if (lane == 0) {
+        ib_next[a0 >> 5] = ibw;
+        sb_next[a0 >> 5] = sbw;
+    }
+    return o;
+}
+
+__device__ __forceinline__ void sir_pull_body(const SirStepArgs& a, int c, uint32_t t, unsigned long long (&cnt)[4])
+{
+    const int lane = threadIdx.x & 31;
+    for_chunks(a, queue_of(a, t, 0), [&](int64_t a0) {
+        const uint8_t o = sir_pull_chunk(a, a0, a.x[c], a.x[c ^ 1], a.ib[c], a.ib[c ^ 1], a.sb[c ^ 1], t);
+        const int64_t i = a0 + lane;
+        if (i < a.n) {
+            cnt[0] += o == kS;
+            cnt[1] += o == kI;
+            cnt[2] += o == kR;
             if (a.digest) cnt[3] += digest_term(static_cast<unsigned long long>(i), o);
         }
-        __syncwarp();
-    }
+    });
 }
 
 __global__ void __launch_bounds__(256) sir_step_kernel(const SirStepArgs a)
 {
-    __shared__ uint32_t wmask[8];
     const uint32_t t = a.t0;
     unsigned long long cnt[4] = {0, 0, 0, 0};
-    sir_step_body(a, a.x[a.cur], a.x[a.cur ^ 1], t, cnt, &wmask[threadIdx.x >> 5]);
+    sir_pull_body(a, a.cur, t, cnt);
     SirSlot* sl = a.ring + (t % a.ring_cap);
     unsigned long long* const outs[4] = {&sl->S, &sl->I, &sl->R, a.digest ? &sl->digest : nullptr};
     block_sum_atomic<4>(cnt, outs);
 }
 
-// All n_steps steps in one cooperative launch (grid barrier between steps).
-// Push step (direction-optimizing, persistent kernel only).  x = state t,
-// y = the other ping-pong buffer, which holds state t-1 because the previous
-// step of this launch wrote it.  Every agent that is S at t was S at t-1, so y
-// already reads S there; only I/R agents and newly infected agents change.
-// All updates of y are 32-bit atomics on the byte's word (exact new-infection
-// count from the returned old value; duplicates from several infected
-// neighbours are harmless).  Result identical to pull by S3.
-__device__ __forceinline__ void sir_push_body(const SirStepArgs& a, const uint8_t* __restrict__ x, uint8_t* y, uint32_t t,
-                                              long long (&d)[3])
+// Bitmaps of a state buffer (after creation or an external column write).
+__global__ void sir_bits_kernel(const uint8_t* __restrict__ x, int64_t n_pad, uint32_t* __restrict__ ib,
+                                uint32_t* __restrict__ sb)
 {
-    uint32_t* yw = reinterpret_cast<uint32_t*>(y);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint8_t st = x[i];
-        if (st == kS || st == kPad) continue;
-        const uint32_t sh = static_cast<uint32_t>(i & 3) * 8;
-        const uint8_t old = y[i];  // state t-1 of agent i: nobody else writes this byte in this step
-        uint8_t nw = kR;
-        if (st == kI) {
-            const uint4 rec = stream_block(a.key, TAG_SIR_REC, static_cast<unsigned long long>(i >> 2), t);
-            const uint32_t k = static_cast<uint32_t>(i & 3);
-            const uint32_t dr = k == 0 ? rec.x : (k == 1 ? rec.y : (k == 2 ? rec.z : rec.w));
-            nw = (static_cast<unsigned long long>(dr) < a.t_gamma) ? kR : kI;
-            if (nw == kR) {
-                d[1] -= 1;
-                d[2] += 1;
-            }
-            const int32_t b = a.row_ptr[i], e = a.row_ptr[i + 1];
-            const uint32_t ii = static_cast<uint32_t>(i);
-            for (int32_t p = b; p < e; ++p) {
-                const uint32_t j = static_cast<uint32_t>(__ldg(a.col + p));
-                if (x[j] != kS) continue;
-                const uint4 w = philox(make_uint4(min(ii, j), max(ii, j), t, TAG_SIR_TX), a.key);
-                if (static_cast<unsigned long long>(w.x) < a.t_beta) {
-                    const uint32_t sj = (j & 3u) * 8u;
-                    const uint32_t prev = atomicOr(yw + (j >> 2), 1u << sj);
-                    if (((prev >> sj) & 0xFFu) == kS) {
-                        d[0] -= 1;
-                        d[1] += 1;
-                    }
-                }
-            }
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t a0 = gw * 32; a0 < n_pad; a0 += nw * 32) {
+        const uint8_t st = x[a0 + lane];
+        const uint32_t iw = __ballot_sync(0xffffffffu, st == kI), sw = __ballot_sync(0xffffffffu, st == kS);
+        if (lane == 0) {
+            ib[a0 >> 5] = iw;
+            sb[a0 >> 5] = sw;
         }
-        if (nw != old) atomicAdd(yw + (i >> 2), static_cast<uint32_t>(nw - old) << sh);
     }
 }
 
+// Push step (infected < susceptible).  Invariant of the back buffers
+// (x, ib, sb)[c ^ 1]: they hold a state B from which the current state is
+// reached by S -> I -> R moves only (the previous step's input; a copy of the
+// current state after creation or a column write), so every agent that is S
+// now is S in B.  One pass, no copy:
+//  * owners of non-S agents write their new state into y (bytes of B) as an
+//    atomic delta on the byte's word, and XOR-correct their bits of the next
+//    I bitmap (B's bits -> survivors) and clear their S bits -- all on bits
+//    and bytes no pusher touches (pushers only touch agents that are S now);
+//  * every agent infected now pushes along its row to neighbours that are S
+//    now (S bitmap) with the same pair-keyed draw as pull (S3); a transmitting
+//    arc sets the neighbour's next I bit with atomicOr, whose old word makes
+//    the new-infection count exact when several pushers hit the same agent;
+//    the first one also clears its S bit and sets its byte to I.
+__device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint32_t t, long long& rec, long long& inf,
+                                              unsigned long long& dig)
+{
+    const int lane = threadIdx.x & 31;
+    const uint8_t* __restrict__ x = a.x[c];
+    const uint32_t* __restrict__ sb = a.sb[c];
+    uint32_t* ib_next = a.ib[c ^ 1];
+    uint32_t* sb_next = a.sb[c ^ 1];
+    uint8_t* y = a.x[c ^ 1];
+    uint32_t* yw = reinterpret_cast<uint32_t*>(y);
+    for_chunks(a, queue_of(a, t, 1), [&](int64_t a0) {
+        const int64_t i = a0 + lane;
+        const int64_t w = a0 >> 5;
+        const uint8_t st = x[i];
+        const bool real = i < a.n;
+        const uint32_t non_s = __ballot_sync(0xffffffffu, real && st != kS);
+        if (a.digest && real && st == kS) dig += digest_term(static_cast<unsigned long long>(i), kS);
+        if (!non_s) return;
+        const bool is_i = st == kI;
+        const uint32_t own = __ballot_sync(0xffffffffu, is_i);
+        // owners: recoveries and the new state of every non-S agent
+        uint8_t nw = st;
+        if (is_i && recovers(a, i, t)) {
+            nw = kR;
+            ++rec;
+        }
+        if ((non_s >> lane) & 1u) {
+            const uint8_t old = y[i];
+            if (nw != old) atomicAdd(yw + (i >> 2), static_cast<uint32_t>(nw - old) << ((i & 3) * 8));
+            if (a.digest) dig += digest_term(static_cast<unsigned long long>(i), nw);
+        }
+        const uint32_t surv = __ballot_sync(0xffffffffu, nw == kI);
+        if (lane == 0) {
+            const uint32_t flip = (ib_next[w] ^ surv) & non_s;
+            if (flip) atomicXor(ib_next + w, flip);
+            if (sb_next[w] & non_s) atomicAnd(sb_next + w, ~non_s);
+        }
+        // pushers
+        if (!own) return;
+        const int32_t rb = is_i ? a.row_ptr[i] : 0, re = is_i ? a.row_ptr[i + 1] : 0;
+        walk_rows<4>(a.col, own, rb, re, [&](uint32_t j, int32_t, int L) {
+            if (!bit_of(sb, j)) return false;
+            const uint32_t s = static_cast<uint32_t>(a0 + L);
+            const uint4 wd = philox(make_uint4(min(s, j), max(s, j), t, TAG_SIR_TX), a.key);
+            if (static_cast<unsigned long long>(wd.x) < a.t_beta) {
+                const uint32_t bit = 1u << (j & 31u);
+                const uint32_t prev = atomicOr(ib_next + (j >> 5), bit);
+                if (!(prev & bit)) {
+                    atomicAnd(sb_next + (j >> 5), ~bit);
+                    atomicOr(yw + (j >> 2), static_cast<uint32_t>(kI) << ((j & 3u) * 8u));
+                    ++inf;
+                    if (a.digest) dig += digest_term(j, kI) - digest_term(j, kS);
+                }
+            }
+            return false;  // an infected agent tries every susceptible neighbour
+        });
+    });
+}
+
 // All n_steps steps in one cooperative launch (grid barrier between steps).
-// Step k > 0 pushes from the infected agents when they are fewer than the
-// susceptible ones (counts of the previous step, read from its ring slot after
-// the barrier, so every block takes the same decision); otherwise it pulls.
-__global__ void __launch_bounds__(256) sir_persistent_kernel(const SirStepArgs a)
+// Direction-optimizing: step k pushes from the infected agents when they are
+// fewer than the susceptible ones (counts of the previous step from its ring
+// slot, so every block takes the same decision), otherwise it pulls.  Both
+// directions give identical results (S3); the tests check it.
+__global__ void __launch_bounds__(256, 3) sir_persistent_kernel(const SirStepArgs a)
 {
     cg::grid_group grid = cg::this_grid();
-    __shared__ uint32_t wmask[8];
     int cur = a.cur;
     for (int64_t k = 0; k < a.n_steps; ++k) {
         const uint32_t t = a.t0 + static_cast<uint32_t>(k);
         SirSlot* sl = a.ring + (t % a.ring_cap);
+        // the counters of step t+1 were last used by step t-1 (finished at the previous barrier)
+        if (a.queue && blockIdx.x == 0 && threadIdx.x < 2 * kRegions) a.queue[((t + 1) & 1u) * 2 * kRegions + threadIdx.x] = 0u;
         bool push = false;
         unsigned long long prev_s = 0, prev_i = 0, prev_r = 0;
-        if (k > 0 && !a.digest) {
-            const SirSlot* pv = a.ring + ((t - 1) % a.ring_cap);
+        if (k > 0 || a.prev_ok) {
+            const SirSlot* pv = a.ring + ((t + a.ring_cap - 1) % a.ring_cap);
             prev_s = pv->S;
             prev_i = pv->I;
             prev_r = pv->R;
             push = prev_i < prev_s;
         }
         if (push) {
-            long long d[3] = {0, 0, 0};
-            sir_push_body(a, a.x[cur], a.x[cur ^ 1], t, d);
-            unsigned long long v[3] = {static_cast<unsigned long long>(d[0]), static_cast<unsigned long long>(d[1]),
-                                       static_cast<unsigned long long>(d[2])};
+            long long rec = 0, inf = 0;
+            unsigned long long dig = 0;
+            sir_push_body(a, cur, t, rec, inf, dig);
+            unsigned long long v[4] = {static_cast<unsigned long long>(-inf), static_cast<unsigned long long>(inf - rec),
+                                       static_cast<unsigned long long>(rec), dig};
             if (blockIdx.x == 0 && threadIdx.x == 0) {
                 v[0] += prev_s;
                 v[1] += prev_i;
                 v[2] += prev_r;
             }
-            unsigned long long* const outs[3] = {&sl->S, &sl->I, &sl->R};
-            block_sum_atomic<3>(v, outs);
+            unsigned long long* const outs[4] = {&sl->S, &sl->I, &sl->R, a.digest ? &sl->digest : nullptr};
+            block_sum_atomic<4>(v, outs);
         } else {
             unsigned long long cnt[4] = {0, 0, 0, 0};
-            sir_step_body(a, a.x[cur], a.x[cur ^ 1], t, cnt, &wmask[threadIdx.x >> 5]);
+            sir_pull_body(a, cur, t, cnt);
             unsigned long long* const outs[4] = {&sl->S, &sl->I, &sl->R, a.digest ? &sl->digest : nullptr};
             block_sum_atomic<4>(cnt, outs);
         }
@@ -457,9 +609,12 @@ public:
     PhiloxKey key{};
     Graphs g;
     DevBuf<uint8_t> x[2];
+    DevBuf<uint32_t> ib[2], sb[2];  // I / S bitmaps of the two state buffers
+    DevBuf<uint32_t> queue;         // persistent launch: chunk counters
     int cur = 0;
     DevBuf<SirSlot> ring;
     int64_t m_first = 0;
+    bool prev_ok = false;  // ring slot t-1 holds the counts of the current state
 
     SirModel(int64_t n_, const amber_sir_params& p_, uint64_t seed_, const amber_runtime* r)
     {
@@ -478,10 +633,38 @@ public:
         std::vector<unsigned long long> seeds{seed};
         build_graphs(rt, seeds, n, m_draws, g);
         for (auto& b : x) b.allocate(&rt, n_pad);
+        for (int c = 0; c < 2; ++c) {
+            ib[c].allocate(&rt, n_pad / 32);
+            sb[c].allocate(&rt, n_pad / 32);
+        }
         build_init_state(rt, seeds, n, n_pad, k_inf, x[0].p);
+        build_bits();
+        queue.allocate(&rt, 4 * kRegions);
         ring.allocate(&rt, metrics_cap);
         ring.zero_async(rt.stream);
+        seed_counts(static_cast<unsigned long long>(n - k_inf), static_cast<unsigned long long>(k_inf), 0ull);
         AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    }
+
+    // Bitmaps of the current state; the back buffers become a copy of it (the
+    // push step's invariant: every agent S now is S in the back state).
+    void build_bits()
+    {
+        sir_bits_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(x[cur].p, n_pad, ib[cur].p, sb[cur].p);
+        check_launch("sir_bits_kernel");
+        AMBER_CUDA(cudaMemcpyAsync(x[cur ^ 1].p, x[cur].p, n_pad, cudaMemcpyDeviceToDevice, rt.stream));
+        AMBER_CUDA(cudaMemcpyAsync(ib[cur ^ 1].p, ib[cur].p, n_pad / 8, cudaMemcpyDeviceToDevice, rt.stream));
+        AMBER_CUDA(cudaMemcpyAsync(sb[cur ^ 1].p, sb[cur].p, n_pad / 8, cudaMemcpyDeviceToDevice, rt.stream));
+    }
+
+    // counts of the current state into ring slot t-1 (direction choice of the next step)
+    void seed_counts(unsigned long long S, unsigned long long I, unsigned long long R)
+    {
+        const SirSlot v{S, I, R, 0};
+        AMBER_CUDA(cudaMemcpyAsync(ring.p + (t + metrics_cap - 1) % metrics_cap, &v, sizeof(v),
+                                   cudaMemcpyHostToDevice, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        prev_ok = true;
     }
 
     ~SirModel() override
@@ -490,7 +673,12 @@ public:
         g.row_ptr.reset();
         g.col.reset();
         for (auto& b : x) b.reset();
+        for (int c = 0; c < 2; ++c) {
+            ib[c].reset();
+            sb[c].reset();
+        }
         ring.reset();
+        queue.reset();
         rt.destroy();
     }
 
@@ -502,6 +690,11 @@ public:
         a.col = g.col.p;
         a.x[0] = x[0].p;
         a.x[1] = x[1].p;
+        for (int c = 0; c < 2; ++c) {
+            a.ib[c] = ib[c].p;
+            a.sb[c] = sb[c].p;
+        }
+        a.prev_ok = prev_ok ? 1 : 0;
         a.n = n;
         a.n_pad = n_pad;
         a.t_beta = bernoulli_threshold_host(p.beta);
@@ -521,7 +714,8 @@ public:
         AMBER_REQUIRE(t + nsteps < (1ll << 32), "step index would exceed 2^32");
         int64_t done = 0;
         while (done < nsteps) {
-            const int64_t chunk = std::min<int64_t>(nsteps - done, metrics_cap);
+            // slot t-1 (counts of the current state) must survive the zeroing of [t, t+chunk)
+            const int64_t chunk = std::min<int64_t>(nsteps - done, metrics_cap - 1);
             sir_zero_slots<<<1, 256, 0, rt.stream>>>(ring.p, metrics_cap, t, chunk);
             check_launch("sir_zero_slots");
             const int threads = block ? static_cast<int>(std::min<int64_t>(block, 256)) : 256;
@@ -530,11 +724,18 @@ public:
                 AMBER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sir_persistent_kernel, threads, 0));
                 // latency-bound: many resident warps help, but the grid barrier
                 // cost grows with the block count; 3 blocks/SM measured best (C2)
-                int blocks = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(std::min(per_sm, 3)) * rt.num_sms,
+                // (C2); large populations are bound by random L2 lookups instead: full occupancy
+                const int per = n_pad > (1ll << 22) ? per_sm : std::min(per_sm, 3);
+                int blocks = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(per) * rt.num_sms,
                                                                 ceil_div(n_pad, threads)));
                 if (grid) blocks = static_cast<int>(std::min<int64_t>(grid, static_cast<int64_t>(per_sm) * rt.num_sms));
                 blocks = std::max(blocks, 1);
                 SirStepArgs a = args(chunk);
+                queue.zero_async(rt.stream);
+                a.queue = queue.p;
+                const int64_t warps = static_cast<int64_t>(blocks) * threads / 32;
+                a.grab = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, (n_pad / 32) / (warps * 8))));
+                if (n_pad / 32 <= 2 * warps) a.queue = nullptr;  // <= 2 chunks per warp: static striding
                 void* kargs[] = {&a};
                 prof.launch(rt.stream, "sir_persistent", [&] {
                     AMBER_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sir_persistent_kernel), blocks,
@@ -543,6 +744,7 @@ public:
                 check_launch("sir_persistent_kernel");
                 t += chunk;
                 if (chunk & 1) cur ^= 1;
+                prev_ok = true;
             } else {
                 for (int64_t k = 0; k < chunk; ++k) {
                     SirStepArgs a = args(1);
@@ -553,6 +755,7 @@ public:
                     cur ^= 1;
                     ++t;
                 }
+                prev_ok = true;
             }
             done += chunk;
         }
@@ -594,6 +797,8 @@ public:
         if (k != "state") fail(AMBER_E_UNKNOWN_NAME, "no column " + k);
         if (bytes < static_cast<size_t>(n)) fail(AMBER_E_BUFFER_TOO_SMALL, "src smaller than state column");
         copy_in(rt, x[cur].p, src, n, on_dev);
+        build_bits();
+        prev_ok = false;  // the next step pulls (and records the counts again)
     }
 
     void read_metrics(const char* name, void* dst, size_t bytes, int64_t* n_out) override
@@ -634,6 +839,7 @@ public:
         AMBER_CUDA(cudaStreamSynchronize(rt.stream));
         t = s;
         m_first = s;
+        prev_ok = false;
     }
 
     bool set_option(const char* key, int64_t v) override
@@ -646,6 +852,7 @@ public:
             ring.allocate(&rt, metrics_cap);
             ring.zero_async(rt.stream);
             m_first = t;
+            prev_ok = false;
             return true;
         }
         if (k == "block") AMBER_REQUIRE(v <= 256, "SIR kernels are built for <= 256 threads per block");

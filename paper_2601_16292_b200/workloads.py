@@ -46,9 +46,17 @@ SIRS_PAPER = dict(kind="sir_space", n=10_000, L=100.0, r=2.0, p_infect=0.1, p_re
 SIRS_SCALE = dict(kind="sir_space", n=10_000_000, L=3162.2776, r=2.0, p_infect=0.1, p_recover=0.05,
                   init_frac=0.01, seed=7, steps=100)
 
+# SURVEY 8(d) added roofline variants (labelled as such; parity stays on C1-C5):
+# V2 = C2's SIR at N = 1e8 (2M ~ 1e9 arcs, HBM-bound CSR streaming), 20 steps;
+# V3 = C3's Boids at N = 1e8 with L = 31,623 (same density 0.1 per unit^2), 10 steps
+V2_SIR_SCALE = dict(kind="sir", n=100_000_000, mean_degree=10.0, beta=0.05, gamma=0.1, init_frac=0.01,
+                    seed=7, steps=20)
+V3_BOIDS_SCALE = dict(kind="boids", n=100_000_000, L=31623.0, R=10.0, rs=2.0, wc=0.01, wa=0.125, ws=0.05,
+                      vmax=2.0, dt=1.0, seed=3, steps=10)
+
 CONFIGS = {"c1": C1_WEALTH_SMALL, "c2": C2_SIR, "c3": C3_BOIDS, "c4": C4_WEALTH_SCALE,
            "c5": C5_SWEEP, "walk": WALK_PAPER, "walk_scale": WALK_SCALE,
-           "sirs": SIRS_PAPER, "sirs_scale": SIRS_SCALE}
+           "sirs": SIRS_PAPER, "sirs_scale": SIRS_SCALE, "v2": V2_SIR_SCALE, "v3": V3_BOIDS_SCALE}
 
 
 def sweep_replicates(cfg=C5_SWEEP):

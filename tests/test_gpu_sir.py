@@ -147,3 +147,44 @@ def test_sweep_edge_cases(orc):
     got = sweep(n, sir_params(6.0, 0.0, 1.0, 0.02), [0.0], [3], 5)
     assert got[0] == 10 / n  # gamma = 1, beta = 0: exactly the initial infected recover
     assert sweep(n, sir_params(6.0, 0.0, 0.1, 0.02), [], [], 5).size == 0
+
+
+@pytest.mark.parametrize("digest", [0, 1])
+def test_large_population_dynamic_chunks(orc, digest):
+    # n large enough that the persistent launch hands out warp chunks from the
+    # per-region queues, with push (I < S) and pull steps and the I/S bitmaps
+    cfg = dict(n=1_000_000, mean_degree=10.0, beta=0.05, gamma=0.1, init_frac=0.01, seed=17, steps=30)
+    m = make(cfg)
+    m.set_option("digest", digest)
+    m.step(1)      # first call: push allowed from the seeded counts
+    m.step(29)
+    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
+    st = orc.sir_init(cfg["n"], 10_000, cfg["seed"])
+    ref, counts, dig = orc.sir_run(rp, col, st, cfg["seed"], cfg["beta"], cfg["gamma"], 0, 30, digests=True)
+    assert np.array_equal(m.read_column("state"), ref)
+    for k, name in enumerate("SIR"):
+        assert np.array_equal(m.metrics(name), counts[:, k]), name
+    if digest:
+        assert np.array_equal(m.metrics("digest"), dig.astype(np.uint64))
+
+
+def test_mixed_launch_modes_and_column_write(orc):
+    cfg = dict(n=300_000, mean_degree=8.0, beta=0.08, gamma=0.15, init_frac=0.002, seed=23, steps=40)
+    a = make(cfg)
+    a.step(40)
+    b = make(cfg)
+    for k, pers in enumerate([1, 0, 1, 1, 0, 0, 1]):  # persistent / per-step pull calls interleaved
+        b.set_option("persistent", pers)
+        b.step([3, 2, 7, 1, 4, 3, 20][k])
+    assert np.array_equal(b.read_column("state"), a.read_column("state"))
+    # a column write mid-epidemic, then push steps from the written state
+    c = make(cfg)
+    c.step(10)
+    mid = c.read_column("state")
+    d = make(dict(cfg, seed=99))  # another graph: only the state matters after the write
+    rp, col = d.read_column("row_ptr"), d.read_column("col_idx")
+    d.write_column("state", mid)
+    d.set_step(10)
+    d.step(15)
+    ref = orc.sir_run(rp, col, mid, 99, cfg["beta"], cfg["gamma"], 10, 15)[0]
+    assert np.array_equal(d.read_column("state"), ref)

@@ -9,6 +9,10 @@ warm-up call; per-kernel device time from the library's event profiler.
 import json
 import os
 import sys
+
+# load every kernel at context creation: lazy module loading inside a timed
+# region would be counted as step time
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 import time
 
 import numpy as np
