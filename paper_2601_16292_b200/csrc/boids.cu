@@ -261,11 +261,18 @@ __global__ void __launch_bounds__(256) boids_step_kernel(const float4* __restric
 // arithmetic to boids_step_kernel (B2-B6), so identical results.
 constexpr int kT = 4, kW = kT + 2, kHalo = kW * kW;
 
+// WRAP = false: the caller guarantees |o - me| <= L/2 per coordinate (both
+// agents in interior cells), where the minimum image is the identity.
+template <bool WRAP = true>
 __device__ __forceinline__ void boid_accumulate(const float4 o, const float4 me, float L, float halfL, float R2,
                                                 float rs2, Acc& acc)
 {
-    const float dx = min_image(__fsub_rn(o.x, me.x), L, halfL);
-    const float dy = min_image(__fsub_rn(o.y, me.y), L, halfL);
+    float dx = __fsub_rn(o.x, me.x), dy = __fsub_rn(o.y, me.y);
+    if constexpr (WRAP) {
+        const float dxm = __fsub_rn(dx, L), dxp = __fadd_rn(dx, L), dym = __fsub_rn(dy, L), dyp = __fadd_rn(dy, L);
+        dx = dx > halfL ? dxm : (dx < -halfL ? dxp : dx);
+        dy = dy > halfL ? dym : (dy < -halfL ? dyp : dy);
+    }
     const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
     if (d2 <= R2) {
         const long long qx = q24(dx), qy = q24(dy);
@@ -279,6 +286,35 @@ __device__ __forceinline__ void boid_accumulate(const float4 o, const float4 me,
             acc.ssy += qy;
         }
     }
+}
+
+// B4-B6 given the four neighbour means (computed by the caller) and the sums.
+__device__ __forceinline__ float4 boid_update_means(const float4 me, const Acc& acc, float cohx, float cohy, float avx,
+                                                    float avy, const BoidsArgs& a)
+{
+    const float L = a.L;
+    float ux = me.z, uy = me.w;
+    if (acc.n > 0) {
+        const float sepx = __double2float_rn(__dmul_rn(static_cast<double>(acc.ssx), 1.0 / 16777216.0));
+        const float sepy = __double2float_rn(__dmul_rn(static_cast<double>(acc.ssy), 1.0 / 16777216.0));
+        ux = __fsub_rn(__fadd_rn(__fadd_rn(me.z, __fmul_rn(a.wc, cohx)), __fmul_rn(a.wa, __fsub_rn(avx, me.z))),
+                       __fmul_rn(a.ws, sepx));
+        uy = __fsub_rn(__fadd_rn(__fadd_rn(me.w, __fmul_rn(a.wc, cohy)), __fmul_rn(a.wa, __fsub_rn(avy, me.w))),
+                       __fmul_rn(a.ws, sepy));
+    }
+    const float s2 = __fadd_rn(__fmul_rn(ux, ux), __fmul_rn(uy, uy));
+    if (s2 > __fmul_rn(a.vmax, a.vmax)) {
+        const float f = __fdiv_rn(a.vmax, __fsqrt_rn(s2));
+        ux = __fmul_rn(ux, f);
+        uy = __fmul_rn(uy, f);
+    }
+    float x = __fadd_rn(me.x, __fmul_rn(ux, a.dt));
+    float y = __fadd_rn(me.y, __fmul_rn(uy, a.dt));
+    if (x < 0.0f) x = __fadd_rn(x, L);
+    if (x >= L) x = __fsub_rn(x, L);
+    if (y < 0.0f) y = __fadd_rn(y, L);
+    if (y >= L) y = __fsub_rn(y, L);
+    return make_float4(x, y, ux, uy);
 }
 
 __device__ __forceinline__ float4 boid_update(const float4 me, const Acc& acc, const BoidsArgs& a)
@@ -455,12 +491,12 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
                                                  float4* __restrict__ out, int32_t* __restrict__ out_ids, BoidsSlot* slot,
                                                  int digest)
 {
+    static_assert(G >= 4, "the update spreads four divisions over the group's lanes");
     const float L = a.L, halfL = __fmul_rn(0.5f, a.L), R2 = __fmul_rn(a.R, a.R), rs2 = __fmul_rn(a.rs, a.rs);
     const int sub = threadIdx.x & (G - 1);
     const int64_t gid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / G;
     const int64_t ng = (static_cast<int64_t>(gridDim.x) * blockDim.x) / G;
     const int64_t rounds = (n + ng - 1) / ng;  // uniform: every lane runs every round (shuffles)
-    const int span = a.nc >= 3 ? 1 : 0;
     double sp_sum = 0.0, ux_sum = 0.0, uy_sum = 0.0;
     unsigned long long dig = 0;
     for (int64_t r = 0; r < rounds; ++r) {
@@ -470,20 +506,49 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
         float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
         if (active) {
             me = sorted[p];
-            const int cx = cell_coord(me.x, a), cy = cell_coord(me.y, a);
-#pragma unroll 1
-            for (int dyc = -span; dyc <= span; ++dyc) {
-                int yy = cy + dyc;
-                yy = yy < 0 ? yy + a.nc : (yy >= a.nc ? yy - a.nc : yy);
-#pragma unroll 1
-                for (int dxc = -span; dxc <= span; ++dxc) {
-                    int xx = cx + dxc;
-                    xx = xx < 0 ? xx + a.nc : (xx >= a.nc ? xx - a.nc : xx);
-                    const int c = yy * a.nc + xx;
-                    const int e = start[c + 1];
-                    for (int q = start[c] + sub; q < e; q += G)
-                        if (q != p) boid_accumulate(sorted[q], me, L, halfL, R2, rs2, acc);
+            auto run = [&](int b, int e) {
+                for (int q = b + sub; q < e; q += G)
+                    if (q != p) boid_accumulate<true>(sorted[q], me, L, halfL, R2, rs2, acc);
+            };
+            // interior agents (stencil inside the box, so every candidate is within
+            // two cells < L/2 per coordinate): no minimum image, rows as runs
+            auto run_in = [&](int b, int e) {
+                int q = b + sub;
+                for (; q + G < e; q += 2 * G) {  // two candidate loads in flight per lane
+                    const float4 o0 = sorted[q], o1 = sorted[q + G];
+                    if (q != p) boid_accumulate<false>(o0, me, L, halfL, R2, rs2, acc);
+                    if (q + G != p) boid_accumulate<false>(o1, me, L, halfL, R2, rs2, acc);
                 }
+                if (q < e && q != p) boid_accumulate<false>(sorted[q], me, L, halfL, R2, rs2, acc);
+            };
+            const int cx0 = a.nc >= 3 ? cell_coord(me.x, a) : 0, cy0 = a.nc >= 3 ? cell_coord(me.y, a) : 0;
+            if (a.nc >= 5 && cx0 >= 1 && cx0 + 1 < a.nc && cy0 >= 1 && cy0 + 1 < a.nc) {
+#pragma unroll 1
+                for (int dyc = -1; dyc <= 1; ++dyc) {
+                    const int row = (cy0 + dyc) * a.nc;
+                    run_in(start[row + cx0 - 1], start[row + cx0 + 2]);
+                }
+            } else if (a.nc >= 3) {
+                const int cx = cx0, cy = cy0;
+#pragma unroll 1
+                for (int dyc = -1; dyc <= 1; ++dyc) {
+                    int yy = cy + dyc;
+                    yy = yy < 0 ? yy + a.nc : (yy >= a.nc ? yy - a.nc : yy);
+                    const int row = yy * a.nc;
+                    if (cx >= 1 && cx + 1 < a.nc) {
+                        // cells cx-1, cx, cx+1 of a row are contiguous in the sorted array
+                        run(start[row + cx - 1], start[row + cx + 2]);
+                    } else {
+#pragma unroll 1
+                        for (int dxc = -1; dxc <= 1; ++dxc) {
+                            int xx = cx + dxc;
+                            xx = xx < 0 ? xx + a.nc : (xx >= a.nc ? xx - a.nc : xx);
+                            run(start[row + xx], start[row + xx + 1]);
+                        }
+                    }
+                }
+            } else {
+                run(start[0], start[1]);  // one cell holding every agent
             }
         }
 #pragma unroll
@@ -496,19 +561,34 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
             acc.ssx += __shfl_xor_sync(0xffffffffu, acc.ssx, off);
             acc.ssy += __shfl_xor_sync(0xffffffffu, acc.ssy, off);
         }
-        if (active && sub == 0) {
-            const float4 nx = boid_update(me, acc, a);
-            out[p] = nx;
-            const int32_t id = sids[p];
-            out_ids[p] = id;
-            const double dvx = static_cast<double>(nx.z), dvy = static_cast<double>(nx.w);
-            const double sp = __dsqrt_rn(__dadd_rn(__dmul_rn(dvx, dvx), __dmul_rn(dvy, dvy)));
-            sp_sum += sp;
-            if (sp > 0.0) {
-                ux_sum += __ddiv_rn(dvx, sp);
-                uy_sum += __ddiv_rn(dvy, sp);
+        // B4's four mean divisions in parallel on lanes 0..3 of the group
+        // (x / 2^24 is exact, so it is a multiplication), gathered by shuffles
+        float mv = 0.0f;
+        if (acc.n > 0 && sub < 4) {
+            const long long sv = sub == 0 ? acc.sdx : (sub == 1 ? acc.sdy : (sub == 2 ? acc.svx : acc.svy));
+            mv = __double2float_rn(__ddiv_rn(__dmul_rn(static_cast<double>(sv), 1.0 / 16777216.0),
+                                             static_cast<double>(acc.n)));
+        }
+        const float cohx = __shfl_sync(0xffffffffu, mv, 0, G), cohy = __shfl_sync(0xffffffffu, mv, 1, G);
+        const float avx = __shfl_sync(0xffffffffu, mv, 2, G), avy = __shfl_sync(0xffffffffu, mv, 3, G);
+        if (active) {
+            const float4 nx = boid_update_means(me, acc, cohx, cohy, avx, avy, a);
+            if (sub == 0) {
+                out[p] = nx;
+                const int32_t id = sids[p];
+                out_ids[p] = id;
+                if (digest) dig += digest_term(static_cast<unsigned long long>(id), __float_as_uint(nx.x));
             }
-            if (digest) dig += digest_term(static_cast<unsigned long long>(id), __float_as_uint(nx.x));
+            // observables (B8) in double, one per lane
+            if (sub < 3) {
+                const double dvx = static_cast<double>(nx.z), dvy = static_cast<double>(nx.w);
+                const double sp = __dsqrt_rn(__dadd_rn(__dmul_rn(dvx, dvx), __dmul_rn(dvy, dvy)));
+                if (sub == 0) sp_sum += sp;
+                else if (sp > 0.0) {
+                    if (sub == 1) ux_sum += __ddiv_rn(dvx, sp);
+                    else uy_sum += __ddiv_rn(dvy, sp);
+                }
+            }
         }
     }
     __shared__ double red[3][8];
@@ -543,7 +623,7 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
 }
 
 template <int G>
-__global__ void __launch_bounds__(256) boids_group_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ sids,
+__global__ void __launch_bounds__(256, 4) boids_group_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ sids,
                                                           const int* __restrict__ start, int64_t n, BoidsArgs a,
                                                           float4* __restrict__ out, int32_t* __restrict__ out_ids,
                                                           BoidsSlot* slot, int digest)
@@ -568,7 +648,7 @@ struct BoidsPersistArgs {
     int digest;
 };
 
-__global__ void __launch_bounds__(256) boids_persistent_kernel(const BoidsPersistArgs P)
+__global__ void __launch_bounds__(256, 4) boids_persistent_kernel(const BoidsPersistArgs P)
 {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -681,6 +761,8 @@ public:
     DevBuf<int32_t> ids, sids;
     DevBuf<int> cnt, start, cursor, cell_of, block_sums;
     DevBuf<float> col_tmp;
+    DevBuf<char> scan_tmp;  // CUB device-scan temporary storage
+    size_t scan_bytes = 0;
     DevBuf<BoidsSlot> ring;
     int64_t m_first = 0;
     int ncell = 0;
@@ -717,6 +799,8 @@ public:
         start.allocate(&rt, ncell + 1);
         cursor.allocate(&rt, ncell + 1);
         cell_of.allocate(&rt, n);
+        AMBER_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, cnt.p, start.p, ncell + 1, rt.stream));
+        scan_tmp.allocate(&rt, scan_bytes + 16);
         ring.allocate(&rt, metrics_cap);
         ring.zero_async(rt.stream);
         AMBER_CUDA(cudaFuncSetAttribute(boids_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -730,7 +814,7 @@ public:
     {
         if (rt.stream) cudaStreamSynchronize(rt.stream);
         st.reset(); sorted.reset(); ids.reset(); sids.reset(); cnt.reset(); start.reset(); cursor.reset();
-        cell_of.reset(); col_tmp.reset(); ring.reset(); block_sums.reset();
+        cell_of.reset(); col_tmp.reset(); ring.reset(); block_sums.reset(); scan_tmp.reset();
         rt.destroy();
     }
 
@@ -784,10 +868,22 @@ public:
                     boids_count_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(st.p, n, ba, cnt.p, cell_of.p);
                 });
                 check_launch("boids_count_kernel");
+                // exclusive scan of the ncell + 1 counts (cnt[ncell] = 0, so start[ncell] = n),
+                // cursors = starts, counts re-zeroed for the next step: one CTA for small
+                // grids, a device-wide scan for large ones (the one-CTA scan took 20 ms at
+                // V3's 10^7 cells, r01)
                 prof.launch(rt.stream, "boids_scan", [&] {
-                    boids_scan_kernel<<<1, 1024, 0, rt.stream>>>(cnt.p, start.p, cursor.p, ncell);
+                    if (ncell <= (1 << 16)) {  // one launch: scan, cursors, re-zeroed counts
+                        boids_scan_kernel<<<1, 1024, 0, rt.stream>>>(cnt.p, start.p, cursor.p, ncell);
+                    } else {
+                        AMBER_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp.p, scan_bytes, cnt.p, start.p, ncell + 1,
+                                                                 rt.stream));
+                        AMBER_CUDA(cudaMemcpyAsync(cursor.p, start.p, static_cast<size_t>(ncell) * sizeof(int),
+                                                   cudaMemcpyDeviceToDevice, rt.stream));
+                        AMBER_CUDA(cudaMemsetAsync(cnt.p, 0, static_cast<size_t>(ncell) * sizeof(int), rt.stream));
+                    }
                 });
-                check_launch("boids_scan_kernel");
+                check_launch("boids_scan");
                 prof.launch(rt.stream, "boids_scatter", [&] {
                     boids_scatter_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(st.p, ids.p, n, cell_of.p,
                                                                                        cursor.p, sorted.p, sids.p);
