@@ -191,10 +191,17 @@ const char* amber_last_error(void);
  * params of the kind's struct (params_size = sizeof), and a 64-bit seed
  * (Philox key, contract R2).  The initial state is built on the device
  * (W: w = w0; S: graph + initial infected; B: contract B1), step count 0.
- * When rt->world > 1 the call is collective over all ranks (wealth only:
- * agents are sharded by contiguous id ranges, see amber_column_info).
+ * When rt->world > 1 the call is collective over all ranks and the agents are
+ * sharded by contiguous id ranges (see amber_column_info for this rank's
+ * slice): AMBER_WEALTH (ranges of ceil(N/world) rounded up to 8; receivers
+ * exchanged per step) and AMBER_SIR_GRAPH (ranges rounded up to 32 agents;
+ * every rank builds the seeded graph and keeps its rows; per step a pull over
+ * the local rows against the global I bitmap, then an all-gather of the
+ * bitmap, N/8 bytes; results identical for any world size).  Sharded SIR
+ * column "state" is the local slice, "row_ptr"/"col_idx" the local rows
+ * (offsets from 0, global neighbour ids); metrics and digests are global.
  * Errors: INVALID_ARG (n_agents < 1, bad params, params_size too small),
- * UNKNOWN_KIND, OOM, CUDA, NCCL, UNSUPPORTED (world > 1 for a non-wealth kind). */
+ * UNKNOWN_KIND, OOM, CUDA, NCCL, UNSUPPORTED (world > 1 for another kind). */
 int amber_model_create(amber_kind kind, int64_t n_agents, const void* params, size_t params_size,
                        uint64_t seed, const amber_runtime* rt, amber_model** out);
 
@@ -297,6 +304,13 @@ int amber_sweep(amber_kind kind, int64_t n_agents, const void* base_params, size
  * two-agent Philox blocks (contract R4) never straddle shards; trailing ranks
  * may be shorter or empty.  Errors: INVALID_ARG. */
 int amber_shard_range(int64_t n_agents, int world, int rank, int64_t* lo, int64_t* hi);
+
+/* Host-only: the agent range [*lo, *hi) of rank `rank` in a sharded
+ * AMBER_SIR_GRAPH model (NEXT-3): shard size = ceil(n/world) rounded up to a
+ * multiple of 32 agents, so one word of the per-step all-gathered I bitmap
+ * never spans two ranks; trailing ranks may be shorter or empty.
+ * Errors: INVALID_ARG. */
+int amber_sir_shard_range(int64_t n_agents, int world, int rank, int64_t* lo, int64_t* hi);
 
 /* Host-only: the replicates [*r0, *r1) that rank `rank` of `world` runs in
  * amber_sweep (blocks of ceil(n_reps/world)).  Errors: INVALID_ARG. */

@@ -7,10 +7,10 @@ never imports oracle/ and has no CPU fallback.
 """
 from . import capi
 from .capi import AmberError
-from .model import (Model, boids_params, loopback_id, make_runtime, nccl_unique_id, shard_range, sir_params,
+from .model import (Model, boids_params, loopback_id, make_runtime, nccl_unique_id, shard_range, sir_params, sir_shard_range,
                     sweep, sweep_range, sir_space_params, walk_params, wealth_params)
 
 from .population import Population, agent_id, col, lit, rand, step_index
 
 __all__ = ["Population", "col", "lit", "rand", "agent_id", "step_index", "capi", "AmberError", "Model", "wealth_params", "sir_params", "boids_params", "sweep",
-           "make_runtime", "nccl_unique_id", "shard_range", "sweep_range", "loopback_id", "walk_params", "sir_space_params"]
+           "make_runtime", "nccl_unique_id", "shard_range", "sir_shard_range", "sweep_range", "loopback_id", "walk_params", "sir_space_params"]

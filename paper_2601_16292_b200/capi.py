@@ -26,7 +26,7 @@ SYMBOLS = ["amber_version", "amber_last_error", "amber_model_create", "amber_mod
            "amber_step", "amber_synchronize", "amber_step_count", "amber_set_step",
            "amber_column_info", "amber_read_column", "amber_write_column", "amber_read_metrics",
            "amber_reset_metrics", "amber_digest", "amber_set_option", "amber_get_option",
-           "amber_profile_enable", "amber_profile_query", "amber_sweep", "amber_shard_range",
+           "amber_profile_enable", "amber_profile_query", "amber_sweep", "amber_shard_range", "amber_sir_shard_range",
            "amber_sweep_range", "amber_nccl_unique_id", "amber_loopback_id",
            "amber_population_create", "amber_population_destroy", "amber_population_add_agents",
            "amber_population_remove_agents", "amber_population_compact", "amber_population_size",
@@ -138,6 +138,7 @@ def load():
                                   P(amber_sweep_stats)]),
         "amber_shard_range": (C.c_int, [C.c_int64, C.c_int, C.c_int, i64p, i64p]),
         "amber_sweep_range": (C.c_int, [C.c_int64, C.c_int, C.c_int, i64p, i64p]),
+        "amber_sir_shard_range": (C.c_int, [C.c_int64, C.c_int, C.c_int, i64p, i64p]),
         "amber_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_size_t]),
         "amber_loopback_id": (C.c_int, [C.c_void_p, C.c_size_t]),
         "amber_population_create": (C.c_int, [P(amber_column_spec), C.c_int, C.c_int64, C.c_uint64,

@@ -60,8 +60,9 @@ int amber_model_create(amber_kind kind, int64_t n_agents, const void* params, si
         *out = nullptr;
         need(params, "params");
         AMBER_REQUIRE(n_agents >= 1, "n_agents must be >= 1");
-        if (rt && rt->world > 1 && kind != AMBER_WEALTH)
-            amber::fail(AMBER_E_UNSUPPORTED, "only AMBER_WEALTH is sharded across ranks (others: replicas/amber_sweep)");
+        if (rt && rt->world > 1 && kind != AMBER_WEALTH && kind != AMBER_SIR_GRAPH)
+            amber::fail(AMBER_E_UNSUPPORTED,
+                        "only AMBER_WEALTH and AMBER_SIR_GRAPH are sharded across ranks (others: replicas/amber_sweep)");
         amber::Model* m = nullptr;
         switch (kind) {
             case AMBER_WEALTH:
@@ -266,6 +267,19 @@ int amber_shard_range(int64_t n_agents, int world, int rank, int64_t* lo, int64_
         need(hi, "hi");
         AMBER_REQUIRE(n_agents >= 1 && world >= 1 && rank >= 0 && rank < world, "bad shard request");
         amber::shard_range(n_agents, world, rank, lo, hi);
+        return 0;
+    });
+}
+
+int amber_sir_shard_range(int64_t n_agents, int world, int rank, int64_t* lo, int64_t* hi)
+{
+    return guarded([&] {
+        need(lo, "lo");
+        need(hi, "hi");
+        AMBER_REQUIRE(n_agents >= 1 && world >= 1 && rank >= 0 && rank < world, "bad shard request");
+        int64_t len = 0, shard = 0;
+        amber::sir_shard_range(n_agents, world, rank, lo, &len, &shard);
+        *hi = *lo + len;
         return 0;
     });
 }

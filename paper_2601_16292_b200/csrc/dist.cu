@@ -328,6 +328,82 @@ void wealth_exchange_allreduce_u64(WealthExchange* x, Runtime& rt, unsigned long
     comm_allreduce_u64(x->comm, rt.stream, d_vals, static_cast<size_t>(n));
 }
 
+// ---------------------------------------------------------------- generic shard communicator
+// All-gather / all-reduce for the sharded models other than wealth (SIR:
+// per-step all-gather of the I bitmap), over NCCL or the loopback transport.
+struct ShardComm {
+    Comm* comm = nullptr;
+    std::shared_ptr<LoopbackHub> hub;
+    int rank = 0, world = 1;
+    std::vector<const void*> peers;  // loopback: posted send buffers
+};
+
+ShardComm* make_shard_comm(Runtime& rt, const amber_runtime* r)
+{
+    AMBER_REQUIRE(r && r->nccl_unique_id, "world > 1 needs amber_runtime.nccl_unique_id");
+    auto* c = new ShardComm;
+    c->rank = rt.rank;
+    c->world = rt.world;
+    if (std::memcmp(r->nccl_unique_id, kLoopbackMagic, sizeof(kLoopbackMagic)) == 0)
+        c->hub = loopback_hub(static_cast<const char*>(r->nccl_unique_id), rt.world);
+    else
+        c->comm = make_comm(r);
+    return c;
+}
+
+void destroy_shard_comm(ShardComm* c)
+{
+    if (!c) return;
+    if (c->comm) destroy_comm(c->comm);
+    c->hub.reset();
+    delete c;
+}
+
+// recv[p * count + k] = send of rank p, k < count (device buffers, stream-ordered).
+void shard_allgather_u32(ShardComm* c, Runtime& rt, const uint32_t* send, uint32_t* recv, size_t count)
+{
+    if (c->hub) {
+        LoopbackHub& h = *c->hub;
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));  // my send block is complete
+        {
+            std::lock_guard<std::mutex> g(h.mu);
+            if (h.vals[c->rank].size() < 1) h.vals[c->rank].resize(1);
+            h.vals[c->rank][0] = reinterpret_cast<unsigned long long>(send);
+        }
+        h.barrier();
+        for (int p = 0; p < c->world; ++p) {
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(h.vals[p][0]);
+            AMBER_CUDA(cudaMemcpyAsync(recv + p * count, src, count * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                                       rt.stream));
+        }
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        h.barrier();  // peers may now overwrite their send blocks
+        return;
+    }
+    nccl_check(nccl().AllGather(send, recv, count, ncclUint32, c->comm->comm, rt.stream), "ncclAllGather");
+}
+
+// In-place sum over ranks of n device values.
+void shard_allreduce_u64(ShardComm* c, Runtime& rt, unsigned long long* d, size_t n)
+{
+    if (c->hub) {
+        LoopbackHub& h = *c->hub;
+        std::vector<unsigned long long> mine(n);
+        AMBER_CUDA(cudaMemcpyAsync(mine.data(), d, n * 8, cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        h.vals[c->rank] = mine;
+        h.barrier();
+        std::vector<unsigned long long> out(n, 0ull);
+        for (int p = 0; p < c->world; ++p)
+            for (size_t k = 0; k < n; ++k) out[k] += h.vals[p][k];
+        h.barrier();
+        AMBER_CUDA(cudaMemcpyAsync(d, out.data(), n * 8, cudaMemcpyHostToDevice, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        return;
+    }
+    comm_allreduce_u64(c->comm, rt.stream, d, n);
+}
+
 }  // namespace amber
 
 extern "C" int amber_loopback_id_impl(void* out, size_t out_bytes)

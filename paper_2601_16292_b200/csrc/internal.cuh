@@ -250,6 +250,13 @@ uint64_t device_digest_u8(Runtime& rt, const uint8_t* col, int64_t n, int64_t id
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Shard communicator for the sharded SIR (dist.cu): NCCL or loopback.
+struct ShardComm;
+ShardComm* make_shard_comm(Runtime& rt, const amber_runtime* r);
+void destroy_shard_comm(ShardComm* c);
+void shard_allgather_u32(ShardComm* c, Runtime& rt, const uint32_t* send, uint32_t* recv, size_t count);
+void shard_allreduce_u64(ShardComm* c, Runtime& rt, unsigned long long* d, size_t n);
+
 // Multi-GPU partitions (host logic).  Wealth: contiguous id
 // ranges of ceil(n/world) rounded up to 8 agents.  Sweep: replicate blocks.
 inline void shard_range(int64_t n, int world, int rank, int64_t* lo, int64_t* hi)
@@ -257,6 +264,15 @@ inline void shard_range(int64_t n, int world, int rank, int64_t* lo, int64_t* hi
     const int64_t shard = ((ceil_div(n, world) + 7) / 8) * 8;
     *lo = std::min<int64_t>(shard * rank, n);
     *hi = std::min<int64_t>(shard * (rank + 1), n);
+}
+
+// Sharded SIR (NEXT-3): contiguous id ranges of ceil(n/world) rounded up to 32
+// agents (one I-bitmap word never spans two ranks).  shard = padded local size.
+inline void sir_shard_range(int64_t n, int world, int rank, int64_t* lo, int64_t* len, int64_t* shard)
+{
+    *shard = ((ceil_div(n, world) + 31) / 32) * 32;
+    *lo = std::min<int64_t>(*shard * rank, n);
+    *len = std::min<int64_t>(*shard * (rank + 1), n) - *lo;
 }
 
 inline void sweep_range(int64_t n_reps, int world, int rank, int64_t* r0, int64_t* r1)

@@ -264,7 +264,8 @@ struct SirStepArgs {
     uint8_t* x[2];           // ping-pong state (n_pad, padding = kPad)
     uint32_t* ib[2];         // ping-pong I bitmaps (n_pad / 32 words): bit i = [x_i == I]
     uint32_t* sb[2];         // ping-pong S bitmaps
-    int64_t n, n_pad;
+    int64_t n, n_pad;        // agents of this shard (all agents unsharded), padded to 32
+    unsigned long long gid0; // global id of local agent 0 (sharded: the shard start; else 0)
     unsigned long long t_beta, t_gamma;
     uint32_t t0;             // first step index
     int64_t n_steps;         // steps in this launch (persistent) or 1
@@ -410,8 +411,8 @@ __device__ __forceinline__ uint8_t sir_pull_chunk(const SirStepArgs& a, int64_t 
     if (s_mask) {
         const int32_t rb = real ? a.row_ptr[i] : 0, re = real ? a.row_ptr[i + 1] : 0;
         hit = walk_rows<4>(a.col, s_mask, rb, re, [&](uint32_t j, int32_t, int L) {
-            if (!bit_of(ib, j)) return false;
-            const uint32_t s = static_cast<uint32_t>(a0 + L);
+            if (!bit_of(ib, j)) return false;  // j is a global id (the bitmap is global)
+            const uint32_t s = static_cast<uint32_t>(a.gid0 + a0 + L);
             const uint4 w = philox(make_uint4(min(s, j), max(s, j), t, TAG_SIR_TX), a.key);
             return static_cast<unsigned long long>(w.x) < a.t_beta;
         });
@@ -420,7 +421,7 @@ __device__ __forceinline__ uint8_t sir_pull_chunk(const SirStepArgs& a, int64_t 
     if (is_s) {
         if ((hit >> lane) & 1u) o = kI;
     } else if (st == kI) {
-        if (recovers(a, i, t)) o = kR;
+        if (recovers(a, static_cast<int64_t>(a.gid0) + i, t)) o = kR;
     }
     y[i] = o;
     const uint32_t ibw = __ballot_sync(0xffffffffu, o == kI), sbw = __ballot_sync(0xffffffffu, o == kS);
@@ -441,7 +442,7 @@ __device__ __forceinline__ void sir_pull_body(const SirStepArgs& a, int c, uint3
             cnt[0] += o == kS;
             cnt[1] += o == kI;
             cnt[2] += o == kR;
-            if (a.digest) cnt[3] += digest_term(static_cast<unsigned long long>(i), o);
+            if (a.digest) cnt[3] += digest_term(a.gid0 + static_cast<unsigned long long>(i), o);
         }
     });
 }
@@ -593,6 +594,13 @@ __global__ void __launch_bounds__(256, 3) sir_persistent_kernel(const SirStepArg
     }
 }
 
+// Sharded graph slice: row offsets rebased to the shard's first arc.
+__global__ void sir_rebase_kernel(const int32_t* __restrict__ rp, int64_t cnt, int32_t base, int32_t* __restrict__ out)
+{
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < cnt; k += (int64_t)gridDim.x * blockDim.x)
+        out[k] = rp[k] - base;
+}
+
 __global__ void sir_zero_slots(SirSlot* ring, int64_t cap, int64_t s0, int64_t count)
 {
     for (int64_t k = threadIdx.x; k < count && k < cap; k += blockDim.x) ring[(s0 + k) % cap] = SirSlot{0, 0, 0, 0};
@@ -615,6 +623,15 @@ public:
     DevBuf<SirSlot> ring;
     int64_t m_first = 0;
     bool prev_ok = false;  // ring slot t-1 holds the counts of the current state
+    // sharded (world > 1, NEXT-3): this rank owns agents [lo, lo + nl) (shard =
+    // multiple of 32 agents so bitmap words never straddle ranks), its CSR rows
+    // (local offsets, global neighbour ids) and state; every step pulls its rows
+    // against the GLOBAL I bitmap, then the shards' next bitmap words are
+    // all-gathered (N/8 bytes per step in total).
+    ShardComm* sc = nullptr;
+    int64_t lo = 0, nl = 0, npl = 0, shard = 0;  // local agents / padded (unsharded: n, n_pad)
+    DevBuf<uint32_t> ib_glob;  // world * shard / 32 words
+    bool glob_ok = false;      // ib_glob holds the current state's bits
 
     SirModel(int64_t n_, const amber_sir_params& p_, uint64_t seed_, const amber_runtime* r)
     {
@@ -632,12 +649,37 @@ public:
         n_pad = ceil_div(n, 32) * 32;
         std::vector<unsigned long long> seeds{seed};
         build_graphs(rt, seeds, n, m_draws, g);
-        for (auto& b : x) b.allocate(&rt, n_pad);
-        for (int c = 0; c < 2; ++c) {
-            ib[c].allocate(&rt, n_pad / 32);
-            sb[c].allocate(&rt, n_pad / 32);
+        nl = n;
+        npl = n_pad;
+        // AMBER_TEST_FORCE_EXCHANGE=1 with a unique id: the sharded path with one rank
+        // (a one-rank NCCL communicator: exercises the all-gather/all-reduce plumbing)
+        const char* force = getenv("AMBER_TEST_FORCE_EXCHANGE");
+        const bool sharded = rt.world > 1 || (force && force[0] == '1' && r && r->nccl_unique_id);
+        if (sharded) {
+            AMBER_REQUIRE(rt.rank >= 0 && rt.rank < rt.world, "rank out of range");
+            sir_shard_range(n, rt.world, rt.rank, &lo, &nl, &shard);
+            npl = shard;
         }
-        build_init_state(rt, seeds, n, n_pad, k_inf, x[0].p);
+        for (auto& b : x) b.allocate(&rt, npl);
+        for (int c = 0; c < 2; ++c) {
+            ib[c].allocate(&rt, npl / 32);
+            sb[c].allocate(&rt, npl / 32);
+        }
+        if (sharded) {
+            // every rank builds the (seeded, deterministic) graph and initial state,
+            // keeps its slice and frees the rest
+            DevBuf<uint8_t> full;
+            full.allocate(&rt, n_pad);
+            build_init_state(rt, seeds, n, n_pad, k_inf, full.p);
+            AMBER_CUDA(cudaMemsetAsync(x[0].p, kPad, npl, rt.stream));
+            if (nl) AMBER_CUDA(cudaMemcpyAsync(x[0].p, full.p + lo, nl, cudaMemcpyDeviceToDevice, rt.stream));
+            slice_graph();
+            ib_glob.allocate(&rt, static_cast<size_t>(rt.world) * (shard / 32));
+            sc = make_shard_comm(rt, r);
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        } else {
+            build_init_state(rt, seeds, n, n_pad, k_inf, x[0].p);
+        }
         build_bits();
         queue.allocate(&rt, 4 * kRegions);
         ring.allocate(&rt, metrics_cap);
@@ -650,11 +692,43 @@ public:
     // push step's invariant: every agent S now is S in the back state).
     void build_bits()
     {
-        sir_bits_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(x[cur].p, n_pad, ib[cur].p, sb[cur].p);
+        sir_bits_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(x[cur].p, npl, ib[cur].p, sb[cur].p);
         check_launch("sir_bits_kernel");
-        AMBER_CUDA(cudaMemcpyAsync(x[cur ^ 1].p, x[cur].p, n_pad, cudaMemcpyDeviceToDevice, rt.stream));
-        AMBER_CUDA(cudaMemcpyAsync(ib[cur ^ 1].p, ib[cur].p, n_pad / 8, cudaMemcpyDeviceToDevice, rt.stream));
-        AMBER_CUDA(cudaMemcpyAsync(sb[cur ^ 1].p, sb[cur].p, n_pad / 8, cudaMemcpyDeviceToDevice, rt.stream));
+        AMBER_CUDA(cudaMemcpyAsync(x[cur ^ 1].p, x[cur].p, npl, cudaMemcpyDeviceToDevice, rt.stream));
+        AMBER_CUDA(cudaMemcpyAsync(ib[cur ^ 1].p, ib[cur].p, npl / 8, cudaMemcpyDeviceToDevice, rt.stream));
+        AMBER_CUDA(cudaMemcpyAsync(sb[cur ^ 1].p, sb[cur].p, npl / 8, cudaMemcpyDeviceToDevice, rt.stream));
+        glob_ok = false;
+    }
+
+    // Sharded: keep the rows [lo, lo + nl) of the full CSR (offsets rebased to 0;
+    // neighbour ids stay global).
+    void slice_graph()
+    {
+        std::vector<int32_t> ends(2);
+        AMBER_CUDA(cudaMemcpyAsync(&ends[0], g.row_ptr.p + lo, 4, cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaMemcpyAsync(&ends[1], g.row_ptr.p + lo + nl, 4, cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        const int64_t arcs = ends[1] - ends[0];
+        DevBuf<int32_t> rp, col;
+        rp.allocate(&rt, nl + 1);
+        col.allocate(&rt, std::max<int64_t>(arcs, 1) + 8);
+        sir_rebase_kernel<<<rt.num_sms * 4, 256, 0, rt.stream>>>(g.row_ptr.p + lo, nl + 1, ends[0], rp.p);
+        check_launch("sir_rebase_kernel");
+        if (arcs)
+            AMBER_CUDA(cudaMemcpyAsync(col.p, g.col.p + ends[0], arcs * 4, cudaMemcpyDeviceToDevice, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        std::swap(g.row_ptr.p, rp.p);
+        std::swap(g.row_ptr.n, rp.n);
+        std::swap(g.col.p, col.p);
+        std::swap(g.col.n, col.n);
+        g.arcs = arcs;
+    }
+
+    // Sharded: all-gather the current state's local I-bitmap words.
+    void gather_bits(const uint32_t* local)
+    {
+        shard_allgather_u32(sc, rt, local, ib_glob.p, static_cast<size_t>(shard / 32));
+        glob_ok = true;
     }
 
     // counts of the current state into ring slot t-1 (direction choice of the next step)
@@ -679,6 +753,8 @@ public:
         }
         ring.reset();
         queue.reset();
+        ib_glob.reset();
+        if (sc) destroy_shard_comm(sc);
         rt.destroy();
     }
 
@@ -695,8 +771,9 @@ public:
             a.sb[c] = sb[c].p;
         }
         a.prev_ok = prev_ok ? 1 : 0;
-        a.n = n;
-        a.n_pad = n_pad;
+        a.n = nl;
+        a.n_pad = npl;
+        a.gid0 = static_cast<unsigned long long>(lo);
         a.t_beta = bernoulli_threshold_host(p.beta);
         a.t_gamma = bernoulli_threshold_host(p.gamma);
         a.t0 = static_cast<uint32_t>(t);
@@ -712,6 +789,10 @@ public:
     {
         AMBER_REQUIRE(nsteps >= 0, "n_steps must be >= 0");
         AMBER_REQUIRE(t + nsteps < (1ll << 32), "step index would exceed 2^32");
+        if (sc) {
+            step_sharded(nsteps);
+            return;
+        }
         int64_t done = 0;
         while (done < nsteps) {
             // slot t-1 (counts of the current state) must survive the zeroing of [t, t+chunk)
@@ -761,18 +842,56 @@ public:
         }
     }
 
+    // Sharded steps: per step one pull launch over the local rows (reading the
+    // global I bitmap), then the all-gather of the next bitmap words.  Pull only:
+    // a push would write remote agents.  Identical results for any rank count
+    // (pair-keyed draws, S3).
+    void step_sharded(int64_t nsteps)
+    {
+        const int threads = block ? static_cast<int>(std::min<int64_t>(block, 256)) : 256;
+        if (!glob_ok) gather_bits(ib[cur].p);
+        for (int64_t k = 0; k < nsteps; ++k) {
+            sir_zero_slots<<<1, 32, 0, rt.stream>>>(ring.p, metrics_cap, t, 1);
+            check_launch("sir_zero_slots");
+            SirStepArgs a = args(1);
+            a.ib[cur] = ib_glob.p;  // read: global bits of state t; write: local bits of t+1
+            int blocks = static_cast<int>(std::max<int64_t>(1, ceil_div(npl, threads)));
+            if (grid) blocks = static_cast<int>(grid);
+            prof.launch(rt.stream, "sir_shard_step", [&] { sir_step_kernel<<<blocks, threads, 0, rt.stream>>>(a); });
+            check_launch("sir_step_kernel");
+            cur ^= 1;
+            ++t;
+            gather_bits(ib[cur].p);
+        }
+        prev_ok = false;
+    }
+
+    // Sharded metrics / digests are global: summed over the ranks (collective).
+    void global_sum(unsigned long long* h, size_t cnt)
+    {
+        if (!sc || !cnt) return;
+        DevBuf<unsigned long long> d;
+        d.allocate(&rt, cnt);
+        AMBER_CUDA(cudaMemcpyAsync(d.p, h, cnt * 8, cudaMemcpyHostToDevice, rt.stream));
+        shard_allreduce_u64(sc, rt, d.p, cnt);
+        AMBER_CUDA(cudaMemcpyAsync(h, d.p, cnt * 8, cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    }
+
+    // Sharded: "state" is this rank's slice [lo, lo + nl) of the global column;
+    // "row_ptr" / "col_idx" are its rows (offsets from 0, global neighbour ids).
     bool column_info(const char* name, amber_dtype* dt, int64_t* glen, int64_t* off, int64_t* len) override
     {
         std::string k(name);
-        int64_t L;
+        int64_t L, G, O = 0;
         amber_dtype d;
-        if (k == "state") { d = AMBER_U8; L = n; }
-        else if (k == "row_ptr") { d = AMBER_I32; L = n + 1; }
-        else if (k == "col_idx") { d = AMBER_I32; L = g.arcs; }
+        if (k == "state") { d = AMBER_U8; L = nl; G = n; O = lo; }
+        else if (k == "row_ptr") { d = AMBER_I32; L = nl + 1; G = L; }
+        else if (k == "col_idx") { d = AMBER_I32; L = g.arcs; G = L; }
         else return false;
         if (dt) *dt = d;
-        if (glen) *glen = L;
-        if (off) *off = 0;
+        if (glen) *glen = G;
+        if (off) *off = O;
         if (len) *len = L;
         return true;
     }
@@ -782,8 +901,8 @@ public:
         std::string k(name);
         const void* src;
         size_t nb;
-        if (k == "state") { src = x[cur].p; nb = n; }
-        else if (k == "row_ptr") { src = g.row_ptr.p; nb = (n + 1) * 4; }
+        if (k == "state") { src = x[cur].p; nb = nl; }
+        else if (k == "row_ptr") { src = g.row_ptr.p; nb = (nl + 1) * 4; }
         else if (k == "col_idx") { src = g.col.p; nb = g.arcs * 4; }
         else fail(AMBER_E_UNKNOWN_NAME, "no column " + k);
         if (bytes < nb) fail(AMBER_E_BUFFER_TOO_SMALL, "dst too small for column " + k);
@@ -795,8 +914,8 @@ public:
         std::string k(name);
         if (k == "row_ptr" || k == "col_idx") fail(AMBER_E_INVALID_ARG, "column " + k + " is read-only");
         if (k != "state") fail(AMBER_E_UNKNOWN_NAME, "no column " + k);
-        if (bytes < static_cast<size_t>(n)) fail(AMBER_E_BUFFER_TOO_SMALL, "src smaller than state column");
-        copy_in(rt, x[cur].p, src, n, on_dev);
+        if (bytes < static_cast<size_t>(nl)) fail(AMBER_E_BUFFER_TOO_SMALL, "src smaller than state column");
+        copy_in(rt, x[cur].p, src, nl, on_dev);
         build_bits();
         prev_ok = false;  // the next step pulls (and records the counts again)
     }
@@ -816,8 +935,11 @@ public:
         const int64_t first = std::max(m_first, t - metrics_cap);
         const int64_t cnt = std::max<int64_t>(t - first, 0);
         if (bytes < static_cast<size_t>(cnt) * 8) fail(AMBER_E_BUFFER_TOO_SMALL, "metrics dst too small");
+        std::vector<unsigned long long> vals(cnt);
         for (int64_t s = first; s < t; ++s)
-            std::memcpy(static_cast<char*>(dst) + (s - first) * 8, reinterpret_cast<const char*>(&h[s % metrics_cap]) + off, 8);
+            std::memcpy(&vals[s - first], reinterpret_cast<const char*>(&h[s % metrics_cap]) + off, 8);
+        global_sum(vals.data(), vals.size());  // sharded: counts and digests of all ranks
+        std::memcpy(dst, vals.data(), cnt * 8);
         if (n_out) *n_out = cnt;
     }
 
@@ -830,7 +952,9 @@ public:
     uint64_t digest(const char* name) override
     {
         if (std::string(name) != "state") fail(AMBER_E_UNKNOWN_NAME, std::string("no column ") + name);
-        return device_digest_u8(rt, x[cur].p, n, 0);
+        unsigned long long d = device_digest_u8(rt, x[cur].p, nl, lo);
+        global_sum(&d, 1);
+        return d;
     }
 
     void set_step(int64_t s) override

@@ -82,6 +82,13 @@ def shard_range(n_agents: int, world: int, rank: int):
     return lo.value, hi.value
 
 
+def sir_shard_range(n_agents: int, world: int, rank: int):
+    """amber_sir_shard_range: this rank's agents [lo, hi) in a sharded SIR model (host logic)."""
+    lo, hi = C.c_int64(), C.c_int64()
+    check(capi.lib().amber_sir_shard_range(int(n_agents), int(world), int(rank), C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
 def sweep_range(n_reps: int, world: int, rank: int):
     """amber_sweep_range: the replicates [r0, r1) this rank runs (host logic, no GPU)."""
     r0, r1 = C.c_int64(), C.c_int64()

@@ -10,7 +10,11 @@ tests cover what the ranks must agree on before any kernel runs:
   * bench.py's max-over-ranks timing reduction;
   * the sharded wealth step: receivers bucketed by owner rank (owner = r / shard
     size, as in the kernel), exchanged with all_to_all, applied by the owner,
-    equal the unsharded oracle step bit for bit.
+    equal the unsharded oracle step bit for bit;
+  * the sharded SIR step (NEXT-3): 32-aligned id ranges (amber_sir_shard_range),
+    local I-bitmap words all-gathered every step, each rank pulling its own rows
+    against the global bitmap with globally keyed draws, equals the unsharded
+    oracle run bit for bit.
 """
 import os
 import socket
@@ -115,6 +119,50 @@ def _sharded_wealth(rank, world):
     g = [None] * world
     dist.all_gather_object(g, (lo, w.tolist()))
     return g
+
+
+def _sharded_sir(rank, world):
+    import oracle
+    from paper_2601_16292_b200 import sir_shard_range
+    n, kbar, seed, beta, gamma, steps = 2003, 6.0, 5, 0.3, 0.2, 12
+    rp, col, _ = oracle.er_graph(n, int(round(n * kbar / 2)), seed)
+    st0 = oracle.sir_init(n, 20, seed)
+    lo, hi = sir_shard_range(n, world, rank)
+    shard = ((-(-n // world) + 31) // 32) * 32
+    assert lo == min(rank * shard, n) and lo % 32 == 0
+    x = st0[lo:hi].copy()
+    T_b, T_g = oracle.bernoulli_threshold(beta), oracle.bernoulli_threshold(gamma)
+    for t in range(steps):
+        # local I-bitmap words (bit b of word w = agent 32w + b of the shard), all-gathered
+        bits = np.zeros(shard, np.uint8)
+        bits[:hi - lo] = x == 1
+        words = torch.tensor(np.packbits(bits, bitorder="little").view(np.uint32).astype(np.int64))
+        g = [torch.zeros_like(words) for _ in range(world)]
+        dist.all_gather(g, words)
+        glob = np.concatenate([w.numpy().astype(np.uint32) for w in g])
+        is_i = lambda j: (glob[j >> 5] >> (j & 31)) & 1
+        y = x.copy()
+        for k in range(hi - lo):
+            s = lo + k
+            if x[k] == 0:  # pull: any I neighbour with a transmitting pair draw (S2, S3)
+                for j in col[rp[s]:rp[s + 1]]:
+                    if is_i(int(j)) and oracle.sir_tx_word(seed, min(s, j), max(s, j), t) < T_b:
+                        y[k] = 1
+                        break
+            elif x[k] == 1 and oracle.lane32(seed, 0x11, s, t) < T_g:
+                y[k] = 2
+        x = y
+    out = [None] * world
+    dist.all_gather_object(out, (lo, x.tolist()))
+    ref = oracle.sir_run(rp, col, st0, seed, beta, gamma, 0, steps)[0]
+    return out, ref.tolist()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_sir_bitmap_allgather_equals_oracle(world):
+    parts, ref = run_world(world, _sharded_sir)[0]
+    x = np.concatenate([np.array(v, np.uint8) for _, v in sorted(parts)])
+    assert np.array_equal(x, np.array(ref, np.uint8))
 
 
 @pytest.mark.parametrize("world", [2, 4])

@@ -110,3 +110,79 @@ def test_nccl_plumbing_single_rank(orc, monkeypatch):
     assert np.array_equal(m.metrics("total_wealth"), tot)
     assert m.digest("wealth") == orc.digest(ref)
     assert m.get_option("replays") > 0
+
+
+def sharded_sir(world, cfg):
+    uid = loopback_id()
+    p = sir_params(cfg["mean_degree"], cfg["beta"], cfg["gamma"], cfg["init_frac"])
+    return [Model("sir", cfg["n"], p, cfg["seed"], rank=r, world=world, unique_id=uid) for r in range(world)]
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_sir_equals_oracle(orc, world):
+    # NEXT-3: id-range shards, pull against the all-gathered I bitmap every step
+    cfg = dict(n=50_003, mean_degree=10.0, beta=0.05, gamma=0.1, init_frac=0.01, seed=7)
+    steps = 40
+    ref_m = Model("sir", cfg["n"], sir_params(cfg["mean_degree"], cfg["beta"], cfg["gamma"], cfg["init_frac"]),
+                  cfg["seed"])
+    rp, col = ref_m.read_column("row_ptr"), ref_m.read_column("col_idx")
+    ref_m.close()
+    st = orc.sir_init(cfg["n"], 500, cfg["seed"])
+    ref, counts, dig = orc.sir_run(rp, col, st, cfg["seed"], cfg["beta"], cfg["gamma"], 0, steps, digests=True)
+    ms = sharded_sir(world, cfg)
+    infos = [m.column_info("state") for m in ms]
+    assert infos[0][2] == 0 and sum(i[3] for i in infos) == cfg["n"]
+    for a, b in zip(infos, infos[1:]):
+        assert a[2] + a[3] == b[2] and a[3] % 32 == 0  # contiguous, 32-aligned slices
+    for m in ms:
+        m.set_option("digest", 1)
+    par(ms, lambda m: (m.step(1), m.step(steps - 1)))
+    x = np.concatenate(par(ms, lambda m: m.read_column("state")))
+    assert np.array_equal(x, ref)
+    for name_k, name in enumerate("SIR"):
+        for v in par(ms, lambda m: m.metrics(name)):
+            assert np.array_equal(v, counts[:, name_k]), name  # global counts on every rank
+    for v in par(ms, lambda m: m.metrics("digest")):
+        assert np.array_equal(v, dig.astype(np.uint64))
+    assert all(d == orc.digest(ref) for d in par(ms, lambda m: m.digest("state")))
+
+
+def test_sharded_sir_local_rows_and_column_write(orc):
+    cfg = dict(n=20_000, mean_degree=6.0, beta=0.1, gamma=0.2, init_frac=0.005, seed=11)
+    full = Model("sir", cfg["n"], sir_params(cfg["mean_degree"], cfg["beta"], cfg["gamma"], cfg["init_frac"]),
+                 cfg["seed"])
+    rp, col = full.read_column("row_ptr"), full.read_column("col_idx")
+    full.step(8)
+    mid = full.read_column("state")
+    ms = sharded_sir(2, cfg)
+    for m in ms:  # local rows: offsets from 0, global neighbour ids
+        _, _, lo, ln = m.column_info("state")
+        lrp, lcol = m.read_column("row_ptr"), m.read_column("col_idx")
+        assert np.array_equal(lrp, rp[lo:lo + ln + 1] - rp[lo])
+        assert np.array_equal(lcol, col[rp[lo]:rp[lo + ln]])
+    # restore a mid-run state into the shards, continue sharded
+    def restore(m):
+        _, _, lo, ln = m.column_info("state")
+        m.write_column("state", mid[lo:lo + ln])
+        m.set_step(8)
+        m.step(12)
+    par(ms, restore)
+    x = np.concatenate(par(ms, lambda m: m.read_column("state")))
+    assert np.array_equal(x, orc.sir_run(rp, col, mid, cfg["seed"], cfg["beta"], cfg["gamma"], 8, 12)[0])
+
+
+def test_sir_nccl_plumbing_single_rank(orc, monkeypatch):
+    # the sharded SIR path over a one-rank NCCL communicator: ncclAllGather of the
+    # I bitmap every step, ncclAllReduce of the metrics and the digest
+    from paper_2601_16292_b200 import nccl_unique_id
+    monkeypatch.setenv("AMBER_TEST_FORCE_EXCHANGE", "1")
+    cfg = dict(n=30_001, mean_degree=8.0, beta=0.06, gamma=0.1, init_frac=0.01, seed=3)
+    m = Model("sir", cfg["n"], sir_params(cfg["mean_degree"], cfg["beta"], cfg["gamma"], cfg["init_frac"]),
+              cfg["seed"], unique_id=nccl_unique_id())
+    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
+    m.step(25)
+    st = orc.sir_init(cfg["n"], 300, cfg["seed"])
+    ref, counts, _ = orc.sir_run(rp, col, st, cfg["seed"], cfg["beta"], cfg["gamma"], 0, 25)
+    assert np.array_equal(m.read_column("state"), ref)
+    assert np.array_equal(m.metrics("I"), counts[:, 1])
+    assert m.digest("state") == orc.digest(ref)
