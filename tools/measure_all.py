@@ -96,9 +96,11 @@ def main():
     ms, prof = timed(m, 200)
     dom = max(prof, key=lambda r: r[2])
     avg = dom[2] / dom[1]
+    senders = float(m.metrics("active")[-201:-1].mean())  # transfers of each timed step
     out.append(dict(config="C4 wealth N=1e8 x200 (of 1000)", us_per_step=ms / 200 * 1e3,
                     agent_updates_per_s=c["n"] * 200 / ms * 1e3, kernels=prof,
-                    hbm_frac=8 * c["n"] / (avg / 1e3) / 1e9 / HBM,
+                    hbm_frac=(8 * c["n"] + 8 * senders) / (avg / 1e3) / 1e9 / HBM,
+                    alg_bytes_rule="8 B/agent + 8 B/transfer (SURVEY 8(d))",
                     bound="L2 atomics (random REDs, profiles/r01_red_ceiling.txt)"))
     m.close()
     # C5
