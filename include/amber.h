@@ -200,6 +200,12 @@ const char* amber_last_error(void);
  * bitmap, N/8 bytes; results identical for any world size).  Sharded SIR
  * column "state" is the local slice, "row_ptr"/"col_idx" the local rows
  * (offsets from 0, global neighbour ids); metrics and digests are global.
+ * AMBER_BOIDS: x-slabs of whole grid-cell columns (rank r owns columns
+ * [r*nc/world, (r+1)*nc/world), nc = cells per side >= max(3, world)); per
+ * step agents migrate to the slab of their cell column and the first / last
+ * column of each slab is sent to the neighbours as halos (variable all-to-all);
+ * bit-identical to one GPU (exact fixed-point sums).  Sharded Boids column
+ * reads / writes / digests are collective and use the whole id-ordered column.
  * Errors: INVALID_ARG (n_agents < 1, bad params, params_size too small),
  * UNKNOWN_KIND, OOM, CUDA, NCCL, UNSUPPORTED (world > 1 for another kind). */
 int amber_model_create(amber_kind kind, int64_t n_agents, const void* params, size_t params_size,

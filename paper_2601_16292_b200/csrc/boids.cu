@@ -749,6 +749,283 @@ __global__ void boids_zero_slots(BoidsSlot* ring, int64_t cap, int64_t s0, int64
     for (int64_t k = threadIdx.x; k < count && k < cap; k += blockDim.x) ring[(s0 + k) % cap] = BoidsSlot{0.0, 0.0, 0.0, 0ull};
 }
 
+
+// ---------------------------------------------------------------- sharded Boids (NEXT-3)
+// x-slabs of whole cell columns: rank r owns columns [col0[r], col0[r+1]).  An
+// agent belongs to the rank whose slab holds its cell column (same cell_coord
+// as the binning, so ownership and stencil always agree).  Per step: migrate
+// agents whose column left the slab, send the first / last own column to the
+// left / right neighbour as halos, bin own + halo agents on a local
+// column-major grid of (w + 2) x nc cells (halo columns 0 and w + 1), and step
+// the own agents (a contiguous range of the sorted array).  Sums are exact
+// fixed point, so the result equals the unsharded step bit for bit.
+struct __align__(16) BoidAgent {
+    float4 s;
+    int32_t id;
+    int32_t role;  // halo: 0 = left halo column of the receiver, 1 = right
+    int32_t pad0, pad1;
+};
+
+struct SlabArgs {
+    BoidsArgs a;
+    const int* col0;  // [world + 1] first cell column of each slab
+    int world, me, c_lo, c_hi;  // my slab [c_lo, c_hi)
+    uint64_t cap;               // send block capacity (agents per destination)
+};
+
+__device__ __forceinline__ int slab_of(int cx, const SlabArgs& g)
+{
+    int lo = 0, hi = g.world - 1;  // largest r with col0[r] <= cx
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (g.col0[mid] <= cx) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Warp-aggregated append to the send block of destination d.
+__device__ __forceinline__ void slab_send(BoidAgent* send, uint32_t* counts, uint64_t cap, int d, const BoidAgent& v)
+{
+    const unsigned peers = __match_any_sync(__activemask(), d);
+    const int leader = __ffs(peers) - 1;
+    const int lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(counts + d, static_cast<uint32_t>(__popc(peers)));
+    base = __shfl_sync(peers, base, leader);
+    const uint32_t pos = base + __popc(peers & ((1u << lane) - 1u));
+    if (pos < cap) send[static_cast<uint64_t>(d) * cap + pos] = v;
+}
+
+// Migration: own agents whose cell column left the slab go to the owner.
+__global__ void slab_route_kernel(const float4* __restrict__ st, const int32_t* __restrict__ ids, int64_t n_own,
+                                  SlabArgs g, float4* __restrict__ keep, int32_t* __restrict__ keep_ids,
+                                  uint32_t* keep_n, BoidAgent* send, uint32_t* counts)
+{
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n_own; p += (int64_t)gridDim.x * blockDim.x) {
+        const float4 x = st[p];
+        const int d = slab_of(cell_coord(x.x, g.a), g);
+        if (d == g.me) {
+            const uint32_t q = atomicAdd(keep_n, 1u);
+            keep[q] = x;
+            keep_ids[q] = ids[p];
+        } else {
+            slab_send(send, counts, g.cap, d, BoidAgent{x, ids[p], 0, 0, 0});
+        }
+    }
+}
+
+__global__ void slab_unpack_kernel(const BoidAgent* __restrict__ in, uint64_t cnt, float4* __restrict__ st,
+                                   int32_t* __restrict__ ids, uint64_t off)
+{
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < static_cast<int64_t>(cnt);
+         k += (int64_t)gridDim.x * blockDim.x) {
+        st[off + k] = in[k].s;
+        ids[off + k] = in[k].id;
+    }
+}
+
+// Halos: the first own column goes to the left neighbour (its right halo), the
+// last to the right neighbour (its left halo); a one-column slab sends both.
+__global__ void slab_halo_kernel(const float4* __restrict__ st, const int32_t* __restrict__ ids, int64_t n_own,
+                                 SlabArgs g, BoidAgent* send, uint32_t* counts)
+{
+    const int left = (g.me + g.world - 1) % g.world, right = (g.me + 1) % g.world;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n_own; p += (int64_t)gridDim.x * blockDim.x) {
+        const float4 x = st[p];
+        const int cx = cell_coord(x.x, g.a);
+        if (cx == g.c_lo) slab_send(send, counts, g.cap, left, BoidAgent{x, ids[p], 1, 0, 0});
+        if (cx == g.c_hi - 1) slab_send(send, counts, g.cap, right, BoidAgent{x, ids[p], 0, 0, 0});
+    }
+}
+
+// Local column-major cell of an own agent (local column 1..w) or a halo agent (0 / w + 1).
+__device__ __forceinline__ int slab_cell(float4 x, int lcol, const BoidsArgs& a)
+{
+    return lcol * a.nc + cell_coord(x.y, a);
+}
+
+__global__ void slab_count_kernel(const float4* __restrict__ st, int64_t n_own, const BoidAgent* __restrict__ halo,
+                                  int64_t n_halo, SlabArgs g, int* __restrict__ cnt, int* __restrict__ cell_of)
+{
+    const int w = g.c_hi - g.c_lo;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n_own + n_halo;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int c;
+        if (p < n_own) {
+            const float4 x = st[p];
+            c = slab_cell(x, cell_coord(x.x, g.a) - g.c_lo + 1, g.a);
+        } else {
+            const BoidAgent h = halo[p - n_own];
+            c = slab_cell(h.s, h.role ? w + 1 : 0, g.a);
+        }
+        cell_of[p] = c;
+        atomicAdd(cnt + c, 1);
+    }
+}
+
+__global__ void slab_scatter_kernel(const float4* __restrict__ st, const int32_t* __restrict__ ids, int64_t n_own,
+                                    const BoidAgent* __restrict__ halo, int64_t n_halo, const int* __restrict__ cell_of,
+                                    int* __restrict__ cursor, float4* __restrict__ sorted, int32_t* __restrict__ sids)
+{
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n_own + n_halo;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int q = atomicAdd(cursor + cell_of[p], 1);
+        if (p < n_own) {
+            sorted[q] = st[p];
+            sids[q] = ids[p];
+        } else {
+            sorted[q] = halo[p - n_own].s;
+            sids[q] = halo[p - n_own].id;
+        }
+    }
+}
+
+// The step for the own agents sorted[own0, own1): G lanes per agent over the
+// 3 x 3 stencil of the local grid (three column runs of three cells; y wraps),
+// minimum image in both coordinates (halos may come across the periodic x edge).
+template <int G>
+__global__ void __launch_bounds__(256, 4) slab_step_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ sids,
+                                                           const int* __restrict__ start, int64_t own0, int64_t own1,
+                                                           SlabArgs g, float4* __restrict__ out,
+                                                           int32_t* __restrict__ out_ids, BoidsSlot* slot, int digest)
+{
+    const BoidsArgs& a = g.a;
+    const float L = a.L, halfL = __fmul_rn(0.5f, a.L), R2 = __fmul_rn(a.R, a.R), rs2 = __fmul_rn(a.rs, a.rs);
+    const int sub = threadIdx.x & (G - 1);
+    const int64_t gid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / G;
+    const int64_t ng = (static_cast<int64_t>(gridDim.x) * blockDim.x) / G;
+    const int64_t n = own1 - own0;
+    const int64_t rounds = (n + ng - 1) / ng;
+    double sp_sum = 0.0, ux_sum = 0.0, uy_sum = 0.0;
+    unsigned long long dig = 0;
+    for (int64_t r = 0; r < rounds; ++r) {
+        const int64_t k = r * ng + gid;
+        const int64_t p = own0 + k;
+        const bool active = k < n;
+        Acc acc{0, 0, 0, 0, 0, 0, 0};
+        float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (active) {
+            me = sorted[p];
+            auto run = [&](int b, int e) {
+                for (int q = b + sub; q < e; q += G)
+                    if (q != p) boid_accumulate<true>(sorted[q], me, L, halfL, R2, rs2, acc);
+            };
+            const int lc = cell_coord(me.x, a) - g.c_lo + 1, cy = cell_coord(me.y, a);
+#pragma unroll 1
+            for (int dc = -1; dc <= 1; ++dc) {
+                const int colb = (lc + dc) * a.nc;
+                if (cy >= 1 && cy + 1 < a.nc) {
+                    run(start[colb + cy - 1], start[colb + cy + 2]);
+                } else {
+#pragma unroll 1
+                    for (int dy = -1; dy <= 1; ++dy) {
+                        int yy = cy + dy;
+                        yy = yy < 0 ? yy + a.nc : (yy >= a.nc ? yy - a.nc : yy);
+                        run(start[colb + yy], start[colb + yy + 1]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) {
+            acc.n += __shfl_xor_sync(0xffffffffu, acc.n, off);
+            acc.sdx += __shfl_xor_sync(0xffffffffu, acc.sdx, off);
+            acc.sdy += __shfl_xor_sync(0xffffffffu, acc.sdy, off);
+            acc.svx += __shfl_xor_sync(0xffffffffu, acc.svx, off);
+            acc.svy += __shfl_xor_sync(0xffffffffu, acc.svy, off);
+            acc.ssx += __shfl_xor_sync(0xffffffffu, acc.ssx, off);
+            acc.ssy += __shfl_xor_sync(0xffffffffu, acc.ssy, off);
+        }
+        float mv = 0.0f;
+        if (acc.n > 0 && sub < 4) {
+            const long long sv = sub == 0 ? acc.sdx : (sub == 1 ? acc.sdy : (sub == 2 ? acc.svx : acc.svy));
+            mv = __double2float_rn(__ddiv_rn(__dmul_rn(static_cast<double>(sv), 1.0 / 16777216.0),
+                                             static_cast<double>(acc.n)));
+        }
+        const float cohx = __shfl_sync(0xffffffffu, mv, 0, G), cohy = __shfl_sync(0xffffffffu, mv, 1, G);
+        const float avx = __shfl_sync(0xffffffffu, mv, 2, G), avy = __shfl_sync(0xffffffffu, mv, 3, G);
+        if (active) {
+            const float4 nx = boid_update_means(me, acc, cohx, cohy, avx, avy, a);
+            if (sub == 0) {
+                out[k] = nx;
+                const int32_t id = sids[p];
+                out_ids[k] = id;
+                if (digest) dig += digest_term(static_cast<unsigned long long>(id), __float_as_uint(nx.x));
+            }
+            if (sub < 3) {
+                const double dvx = static_cast<double>(nx.z), dvy = static_cast<double>(nx.w);
+                const double sp = __dsqrt_rn(__dadd_rn(__dmul_rn(dvx, dvx), __dmul_rn(dvy, dvy)));
+                if (sub == 0) sp_sum += sp;
+                else if (sp > 0.0) {
+                    if (sub == 1) ux_sum += __ddiv_rn(dvx, sp);
+                    else uy_sum += __ddiv_rn(dvy, sp);
+                }
+            }
+        }
+    }
+    __shared__ double red[3][8];
+    __shared__ unsigned long long dred[8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    sp_sum = warp_sum_f64(sp_sum);
+    ux_sum = warp_sum_f64(ux_sum);
+    uy_sum = warp_sum_f64(uy_sum);
+    dig = warp_sum_u64(dig);
+    if (lane == 0) {
+        red[0][wid] = sp_sum;
+        red[1][wid] = ux_sum;
+        red[2][wid] = uy_sum;
+        dred[wid] = dig;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s0 = 0, s1 = 0, s2v = 0;
+        unsigned long long d = 0;
+        for (int w = 0; w < nw; ++w) {
+            s0 += red[0][w];
+            s1 += red[1][w];
+            s2v += red[2][w];
+            d += dred[w];
+        }
+        atomicAdd(&slot->mean_speed, s0);
+        atomicAdd(&slot->polar_x, s1);
+        atomicAdd(&slot->polar_y, s2v);
+        if (digest) atomicAdd(&slot->digest, d);
+    }
+}
+
+// Id-ordered column (bit patterns) of the own agents, zero elsewhere: summed over
+// the ranks it is the global column (each id is owned by exactly one rank).
+__global__ void slab_column_kernel(const float4* __restrict__ st, const int32_t* __restrict__ ids, int64_t n_own, int k,
+                                   unsigned long long* __restrict__ out)
+{
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n_own; p += (int64_t)gridDim.x * blockDim.x) {
+        const float4 s = st[p];
+        const float v = k == 0 ? s.x : (k == 1 ? s.y : (k == 2 ? s.z : s.w));
+        out[ids[p]] = __float_as_uint(v);
+    }
+}
+
+__global__ void u64_to_f32_kernel(const unsigned long long* __restrict__ in, int64_t n, float* __restrict__ out)
+{
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+        out[p] = __uint_as_float(static_cast<uint32_t>(in[p]));
+}
+
+// Own agents of a freshly initialised (or rewritten) full population.
+__global__ void slab_pick_kernel(const float4* __restrict__ st, const int32_t* __restrict__ ids, int64_t n, SlabArgs g,
+                                 float4* __restrict__ own, int32_t* __restrict__ own_ids, uint32_t* n_own)
+{
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const float4 x = st[p];
+        if (slab_of(cell_coord(x.x, g.a), g) == g.me) {
+            const uint32_t q = atomicAdd(n_own, 1u);
+            own[q] = x;
+            own_ids[q] = ids[p];
+        }
+    }
+}
+
 }  // namespace
 
 class BoidsModel final : public Model {
@@ -1061,8 +1338,339 @@ public:
     }
 };
 
+// Sharded Boids (NEXT-3): see the slab kernels above.  Columns and digests
+// are global (collective reads); metrics are summed over the ranks.
+class BoidsShardModel final : public Model {
+public:
+    int64_t n = 0;
+    amber_boids_params p{};
+    BoidsArgs ba{};
+    ShardComm* sc = nullptr;
+    std::vector<int> col0;      // [world + 1]
+    DevBuf<int> d_col0;
+    int c_lo = 0, c_hi = 0, w = 0;
+    int64_t n_own = 0, cap = 0;
+    DevBuf<float4> st, st2, sorted;
+    DevBuf<int32_t> ids, ids2, sids, cell_of;
+    DevBuf<BoidAgent> send, recv;
+    DevBuf<uint32_t> counts, keep_n;
+    DevBuf<int> cnt, start, cursor;
+    DevBuf<char> scan_tmp;
+    size_t scan_bytes = 0;
+    int ncell_loc = 0;
+    DevBuf<BoidsSlot> ring;
+    int64_t m_first = 0;
+
+    BoidsShardModel(int64_t n_, const amber_boids_params& p_, uint64_t seed, const amber_runtime* r)
+    {
+        rt.init(r);
+        n = n_;
+        p = p_;
+        AMBER_REQUIRE(n >= 1 && n < (1ll << 31), "Boids needs 1 <= n_agents < 2^31");
+        AMBER_REQUIRE(p.L > 0 && p.R > 0 && p.rs >= 0 && p.rs <= p.R && p.vmax > 0 && p.dt >= 0,
+                      "Boids params out of range (need L, R, vmax > 0, 0 <= rs <= R, dt >= 0)");
+        AMBER_REQUIRE(p.R < 0.5f * p.L && p.vmax * p.dt < 0.5f * p.L, "Boids needs R < L/2 and vmax*dt < L/2");
+        ba = BoidsArgs{p.L, p.R, p.rs, p.wc, p.wa, p.ws, p.vmax, p.dt, 0, 0.f};
+        double nc = std::floor(static_cast<double>(p.L) / (static_cast<double>(p.R) * 1.001));
+        nc = std::min(nc, 4096.0);
+        AMBER_REQUIRE(nc >= 3 && nc >= rt.world, "sharded Boids needs >= 3 cells per side and >= 1 cell column per rank");
+        ba.nc = static_cast<int>(nc);
+        ba.inv_cs = static_cast<float>(ba.nc / static_cast<double>(p.L));
+        col0.resize(rt.world + 1);
+        for (int q = 0; q <= rt.world; ++q) col0[q] = static_cast<int>(static_cast<int64_t>(q) * ba.nc / rt.world);
+        c_lo = col0[rt.rank];
+        c_hi = col0[rt.rank + 1];
+        w = c_hi - c_lo;
+        ncell_loc = (w + 2) * ba.nc;
+        d_col0.allocate(&rt, rt.world + 1);
+        AMBER_CUDA(cudaMemcpyAsync(d_col0.p, col0.data(), col0.size() * sizeof(int), cudaMemcpyHostToDevice, rt.stream));
+        cap = n;  // per-destination send capacity: any distribution of the agents fits
+        for (auto* b : {&st, &st2}) b->allocate(&rt, n);
+        for (auto* b : {&ids, &ids2}) b->allocate(&rt, n);
+        sorted.allocate(&rt, 2 * n);
+        sids.allocate(&rt, 2 * n);
+        cell_of.allocate(&rt, 2 * n);
+        send.allocate(&rt, static_cast<size_t>(rt.world) * cap);
+        recv.allocate(&rt, n);
+        counts.allocate(&rt, rt.world);
+        keep_n.allocate(&rt, 1);
+        cnt.allocate(&rt, ncell_loc + 1);
+        cnt.zero_async(rt.stream);
+        start.allocate(&rt, ncell_loc + 1);
+        cursor.allocate(&rt, ncell_loc + 1);
+        AMBER_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, cnt.p, start.p, ncell_loc + 1, rt.stream));
+        scan_tmp.allocate(&rt, scan_bytes + 16);
+        ring.allocate(&rt, metrics_cap);
+        ring.zero_async(rt.stream);
+        // every rank draws the full seeded population (B1) and keeps its slab
+        boids_init_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(philox_key(seed), n, p.L, st2.p, ids2.p);
+        check_launch("boids_init_kernel");
+        pick(st2.p, ids2.p);
+        sc = make_shard_comm(rt, r);
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    }
+
+    ~BoidsShardModel() override
+    {
+        if (rt.stream) cudaStreamSynchronize(rt.stream);
+        for (auto* b : {&st, &st2, &sorted}) b->reset();
+        for (auto* b : {&ids, &ids2, &sids, &cell_of}) b->reset();
+        send.reset(); recv.reset(); counts.reset(); keep_n.reset(); cnt.reset(); start.reset(); cursor.reset();
+        scan_tmp.reset(); ring.reset(); d_col0.reset();
+        if (sc) destroy_shard_comm(sc);
+        rt.destroy();
+    }
+
+    SlabArgs args() const { return SlabArgs{ba, d_col0.p, rt.world, rt.rank, c_lo, c_hi, static_cast<uint64_t>(cap)}; }
+    int grid_for(int64_t items) const
+    {
+        return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), rt.num_sms * 16)));
+    }
+
+    // own agents of a full id-ordered population (st_full, ids_full)
+    void pick(const float4* st_full, const int32_t* ids_full)
+    {
+        keep_n.zero_async(rt.stream);
+        slab_pick_kernel<<<grid_for(n), 256, 0, rt.stream>>>(st_full, ids_full, n, args(), st.p, ids.p, keep_n.p);
+        check_launch("slab_pick_kernel");
+        uint32_t h = 0;
+        AMBER_CUDA(cudaMemcpyAsync(&h, keep_n.p, 4, cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        n_own = h;
+    }
+
+    void step(int64_t nsteps) override
+    {
+        AMBER_REQUIRE(nsteps >= 0, "n_steps must be >= 0");
+        const SlabArgs g = args();
+        for (int64_t k = 0; k < nsteps; ++k) {
+            boids_zero_slots<<<1, 32, 0, rt.stream>>>(ring.p, metrics_cap, t, 1);
+            check_launch("boids_zero_slots");
+            // 1) migration
+            counts.zero_async(rt.stream);
+            keep_n.zero_async(rt.stream);
+            prof.launch(rt.stream, "boids_slab_route", [&] {
+                slab_route_kernel<<<grid_for(n_own), 256, 0, rt.stream>>>(st.p, ids.p, n_own, g, st2.p, ids2.p,
+                                                                           keep_n.p, send.p, counts.p);
+            });
+            check_launch("slab_route_kernel");
+            const uint64_t got = shard_alltoallv(sc, rt, send.p, counts.p, cap, sizeof(BoidAgent), recv.p, n);
+            uint32_t kept = 0;
+            AMBER_CUDA(cudaMemcpyAsync(&kept, keep_n.p, 4, cudaMemcpyDeviceToHost, rt.stream));
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            if (got)
+                slab_unpack_kernel<<<grid_for(got), 256, 0, rt.stream>>>(recv.p, got, st2.p, ids2.p, kept);
+            n_own = kept + static_cast<int64_t>(got);
+            std::swap(st.p, st2.p);
+            std::swap(ids.p, ids2.p);
+            // 2) halos
+            counts.zero_async(rt.stream);
+            prof.launch(rt.stream, "boids_slab_halo", [&] {
+                slab_halo_kernel<<<grid_for(n_own), 256, 0, rt.stream>>>(st.p, ids.p, n_own, g, send.p, counts.p);
+            });
+            check_launch("slab_halo_kernel");
+            const int64_t n_halo = static_cast<int64_t>(
+                shard_alltoallv(sc, rt, send.p, counts.p, cap, sizeof(BoidAgent), recv.p, n));
+            // 3) local binning (column-major, halo columns 0 and w + 1)
+            const int64_t tot = n_own + n_halo;
+            prof.launch(rt.stream, "boids_slab_bin", [&] {
+                slab_count_kernel<<<grid_for(tot), 256, 0, rt.stream>>>(st.p, n_own, recv.p, n_halo, g, cnt.p,
+                                                                         cell_of.p);
+                AMBER_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp.p, scan_bytes, cnt.p, start.p, ncell_loc + 1,
+                                                         rt.stream));
+                AMBER_CUDA(cudaMemcpyAsync(cursor.p, start.p, static_cast<size_t>(ncell_loc) * sizeof(int),
+                                           cudaMemcpyDeviceToDevice, rt.stream));
+                AMBER_CUDA(cudaMemsetAsync(cnt.p, 0, static_cast<size_t>(ncell_loc) * sizeof(int), rt.stream));
+                slab_scatter_kernel<<<grid_for(tot), 256, 0, rt.stream>>>(st.p, ids.p, n_own, recv.p, n_halo,
+                                                                           cell_of.p, cursor.p, sorted.p, sids.p);
+            });
+            check_launch("slab_scatter_kernel");
+            // 4) the step of the own agents: sorted[start[nc], start[(w + 1) nc])
+            int own_rng[2] = {0, 0};
+            AMBER_CUDA(cudaMemcpyAsync(&own_rng[0], start.p + ba.nc, 4, cudaMemcpyDeviceToHost, rt.stream));
+            AMBER_CUDA(cudaMemcpyAsync(&own_rng[1], start.p + (w + 1) * ba.nc, 4, cudaMemcpyDeviceToHost, rt.stream));
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            AMBER_REQUIRE(own_rng[1] - own_rng[0] == n_own, "sharded Boids: own agents outside the slab columns");
+            const int gsteps = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_own * 8, 256),
+                                                                                        rt.num_sms * 8)));
+            BoidsSlot* sl = ring.p + (t % metrics_cap);
+            const int dg = digest_on ? 1 : 0;
+            prof.launch(rt.stream, "boids_slab_step", [&] {
+                slab_step_kernel<8><<<gsteps, 256, 0, rt.stream>>>(sorted.p, sids.p, start.p, own_rng[0], own_rng[1], g,
+                                                                    st.p, ids.p, sl, dg);
+            });
+            check_launch("slab_step_kernel");
+            ++t;
+        }
+    }
+
+    int col_index(const std::string& k) const
+    {
+        if (k == "pos_x") return 0;
+        if (k == "pos_y") return 1;
+        if (k == "vel_x") return 2;
+        if (k == "vel_y") return 3;
+        return -1;
+    }
+
+    bool column_info(const char* name, amber_dtype* dt, int64_t* glen, int64_t* off, int64_t* len) override
+    {
+        if (col_index(name) < 0) return false;
+        if (dt) *dt = AMBER_F32;
+        if (glen) *glen = n;
+        if (off) *off = 0;
+        if (len) *len = n;  // reads are collective and return the whole id-ordered column
+        return true;
+    }
+
+    // Global id-ordered column on every rank (collective): own values by id, zero
+    // elsewhere, summed over the ranks as bit patterns.
+    void gather_column(int k, unsigned long long* dcol)
+    {
+        AMBER_CUDA(cudaMemsetAsync(dcol, 0, n * 8, rt.stream));
+        slab_column_kernel<<<grid_for(n_own), 256, 0, rt.stream>>>(st.p, ids.p, n_own, k, dcol);
+        check_launch("slab_column_kernel");
+        shard_allreduce_u64(sc, rt, dcol, static_cast<size_t>(n));
+    }
+
+    void read_column(const char* name, void* dst, size_t bytes, bool on_dev) override
+    {
+        const int k = col_index(name);
+        if (k < 0) fail(AMBER_E_UNKNOWN_NAME, std::string("no column ") + name);
+        if (bytes < static_cast<size_t>(n) * 4) fail(AMBER_E_BUFFER_TOO_SMALL, "dst too small");
+        DevBuf<unsigned long long> col;
+        col.allocate(&rt, n);
+        DevBuf<float> f;
+        f.allocate(&rt, n);
+        gather_column(k, col.p);
+        u64_to_f32_kernel<<<grid_for(n), 256, 0, rt.stream>>>(col.p, n, f.p);
+        check_launch("u64_to_f32_kernel");
+        copy_out(rt, dst, f.p, n * 4, on_dev);
+    }
+
+    // Collective: every rank passes the same whole id-ordered column; agents whose
+    // position changes slabs migrate at the next step.
+    void write_column(const char* name, const void* src, size_t bytes, bool on_dev) override
+    {
+        const int k = col_index(name);
+        if (k < 0) fail(AMBER_E_UNKNOWN_NAME, std::string("no column ") + name);
+        if (bytes < static_cast<size_t>(n) * 4) fail(AMBER_E_BUFFER_TOO_SMALL, "src too small");
+        DevBuf<float> f;
+        f.allocate(&rt, n);
+        copy_in(rt, f.p, src, n * 4, on_dev);
+        boids_put_column<<<grid_for(n_own), 256, 0, rt.stream>>>(st.p, ids.p, n_own, k, f.p);
+        check_launch("boids_put_column");
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    }
+
+    void read_metrics(const char* name, void* dst, size_t bytes, int64_t* n_out) override
+    {
+        std::string k(name);
+        if (k != "mean_speed" && k != "polarisation" && !(k == "digest" && digest_on))
+            fail(AMBER_E_UNKNOWN_NAME, "no metric " + k);
+        std::vector<BoidsSlot> h(metrics_cap);
+        AMBER_CUDA(cudaMemcpyAsync(h.data(), ring.p, metrics_cap * sizeof(BoidsSlot), cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        const int64_t first = std::max(m_first, t - metrics_cap + 1);
+        const int64_t cnt_ = std::max<int64_t>(t - first, 0);
+        if (bytes < static_cast<size_t>(cnt_) * 8) fail(AMBER_E_BUFFER_TOO_SMALL, "metrics dst too small");
+        // sum the per-rank slots (doubles as bit patterns would not add: gather them instead)
+        std::vector<unsigned long long> mine(4 * cnt_);
+        for (int64_t s = first; s < t; ++s) {
+            const BoidsSlot& x = h[s % metrics_cap];
+            std::memcpy(&mine[4 * (s - first)], &x, sizeof(BoidsSlot));
+        }
+        std::vector<double> all;
+        if (cnt_) {
+            DevBuf<unsigned long long> d;
+            d.allocate(&rt, 4 * cnt_ * rt.world);
+            DevBuf<unsigned long long> m;
+            m.allocate(&rt, 4 * cnt_);
+            AMBER_CUDA(cudaMemcpyAsync(m.p, mine.data(), mine.size() * 8, cudaMemcpyHostToDevice, rt.stream));
+            shard_allgather_u32(sc, rt, reinterpret_cast<const uint32_t*>(m.p), reinterpret_cast<uint32_t*>(d.p),
+                                8 * cnt_);
+            all.resize(4 * cnt_ * rt.world);
+            AMBER_CUDA(cudaMemcpyAsync(all.data(), d.p, all.size() * 8, cudaMemcpyDeviceToHost, rt.stream));
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        }
+        for (int64_t s = 0; s < cnt_; ++s) {
+            double sp = 0, px = 0, py = 0;
+            unsigned long long dg = 0;
+            for (int q = 0; q < rt.world; ++q) {
+                const double* v = all.data() + (static_cast<size_t>(q) * cnt_ + s) * 4;
+                sp += v[0];
+                px += v[1];
+                py += v[2];
+                unsigned long long u;
+                std::memcpy(&u, v + 3, 8);
+                dg += u;
+            }
+            if (k == "mean_speed") static_cast<double*>(dst)[s] = sp / static_cast<double>(n);
+            else if (k == "polarisation") static_cast<double*>(dst)[s] = std::sqrt(px * px + py * py) / static_cast<double>(n);
+            else static_cast<unsigned long long*>(dst)[s] = dg;
+        }
+        if (n_out) *n_out = cnt_;
+    }
+
+    void reset_metrics() override
+    {
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        m_first = t;
+    }
+
+    uint64_t digest(const char* name) override
+    {
+        const int k = col_index(name);
+        if (k < 0) fail(AMBER_E_UNKNOWN_NAME, std::string("no column ") + name);
+        DevBuf<unsigned long long> col;
+        col.allocate(&rt, n);
+        gather_column(k, col.p);
+        DevBuf<uint32_t> c32;
+        c32.allocate(&rt, n);
+        u64_to_f32_kernel<<<grid_for(n), 256, 0, rt.stream>>>(col.p, n, reinterpret_cast<float*>(c32.p));
+        check_launch("u64_to_f32_kernel");
+        return device_digest_u32(rt, c32.p, n, 0);
+    }
+
+    void set_step(int64_t s) override
+    {
+        AMBER_REQUIRE(s >= 0, "step out of range");
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        t = s;
+        m_first = s;
+    }
+
+    bool set_option(const char* key, int64_t v) override
+    {
+        std::string k(key);
+        if (k == "metrics_capacity") {
+            AMBER_REQUIRE(v >= 16, "metrics_capacity must be >= 16");
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            metrics_cap = v;
+            ring.allocate(&rt, metrics_cap);
+            ring.zero_async(rt.stream);
+            m_first = t;
+            return true;
+        }
+        return Model::set_option(key, v);
+    }
+
+    bool get_option(const char* key, int64_t* v) override
+    {
+        std::string k(key);
+        if (k == "cells_per_side") { *v = ba.nc; return true; }
+        if (k == "own_agents") { *v = n_own; return true; }
+        if (k == "slab_columns") { *v = w; return true; }
+        return Model::get_option(key, v);
+    }
+};
+
 Model* make_boids(int64_t n, const amber_boids_params& p, uint64_t seed, const amber_runtime* rt)
 {
+    // AMBER_TEST_FORCE_EXCHANGE=1 with a unique id: the sharded path with one rank
+    const char* force = getenv("AMBER_TEST_FORCE_EXCHANGE");
+    if ((rt && rt->world > 1) || (force && force[0] == '1' && rt && rt->nccl_unique_id))
+        return new BoidsShardModel(n, p, seed, rt);
     return new BoidsModel(n, p, seed, rt);
 }
 

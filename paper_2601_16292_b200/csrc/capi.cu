@@ -60,9 +60,9 @@ int amber_model_create(amber_kind kind, int64_t n_agents, const void* params, si
         *out = nullptr;
         need(params, "params");
         AMBER_REQUIRE(n_agents >= 1, "n_agents must be >= 1");
-        if (rt && rt->world > 1 && kind != AMBER_WEALTH && kind != AMBER_SIR_GRAPH)
-            amber::fail(AMBER_E_UNSUPPORTED,
-                        "only AMBER_WEALTH and AMBER_SIR_GRAPH are sharded across ranks (others: replicas/amber_sweep)");
+        if (rt && rt->world > 1 && kind != AMBER_WEALTH && kind != AMBER_SIR_GRAPH && kind != AMBER_BOIDS)
+            amber::fail(AMBER_E_UNSUPPORTED, "only AMBER_WEALTH, AMBER_SIR_GRAPH and AMBER_BOIDS are sharded across "
+                                             "ranks (others: replicas / amber_sweep)");
         amber::Model* m = nullptr;
         switch (kind) {
             case AMBER_WEALTH:

@@ -383,6 +383,70 @@ void shard_allgather_u32(ShardComm* c, Runtime& rt, const uint32_t* send, uint32
     nccl_check(nccl().AllGather(send, recv, count, ncclUint32, c->comm->comm, rt.stream), "ncclAllGather");
 }
 
+// Variable all-to-all of fixed-size elements.  send holds `world` blocks of
+// `cap` elements (block p for rank p), d_counts[p] elements of block p are
+// valid.  The received elements are stored contiguously in peer order in recv
+// (capacity recv_cap elements); returns their number.  Synchronising.
+uint64_t shard_alltoallv(ShardComm* c, Runtime& rt, const void* send, const uint32_t* d_counts, size_t cap,
+                         size_t elem, void* recv, size_t recv_cap)
+{
+    const int W = c->world, me = c->rank;
+    std::vector<uint32_t> hs(W);
+    AMBER_CUDA(cudaMemcpyAsync(hs.data(), d_counts, W * sizeof(uint32_t), cudaMemcpyDeviceToHost, rt.stream));
+    AMBER_CUDA(cudaStreamSynchronize(rt.stream));  // counts and send blocks complete
+    for (int p = 0; p < W; ++p)
+        if (hs[p] > cap) fail(AMBER_E_CUDA, "shard exchange: send bucket overflow (capacity " + std::to_string(cap) + ")");
+    const char* sb = static_cast<const char*>(send);
+    char* rb = static_cast<char*>(recv);
+    if (c->hub) {
+        LoopbackHub& h = *c->hub;
+        h.counts[me].assign(hs.begin(), hs.end());
+        h.send_ids[me] = static_cast<const uint32_t*>(send);
+        h.send_cap[me] = cap;
+        h.barrier();
+        uint64_t total = 0;
+        for (int p = 0; p < W; ++p) {
+            const uint64_t k = h.counts[p][me];
+            if (total + k > recv_cap) fail(AMBER_E_CUDA, "shard exchange: receive buffer overflow");
+            if (k)
+                AMBER_CUDA(cudaMemcpyAsync(rb + total * elem,
+                                           reinterpret_cast<const char*>(h.send_ids[p]) + static_cast<uint64_t>(me) * cap * elem,
+                                           k * elem, cudaMemcpyDeviceToDevice, rt.stream));
+            total += k;
+        }
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        h.barrier();  // peers may now reuse their send blocks
+        return total;
+    }
+    NcclApi& api = nccl();
+    DevBuf<uint32_t> rc;
+    rc.allocate(&rt, W);
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    for (int p = 0; p < W; ++p) {
+        nccl_check(api.Send(d_counts + p, 1, ncclUint32, p, c->comm->comm, rt.stream), "ncclSend(count)");
+        nccl_check(api.Recv(rc.p + p, 1, ncclUint32, p, c->comm->comm, rt.stream), "ncclRecv(count)");
+    }
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+    std::vector<uint32_t> hr(W);
+    AMBER_CUDA(cudaMemcpyAsync(hr.data(), rc.p, W * sizeof(uint32_t), cudaMemcpyDeviceToHost, rt.stream));
+    AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    uint64_t total = 0;
+    for (int p = 0; p < W; ++p) total += hr[p];
+    if (total > recv_cap) fail(AMBER_E_CUDA, "shard exchange: receive buffer overflow");
+    uint64_t off = 0;
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    for (int p = 0; p < W; ++p) {
+        if (hs[p])
+            nccl_check(api.Send(sb + static_cast<uint64_t>(p) * cap * elem, hs[p] * elem, ncclChar, p, c->comm->comm,
+                                rt.stream), "ncclSend");
+        if (hr[p]) nccl_check(api.Recv(rb + off * elem, hr[p] * elem, ncclChar, p, c->comm->comm, rt.stream), "ncclRecv");
+        off += hr[p];
+    }
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+    AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    return total;
+}
+
 // In-place sum over ranks of n device values.
 void shard_allreduce_u64(ShardComm* c, Runtime& rt, unsigned long long* d, size_t n)
 {

@@ -256,6 +256,8 @@ ShardComm* make_shard_comm(Runtime& rt, const amber_runtime* r);
 void destroy_shard_comm(ShardComm* c);
 void shard_allgather_u32(ShardComm* c, Runtime& rt, const uint32_t* send, uint32_t* recv, size_t count);
 void shard_allreduce_u64(ShardComm* c, Runtime& rt, unsigned long long* d, size_t n);
+uint64_t shard_alltoallv(ShardComm* c, Runtime& rt, const void* send, const uint32_t* d_counts, size_t cap,
+                         size_t elem, void* recv, size_t recv_cap);
 
 // Multi-GPU partitions (host logic).  Wealth: contiguous id
 // ranges of ceil(n/world) rounded up to 8 agents.  Sweep: replicate blocks.

@@ -14,7 +14,11 @@ tests cover what the ranks must agree on before any kernel runs:
   * the sharded SIR step (NEXT-3): 32-aligned id ranges (amber_sir_shard_range),
     local I-bitmap words all-gathered every step, each rank pulling its own rows
     against the global bitmap with globally keyed draws, equals the unsharded
-    oracle run bit for bit.
+    oracle run bit for bit;
+  * the sharded Boids step (NEXT-3): x-slabs of whole cell columns, agents
+    migrating to the slab of their cell column and the edge columns exchanged
+    as halos; each rank steps its own agents from own + halo agents only, and
+    the union equals the unsharded oracle run bit for bit.
 """
 import os
 import socket
@@ -156,6 +160,55 @@ def _sharded_sir(rank, world):
     dist.all_gather_object(out, (lo, x.tolist()))
     ref = oracle.sir_run(rp, col, st0, seed, beta, gamma, 0, steps)[0]
     return out, ref.tolist()
+
+
+def _sharded_boids(rank, world):
+    import oracle
+    L, R, n, seed, steps = 120.0, 10.0, 800, 4, 8
+    P = oracle.boids_params(L=L, R=R)
+    nc = int(np.floor(L / (R * 1.001)))
+    inv_cs = np.float32(nc / L)
+    col0 = [q * nc // world for q in range(world + 1)]
+    c_lo, c_hi = col0[rank], col0[rank + 1]
+
+    def col_of(x):  # the kernels' cell_coord: float32 product, truncated, clamped
+        return np.clip((np.asarray(x, np.float32) * inv_cs).astype(np.int64), 0, nc - 1)
+
+    def owner(x):
+        return np.searchsorted(np.array(col0[1:]), col_of(x), side="right")
+
+    full = [np.asarray(a, np.float32) for a in oracle.boids_init(n, L, seed)]
+    ids = np.arange(n)
+    own = ids[owner(full[0]) == rank]
+    st = {int(i): tuple(float(a[i]) for a in full) for i in own}  # id -> (x, y, vx, vy) as float32 values
+    for t in range(steps):
+        # migration (to the slab of the cell column) and halos (edge columns), via all_gather
+        mine = [(i, v) for i, v in st.items()]
+        everyone = [None] * world
+        dist.all_gather_object(everyone, mine)
+        st = {i: v for part in everyone for i, v in part if owner(np.float32(v[0])) == rank}
+        left_col, right_col = (c_lo - 1) % nc, c_hi % nc
+        halo = {i: v for part in everyone for i, v in part
+                if i not in st and col_of(np.float32(v[0])) in (left_col, right_col)}
+        # step own agents from own + halo agents only (a smaller population in the same box)
+        loc_ids = list(st) + list(halo)
+        loc = [np.array([(st.get(i) or halo[i])[k] for i in loc_ids], np.float32) for k in range(4)]
+        out = oracle.boids_step_sample(loc, P, np.arange(len(st)))
+        st = {i: tuple(float(out[k][j]) for k in range(4)) for j, i in enumerate(loc_ids[:len(st)])}
+    everyone = [None] * world
+    dist.all_gather_object(everyone, list(st.items()))
+    ref = oracle.boids_run(tuple(full), P, steps)[0]
+    return everyone, [np.asarray(a, np.float32).tolist() for a in ref]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_boids_slab_halo_equals_oracle(world):
+    parts, ref = run_world(world, _sharded_boids)[0]
+    got = dict(kv for part in parts for kv in part)
+    assert sorted(got) == list(range(len(ref[0])))
+    for k in range(4):
+        col = np.array([got[i][k] for i in range(len(ref[0]))], np.float32)
+        assert np.array_equal(col.view(np.uint32), np.array(ref[k], np.float32).view(np.uint32))
 
 
 @pytest.mark.parametrize("world", [2, 4])

@@ -12,7 +12,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-from paper_2601_16292_b200 import Model, loopback_id, shard_range, sir_params, sweep, wealth_params
+from paper_2601_16292_b200 import Model, boids_params, loopback_id, shard_range, sir_params, sweep, wealth_params
 from paper_2601_16292_b200.workloads import C5_SWEEP, sweep_replicates
 
 
@@ -186,3 +186,81 @@ def test_sir_nccl_plumbing_single_rank(orc, monkeypatch):
     assert np.array_equal(m.read_column("state"), ref)
     assert np.array_equal(m.metrics("I"), counts[:, 1])
     assert m.digest("state") == orc.digest(ref)
+
+
+BKEYS = ("L", "R", "rs", "wc", "wa", "ws", "vmax", "dt")
+
+
+def sharded_boids(world, cfg):
+    uid = loopback_id()
+    p = boids_params(*[cfg[k] for k in BKEYS])
+    return [Model("boids", cfg["n"], p, cfg["seed"], rank=r, world=world, unique_id=uid) for r in range(world)]
+
+
+def boids_state(ms):
+    # collective column reads: every rank returns the whole id-ordered column
+    cols = []
+    for c in ("pos_x", "pos_y", "vel_x", "vel_y"):
+        got = par(ms, lambda m: m.read_column(c))
+        assert all(np.array_equal(g.view(np.uint32), got[0].view(np.uint32)) for g in got)
+        cols.append(got[0])
+    return cols
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_sharded_boids_equals_oracle(orc, world):
+    # NEXT-3: x-slabs of cell columns, migration + halo exchange every step;
+    # exact fixed-point sums -> bit-identical to the unsharded oracle
+    cfg = dict(n=6000, L=200.0, R=10.0, rs=2.0, wc=0.01, wa=0.125, ws=0.05, vmax=2.0, dt=1.0, seed=3)
+    steps = 25
+    P = orc.boids_params(**{k: cfg[k] for k in BKEYS})
+    ref = orc.boids_run(orc.boids_init(cfg["n"], cfg["L"], cfg["seed"]), P, steps)
+    ms = sharded_boids(world, cfg)
+    own0 = par(ms, lambda m: m.get_option("own_agents"))
+    assert sum(own0) == cfg["n"]
+    for m in ms:
+        m.set_option("digest", 1)
+    par(ms, lambda m: (m.step(1), m.step(steps - 1)))
+    got = boids_state(ms)
+    want = ref[0]
+    for a, b in zip(got, want):
+        assert np.array_equal(a.view(np.uint32), np.asarray(b, np.float32).view(np.uint32))
+    assert sum(par(ms, lambda m: m.get_option("own_agents"))) == cfg["n"]  # agents migrated, none lost
+    # global observables agree on every rank and with one GPU
+    one = Model("boids", cfg["n"], boids_params(*[cfg[k] for k in BKEYS]), cfg["seed"])
+    one.set_option("digest", 1)
+    one.step(steps)
+    for v in par(ms, lambda m: m.metrics("digest")):
+        assert np.array_equal(v, one.metrics("digest"))
+    for v in par(ms, lambda m: m.metrics("mean_speed")):
+        assert np.allclose(v, one.metrics("mean_speed"), rtol=1e-12, atol=0)
+    dg = par(ms, lambda m: m.digest("pos_x"))
+    assert all(d == one.digest("pos_x") for d in dg)
+
+
+def test_sharded_boids_column_write_and_single_rank_nccl(orc, monkeypatch):
+    cfg = dict(n=3000, L=150.0, R=10.0, rs=2.0, wc=0.01, wa=0.125, ws=0.05, vmax=2.0, dt=1.0, seed=9)
+    one = Model("boids", cfg["n"], boids_params(*[cfg[k] for k in BKEYS]), cfg["seed"])
+    one.step(5)
+    mid = [one.read_column(c) for c in ("pos_x", "pos_y", "vel_x", "vel_y")]
+    one.step(10)
+    want = [one.read_column(c) for c in ("pos_x", "pos_y", "vel_x", "vel_y")]
+    ms = sharded_boids(3, cfg)  # fresh shards, state restored from the id-ordered columns
+
+    def restore(m):
+        for c, v in zip(("pos_x", "pos_y", "vel_x", "vel_y"), mid):
+            m.write_column(c, v)
+        m.set_step(5)
+        m.step(10)
+    par(ms, restore)
+    for a, b in zip(boids_state(ms), want):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    # one-rank NCCL communicator: ncclSend/ncclRecv of the migration and halo
+    # buffers (self exchange), ncclAllGather of the metrics, ncclAllReduce of columns
+    from paper_2601_16292_b200 import nccl_unique_id
+    monkeypatch.setenv("AMBER_TEST_FORCE_EXCHANGE", "1")
+    m = Model("boids", cfg["n"], boids_params(*[cfg[k] for k in BKEYS]), cfg["seed"], unique_id=nccl_unique_id())
+    assert m.get_option("slab_columns") == m.get_option("cells_per_side")
+    m.step(15)
+    for c, b in zip(("pos_x", "pos_y", "vel_x", "vel_y"), want):
+        assert np.array_equal(m.read_column(c).view(np.uint32), b.view(np.uint32))
