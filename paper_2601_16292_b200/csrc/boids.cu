@@ -73,9 +73,15 @@ __global__ void boids_init_kernel(PhiloxKey key, int64_t n, float L, float4* st,
     }
 }
 
+struct BoidsSlot {
+    double mean_speed, polar_x, polar_y;
+    unsigned long long digest;
+};
+
 __global__ void boids_count_kernel(const float4* __restrict__ st, int64_t n, BoidsArgs a, int* __restrict__ cnt,
-                                   int* __restrict__ cell_of)
+                                   int* __restrict__ cell_of, BoidsSlot* slot_zero)
 {
+    if (slot_zero && blockIdx.x == 0 && threadIdx.x == 0) *slot_zero = BoidsSlot{0.0, 0.0, 0.0, 0ull};  // this step's record
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
         const float4 s = st[p];
         const int c = cell_coord(s.y, a) * a.nc + cell_coord(s.x, a);
@@ -87,24 +93,52 @@ __global__ void boids_count_kernel(const float4* __restrict__ st, int64_t n, Boi
 // Exclusive scan of the cell counts by one CTA: each thread owns a contiguous
 // run of cells (sequential sum), one block-wide scan of the run totals, then a
 // sequential write-back.  Also zeroes the counts for the next step.
+// One CTA: warp w owns a contiguous segment of cells, read 32 at a time
+// (coalesced).  Pass 1 sums each segment, warp 0 scans the 32 segment totals,
+// pass 2 re-walks each segment with a warp inclusive scan plus a running carry
+// and writes start / cursor and the zeroed counts.
 __global__ void __launch_bounds__(1024) boids_scan_kernel(int* cnt, int* start, int* cursor, int ncell)
 {
-    using Scan = cub::BlockScan<int, 1024>;
-    __shared__ typename Scan::TempStorage tmp;
-    const int per = (ncell + 1023) / 1024;
-    const int c0 = threadIdx.x * per;
+    __shared__ int seg_off[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per = ((ncell + 31) / 32 + 31) & ~31;  // cells per warp segment (multiple of 32)
+    const int s0 = warp * per, s1 = min(s0 + per, ncell);
     int sum = 0;
-    for (int c = c0; c < c0 + per && c < ncell; ++c) sum += cnt[c];
-    int ex, agg;
-    Scan(tmp).ExclusiveSum(sum, ex, agg);
-    for (int c = c0; c < c0 + per && c < ncell; ++c) {
-        const int v = cnt[c];
-        start[c] = ex;
-        cursor[c] = ex;
-        cnt[c] = 0;
-        ex += v;
+#pragma unroll 4
+    for (int c = s0 + lane; c < s1; c += 32) sum += cnt[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) seg_off[warp] = sum;
+    __syncthreads();
+    if (warp == 0) {
+        const int v = seg_off[lane];
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        seg_off[lane] = incl - v;
+        if (lane == 31) start[ncell] = incl;
     }
-    if (threadIdx.x == 0) start[ncell] = agg;
+    __syncthreads();
+    int carry = seg_off[warp];
+    for (int b = s0; b < s1; b += 32) {
+        const int c = b + lane;
+        const int v = c < s1 ? cnt[c] : 0;
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        if (c < s1) {
+            start[c] = carry + incl - v;
+            cursor[c] = carry + incl - v;
+            cnt[c] = 0;
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
 }
 
 __global__ void boids_scatter_kernel(const float4* __restrict__ st, const int32_t* __restrict__ ids, int64_t n,
@@ -131,10 +165,6 @@ __device__ __forceinline__ float min_image(float d, float L, float halfL)
     return d;
 }
 
-struct BoidsSlot {
-    double mean_speed, polar_x, polar_y;
-    unsigned long long digest;
-};
 
 // B2-B6 for every agent (sorted order in, sorted order out).
 __global__ void __launch_bounds__(256) boids_step_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ sids,
@@ -1131,9 +1161,9 @@ public:
         }
         const int threads = block ? static_cast<int>(std::min<int64_t>(block, 256)) : 256;
         for (int64_t k = 0; k < nsteps; ++k) {
-            boids_zero_slots<<<1, 32, 0, rt.stream>>>(ring.p, metrics_cap, t, 1);
-            check_launch("boids_zero_slots");
             if (ba.nc == 1) {
+                boids_zero_slots<<<1, 32, 0, rt.stream>>>(ring.p, metrics_cap, t, 1);
+                check_launch("boids_zero_slots");
                 // degenerate small box: one cell holding every agent (the stencil
                 // visits it once); count = n, start = {0, n}
                 const int h[2] = {0, static_cast<int>(n)};
@@ -1142,7 +1172,8 @@ public:
                 AMBER_CUDA(cudaMemcpyAsync(sids.p, ids.p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, rt.stream));
             } else {
                 prof.launch(rt.stream, "boids_bin", [&] {
-                    boids_count_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(st.p, n, ba, cnt.p, cell_of.p);
+                    boids_count_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(st.p, n, ba, cnt.p, cell_of.p,
+                                                                                     ring.p + (t % metrics_cap));
                 });
                 check_launch("boids_count_kernel");
                 // exclusive scan of the ncell + 1 counts (cnt[ncell] = 0, so start[ncell] = n),
