@@ -371,6 +371,9 @@ public:
     bool pending = false;
     int64_t win_start = -1;
     DevBuf<Slot> ring;
+    Slot* h_ring = nullptr;  // pinned host mirror of the ring (only the needed slots are copied)
+    int64_t h_ring_cap = 0;
+    int64_t h_lo = 0, h_hi = 0;  // slots [h_lo, h_hi) of the mirror are current
     int64_t m_first = 0, replays = 0;
     // range-partitioned scatter (default on one GPU, wealth_bins.cu)
     bool bins = false;
@@ -492,6 +495,7 @@ public:
                         &sgb.tcnt[0], &sgb.tcnt[1]})
             v->reset();
         ring.reset();
+        if (h_ring) cudaFreeHost(h_ring);
         send_ids.reset();
         recv_ids.reset();
         send_counts.reset();
@@ -621,6 +625,7 @@ public:
     void step(int64_t nsteps) override
     {
         AMBER_REQUIRE(nsteps >= 0, "n_steps must be >= 0");
+        h_hi = h_lo;  // the ring changes: the host mirror is stale
         AMBER_REQUIRE(t + nsteps < (1ll << 32) - 2, "step index would exceed 2^32");
         if (small_path() && nsteps > 0) {
             // no pending scatter across calls on this path; flush any from the large path
@@ -731,6 +736,37 @@ public:
         }
     }
 
+    // Copy ring slots [s0, s1) into the pinned mirror (same slot positions; at most
+    // two contiguous pieces) and wait: per-step reads move only the slots they use.
+    const Slot* fetch_slots(int64_t s0, int64_t s1)
+    {
+        if (h_ring_cap == metrics_cap && s0 >= h_lo && s1 <= h_hi) return h_ring;  // fetched since the last step
+        if (h_ring_cap != metrics_cap) {
+            if (h_ring) cudaFreeHost(h_ring);
+            AMBER_CUDA(cudaMallocHost(&h_ring, metrics_cap * sizeof(Slot)));
+            h_ring_cap = metrics_cap;
+        }
+        if (s1 > s0) {
+            if (s1 - s0 >= metrics_cap) {
+                AMBER_CUDA(cudaMemcpyAsync(h_ring, ring.p, metrics_cap * sizeof(Slot), cudaMemcpyDeviceToHost, rt.stream));
+            } else {
+                const int64_t a = s0 % metrics_cap, b = (s1 - 1) % metrics_cap;
+                if (a <= b) {
+                    AMBER_CUDA(cudaMemcpyAsync(h_ring + a, ring.p + a, (b - a + 1) * sizeof(Slot), cudaMemcpyDeviceToHost,
+                                               rt.stream));
+                } else {
+                    AMBER_CUDA(cudaMemcpyAsync(h_ring + a, ring.p + a, (metrics_cap - a) * sizeof(Slot),
+                                               cudaMemcpyDeviceToHost, rt.stream));
+                    AMBER_CUDA(cudaMemcpyAsync(h_ring, ring.p, (b + 1) * sizeof(Slot), cudaMemcpyDeviceToHost, rt.stream));
+                }
+            }
+        }
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        h_lo = s0;
+        h_hi = s1;
+        return h_ring;
+    }
+
     // Exact overflow check of the open window; replays it with 32-bit counters if needed.
     void verify()
     {
@@ -738,9 +774,7 @@ public:
             AMBER_CUDA(cudaStreamSynchronize(rt.stream));
             return;
         }
-        std::vector<Slot> h(metrics_cap);
-        AMBER_CUDA(cudaMemcpyAsync(h.data(), ring.p, metrics_cap * sizeof(Slot), cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        const Slot* h = fetch_slots(win_start, t);
         bool bad = false;
         for (int64_t s = win_start; s < t; ++s) {
             const Slot& x = h[s % metrics_cap];
@@ -765,6 +799,7 @@ public:
     void replay(int64_t s0, int64_t s1)
     {
         ++replays;
+        h_hi = h_lo;
         slot_ready = false;
         reset_fb();
         for (auto& b : bb.cnt) b.zero_async(rt.stream);
@@ -841,11 +876,9 @@ public:
         else if (k == "active") off = offsetof(Slot, active);
         else if (k == "digest" && digest_on) off = offsetof(Slot, digest);
         else fail(AMBER_E_UNKNOWN_NAME, "no metric " + k + (k == "digest" ? " (set option digest=1)" : ""));
-        std::vector<Slot> h(metrics_cap);
-        AMBER_CUDA(cudaMemcpyAsync(h.data(), ring.p, metrics_cap * sizeof(Slot), cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
         const int64_t first = std::max(m_first, t - metrics_cap + 3);
         const int64_t cnt = std::max<int64_t>(t - first, 0);
+        const Slot* h = fetch_slots(first, t);
         if (bytes < static_cast<size_t>(cnt) * 8) fail(AMBER_E_BUFFER_TOO_SMALL, "metrics dst too small");
         std::vector<unsigned long long> vals(cnt);
         for (int64_t s = first; s < t; ++s)
