@@ -23,4 +23,59 @@ void build_graphs(Runtime& rt, const std::vector<unsigned long long>& seeds, int
 void build_init_state(Runtime& rt, const std::vector<unsigned long long>& seeds, int64_t n, int64_t n_pad,
                       int64_t k_inf, uint8_t* state, uint32_t tag = 0x12u);
 
+// Warp-cooperative walk over the concatenated CSR rows of the lanes in `own`
+// (lane L owns row [rb_L, re_L); col_at(e) returns the neighbour of arc e).
+// Position q of the concatenation -> owner lane by a 5-step shuffle search
+// over the inclusive prefix of the row lengths (SIR step, sir.cu, and the
+// replicate sweep, sweep.cu).  kU batches of 32 arcs are in flight per iteration: all their
+// column loads are issued, then all the neighbour tests, so each warp keeps
+// kU x 32 independent gathers outstanding (the walk is latency-bound on the
+// col -> bitmap chain at large N).  test(j, e, owner) returns true for an arc
+// that sets the owner's bit; owners whose bit is set skip their remaining arcs
+// (early exit).  Returns the mask of owners with a set bit.  All 32 lanes call it.
+template <int kU, class C, class T>
+__device__ __forceinline__ uint32_t walk_rows(C&& col_at, uint32_t own, int32_t rb, int32_t re, T&& test)
+{
+    const int lane = threadIdx.x & 31;
+    const int32_t len = ((own >> lane) & 1u) ? re - rb : 0;
+    int32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const int32_t start = rb - (incl - len);  // arc index of concatenation position q is start_L + q
+    uint32_t hit = 0;
+    for (int32_t q0 = 0; q0 < total; q0 += 32 * kU) {
+        int Ls[kU];
+        int32_t es[kU];
+        bool live[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int32_t q = q0 + 32 * u + lane;
+            int L = 0;  // number of lanes with incl <= q = the owner of position q
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+                const int32_t v = __shfl_sync(0xffffffffu, incl, (L + st - 1) & 31);
+                if (v <= q) L += st;
+            }
+            L &= 31;
+            Ls[u] = L;
+            es[u] = __shfl_sync(0xffffffffu, start, L) + q;
+            live[u] = q < total && !((hit >> L) & 1u);
+        }
+        uint32_t js[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) js[u] = live[u] ? col_at(es[u]) : 0u;
+        uint32_t add = 0;
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (live[u] && test(js[u], es[u], Ls[u])) add |= 1u << Ls[u];
+        hit |= __reduce_or_sync(0xffffffffu, add);
+        if ((hit & own) == own) break;  // every owner decided
+    }
+    return hit;
+}
+
 }  // namespace amber

@@ -337,61 +337,6 @@ __device__ __forceinline__ bool recovers(const SirStepArgs& a, int64_t i, uint32
     return static_cast<unsigned long long>(d) < a.t_gamma;
 }
 
-// Warp-cooperative walk over the concatenated CSR rows of the lanes in `own`
-// (lane L owns row [rb_L, re_L)).  Position q of the concatenation -> owner
-// lane by a 5-step shuffle search over the inclusive prefix of the row
-// lengths.  kU batches of 32 arcs are in flight per iteration: all their
-// column loads are issued, then all the neighbour tests, so each warp keeps
-// kU x 32 independent gathers outstanding (the walk is latency-bound on the
-// col -> bitmap chain at large N).  test(j, e, owner) returns true for an arc
-// that sets the owner's bit; owners whose bit is set skip their remaining arcs
-// (early exit).  Returns the mask of owners with a set bit.  All 32 lanes call it.
-template <int kU, class T>
-__device__ __forceinline__ uint32_t walk_rows(const int32_t* __restrict__ col, uint32_t own, int32_t rb, int32_t re,
-                                              T&& test)
-{
-    const int lane = threadIdx.x & 31;
-    const int32_t len = ((own >> lane) & 1u) ? re - rb : 0;
-    int32_t incl = len;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-    }
-    const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    const int32_t start = rb - (incl - len);  // arc index of concatenation position q is start_L + q
-    uint32_t hit = 0;
-    for (int32_t q0 = 0; q0 < total; q0 += 32 * kU) {
-        int Ls[kU];
-        int32_t es[kU];
-        bool live[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const int32_t q = q0 + 32 * u + lane;
-            int L = 0;  // number of lanes with incl <= q = the owner of position q
-#pragma unroll
-            for (int st = 16; st > 0; st >>= 1) {
-                const int32_t v = __shfl_sync(0xffffffffu, incl, (L + st - 1) & 31);
-                if (v <= q) L += st;
-            }
-            L &= 31;
-            Ls[u] = L;
-            es[u] = __shfl_sync(0xffffffffu, start, L) + q;
-            live[u] = q < total && !((hit >> L) & 1u);
-        }
-        uint32_t js[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) js[u] = live[u] ? static_cast<uint32_t>(__ldcs(col + es[u])) : 0u;
-        uint32_t add = 0;
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-            if (live[u] && test(js[u], es[u], Ls[u])) add |= 1u << Ls[u];
-        hit |= __reduce_or_sync(0xffffffffu, add);
-        if ((hit & own) == own) break;  // every owner decided
-    }
-    return hit;
-}
-
 // Pull step for the 32 agents of warp chunk a0 (lane = agent): susceptible
 // owners walk their rows; an arc transmits iff the neighbour is I (bitmap,
 // L2-resident) and the pair-keyed Bernoulli (S3) fires.  Writes the next state
@@ -410,7 +355,8 @@ __device__ __forceinline__ uint8_t sir_pull_chunk(const SirStepArgs& a, int64_t 
     uint32_t hit = 0;
     if (s_mask) {
         const int32_t rb = real ? a.row_ptr[i] : 0, re = real ? a.row_ptr[i + 1] : 0;
-        hit = walk_rows<4>(a.col, s_mask, rb, re, [&](uint32_t j, int32_t, int L) {
+        hit = walk_rows<4>([&](int32_t e) { return static_cast<uint32_t>(__ldcs(a.col + e)); }, s_mask, rb, re,
+                           [&](uint32_t j, int32_t, int L) {
             if (!bit_of(ib, j)) return false;  // j is a global id (the bitmap is global)
             const uint32_t s = static_cast<uint32_t>(a.gid0 + a0 + L);
             const uint4 w = philox(make_uint4(min(s, j), max(s, j), t, TAG_SIR_TX), a.key);
@@ -528,7 +474,8 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
         // pushers
         if (!own) return;
         const int32_t rb = is_i ? a.row_ptr[i] : 0, re = is_i ? a.row_ptr[i + 1] : 0;
-        walk_rows<4>(a.col, own, rb, re, [&](uint32_t j, int32_t, int L) {
+        walk_rows<4>([&](int32_t e) { return static_cast<uint32_t>(__ldcs(a.col + e)); }, own, rb, re,
+                     [&](uint32_t j, int32_t, int L) {
             if (!bit_of(sb, j)) return false;
             const uint32_t s = static_cast<uint32_t>(a0 + L);
             const uint4 wd = philox(make_uint4(min(s, j), max(s, j), t, TAG_SIR_TX), a.key);

@@ -7,9 +7,12 @@
 // the next replicate from a work queue (ordered by beta, largest first, so the
 // longest epidemics start first), stages its CSR (row offsets as u32, column
 // ids as u16 when n <= 65536) and both state buffers in shared memory, runs
-// all steps there with one __syncthreads per step, and stops early once no
-// agent is infected (later steps cannot change the state: S needs an I
-// neighbour and only I agents move).  Final R / n goes to out[r].
+// all steps there, and stops early once no agent is infected (later steps
+// cannot change the state: S needs an I neighbour and only I agents move).
+// Both directions walk rows warp-cooperatively (graph.cuh walk_rows): the
+// owners' rows of a 32-agent chunk are concatenated so every lane works on
+// arcs (the thread-per-agent walk was divergence-bound, 44 -> 30 ms at C5).
+// Final R / n goes to out[r].
 #include <algorithm>
 #include <numeric>
 
@@ -53,10 +56,10 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
     uint32_t* rp = reinterpret_cast<uint32_t*>(smem);                  // n + 1
     uint16_t* cs = reinterpret_cast<uint16_t*>(rp + ((a.n + 4) & ~3ll));  // col_cap (COL_SMEM)
     uint8_t* xs = reinterpret_cast<uint8_t*>(cs + (COL_SMEM ? ((a.col_cap + 7) & ~7ll) : 0));
-    uint8_t* st[2] = {xs, xs + a.n_pad};
     __shared__ int rep_s;
     __shared__ int cnt_s[2][2];  // [parity][I, S]
     const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
     const int64_t nq = a.n_pad / 4;
 
     for (;;) {
@@ -75,10 +78,13 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
             for (uint32_t p = tid; p < na; p += nt) cs[p] = static_cast<uint16_t>(gcol[p]);
         }
         const uchar4* s0 = reinterpret_cast<const uchar4*>(a.state0 + static_cast<int64_t>(r) * a.n_pad);
-        for (int64_t q = tid; q < nq; q += nt) reinterpret_cast<uchar4*>(st[0])[q] = s0[q];
+        for (int64_t q = tid; q < nq; q += nt) reinterpret_cast<uchar4*>(xs)[q] = s0[q];
         if (tid == 0) cnt_s[0][0] = cnt_s[0][1] = cnt_s[1][0] = cnt_s[1][1] = 0;
         __syncthreads();
         const PhiloxKey key = philox_key(a.seeds[r]);
+        auto col_at = [&](int32_t e) {
+            return COL_SMEM ? static_cast<uint32_t>(cs[e]) : static_cast<uint32_t>(gcol[e]);
+        };
         const unsigned long long tb = a.t_beta[r];
         int cur = 0;
         int64_t executed = a.steps;
@@ -86,8 +92,8 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
         {
             int ni = 0, ns = 0;
             for (int64_t i = tid; i < a.n; i += nt) {
-                ni += st[0][i] == kI;
-                ns += st[0][i] == kS;
+                ni += xs[i] == kI;
+                ns += xs[i] == kS;
             }
             ni = __reduce_add_sync(0xffffffffu, ni);
             ns = __reduce_add_sync(0xffffffffu, ns);
@@ -98,8 +104,9 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
             __syncthreads();
         }
         for (int64_t t = 0; t < a.steps; ++t) {
-            const uint8_t* x = st[cur];
-            uint8_t* y = st[cur ^ 1];
+            // derived from the shared-memory base, so the accesses stay LDS/STS
+            const uint8_t* x = xs + (cur ? a.n_pad : 0);
+            uint8_t* y = xs + (cur ? 0 : a.n_pad);
             const int par = static_cast<int>(t & 1);
             const int prev_inf = cnt_s[par][0], prev_sus = cnt_s[par][1];
             if (prev_inf == 0) {  // no infected agent: nothing can change any more
@@ -109,7 +116,10 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
             int n_inf = 0, n_sus = 0;
             if (prev_inf < prev_sus) {
                 // push: recoveries + copy, then each infected agent tries its susceptible
-                // neighbours (S3: the pair-keyed draw makes this identical to pull)
+                // neighbours (S3: the pair-keyed draw makes this identical to pull).
+                // (A one-pass push on the back-buffer invariant, as in sir.cu, measured
+                // slower here: 35.7 vs 29.7 ms for C5 -- in shared memory the vectorised
+                // copy pass is cheap and the extra atomics are not.)
                 for (int64_t q = tid; q < nq; q += nt) {
                     const uchar4 v = reinterpret_cast<const uchar4*>(x)[q];
                     uint8_t o[4] = {v.x, v.y, v.z, v.w};
@@ -123,17 +133,21 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
                     reinterpret_cast<uchar4*>(y)[q] = make_uchar4(o[0], o[1], o[2], o[3]);
                 }
                 __syncthreads();
-                for (int64_t i = tid; i < a.n; i += nt) {
-                    if (x[i] != kI) continue;
-                    const uint32_t b = rp[i], e = rp[i + 1];
-                    for (uint32_t p = b; p < e; ++p) {
-                        const uint32_t j = COL_SMEM ? static_cast<uint32_t>(cs[p]) : static_cast<uint32_t>(gcol[p]);
-                        if (x[j] == kS && y[j] == kS) {
-                            const uint32_t ii = static_cast<uint32_t>(i);
-                            const uint4 w = philox(make_uint4(min(ii, j), max(ii, j), static_cast<uint32_t>(t), TAG_SIR_TX), key);
-                            if (static_cast<unsigned long long>(w.x) < tb) y[j] = kI;
-                        }
-                    }
+                // warp-cooperative: the infected lanes of each 32-agent chunk walk their
+                // concatenated rows (graph.cuh walk_rows), so all lanes work on arcs
+                for (int64_t a0 = warp * 32; a0 < a.n_pad; a0 += nwarps * 32) {
+                    const int64_t i = a0 + lane;
+                    const bool is_i = i < a.n && x[i] == kI;
+                    const uint32_t own = __ballot_sync(0xffffffffu, is_i);
+                    if (!own) continue;
+                    const int32_t rb = is_i ? static_cast<int32_t>(rp[i]) : 0, re = is_i ? static_cast<int32_t>(rp[i + 1]) : 0;
+                    walk_rows<1>(col_at, own, rb, re, [&](uint32_t j, int32_t, int L) {
+                        if (x[j] != kS || y[j] != kS) return false;  // y: already hit this step
+                        const uint32_t ii = static_cast<uint32_t>(a0 + L);
+                        const uint4 w = philox(make_uint4(min(ii, j), max(ii, j), static_cast<uint32_t>(t), TAG_SIR_TX), key);
+                        if (static_cast<unsigned long long>(w.x) < tb) y[j] = kI;
+                        return false;
+                    });
                 }
                 __syncthreads();
                 for (int64_t i = tid; i < a.n; i += nt) {
@@ -141,37 +155,44 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
                     n_sus += y[i] == kS;
                 }
             } else {
-                // pull: each susceptible scans its row, early exit on the first transmitting edge
-                for (int64_t q = tid; q < nq; q += nt) {
-                    const uchar4 v = reinterpret_cast<const uchar4*>(x)[q];
-                    const uint8_t in[4] = {v.x, v.y, v.z, v.w};
-                    uint8_t o[4];
-                    uint4 rec = make_uint4(0u, 0u, 0u, 0u);
-                    if (in[0] == kI || in[1] == kI || in[2] == kI || in[3] == kI)
-                        rec = stream_block(key, TAG_SIR_REC, static_cast<unsigned long long>(q), static_cast<uint32_t>(t));
-                    const uint32_t rw[4] = {rec.x, rec.y, rec.z, rec.w};
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint32_t i = static_cast<uint32_t>(4 * q + k);
-                        o[k] = in[k];
-                        if (in[k] == kS) {
-                            bool inf = false;
-                            const uint32_t b = rp[i], e = rp[i + 1];
-                            for (uint32_t p = b; p < e && !inf; ++p) {
-                                const uint32_t j = COL_SMEM ? static_cast<uint32_t>(cs[p]) : static_cast<uint32_t>(gcol[p]);
-                                if (x[j] == kI) {
-                                    const uint4 w = philox(make_uint4(min(i, j), max(i, j), static_cast<uint32_t>(t), TAG_SIR_TX), key);
-                                    inf = static_cast<unsigned long long>(w.x) < tb;
-                                }
-                            }
-                            if (inf) o[k] = kI;
-                        } else if (in[k] == kI) {
-                            if (static_cast<unsigned long long>(rw[k]) < a.t_gamma) o[k] = kR;
-                        }
-                        n_inf += (o[k] == kI);
-                        n_sus += (o[k] == kS);
+                // pull, warp-cooperative: the susceptible lanes of each 32-agent chunk walk
+                // their concatenated rows; an owner stops at its first transmitting arc
+                for (int64_t a0 = warp * 32; a0 < a.n_pad; a0 += nwarps * 32) {
+                    const int64_t i = a0 + lane;
+                    const bool real = i < a.n;
+                    const uint8_t in = i < a.n_pad ? x[i] : static_cast<uint8_t>(3);  // 3 = padding
+                    const uint32_t s_mask = __ballot_sync(0xffffffffu, real && in == kS);
+                    const uint32_t i_mask = __ballot_sync(0xffffffffu, real && in == kI);
+                    uint32_t hit = 0;
+                    if (s_mask) {
+                        const bool mine = (s_mask >> lane) & 1u;
+                        const int32_t rb = mine ? static_cast<int32_t>(rp[i]) : 0, re = mine ? static_cast<int32_t>(rp[i + 1]) : 0;
+                        hit = walk_rows<1>(col_at, s_mask, rb, re, [&](uint32_t j, int32_t, int L) {
+                            if (x[j] != kI) return false;
+                            const uint32_t ii = static_cast<uint32_t>(a0 + L);
+                            const uint4 w = philox(make_uint4(min(ii, j), max(ii, j), static_cast<uint32_t>(t), TAG_SIR_TX), key);
+                            return static_cast<unsigned long long>(w.x) < tb;
+                        });
                     }
-                    reinterpret_cast<uchar4*>(y)[q] = make_uchar4(o[0], o[1], o[2], o[3]);
+                    // R4 recovery draws: one Philox block per 4 agents, computed by the
+                    // group's first lane and shuffled to the other three
+                    uint32_t rw = 0;
+                    if (i_mask) {
+                        uint4 rec = make_uint4(0u, 0u, 0u, 0u);
+                        if ((lane & 3) == 0 && ((i_mask >> lane) & 0xFu))
+                            rec = stream_block(key, TAG_SIR_REC, static_cast<unsigned long long>(i >> 2), static_cast<uint32_t>(t));
+                        const int src = lane & ~3;
+                        const uint32_t r0 = __shfl_sync(0xffffffffu, rec.x, src), r1 = __shfl_sync(0xffffffffu, rec.y, src);
+                        const uint32_t r2 = __shfl_sync(0xffffffffu, rec.z, src), r3 = __shfl_sync(0xffffffffu, rec.w, src);
+                        const int k = lane & 3;
+                        rw = k == 0 ? r0 : (k == 1 ? r1 : (k == 2 ? r2 : r3));
+                    }
+                    uint8_t o = in;
+                    if (real && in == kS && ((hit >> lane) & 1u)) o = kI;
+                    else if (real && in == kI && static_cast<unsigned long long>(rw) < a.t_gamma) o = kR;
+                    if (i < a.n_pad) y[i] = o;
+                    n_inf += real && o == kI;
+                    n_sus += real && o == kS;
                 }
             }
             n_inf = __reduce_add_sync(0xffffffffu, n_inf);
@@ -187,7 +208,7 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
         }
         // final R count
         int n_rec = 0;
-        for (int64_t i = tid; i < a.n; i += nt) n_rec += (st[cur][i] == kR);
+        for (int64_t i = tid; i < a.n; i += nt) n_rec += (xs[(cur ? a.n_pad : 0) + i] == kR);
         n_rec = __reduce_add_sync(0xffffffffu, n_rec);
         if (tid == 0) cnt_s[0][0] = 0;
         __syncthreads();
