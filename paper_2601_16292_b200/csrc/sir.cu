@@ -279,6 +279,10 @@ struct SirStepArgs {
 };
 
 constexpr int kRegions = 16;
+#ifndef AMBER_SIR_WALK_U
+#define AMBER_SIR_WALK_U 4
+#endif
+constexpr int kWalkU = AMBER_SIR_WALK_U;  // 32-arc batches in flight per warp (walk_rows)
 
 // Warp chunks (32 agents each) of the padded population.  Persistent launch
 // (queue != nullptr): dynamic -- the chunk range is split into kRegions
@@ -355,7 +359,7 @@ __device__ __forceinline__ uint8_t sir_pull_chunk(const SirStepArgs& a, int64_t 
     uint32_t hit = 0;
     if (s_mask) {
         const int32_t rb = real ? a.row_ptr[i] : 0, re = real ? a.row_ptr[i + 1] : 0;
-        hit = walk_rows<4>([&](int32_t e) { return static_cast<uint32_t>(__ldcs(a.col + e)); }, s_mask, rb, re,
+        hit = walk_rows<kWalkU>([&](int32_t e) { return static_cast<uint32_t>(__ldcs(a.col + e)); }, s_mask, rb, re,
                            [&](uint32_t j, int32_t, int L) {
             if (!bit_of(ib, j)) return false;  // j is a global id (the bitmap is global)
             const uint32_t s = static_cast<uint32_t>(a.gid0 + a0 + L);
@@ -474,7 +478,7 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
         // pushers
         if (!own) return;
         const int32_t rb = is_i ? a.row_ptr[i] : 0, re = is_i ? a.row_ptr[i + 1] : 0;
-        walk_rows<4>([&](int32_t e) { return static_cast<uint32_t>(__ldcs(a.col + e)); }, own, rb, re,
+        walk_rows<kWalkU>([&](int32_t e) { return static_cast<uint32_t>(__ldcs(a.col + e)); }, own, rb, re,
                      [&](uint32_t j, int32_t, int L) {
             if (!bit_of(sb, j)) return false;
             const uint32_t s = static_cast<uint32_t>(a0 + L);
