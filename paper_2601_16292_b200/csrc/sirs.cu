@@ -121,10 +121,11 @@ struct SirsSlot {
 
 struct SirsArgs {
     PhiloxKey key;
-    const int32_t* row_ptr;
+    const int32_t* row_ptr;  // internal (cell-ordered) CSR: neighbours as internal indices
     const int32_t* col;
-    uint8_t* x[2];
-    int64_t n;
+    const int32_t* sid;      // internal index -> agent id (the draws are keyed by id)
+    uint8_t* x[2];           // state in internal order (n_pad, padding = 3)
+    int64_t n, n_pad;
     unsigned long long t_inf, t_rec;
     uint32_t t0;
     int64_t steps;
@@ -139,32 +140,56 @@ __device__ __forceinline__ uint32_t lane32_word(const uint4& w, uint32_t k)
     return k == 0 ? w.x : (k == 1 ? w.y : (k == 2 ? w.z : w.w));
 }
 
+// Steps on the internal layout: agents renumbered in grid-cell order at
+// creation, so an agent's contacts are a few cells away in memory (state
+// gathers hit L1/L2 lines already in use) -- the result is independent of the
+// numbering because every draw is keyed by the agent id (sid).  A warp owns 32
+// consecutive internal agents; the susceptible lanes' rows are walked
+// cooperatively (graph.cuh walk_rows) and an owner stops at its first infected
+// contact (Listing 2: one draw per exposed susceptible, so only existence
+// matters).
 __global__ void __launch_bounds__(256) sirs_persistent_kernel(const SirsArgs a)
 {
     cg::grid_group grid = cg::this_grid();
     int cur = a.cur;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     for (int64_t k = 0; k < a.steps; ++k) {
         const uint32_t t = a.t0 + static_cast<uint32_t>(k);
         const uint8_t* x = a.x[cur];
         uint8_t* y = a.x[cur ^ 1];
         unsigned long long cnt[4] = {0, 0, 0, 0};
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
-            const uint8_t st = x[i];
-            uint8_t o = st;
-            if (st == kS) {
-                bool exposed = false;
-                for (int32_t p = a.row_ptr[i]; p < a.row_ptr[i + 1] && !exposed; ++p) exposed = x[a.col[p]] == kI;
-                if (exposed) {
-                    const uint4 w = stream_block(a.key, TAG_SIRS_TX, static_cast<unsigned long long>(i) >> 2, t);
-                    if (static_cast<unsigned long long>(lane32_word(w, static_cast<uint32_t>(i & 3))) < a.t_inf) o = kI;
-                }
-            } else if (st == kI) {
-                const uint4 w = stream_block(a.key, TAG_SIRS_REC, static_cast<unsigned long long>(i) >> 2, t);
-                if (static_cast<unsigned long long>(lane32_word(w, static_cast<uint32_t>(i & 3))) < a.t_rec) o = kR;
+        for (int64_t a0 = gw * 32; a0 < a.n_pad; a0 += nw * 32) {
+            const int64_t u = a0 + lane;
+            const bool real = u < a.n;
+            const uint8_t st = x[u];
+            const uint32_t s_mask = __ballot_sync(0xffffffffu, real && st == kS);
+            uint32_t exposed = 0;
+            if (s_mask) {
+                const bool mine = (s_mask >> lane) & 1u;
+                const int32_t rb = mine ? a.row_ptr[u] : 0, re = mine ? a.row_ptr[u + 1] : 0;
+                exposed = walk_rows<4>([&](int32_t e) { return static_cast<uint32_t>(__ldg(a.col + e)); }, s_mask, rb, re,
+                                       [&](uint32_t j, int32_t, int) { return x[j] == kI; });
             }
-            y[i] = o;
-            cnt[o] += 1;
-            if (a.digest) cnt[3] += digest_term(static_cast<unsigned long long>(i), o);
+            uint8_t o = st;
+            if (real && (st == kI || ((exposed >> lane) & 1u))) {
+                const uint32_t id = static_cast<uint32_t>(a.sid[u]);
+                const uint4 w = stream_block(a.key, st == kI ? TAG_SIRS_REC : TAG_SIRS_TX, id >> 2, t);
+                const uint32_t d = lane32_word(w, id & 3u);
+                if (st == kI) {
+                    if (static_cast<unsigned long long>(d) < a.t_rec) o = kR;
+                } else if (static_cast<unsigned long long>(d) < a.t_inf) {
+                    o = kI;
+                }
+            }
+            y[u] = o;
+            if (real) {
+                cnt[0] += o == kS;
+                cnt[1] += o == kI;
+                cnt[2] += o == kR;
+                if (a.digest) cnt[3] += digest_term(static_cast<unsigned long long>(a.sid[u]), o);
+            }
         }
         SirsSlot* sl = a.ring + (t % a.ring_cap);
         unsigned long long* const outs[4] = {&sl->S, &sl->I, &sl->R, a.digest ? &sl->digest : nullptr};
@@ -172,6 +197,49 @@ __global__ void __launch_bounds__(256) sirs_persistent_kernel(const SirsArgs a)
         cur ^= 1;
         grid.sync();
     }
+}
+
+// id order <-> internal order
+__global__ void sirs_to_internal(const uint8_t* __restrict__ src, const int32_t* __restrict__ sid, int64_t n,
+                                 uint8_t* __restrict__ dst)
+{
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+        dst[u] = src[sid[u]];
+}
+
+__global__ void sirs_to_ids(const uint8_t* __restrict__ src, const int32_t* __restrict__ sid, int64_t n,
+                            uint8_t* __restrict__ dst)
+{
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+        dst[sid[u]] = src[u];
+}
+
+// Internal CSR from the id-order CSR: row u = row of agent sid[u], neighbours
+// relabelled through inv (id -> internal index).
+__global__ void sirs_int_deg(const int32_t* __restrict__ rp_id, const int32_t* __restrict__ sid, int64_t n,
+                             int* __restrict__ deg)
+{
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = sid[u];
+        deg[u] = rp_id[i + 1] - rp_id[i];
+    }
+}
+
+__global__ void sirs_int_fill(const int32_t* __restrict__ rp_id, const int32_t* __restrict__ col_id,
+                              const int32_t* __restrict__ sid, const int32_t* __restrict__ inv, int64_t n,
+                              const int32_t* __restrict__ rp_int, int32_t* __restrict__ col_int)
+{
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = sid[u];
+        const int32_t b = rp_id[i], e = rp_id[i + 1], o = rp_int[u];
+        for (int32_t p = b; p < e; ++p) col_int[o + (p - b)] = inv[col_id[p]];
+    }
+}
+
+__global__ void sirs_inv(const int32_t* __restrict__ sid, int64_t n, int32_t* __restrict__ inv)
+{
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+        inv[sid[u]] = static_cast<int32_t>(u);
 }
 
 __global__ void sirs_zero_slots(SirsSlot* ring, int64_t cap, int64_t s0, int64_t count)
@@ -183,12 +251,15 @@ __global__ void sirs_zero_slots(SirsSlot* ring, int64_t cap, int64_t s0, int64_t
 
 class SirSpaceModel final : public Model {
 public:
-    int64_t n = 0, arcs = 0, k_inf = 0;
+    int64_t n = 0, n_pad = 0, arcs = 0, k_inf = 0;
     amber_sir_space_params p{};
     PhiloxKey key{};
     DevBuf<float> px, py;
-    DevBuf<int32_t> row_ptr, col;
-    DevBuf<uint8_t> x[2];
+    DevBuf<int32_t> row_ptr, col;      // id-order contact CSR (the public columns)
+    DevBuf<int32_t> row_int, col_int;  // the same graph on the internal (cell-ordered) numbering
+    DevBuf<int32_t> sid;               // internal index -> agent id
+    DevBuf<uint8_t> x[2];              // state, internal order
+    DevBuf<uint8_t> tmp;               // id-order staging for column I/O
     int cur = 0;
     DevBuf<SirsSlot> ring;
     int64_t m_first = 0;
@@ -210,9 +281,14 @@ public:
         py.allocate(&rt, n);
         sirs_pos_kernel<<<gsz, 256, 0, s>>>(key, n, p.L, px.p, py.p);
         check_launch("sirs_pos_kernel");
-        for (auto& b : x) b.allocate(&rt, n + 16);
+        n_pad = ceil_div(n, 32) * 32;
+        for (auto& b : x) {
+            b.allocate(&rt, n_pad + 16);
+            AMBER_CUDA(cudaMemsetAsync(b.p, 3, n_pad + 16, s));  // padding agents (never S or I)
+        }
+        tmp.allocate(&rt, n + 16);
         std::vector<unsigned long long> seeds{seed};
-        build_init_state(rt, seeds, n, n, k_inf, x[0].p, TAG_SIRS_INIT);
+        build_init_state(rt, seeds, n, n, k_inf, tmp.p, TAG_SIRS_INIT);
         // contact graph, once
         Grid2 g{};
         double ncd = std::floor(static_cast<double>(p.L) / (static_cast<double>(p.r) * 1.001));
@@ -222,7 +298,6 @@ public:
         const int ncell = g.nc * g.nc;
         DevBuf<int> cell, cnt, start, cursor, deg;
         DevBuf<float2> sp;
-        DevBuf<int32_t> sid;
         cell.allocate(&rt, n);
         cnt.allocate(&rt, ncell + 1);
         cnt.zero_async(s);
@@ -252,6 +327,24 @@ public:
         sirs_contacts_kernel<true><<<gsz, 256, 0, s>>>(px.p, py.p, n, g, r2, start.p, sp.p, sid.p, nullptr,
                                                        row_ptr.p, col.p);
         check_launch("sirs_contacts_kernel<fill>");
+        // internal numbering = the cell order of the binning (sid): contacts become
+        // near indices, so the per-step state gathers are local
+        {
+            DevBuf<int32_t> inv;
+            inv.allocate(&rt, n);
+            sirs_inv<<<gsz, 256, 0, s>>>(sid.p, n, inv.p);
+            check_launch("sirs_inv");
+            deg.zero_async(s);
+            sirs_int_deg<<<gsz, 256, 0, s>>>(row_ptr.p, sid.p, n, deg.p);
+            check_launch("sirs_int_deg");
+            row_int.allocate(&rt, n + 1);
+            scan(deg.p, row_int.p, n + 1);
+            col_int.allocate(&rt, std::max<int64_t>(arcs, 1));
+            sirs_int_fill<<<gsz, 256, 0, s>>>(row_ptr.p, col.p, sid.p, inv.p, n, row_int.p, col_int.p);
+            check_launch("sirs_int_fill");
+        }
+        sirs_to_internal<<<gsz, 256, 0, s>>>(tmp.p, sid.p, n, x[0].p);
+        check_launch("sirs_to_internal");
         ring.allocate(&rt, metrics_cap);
         ring.zero_async(s);
         AMBER_CUDA(cudaStreamSynchronize(s));
@@ -270,7 +363,8 @@ public:
     ~SirSpaceModel() override
     {
         if (rt.stream) cudaStreamSynchronize(rt.stream);
-        px.reset(); py.reset(); row_ptr.reset(); col.reset();
+        px.reset(); py.reset(); row_ptr.reset(); col.reset(); row_int.reset(); col_int.reset(); sid.reset();
+        tmp.reset();
         for (auto& b : x) b.reset();
         ring.reset();
         rt.destroy();
@@ -286,12 +380,12 @@ public:
             check_launch("sirs_zero_slots");
             int per_sm = 0;
             AMBER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sirs_persistent_kernel, 256, 0));
-            int blocks = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(std::min(per_sm, 3)) * rt.num_sms,
-                                                            std::max<int64_t>(1, ceil_div(n, 256))));
+            int blocks = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(n_pad > (1 << 22) ? per_sm : std::min(per_sm, 3)) * rt.num_sms,
+                                                            std::max<int64_t>(1, ceil_div(n_pad, 256))));
             if (grid) blocks = static_cast<int>(std::min<int64_t>(grid, static_cast<int64_t>(per_sm) * rt.num_sms));
-            SirsArgs a{key, row_ptr.p, col.p, {x[0].p, x[1].p}, n, bernoulli_threshold_host(p.p_infect),
-                       bernoulli_threshold_host(p.p_recover), static_cast<uint32_t>(t), chunk, cur, ring.p,
-                       metrics_cap, digest_on ? 1 : 0};
+            SirsArgs a{key, row_int.p, col_int.p, sid.p, {x[0].p, x[1].p}, n, n_pad,
+                       bernoulli_threshold_host(p.p_infect), bernoulli_threshold_host(p.p_recover),
+                       static_cast<uint32_t>(t), chunk, cur, ring.p, metrics_cap, digest_on ? 1 : 0};
             void* kargs[] = {&a};
             prof.launch(rt.stream, "sirs_persistent", [&] {
                 AMBER_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sirs_persistent_kernel), blocks, 256,
@@ -326,7 +420,7 @@ public:
         std::string k(name);
         const void* src;
         size_t nb;
-        if (k == "state") { src = x[cur].p; nb = n; }
+        if (k == "state") { src = state_ids(); nb = n; }
         else if (k == "pos_x") { src = px.p; nb = n * 4; }
         else if (k == "pos_y") { src = py.p; nb = n * 4; }
         else if (k == "row_ptr") { src = row_ptr.p; nb = (n + 1) * 4; }
@@ -341,7 +435,18 @@ public:
         std::string k(name);
         if (k != "state") fail(AMBER_E_INVALID_ARG, "only the state column is writable (positions are static)");
         if (bytes < static_cast<size_t>(n)) fail(AMBER_E_BUFFER_TOO_SMALL, "src smaller than state column");
-        copy_in(rt, x[cur].p, src, n, on_dev);
+        copy_in(rt, tmp.p, src, n, on_dev);
+        sirs_to_internal<<<rt.num_sms * 8, 256, 0, rt.stream>>>(tmp.p, sid.p, n, x[cur].p);
+        check_launch("sirs_to_internal");
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    }
+
+    // the current state in id order (staging buffer)
+    const uint8_t* state_ids()
+    {
+        sirs_to_ids<<<rt.num_sms * 8, 256, 0, rt.stream>>>(x[cur].p, sid.p, n, tmp.p);
+        check_launch("sirs_to_ids");
+        return tmp.p;
     }
 
     void read_metrics(const char* name, void* dst, size_t bytes, int64_t* n_out) override
@@ -373,7 +478,7 @@ public:
     uint64_t digest(const char* name) override
     {
         if (std::string(name) != "state") fail(AMBER_E_UNKNOWN_NAME, std::string("no column ") + name);
-        return device_digest_u8(rt, x[cur].p, n, 0);
+        return device_digest_u8(rt, state_ids(), n, 0);
     }
 
     void set_step(int64_t s) override
