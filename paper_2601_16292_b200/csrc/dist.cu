@@ -217,9 +217,12 @@ WealthExchange* make_wealth_exchange_rt(Runtime& rt, const amber_runtime* r)
     return x;
 }
 
+void wealth_p2p_close(WealthExchange* x);
+
 void destroy_wealth_exchange(WealthExchange* x)
 {
     if (!x) return;
+    wealth_p2p_close(x);
     if (x->comm) destroy_comm(x->comm);
     x->hub.reset();
     x->send_counts_copy.reset();
@@ -288,6 +291,110 @@ void wealth_exchange_run(WealthExchange* x, Runtime& rt, const unsigned int* d_s
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
     AMBER_CUDA(cudaMemcpyAsync(d_recv_total, &total, sizeof(total), cudaMemcpyHostToDevice, rt.stream));
     AMBER_CUDA(cudaStreamSynchronize(rt.stream));  // `total` lives on this host stack frame
+}
+
+// ---------------------------------------------------------------- wealth P2P exchange
+// The fused compute + transfer path: every rank keeps its send
+// buckets (both step parities, one cudaMalloc) mapped into its peers' address
+// spaces; after a stream-ordered barrier the owner's receive kernel reads the
+// buckets addressed to it straight out of the peers' memory over NVLink and
+// applies them as counter atomics -- no counts round trip through the host,
+// no staging copies.  Mapping: CUDA IPC handles all-gathered over NCCL
+// (multi-process) or raw pointers through the hub (loopback, one process).
+struct P2PMap {
+    std::vector<void*> peers;   // [world] base of each rank's bucket block (mine included)
+    std::vector<bool> opened;   // IPC-opened (to close)
+    DevBuf<unsigned int> token; // 1-element barrier all-reduce
+};
+
+static std::map<WealthExchange*, std::unique_ptr<P2PMap>>& p2p_maps()
+{
+    static std::map<WealthExchange*, std::unique_ptr<P2PMap>> m;
+    return m;
+}
+
+// Maps my bucket block into every peer; false (on every rank) if any rank cannot.
+bool wealth_p2p_open(WealthExchange* x, Runtime& rt, void* my_base, std::vector<void*>& peers)
+{
+    auto map = std::make_unique<P2PMap>();
+    const int W = x->world, me = x->rank;
+    map->peers.assign(W, nullptr);
+    map->opened.assign(W, false);
+    if (x->hub) {
+        LoopbackHub& h = *x->hub;
+        h.send_ids[me] = static_cast<const uint32_t*>(my_base);
+        h.barrier();
+        for (int p = 0; p < W; ++p) map->peers[p] = const_cast<uint32_t*>(h.send_ids[p]);
+        h.barrier();
+    } else {
+        bool ok = true;
+        cudaIpcMemHandle_t mine;
+        if (cudaIpcGetMemHandle(&mine, my_base) != cudaSuccess) ok = false;
+        cudaGetLastError();
+        DevBuf<char> all;
+        all.allocate(&rt, static_cast<size_t>(W) * sizeof(mine));
+        DevBuf<char> one;
+        one.allocate(&rt, sizeof(mine));
+        AMBER_CUDA(cudaMemcpyAsync(one.p, &mine, sizeof(mine), cudaMemcpyHostToDevice, rt.stream));
+        nccl_check(nccl().AllGather(one.p, all.p, sizeof(mine), ncclChar, x->comm->comm, rt.stream), "ncclAllGather(ipc)");
+        std::vector<cudaIpcMemHandle_t> hs(W);
+        AMBER_CUDA(cudaMemcpyAsync(hs.data(), all.p, W * sizeof(mine), cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        map->peers[me] = my_base;
+        for (int p = 0; p < W && ok; ++p) {
+            if (p == me) continue;
+            void* ptr = nullptr;
+            if (cudaIpcOpenMemHandle(&ptr, hs[p], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                ok = false;
+                break;
+            }
+            map->peers[p] = ptr;
+            map->opened[p] = true;
+        }
+        // every rank must take the same path
+        DevBuf<unsigned long long> flag;
+        flag.allocate(&rt, 1);
+        unsigned long long bad = ok ? 0ull : 1ull;
+        AMBER_CUDA(cudaMemcpyAsync(flag.p, &bad, 8, cudaMemcpyHostToDevice, rt.stream));
+        comm_allreduce_u64(x->comm, rt.stream, flag.p, 1);
+        AMBER_CUDA(cudaMemcpyAsync(&bad, flag.p, 8, cudaMemcpyDeviceToHost, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        if (bad) {
+            for (int p = 0; p < W; ++p)
+                if (map->opened[p]) cudaIpcCloseMemHandle(map->peers[p]);
+            return false;
+        }
+        map->token.allocate(&rt, 1);
+        map->token.zero_async(rt.stream);
+    }
+    peers = map->peers;
+    p2p_maps()[x] = std::move(map);
+    return true;
+}
+
+void wealth_p2p_close(WealthExchange* x)
+{
+    auto it = p2p_maps().find(x);
+    if (it == p2p_maps().end()) return;
+    for (size_t p = 0; p < it->second->peers.size(); ++p)
+        if (it->second->opened[p]) cudaIpcCloseMemHandle(it->second->peers[p]);
+    p2p_maps().erase(it);
+}
+
+// Every rank's buckets of this step are complete before anyone reads them:
+// a one-element all-reduce on the stream (NCCL; no host round trip), or a
+// host barrier after the stream drains (loopback).
+void wealth_p2p_barrier(WealthExchange* x, Runtime& rt)
+{
+    if (x->hub) {
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        x->hub->barrier();
+        return;
+    }
+    P2PMap& m = *p2p_maps().at(x);
+    nccl_check(nccl().AllReduce(m.token.p, m.token.p, 1, ncclUint32, ncclSum, x->comm->comm, rt.stream),
+               "ncclAllReduce(barrier)");
 }
 
 // loopback all-reduce (sum) of n host values

@@ -334,6 +334,33 @@ __global__ void wealth_recv_kernel(const uint32_t* __restrict__ ids, const unsig
     block_sum_atomic<1>(vals, outs);
 }
 
+// P2P receive (fused transfer + apply): block row y = peer p; the bucket rank p
+// filled for this rank in the scattered step's parity is read straight from
+// p's memory (mapped over NVLink; __ldcv/__ldcs: never a stale cached copy)
+// and applied to the local counters.
+template <int B>
+__global__ void wealth_recv_p2p_kernel(const unsigned long long* __restrict__ peer_base, int world, int me,
+                                       size_t cnt_off, size_t ids_off, unsigned long long cap, unsigned long long lo,
+                                       uint32_t* inc, Slot* slot)
+{
+    const int p = blockIdx.y;
+    unsigned long long got = 0;
+    if (p != me) {
+        const unsigned char* base = reinterpret_cast<const unsigned char*>(peer_base[p]);
+        const unsigned int n = __ldcv(reinterpret_cast<const unsigned int*>(base + cnt_off) + me);
+        const unsigned long long m = n < cap ? n : cap;
+        const uint32_t* ids = reinterpret_cast<const uint32_t*>(base + ids_off) + static_cast<unsigned long long>(me) * cap;
+        for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < m;
+             k += (unsigned long long)gridDim.x * blockDim.x) {
+            add_count<B>(inc, static_cast<unsigned long long>(__ldcs(ids + k)) - lo, policy_evict_last());
+            got += 1;
+        }
+    }
+    unsigned long long vals[1] = {got};
+    unsigned long long* const outs[1] = {&slot->sent};
+    block_sum_atomic<1>(vals, outs);
+}
+
 __global__ void wealth_fill_kernel(int32_t* w, int64_t n_loc, int64_t n_pad, int32_t w0)
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pad; i += (int64_t)gridDim.x * blockDim.x)
@@ -356,6 +383,8 @@ void wealth_exchange_run(WealthExchange* x, Runtime& rt, const unsigned int* d_s
 bool wealth_exchange_any(WealthExchange* x, Runtime& rt, bool local_flag);
 void wealth_exchange_allreduce_u64(WealthExchange* x, Runtime& rt, unsigned long long* d_vals, int n);
 void destroy_wealth_exchange(WealthExchange* x);
+bool wealth_p2p_open(WealthExchange* x, Runtime& rt, void* my_base, std::vector<void*>& peers);
+void wealth_p2p_barrier(WealthExchange* x, Runtime& rt);
 
 class WealthModel final : public Model {
 public:
@@ -393,6 +422,12 @@ public:
     WealthExchange* xch = nullptr;
     DevBuf<uint32_t> send_ids, recv_ids;
     DevBuf<unsigned int> send_counts;
+    // P2P exchange (default when every rank can map its peers' buckets): both
+    // parities' buckets in one cudaMalloc block (IPC-exportable)
+    bool p2p = false, p2p_wanted = false;
+    void* p2p_block = nullptr;
+    size_t p2p_cnt_off[2] = {0, 0}, p2p_ids_off[2] = {0, 0};
+    DevBuf<unsigned long long> p2p_peers;
     DevBuf<unsigned long long> recv_total;
     uint64_t send_cap = 0;
 
@@ -467,20 +502,58 @@ public:
         const bool force_x = force && force[0] == '1' && r && r->nccl_unique_id && rt.world == 1;
         if (rt.world > 1 || force_x) {
             xch = make_wealth_exchange_rt(rt, r);
-            send_cap = static_cast<uint64_t>(std::max<int64_t>(n_loc, 1));
+            send_cap = static_cast<uint64_t>(std::max<int64_t>(shard, 1));  // same on every rank: peers index each other's buckets
             send_ids.allocate(&rt, send_cap * rt.world);
             recv_ids.allocate(&rt, static_cast<size_t>(shard) * rt.world + 1);
             send_counts.allocate(&rt, rt.world);
             send_counts.zero_async(rt.stream);
+            const char* mode = getenv("AMBER_WEALTH_EXCHANGE");
+            p2p_wanted = !(mode && std::string(mode) == "nccl");  // mapped at the first exchange (collective)
             recv_total.allocate(&rt, 1);
         }
         AMBER_CUDA(cudaStreamSynchronize(rt.stream));
     }
 
+    // Bucket block [counts par 0 | counts par 1 | ids par 0 | ids par 1] mapped into
+    // every peer (dist.cu wealth_p2p_open); falls back to the NCCL send/recv
+    // exchange if any rank cannot map its peers.
+    void setup_p2p()
+    {
+        const size_t cbytes = ((static_cast<size_t>(rt.world) * 4 + 255) / 256) * 256;
+        const size_t ibytes = static_cast<size_t>(rt.world) * send_cap * 4;
+        p2p_cnt_off[0] = 0;
+        p2p_cnt_off[1] = cbytes;
+        p2p_ids_off[0] = 2 * cbytes;
+        p2p_ids_off[1] = 2 * cbytes + ibytes;
+        if (cudaMalloc(&p2p_block, 2 * cbytes + 2 * ibytes) != cudaSuccess) {
+            cudaGetLastError();
+            p2p_block = nullptr;
+        }
+        AMBER_CUDA(cudaMemsetAsync(p2p_block, 0, 2 * cbytes, rt.stream));
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        std::vector<void*> peers;
+        if (p2p_block && wealth_p2p_open(xch, rt, p2p_block, peers)) {
+            std::vector<unsigned long long> h(peers.size());
+            for (size_t k = 0; k < peers.size(); ++k) h[k] = reinterpret_cast<unsigned long long>(peers[k]);
+            p2p_peers.allocate(&rt, h.size());
+            AMBER_CUDA(cudaMemcpyAsync(p2p_peers.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, rt.stream));
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            p2p = true;
+        } else if (p2p_block) {
+            cudaFree(p2p_block);
+            p2p_block = nullptr;
+        }
+    }
+
+    unsigned int* p2p_counts(int par) { return reinterpret_cast<unsigned int*>(static_cast<char*>(p2p_block) + p2p_cnt_off[par]); }
+    uint32_t* p2p_ids(int par) { return reinterpret_cast<uint32_t*>(static_cast<char*>(p2p_block) + p2p_ids_off[par]); }
+
     ~WealthModel() override
     {
         if (rt.stream) cudaStreamSynchronize(rt.stream);
         if (xch) destroy_wealth_exchange(xch);
+        if (p2p_block) cudaFree(p2p_block);
+        p2p_peers.reset();
         for (auto& b : wb) b.reset();
         for (auto& b : inc) b.reset();
         for (auto& b : inc32) b.reset();
@@ -573,13 +646,23 @@ public:
         a.slot_scatter = scatter ? slot(ts) : nullptr;
         a.slot_zero = (apply && scatter) ? slot(ta + 2) : nullptr;
         const bool remote = xch != nullptr && scatter;
+        if (remote && p2p_wanted) {  // collective: every rank reaches its first exchange here
+            p2p_wanted = false;
+            setup_p2p();
+        }
         if (remote) {
             a.world = rt.world;
             a.shard_size = static_cast<unsigned long long>(shard);
             a.remote_ids = send_ids.p;
             a.remote_count = send_counts.p;
             a.remote_cap = send_cap;
-            send_counts.zero_async(rt.stream);
+            if (p2p) {  // the scattered step's parity; its previous readers finished (barrier of ts - 1)
+                a.remote_ids = p2p_ids(ts & 1);
+                a.remote_count = p2p_counts(ts & 1);
+                AMBER_CUDA(cudaMemsetAsync(a.remote_count, 0, rt.world * sizeof(unsigned int), rt.stream));
+            } else {
+                send_counts.zero_async(rt.stream);
+            }
         }
         const bool dig = digest_on != 0;
         switch (bits) {
@@ -597,6 +680,27 @@ public:
     void exchange(int bits, bool exact, int64_t ts)
     {
         DevBuf<uint32_t>* ib = exact ? inc32 : inc;
+        if (p2p) {
+            wealth_p2p_barrier(xch, rt);
+            auto launch_p2p = [&](auto kern) {
+                const dim3 g(static_cast<unsigned>(std::max(1, rt.num_sms * 8 / std::max(rt.world - 1, 1))),
+                             static_cast<unsigned>(rt.world));
+                prof.launch(rt.stream, "wealth_recv_p2p", [&] {
+                    kern<<<g, 256, 0, rt.stream>>>(p2p_peers.p, rt.world, rt.rank, p2p_cnt_off[ts & 1],
+                                                   p2p_ids_off[ts & 1], static_cast<unsigned long long>(send_cap),
+                                                   static_cast<unsigned long long>(lo), ib[ts & 1].p, slot(ts));
+                });
+                check_launch("wealth_recv_p2p_kernel");
+            };
+            switch (bits) {
+                case 2: launch_p2p(wealth_recv_p2p_kernel<2>); break;
+                case 4: launch_p2p(wealth_recv_p2p_kernel<4>); break;
+                case 8: launch_p2p(wealth_recv_p2p_kernel<8>); break;
+                case 16: launch_p2p(wealth_recv_p2p_kernel<16>); break;
+                default: launch_p2p(wealth_recv_p2p_kernel<32>); break;
+            }
+            return;
+        }
         wealth_exchange_run(xch, rt, send_counts.p, send_ids.p, send_cap, recv_ids.p, recv_total.p);
         auto launch_recv = [&](auto kern) {
             prof.launch(rt.stream, "wealth_recv_apply", [&] {
@@ -811,6 +915,7 @@ public:
         }
         ring.zero_async(rt.stream);
         if (xch) send_counts.zero_async(rt.stream);
+        if (p2p) AMBER_CUDA(cudaMemsetAsync(p2p_block, 0, p2p_ids_off[0], rt.stream));
         for (int64_t s = s0; s < s1; ++s) {
             if (s == s0) launch(32, true, false, true, s, s, cur, cur);
             const int dst = other(cur, -1);
@@ -982,6 +1087,10 @@ public:
         }
         if (k == "counter_bits") {
             *v = B;
+            return true;
+        }
+        if (k == "exchange") {  // 0: none (one rank), 1: NCCL send/recv, 2: P2P (peer-mapped buckets)
+            *v = xch ? (p2p ? 2 : 1) : 0;
             return true;
         }
         if (k == "scatter") {  // 0: range-partitioned bins, 1: packed-counter atomics, 2: fused binned, 3: segmented bins

@@ -62,6 +62,23 @@ def test_sharded_wealth_equals_oracle(orc, world, n):
     assert all(d == orc.digest(ref) for d in dg)
 
 
+@pytest.mark.parametrize("mode", ["p2p", "nccl"])
+def test_sharded_wealth_exchange_modes(orc, monkeypatch, mode):
+    # p2p (default): owners read the peers' buckets in place after a stream-ordered
+    # barrier; nccl: counts + payload send/recv through the transport
+    if mode == "nccl":
+        monkeypatch.setenv("AMBER_WEALTH_EXCHANGE", "nccl")
+    world, n, seed, steps = 4, 30_011, 21, 20
+    ms = sharded(world, n, seed)
+    par(ms, lambda m: (m.step(7), m.step(13)))
+    assert all(m.get_option("exchange") == (2 if mode == "p2p" else 1) for m in ms)  # mapped at the first step
+    w = np.concatenate(par(ms, lambda m: m.read_column("wealth")))
+    ref, tot, _, _ = orc.wealth_run(np.ones(n, np.int32), seed, 0, steps)
+    assert np.array_equal(w, ref)
+    for tt in par(ms, lambda m: m.metrics("total_wealth")):
+        assert np.array_equal(tt, tot)
+
+
 def test_sharded_overflow_replay_is_collective(orc):
     # 2-bit counters overflow on some shard nearly every window: all shards replay
     world, n, seed, steps = 4, 40_000, 5, 12
