@@ -138,3 +138,32 @@ def test_geometry_invariance_and_io(orc):
     c.write_column("vel_x", s[2] * 0.5)
     assert np.array_equal(c.read_column("vel_x"), (s[2] * 0.5).astype(np.float32))
     assert c.digest("pos_x") == orc.digest(s[0])
+
+
+@pytest.mark.parametrize("n", [1, 2, 7])
+def test_tiny_populations(orc, n):
+    # degenerate cases: a single agent (no neighbours: straight line with wrap), pairs
+    cfg = dict(C3_BOIDS, n=n, L=40.0, seed=13)
+    m = make(cfg)
+    st = state(m)
+    m.step(30)
+    P = oparams(orc, cfg)
+    for _ in range(30):
+        st = orc.boids_step(st, P)
+    for a, b in zip(state(m), st):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_large_grid_device_scan_and_edges(orc):
+    # > 2^16 cells: the device-wide cell scan; sparse agents, so most stencils touch
+    # the box edges' wrapped rows/columns as well as interior runs
+    cfg = dict(C3_BOIDS, n=30_000, L=3000.0, seed=17)
+    m = make(cfg)
+    assert m.get_option("cells_per_side") ** 2 > (1 << 16)
+    st = state(m)
+    m.step(12)
+    P = oparams(orc, cfg)
+    for _ in range(12):
+        st = orc.boids_step(st, P)
+    for a, b in zip(state(m), st):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))

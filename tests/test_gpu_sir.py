@@ -188,3 +188,15 @@ def test_mixed_launch_modes_and_column_write(orc):
     d.step(15)
     ref = orc.sir_run(rp, col, mid, 99, cfg["beta"], cfg["gamma"], 10, 15)[0]
     assert np.array_equal(d.read_column("state"), ref)
+
+
+def test_full_occupancy_path_bit_exact(orc):
+    # n_pad > 2^22: full-occupancy persistent launch with dynamic chunk queues
+    cfg = dict(n=5_000_000, mean_degree=10.0, beta=0.05, gamma=0.1, init_frac=0.002, seed=29, steps=14)
+    m = make(cfg)
+    m.step(cfg["steps"])
+    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
+    st = orc.sir_init(cfg["n"], 10_000, cfg["seed"])
+    ref, counts, _ = orc.sir_run(rp, col, st, cfg["seed"], cfg["beta"], cfg["gamma"], 0, cfg["steps"])
+    assert np.array_equal(m.read_column("state"), ref)
+    assert np.array_equal(m.metrics("I"), counts[:, 1])
