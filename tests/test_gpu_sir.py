@@ -200,3 +200,19 @@ def test_full_occupancy_path_bit_exact(orc):
     ref, counts, _ = orc.sir_run(rp, col, st, cfg["seed"], cfg["beta"], cfg["gamma"], 0, cfg["steps"])
     assert np.array_equal(m.read_column("state"), ref)
     assert np.array_equal(m.metrics("I"), counts[:, 1])
+
+
+def test_small_metrics_ring_wraps(orc):
+    # metrics_capacity 16 over 70 steps: the ring wraps several times; the counts slot
+    # that steers push/pull (step t-1) must survive every chunk's slot zeroing
+    cfg = dict(n=50_000, mean_degree=8.0, beta=0.07, gamma=0.1, init_frac=0.01, seed=41, steps=70)
+    m = make(cfg)
+    m.set_option("metrics_capacity", 16)
+    m.step(33)
+    m.step(37)
+    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
+    st = orc.sir_init(cfg["n"], 500, cfg["seed"])
+    ref, counts, _ = orc.sir_run(rp, col, st, cfg["seed"], cfg["beta"], cfg["gamma"], 0, cfg["steps"])
+    assert np.array_equal(m.read_column("state"), ref)
+    got = m.metrics("I")
+    assert len(got) == 16 and np.array_equal(got, counts[-16:, 1])

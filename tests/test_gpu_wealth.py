@@ -254,3 +254,21 @@ def test_segmented_bins_full_size_first_steps(orc):
     w = orc.wealth_run(np.full(cfg["n"], 1, np.int32), cfg["seed"], 0, 2)[0]
     assert np.array_equal(m.read_column("wealth"), w)
     assert m.get_option("replays") == 0
+
+
+def test_small_metrics_ring_and_per_step_reads(orc):
+    # metrics_capacity 16: overflow-check windows close every few steps; per-step
+    # reads (as bench.py's end-to-end loop does) see exactly that step's record
+    n, seed = 300_000, 27
+    m = make(n, seed, bits=2)  # 2-bit counters: replays happen inside the windows
+    m.set_option("metrics_capacity", 16)
+    w = np.ones(n, np.int32)
+    for t in range(40):
+        m.step(1)
+        act = m.metrics("active")
+        w_next, tot, a, _ = orc.wealth_run(w, seed, t, 1)
+        assert act[-1] == a[0], t
+        m.reset_metrics()
+        w = w_next
+    assert np.array_equal(m.read_column("wealth"), w)
+    assert m.get_option("replays") > 0
