@@ -538,7 +538,7 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
             me = sorted[p];
             auto run = [&](int b, int e) {
                 for (int q = b + sub; q < e; q += G)
-                    if (q != p) boid_accumulate<true>(sorted[q], me, L, halfL, R2, rs2, acc);
+                    boid_accumulate<true>(sorted[q], me, L, halfL, R2, rs2, acc);
             };
             // interior agents (stencil inside the box, so every candidate is within
             // two cells < L/2 per coordinate): no minimum image, rows as runs
@@ -546,10 +546,10 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
                 int q = b + sub;
                 for (; q + G < e; q += 2 * G) {  // two candidate loads in flight per lane
                     const float4 o0 = sorted[q], o1 = sorted[q + G];
-                    if (q != p) boid_accumulate<false>(o0, me, L, halfL, R2, rs2, acc);
-                    if (q + G != p) boid_accumulate<false>(o1, me, L, halfL, R2, rs2, acc);
+                    boid_accumulate<false>(o0, me, L, halfL, R2, rs2, acc);
+                    boid_accumulate<false>(o1, me, L, halfL, R2, rs2, acc);
                 }
-                if (q < e && q != p) boid_accumulate<false>(sorted[q], me, L, halfL, R2, rs2, acc);
+                if (q < e) boid_accumulate<false>(sorted[q], me, L, halfL, R2, rs2, acc);
             };
             const int cx0 = a.nc >= 3 ? cell_coord(me.x, a) : 0, cy0 = a.nc >= 3 ? cell_coord(me.y, a) : 0;
             if (a.nc >= 5 && cx0 >= 1 && cx0 + 1 < a.nc && cy0 >= 1 && cy0 + 1 < a.nc) {
@@ -590,6 +590,11 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
             acc.svy += __shfl_xor_sync(0xffffffffu, acc.svy, off);
             acc.ssx += __shfl_xor_sync(0xffffffffu, acc.ssx, off);
             acc.ssy += __shfl_xor_sync(0xffffffffu, acc.ssy, off);
+        }
+        if (active) {  // the agent itself was accumulated once (d = 0, inside both radii): take it out
+            acc.n -= 1;
+            acc.svx -= q24(me.z);
+            acc.svy -= q24(me.w);
         }
         // B4's four mean divisions in parallel on lanes 0..3 of the group
         // (x / 2^24 is exact, so it is a multiplication), gathered by shuffles
@@ -938,8 +943,7 @@ __global__ void __launch_bounds__(256, 4) slab_step_kernel(const float4* __restr
         if (active) {
             me = sorted[p];
             auto run = [&](int b, int e) {
-                for (int q = b + sub; q < e; q += G)
-                    if (q != p) boid_accumulate<true>(sorted[q], me, L, halfL, R2, rs2, acc);
+                for (int q = b + sub; q < e; q += G) boid_accumulate<true>(sorted[q], me, L, halfL, R2, rs2, acc);
             };
             const int lc = cell_coord(me.x, a) - g.c_lo + 1, cy = cell_coord(me.y, a);
 #pragma unroll 1
@@ -966,6 +970,11 @@ __global__ void __launch_bounds__(256, 4) slab_step_kernel(const float4* __restr
             acc.svy += __shfl_xor_sync(0xffffffffu, acc.svy, off);
             acc.ssx += __shfl_xor_sync(0xffffffffu, acc.ssx, off);
             acc.ssy += __shfl_xor_sync(0xffffffffu, acc.ssy, off);
+        }
+        if (active) {  // the agent itself was accumulated once: take it out
+            acc.n -= 1;
+            acc.svx -= q24(me.z);
+            acc.svy -= q24(me.w);
         }
         float mv = 0.0f;
         if (acc.n > 0 && sub < 4) {
