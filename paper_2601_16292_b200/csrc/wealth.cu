@@ -222,7 +222,11 @@ __global__ void __launch_bounds__(256, AMBER_WEALTH_MINB) wealth_step_kernel(con
                         const Id rl = r - lo;
                         bool local = s;
                         if constexpr (REMOTE) local = s && rl < n_loc;
+#ifndef AMBER_EXPERIMENT_NO_RED
                         if (local) add_count<B>(a.inc_next, rl, pol);
+#else
+                        if (local && rl == ~Id(0)) add_count<B>(a.inc_next, rl, pol);  // never: cost without REDs
+#endif
                         sent += local;
                         if constexpr (REMOTE) remote_append(a, s && !local, r);
                     }
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(256, AMBER_WEALTH_MINB) wealth_step_kernel(con
 // wealth column and exact 32-bit receiver counters live in shared memory, so
 // a step costs two __syncthreads instead of a kernel launch, and no counter
 // can overflow (sent == got by construction).
-constexpr int kSmallMax = 16384;  // agents (64 KB column + 64 KB counters)
+constexpr int kSmallMax = 16384;  // agents (64 KB column + 2 x 64 KB counters)
 
 struct SmallArgs {
     PhiloxKey key;
@@ -261,58 +265,107 @@ struct SmallArgs {
     int digest;
 };
 
+// One __syncthreads per step: a thread applies step t to its own agent pairs
+// (the counts of step t were completed before the barrier), then immediately
+// scatters step t+1 from the new wealth of the same pair into the other
+// counter buffer and re-zeroes its entries of this one; per-step observables
+// are warp-reduced into shared accumulators (three rotating sets: step t's
+// values are complete after the barrier while steps t+1, t+2 accumulate) and
+// written to the ring by thread 0.
 __global__ void __launch_bounds__(1024, 1) wealth_small_kernel(const SmallArgs a)
 {
     extern __shared__ __align__(16) int32_t sw[];
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(sw + kSmallMax);
-    const int tid = threadIdx.x, nt = blockDim.x;
+    uint32_t* cnt0 = reinterpret_cast<uint32_t*>(sw + kSmallMax);
+    uint32_t* cnt1 = cnt0 + kSmallMax;
+    __shared__ unsigned long long acc[3][5];  // {total, active, digest, sent, got}
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
     const uint32_t n = static_cast<uint32_t>(a.n);
     const unsigned long long m = a.n - (a.exclude_self ? 1 : 0);
     for (uint32_t i = tid; i < n; i += nt) {
         sw[i] = a.w_in[i];
-        cnt[i] = 0u;
+        cnt0[i] = 0u;
+        cnt1[i] = 0u;
+    }
+    if (tid < 15) (&acc[0][0])[tid] = 0ull;
+    __syncthreads();
+    auto warp_add = [&](unsigned long long v, unsigned long long* dst) {
+        v = warp_sum_u64(v);
+        if (lane == 0 && v) atomicAdd(dst, v);
+    };
+    // scatter of step t from the pair (i0, i0 + 1) with wealth (v0, v1)
+    auto scatter = [&](uint32_t p, int32_t v0, int32_t v1, uint32_t t, uint32_t* cnt) -> unsigned long long {
+        const uint32_t i0 = 2 * p;
+        const bool s0 = v0 >= a.amount, s1 = (i0 + 1 < n) && v1 >= a.amount;
+        unsigned long long sent = 0;
+        if (s0 || s1) {
+            const uint4 x = stream_block(a.key, TAG_WEALTH_RECV, p, t);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (h ? s1 : s0) {
+                    unsigned long long r = mulhi64(lane64_of(x, h), m);
+                    if (a.exclude_self) r += (r >= i0 + h);
+                    atomicAdd(cnt + r, 1u);
+                    ++sent;
+                }
+            }
+        }
+        return sent;
+    };
+    const uint32_t npairs = (n + 1) / 2;
+    const uint32_t ring_cap = static_cast<uint32_t>(a.ring_cap);
+    uint32_t slot_idx = static_cast<uint32_t>(a.t0 % a.ring_cap);
+    {   // prime: scatter of step t0
+        unsigned long long sent = 0;
+        for (uint32_t p = tid; p < npairs; p += nt)
+            sent += scatter(p, sw[2 * p], 2 * p + 1 < n ? sw[2 * p + 1] : 0, a.t0, (a.t0 & 1) ? cnt1 : cnt0);
+        warp_add(sent, &acc[a.t0 % 3][3]);
     }
     __syncthreads();
     for (int64_t k = 0; k < a.steps; ++k) {
         const uint32_t t = a.t0 + static_cast<uint32_t>(k);
-        // scatter: one Philox block per pair of agents (R4)
-        unsigned long long sent = 0;
-        for (uint32_t p = tid; 2 * p < n; p += nt) {
-            const uint32_t i0 = 2 * p;
-            const bool s0 = sw[i0] >= a.amount, s1 = (i0 + 1 < n) && sw[i0 + 1] >= a.amount;
-            if (s0 || s1) {
-                const uint4 x = stream_block(a.key, TAG_WEALTH_RECV, p, t);
+        uint32_t* cur = (t & 1) ? cnt1 : cnt0;
+        uint32_t* nxt = (t & 1) ? cnt0 : cnt1;
+        const bool more = k + 1 < a.steps;
+        unsigned long long tot = 0, act = 0, got = 0, dig = 0, sent = 0;
+        for (uint32_t p = tid; p < npairs; p += nt) {
+            int32_t v[2] = {0, 0};
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (h ? s1 : s0) {
-                        unsigned long long r = mulhi64(lane64_of(x, h), m);
-                        if (a.exclude_self) r += (r >= i0 + h);
-                        atomicAdd(cnt + r, 1u);
-                        ++sent;
-                    }
-                }
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t i = 2 * p + h;
+                if (i >= n) continue;
+                const uint32_t c = cur[i];
+                cur[i] = 0u;
+                int32_t x = sw[i];
+                x = x - (x >= a.amount ? a.amount : 0) + a.amount * static_cast<int32_t>(c);
+                sw[i] = x;
+                v[h] = x;
+                tot += static_cast<unsigned long long>(static_cast<long long>(x));
+                act += x > 0;
+                got += c;
+                if (a.digest) dig += digest_term(i, static_cast<uint32_t>(x));
             }
+            if (more) sent += scatter(p, v[0], v[1], t + 1, nxt);
         }
-        __syncthreads();
-        // apply + observables
-        unsigned long long tot = 0, act = 0, got = 0, dig = 0;
-        for (uint32_t i = tid; i < n; i += nt) {
-            const uint32_t c = cnt[i];
-            cnt[i] = 0u;
-            int32_t v = sw[i];
-            v = v - (v >= a.amount ? a.amount : 0) + a.amount * static_cast<int32_t>(c);
-            sw[i] = v;
-            tot += static_cast<unsigned long long>(static_cast<long long>(v));
-            act += v > 0;
-            got += c;
-            if (a.digest) dig += digest_term(i, static_cast<uint32_t>(v));
+        // per-warp sums fit 32 bits (total wealth < 2^31 is checked at creation):
+        // one REDUX each; only the digest needs a 64-bit shuffle reduction
+        const int tw = __reduce_add_sync(0xffffffffu, static_cast<int>(static_cast<long long>(tot)));
+        const unsigned aw = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(act));
+        const unsigned gw = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(got));
+        const unsigned sw_ = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(sent));
+        if (lane == 0) {
+            if (tw) atomicAdd(&acc[t % 3][0], static_cast<unsigned long long>(static_cast<long long>(tw)));
+            if (aw) atomicAdd(&acc[t % 3][1], static_cast<unsigned long long>(aw));
+            if (gw) atomicAdd(&acc[t % 3][4], static_cast<unsigned long long>(gw));
+            if (sw_) atomicAdd(&acc[(t + 1) % 3][3], static_cast<unsigned long long>(sw_));
         }
-        Slot* sl = a.ring + (t % a.ring_cap);
-        if (tid == 0) *sl = Slot{0, 0, 0, 0, 0};
+        if (a.digest) warp_add(dig, &acc[t % 3][2]);
         __syncthreads();
-        unsigned long long vals[5] = {tot, act, dig, sent, got};
-        unsigned long long* const outs[5] = {&sl->total, &sl->active, a.digest ? &sl->digest : nullptr, &sl->sent, &sl->got};
-        block_sum_atomic<5>(vals, outs);
+        if (tid < 5) {  // step t's record is complete; its accumulator set is next used by step t + 3
+            unsigned long long* x = acc[t % 3];
+            (&a.ring[slot_idx].total)[tid] = x[tid];
+            x[tid] = 0ull;
+        }
+        if (++slot_idx == ring_cap) slot_idx = 0;
     }
     for (uint32_t i = tid; i < n; i += nt) a.w_out[i] = sw[i];
 }
@@ -740,10 +793,11 @@ public:
                 const int64_t chunk = std::min<int64_t>(nsteps - done, metrics_cap - 4);
                 SmallArgs a{key, wb[cur].p, wb[other(cur, -1)].p, n, p.amount, p.exclude_self,
                             static_cast<uint32_t>(t), chunk, ring.p, metrics_cap, digest_on ? 1 : 0};
-                const size_t smem = static_cast<size_t>(kSmallMax) * 8;
+                const size_t smem = static_cast<size_t>(kSmallMax) * 12;  // column + two counter buffers
                 AMBER_CUDA(cudaFuncSetAttribute(wealth_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 static_cast<int>(smem)));
-                int threads = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(32, ceil_div(n, 32) * 32)));
+                // one thread per agent pair (R4: one Philox block feeds a pair)
+                int threads = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(32, ceil_div((n + 1) / 2, 32) * 32)));
                 if (block) threads = static_cast<int>(block);
                 prof.launch(rt.stream, "wealth_small_persistent", [&] {
                     wealth_small_kernel<<<1, threads, smem, rt.stream>>>(a);
