@@ -276,7 +276,16 @@ int amber_digest(amber_model* m, const char* name, uint64_t* out);
  * observable), "metrics_capacity" (ring size, >= 16), "block" (threads per
  * block for launch-geometry invariance tests; 0 = tuned default),
  * "grid" (persistent grid size; 0 = tuned default), "persistent"
- * (SIR/Boids: 0 = per-step kernels, 1 = graph-captured step sequence). */
+ * (wealth/SIR: 1 = all steps of a call in one launch (single-CTA kernel for
+ * wealth N <= 16384; cooperative direction-optimizing kernel for SIR),
+ * 0 = one launch per step, pull only for SIR); Boids: "lanes" (1/4/8/16 lanes
+ * per agent in the stencil), "tiled", "fused" (measured alternatives).
+ * Read-only (amber_get_option): wealth "replays" (exact-replay count, after
+ * the overflow check), "counter_bits", "scatter" (0 bins, 1 packed-counter
+ * atomics, 2 fused bins, 3 segmented bins), "exchange" (sharded: 0 none,
+ * 1 NCCL send/recv, 2 P2P peer-mapped buckets; set at the first step); SIR
+ * "edges"; Boids "cells_per_side", sharded Boids "own_agents" and
+ * "slab_columns". */
 int amber_set_option(amber_model* m, const char* key, int64_t value);
 int amber_get_option(amber_model* m, const char* key, int64_t* value);
 
