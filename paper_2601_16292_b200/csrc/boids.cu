@@ -37,6 +37,7 @@ struct BoidsArgs {
     float L, R, rs, wc, wa, ws, vmax, dt;
     int nc;       // cells per side
     float inv_cs; // nc / L
+    int span = 1; // stencil half-width in cells: 1 (cells >= R) or 2 (cells >= R/2)
 };
 
 __device__ __forceinline__ int cell_coord(float x, const BoidsArgs& a)
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(256) boids_step_kernel(const float4* __restric
         const float4 me = sorted[p];
         const int cx = cell_coord(me.x, a), cy = cell_coord(me.y, a);
         Acc acc{0, 0, 0, 0, 0, 0, 0};
-        const int span = a.nc >= 3 ? 1 : 0;  // nc == 1: the single cell is visited once
+        const int span = a.nc >= 3 ? a.span : 0;  // nc == 1: the single cell is visited once
 #pragma unroll 1
         for (int dyc = -span; dyc <= span; ++dyc) {
             int yy = cy + dyc;
@@ -551,26 +552,28 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
                 }
                 if (q < e) boid_accumulate<false>(sorted[q], me, L, halfL, R2, rs2, acc);
             };
+            const int sp = a.span;
             const int cx0 = a.nc >= 3 ? cell_coord(me.x, a) : 0, cy0 = a.nc >= 3 ? cell_coord(me.y, a) : 0;
-            if (a.nc >= 5 && cx0 >= 1 && cx0 + 1 < a.nc && cy0 >= 1 && cy0 + 1 < a.nc) {
+            // interior: the whole stencil inside the box and (sp + 1) cells <= L/2
+            if (a.nc >= 2 * sp + 3 && cx0 >= sp && cx0 + sp < a.nc && cy0 >= sp && cy0 + sp < a.nc) {
 #pragma unroll 1
-                for (int dyc = -1; dyc <= 1; ++dyc) {
+                for (int dyc = -sp; dyc <= sp; ++dyc) {
                     const int row = (cy0 + dyc) * a.nc;
-                    run_in(start[row + cx0 - 1], start[row + cx0 + 2]);
+                    run_in(start[row + cx0 - sp], start[row + cx0 + sp + 1]);
                 }
             } else if (a.nc >= 3) {
                 const int cx = cx0, cy = cy0;
 #pragma unroll 1
-                for (int dyc = -1; dyc <= 1; ++dyc) {
+                for (int dyc = -sp; dyc <= sp; ++dyc) {
                     int yy = cy + dyc;
                     yy = yy < 0 ? yy + a.nc : (yy >= a.nc ? yy - a.nc : yy);
                     const int row = yy * a.nc;
-                    if (cx >= 1 && cx + 1 < a.nc) {
-                        // cells cx-1, cx, cx+1 of a row are contiguous in the sorted array
-                        run(start[row + cx - 1], start[row + cx + 2]);
+                    if (cx >= sp && cx + sp < a.nc) {
+                        // cells cx-sp .. cx+sp of a row are contiguous in the sorted array
+                        run(start[row + cx - sp], start[row + cx + sp + 1]);
                     } else {
 #pragma unroll 1
-                        for (int dxc = -1; dxc <= 1; ++dxc) {
+                        for (int dxc = -sp; dxc <= sp; ++dxc) {
                             int xx = cx + dxc;
                             xx = xx < 0 ? xx + a.nc : (xx >= a.nc ? xx - a.nc : xx);
                             run(start[row + xx], start[row + xx + 1]);
@@ -1096,14 +1099,25 @@ public:
         AMBER_REQUIRE(p.L > 0 && p.R > 0 && p.rs >= 0 && p.rs <= p.R && p.vmax > 0 && p.dt >= 0,
                       "Boids params out of range (need L, R, vmax > 0, 0 <= rs <= R, dt >= 0)");
         AMBER_REQUIRE(p.R < 0.5f * p.L && p.vmax * p.dt < 0.5f * p.L, "Boids needs R < L/2 and vmax*dt < L/2");
-        ba = BoidsArgs{p.L, p.R, p.rs, p.wc, p.wa, p.ws, p.vmax, p.dt, 0, 0.f};
-        // Cells of side >= R*(1+1e-3): float rounding of the cell index can then
-        // never hide a neighbour outside the 3x3 stencil.  The stencil needs >= 3
-        // distinct cells per side; boxes with fewer use one cell holding every
-        // agent (each agent then scans all others, i.e. the brute-force definition).
-        double nc = std::floor(static_cast<double>(p.L) / (static_cast<double>(p.R) * 1.001));
-        nc = std::min(nc, 4096.0);
-        ba.nc = static_cast<int>(nc >= 3 ? nc : 1);
+        ba = BoidsArgs{p.L, p.R, p.rs, p.wc, p.wa, p.ws, p.vmax, p.dt, 0, 0.f, 1};
+        // Cells of side >= R*(1+1e-3) with a 3x3 stencil (default), or >= R/2*(1+1e-3)
+        // with a 5x5 stencil (AMBER_BOIDS_SPAN=2: 25 (R/2)^2 vs 9 R^2, about 30% fewer
+        // candidates, but five short row runs per agent instead of three: measured
+        // slower, C3 99 vs 83 us/step, V3 34.9 vs 32.1 ms/step).  The margin means float
+        // rounding of the cell index can never hide a neighbour outside the
+        // stencil.  The stencil needs >= 3 distinct cells per side; boxes with
+        // fewer use one cell holding every agent (each agent then scans all
+        // others, i.e. the brute-force definition).  Any covering stencil gives
+        // the same result (exact fixed-point sums, B3).
+        const double nc1 = std::min(std::floor(static_cast<double>(p.L) / (static_cast<double>(p.R) * 1.001)), 4096.0);
+        const double nc2 = std::min(std::floor(static_cast<double>(p.L) / (static_cast<double>(p.R) * 0.5005)), 8192.0);
+        const double area1 = 9.0 * std::pow(p.L / std::max(nc1, 1.0), 2), area2 = 25.0 * std::pow(p.L / std::max(nc2, 1.0), 2);
+        const char* hc = getenv("AMBER_BOIDS_SPAN");
+        const bool half = nc2 >= 7 && hc && hc[0] == '2';
+        (void)area1;
+        (void)area2;
+        ba.nc = half ? static_cast<int>(nc2) : static_cast<int>(nc1 >= 3 ? nc1 : 1);
+        ba.span = half ? 2 : 1;
         ba.inv_cs = static_cast<float>(ba.nc / static_cast<double>(p.L));
         ncell = ba.nc * ba.nc;
         st.allocate(&rt, n);
@@ -1208,7 +1222,7 @@ public:
                 check_launch("boids_scatter_kernel");
             }
             const BoidsArgs a = ba;
-            if (ba.nc >= 3 && tiled) {
+            if (ba.nc >= 3 && tiled && ba.span == 1) {  // the tiled stencil is 3x3 only
                 const int tps = (ba.nc + kT - 1) / kT;
                 prof.launch(rt.stream, "boids_step", [&] {
                     boids_tile_kernel<<<tps * tps, 256, kTileCap * sizeof(float4), rt.stream>>>(
@@ -1366,6 +1380,10 @@ public:
             *v = ba.nc;
             return true;
         }
+        if (std::string(key) == "stencil_span") {
+            *v = ba.span;
+            return true;
+        }
         if (std::string(key) == "tiled") {
             *v = tiled;
             return true;
@@ -1410,7 +1428,7 @@ public:
         AMBER_REQUIRE(p.L > 0 && p.R > 0 && p.rs >= 0 && p.rs <= p.R && p.vmax > 0 && p.dt >= 0,
                       "Boids params out of range (need L, R, vmax > 0, 0 <= rs <= R, dt >= 0)");
         AMBER_REQUIRE(p.R < 0.5f * p.L && p.vmax * p.dt < 0.5f * p.L, "Boids needs R < L/2 and vmax*dt < L/2");
-        ba = BoidsArgs{p.L, p.R, p.rs, p.wc, p.wa, p.ws, p.vmax, p.dt, 0, 0.f};
+        ba = BoidsArgs{p.L, p.R, p.rs, p.wc, p.wa, p.ws, p.vmax, p.dt, 0, 0.f, 1};  // 3x3 stencil, halo 1 column
         double nc = std::floor(static_cast<double>(p.L) / (static_cast<double>(p.R) * 1.001));
         nc = std::min(nc, 4096.0);
         AMBER_REQUIRE(nc >= 3 && nc >= rt.world, "sharded Boids needs >= 3 cells per side and >= 1 cell column per rank");

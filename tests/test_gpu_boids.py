@@ -79,11 +79,15 @@ def test_c3_hundred_steps_ensemble(orc):
     assert match == 1.0
 
 
-def test_dense_flock_tile_overflow_path(orc):
+@pytest.mark.parametrize("span", ["1", "2"])
+def test_dense_flock_tile_overflow_path(orc, monkeypatch, span):
     # strong cohesion packs agents into few cells: tiles exceed the shared-memory
-    # staging and take the global-memory path; results must still be exact
+    # staging and take the global-memory path; results must still be exact.
+    # span 1: 3x3 stencil of R cells (the tiled kernel); span 2: 5x5 of R/2 cells
+    monkeypatch.setenv("AMBER_BOIDS_SPAN", span)
     cfg = dict(C3_BOIDS, n=6000, L=100.0, R=10.0, rs=0.5, wc=0.5, wa=0.5, ws=0.0, vmax=2.0, seed=9)
     m = make(cfg)
+    assert m.get_option("stencil_span") == int(span)
     m.set_option("tiled", 1)
     st = state(m)
     P = oparams(orc, cfg)
@@ -108,10 +112,16 @@ def test_small_boxes_and_params(orc, kw):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
 
 
-def test_geometry_invariance_and_io(orc):
+def test_geometry_invariance_and_io(orc, monkeypatch):
     cfg = dict(C3_BOIDS, n=20_000, L=450.0)
     a = make(cfg)
     a.step(10)
+    monkeypatch.setenv("AMBER_BOIDS_SPAN", "2")  # the other stencil (5x5 of R/2 cells) gives the same bits
+    s1 = make(cfg)
+    assert s1.get_option("stencil_span") == 2 and a.get_option("stencil_span") == 1
+    s1.step(10)
+    for x, y in zip(state(a), state(s1)):
+        assert np.array_equal(x, y)
     b = make(cfg)
     b.set_option("tiled", 1)  # shared-memory tiled stencil kernel instead of the per-agent one
     b.set_option("block", 64)
