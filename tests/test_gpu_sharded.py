@@ -122,6 +122,7 @@ def test_nccl_plumbing_single_rank(orc, monkeypatch):
     n, seed = 70_001, 12
     m = Model("wealth", n, wealth_params(counter_bits=2), seed, unique_id=nccl_unique_id())
     m.step(15)
+    assert m.get_option("exchange") == 2  # P2P: IPC export + ncclAllGather of the handles + barrier all-reduces
     ref, tot, _, _ = orc.wealth_run(np.ones(n, np.int32), seed, 0, 15)
     assert np.array_equal(m.read_column("wealth"), ref)
     assert np.array_equal(m.metrics("total_wealth"), tot)
