@@ -216,3 +216,18 @@ def test_small_metrics_ring_wraps(orc):
     assert np.array_equal(m.read_column("state"), ref)
     got = m.metrics("I")
     assert len(got) == 16 and np.array_equal(got, counts[-16:, 1])
+
+
+def test_sweep_full_c5_all_replicates_vs_oracle_golden():
+    # all 4,096 final R fractions of BASELINE config 5 against the oracle's values
+    # (tests/golden/c5_sweep_oracle.txt, written by tools/make_oracle_goldens.py,
+    # which calls only oracle/); exact ratios, so compared bit for bit
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "c5_sweep_oracle.txt")
+    rows = [ln.split() for ln in open(path) if not ln.startswith("#")]
+    want = np.array([float(r[3]) for r in rows])
+    c = C5_SWEEP
+    betas, seeds = sweep_replicates(c)
+    assert np.array_equal(np.array([float(r[1]) for r in rows]), betas)
+    got = sweep(c["n"], sir_params(c["mean_degree"], 0.0, c["gamma"], c["init_frac"]), betas, seeds, c["steps"])
+    assert np.array_equal(got, want)

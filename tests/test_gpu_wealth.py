@@ -272,3 +272,24 @@ def test_small_metrics_ring_and_per_step_reads(orc):
         w = w_next
     assert np.array_equal(m.read_column("wealth"), w)
     assert m.get_option("replays") > 0
+
+
+def test_c4_all_1000_steps_vs_oracle_golden():
+    # BASELINE config 4 at full size, all 1,000 steps, in the bench configuration
+    # (default scatter, one fused launch per step): the per-step D1 digest of the
+    # whole column, total wealth and active count against the oracle's values
+    # (tests/golden/c4_wealth_oracle.txt, tools/make_oracle_goldens.py, oracle/ only)
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "c4_wealth_oracle.txt")
+    if not os.path.exists(path):
+        pytest.skip("golden file not generated (tools/make_oracle_goldens.py c4, ~1 h of CPU)")
+    rows = np.array([[int(x) for x in ln.split()] for ln in open(path) if not ln.startswith("#")], dtype=object)
+    cfg = C4_WEALTH_SCALE
+    m = make(cfg["n"], cfg["seed"])
+    m.set_option("digest", 1)
+    m.step(cfg["steps"])
+    dig = m.metrics("digest")
+    assert len(dig) == cfg["steps"]
+    assert [int(x) for x in dig] == [int(x) for x in rows[:, 1]]
+    assert [int(x) for x in m.metrics("total_wealth")] == [int(x) for x in rows[:, 2]]
+    assert [int(x) for x in m.metrics("active")] == [int(x) for x in rows[:, 3]]
