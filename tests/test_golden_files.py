@@ -1,0 +1,41 @@
+"""CPU checks of the oracle-written full-size golden files (tools/make_oracle_goldens.py):
+format, exact-ratio consistency and the invariants the paper fixes (wealth is
+conserved; R fractions lie in [0, 1] and rise with beta)."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2601_16292_b200.workloads import C4_WEALTH_SCALE, C5_SWEEP, sweep_replicates
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def rows(name):
+    return [ln.split() for ln in open(os.path.join(GOLD, name)) if not ln.startswith("#")]
+
+
+def test_c5_golden_consistent():
+    r = rows("c5_sweep_oracle.txt")
+    betas, _ = sweep_replicates(C5_SWEEP)
+    assert len(r) == 4096 and [int(x[0]) for x in r] == list(range(4096))
+    assert np.array_equal(np.array([float(x[1]) for x in r]), betas)
+    cnt = np.array([int(x[2]) for x in r])
+    frac = np.array([float(x[3]) for x in r])
+    assert np.array_equal(frac, cnt / C5_SWEEP["n"])  # exact ratios (S5)
+    assert (cnt >= 100).all() and (cnt <= C5_SWEEP["n"]).all()  # the 1% initially infected recover (gamma > 0)
+    per_beta = frac.reshape(64, 64).mean(axis=1)
+    assert per_beta[-1] > 0.95 and per_beta[0] < 0.3 and per_beta[-1] > per_beta[0]
+
+
+def test_c4_golden_consistent():
+    path = os.path.join(GOLD, "c4_wealth_oracle.txt")
+    if not os.path.exists(path):
+        pytest.skip("c4 golden not generated yet")
+    r = np.array([[int(v) for v in x] for x in rows("c4_wealth_oracle.txt")], dtype=np.int64)
+    c = C4_WEALTH_SCALE
+    assert r.shape == (c["steps"], 4) and (r[:, 0] == np.arange(c["steps"])).all()
+    assert (r[:, 2] == c["n"] * c["w0"]).all()  # W pin (i): total wealth conserved at every step
+    assert ((r[:, 3] > 0) & (r[:, 3] <= c["n"])).all()
+    # active fraction settles near 2 - sqrt(2) (sanity band only)
+    assert abs(r[-100:, 3].mean() / c["n"] - (2 - np.sqrt(2))) < 0.02
