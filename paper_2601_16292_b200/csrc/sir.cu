@@ -503,7 +503,11 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
 // fewer than the susceptible ones (counts of the previous step from its ring
 // slot, so every block takes the same decision), otherwise it pulls.  Both
 // directions give identical results (S3); the tests check it.
-__global__ void __launch_bounds__(256, 3) sir_persistent_kernel(const SirStepArgs a)
+#ifndef AMBER_SIR_PT
+#define AMBER_SIR_PT 256
+#endif
+constexpr int kSirPT = AMBER_SIR_PT;  // threads per block of the persistent kernel
+__global__ void __launch_bounds__(kSirPT, 768 / kSirPT) sir_persistent_kernel(const SirStepArgs a)
 {
     cg::grid_group grid = cg::this_grid();
     int cur = a.cur;
@@ -752,26 +756,27 @@ public:
             check_launch("sir_zero_slots");
             const int threads = block ? static_cast<int>(std::min<int64_t>(block, 256)) : 256;
             if (persistent && chunk > 1) {
+                const int pthreads = block ? threads : kSirPT;
                 int per_sm = 0;
-                AMBER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sir_persistent_kernel, threads, 0));
+                AMBER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sir_persistent_kernel, pthreads, 0));
                 // latency-bound: many resident warps help, but the grid barrier
                 // cost grows with the block count; 3 blocks/SM measured best (C2)
                 // (C2); large populations are bound by random L2 lookups instead: full occupancy
-                const int per = n_pad > (1ll << 22) ? per_sm : std::min(per_sm, 3);
+                const int per = n_pad > (1ll << 22) ? per_sm : std::min(per_sm, std::max(1, 768 / pthreads));
                 int blocks = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(per) * rt.num_sms,
-                                                                ceil_div(n_pad, threads)));
+                                                                ceil_div(n_pad, pthreads)));
                 if (grid) blocks = static_cast<int>(std::min<int64_t>(grid, static_cast<int64_t>(per_sm) * rt.num_sms));
                 blocks = std::max(blocks, 1);
                 SirStepArgs a = args(chunk);
                 queue.zero_async(rt.stream);
                 a.queue = queue.p;
-                const int64_t warps = static_cast<int64_t>(blocks) * threads / 32;
+                const int64_t warps = static_cast<int64_t>(blocks) * pthreads / 32;
                 a.grab = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, (n_pad / 32) / (warps * 8))));
                 if (n_pad / 32 <= 2 * warps) a.queue = nullptr;  // <= 2 chunks per warp: static striding
                 void* kargs[] = {&a};
                 prof.launch(rt.stream, "sir_persistent", [&] {
                     AMBER_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sir_persistent_kernel), blocks,
-                                                           threads, kargs, 0, rt.stream));
+                                                           pthreads, kargs, 0, rt.stream));
                 });
                 check_launch("sir_persistent_kernel");
                 t += chunk;
