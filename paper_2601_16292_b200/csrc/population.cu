@@ -24,7 +24,8 @@ constexpr size_t kStackBytes = kMaxStack * kTile * sizeof(double);   // 64 KB pe
 
 struct Prog {
     int n;
-    int uses_id;  // program reads the agent id (ID / RAND): load the id column
+    int uses_id;    // program reads the agent id (ID / RAND): load the id column
+    int max_depth;  // deepest stack the program reaches (sizes the shared stack tile)
     amber_instr ins[kMaxProg];
 };
 
@@ -580,10 +581,16 @@ struct Population {
         cap = nc;
     }
 
-    int tiles_grid() const
+    static size_t stack_bytes(const Prog& a, const Prog& b)
     {
+        return static_cast<size_t>(std::max(1, std::max(a.max_depth, b.max_depth))) * kTile * sizeof(double);
+    }
+
+    int tiles_grid(size_t smem = kStackBytes) const
+    {
+        const int per_sm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(2048 / kThreads, (220u << 10) / smem)));
         return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(rows, 1), kTile),
-                                                                        rt.num_sms * 3)));
+                                                                        static_cast<int64_t>(rt.num_sms) * per_sm)));
     }
 
     int grid_for(int64_t n) const
@@ -704,6 +711,7 @@ struct Population {
             AMBER_REQUIRE(depth >= pop, "expression stack underflow");
             depth += push - pop;
             AMBER_REQUIRE(depth <= kMaxStack, "expression stack deeper than 8");
+            P.max_depth = std::max(P.max_depth, depth);
             P.ins[k] = ins[k];
         }
         AMBER_REQUIRE(n == 0 || depth == 1, "expression must leave exactly one value");
@@ -767,7 +775,11 @@ struct Population {
                                                        alive.p, rows, cnt_p);
             check_launch("pop_binop_kernel");
         } else if (rows) {
-            pop_update_kernel<<<tiles_grid(), kThreads, kStackBytes, rt.stream>>>(pe, pw, views(), tgt, ids.p, alive.p, rows,
+            // the shared stack tile only needs the programs' deepest stack: shallow
+            // programs (the common case) run more blocks per SM, so more column
+            // loads are in flight (measured: depth 3 -> 64 KB -> 24 KB per block)
+            const size_t smem = stack_bytes(pe, pw);
+            pop_update_kernel<<<tiles_grid(smem), kThreads, smem, rt.stream>>>(pe, pw, views(), tgt, ids.p, alive.p, rows,
                                                                      static_cast<uint32_t>(step), key, cnt_p);
             check_launch("pop_update_kernel");
         }
@@ -782,12 +794,13 @@ struct Population {
     {
         AMBER_REQUIRE(agg >= AMBER_AGG_SUM && agg <= AMBER_AGG_COUNT, "unknown aggregate");
         const Prog pe = prog(e, ne, agg == AMBER_AGG_COUNT), pw = prog(w, nw, true);
-        const int g = tiles_grid();
+        const size_t smem = stack_bytes(pe, pw);
+        const int g = tiles_grid(smem);
         DevBuf<double> part;
         part.allocate(&rt, 4 * g);
         std::vector<double> h(4 * g, 0.0);
         if (rows) {
-            pop_aggregate_kernel<<<g, kThreads, kStackBytes, rt.stream>>>(pe, pw, views(), ids.p, alive.p, rows,
+            pop_aggregate_kernel<<<g, kThreads, smem, rt.stream>>>(pe, pw, views(), ids.p, alive.p, rows,
                                                            static_cast<uint32_t>(step), key, part.p);
             check_launch("pop_aggregate_kernel");
             AMBER_CUDA(cudaMemcpyAsync(h.data(), part.p, h.size() * 8, cudaMemcpyDeviceToHost, rt.stream));
