@@ -389,29 +389,38 @@ def bench_small(args):
                                        "note": "CUDA events over 50 asynchronous update calls"}}))
         return 0
     if w == "population":
-        # NEXT-4 generic columnar update through the expression interpreter (not the
-        # Listing-1 fast path): a filtered update with a counter-based draw over 1e8 rows
+        # NEXT-4 general columnar updates (not the Listing-1 fast path): programs are
+        # compiled at run time into straight-line kernels (or interpreted, AMBER_POP_JIT=0)
         from paper_2601_16292_b200.population import Population, col, rand
         n = 100_000_000
-        p = Population({"wealth": "i32", "state": "u8"}, capacity=n)
-        p.add_agents(n, wealth=3, state=0)
-        prog = ((col("wealth") - 1).max(0) + (rand(7) < 0.5), col("state") == 0)
-        p.update("wealth", prog[0], where=prog[1])
-        p.synchronize()
-        k = 20
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(p.stream)
-        for _ in range(k):
-            p.update("wealth", prog[0], where=prog[1], count=False)
-        e1.record(p.stream)
-        p.synchronize()
-        dt = e0.elapsed_time(e1) / k / 1e3
         hbm, kind = peaks()
-        ach = 10.0 * n / dt / 1e9  # alive mask 1 B + state 1 B + wealth read 4 B + write 4 B per row
-        print(json.dumps({"workload": "population", "n": n, "ms_per_update": dt * 1e3, "value": n / dt,
-                          "unit": "rows/s", "program": "wealth = max(wealth-1, 0) + (rand < 0.5) where state == 0",
-                          "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                                       "frac": ach / hbm, "alg_bytes_per_row": 10}}))
+        cases = [("wealth = max(wealth-1, 0) + 2*state where state == 0",
+                  (col("wealth") - 1).max(0) + col("state") * 2, col("state") == 0, 10.0,
+                  "alive 1 + state 1 + wealth 4 read + 4 written"),
+                 ("wealth = max(wealth-1, 0) + (rand < 0.5) where state == 0",
+                  (col("wealth") - 1).max(0) + (rand(7) < 0.5), col("state") == 0, 18.0,
+                  "alive 1 + state 1 + agent id 8 (keys the draw) + wealth 4 read + 4 written")]
+        res = []
+        for name, e, wh, bpr, rule in cases:
+            p = Population({"wealth": "i32", "state": "u8"}, capacity=n)
+            p.add_agents(n, wealth=3, state=0)
+            p.update("wealth", e, where=wh)
+            p.synchronize()
+            k = 20
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(p.stream)
+            for _ in range(k):
+                p.update("wealth", e, where=wh, count=False)
+            e1.record(p.stream)
+            p.synchronize()
+            dt = e0.elapsed_time(e1) / k / 1e3
+            ach = bpr * n / dt / 1e9
+            res.append({"program": name, "ms_per_update": dt * 1e3, "rows_per_s": n / dt,
+                        "paths_jit_interp": p.update_paths(),
+                        "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                                     "alg_bytes_per_row": bpr, "rule": rule}})
+            p.close()
+        print(json.dumps({"workload": "population", "n": n, "cases": res}))
         return 0
     if w in ("sirs", "sirs_scale"):
         c = W.CONFIGS[w]

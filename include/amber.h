@@ -394,6 +394,13 @@ int amber_population_compact(amber_population* p);
 /* *live = live agents, *rows = rows in use (live + dead before compaction). */
 int amber_population_size(amber_population* p, int64_t* live, int64_t* rows);
 
+/* Host-only counters: general-program updates (not the Listing-1 fast path)
+ * run so far as runtime-compiled kernels (*n_jit: NVRTC, sm_100a; the
+ * expression becomes straight-line double code) or through the columnar
+ * interpreter (*n_interp: no NVRTC, a failed compile, or AMBER_POP_JIT=0 when
+ * the population was created).  Both paths compute identical values. */
+int amber_population_update_paths(amber_population* p, int64_t* n_jit, int64_t* n_interp);
+
 /* Synchronous population-wide update: for every live row where `where`
  * evaluates != 0 (n_where == 0: every live row), target = expr(row), all rows
  * reading the pre-update snapshot (SPEC update_column / update_where).

@@ -31,7 +31,8 @@ SYMBOLS = ["amber_version", "amber_last_error", "amber_model_create", "amber_mod
            "amber_population_create", "amber_population_destroy", "amber_population_add_agents",
            "amber_population_remove_agents", "amber_population_compact", "amber_population_size",
            "amber_population_update", "amber_population_aggregate", "amber_population_read_column",
-           "amber_population_batch_set", "amber_population_synchronize", "amber_population_set_step"]
+           "amber_population_batch_set", "amber_population_synchronize", "amber_population_set_step",
+           "amber_population_update_paths"]
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -156,6 +157,7 @@ def load():
         "amber_population_batch_set": (C.c_int, [C.c_void_p, C.c_char_p, i64p, P(C.c_double), C.c_int64]),
         "amber_population_set_step": (C.c_int, [C.c_void_p, C.c_int64]),
         "amber_population_synchronize": (C.c_int, [C.c_void_p]),
+        "amber_population_update_paths": (C.c_int, [C.c_void_p, i64p, i64p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -357,6 +357,14 @@ int amber_population_size(amber_population* p, int64_t* live, int64_t* rows)
     });
 }
 
+int amber_population_update_paths(amber_population* p, int64_t* n_jit, int64_t* n_interp)
+{
+    return guarded([&] {
+        amber::population_update_paths(pimpl(p), n_jit, n_interp);
+        return 0;
+    });
+}
+
 int amber_population_update(amber_population* p, const char* target, const amber_instr* expr, int n_expr,
                             const amber_instr* where, int n_where, int64_t* n_updated)
 {

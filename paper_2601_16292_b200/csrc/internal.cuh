@@ -174,6 +174,7 @@ int64_t population_add(Population* p, int64_t n, const double* defaults);
 void population_remove(Population* p, const int64_t* ids, int64_t n);
 void population_compact(Population* p);
 void population_size(Population* p, int64_t* live, int64_t* rows);
+void population_update_paths(Population* p, int64_t* jit, int64_t* interp);
 int64_t population_update(Population* p, const char* target, const amber_instr* e, int ne, const amber_instr* w, int nw,
                           bool want_count);
 void population_synchronize(Population* p);

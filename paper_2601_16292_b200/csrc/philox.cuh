@@ -6,7 +6,12 @@
 // from the constant bank (no per-thread key schedule).
 #pragma once
 
+#ifdef __CUDACC_RTC__  // runtime-compiled expression kernels (population.cu JIT): no host headers
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+#else
 #include <cstdint>
+#endif
 
 namespace amber {
 
@@ -85,6 +90,7 @@ __device__ __forceinline__ uint32_t mulhi64_n32(unsigned long long x, uint32_t n
 }
 
 // R7: T(p) = ceil(p * 2^32) (host); Bernoulli draw is [x32 < T] compared in 64 bits.
+#ifndef __CUDACC_RTC__
 inline unsigned long long bernoulli_threshold_host(double p)
 {
     if (!(p >= 0.0)) return 0ull;
@@ -93,6 +99,7 @@ inline unsigned long long bernoulli_threshold_host(double p)
     unsigned long long f = static_cast<unsigned long long>(v);
     return (static_cast<double>(f) < v) ? f + 1 : f;
 }
+#endif
 
 // R8: uniform float in [0, 1).
 __device__ __forceinline__ float u01(uint32_t x) { return static_cast<float>(x >> 8) * (1.0f / 16777216.0f); }

@@ -6,10 +6,13 @@
 // population-wide updates / aggregates given as postfix expression programs
 // that one kernel evaluates per row (a tiny vectorised expression engine:
 // Listing 1's `wealth + 10` is [COL wealth][CONST 10][ADD]).
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cub/cub.cuh>
 #include <map>
+#include <mutex>
 
 #include "internal.cuh"
 #include "philox.cuh"
@@ -489,8 +492,230 @@ size_t dtype_size(int dt)
 
 }  // namespace
 
+// ---------------------------------------------------------------- expression JIT
+// General update programs are compiled at run time (NVRTC, sm_100a) into a
+// straight-line kernel: every referenced column of a row is loaded with its
+// own type, the postfix program becomes a chain of double expressions (the
+// interpreter's exact semantics: same ops, --fmad=false, IEEE div/sqrt, C store
+// conversion), the filter selects the store.  4 rows per thread, branch-free
+// loads, one count atomic per block.  Kernels are cached by source text;
+// without NVRTC (or if a compile fails) the interpreter runs instead.
+struct JitArgs {
+    void* col[kMaxCols];
+    const int64_t* ids;
+    const uint8_t* alive;
+    long long rows;
+    unsigned step;
+    unsigned k0[10], k1[10];
+    unsigned long long* count;
+};
+
+struct NvrtcApi {
+    void* h = nullptr;
+    int (*create)(void**, const char*, const char*, int, const char* const*, const char* const*) = nullptr;
+    int (*compile)(void*, int, const char* const*) = nullptr;
+    int (*cubin_size)(void*, size_t*) = nullptr;
+    int (*cubin)(void*, char*) = nullptr;
+    int (*log_size)(void*, size_t*) = nullptr;
+    int (*log)(void*, char*) = nullptr;
+    int (*destroy)(void**) = nullptr;
+    std::string csrc;  // include dir (this library's csrc/)
+    bool ok = false;
+};
+
+static NvrtcApi& nvrtc()
+{
+    static NvrtcApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        for (const char* name : {"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"}) {
+            api.h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
+            if (api.h) break;
+        }
+        if (!api.h) return;
+        api.create = reinterpret_cast<decltype(api.create)>(dlsym(api.h, "nvrtcCreateProgram"));
+        api.compile = reinterpret_cast<decltype(api.compile)>(dlsym(api.h, "nvrtcCompileProgram"));
+        api.cubin_size = reinterpret_cast<decltype(api.cubin_size)>(dlsym(api.h, "nvrtcGetCUBINSize"));
+        api.cubin = reinterpret_cast<decltype(api.cubin)>(dlsym(api.h, "nvrtcGetCUBIN"));
+        api.log_size = reinterpret_cast<decltype(api.log_size)>(dlsym(api.h, "nvrtcGetProgramLogSize"));
+        api.log = reinterpret_cast<decltype(api.log)>(dlsym(api.h, "nvrtcGetProgramLog"));
+        api.destroy = reinterpret_cast<decltype(api.destroy)>(dlsym(api.h, "nvrtcDestroyProgram"));
+        Dl_info info{};
+        if (!dladdr(reinterpret_cast<void*>(&nvrtc), &info) || !info.dli_fname) return;
+        std::string so(info.dli_fname);
+        api.csrc = so.substr(0, so.rfind('/') + 1) + "csrc";
+        FILE* f = fopen((api.csrc + "/philox.cuh").c_str(), "r");
+        if (!f) return;
+        fclose(f);
+        api.ok = api.create && api.compile && api.cubin_size && api.cubin && api.log_size && api.log && api.destroy;
+    });
+    return api;
+}
+
+static const char* jit_ctype(int dt)
+{
+    switch (dt) {
+        case AMBER_I32: return "int";
+        case AMBER_I64: return "long long";
+        case AMBER_F32: return "float";
+        case AMBER_F64: return "double";
+        default: return "unsigned char";
+    }
+}
+
+// Postfix program -> C expression statements; returns the result variable.
+static std::string jit_emit(const Prog& P, const Cols& C, const std::string& pfx, std::string& body)
+{
+    std::vector<std::string> st;
+    char buf[256];
+    for (int k = 0; k < P.n; ++k) {
+        const amber_instr& in = P.ins[k];
+        const std::string v = pfx + std::to_string(k);
+        auto pop1 = [&] { std::string x = st.back(); st.pop_back(); return x; };
+        switch (in.op) {
+            case AMBER_OP_CONST: {  // exact bit pattern (also inf / nan)
+                unsigned long long bits;
+                std::memcpy(&bits, &in.value, 8);
+                snprintf(buf, sizeof buf, "__longlong_as_double((long long)0x%llxULL)", bits);
+                body += "const double " + v + " = " + buf + ";\n";
+                break;
+            }
+            case AMBER_OP_COL:
+                body += "const double " + v + " = (double)((const " + jit_ctype(C.c[in.arg].dtype) + "*)a.col[" +
+                        std::to_string(in.arg) + "])[rc];\n";
+                break;
+            case AMBER_OP_ID: body += "const double " + v + " = (double)id;\n"; break;
+            case AMBER_OP_RAND: body += "const double " + v + " = rnd(K, " + std::to_string(in.arg) + "u, id, a.step);\n"; break;
+            case AMBER_OP_STEP: body += "const double " + v + " = (double)a.step;\n"; break;
+            case AMBER_OP_NEG: body += "const double " + v + " = -" + pop1() + ";\n"; break;
+            case AMBER_OP_ABS: body += "const double " + v + " = fabs(" + pop1() + ");\n"; break;
+            case AMBER_OP_FLOOR: body += "const double " + v + " = floor(" + pop1() + ");\n"; break;
+            case AMBER_OP_SQRT: body += "const double " + v + " = sqrt(" + pop1() + ");\n"; break;
+            case AMBER_OP_NOT: { const std::string x = pop1(); body += "const double " + v + " = " + x + " == 0.0 ? 1.0 : 0.0;\n"; break; }
+            case AMBER_OP_SELECT: {
+                const std::string b = pop1(), x = pop1(), c = pop1();
+                body += "const double " + v + " = " + c + " != 0.0 ? " + x + " : " + b + ";\n";
+                break;
+            }
+            default: {
+                const std::string b = pop1(), x = pop1();
+                std::string e;
+                switch (in.op) {
+                    case AMBER_OP_ADD: e = x + " + " + b; break;
+                    case AMBER_OP_SUB: e = x + " - " + b; break;
+                    case AMBER_OP_MUL: e = x + " * " + b; break;
+                    case AMBER_OP_DIV: e = x + " / " + b; break;
+                    case AMBER_OP_MIN: e = "fmin(" + x + ", " + b + ")"; break;
+                    case AMBER_OP_MAX: e = "fmax(" + x + ", " + b + ")"; break;
+                    case AMBER_OP_LT: e = "(" + x + " < " + b + ") ? 1.0 : 0.0"; break;
+                    case AMBER_OP_LE: e = "(" + x + " <= " + b + ") ? 1.0 : 0.0"; break;
+                    case AMBER_OP_GT: e = "(" + x + " > " + b + ") ? 1.0 : 0.0"; break;
+                    case AMBER_OP_GE: e = "(" + x + " >= " + b + ") ? 1.0 : 0.0"; break;
+                    case AMBER_OP_EQ: e = "(" + x + " == " + b + ") ? 1.0 : 0.0"; break;
+                    case AMBER_OP_NE: e = "(" + x + " != " + b + ") ? 1.0 : 0.0"; break;
+                    case AMBER_OP_AND: e = "(" + x + " != 0.0 && " + b + " != 0.0) ? 1.0 : 0.0"; break;
+                    case AMBER_OP_OR: e = "(" + x + " != 0.0 || " + b + " != 0.0) ? 1.0 : 0.0"; break;
+                    default: e = "0.0"; break;
+                }
+                body += "const double " + v + " = " + e + ";\n";
+            }
+        }
+        st.push_back(v);
+    }
+    return st.empty() ? std::string("1.0") : st.back();
+}
+
+static std::string jit_update_source(const Prog& pe, const Prog& pw, const Cols& C, int tgt)
+{
+    std::string body;
+    const std::string rw = pw.n ? jit_emit(pw, C, "w", body) : std::string("1.0");
+    const std::string re = jit_emit(pe, C, "e", body);
+    const bool uses_id = pe.uses_id || pw.uses_id;
+    std::string s;
+    s += "#include \"philox.cuh\"\n";
+    s += "struct JitArgs { void* col[" + std::to_string(kMaxCols) +
+         "]; const long long* ids; const unsigned char* alive; long long rows; unsigned step; unsigned k0[10], k1[10]; "
+         "unsigned long long* count; };\n";
+    s += "__device__ __forceinline__ double rnd(const amber::PhiloxKey& K, unsigned tag, long long id, unsigned step) {\n"
+         "  const uint4 w = amber::stream_block(K, tag, (unsigned long long)id >> 2, step);\n"
+         "  const unsigned q = (unsigned)(id & 3);\n"
+         "  return (double)amber::u01(q == 0 ? w.x : (q == 1 ? w.y : (q == 2 ? w.z : w.w)));\n}\n";
+    s += "extern \"C\" __global__ void __launch_bounds__(256) amber_jit_update(const JitArgs a) {\n"
+         "  amber::PhiloxKey K;\n  for (int i = 0; i < 10; ++i) { K.k0[i] = a.k0[i]; K.k1[i] = a.k1[i]; }\n"
+         "  unsigned long long cnt = 0;\n"
+         "  const long long stride = (long long)gridDim.x * 1024;\n"
+         "  for (long long base = (long long)blockIdx.x * 1024 + threadIdx.x; base < a.rows; base += stride) {\n"
+         "#pragma unroll\n  for (int m = 0; m < 4; ++m) {\n"
+         "    const long long r = base + m * 256;\n"
+         "    const bool valid = r < a.rows;\n"
+         "    const long long rc = valid ? r : 0;\n"
+         "    const bool live = valid && a.alive[rc];\n";
+    if (uses_id) s += "    const long long id = a.ids[rc];\n";
+    s += body;
+    s += "    if (live && (" + rw + ") != 0.0) {\n"
+         "      ((" + std::string(jit_ctype(C.c[tgt].dtype)) + "*)a.col[" + std::to_string(tgt) + "])[r] = (" +
+         jit_ctype(C.c[tgt].dtype) + ")(" + re + ");\n      ++cnt;\n    }\n  }\n  }\n"
+         "  if (a.count) {\n"
+         "    __shared__ unsigned long long red[8];\n"
+         "    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);\n"
+         "    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;\n"
+         "    __syncthreads();\n"
+         "    if (threadIdx.x == 0) { unsigned long long t = 0; for (int w = 0; w < 8; ++w) t += red[w];\n"
+         "      if (t) atomicAdd(a.count, t); }\n  }\n}\n";
+    return s;
+}
+
+struct JitCache {
+    std::mutex mu;
+    std::map<std::string, cudaKernel_t> kernels;
+    std::vector<cudaLibrary_t> libs;
+};
+
+static JitCache& jit_cache()
+{
+    static JitCache c;
+    return c;
+}
+
+// Compiled kernel for this source, or nullptr (no NVRTC / compile error: interpret instead).
+static cudaKernel_t jit_kernel(const std::string& src)
+{
+    NvrtcApi& api = nvrtc();
+    if (!api.ok) return nullptr;
+    JitCache& jc = jit_cache();
+    std::lock_guard<std::mutex> g(jc.mu);
+    auto it = jc.kernels.find(src);
+    if (it != jc.kernels.end()) return it->second;
+    cudaKernel_t kern = nullptr;
+    void* prog = nullptr;
+    if (api.create(&prog, src.c_str(), "amber_jit_update.cu", 0, nullptr, nullptr) == 0) {
+        const std::string inc = "-I" + api.csrc;
+        const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--prec-div=true", "--prec-sqrt=true",
+                              "--std=c++17", inc.c_str()};
+        if (api.compile(prog, 6, opts) == 0) {
+            size_t n = 0;
+            api.cubin_size(prog, &n);
+            std::vector<char> cubin(n);
+            api.cubin(prog, cubin.data());
+            cudaLibrary_t lib = nullptr;
+            if (cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) == cudaSuccess &&
+                cudaLibraryGetKernel(&kern, lib, "amber_jit_update") == cudaSuccess) {
+                jc.libs.push_back(lib);
+            } else {
+                cudaGetLastError();
+                kern = nullptr;
+            }
+        }
+        api.destroy(&prog);
+    }
+    jc.kernels[src] = kern;  // failures cached too (interpreted from then on)
+    return kern;
+}
+
 struct Population {
     Runtime rt;
+    bool jit = true;                      // AMBER_POP_JIT=0 at creation: interpreter only
+    int64_t n_jit = 0, n_interp = 0;      // general-program updates by path
     PhiloxKey key{};
     struct Column {
         std::string name;
@@ -504,6 +729,7 @@ struct Population {
 
     Population(const amber_column_spec* specs, int n, int64_t capacity, uint64_t seed, const amber_runtime* r)
     {
+        if (const char* e = getenv("AMBER_POP_JIT")) jit = e[0] != '0';
         rt.init(r);
         key = philox_key(seed);
         AMBER_REQUIRE(n >= 1 && n <= kMaxCols, "population needs 1..32 columns");
@@ -733,6 +959,7 @@ struct Population {
                           (pe.ins[1].op == AMBER_OP_CONST || pe.ins[1].op == AMBER_OP_COL) &&
                           pe.ins[2].op >= AMBER_OP_ADD && pe.ins[2].op <= AMBER_OP_MAX;
         const Cols C = views();
+        cudaKernel_t jk = nullptr;
         const int bcol = (fast && pe.ins[1].op == AMBER_OP_COL) ? pe.ins[1].arg : -1;
         const bool same_type = fast && C.c[pe.ins[0].arg].dtype == C.c[tgt].dtype &&
                                (bcol < 0 || C.c[bcol].dtype == C.c[tgt].dtype);
@@ -774,10 +1001,28 @@ struct Population {
                                                        pe.ins[1].op == AMBER_OP_CONST, pe.ins[1].value, pe.ins[2].op,
                                                        alive.p, rows, cnt_p);
             check_launch("pop_binop_kernel");
+        } else if (rows && jit && (jk = jit_kernel(jit_update_source(pe, pw, C, tgt)))) {
+            ++n_jit;
+            JitArgs ja{};
+            for (int k = 0; k < C.n; ++k) ja.col[k] = C.c[k].p;
+            ja.ids = ids.p;
+            ja.alive = alive.p;
+            ja.rows = rows;
+            ja.step = static_cast<uint32_t>(step);
+            for (int i = 0; i < 10; ++i) {
+                ja.k0[i] = key.k0[i];
+                ja.k1[i] = key.k1[i];
+            }
+            ja.count = cnt_p;
+            void* kargs[] = {&ja};
+            const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 1024), rt.num_sms * 8)));
+            AMBER_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(jk), dim3(g), dim3(256), kargs, 0, rt.stream));
+            check_launch("amber_jit_update");
         } else if (rows) {
             // the shared stack tile only needs the programs' deepest stack: shallow
             // programs (the common case) run more blocks per SM, so more column
             // loads are in flight (measured: depth 3 -> 64 KB -> 24 KB per block)
+            ++n_interp;
             const size_t smem = stack_bytes(pe, pw);
             pop_update_kernel<<<tiles_grid(smem), kThreads, smem, rt.stream>>>(pe, pw, views(), tgt, ids.p, alive.p, rows,
                                                                      static_cast<uint32_t>(step), key, cnt_p);
@@ -892,6 +1137,12 @@ void destroy_population(Population* p) { delete p; }
 int64_t population_add(Population* p, int64_t n, const double* d) { return p->add(n, d); }
 void population_remove(Population* p, const int64_t* ids, int64_t n) { p->remove(ids, n); }
 void population_compact(Population* p) { p->compact(); }
+void population_update_paths(Population* p, int64_t* jit, int64_t* interp)
+{
+    if (jit) *jit = p->n_jit;
+    if (interp) *interp = p->n_interp;
+}
+
 void population_size(Population* p, int64_t* live, int64_t* rows)
 {
     if (live) *live = p->live;

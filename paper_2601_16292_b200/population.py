@@ -164,6 +164,12 @@ class Population:
                                                C.byref(k) if count else None))
         return k.value if count else None
 
+    def update_paths(self):
+        """(jit, interpreted) general-program update counts (amber_population_update_paths)."""
+        j, i = C.c_int64(), C.c_int64()
+        check(self.lib.amber_population_update_paths(self.h, C.byref(j), C.byref(i)))
+        return j.value, i.value
+
     def synchronize(self):
         check(self.lib.amber_population_synchronize(self.h))
 

@@ -60,8 +60,11 @@ def random_expr(rng, depth=3):
             lambda: a.abs(), lambda: a.floor(), lambda: a / (Expr.of(b).abs() + 1)][op]()
 
 
+@pytest.mark.parametrize("jit", ["1", "0"])
 @pytest.mark.parametrize("seed", range(6))
-def test_random_programs_match_reference(seed):
+def test_random_programs_match_reference(seed, jit, monkeypatch):
+    # jit "1": general programs compiled at run time (NVRTC); "0": the interpreter
+    monkeypatch.setenv("AMBER_POP_JIT", jit)
     rng = np.random.default_rng(seed)
     n = 5000
     p, r = Population(SCHEMA, seed=seed), PopulationRef(SCHEMA, seed=seed)
@@ -101,6 +104,8 @@ def test_random_programs_match_reference(seed):
                 continue
             g = p.aggregate(kind, col("y"), where=col("a") > 0)
             assert g == pytest.approx(h, rel=1e-12, abs=1e-9)
+    nj, ni = p.update_paths()
+    assert (nj > 0 and ni == 0) if jit == "1" else (nj == 0 and ni > 0)
     if seed % 2:
         p.compact()
         r.compact()
