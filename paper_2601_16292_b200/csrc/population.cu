@@ -580,9 +580,8 @@ static std::string jit_emit(const Prog& P, const Cols& C, const std::string& pfx
                 body += "const double " + v + " = " + buf + ";\n";
                 break;
             }
-            case AMBER_OP_COL:
-                body += "const double " + v + " = (double)((const " + jit_ctype(C.c[in.arg].dtype) + "*)a.col[" +
-                        std::to_string(in.arg) + "])[rc];\n";
+            case AMBER_OP_COL:  // component of the column's 4-row vector (loaded once per group)
+                body += "const double " + v + " = (double)c" + std::to_string(in.arg) + "[j];\n";
                 break;
             case AMBER_OP_ID: body += "const double " + v + " = (double)id;\n"; break;
             case AMBER_OP_RAND: body += "const double " + v + " = rnd(K, " + std::to_string(in.arg) + "u, id, a.step);\n"; break;
@@ -625,12 +624,24 @@ static std::string jit_emit(const Prog& P, const Cols& C, const std::string& pfx
     return st.empty() ? std::string("1.0") : st.back();
 }
 
+static void jit_cols(const Prog& P, std::vector<int>& used)
+{
+    for (int k = 0; k < P.n; ++k)
+        if (P.ins[k].op == AMBER_OP_COL && std::find(used.begin(), used.end(), P.ins[k].arg) == used.end())
+            used.push_back(P.ins[k].arg);
+}
+
 static std::string jit_update_source(const Prog& pe, const Prog& pw, const Cols& C, int tgt)
 {
     std::string body;
     const std::string rw = pw.n ? jit_emit(pw, C, "w", body) : std::string("1.0");
     const std::string re = jit_emit(pe, C, "e", body);
     const bool uses_id = pe.uses_id || pw.uses_id;
+    std::vector<int> used;
+    jit_cols(pw, used);
+    jit_cols(pe, used);
+    if (std::find(used.begin(), used.end(), tgt) == used.end()) used.push_back(tgt);  // merged store reads it
+    const std::string tt = jit_ctype(C.c[tgt].dtype);
     std::string s;
     s += "#include \"philox.cuh\"\n";
     s += "struct JitArgs { void* col[" + std::to_string(kMaxCols) +
@@ -640,21 +651,40 @@ static std::string jit_update_source(const Prog& pe, const Prog& pw, const Cols&
          "  const uint4 w = amber::stream_block(K, tag, (unsigned long long)id >> 2, step);\n"
          "  const unsigned q = (unsigned)(id & 3);\n"
          "  return (double)amber::u01(q == 0 ? w.x : (q == 1 ? w.y : (q == 2 ? w.z : w.w)));\n}\n";
+    // 4 consecutive rows per thread: every column of the group is one (or two, for
+    // 8-byte types) 16-byte vector load; capacities are multiples of 4 rows and
+    // allocations 256-byte aligned, so the group never leaves the buffers
+    s += "template <class T> __device__ __forceinline__ void ld4(const void* p, long long r0, T (&v)[4]) {\n"
+         "  if (sizeof(T) == 1) { const uchar4 x = *(const uchar4*)((const T*)p + r0); v[0] = (T)x.x; v[1] = (T)x.y; v[2] = (T)x.z; v[3] = (T)x.w; }\n"
+         "  else if (sizeof(T) == 4) { const uint4 x = *(const uint4*)((const T*)p + r0);\n"
+         "    const unsigned u[4] = {x.x, x.y, x.z, x.w}; for (int j = 0; j < 4; ++j) v[j] = *(const T*)&u[j]; }\n"
+         "  else { const ulonglong2 x = *(const ulonglong2*)((const T*)p + r0), y = *(const ulonglong2*)((const T*)p + r0 + 2);\n"
+         "    const unsigned long long u[4] = {x.x, x.y, y.x, y.y}; for (int j = 0; j < 4; ++j) v[j] = *(const T*)&u[j]; }\n}\n";
+    s += "template <class T> __device__ __forceinline__ void st4(void* p, long long r0, const T (&v)[4]) {\n"
+         "  if (sizeof(T) == 1) { *(uchar4*)((T*)p + r0) = make_uchar4((unsigned char)v[0], (unsigned char)v[1], (unsigned char)v[2], (unsigned char)v[3]); }\n"
+         "  else if (sizeof(T) == 4) { unsigned u[4]; for (int j = 0; j < 4; ++j) u[j] = *(const unsigned*)&v[j];\n"
+         "    *(uint4*)((T*)p + r0) = make_uint4(u[0], u[1], u[2], u[3]); }\n"
+         "  else { unsigned long long u[4]; for (int j = 0; j < 4; ++j) u[j] = *(const unsigned long long*)&v[j];\n"
+         "    *(ulonglong2*)((T*)p + r0) = make_ulonglong2(u[0], u[1]); *(ulonglong2*)((T*)p + r0 + 2) = make_ulonglong2(u[2], u[3]); }\n}\n";
     s += "extern \"C\" __global__ void __launch_bounds__(256) amber_jit_update(const JitArgs a) {\n"
          "  amber::PhiloxKey K;\n  for (int i = 0; i < 10; ++i) { K.k0[i] = a.k0[i]; K.k1[i] = a.k1[i]; }\n"
          "  unsigned long long cnt = 0;\n"
-         "  const long long stride = (long long)gridDim.x * 1024;\n"
-         "  for (long long base = (long long)blockIdx.x * 1024 + threadIdx.x; base < a.rows; base += stride) {\n"
-         "#pragma unroll\n  for (int m = 0; m < 4; ++m) {\n"
-         "    const long long r = base + m * 256;\n"
-         "    const bool valid = r < a.rows;\n"
-         "    const long long rc = valid ? r : 0;\n"
-         "    const bool live = valid && a.alive[rc];\n";
-    if (uses_id) s += "    const long long id = a.ids[rc];\n";
+         "  const long long stride = (long long)gridDim.x * 256;\n"
+         "  for (long long g = (long long)blockIdx.x * 256 + threadIdx.x; 4 * g < a.rows; g += stride) {\n"
+         "    const long long r0 = 4 * g;\n"
+         "    unsigned char al[4]; ld4(a.alive, r0, al);\n";
+    for (int k : used)
+        s += "    " + std::string(jit_ctype(C.c[k].dtype)) + " c" + std::to_string(k) + "[4]; ld4(a.col[" +
+             std::to_string(k) + "], r0, c" + std::to_string(k) + ");\n";
+    if (uses_id) s += "    long long idv[4]; ld4(a.ids, r0, idv);\n";
+    s += "    " + tt + " out[4];\n";
+    s += "#pragma unroll\n    for (int j = 0; j < 4; ++j) {\n";
+    if (uses_id) s += "      const long long id = idv[j];\n";
     s += body;
-    s += "    if (live && (" + rw + ") != 0.0) {\n"
-         "      ((" + std::string(jit_ctype(C.c[tgt].dtype)) + "*)a.col[" + std::to_string(tgt) + "])[r] = (" +
-         jit_ctype(C.c[tgt].dtype) + ")(" + re + ");\n      ++cnt;\n    }\n  }\n  }\n"
+    s += "      const bool sel = r0 + j < a.rows && al[j] && (" + rw + ") != 0.0;\n"
+         "      out[j] = sel ? (" + tt + ")(" + re + ") : c" + std::to_string(tgt) + "[j];\n"
+         "      cnt += sel;\n    }\n"
+         "    st4(a.col[" + std::to_string(tgt) + "], r0, out);\n  }\n"
          "  if (a.count) {\n"
          "    __shared__ unsigned long long red[8];\n"
          "    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);\n"
@@ -779,7 +809,7 @@ struct Population {
     void reserve(int64_t want)
     {
         if (want <= cap) return;
-        const int64_t nc = std::max<int64_t>(want, cap * 2);
+        const int64_t nc = (std::max<int64_t>(want, cap * 2) + 3) & ~3ll;  // JIT kernels move 4 rows per vector
         auto grow = [&](DevBuf<char>& b, size_t esz) {
             DevBuf<char> nb;
             nb.allocate(&rt, nc * esz);
@@ -1015,7 +1045,7 @@ struct Population {
             }
             ja.count = cnt_p;
             void* kargs[] = {&ja};
-            const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 1024), rt.num_sms * 8)));
+            const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 1024), rt.num_sms * 16)));
             AMBER_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(jk), dim3(g), dim3(256), kargs, 0, rt.stream));
             check_launch("amber_jit_update");
         } else if (rows) {
