@@ -508,6 +508,7 @@ struct JitArgs {
     unsigned step;
     unsigned k0[10], k1[10];
     unsigned long long* count;
+    double* partial;
 };
 
 struct NvrtcApi {
@@ -624,6 +625,21 @@ static std::string jit_emit(const Prog& P, const Cols& C, const std::string& pfx
     return st.empty() ? std::string("1.0") : st.back();
 }
 
+static const char* kJitPrelude =
+    "#include \"philox.cuh\"\n"
+    "struct JitArgs { void* col[32]; const long long* ids; const unsigned char* alive; long long rows; unsigned step; "
+    "unsigned k0[10], k1[10]; unsigned long long* count; double* partial; };\n"
+    "__device__ __forceinline__ double rnd(const amber::PhiloxKey& K, unsigned tag, long long id, unsigned step) {\n"
+    "  const uint4 w = amber::stream_block(K, tag, (unsigned long long)id >> 2, step);\n"
+    "  const unsigned q = (unsigned)(id & 3);\n"
+    "  return (double)amber::u01(q == 0 ? w.x : (q == 1 ? w.y : (q == 2 ? w.z : w.w)));\n}\n"
+    "template <class T> __device__ __forceinline__ void ld4(const void* p, long long r0, T (&v)[4]) {\n"
+    "  if (sizeof(T) == 1) { const uchar4 x = *(const uchar4*)((const T*)p + r0); v[0] = (T)x.x; v[1] = (T)x.y; v[2] = (T)x.z; v[3] = (T)x.w; }\n"
+    "  else if (sizeof(T) == 4) { const uint4 x = *(const uint4*)((const T*)p + r0);\n"
+    "    const unsigned u[4] = {x.x, x.y, x.z, x.w}; for (int j = 0; j < 4; ++j) v[j] = *(const T*)&u[j]; }\n"
+    "  else { const ulonglong2 x = *(const ulonglong2*)((const T*)p + r0), y = *(const ulonglong2*)((const T*)p + r0 + 2);\n"
+    "    const unsigned long long u[4] = {x.x, x.y, y.x, y.y}; for (int j = 0; j < 4; ++j) v[j] = *(const T*)&u[j]; }\n}\n";
+
 static void jit_cols(const Prog& P, std::vector<int>& used)
 {
     for (int k = 0; k < P.n; ++k)
@@ -631,8 +647,52 @@ static void jit_cols(const Prog& P, std::vector<int>& used)
             used.push_back(P.ins[k].arg);
 }
 
+static std::string jit_aggregate_source(const Prog& pe, const Prog& pw, const Cols& C)
+{
+    std::string body;
+    const std::string rw = pw.n ? jit_emit(pw, C, "w", body) : std::string("1.0");
+    const std::string re = pe.n ? jit_emit(pe, C, "e", body) : std::string("0.0");
+    const bool uses_id = pe.uses_id || pw.uses_id;
+    std::vector<int> used;
+    jit_cols(pw, used);
+    jit_cols(pe, used);
+    std::string s = kJitPrelude;
+    s += "extern \"C\" __global__ void __launch_bounds__(256) amber_jit_aggregate(const JitArgs a) {\n"
+         "  amber::PhiloxKey K;\n  for (int i = 0; i < 10; ++i) { K.k0[i] = a.k0[i]; K.k1[i] = a.k1[i]; }\n"
+         "  double S = 0.0, MN = __longlong_as_double(0x7ff0000000000000LL), MX = -MN, CC = 0.0;\n"
+         "  const long long stride = (long long)gridDim.x * 256;\n"
+         "  for (long long g = (long long)blockIdx.x * 256 + threadIdx.x; 4 * g < a.rows; g += stride) {\n"
+         "    const long long r0 = 4 * g;\n"
+         "    unsigned char al[4]; ld4(a.alive, r0, al);\n";
+    for (int k : used)
+        s += "    " + std::string(jit_ctype(C.c[k].dtype)) + " c" + std::to_string(k) + "[4]; ld4(a.col[" +
+             std::to_string(k) + "], r0, c" + std::to_string(k) + ");\n";
+    if (uses_id) s += "    long long idv[4]; ld4(a.ids, r0, idv);\n";
+    s += "#pragma unroll\n    for (int j = 0; j < 4; ++j) {\n";
+    if (uses_id) s += "      const long long id = idv[j];\n";
+    s += body;
+    s += "      if (r0 + j < a.rows && al[j] && (" + rw + ") != 0.0) {\n"
+         "        const double v = " + re + ";\n"
+         "        S += v; MN = fmin(MN, v); MX = fmax(MX, v); CC += 1.0;\n      }\n    }\n  }\n"
+         "  __shared__ double red[4][8];\n"
+         "  for (int o = 16; o > 0; o >>= 1) { S += __shfl_xor_sync(0xffffffffu, S, o);\n"
+         "    MN = fmin(MN, __shfl_xor_sync(0xffffffffu, MN, o)); MX = fmax(MX, __shfl_xor_sync(0xffffffffu, MX, o));\n"
+         "    CC += __shfl_xor_sync(0xffffffffu, CC, o); }\n"
+         "  const int w = threadIdx.x >> 5;\n"
+         "  if ((threadIdx.x & 31) == 0) { red[0][w] = S; red[1][w] = MN; red[2][w] = MX; red[3][w] = CC; }\n"
+         "  __syncthreads();\n"
+         "  if (threadIdx.x == 0) { double s0 = 0.0, s1 = red[1][0], s2 = red[2][0], s3 = 0.0;\n"
+         "    for (int k = 0; k < 8; ++k) { s0 += red[0][k]; s1 = fmin(s1, red[1][k]); s2 = fmax(s2, red[2][k]); s3 += red[3][k]; }\n"
+         "    a.partial[4 * blockIdx.x] = s0; a.partial[4 * blockIdx.x + 1] = s1; a.partial[4 * blockIdx.x + 2] = s2;\n"
+         "    a.partial[4 * blockIdx.x + 3] = s3; }\n}\n";
+    return s;
+}
+
+// tgt >= 0: update kernel (merged vector store of the target column);
+// tgt < 0: aggregate kernel (per-block sum / min / max / count partials).
 static std::string jit_update_source(const Prog& pe, const Prog& pw, const Cols& C, int tgt)
 {
+    if (tgt < 0) return jit_aggregate_source(pe, pw, C);
     std::string body;
     const std::string rw = pw.n ? jit_emit(pw, C, "w", body) : std::string("1.0");
     const std::string re = jit_emit(pe, C, "e", body);
@@ -642,24 +702,7 @@ static std::string jit_update_source(const Prog& pe, const Prog& pw, const Cols&
     jit_cols(pe, used);
     if (std::find(used.begin(), used.end(), tgt) == used.end()) used.push_back(tgt);  // merged store reads it
     const std::string tt = jit_ctype(C.c[tgt].dtype);
-    std::string s;
-    s += "#include \"philox.cuh\"\n";
-    s += "struct JitArgs { void* col[" + std::to_string(kMaxCols) +
-         "]; const long long* ids; const unsigned char* alive; long long rows; unsigned step; unsigned k0[10], k1[10]; "
-         "unsigned long long* count; };\n";
-    s += "__device__ __forceinline__ double rnd(const amber::PhiloxKey& K, unsigned tag, long long id, unsigned step) {\n"
-         "  const uint4 w = amber::stream_block(K, tag, (unsigned long long)id >> 2, step);\n"
-         "  const unsigned q = (unsigned)(id & 3);\n"
-         "  return (double)amber::u01(q == 0 ? w.x : (q == 1 ? w.y : (q == 2 ? w.z : w.w)));\n}\n";
-    // 4 consecutive rows per thread: every column of the group is one (or two, for
-    // 8-byte types) 16-byte vector load; capacities are multiples of 4 rows and
-    // allocations 256-byte aligned, so the group never leaves the buffers
-    s += "template <class T> __device__ __forceinline__ void ld4(const void* p, long long r0, T (&v)[4]) {\n"
-         "  if (sizeof(T) == 1) { const uchar4 x = *(const uchar4*)((const T*)p + r0); v[0] = (T)x.x; v[1] = (T)x.y; v[2] = (T)x.z; v[3] = (T)x.w; }\n"
-         "  else if (sizeof(T) == 4) { const uint4 x = *(const uint4*)((const T*)p + r0);\n"
-         "    const unsigned u[4] = {x.x, x.y, x.z, x.w}; for (int j = 0; j < 4; ++j) v[j] = *(const T*)&u[j]; }\n"
-         "  else { const ulonglong2 x = *(const ulonglong2*)((const T*)p + r0), y = *(const ulonglong2*)((const T*)p + r0 + 2);\n"
-         "    const unsigned long long u[4] = {x.x, x.y, y.x, y.y}; for (int j = 0; j < 4; ++j) v[j] = *(const T*)&u[j]; }\n}\n";
+    std::string s = kJitPrelude;
     s += "template <class T> __device__ __forceinline__ void st4(void* p, long long r0, const T (&v)[4]) {\n"
          "  if (sizeof(T) == 1) { *(uchar4*)((T*)p + r0) = make_uchar4((unsigned char)v[0], (unsigned char)v[1], (unsigned char)v[2], (unsigned char)v[3]); }\n"
          "  else if (sizeof(T) == 4) { unsigned u[4]; for (int j = 0; j < 4; ++j) u[j] = *(const unsigned*)&v[j];\n"
@@ -708,7 +751,7 @@ static JitCache& jit_cache()
 }
 
 // Compiled kernel for this source, or nullptr (no NVRTC / compile error: interpret instead).
-static cudaKernel_t jit_kernel(const std::string& src)
+static cudaKernel_t jit_kernel(const std::string& src, const char* name = "amber_jit_update")
 {
     NvrtcApi& api = nvrtc();
     if (!api.ok) return nullptr;
@@ -729,7 +772,7 @@ static cudaKernel_t jit_kernel(const std::string& src)
             api.cubin(prog, cubin.data());
             cudaLibrary_t lib = nullptr;
             if (cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) == cudaSuccess &&
-                cudaLibraryGetKernel(&kern, lib, "amber_jit_update") == cudaSuccess) {
+                cudaLibraryGetKernel(&kern, lib, name) == cudaSuccess) {
                 jc.libs.push_back(lib);
             } else {
                 cudaGetLastError();
@@ -1074,7 +1117,28 @@ struct Population {
         DevBuf<double> part;
         part.allocate(&rt, 4 * g);
         std::vector<double> h(4 * g, 0.0);
-        if (rows) {
+        cudaKernel_t jk = nullptr;
+        const Cols C = views();
+        if (rows && jit && (jk = jit_kernel(jit_update_source(pe, pw, C, -1), "amber_jit_aggregate"))) {
+            ++n_jit;
+            JitArgs ja{};
+            for (int k = 0; k < C.n; ++k) ja.col[k] = C.c[k].p;
+            ja.ids = ids.p;
+            ja.alive = alive.p;
+            ja.rows = rows;
+            ja.step = static_cast<uint32_t>(step);
+            for (int i = 0; i < 10; ++i) {
+                ja.k0[i] = key.k0[i];
+                ja.k1[i] = key.k1[i];
+            }
+            ja.partial = part.p;
+            void* kargs[] = {&ja};
+            AMBER_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(jk), dim3(g), dim3(256), kargs, 0, rt.stream));
+            check_launch("amber_jit_aggregate");
+            AMBER_CUDA(cudaMemcpyAsync(h.data(), part.p, h.size() * 8, cudaMemcpyDeviceToHost, rt.stream));
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        } else if (rows) {
+            ++n_interp;
             pop_aggregate_kernel<<<g, kThreads, smem, rt.stream>>>(pe, pw, views(), ids.p, alive.p, rows,
                                                            static_cast<uint32_t>(step), key, part.p);
             check_launch("pop_aggregate_kernel");
