@@ -33,8 +33,9 @@ void build_init_state(Runtime& rt, const std::vector<unsigned long long>& seeds,
 // col -> bitmap chain at large N).  test(j, e, owner) returns true for an arc
 // that sets the owner's bit; owners whose bit is set skip their remaining arcs
 // (early exit).  Returns the mask of owners with a set bit.  All 32 lanes call it.
-template <int kU, class C, class T>
-__device__ __forceinline__ uint32_t walk_rows(C&& col_at, uint32_t own, int32_t rb, int32_t re, T&& test)
+template <int kU, bool kPay, class C, class T>
+__device__ __forceinline__ uint32_t walk_rows_core(C&& col_at, uint32_t own, int32_t rb, int32_t re, uint32_t pay,
+                                                   T&& test)
 {
     const int lane = threadIdx.x & 31;
     const int32_t len = ((own >> lane) & 1u) ? re - rb : 0;
@@ -50,9 +51,15 @@ __device__ __forceinline__ uint32_t walk_rows(C&& col_at, uint32_t own, int32_t 
     for (int32_t q0 = 0; q0 < total; q0 += 32 * kU) {
         int Ls[kU];
         int32_t es[kU];
+        uint32_t ps[kU];
         bool live[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
+            live[u] = false;
+            Ls[u] = 0;
+            es[u] = 0;
+            ps[u] = 0;
+            if (q0 + 32 * u >= total) continue;  // warp-uniform: no dead batches
             const int32_t q = q0 + 32 * u + lane;
             int L = 0;  // number of lanes with incl <= q = the owner of position q
 #pragma unroll
@@ -63,6 +70,7 @@ __device__ __forceinline__ uint32_t walk_rows(C&& col_at, uint32_t own, int32_t 
             L &= 31;
             Ls[u] = L;
             es[u] = __shfl_sync(0xffffffffu, start, L) + q;
+            if constexpr (kPay) ps[u] = __shfl_sync(0xffffffffu, pay, L);
             live[u] = q < total && !((hit >> L) & 1u);
         }
         uint32_t js[kU];
@@ -70,12 +78,32 @@ __device__ __forceinline__ uint32_t walk_rows(C&& col_at, uint32_t own, int32_t 
         for (int u = 0; u < kU; ++u) js[u] = live[u] ? col_at(es[u]) : 0u;
         uint32_t add = 0;
 #pragma unroll
-        for (int u = 0; u < kU; ++u)
-            if (live[u] && test(js[u], es[u], Ls[u])) add |= 1u << Ls[u];
+        for (int u = 0; u < kU; ++u) {
+            bool h = false;
+            if constexpr (kPay) h = live[u] && test(js[u], es[u], Ls[u], ps[u]);
+            else h = live[u] && test(js[u], es[u], Ls[u]);
+            if (h) add |= 1u << Ls[u];
+        }
         hit |= __reduce_or_sync(0xffffffffu, add);
         if ((hit & own) == own) break;  // every owner decided
     }
     return hit;
+}
+
+template <int kU, class C, class T>
+__device__ __forceinline__ uint32_t walk_rows(C&& col_at, uint32_t own, int32_t rb, int32_t re, T&& test)
+{
+    return walk_rows_core<kU, false>(col_at, own, rb, re, 0u, test);
+}
+
+// walk_rows with a per-owner payload: test(j, e, owner, pay_of_owner).  Used
+// when the owner lanes were compacted from several warp chunks (the owner's
+// agent id is no longer chunk base + lane).
+template <int kU, class C, class T>
+__device__ __forceinline__ uint32_t walk_rows_pay(C&& col_at, uint32_t own, int32_t rb, int32_t re, uint32_t pay,
+                                                  T&& test)
+{
+    return walk_rows_core<kU, true>(col_at, own, rb, re, pay, test);
 }
 
 }  // namespace amber

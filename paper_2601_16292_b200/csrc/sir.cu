@@ -276,6 +276,7 @@ struct SirStepArgs {
     int digest;
     uint32_t* queue;         // persistent launch: [2 parities][2 phases][kRegions] chunk counters
     int grab;                // chunks per queue grab
+    int dir;                 // 0: direction-optimizing; 1: pull only; 2: push whenever possible (tests, probes)
 };
 
 constexpr int kRegions = 16;
@@ -283,23 +284,42 @@ constexpr int kRegions = 16;
 #define AMBER_SIR_WALK_U 4
 #endif
 constexpr int kWalkU = AMBER_SIR_WALK_U;  // 32-arc batches in flight per warp (walk_rows)
+#ifndef AMBER_SIR_PT
+#define AMBER_SIR_PT 256
+#endif
+constexpr int kSirPT = AMBER_SIR_PT;  // threads per block of the persistent kernel
 
-// Warp chunks (32 agents each) of the padded population.  Persistent launch
-// (queue != nullptr): dynamic -- the chunk range is split into kRegions
-// contiguous regions, warp w draws batches of `grab` chunks from region
-// w % kRegions with one atomic (per-region counters, so the atomics spread);
-// the pull and push walks cost very different amounts per chunk, and static
-// striding left most warps waiting at the step barrier (r01 ncu: 43% of stall
-// samples).  Per-step launch: one chunk per warp, the block scheduler balances.
+// Warp chunks of kChunk = 128 agents: lane L holds agents 4L..4L+3 of the
+// chunk (one 32-bit load of the state bytes, one Philox block for the four
+// recovery draws, R4).  The state buffers and bitmaps are allocated to a
+// multiple of 128 agents (padding = kPad).  Persistent launch (queue !=
+// nullptr): dynamic -- the chunk range is split into kRegions contiguous
+// regions, warp w draws batches of `grab` chunks from region w % kRegions with
+// one atomic (per-region counters, so the atomics spread); the pull and push
+// walks cost very different amounts per chunk, and static striding left most
+// warps waiting at the step barrier (r01 ncu: 43% of stall samples).  Per-step
+// launch: one chunk per warp, the block scheduler balances.
+constexpr int kChunk = 128;
+constexpr int kQCap = 160;  // owner queue per warp: < 32 carried + 128 of one chunk
+
+struct SirSmem {
+    int32_t id[kSirPT / 32][kQCap];  // owner: agent offset (pull: in the chunk; push: local agent id)
+    int32_t rb[kSirPT / 32][kQCap];  // owner's row [rb, re)
+    int32_t re[kSirPT / 32][kQCap];
+    uint32_t h[kSirPT / 32][4];      // pull: infected bits of the chunk's 128 agents
+};
+
+__host__ __device__ constexpr int64_t sir_chunks(int64_t n_pad) { return (n_pad + kChunk - 1) / kChunk; }
+
 template <class F>
 __device__ __forceinline__ void for_chunks(const SirStepArgs& a, uint32_t* q, F&& f)
 {
     const int lane = threadIdx.x & 31;
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    const int64_t nchunks = a.n_pad >> 5;
+    const int64_t nchunks = sir_chunks(a.n_pad);
     if (!q || nw < kRegions) {
-        for (int64_t c = gw; c < nchunks; c += nw) f(c << 5);
+        for (int64_t c = gw; c < nchunks; c += nw) f(c * kChunk);
         return;
     }
     const int r = static_cast<int>(gw % kRegions);
@@ -310,7 +330,7 @@ __device__ __forceinline__ void for_chunks(const SirStepArgs& a, uint32_t* q, F&
         c0 = __shfl_sync(0xffffffffu, c0, 0);
         if (lo + c0 >= hi) break;
         const int64_t e = lo + c0 + a.grab < hi ? lo + c0 + a.grab : hi;
-        for (int64_t c = lo + c0; c < e; ++c) f(c << 5);
+        for (int64_t c = lo + c0; c < e; ++c) f(c * kChunk);
     }
 }
 
@@ -333,75 +353,161 @@ __device__ __forceinline__ bool bit_of(const uint32_t* bits, uint32_t j)
     return (w >> (j & 31u)) & 1u;
 }
 
-__device__ __forceinline__ bool recovers(const SirStepArgs& a, int64_t i, uint32_t t)
+// Recovery draws of the lane's four agents i0..i0+3 (i0 = global id, multiple
+// of 4): one Philox block, lane k of block i0/4 (R4).  Bit k set iff agent
+// i0 + k is in `inf` and recovers.
+__device__ __forceinline__ uint32_t recover_nib(const SirStepArgs& a, unsigned long long i0, uint32_t t, uint32_t inf)
 {
-    const uint4 rec = stream_block(a.key, TAG_SIR_REC, static_cast<unsigned long long>(i >> 2), t);  // R4
-    const uint32_t k = static_cast<uint32_t>(i & 3);
-    const uint32_t d = k == 0 ? rec.x : (k == 1 ? rec.y : (k == 2 ? rec.z : rec.w));
-    return static_cast<unsigned long long>(d) < a.t_gamma;
+    if (!inf) return 0u;
+    const uint4 r = stream_block(a.key, TAG_SIR_REC, i0 >> 2, t);
+    return ((inf & 1u) && r.x < a.t_gamma ? 1u : 0u) | ((inf & 2u) && r.y < a.t_gamma ? 2u : 0u) |
+           ((inf & 4u) && r.z < a.t_gamma ? 4u : 0u) | ((inf & 8u) && r.w < a.t_gamma ? 8u : 0u);
 }
 
-// Pull step for the 32 agents of warp chunk a0 (lane = agent): susceptible
-// owners walk their rows; an arc transmits iff the neighbour is I (bitmap,
-// L2-resident) and the pair-keyed Bernoulli (S3) fires.  Writes the next state
-// and the next bitmaps; returns the new state of the lane's agent.
-__device__ __forceinline__ uint8_t sir_pull_chunk(const SirStepArgs& a, int64_t a0, const uint8_t* __restrict__ x,
-                                                  uint8_t* __restrict__ y, const uint32_t* __restrict__ ib,
-                                                  uint32_t* __restrict__ ib_next, uint32_t* __restrict__ sb_next,
-                                                  uint32_t t)
+// Exclusive warp prefix sum; *total = the warp's sum.
+__device__ __forceinline__ uint32_t warp_excl(uint32_t v, uint32_t* total)
 {
     const int lane = threadIdx.x & 31;
-    const int64_t i = a0 + lane;
-    const bool real = i < a.n;
-    const uint8_t st = x[i];
-    const bool is_s = st == kS;
-    const uint32_t s_mask = __ballot_sync(0xffffffffu, is_s);
-    uint32_t hit = 0;
-    if (s_mask) {
-        const int32_t rb = real ? a.row_ptr[i] : 0, re = real ? a.row_ptr[i + 1] : 0;
-        hit = walk_rows<kWalkU>([&](int32_t e) { return static_cast<uint32_t>(__ldcs(a.col + e)); }, s_mask, rb, re,
-                           [&](uint32_t j, int32_t, int L) {
-            if (!bit_of(ib, j)) return false;  // j is a global id (the bitmap is global)
-            const uint32_t s = static_cast<uint32_t>(a.gid0 + a0 + L);
-            const uint4 w = philox(make_uint4(min(s, j), max(s, j), t, TAG_SIR_TX), a.key);
-            return static_cast<unsigned long long>(w.x) < a.t_beta;
-        });
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
     }
-    uint8_t o = st;
-    if (is_s) {
-        if ((hit >> lane) & 1u) o = kI;
-    } else if (st == kI) {
-        if (recovers(a, static_cast<int64_t>(a.gid0) + i, t)) o = kR;
-    }
-    y[i] = o;
-    const uint32_t ibw = __ballot_sync(0xffffffffu, o == kI), sbw = __ballot_sync(0xffffffffu, o == kS);
-    if (lane == 0) {
-        ib_next[a0 >> 5] = ibw;
-        sb_next[a0 >> 5] = sbw;
-    }
-    return o;
+    *total = __shfl_sync(0xffffffffu, incl, 31);
+    return incl - v;
 }
 
-__device__ __forceinline__ void sir_pull_body(const SirStepArgs& a, int c, uint32_t t, unsigned long long (&cnt)[4])
+// Bitmap word m of a 128-agent chunk from the lanes' 4-bit nibbles: lanes
+// 8m..8m+7 hold agents 32m..32m+31; every lane of the group gets the word.
+__device__ __forceinline__ uint32_t word_of(uint32_t nib)
 {
-    const int lane = threadIdx.x & 31;
-    for_chunks(a, queue_of(a, t, 0), [&](int64_t a0) {
-        const uint8_t o = sir_pull_chunk(a, a0, a.x[c], a.x[c ^ 1], a.ib[c], a.ib[c ^ 1], a.sb[c ^ 1], t);
-        const int64_t i = a0 + lane;
-        if (i < a.n) {
-            cnt[0] += o == kS;
-            cnt[1] += o == kI;
-            cnt[2] += o == kR;
-            if (a.digest) cnt[3] += digest_term(a.gid0 + static_cast<unsigned long long>(i), o);
+    uint32_t v = nib << ((threadIdx.x & 7) * 4);
+    v |= __shfl_xor_sync(0xffffffffu, v, 1);
+    v |= __shfl_xor_sync(0xffffffffu, v, 2);
+    v |= __shfl_xor_sync(0xffffffffu, v, 4);
+    return v;
+}
+
+// Appends the lane's agents in `nib` (local ids i0 + k, or chunk offsets when
+// `chunk_off`) with their CSR rows to the warp's owner queue at qn + rank;
+// returns the number appended by the warp.
+__device__ __forceinline__ uint32_t queue_owners(const SirStepArgs& a, SirSmem& sm, uint32_t qn, int64_t i0,
+                                                 uint32_t nib, int32_t id_base)
+{
+    const int wq = threadIdx.x >> 5;
+    uint32_t T;
+    uint32_t k = qn + warp_excl(__popc(nib), &T);
+    if (nib) {
+        int32_t r[5];
+        if (i0 + 4 <= a.n) {
+            const int4 v = *reinterpret_cast<const int4*>(a.row_ptr + i0);
+            r[0] = v.x;
+            r[1] = v.y;
+            r[2] = v.z;
+            r[3] = v.w;
+            r[4] = a.row_ptr[i0 + 4];
+        } else {
+#pragma unroll
+            for (int q = 0; q < 5; ++q) r[q] = i0 + q <= a.n ? a.row_ptr[i0 + q] : 0;
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if ((nib >> q) & 1u) {
+                sm.id[wq][k] = id_base + q;
+                sm.rb[wq][k] = r[q];
+                sm.re[wq][k] = r[q + 1];
+                ++k;
+            }
+    }
+    return T;
+}
+
+// Pull step for the 128 agents of chunk a0: the susceptible agents, compacted
+// into groups of 32 owners, walk their rows warp-cooperatively; an arc
+// transmits iff the neighbour is I (bitmap, L2-resident) and the pair-keyed
+// Bernoulli (S3) fires.  Writes the next state and the next bitmap words and
+// adds the S/I/R counts (and digest terms) of the new states to cnt.
+__device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0, const uint8_t* __restrict__ x,
+                                               uint8_t* __restrict__ y, const uint32_t* __restrict__ ib,
+                                               uint32_t* __restrict__ ib_next, uint32_t* __restrict__ sb_next,
+                                               uint32_t t, SirSmem& sm, unsigned long long (&cnt)[4])
+{
+    const int lane = threadIdx.x & 31;
+    const int wq = threadIdx.x >> 5;
+    const int64_t i0 = a0 + 4 * lane;
+    const uint32_t xw = *reinterpret_cast<const uint32_t*>(x + i0);
+    uint32_t nib_s = 0, nib_i = 0, nib_r = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t st = (xw >> (8 * k)) & 0xffu;
+        nib_s |= (st == kS ? 1u : 0u) << k;
+        nib_i |= (st == kI ? 1u : 0u) << k;
+        nib_r |= (st == kR ? 1u : 0u) << k;
+    }
+    uint32_t hitnib = 0;
+    if (__any_sync(0xffffffffu, nib_s != 0)) {
+        if (lane < 4) sm.h[wq][lane] = 0u;
+        const uint32_t T = queue_owners(a, sm, 0, i0, nib_s, 4 * lane);
+        __syncwarp();
+        for (uint32_t g0 = 0; g0 < T; g0 += 32) {
+            const uint32_t nown = T - g0 < 32 ? T - g0 : 32;
+            const bool mine = static_cast<uint32_t>(lane) < nown;
+            const int32_t lid = mine ? sm.id[wq][g0 + lane] : 0;
+            const int32_t rb = mine ? sm.rb[wq][g0 + lane] : 0, re = mine ? sm.re[wq][g0 + lane] : 0;
+            const uint32_t own = nown >= 32 ? 0xffffffffu : ((1u << nown) - 1u);
+            const uint32_t sid = static_cast<uint32_t>(a.gid0 + static_cast<unsigned long long>(a0 + lid));
+            const uint32_t hit = walk_rows_pay<kWalkU>(
+                [&](int32_t e) { return static_cast<uint32_t>(__ldcs(a.col + e)); }, own, rb, re, sid,
+                [&](uint32_t j, int32_t, int, uint32_t s) {
+                    if (!bit_of(ib, j)) return false;  // j is a global id (the bitmap is global)
+                    const uint4 w = philox(make_uint4(min(s, j), max(s, j), t, TAG_SIR_TX), a.key);
+                    return static_cast<unsigned long long>(w.x) < a.t_beta;
+                });
+            if ((hit >> lane) & 1u) atomicOr(&sm.h[wq][lid >> 5], 1u << (lid & 31));
+        }
+        __syncwarp();
+        hitnib = (sm.h[wq][lane >> 3] >> ((lane & 7) * 4)) & 0xfu;
+        __syncwarp();  // the next chunk rewrites the queue and h
+    }
+    const uint32_t recnib = recover_nib(a, a.gid0 + static_cast<unsigned long long>(i0), t, nib_i);
+    const uint32_t s2 = nib_s & ~hitnib, i2 = (nib_s & hitnib) | (nib_i & ~recnib), r2 = nib_r | recnib;
+    uint32_t yw = xw;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (((nib_s & hitnib) | recnib) >> k & 1u)
+            yw = (yw & ~(0xffu << (8 * k))) | (static_cast<uint32_t>((i2 >> k) & 1u ? kI : kR) << (8 * k));
+    *reinterpret_cast<uint32_t*>(y + i0) = yw;
+    const uint32_t wi = word_of(i2), ws = word_of(s2);
+    if ((lane & 7) == 0) {
+        ib_next[(a0 >> 5) + (lane >> 3)] = wi;
+        sb_next[(a0 >> 5) + (lane >> 3)] = ws;
+    }
+    // pads (kPad) are in none of the nibbles
+    cnt[0] += __popc(s2);
+    cnt[1] += __popc(i2);
+    cnt[2] += __popc(r2);
+    if (a.digest) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (i0 + k < a.n) cnt[3] += digest_term(a.gid0 + static_cast<unsigned long long>(i0 + k), (yw >> (8 * k)) & 0xffu);
+    }
+}
+
+__device__ __forceinline__ void sir_pull_body(const SirStepArgs& a, int c, uint32_t t, SirSmem& sm,
+                                              unsigned long long (&cnt)[4])
+{
+    for_chunks(a, queue_of(a, t, 0), [&](int64_t a0) {
+        sir_pull_chunk(a, a0, a.x[c], a.x[c ^ 1], a.ib[c], a.ib[c ^ 1], a.sb[c ^ 1], t, sm, cnt);
     });
 }
 
 __global__ void __launch_bounds__(256) sir_step_kernel(const SirStepArgs a)
 {
+    __shared__ SirSmem sm;
     const uint32_t t = a.t0;
     unsigned long long cnt[4] = {0, 0, 0, 0};
-    sir_pull_body(a, a.cur, t, cnt);
+    sir_pull_body(a, a.cur, t, sm, cnt);
     SirSlot* sl = a.ring + (t % a.ring_cap);
     unsigned long long* const outs[4] = {&sl->S, &sl->I, &sl->R, a.digest ? &sl->digest : nullptr};
     block_sum_atomic<4>(cnt, outs);
@@ -429,59 +535,38 @@ __global__ void sir_bits_kernel(const uint8_t* __restrict__ x, int64_t n_pad, ui
 // reached by S -> I -> R moves only (the previous step's input; a copy of the
 // current state after creation or a column write), so every agent that is S
 // now is S in B.  One pass, no copy:
-//  * owners of non-S agents write their new state into y (bytes of B) as an
-//    atomic delta on the byte's word, and XOR-correct their bits of the next
-//    I bitmap (B's bits -> survivors) and clear their S bits -- all on bits
-//    and bytes no pusher touches (pushers only touch agents that are S now);
+//  * owners of non-S agents write their new states into y (bytes of B) as one
+//    atomic delta on the lane's word, and XOR-correct their bits of the next I
+//    bitmap (B's bits -> survivors) and clear their S bits -- all on bits and
+//    bytes no pusher touches (pushers only touch agents that are S now);
 //  * every agent infected now pushes along its row to neighbours that are S
 //    now (S bitmap) with the same pair-keyed draw as pull (S3); a transmitting
 //    arc sets the neighbour's next I bit with atomicOr, whose old word makes
 //    the new-infection count exact when several pushers hit the same agent;
 //    the first one also clears its S bit and sets its byte to I.
-__device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint32_t t, long long& rec, long long& inf,
-                                              unsigned long long& dig)
+// Pushers are compacted across chunks into the warp's owner queue and walked
+// 32 owners at a time, so the concatenated rows fill the walk's 32-arc batches
+// even when few agents are infected.
+__device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint32_t t, SirSmem& sm, long long& rec,
+                                              long long& inf, unsigned long long& dig)
 {
     const int lane = threadIdx.x & 31;
+    const int wq = threadIdx.x >> 5;
     const uint8_t* __restrict__ x = a.x[c];
     const uint32_t* __restrict__ sb = a.sb[c];
     uint32_t* ib_next = a.ib[c ^ 1];
     uint32_t* sb_next = a.sb[c ^ 1];
     uint8_t* y = a.x[c ^ 1];
     uint32_t* yw = reinterpret_cast<uint32_t*>(y);
-    for_chunks(a, queue_of(a, t, 1), [&](int64_t a0) {
-        const int64_t i = a0 + lane;
-        const int64_t w = a0 >> 5;
-        const uint8_t st = x[i];
-        const bool real = i < a.n;
-        const uint32_t non_s = __ballot_sync(0xffffffffu, real && st != kS);
-        if (a.digest && real && st == kS) dig += digest_term(static_cast<unsigned long long>(i), kS);
-        if (!non_s) return;
-        const bool is_i = st == kI;
-        const uint32_t own = __ballot_sync(0xffffffffu, is_i);
-        // owners: recoveries and the new state of every non-S agent
-        uint8_t nw = st;
-        if (is_i && recovers(a, i, t)) {
-            nw = kR;
-            ++rec;
-        }
-        if ((non_s >> lane) & 1u) {
-            const uint8_t old = y[i];
-            if (nw != old) atomicAdd(yw + (i >> 2), static_cast<uint32_t>(nw - old) << ((i & 3) * 8));
-            if (a.digest) dig += digest_term(static_cast<unsigned long long>(i), nw);
-        }
-        const uint32_t surv = __ballot_sync(0xffffffffu, nw == kI);
-        if (lane == 0) {
-            const uint32_t flip = (ib_next[w] ^ surv) & non_s;
-            if (flip) atomicXor(ib_next + w, flip);
-            if (sb_next[w] & non_s) atomicAnd(sb_next + w, ~non_s);
-        }
-        // pushers
-        if (!own) return;
-        const int32_t rb = is_i ? a.row_ptr[i] : 0, re = is_i ? a.row_ptr[i + 1] : 0;
-        walk_rows<kWalkU>([&](int32_t e) { return static_cast<uint32_t>(__ldcs(a.col + e)); }, own, rb, re,
-                     [&](uint32_t j, int32_t, int L) {
+    uint32_t qn = 0;  // queued pushers (warp-uniform; < 32 between chunks)
+    auto walk = [&](uint32_t g0, uint32_t nown) {
+        const bool mine = static_cast<uint32_t>(lane) < nown;
+        const int32_t rb = mine ? sm.rb[wq][g0 + lane] : 0, re = mine ? sm.re[wq][g0 + lane] : 0;
+        const uint32_t id = mine ? static_cast<uint32_t>(sm.id[wq][g0 + lane]) : 0u;
+        const uint32_t own = nown >= 32 ? 0xffffffffu : ((1u << nown) - 1u);
+        walk_rows_pay<kWalkU>([&](int32_t e) { return static_cast<uint32_t>(__ldcs(a.col + e)); }, own, rb, re, id,
+                              [&](uint32_t j, int32_t, int, uint32_t s) {
             if (!bit_of(sb, j)) return false;
-            const uint32_t s = static_cast<uint32_t>(a0 + L);
             const uint4 wd = philox(make_uint4(min(s, j), max(s, j), t, TAG_SIR_TX), a.key);
             if (static_cast<unsigned long long>(wd.x) < a.t_beta) {
                 const uint32_t bit = 1u << (j & 31u);
@@ -495,7 +580,70 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
             }
             return false;  // an infected agent tries every susceptible neighbour
         });
+    };
+    for_chunks(a, queue_of(a, t, 1), [&](int64_t a0) {
+        const int64_t i0 = a0 + 4 * lane;
+        const uint32_t xw = *reinterpret_cast<const uint32_t*>(x + i0);
+        uint32_t nib_s = 0, nib_i = 0, nons = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t st = (xw >> (8 * k)) & 0xffu;
+            nib_s |= (st == kS ? 1u : 0u) << k;
+            nib_i |= (st == kI ? 1u : 0u) << k;
+            nons |= (st == kI || st == kR ? 1u : 0u) << k;  // pads are neither
+        }
+        if (a.digest && nib_s) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if ((nib_s >> k) & 1u) dig += digest_term(static_cast<unsigned long long>(i0 + k), kS);
+        }
+        if (!__any_sync(0xffffffffu, nons != 0)) return;
+        // owners: recoveries and the new state of every non-S agent
+        const uint32_t recnib = recover_nib(a, static_cast<unsigned long long>(i0), t, nib_i);
+        rec += __popc(recnib);
+        if (nons) {
+            const uint32_t yold = yw[i0 >> 2];
+            uint32_t delta = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if ((nons >> k) & 1u) {
+                    const uint32_t nw = (recnib >> k) & 1u ? kR : (xw >> (8 * k)) & 0xffu;
+                    delta += (nw - ((yold >> (8 * k)) & 0xffu)) << (8 * k);  // mod 2^32: bytes stay in 0..3
+                    if (a.digest) dig += digest_term(static_cast<unsigned long long>(i0 + k), nw);
+                }
+            if (delta) atomicAdd(yw + (i0 >> 2), delta);
+        }
+        const uint32_t wsurv = word_of(nib_i & ~recnib), wnons = word_of(nons);
+        if ((lane & 7) == 0 && wnons) {
+            const int64_t w = (a0 >> 5) + (lane >> 3);
+            const uint32_t flip = (ib_next[w] ^ wsurv) & wnons;
+            if (flip) atomicXor(ib_next + w, flip);
+            if (sb_next[w] & wnons) atomicAnd(sb_next + w, ~wnons);
+        }
+        // pushers: queue, walk whenever 32 are queued
+        if (!__any_sync(0xffffffffu, nib_i != 0)) return;
+        qn += queue_owners(a, sm, qn, i0, nib_i, static_cast<int32_t>(i0));
+        __syncwarp();
+        if (qn < 32) return;
+        uint32_t g0 = 0;
+        for (; qn - g0 >= 32; g0 += 32) walk(g0, 32);
+        const uint32_t rem = qn - g0;
+        int32_t vi = 0, vb = 0, ve = 0;
+        if (static_cast<uint32_t>(lane) < rem) {
+            vi = sm.id[wq][g0 + lane];
+            vb = sm.rb[wq][g0 + lane];
+            ve = sm.re[wq][g0 + lane];
+        }
+        __syncwarp();
+        if (static_cast<uint32_t>(lane) < rem) {
+            sm.id[wq][lane] = vi;
+            sm.rb[wq][lane] = vb;
+            sm.re[wq][lane] = ve;
+        }
+        __syncwarp();
+        qn = rem;
     });
+    if (qn) walk(0, qn);
 }
 
 // All n_steps steps in one cooperative launch (grid barrier between steps).
@@ -503,12 +651,9 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
 // fewer than the susceptible ones (counts of the previous step from its ring
 // slot, so every block takes the same decision), otherwise it pulls.  Both
 // directions give identical results (S3); the tests check it.
-#ifndef AMBER_SIR_PT
-#define AMBER_SIR_PT 256
-#endif
-constexpr int kSirPT = AMBER_SIR_PT;  // threads per block of the persistent kernel
-__global__ void __launch_bounds__(kSirPT, 768 / kSirPT) sir_persistent_kernel(const SirStepArgs a)
+__global__ void __launch_bounds__(kSirPT, 1024 / kSirPT) sir_persistent_kernel(const SirStepArgs a)
 {
+    __shared__ SirSmem sm;
     cg::grid_group grid = cg::this_grid();
     int cur = a.cur;
     for (int64_t k = 0; k < a.n_steps; ++k) {
@@ -523,12 +668,12 @@ __global__ void __launch_bounds__(kSirPT, 768 / kSirPT) sir_persistent_kernel(co
             prev_s = pv->S;
             prev_i = pv->I;
             prev_r = pv->R;
-            push = prev_i < prev_s;
+            push = a.dir == 0 ? prev_i < prev_s : a.dir == 2;
         }
         if (push) {
             long long rec = 0, inf = 0;
             unsigned long long dig = 0;
-            sir_push_body(a, cur, t, rec, inf, dig);
+            sir_push_body(a, cur, t, sm, rec, inf, dig);
             unsigned long long v[4] = {static_cast<unsigned long long>(-inf), static_cast<unsigned long long>(inf - rec),
                                        static_cast<unsigned long long>(rec), dig};
             if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -540,7 +685,7 @@ __global__ void __launch_bounds__(kSirPT, 768 / kSirPT) sir_persistent_kernel(co
             block_sum_atomic<4>(v, outs);
         } else {
             unsigned long long cnt[4] = {0, 0, 0, 0};
-            sir_pull_body(a, cur, t, cnt);
+            sir_pull_body(a, cur, t, sm, cnt);
             unsigned long long* const outs[4] = {&sl->S, &sl->I, &sl->R, a.digest ? &sl->digest : nullptr};
             block_sum_atomic<4>(cnt, outs);
         }
@@ -578,6 +723,7 @@ public:
     DevBuf<SirSlot> ring;
     int64_t m_first = 0;
     bool prev_ok = false;  // ring slot t-1 holds the counts of the current state
+    int dir = 0;           // "direction" option (SirStepArgs::dir)
     // sharded (world > 1, NEXT-3): this rank owns agents [lo, lo + nl) (shard =
     // multiple of 32 agents so bitmap words never straddle ranks), its CSR rows
     // (local offsets, global neighbour ids) and state; every step pulls its rows
@@ -585,6 +731,7 @@ public:
     // all-gathered (N/8 bytes per step in total).
     ShardComm* sc = nullptr;
     int64_t lo = 0, nl = 0, npl = 0, shard = 0;  // local agents / padded (unsharded: n, n_pad)
+    int64_t nq = 0;                              // npl rounded up to whole 128-agent chunks
     DevBuf<uint32_t> ib_glob;  // world * shard / 32 words
     bool glob_ok = false;      // ib_glob holds the current state's bits
 
@@ -615,10 +762,14 @@ public:
             sir_shard_range(n, rt.world, rt.rank, &lo, &nl, &shard);
             npl = shard;
         }
-        for (auto& b : x) b.allocate(&rt, npl);
+        nq = sir_chunks(npl) * kChunk;  // the step kernels work on 128-agent chunks
+        for (auto& b : x) {
+            b.allocate(&rt, nq);
+            AMBER_CUDA(cudaMemsetAsync(b.p, kPad, nq, rt.stream));
+        }
         for (int c = 0; c < 2; ++c) {
-            ib[c].allocate(&rt, npl / 32);
-            sb[c].allocate(&rt, npl / 32);
+            ib[c].allocate(&rt, nq / 32);
+            sb[c].allocate(&rt, nq / 32);
         }
         if (sharded) {
             // every rank builds the (seeded, deterministic) graph and initial state,
@@ -647,11 +798,11 @@ public:
     // push step's invariant: every agent S now is S in the back state).
     void build_bits()
     {
-        sir_bits_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(x[cur].p, npl, ib[cur].p, sb[cur].p);
+        sir_bits_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(x[cur].p, nq, ib[cur].p, sb[cur].p);
         check_launch("sir_bits_kernel");
-        AMBER_CUDA(cudaMemcpyAsync(x[cur ^ 1].p, x[cur].p, npl, cudaMemcpyDeviceToDevice, rt.stream));
-        AMBER_CUDA(cudaMemcpyAsync(ib[cur ^ 1].p, ib[cur].p, npl / 8, cudaMemcpyDeviceToDevice, rt.stream));
-        AMBER_CUDA(cudaMemcpyAsync(sb[cur ^ 1].p, sb[cur].p, npl / 8, cudaMemcpyDeviceToDevice, rt.stream));
+        AMBER_CUDA(cudaMemcpyAsync(x[cur ^ 1].p, x[cur].p, nq, cudaMemcpyDeviceToDevice, rt.stream));
+        AMBER_CUDA(cudaMemcpyAsync(ib[cur ^ 1].p, ib[cur].p, nq / 8, cudaMemcpyDeviceToDevice, rt.stream));
+        AMBER_CUDA(cudaMemcpyAsync(sb[cur ^ 1].p, sb[cur].p, nq / 8, cudaMemcpyDeviceToDevice, rt.stream));
         glob_ok = false;
     }
 
@@ -737,6 +888,7 @@ public:
         a.ring = ring.p;
         a.ring_cap = metrics_cap;
         a.digest = digest_on ? 1 : 0;
+        a.dir = dir;
         return a;
     }
 
@@ -755,7 +907,7 @@ public:
             sir_zero_slots<<<1, 256, 0, rt.stream>>>(ring.p, metrics_cap, t, chunk);
             check_launch("sir_zero_slots");
             const int threads = block ? static_cast<int>(std::min<int64_t>(block, 256)) : 256;
-            if (persistent && chunk > 1) {
+            if (persistent && (chunk > 1 || dir != 0)) {
                 const int pthreads = block ? threads : kSirPT;
                 int per_sm = 0;
                 AMBER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sir_persistent_kernel, pthreads, 0));
@@ -764,15 +916,15 @@ public:
                 // (C2); large populations are bound by random L2 lookups instead: full occupancy
                 const int per = n_pad > (1ll << 22) ? per_sm : std::min(per_sm, std::max(1, 768 / pthreads));
                 int blocks = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(per) * rt.num_sms,
-                                                                ceil_div(n_pad, pthreads)));
+                                                                ceil_div(sir_chunks(n_pad), std::max(1, pthreads / 32))));
                 if (grid) blocks = static_cast<int>(std::min<int64_t>(grid, static_cast<int64_t>(per_sm) * rt.num_sms));
                 blocks = std::max(blocks, 1);
                 SirStepArgs a = args(chunk);
                 queue.zero_async(rt.stream);
                 a.queue = queue.p;
                 const int64_t warps = static_cast<int64_t>(blocks) * pthreads / 32;
-                a.grab = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, (n_pad / 32) / (warps * 8))));
-                if (n_pad / 32 <= 2 * warps) a.queue = nullptr;  // <= 2 chunks per warp: static striding
+                a.grab = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, sir_chunks(n_pad) / (warps * 8))));
+                if (sir_chunks(n_pad) <= 2 * warps) a.queue = nullptr;  // <= 2 chunks per warp: static striding
                 void* kargs[] = {&a};
                 prof.launch(rt.stream, "sir_persistent", [&] {
                     AMBER_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sir_persistent_kernel), blocks,
@@ -785,7 +937,7 @@ public:
             } else {
                 for (int64_t k = 0; k < chunk; ++k) {
                     SirStepArgs a = args(1);
-                    int blocks = static_cast<int>(ceil_div(n_pad, threads));
+                    int blocks = static_cast<int>(ceil_div(sir_chunks(n_pad), std::max(1, threads / 32)));
                     if (grid) blocks = static_cast<int>(grid);
                     prof.launch(rt.stream, "sir_step", [&] { sir_step_kernel<<<blocks, threads, 0, rt.stream>>>(a); });
                     check_launch("sir_step_kernel");
@@ -811,7 +963,7 @@ public:
             check_launch("sir_zero_slots");
             SirStepArgs a = args(1);
             a.ib[cur] = ib_glob.p;  // read: global bits of state t; write: local bits of t+1
-            int blocks = static_cast<int>(std::max<int64_t>(1, ceil_div(npl, threads)));
+            int blocks = static_cast<int>(std::max<int64_t>(1, ceil_div(sir_chunks(npl), std::max(1, threads / 32))));
             if (grid) blocks = static_cast<int>(grid);
             prof.launch(rt.stream, "sir_shard_step", [&] { sir_step_kernel<<<blocks, threads, 0, rt.stream>>>(a); });
             check_launch("sir_step_kernel");
@@ -936,6 +1088,12 @@ public:
             return true;
         }
         if (k == "block") AMBER_REQUIRE(v <= 256, "SIR kernels are built for <= 256 threads per block");
+        if (k == "direction") {
+            AMBER_REQUIRE(v >= 0 && v <= 2, "direction must be 0 (auto), 1 (pull) or 2 (push)");
+            AMBER_REQUIRE(!sc || v != 2, "sharded SIR steps pull only");
+            dir = static_cast<int>(v);
+            return true;
+        }
         return Model::set_option(key, v);
     }
 
@@ -943,6 +1101,7 @@ public:
     {
         std::string k(key);
         if (k == "edges") { *v = g.arcs / 2; return true; }
+        if (k == "direction") { *v = dir; return true; }
         return Model::get_option(key, v);
     }
 };

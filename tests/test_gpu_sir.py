@@ -231,3 +231,28 @@ def test_sweep_full_c5_all_replicates_vs_oracle_golden():
     assert np.array_equal(np.array([float(r[1]) for r in rows]), betas)
     got = sweep(c["n"], sir_params(c["mean_degree"], 0.0, c["gamma"], c["init_frac"]), betas, seeds, c["steps"])
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("n", [37, 129, 4_097, 100_003])
+@pytest.mark.parametrize("direction", [1, 2])
+def test_forced_direction_every_step_ragged(orc, n, direction):
+    # "direction" 1 = pull only, 2 = push whenever possible; both are the same
+    # S3 draws, so each step must equal the oracle (128-agent chunks with a
+    # ragged tail, one-step cooperative launches and multi-step launches)
+    cfg = dict(n=n, mean_degree=6.0, beta=0.2, gamma=0.15, init_frac=0.05, seed=n % 97)
+    m = make(cfg)
+    m.set_option("direction", direction)
+    m.set_option("digest", 1)
+    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
+    x = orc.sir_init(n, sir_counts(cfg)[1], cfg["seed"])
+    t = 0
+    for chunk in (1, 1, 3, 1, 5, 2):
+        m.step(chunk)
+        for _ in range(chunk):
+            x = orc.sir_step(rp, col, x, cfg["seed"], t, cfg["beta"], cfg["gamma"])
+            t += 1
+        assert np.array_equal(m.read_column("state"), x), f"step {t}"
+    counts = np.array([(x == s).sum() for s in range(3)])
+    assert [int(m.metrics(k)[-1]) for k in "SIR"] == counts.tolist()
+    assert m.digest("state") == orc.digest(x)
+    assert int(m.metrics("digest")[-1]) == orc.digest(x)

@@ -11,6 +11,8 @@
 //   dsmem_red : red.shared::cluster.add.u32 to a random CTA of a cluster of 8
 //   stg_coal  : coalesced 4-byte global stores (bin write reference)
 //   nop       : hashing only
+//   ldg_rand  : random 4-byte loads from a 16 MB (L2-resident) array, summed
+//               (the neighbour-bitmap lookup of the SIR walk at large N)
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -31,6 +33,7 @@ __global__ void __launch_bounds__(1024, 2) probe(unsigned* g, unsigned gmask, un
     for (int i = threadIdx.x; i < kWords; i += blockDim.x) s[i] = 0;
     __syncthreads();
     unsigned h = hash32(blockIdx.x * blockDim.x + threadIdx.x);
+    unsigned acc = 0;
     const unsigned long long gi = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
     for (int i = 0; i < kIters; ++i) {
         h = hash32(h + i);
@@ -41,9 +44,11 @@ __global__ void __launch_bounds__(1024, 2) probe(unsigned* g, unsigned gmask, un
         if constexpr (MODE == 4) atomicAdd(s + (h % kWords), (h >> 30) | 1u);
         if constexpr (MODE == 5) g[(gi + (unsigned long long)i * gridDim.x * blockDim.x) & gmask] = h;
         if constexpr (MODE == 6) if (h == 0x12345678u) sink[0] = h;
+        if constexpr (MODE == 7) acc += __ldcg(g + (h & gmask));
     }
     __syncthreads();
     if (threadIdx.x == 0) sink[1 + blockIdx.x % 64] += s[h % kWords];
+    if (acc == 0x9e3779b9u) sink[0] = acc;
 }
 
 __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(1024, 2) probe_dsmem(unsigned* sink)
@@ -95,6 +100,7 @@ int main()
     run("atoms_var", [&](int gr) { probe<4><<<gr, thr>>>(g, mask, sink); }, grid);
     run("sts", [&](int gr) { probe<2><<<gr, thr>>>(g, mask, sink); }, grid);
     run("rmw", [&](int gr) { probe<3><<<gr, thr>>>(g, mask, sink); }, grid);
+    run("ldg_rand", [&](int gr) { probe<7><<<gr, thr>>>(g, (16u << 20) / 4 - 1, sink); }, grid);
     run("stg_coal", [&](int gr) { probe<5><<<gr, thr>>>(g, (16u << 20) - 1, sink); }, grid);
     int ncl = 0;
     {
