@@ -307,6 +307,9 @@ struct P2PMap {
     DevBuf<unsigned int> token; // 1-element barrier all-reduce
 };
 
+// Registry of the open mappings.  Ranks of a loopback group open and close
+// theirs from their own host threads, so every access holds p2p_mu.
+static std::mutex p2p_mu;
 static std::map<WealthExchange*, std::unique_ptr<P2PMap>>& p2p_maps()
 {
     static std::map<WealthExchange*, std::unique_ptr<P2PMap>> m;
@@ -369,12 +372,14 @@ bool wealth_p2p_open(WealthExchange* x, Runtime& rt, void* my_base, std::vector<
         map->token.zero_async(rt.stream);
     }
     peers = map->peers;
+    std::lock_guard<std::mutex> g(p2p_mu);
     p2p_maps()[x] = std::move(map);
     return true;
 }
 
 void wealth_p2p_close(WealthExchange* x)
 {
+    std::lock_guard<std::mutex> g(p2p_mu);
     auto it = p2p_maps().find(x);
     if (it == p2p_maps().end()) return;
     for (size_t p = 0; p < it->second->peers.size(); ++p)
@@ -392,7 +397,12 @@ void wealth_p2p_barrier(WealthExchange* x, Runtime& rt)
         x->hub->barrier();
         return;
     }
-    P2PMap& m = *p2p_maps().at(x);
+    P2PMap* mp;
+    {
+        std::lock_guard<std::mutex> g(p2p_mu);
+        mp = p2p_maps().at(x).get();
+    }
+    P2PMap& m = *mp;
     nccl_check(nccl().AllReduce(m.token.p, m.token.p, 1, ncclUint32, ncclSum, x->comm->comm, rt.stream),
                "ncclAllReduce(barrier)");
 }

@@ -289,37 +289,39 @@ constexpr int kWalkU = AMBER_SIR_WALK_U;  // 32-arc batches in flight per warp (
 #endif
 constexpr int kSirPT = AMBER_SIR_PT;  // threads per block of the persistent kernel
 
-// Warp chunks of kChunk = 128 agents: lane L holds agents 4L..4L+3 of the
-// chunk (one 32-bit load of the state bytes, one Philox block for the four
-// recovery draws, R4).  The state buffers and bitmaps are allocated to a
-// multiple of 128 agents (padding = kPad).  Persistent launch (queue !=
-// nullptr): dynamic -- the chunk range is split into kRegions contiguous
-// regions, warp w draws batches of `grab` chunks from region w % kRegions with
-// one atomic (per-region counters, so the atomics spread); the pull and push
-// walks cost very different amounts per chunk, and static striding left most
-// warps waiting at the step barrier (r01 ncu: 43% of stall samples).  Per-step
+// Warp chunks of 32 * APL agents: lane L holds agents APL*L .. APL*L+APL-1 of
+// the chunk (one load of its state bytes; for APL = 4 one Philox block serves
+// the lane's four recovery draws, R4).  APL = 4 (128-agent chunks) for large
+// populations, APL = 1 where latency rules (C2: more, shorter warp tasks).
+// The state buffers and bitmaps are allocated to a multiple of kChunkMax
+// agents (padding = kPad).  Persistent launch (queue != nullptr): dynamic --
+// the chunk range is split into kRegions contiguous regions, warp w draws
+// batches of `grab` chunks from region w % kRegions with one atomic
+// (per-region counters, so the atomics spread); the pull and push walks cost
+// very different amounts per chunk, and static striding left most warps
+// waiting at the step barrier (r01 ncu: 43% of stall samples).  Per-step
 // launch: one chunk per warp, the block scheduler balances.
-constexpr int kChunk = 128;
-constexpr int kQCap = 160;  // owner queue per warp: < 32 carried + 128 of one chunk
+constexpr int kChunkMax = 128;
+constexpr int kQCap = 32 + kChunkMax;  // owner queue per warp: < 32 carried + one chunk
 
 struct SirSmem {
     int32_t id[kSirPT / 32][kQCap];  // owner: agent offset (pull: in the chunk; push: local agent id)
     int32_t rb[kSirPT / 32][kQCap];  // owner's row [rb, re)
     int32_t re[kSirPT / 32][kQCap];
-    uint32_t h[kSirPT / 32][4];      // pull: infected bits of the chunk's 128 agents
+    uint32_t h[kSirPT / 32][kChunkMax / 32];  // pull: infected bits of the chunk's agents
 };
 
-__host__ __device__ constexpr int64_t sir_chunks(int64_t n_pad) { return (n_pad + kChunk - 1) / kChunk; }
+__host__ __device__ constexpr int64_t sir_chunks(int64_t n_pad, int apl) { return (n_pad + 32 * apl - 1) / (32 * apl); }
 
-template <class F>
+template <int APL, class F>
 __device__ __forceinline__ void for_chunks(const SirStepArgs& a, uint32_t* q, F&& f)
 {
     const int lane = threadIdx.x & 31;
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    const int64_t nchunks = sir_chunks(a.n_pad);
+    const int64_t nchunks = sir_chunks(a.n_pad, APL);
     if (!q || nw < kRegions) {
-        for (int64_t c = gw; c < nchunks; c += nw) f(c * kChunk);
+        for (int64_t c = gw; c < nchunks; c += nw) f(c * 32 * APL);
         return;
     }
     const int r = static_cast<int>(gw % kRegions);
@@ -330,7 +332,7 @@ __device__ __forceinline__ void for_chunks(const SirStepArgs& a, uint32_t* q, F&
         c0 = __shfl_sync(0xffffffffu, c0, 0);
         if (lo + c0 >= hi) break;
         const int64_t e = lo + c0 + a.grab < hi ? lo + c0 + a.grab : hi;
-        for (int64_t c = lo + c0; c < e; ++c) f(c * kChunk);
+        for (int64_t c = lo + c0; c < e; ++c) f(c * 32 * APL);
     }
 }
 
@@ -353,15 +355,40 @@ __device__ __forceinline__ bool bit_of(const uint32_t* bits, uint32_t j)
     return (w >> (j & 31u)) & 1u;
 }
 
-// Recovery draws of the lane's four agents i0..i0+3 (i0 = global id, multiple
-// of 4): one Philox block, lane k of block i0/4 (R4).  Bit k set iff agent
-// i0 + k is in `inf` and recovers.
+// The lane's APL state bytes (agents i0 .. i0+APL-1) as one word.
+template <int APL>
+__device__ __forceinline__ uint32_t load_states(const uint8_t* x, int64_t i0)
+{
+    if constexpr (APL == 4) return *reinterpret_cast<const uint32_t*>(x + i0);
+    else if constexpr (APL == 2) return *reinterpret_cast<const uint16_t*>(x + i0);
+    else return x[i0];
+}
+
+template <int APL>
+__device__ __forceinline__ void store_states(uint8_t* y, int64_t i0, uint32_t v)
+{
+    if constexpr (APL == 4) *reinterpret_cast<uint32_t*>(y + i0) = v;
+    else if constexpr (APL == 2) *reinterpret_cast<uint16_t*>(y + i0) = static_cast<uint16_t>(v);
+    else y[i0] = static_cast<uint8_t>(v);
+}
+
+// Recovery draws of the lane's agents i0 .. i0+APL-1 (global ids; i0 is a
+// multiple of APL): lane i & 3 of Philox block i / 4 (R4) -- one block for the
+// whole lane when APL = 4.  Bit k set iff agent i0 + k is in `inf` and recovers.
+template <int APL>
 __device__ __forceinline__ uint32_t recover_nib(const SirStepArgs& a, unsigned long long i0, uint32_t t, uint32_t inf)
 {
     if (!inf) return 0u;
     const uint4 r = stream_block(a.key, TAG_SIR_REC, i0 >> 2, t);
-    return ((inf & 1u) && r.x < a.t_gamma ? 1u : 0u) | ((inf & 2u) && r.y < a.t_gamma ? 2u : 0u) |
-           ((inf & 4u) && r.z < a.t_gamma ? 4u : 0u) | ((inf & 8u) && r.w < a.t_gamma ? 8u : 0u);
+    const uint32_t d[4] = {r.x, r.y, r.z, r.w};
+    uint32_t out = 0;
+#pragma unroll
+    for (int k = 0; k < APL; ++k) {
+        const uint32_t q = static_cast<uint32_t>((i0 + k) & 3u);
+        const uint32_t v = q == 0 ? d[0] : (q == 1 ? d[1] : (q == 2 ? d[2] : d[3]));
+        if (((inf >> k) & 1u) && v < a.t_gamma) out |= 1u << k;
+    }
+    return out;
 }
 
 // Exclusive warp prefix sum; *total = the warp's sum.
@@ -378,20 +405,23 @@ __device__ __forceinline__ uint32_t warp_excl(uint32_t v, uint32_t* total)
     return incl - v;
 }
 
-// Bitmap word m of a 128-agent chunk from the lanes' 4-bit nibbles: lanes
-// 8m..8m+7 hold agents 32m..32m+31; every lane of the group gets the word.
+// Bitmap word of the lane's agents from the lanes' APL-bit nibbles: lanes
+// g*(32/APL) .. (g+1)*(32/APL)-1 hold the 32 agents of word g of the chunk;
+// every lane of the group gets the word.
+template <int APL>
 __device__ __forceinline__ uint32_t word_of(uint32_t nib)
 {
-    uint32_t v = nib << ((threadIdx.x & 7) * 4);
-    v |= __shfl_xor_sync(0xffffffffu, v, 1);
-    v |= __shfl_xor_sync(0xffffffffu, v, 2);
-    v |= __shfl_xor_sync(0xffffffffu, v, 4);
+    if constexpr (APL == 1) return __ballot_sync(0xffffffffu, nib & 1u);
+    constexpr int G = 32 / APL;  // lanes per word
+    uint32_t v = nib << ((threadIdx.x & (G - 1)) * APL);
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
 
-// Appends the lane's agents in `nib` (local ids i0 + k, or chunk offsets when
-// `chunk_off`) with their CSR rows to the warp's owner queue at qn + rank;
-// returns the number appended by the warp.
+// Appends the lane's agents in `nib` (ids id_base + k) with their CSR rows to
+// the warp's owner queue at qn + rank; returns the number the warp appended.
+template <int APL>
 __device__ __forceinline__ uint32_t queue_owners(const SirStepArgs& a, SirSmem& sm, uint32_t qn, int64_t i0,
                                                  uint32_t nib, int32_t id_base)
 {
@@ -399,20 +429,25 @@ __device__ __forceinline__ uint32_t queue_owners(const SirStepArgs& a, SirSmem& 
     uint32_t T;
     uint32_t k = qn + warp_excl(__popc(nib), &T);
     if (nib) {
-        int32_t r[5];
-        if (i0 + 4 <= a.n) {
-            const int4 v = *reinterpret_cast<const int4*>(a.row_ptr + i0);
-            r[0] = v.x;
-            r[1] = v.y;
-            r[2] = v.z;
-            r[3] = v.w;
-            r[4] = a.row_ptr[i0 + 4];
+        int32_t r[APL + 1];
+        if constexpr (APL == 4) {
+            if (i0 + 4 <= a.n) {
+                const int4 v = *reinterpret_cast<const int4*>(a.row_ptr + i0);
+                r[0] = v.x;
+                r[1] = v.y;
+                r[2] = v.z;
+                r[3] = v.w;
+                r[4] = a.row_ptr[i0 + 4];
+            } else {
+#pragma unroll
+                for (int q = 0; q < 5; ++q) r[q] = i0 + q <= a.n ? a.row_ptr[i0 + q] : 0;
+            }
         } else {
 #pragma unroll
-            for (int q = 0; q < 5; ++q) r[q] = i0 + q <= a.n ? a.row_ptr[i0 + q] : 0;
+            for (int q = 0; q <= APL; ++q) r[q] = i0 + q <= a.n ? a.row_ptr[i0 + q] : 0;
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < APL; ++q)
             if ((nib >> q) & 1u) {
                 sm.id[wq][k] = id_base + q;
                 sm.rb[wq][k] = r[q];
@@ -423,23 +458,25 @@ __device__ __forceinline__ uint32_t queue_owners(const SirStepArgs& a, SirSmem& 
     return T;
 }
 
-// Pull step for the 128 agents of chunk a0: the susceptible agents, compacted
-// into groups of 32 owners, walk their rows warp-cooperatively; an arc
-// transmits iff the neighbour is I (bitmap, L2-resident) and the pair-keyed
-// Bernoulli (S3) fires.  Writes the next state and the next bitmap words and
-// adds the S/I/R counts (and digest terms) of the new states to cnt.
+// Pull step for the 32 * APL agents of chunk a0: the susceptible agents,
+// compacted into groups of 32 owners, walk their rows warp-cooperatively; an
+// arc transmits iff the neighbour is I (bitmap, L2-resident) and the
+// pair-keyed Bernoulli (S3) fires.  Writes the next state and the next bitmap
+// words and adds the S/I/R counts (and digest terms) of the new states to cnt.
+template <int APL>
 __device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0, const uint8_t* __restrict__ x,
                                                uint8_t* __restrict__ y, const uint32_t* __restrict__ ib,
                                                uint32_t* __restrict__ ib_next, uint32_t* __restrict__ sb_next,
                                                uint32_t t, SirSmem& sm, unsigned long long (&cnt)[4])
 {
+    constexpr uint32_t kM = (1u << APL) - 1u;
     const int lane = threadIdx.x & 31;
     const int wq = threadIdx.x >> 5;
-    const int64_t i0 = a0 + 4 * lane;
-    const uint32_t xw = *reinterpret_cast<const uint32_t*>(x + i0);
+    const int64_t i0 = a0 + APL * lane;
+    const uint32_t xw = load_states<APL>(x, i0);
     uint32_t nib_s = 0, nib_i = 0, nib_r = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < APL; ++k) {
         const uint32_t st = (xw >> (8 * k)) & 0xffu;
         nib_s |= (st == kS ? 1u : 0u) << k;
         nib_i |= (st == kI ? 1u : 0u) << k;
@@ -447,8 +484,8 @@ __device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0,
     }
     uint32_t hitnib = 0;
     if (__any_sync(0xffffffffu, nib_s != 0)) {
-        if (lane < 4) sm.h[wq][lane] = 0u;
-        const uint32_t T = queue_owners(a, sm, 0, i0, nib_s, 4 * lane);
+        if (lane < APL) sm.h[wq][lane] = 0u;
+        const uint32_t T = queue_owners<APL>(a, sm, 0, i0, nib_s, APL * lane);
         __syncwarp();
         for (uint32_t g0 = 0; g0 < T; g0 += 32) {
             const uint32_t nown = T - g0 < 32 ? T - g0 : 32;
@@ -467,21 +504,21 @@ __device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0,
             if ((hit >> lane) & 1u) atomicOr(&sm.h[wq][lid >> 5], 1u << (lid & 31));
         }
         __syncwarp();
-        hitnib = (sm.h[wq][lane >> 3] >> ((lane & 7) * 4)) & 0xfu;
+        hitnib = (sm.h[wq][(APL * lane) >> 5] >> ((APL * lane) & 31)) & kM;
         __syncwarp();  // the next chunk rewrites the queue and h
     }
-    const uint32_t recnib = recover_nib(a, a.gid0 + static_cast<unsigned long long>(i0), t, nib_i);
+    const uint32_t recnib = recover_nib<APL>(a, a.gid0 + static_cast<unsigned long long>(i0), t, nib_i);
     const uint32_t s2 = nib_s & ~hitnib, i2 = (nib_s & hitnib) | (nib_i & ~recnib), r2 = nib_r | recnib;
     uint32_t yw = xw;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-        if (((nib_s & hitnib) | recnib) >> k & 1u)
+    for (int k = 0; k < APL; ++k)
+        if ((((nib_s & hitnib) | recnib) >> k) & 1u)
             yw = (yw & ~(0xffu << (8 * k))) | (static_cast<uint32_t>((i2 >> k) & 1u ? kI : kR) << (8 * k));
-    *reinterpret_cast<uint32_t*>(y + i0) = yw;
-    const uint32_t wi = word_of(i2), ws = word_of(s2);
-    if ((lane & 7) == 0) {
-        ib_next[(a0 >> 5) + (lane >> 3)] = wi;
-        sb_next[(a0 >> 5) + (lane >> 3)] = ws;
+    store_states<APL>(y, i0, yw);
+    const uint32_t wi = word_of<APL>(i2), ws = word_of<APL>(s2);
+    if ((lane & (32 / APL - 1)) == 0) {
+        ib_next[(a0 >> 5) + lane / (32 / APL)] = wi;
+        sb_next[(a0 >> 5) + lane / (32 / APL)] = ws;
     }
     // pads (kPad) are in none of the nibbles
     cnt[0] += __popc(s2);
@@ -489,25 +526,27 @@ __device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0,
     cnt[2] += __popc(r2);
     if (a.digest) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < APL; ++k)
             if (i0 + k < a.n) cnt[3] += digest_term(a.gid0 + static_cast<unsigned long long>(i0 + k), (yw >> (8 * k)) & 0xffu);
     }
 }
 
+template <int APL>
 __device__ __forceinline__ void sir_pull_body(const SirStepArgs& a, int c, uint32_t t, SirSmem& sm,
                                               unsigned long long (&cnt)[4])
 {
-    for_chunks(a, queue_of(a, t, 0), [&](int64_t a0) {
-        sir_pull_chunk(a, a0, a.x[c], a.x[c ^ 1], a.ib[c], a.ib[c ^ 1], a.sb[c ^ 1], t, sm, cnt);
+    for_chunks<APL>(a, queue_of(a, t, 0), [&](int64_t a0) {
+        sir_pull_chunk<APL>(a, a0, a.x[c], a.x[c ^ 1], a.ib[c], a.ib[c ^ 1], a.sb[c ^ 1], t, sm, cnt);
     });
 }
 
+template <int APL>
 __global__ void __launch_bounds__(256) sir_step_kernel(const SirStepArgs a)
 {
     __shared__ SirSmem sm;
     const uint32_t t = a.t0;
     unsigned long long cnt[4] = {0, 0, 0, 0};
-    sir_pull_body(a, a.cur, t, sm, cnt);
+    sir_pull_body<APL>(a, a.cur, t, sm, cnt);
     SirSlot* sl = a.ring + (t % a.ring_cap);
     unsigned long long* const outs[4] = {&sl->S, &sl->I, &sl->R, a.digest ? &sl->digest : nullptr};
     block_sum_atomic<4>(cnt, outs);
@@ -547,6 +586,7 @@ __global__ void sir_bits_kernel(const uint8_t* __restrict__ x, int64_t n_pad, ui
 // Pushers are compacted across chunks into the warp's owner queue and walked
 // 32 owners at a time, so the concatenated rows fill the walk's 32-arc batches
 // even when few agents are infected.
+template <int APL>
 __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint32_t t, SirSmem& sm, long long& rec,
                                               long long& inf, unsigned long long& dig)
 {
@@ -581,12 +621,12 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
             return false;  // an infected agent tries every susceptible neighbour
         });
     };
-    for_chunks(a, queue_of(a, t, 1), [&](int64_t a0) {
-        const int64_t i0 = a0 + 4 * lane;
-        const uint32_t xw = *reinterpret_cast<const uint32_t*>(x + i0);
+    for_chunks<APL>(a, queue_of(a, t, 1), [&](int64_t a0) {
+        const int64_t i0 = a0 + APL * lane;
+        const uint32_t xw = load_states<APL>(x, i0);
         uint32_t nib_s = 0, nib_i = 0, nons = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < APL; ++k) {
             const uint32_t st = (xw >> (8 * k)) & 0xffu;
             nib_s |= (st == kS ? 1u : 0u) << k;
             nib_i |= (st == kI ? 1u : 0u) << k;
@@ -594,35 +634,37 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
         }
         if (a.digest && nib_s) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
+            for (int k = 0; k < APL; ++k)
                 if ((nib_s >> k) & 1u) dig += digest_term(static_cast<unsigned long long>(i0 + k), kS);
         }
         if (!__any_sync(0xffffffffu, nons != 0)) return;
         // owners: recoveries and the new state of every non-S agent
-        const uint32_t recnib = recover_nib(a, static_cast<unsigned long long>(i0), t, nib_i);
+        const uint32_t recnib = recover_nib<APL>(a, static_cast<unsigned long long>(i0), t, nib_i);
         rec += __popc(recnib);
         if (nons) {
-            const uint32_t yold = yw[i0 >> 2];
+            // the lane's bytes sit in one 32-bit word (i0 is a multiple of APL)
+            const uint32_t sh0 = static_cast<uint32_t>(i0 & 3) * 8u;
+            const uint32_t yold = yw[i0 >> 2] >> sh0;
             uint32_t delta = 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
+            for (int k = 0; k < APL; ++k)
                 if ((nons >> k) & 1u) {
                     const uint32_t nw = (recnib >> k) & 1u ? kR : (xw >> (8 * k)) & 0xffu;
                     delta += (nw - ((yold >> (8 * k)) & 0xffu)) << (8 * k);  // mod 2^32: bytes stay in 0..3
                     if (a.digest) dig += digest_term(static_cast<unsigned long long>(i0 + k), nw);
                 }
-            if (delta) atomicAdd(yw + (i0 >> 2), delta);
+            if (delta) atomicAdd(yw + (i0 >> 2), delta << sh0);
         }
-        const uint32_t wsurv = word_of(nib_i & ~recnib), wnons = word_of(nons);
-        if ((lane & 7) == 0 && wnons) {
-            const int64_t w = (a0 >> 5) + (lane >> 3);
+        const uint32_t wsurv = word_of<APL>(nib_i & ~recnib), wnons = word_of<APL>(nons);
+        if ((lane & (32 / APL - 1)) == 0 && wnons) {
+            const int64_t w = (a0 >> 5) + lane / (32 / APL);
             const uint32_t flip = (ib_next[w] ^ wsurv) & wnons;
             if (flip) atomicXor(ib_next + w, flip);
             if (sb_next[w] & wnons) atomicAnd(sb_next + w, ~wnons);
         }
         // pushers: queue, walk whenever 32 are queued
         if (!__any_sync(0xffffffffu, nib_i != 0)) return;
-        qn += queue_owners(a, sm, qn, i0, nib_i, static_cast<int32_t>(i0));
+        qn += queue_owners<APL>(a, sm, qn, i0, nib_i, static_cast<int32_t>(i0));
         __syncwarp();
         if (qn < 32) return;
         uint32_t g0 = 0;
@@ -651,6 +693,7 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
 // fewer than the susceptible ones (counts of the previous step from its ring
 // slot, so every block takes the same decision), otherwise it pulls.  Both
 // directions give identical results (S3); the tests check it.
+template <int APL>
 __global__ void __launch_bounds__(kSirPT, 1024 / kSirPT) sir_persistent_kernel(const SirStepArgs a)
 {
     __shared__ SirSmem sm;
@@ -673,7 +716,7 @@ __global__ void __launch_bounds__(kSirPT, 1024 / kSirPT) sir_persistent_kernel(c
         if (push) {
             long long rec = 0, inf = 0;
             unsigned long long dig = 0;
-            sir_push_body(a, cur, t, sm, rec, inf, dig);
+            sir_push_body<APL>(a, cur, t, sm, rec, inf, dig);
             unsigned long long v[4] = {static_cast<unsigned long long>(-inf), static_cast<unsigned long long>(inf - rec),
                                        static_cast<unsigned long long>(rec), dig};
             if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -685,7 +728,7 @@ __global__ void __launch_bounds__(kSirPT, 1024 / kSirPT) sir_persistent_kernel(c
             block_sum_atomic<4>(v, outs);
         } else {
             unsigned long long cnt[4] = {0, 0, 0, 0};
-            sir_pull_body(a, cur, t, sm, cnt);
+            sir_pull_body<APL>(a, cur, t, sm, cnt);
             unsigned long long* const outs[4] = {&sl->S, &sl->I, &sl->R, a.digest ? &sl->digest : nullptr};
             block_sum_atomic<4>(cnt, outs);
         }
@@ -724,6 +767,7 @@ public:
     int64_t m_first = 0;
     bool prev_ok = false;  // ring slot t-1 holds the counts of the current state
     int dir = 0;           // "direction" option (SirStepArgs::dir)
+    int apl = 0;           // "apl" option: agents per lane of the step kernels (0 = auto, 1, 2, 4)
     // sharded (world > 1, NEXT-3): this rank owns agents [lo, lo + nl) (shard =
     // multiple of 32 agents so bitmap words never straddle ranks), its CSR rows
     // (local offsets, global neighbour ids) and state; every step pulls its rows
@@ -762,7 +806,7 @@ public:
             sir_shard_range(n, rt.world, rt.rank, &lo, &nl, &shard);
             npl = shard;
         }
-        nq = sir_chunks(npl) * kChunk;  // the step kernels work on 128-agent chunks
+        nq = sir_chunks(npl, 4) * kChunkMax;  // the step kernels work on chunks of up to 128 agents
         for (auto& b : x) {
             b.allocate(&rt, nq);
             AMBER_CUDA(cudaMemsetAsync(b.p, kPad, nq, rt.stream));
@@ -892,6 +936,17 @@ public:
         return a;
     }
 
+    // agents per lane of the step kernels ("apl" option; auto: 4 for large
+    // populations, 1 where the step is latency-bound -- shorter warp tasks)
+    int lanes_apl() const { return apl ? apl : (npl > (1ll << 22) ? 4 : 1); }
+
+    void launch_step(int L, int blocks, int threads, const SirStepArgs& a)
+    {
+        if (L == 4) sir_step_kernel<4><<<blocks, threads, 0, rt.stream>>>(a);
+        else if (L == 2) sir_step_kernel<2><<<blocks, threads, 0, rt.stream>>>(a);
+        else sir_step_kernel<1><<<blocks, threads, 0, rt.stream>>>(a);
+    }
+
     void step(int64_t nsteps) override
     {
         AMBER_REQUIRE(nsteps >= 0, "n_steps must be >= 0");
@@ -907,28 +962,31 @@ public:
             sir_zero_slots<<<1, 256, 0, rt.stream>>>(ring.p, metrics_cap, t, chunk);
             check_launch("sir_zero_slots");
             const int threads = block ? static_cast<int>(std::min<int64_t>(block, 256)) : 256;
+            const int L = lanes_apl();
             if (persistent && (chunk > 1 || dir != 0)) {
                 const int pthreads = block ? threads : kSirPT;
+                const void* fn = L == 4 ? reinterpret_cast<const void*>(sir_persistent_kernel<4>)
+                               : L == 2 ? reinterpret_cast<const void*>(sir_persistent_kernel<2>)
+                                        : reinterpret_cast<const void*>(sir_persistent_kernel<1>);
                 int per_sm = 0;
-                AMBER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sir_persistent_kernel, pthreads, 0));
+                AMBER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, pthreads, 0));
                 // latency-bound: many resident warps help, but the grid barrier
                 // cost grows with the block count; 3 blocks/SM measured best (C2)
                 // (C2); large populations are bound by random L2 lookups instead: full occupancy
                 const int per = n_pad > (1ll << 22) ? per_sm : std::min(per_sm, std::max(1, 768 / pthreads));
                 int blocks = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(per) * rt.num_sms,
-                                                                ceil_div(sir_chunks(n_pad), std::max(1, pthreads / 32))));
+                                                                ceil_div(sir_chunks(n_pad, L), std::max(1, pthreads / 32))));
                 if (grid) blocks = static_cast<int>(std::min<int64_t>(grid, static_cast<int64_t>(per_sm) * rt.num_sms));
                 blocks = std::max(blocks, 1);
                 SirStepArgs a = args(chunk);
                 queue.zero_async(rt.stream);
                 a.queue = queue.p;
                 const int64_t warps = static_cast<int64_t>(blocks) * pthreads / 32;
-                a.grab = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, sir_chunks(n_pad) / (warps * 8))));
-                if (sir_chunks(n_pad) <= 2 * warps) a.queue = nullptr;  // <= 2 chunks per warp: static striding
+                a.grab = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, sir_chunks(n_pad, L) / (warps * 8))));
+                if (sir_chunks(n_pad, L) <= 2 * warps) a.queue = nullptr;  // <= 2 chunks per warp: static striding
                 void* kargs[] = {&a};
                 prof.launch(rt.stream, "sir_persistent", [&] {
-                    AMBER_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sir_persistent_kernel), blocks,
-                                                           pthreads, kargs, 0, rt.stream));
+                    AMBER_CUDA(cudaLaunchCooperativeKernel(fn, blocks, pthreads, kargs, 0, rt.stream));
                 });
                 check_launch("sir_persistent_kernel");
                 t += chunk;
@@ -937,9 +995,9 @@ public:
             } else {
                 for (int64_t k = 0; k < chunk; ++k) {
                     SirStepArgs a = args(1);
-                    int blocks = static_cast<int>(ceil_div(sir_chunks(n_pad), std::max(1, threads / 32)));
+                    int blocks = static_cast<int>(ceil_div(sir_chunks(n_pad, L), std::max(1, threads / 32)));
                     if (grid) blocks = static_cast<int>(grid);
-                    prof.launch(rt.stream, "sir_step", [&] { sir_step_kernel<<<blocks, threads, 0, rt.stream>>>(a); });
+                    prof.launch(rt.stream, "sir_step", [&] { launch_step(L, blocks, threads, a); });
                     check_launch("sir_step_kernel");
                     cur ^= 1;
                     ++t;
@@ -963,9 +1021,10 @@ public:
             check_launch("sir_zero_slots");
             SirStepArgs a = args(1);
             a.ib[cur] = ib_glob.p;  // read: global bits of state t; write: local bits of t+1
-            int blocks = static_cast<int>(std::max<int64_t>(1, ceil_div(sir_chunks(npl), std::max(1, threads / 32))));
+            const int L = lanes_apl();
+            int blocks = static_cast<int>(std::max<int64_t>(1, ceil_div(sir_chunks(npl, L), std::max(1, threads / 32))));
             if (grid) blocks = static_cast<int>(grid);
-            prof.launch(rt.stream, "sir_shard_step", [&] { sir_step_kernel<<<blocks, threads, 0, rt.stream>>>(a); });
+            prof.launch(rt.stream, "sir_shard_step", [&] { launch_step(L, blocks, threads, a); });
             check_launch("sir_step_kernel");
             cur ^= 1;
             ++t;
@@ -1088,6 +1147,11 @@ public:
             return true;
         }
         if (k == "block") AMBER_REQUIRE(v <= 256, "SIR kernels are built for <= 256 threads per block");
+        if (k == "apl") {
+            AMBER_REQUIRE(v == 0 || v == 1 || v == 2 || v == 4, "apl must be 0 (auto), 1, 2 or 4");
+            apl = static_cast<int>(v);
+            return true;
+        }
         if (k == "direction") {
             AMBER_REQUIRE(v >= 0 && v <= 2, "direction must be 0 (auto), 1 (pull) or 2 (push)");
             AMBER_REQUIRE(!sc || v != 2, "sharded SIR steps pull only");
@@ -1102,6 +1166,7 @@ public:
         std::string k(key);
         if (k == "edges") { *v = g.arcs / 2; return true; }
         if (k == "direction") { *v = dir; return true; }
+        if (k == "apl") { *v = lanes_apl(); return true; }
         return Model::get_option(key, v);
     }
 };

@@ -235,13 +235,16 @@ def test_sweep_full_c5_all_replicates_vs_oracle_golden():
 
 @pytest.mark.parametrize("n", [37, 129, 4_097, 100_003])
 @pytest.mark.parametrize("direction", [1, 2])
-def test_forced_direction_every_step_ragged(orc, n, direction):
+@pytest.mark.parametrize("apl", [1, 2, 4])
+def test_forced_direction_every_step_ragged(orc, n, direction, apl):
     # "direction" 1 = pull only, 2 = push whenever possible; both are the same
     # S3 draws, so each step must equal the oracle (128-agent chunks with a
     # ragged tail, one-step cooperative launches and multi-step launches)
     cfg = dict(n=n, mean_degree=6.0, beta=0.2, gamma=0.15, init_frac=0.05, seed=n % 97)
     m = make(cfg)
     m.set_option("direction", direction)
+    m.set_option("apl", apl)  # agents per lane of the step kernels
+    assert m.get_option("apl") == apl
     m.set_option("digest", 1)
     rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
     x = orc.sir_init(n, sir_counts(cfg)[1], cfg["seed"])
