@@ -33,9 +33,17 @@ void build_init_state(Runtime& rt, const std::vector<unsigned long long>& seeds,
 // col -> bitmap chain at large N).  test(j, e, owner) returns true for an arc
 // that sets the owner's bit; owners whose bit is set skip their remaining arcs
 // (early exit).  Returns the mask of owners with a set bit.  All 32 lanes call it.
-template <int kU, bool kPay, class C, class T>
+struct NoProbe {
+    __device__ __forceinline__ uint32_t operator()(uint32_t) const { return 1u; }
+};
+
+// probe(j) (optional) is the arc's neighbour lookup: it runs for all kU
+// batches before any test, so their kU x 32 loads are in flight together (a
+// load inside test() is ordered after the previous batch's branch on its own
+// load); test() then sees only arcs whose probe returned non-zero.
+template <int kU, bool kPay, class C, class P, class T>
 __device__ __forceinline__ uint32_t walk_rows_core(C&& col_at, uint32_t own, int32_t rb, int32_t re, uint32_t pay,
-                                                   T&& test)
+                                                   P&& probe, T&& test)
 {
     const int lane = threadIdx.x & 31;
     const int32_t len = ((own >> lane) & 1u) ? re - rb : 0;
@@ -76,12 +84,15 @@ __device__ __forceinline__ uint32_t walk_rows_core(C&& col_at, uint32_t own, int
         uint32_t js[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) js[u] = live[u] ? col_at(es[u]) : 0u;
+        uint32_t pb[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) pb[u] = live[u] ? probe(js[u]) : 0u;
         uint32_t add = 0;
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             bool h = false;
-            if constexpr (kPay) h = live[u] && test(js[u], es[u], Ls[u], ps[u]);
-            else h = live[u] && test(js[u], es[u], Ls[u]);
+            if constexpr (kPay) h = pb[u] && test(js[u], es[u], Ls[u], ps[u]);
+            else h = pb[u] && test(js[u], es[u], Ls[u]);
             if (h) add |= 1u << Ls[u];
         }
         hit |= __reduce_or_sync(0xffffffffu, add);
@@ -93,17 +104,17 @@ __device__ __forceinline__ uint32_t walk_rows_core(C&& col_at, uint32_t own, int
 template <int kU, class C, class T>
 __device__ __forceinline__ uint32_t walk_rows(C&& col_at, uint32_t own, int32_t rb, int32_t re, T&& test)
 {
-    return walk_rows_core<kU, false>(col_at, own, rb, re, 0u, test);
+    return walk_rows_core<kU, false>(col_at, own, rb, re, 0u, NoProbe{}, test);
 }
 
 // walk_rows with a per-owner payload: test(j, e, owner, pay_of_owner).  Used
 // when the owner lanes were compacted from several warp chunks (the owner's
 // agent id is no longer chunk base + lane).
-template <int kU, class C, class T>
+template <int kU, class C, class P, class T>
 __device__ __forceinline__ uint32_t walk_rows_pay(C&& col_at, uint32_t own, int32_t rb, int32_t re, uint32_t pay,
-                                                  T&& test)
+                                                  P&& probe, T&& test)
 {
-    return walk_rows_core<kU, true>(col_at, own, rb, re, pay, test);
+    return walk_rows_core<kU, true>(col_at, own, rb, re, pay, probe, test);
 }
 
 }  // namespace amber

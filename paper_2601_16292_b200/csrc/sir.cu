@@ -313,6 +313,8 @@ struct SirSmem {
 
 __host__ __device__ constexpr int64_t sir_chunks(int64_t n_pad, int apl) { return (n_pad + 32 * apl - 1) / (32 * apl); }
 
+// f(a0, next): next = the base of the chunk this warp processes after a0 when
+// it is already known (-1 otherwise), so the body can prefetch its inputs.
 template <int APL, class F>
 __device__ __forceinline__ void for_chunks(const SirStepArgs& a, uint32_t* q, F&& f)
 {
@@ -321,7 +323,7 @@ __device__ __forceinline__ void for_chunks(const SirStepArgs& a, uint32_t* q, F&
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     const int64_t nchunks = sir_chunks(a.n_pad, APL);
     if (!q || nw < kRegions) {
-        for (int64_t c = gw; c < nchunks; c += nw) f(c * 32 * APL);
+        for (int64_t c = gw; c < nchunks; c += nw) f(c * 32 * APL, c + nw < nchunks ? (c + nw) * 32 * APL : -1);
         return;
     }
     const int r = static_cast<int>(gw % kRegions);
@@ -332,7 +334,7 @@ __device__ __forceinline__ void for_chunks(const SirStepArgs& a, uint32_t* q, F&
         c0 = __shfl_sync(0xffffffffu, c0, 0);
         if (lo + c0 >= hi) break;
         const int64_t e = lo + c0 + a.grab < hi ? lo + c0 + a.grab : hi;
-        for (int64_t c = lo + c0; c < e; ++c) f(c * 32 * APL);
+        for (int64_t c = lo + c0; c < e; ++c) f(c * 32 * APL, c + 1 < e ? (c + 1) * 32 * APL : -1);
     }
 }
 
@@ -370,6 +372,24 @@ __device__ __forceinline__ void store_states(uint8_t* y, int64_t i0, uint32_t v)
     if constexpr (APL == 4) *reinterpret_cast<uint32_t*>(y + i0) = v;
     else if constexpr (APL == 2) *reinterpret_cast<uint16_t*>(y + i0) = static_cast<uint16_t>(v);
     else y[i0] = static_cast<uint8_t>(v);
+}
+
+// The lane's APL bits (agents a0 + APL*lane + k) of a bitmap whose word 0
+// holds agents a0 .. a0+31 (a0 a multiple of 32); the lanes of a word share
+// one load.
+template <int APL>
+__device__ __forceinline__ uint32_t lane_bits(const uint32_t* w0)
+{
+    const int lane = threadIdx.x & 31;
+    return (w0[(APL * lane) >> 5] >> ((APL * lane) & 31)) & ((1u << APL) - 1u);
+}
+
+// Bits of the lane's agents that are real (id < n); padding is neither S nor I.
+template <int APL>
+__device__ __forceinline__ uint32_t lane_real(int64_t i0, int64_t n)
+{
+    const int64_t r = n - i0;
+    return r >= APL ? (1u << APL) - 1u : (r <= 0 ? 0u : (1u << r) - 1u);
 }
 
 // Recovery draws of the lane's agents i0 .. i0+APL-1 (global ids; i0 is a
@@ -419,33 +439,23 @@ __device__ __forceinline__ uint32_t word_of(uint32_t nib)
     return v;
 }
 
-// Appends the lane's agents in `nib` (ids id_base + k) with their CSR rows to
-// the warp's owner queue at qn + rank; returns the number the warp appended.
-template <int APL>
-__device__ __forceinline__ uint32_t queue_owners(const SirStepArgs& a, SirSmem& sm, uint32_t qn, int64_t i0,
-                                                 uint32_t nib, int32_t id_base)
+// Appends the lane's agents in `nib` (ids id_base + k) with their CSR rows
+// (kRows; else the ids only) to the warp's owner queue at qn + rank; returns
+// the number the warp appended.
+template <int APL, bool kRows = true>
+__device__ __forceinline__ uint32_t queue_owners(SirSmem& sm, uint32_t qn, uint32_t nib, int32_t id_base,
+                                                 const int32_t* r = nullptr)
 {
     const int wq = threadIdx.x >> 5;
     uint32_t T;
     uint32_t k = qn + warp_excl(__popc(nib), &T);
+    if (!kRows) {
+#pragma unroll
+        for (int q = 0; q < APL; ++q)
+            if ((nib >> q) & 1u) sm.id[wq][k++] = id_base + q;
+        return T;
+    }
     if (nib) {
-        int32_t r[APL + 1];
-        if constexpr (APL == 4) {
-            if (i0 + 4 <= a.n) {
-                const int4 v = *reinterpret_cast<const int4*>(a.row_ptr + i0);
-                r[0] = v.x;
-                r[1] = v.y;
-                r[2] = v.z;
-                r[3] = v.w;
-                r[4] = a.row_ptr[i0 + 4];
-            } else {
-#pragma unroll
-                for (int q = 0; q < 5; ++q) r[q] = i0 + q <= a.n ? a.row_ptr[i0 + q] : 0;
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q <= APL; ++q) r[q] = i0 + q <= a.n ? a.row_ptr[i0 + q] : 0;
-        }
 #pragma unroll
         for (int q = 0; q < APL; ++q)
             if ((nib >> q) & 1u) {
@@ -458,13 +468,45 @@ __device__ __forceinline__ uint32_t queue_owners(const SirStepArgs& a, SirSmem& 
     return T;
 }
 
+// Inputs of a pull chunk: the lane's S and I bitmap words (L2) and its CSR
+// row offsets (HBM), all issued together.  (Loading them one chunk ahead
+// through for_chunks' `next` measured slower: register spills at 64.)
+template <int APL>
+struct PullIn {
+    uint32_t ws, wi;
+    int32_t r[APL + 1];
+};
+
+template <int APL>
+__device__ __forceinline__ void pull_load(const SirStepArgs& a, int64_t a0, const uint32_t* sb, const uint32_t* ib,
+                                          PullIn<APL>& p)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t i0 = a0 + APL * lane;
+    p.ws = sb[(a0 >> 5) + ((APL * lane) >> 5)];
+    p.wi = ib[((a.gid0 + static_cast<unsigned long long>(a0)) >> 5) + ((APL * lane) >> 5)];
+    if constexpr (APL == 4) {
+        if (i0 + 4 <= a.n) {
+            const int4 v = *reinterpret_cast<const int4*>(a.row_ptr + i0);
+            p.r[0] = v.x;
+            p.r[1] = v.y;
+            p.r[2] = v.z;
+            p.r[3] = v.w;
+            p.r[4] = a.row_ptr[i0 + 4];
+            return;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q <= APL; ++q) p.r[q] = i0 + q <= a.n ? a.row_ptr[i0 + q] : 0;
+}
+
 // Pull step for the 32 * APL agents of chunk a0: the susceptible agents,
 // compacted into groups of 32 owners, walk their rows warp-cooperatively; an
 // arc transmits iff the neighbour is I (bitmap, L2-resident) and the
 // pair-keyed Bernoulli (S3) fires.  Writes the next state and the next bitmap
 // words and adds the S/I/R counts (and digest terms) of the new states to cnt.
 template <int APL>
-__device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0, const uint8_t* __restrict__ x,
+__device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0, const PullIn<APL>& in,
                                                uint8_t* __restrict__ y, const uint32_t* __restrict__ ib,
                                                uint32_t* __restrict__ ib_next, uint32_t* __restrict__ sb_next,
                                                uint32_t t, SirSmem& sm, unsigned long long (&cnt)[4])
@@ -473,19 +515,17 @@ __device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0,
     const int lane = threadIdx.x & 31;
     const int wq = threadIdx.x >> 5;
     const int64_t i0 = a0 + APL * lane;
-    const uint32_t xw = load_states<APL>(x, i0);
-    uint32_t nib_s = 0, nib_i = 0, nib_r = 0;
-#pragma unroll
-    for (int k = 0; k < APL; ++k) {
-        const uint32_t st = (xw >> (8 * k)) & 0xffu;
-        nib_s |= (st == kS ? 1u : 0u) << k;
-        nib_i |= (st == kI ? 1u : 0u) << k;
-        nib_r |= (st == kR ? 1u : 0u) << k;
-    }
+    // the current state from the bitmaps (L2-resident; the state bytes are
+    // only written): own I bits from the global I bitmap (sharded: ib is
+    // global, gid0 a multiple of 32), S bits from the local S bitmap
+    // (sharded: a chunk may reach past the shard into the next rank's bits)
+    const uint32_t real = lane_real<APL>(i0, a.n);
+    const uint32_t nib_s = (in.ws >> ((APL * lane) & 31)) & kM & real;
+    const uint32_t nib_i = (in.wi >> ((APL * lane) & 31)) & kM & real;
     uint32_t hitnib = 0;
     if (__any_sync(0xffffffffu, nib_s != 0)) {
         if (lane < APL) sm.h[wq][lane] = 0u;
-        const uint32_t T = queue_owners<APL>(a, sm, 0, i0, nib_s, APL * lane);
+        const uint32_t T = queue_owners<APL>(sm, 0, nib_s, APL * lane, in.r);
         __syncwarp();
         for (uint32_t g0 = 0; g0 < T; g0 += 32) {
             const uint32_t nown = T - g0 < 32 ? T - g0 : 32;
@@ -496,8 +536,8 @@ __device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0,
             const uint32_t sid = static_cast<uint32_t>(a.gid0 + static_cast<unsigned long long>(a0 + lid));
             const uint32_t hit = walk_rows_pay<kWalkU>(
                 [&](int32_t e) { return static_cast<uint32_t>(__ldcs(a.col + e)); }, own, rb, re, sid,
+                [&](uint32_t j) { return static_cast<uint32_t>(bit_of(ib, j)); },  // j: global id (global bitmap)
                 [&](uint32_t j, int32_t, int, uint32_t s) {
-                    if (!bit_of(ib, j)) return false;  // j is a global id (the bitmap is global)
                     const uint4 w = philox(make_uint4(min(s, j), max(s, j), t, TAG_SIR_TX), a.key);
                     return static_cast<unsigned long long>(w.x) < a.t_beta;
                 });
@@ -508,12 +548,13 @@ __device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0,
         __syncwarp();  // the next chunk rewrites the queue and h
     }
     const uint32_t recnib = recover_nib<APL>(a, a.gid0 + static_cast<unsigned long long>(i0), t, nib_i);
-    const uint32_t s2 = nib_s & ~hitnib, i2 = (nib_s & hitnib) | (nib_i & ~recnib), r2 = nib_r | recnib;
-    uint32_t yw = xw;
+    const uint32_t s2 = nib_s & ~hitnib, i2 = (nib_s & hitnib) | (nib_i & ~recnib), r2 = real & ~s2 & ~i2;
+    uint32_t yw = 0;
 #pragma unroll
-    for (int k = 0; k < APL; ++k)
-        if ((((nib_s & hitnib) | recnib) >> k) & 1u)
-            yw = (yw & ~(0xffu << (8 * k))) | (static_cast<uint32_t>((i2 >> k) & 1u ? kI : kR) << (8 * k));
+    for (int k = 0; k < APL; ++k) {
+        const uint32_t st = (s2 >> k) & 1u ? kS : ((i2 >> k) & 1u ? kI : ((r2 >> k) & 1u ? kR : kPad));
+        yw |= st << (8 * k);
+    }
     store_states<APL>(y, i0, yw);
     const uint32_t wi = word_of<APL>(i2), ws = word_of<APL>(s2);
     if ((lane & (32 / APL - 1)) == 0) {
@@ -535,8 +576,10 @@ template <int APL>
 __device__ __forceinline__ void sir_pull_body(const SirStepArgs& a, int c, uint32_t t, SirSmem& sm,
                                               unsigned long long (&cnt)[4])
 {
-    for_chunks<APL>(a, queue_of(a, t, 0), [&](int64_t a0) {
-        sir_pull_chunk<APL>(a, a0, a.x[c], a.x[c ^ 1], a.ib[c], a.ib[c ^ 1], a.sb[c ^ 1], t, sm, cnt);
+    for_chunks<APL>(a, queue_of(a, t, 0), [&](int64_t a0, int64_t) {
+        PullIn<APL> in;
+        pull_load<APL>(a, a0, a.sb[c], a.ib[c], in);
+        sir_pull_chunk<APL>(a, a0, in, a.x[c ^ 1], a.ib[c], a.ib[c ^ 1], a.sb[c ^ 1], t, sm, cnt);
     });
 }
 
@@ -592,7 +635,7 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
 {
     const int lane = threadIdx.x & 31;
     const int wq = threadIdx.x >> 5;
-    const uint8_t* __restrict__ x = a.x[c];
+    const uint32_t* __restrict__ ib = a.ib[c];
     const uint32_t* __restrict__ sb = a.sb[c];
     uint32_t* ib_next = a.ib[c ^ 1];
     uint32_t* sb_next = a.sb[c ^ 1];
@@ -600,13 +643,15 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
     uint32_t* yw = reinterpret_cast<uint32_t*>(y);
     uint32_t qn = 0;  // queued pushers (warp-uniform; < 32 between chunks)
     auto walk = [&](uint32_t g0, uint32_t nown) {
+        // rows are loaded here, 32 owners at a time, not per chunk: one row_ptr
+        // round trip per walk instead of one per chunk with an infected agent
         const bool mine = static_cast<uint32_t>(lane) < nown;
-        const int32_t rb = mine ? sm.rb[wq][g0 + lane] : 0, re = mine ? sm.re[wq][g0 + lane] : 0;
         const uint32_t id = mine ? static_cast<uint32_t>(sm.id[wq][g0 + lane]) : 0u;
+        const int32_t rb = mine ? a.row_ptr[id] : 0, re = mine ? a.row_ptr[id + 1] : 0;
         const uint32_t own = nown >= 32 ? 0xffffffffu : ((1u << nown) - 1u);
         walk_rows_pay<kWalkU>([&](int32_t e) { return static_cast<uint32_t>(__ldcs(a.col + e)); }, own, rb, re, id,
+                              [&](uint32_t j) { return static_cast<uint32_t>(bit_of(sb, j)); },
                               [&](uint32_t j, int32_t, int, uint32_t s) {
-            if (!bit_of(sb, j)) return false;
             const uint4 wd = philox(make_uint4(min(s, j), max(s, j), t, TAG_SIR_TX), a.key);
             if (static_cast<unsigned long long>(wd.x) < a.t_beta) {
                 const uint32_t bit = 1u << (j & 31u);
@@ -621,17 +666,18 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
             return false;  // an infected agent tries every susceptible neighbour
         });
     };
-    for_chunks<APL>(a, queue_of(a, t, 1), [&](int64_t a0) {
+    for_chunks<APL>(a, queue_of(a, t, 1), [&](int64_t a0, int64_t) {
         const int64_t i0 = a0 + APL * lane;
-        const uint32_t xw = load_states<APL>(x, i0);
-        uint32_t nib_s = 0, nib_i = 0, nons = 0;
-#pragma unroll
-        for (int k = 0; k < APL; ++k) {
-            const uint32_t st = (xw >> (8 * k)) & 0xffu;
-            nib_s |= (st == kS ? 1u : 0u) << k;
-            nib_i |= (st == kI ? 1u : 0u) << k;
-            nons |= (st == kI || st == kR ? 1u : 0u) << k;  // pads are neither
-        }
+        // current state and back state B from the bitmaps (L2-resident, four
+        // independent loads): no state byte is read.  B's bits of a non-S agent
+        // are only changed by this lane (pushers touch agents that are S now).
+        constexpr uint32_t kM = (1u << APL) - 1u;
+        const int64_t wl = (a0 >> 5) + ((APL * lane) >> 5);  // the lane's bitmap word
+        const uint32_t sh = (APL * lane) & 31;
+        const uint32_t Ws = sb[wl], Wi = ib[wl], Wbs = sb_next[wl], Wbi = ib_next[wl];
+        const uint32_t nib_s = (Ws >> sh) & kM, nib_i = (Wi >> sh) & kM;
+        const uint32_t b_s = (Wbs >> sh) & kM, b_i = (Wbi >> sh) & kM;
+        const uint32_t nons = lane_real<APL>(i0, a.n) & ~nib_s;
         if (a.digest && nib_s) {
 #pragma unroll
             for (int k = 0; k < APL; ++k)
@@ -644,44 +690,37 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
         if (nons) {
             // the lane's bytes sit in one 32-bit word (i0 is a multiple of APL)
             const uint32_t sh0 = static_cast<uint32_t>(i0 & 3) * 8u;
-            const uint32_t yold = yw[i0 >> 2] >> sh0;
             uint32_t delta = 0;
 #pragma unroll
             for (int k = 0; k < APL; ++k)
                 if ((nons >> k) & 1u) {
-                    const uint32_t nw = (recnib >> k) & 1u ? kR : (xw >> (8 * k)) & 0xffu;
-                    delta += (nw - ((yold >> (8 * k)) & 0xffu)) << (8 * k);  // mod 2^32: bytes stay in 0..3
+                    const uint32_t nw = ((nib_i & ~recnib) >> k) & 1u ? kI : kR;
+                    const uint32_t old = (b_s >> k) & 1u ? kS : ((b_i >> k) & 1u ? kI : kR);
+                    delta += (nw - old) << (8 * k);  // mod 2^32: bytes stay in 0..3
                     if (a.digest) dig += digest_term(static_cast<unsigned long long>(i0 + k), nw);
                 }
             if (delta) atomicAdd(yw + (i0 >> 2), delta << sh0);
         }
         const uint32_t wsurv = word_of<APL>(nib_i & ~recnib), wnons = word_of<APL>(nons);
+        // B's bits of the non-S agents -> survivors / cleared S (B's words
+        // as loaded above: exact on the non-S bits, which only this group changes)
         if ((lane & (32 / APL - 1)) == 0 && wnons) {
-            const int64_t w = (a0 >> 5) + lane / (32 / APL);
-            const uint32_t flip = (ib_next[w] ^ wsurv) & wnons;
-            if (flip) atomicXor(ib_next + w, flip);
-            if (sb_next[w] & wnons) atomicAnd(sb_next + w, ~wnons);
+            const uint32_t flip = (Wbi ^ wsurv) & wnons;
+            if (flip) atomicXor(ib_next + wl, flip);
+            if (Wbs & wnons) atomicAnd(sb_next + wl, ~wnons);
         }
         // pushers: queue, walk whenever 32 are queued
         if (!__any_sync(0xffffffffu, nib_i != 0)) return;
-        qn += queue_owners<APL>(a, sm, qn, i0, nib_i, static_cast<int32_t>(i0));
+        qn += queue_owners<APL, false>(sm, qn, nib_i, static_cast<int32_t>(i0));
         __syncwarp();
         if (qn < 32) return;
         uint32_t g0 = 0;
         for (; qn - g0 >= 32; g0 += 32) walk(g0, 32);
         const uint32_t rem = qn - g0;
-        int32_t vi = 0, vb = 0, ve = 0;
-        if (static_cast<uint32_t>(lane) < rem) {
-            vi = sm.id[wq][g0 + lane];
-            vb = sm.rb[wq][g0 + lane];
-            ve = sm.re[wq][g0 + lane];
-        }
+        int32_t vi = 0;
+        if (static_cast<uint32_t>(lane) < rem) vi = sm.id[wq][g0 + lane];
         __syncwarp();
-        if (static_cast<uint32_t>(lane) < rem) {
-            sm.id[wq][lane] = vi;
-            sm.rb[wq][lane] = vb;
-            sm.re[wq][lane] = ve;
-        }
+        if (static_cast<uint32_t>(lane) < rem) sm.id[wq][lane] = vi;
         __syncwarp();
         qn = rem;
     });
@@ -824,7 +863,7 @@ public:
             AMBER_CUDA(cudaMemsetAsync(x[0].p, kPad, npl, rt.stream));
             if (nl) AMBER_CUDA(cudaMemcpyAsync(x[0].p, full.p + lo, nl, cudaMemcpyDeviceToDevice, rt.stream));
             slice_graph();
-            ib_glob.allocate(&rt, static_cast<size_t>(rt.world) * (shard / 32));
+            ib_glob.allocate(&rt, static_cast<size_t>(rt.world) * (shard / 32) + kChunkMax / 32);  // + one chunk of slack
             sc = make_shard_comm(rt, r);
             AMBER_CUDA(cudaStreamSynchronize(rt.stream));
         } else {
