@@ -279,7 +279,7 @@ int amber_digest(amber_model* m, const char* name, uint64_t* out);
  * (wealth/SIR: 1 = all steps of a call in one launch (single-CTA kernel for
  * wealth N <= 16384; cooperative direction-optimizing kernel for SIR),
  * 0 = one launch per step, pull only for SIR), SIR "direction" (0 = choose
- * per step, push when I < S; 1 = always pull; 2 = push whenever the previous
+ * per step, push when 4I < 3S; 1 = always pull; 2 = push whenever the previous
  * counts are known -- identical results, for tests and probes; 1 or 2 also
  * run a single step through the cooperative kernel); Boids: "lanes" (1/4/8/16 lanes
  * per agent in the stencil), "tiled", "fused" (measured alternatives).

@@ -288,6 +288,10 @@ constexpr int kWalkU = AMBER_SIR_WALK_U;  // 32-arc batches in flight per warp (
 #define AMBER_SIR_PT 256
 #endif
 constexpr int kSirPT = AMBER_SIR_PT;  // threads per block of the persistent kernel
+#ifndef AMBER_SIR_MINB
+#define AMBER_SIR_MINB (1024 / AMBER_SIR_PT)
+#endif
+constexpr int kSirMinB = AMBER_SIR_MINB;  // min resident blocks per SM (register cap 64 at 256 threads)
 
 // Warp chunks of 32 * APL agents: lane L holds agents APL*L .. APL*L+APL-1 of
 // the chunk (one load of its state bytes; for APL = 4 one Philox block serves
@@ -729,11 +733,11 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
 
 // All n_steps steps in one cooperative launch (grid barrier between steps).
 // Direction-optimizing: step k pushes from the infected agents when they are
-// fewer than the susceptible ones (counts of the previous step from its ring
+// fewer than 3/4 of the susceptible ones (counts of the previous step from its ring
 // slot, so every block takes the same decision), otherwise it pulls.  Both
 // directions give identical results (S3); the tests check it.
 template <int APL>
-__global__ void __launch_bounds__(kSirPT, 1024 / kSirPT) sir_persistent_kernel(const SirStepArgs a)
+__global__ void __launch_bounds__(kSirPT, kSirMinB) sir_persistent_kernel(const SirStepArgs a)
 {
     __shared__ SirSmem sm;
     cg::grid_group grid = cg::this_grid();
@@ -750,7 +754,10 @@ __global__ void __launch_bounds__(kSirPT, 1024 / kSirPT) sir_persistent_kernel(c
             prev_s = pv->S;
             prev_i = pv->I;
             prev_r = pv->R;
-            push = a.dir == 0 ? prev_i < prev_s : a.dir == 2;
+            // per traversed agent a push costs ~1.35x a pull (every arc of a
+            // pusher is walked, with a draw per S neighbour; pullers stop at
+            // their first transmission): V2, tools/v2_steps.py
+            push = a.dir == 0 ? 4 * prev_i < 3 * prev_s : a.dir == 2;
         }
         if (push) {
             long long rec = 0, inf = 0;
