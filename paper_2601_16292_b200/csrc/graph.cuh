@@ -107,6 +107,15 @@ __device__ __forceinline__ uint32_t walk_rows(C&& col_at, uint32_t own, int32_t 
     return walk_rows_core<kU, false>(col_at, own, rb, re, 0u, NoProbe{}, test);
 }
 
+// walk_rows with a neighbour probe (see walk_rows_core): test(j, e, owner)
+// runs only where probe(j) != 0.
+template <int kU, class C, class P, class T>
+__device__ __forceinline__ uint32_t walk_rows_probe(C&& col_at, uint32_t own, int32_t rb, int32_t re, P&& probe,
+                                                    T&& test)
+{
+    return walk_rows_core<kU, false>(col_at, own, rb, re, 0u, probe, test);
+}
+
 // walk_rows with a per-owner payload: test(j, e, owner, pay_of_owner).  Used
 // when the owner lanes were compacted from several warp chunks (the owner's
 // agent id is no longer chunk base + lane).

@@ -141,8 +141,9 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
                     const uint32_t own = __ballot_sync(0xffffffffu, is_i);
                     if (!own) continue;
                     const int32_t rb = is_i ? static_cast<int32_t>(rp[i]) : 0, re = is_i ? static_cast<int32_t>(rp[i + 1]) : 0;
-                    walk_rows<1>(col_at, own, rb, re, [&](uint32_t j, int32_t, int L) {
-                        if (x[j] != kS || y[j] != kS) return false;  // y: already hit this step
+                    walk_rows_probe<1>(col_at, own, rb, re,
+                                       [&](uint32_t j) { return static_cast<uint32_t>(x[j] == kS && y[j] == kS); },
+                                       [&](uint32_t j, int32_t, int L) {  // y: already hit this step
                         const uint32_t ii = static_cast<uint32_t>(a0 + L);
                         const uint4 w = philox(make_uint4(min(ii, j), max(ii, j), static_cast<uint32_t>(t), TAG_SIR_TX), key);
                         if (static_cast<unsigned long long>(w.x) < tb) y[j] = kI;
@@ -167,8 +168,9 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
                     if (s_mask) {
                         const bool mine = (s_mask >> lane) & 1u;
                         const int32_t rb = mine ? static_cast<int32_t>(rp[i]) : 0, re = mine ? static_cast<int32_t>(rp[i + 1]) : 0;
-                        hit = walk_rows<1>(col_at, s_mask, rb, re, [&](uint32_t j, int32_t, int L) {
-                            if (x[j] != kI) return false;
+                        hit = walk_rows_probe<1>(col_at, s_mask, rb, re,
+                                                 [&](uint32_t j) { return static_cast<uint32_t>(x[j] == kI); },
+                                                 [&](uint32_t j, int32_t, int L) {
                             const uint32_t ii = static_cast<uint32_t>(a0 + L);
                             const uint4 w = philox(make_uint4(min(ii, j), max(ii, j), static_cast<uint32_t>(t), TAG_SIR_TX), key);
                             return static_cast<unsigned long long>(w.x) < tb;
