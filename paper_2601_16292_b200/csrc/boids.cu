@@ -520,7 +520,8 @@ template <int G>
 __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sorted, const int32_t* __restrict__ sids,
                                                  const int* __restrict__ start, int64_t n, const BoidsArgs& a,
                                                  float4* __restrict__ out, int32_t* __restrict__ out_ids, BoidsSlot* slot,
-                                                 int digest)
+                                                 int digest, int* __restrict__ next_cnt = nullptr,
+                                                 int* __restrict__ next_cell = nullptr)
 {
     static_assert(G >= 4, "the update spreads four divisions over the group's lanes");
     const float L = a.L, halfL = __fmul_rn(0.5f, a.L), R2 = __fmul_rn(a.R, a.R), rs2 = __fmul_rn(a.rs, a.rs);
@@ -609,6 +610,7 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
         }
         const float cohx = __shfl_sync(0xffffffffu, mv, 0, G), cohy = __shfl_sync(0xffffffffu, mv, 1, G);
         const float avx = __shfl_sync(0xffffffffu, mv, 2, G), avy = __shfl_sync(0xffffffffu, mv, 3, G);
+        int ncell_of = -1;  // the agent's cell in the next step's binning (next_cnt)
         if (active) {
             const float4 nx = boid_update_means(me, acc, cohx, cohy, avx, avy, a);
             if (sub == 0) {
@@ -616,6 +618,10 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
                 const int32_t id = sids[p];
                 out_ids[p] = id;
                 if (digest) dig += digest_term(static_cast<unsigned long long>(id), __float_as_uint(nx.x));
+                if (next_cnt) {
+                    ncell_of = cell_coord(nx.y, a) * a.nc + cell_coord(nx.x, a);
+                    next_cell[p] = ncell_of;
+                }
             }
             // observables (B8) in double, one per lane
             if (sub < 3) {
@@ -627,6 +633,22 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
                     else uy_sum += __ddiv_rn(dvy, sp);
                 }
             }
+        }
+        if (next_cnt) {
+            // the next step's cell counts (fused count pass): the warp's agents
+            // (lanes 0, G, 2G, ...) are consecutive in cell order and mostly stay
+            // in their cell, so a run of equal cells is one atomic by its head
+            const int lane = threadIdx.x & 31;
+            const int prev = __shfl_up_sync(0xffffffffu, ncell_of, G);
+            int run = 1;
+            bool more = true;
+#pragma unroll
+            for (int k = 1; k < 32 / G; ++k) {
+                const int nx = __shfl_down_sync(0xffffffffu, ncell_of, k * G);
+                more = more && lane + k * G < 32 && nx == ncell_of;
+                run += more ? 1 : 0;
+            }
+            if (ncell_of >= 0 && (lane < G || prev != ncell_of)) atomicAdd(next_cnt + ncell_of, run);
         }
     }
     __shared__ double red[3][8];
@@ -664,9 +686,10 @@ template <int G>
 __global__ void __launch_bounds__(256, 4) boids_group_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ sids,
                                                           const int* __restrict__ start, int64_t n, BoidsArgs a,
                                                           float4* __restrict__ out, int32_t* __restrict__ out_ids,
-                                                          BoidsSlot* slot, int digest)
+                                                          BoidsSlot* slot, int digest, int* __restrict__ next_cnt,
+                                                          int* __restrict__ next_cell)
 {
-    boids_group_body<G>(sorted, sids, start, n, a, out, out_ids, slot, digest);
+    boids_group_body<G>(sorted, sids, start, n, a, out, out_ids, slot, digest, next_cnt, next_cell);
 }
 
 // All steps of a call in ONE cooperative launch: per step, bin counts ->
@@ -1088,6 +1111,7 @@ public:
     int64_t tiled = 0;  // 1: shared-memory tiled stencil kernel (slower once flocks cluster)
     int64_t lanes = 8;  // lanes per agent in the stencil scan (1 = one-lane kernel; 4, 8, 16)
     int64_t fused = 0;  // 1: all phases of all steps in one cooperative launch (measured slower, r01)
+    bool counted = false;  // cnt / cell_of hold the cell counts of the current state (from the last group step)
 
     BoidsModel(int64_t n_, const amber_boids_params& p_, uint64_t seed_, const amber_runtime* r)
     {
@@ -1158,6 +1182,8 @@ public:
     {
         AMBER_REQUIRE(nsteps >= 0, "n_steps must be >= 0");
         if (fused && ba.nc >= 3 && !tiled && lanes == 8 && nsteps > 0) {
+            // the cooperative kernel counts from zeroed counters
+            if (counted) AMBER_CUDA(cudaMemsetAsync(cnt.p, 0, static_cast<size_t>(ncell) * sizeof(int), rt.stream));
             int64_t done = 0;
             while (done < nsteps) {
                 const int64_t chunk = std::min<int64_t>(nsteps - done, metrics_cap);
@@ -1180,13 +1206,16 @@ public:
                 t += chunk;
                 done += chunk;
             }
+            counted = false;
             return;
         }
         const int threads = block ? static_cast<int>(std::min<int64_t>(block, 256)) : 256;
         for (int64_t k = 0; k < nsteps; ++k) {
-            if (ba.nc == 1) {
-                boids_zero_slots<<<1, 32, 0, rt.stream>>>(ring.p, metrics_cap, t, 1);
+            if (k % metrics_cap == 0) {  // this call's records, a ring's worth at a time
+                boids_zero_slots<<<1, 256, 0, rt.stream>>>(ring.p, metrics_cap, t, std::min(nsteps - k, metrics_cap));
                 check_launch("boids_zero_slots");
+            }
+            if (ba.nc == 1) {
                 // degenerate small box: one cell holding every agent (the stencil
                 // visits it once); count = n, start = {0, n}
                 const int h[2] = {0, static_cast<int>(n)};
@@ -1194,11 +1223,15 @@ public:
                 AMBER_CUDA(cudaMemcpyAsync(sorted.p, st.p, n * sizeof(float4), cudaMemcpyDeviceToDevice, rt.stream));
                 AMBER_CUDA(cudaMemcpyAsync(sids.p, ids.p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, rt.stream));
             } else {
-                prof.launch(rt.stream, "boids_bin", [&] {
-                    boids_count_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(st.p, n, ba, cnt.p, cell_of.p,
-                                                                                     ring.p + (t % metrics_cap));
-                });
-                check_launch("boids_count_kernel");
+                // the cell counts: from the previous group step (fused), else a count pass
+                if (!counted) {
+                    prof.launch(rt.stream, "boids_bin", [&] {
+                        boids_count_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(st.p, n, ba, cnt.p, cell_of.p,
+                                                                                         nullptr);
+                    });
+                    check_launch("boids_count_kernel");
+                }
+                counted = false;
                 // exclusive scan of the ncell + 1 counts (cnt[ncell] = 0, so start[ncell] = n),
                 // cursors = starts, counts re-zeroed for the next step: one CTA for small
                 // grids, a device-wide scan for large ones (the one-CTA scan took 20 ms at
@@ -1245,14 +1278,23 @@ public:
                 BoidsSlot* sl = ring.p + (t % metrics_cap);
                 const int dg = digest_on ? 1 : 0;
                 prof.launch(rt.stream, "boids_step", [&] {
+                    // small populations: the group step also counts the next step's
+                    // cells (one launch less per step: C3 83 -> 75 us); large ones keep
+                    // the streaming count pass (the stencil kernel is issue-bound there:
+                    // fused, V3 32.8 -> 33.7 ms)
+                    int* nc_cnt = ba.nc > 1 && n <= (1ll << 22) ? cnt.p : nullptr;
                     if (lanes == 4)
-                        boids_group_kernel<4><<<g, threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a, st.p, ids.p, sl, dg);
+                        boids_group_kernel<4><<<g, threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a, st.p, ids.p,
+                                                                            sl, dg, nc_cnt, cell_of.p);
                     else if (lanes == 16)
-                        boids_group_kernel<16><<<g, threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a, st.p, ids.p, sl, dg);
+                        boids_group_kernel<16><<<g, threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a, st.p, ids.p,
+                                                                             sl, dg, nc_cnt, cell_of.p);
                     else
-                        boids_group_kernel<8><<<g, threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a, st.p, ids.p, sl, dg);
+                        boids_group_kernel<8><<<g, threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a, st.p, ids.p,
+                                                                            sl, dg, nc_cnt, cell_of.p);
                 });
                 check_launch("boids_group_kernel");
+                counted = ba.nc > 1 && n <= (1ll << 22);
             }
             ++t;
         }
@@ -1297,7 +1339,11 @@ public:
         copy_in(rt, col_tmp.p, src, n * 4, on_dev);
         boids_put_column<<<grid_for(256), 256, 0, rt.stream>>>(st.p, ids.p, n, k, col_tmp.p);
         check_launch("boids_put_column");
+        // positions changed: drop the counts the last group step left (the next
+        // step counts again from zero)
+        if (counted) AMBER_CUDA(cudaMemsetAsync(cnt.p, 0, static_cast<size_t>(ncell) * sizeof(int), rt.stream));
         AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        counted = false;
     }
 
     void read_metrics(const char* name, void* dst, size_t bytes, int64_t* n_out) override

@@ -177,3 +177,29 @@ def test_large_grid_device_scan_and_edges(orc):
         st = orc.boids_step(st, P)
     for a, b in zip(state(m), st):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_fused_counts_across_calls_options_and_writes(orc):
+    # the group step counts the next step's cells (small N): the counts must stay
+    # valid across step calls, option switches (lanes, tiled, fused) and column
+    # writes -- every step against the oracle, bit for bit
+    cfg = dict(C3_BOIDS, n=6_001, L=250.0, seed=29)
+    m = make(cfg)
+    P = oparams(orc, cfg)
+    st = state(m)
+    plan = [(2, {}), (1, {"lanes": 4}), (2, {"lanes": 8}), (1, {"tiled": 1}), (2, {"tiled": 0}),
+            (2, {"fused": 1}), (1, {"fused": 0}), ("write", None), (3, {})]
+    for k, opts in plan:
+        if k == "write":
+            vx = (st[2] * np.float32(0.75)).astype(np.float32)
+            m.write_column("vel_x", vx)
+            st = (st[0], st[1], vx, st[3])
+            continue
+        for key, v in opts.items():
+            m.set_option(key, v)
+        m.step(k)
+        for _ in range(k):
+            st = orc.boids_step(st, P)
+        for a, b in zip(state(m), st):
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert m.metrics("mean_speed").shape[0] >= 1
