@@ -91,21 +91,21 @@ __global__ void boids_count_kernel(const float4* __restrict__ st, int64_t n, Boi
     }
 }
 
-// Exclusive scan of the cell counts by one CTA: each thread owns a contiguous
-// run of cells (sequential sum), one block-wide scan of the run totals, then a
-// sequential write-back.  Also zeroes the counts for the next step.
-// One CTA: warp w owns a contiguous segment of cells, read 32 at a time
-// (coalesced).  Pass 1 sums each segment, warp 0 scans the 32 segment totals,
-// pass 2 re-walks each segment with a warp inclusive scan plus a running carry
-// and writes start / cursor and the zeroed counts.
-__global__ void __launch_bounds__(1024) boids_scan_kernel(int* cnt, int* start, int* cursor, int ncell)
+// Exclusive scan of the cell counts by one CTA (ncell <= 2^16): warp w owns a
+// contiguous segment of cells, read 32 at a time (coalesced).  Pass 1 sums each
+// segment, warp 0 scans the 32 segment totals, pass 2 re-walks each segment
+// with warp inclusive scans plus a running carry, its loads issued eight
+// batches at a time (restrict pointers: nothing aliases the counts, which the
+// scatter kernel zeroes afterwards), and writes start / cursor.
+__global__ void __launch_bounds__(1024) boids_scan_kernel(const int* __restrict__ cnt, int* __restrict__ start,
+                                                          int* __restrict__ cursor, int ncell)
 {
     __shared__ int seg_off[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int per = ((ncell + 31) / 32 + 31) & ~31;  // cells per warp segment (multiple of 32)
     const int s0 = warp * per, s1 = min(s0 + per, ncell);
     int sum = 0;
-#pragma unroll 4
+#pragma unroll 8
     for (int c = s0 + lane; c < s1; c += 32) sum += cnt[c];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -124,29 +124,40 @@ __global__ void __launch_bounds__(1024) boids_scan_kernel(int* cnt, int* start, 
     }
     __syncthreads();
     int carry = seg_off[warp];
-    for (int b = s0; b < s1; b += 32) {
-        const int c = b + lane;
-        const int v = c < s1 ? cnt[c] : 0;
-        int incl = v;
+    for (int b = s0; b < s1; b += 32 * 8) {
+        int v[8];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int u = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += u;
+        for (int j = 0; j < 8; ++j) {
+            const int c = b + 32 * j + lane;
+            v[j] = c < s1 ? cnt[c] : 0;
         }
-        if (c < s1) {
-            start[c] = carry + incl - v;
-            cursor[c] = carry + incl - v;
-            cnt[c] = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = b + 32 * j + lane;
+            int incl = v[j];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            if (c < s1) {
+                start[c] = carry + incl - v[j];
+                cursor[c] = carry + incl - v[j];
+            }
+            carry += __shfl_sync(0xffffffffu, incl, 31);
         }
-        carry += __shfl_sync(0xffffffffu, incl, 31);
     }
 }
 
+// Counting-sort scatter; also zeroes the cell counts for the next count pass
+// (ncell_zero cells; 0 when the counts were cleared otherwise).
 __global__ void boids_scatter_kernel(const float4* __restrict__ st, const int32_t* __restrict__ ids, int64_t n,
                                      const int* __restrict__ cell_of, int* __restrict__ cursor, float4* __restrict__ sorted,
-                                     int32_t* __restrict__ sorted_ids)
+                                     int32_t* __restrict__ sorted_ids, int* __restrict__ cnt, int ncell_zero)
 {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t c = tid; c < ncell_zero; c += nt) cnt[c] = 0;
+    for (int64_t p = tid; p < n; p += nt) {
         const int q = atomicAdd(cursor + cell_of[p], 1);
         sorted[q] = st[p];
         sorted_ids[q] = ids[p];
@@ -1249,8 +1260,8 @@ public:
                 });
                 check_launch("boids_scan");
                 prof.launch(rt.stream, "boids_scatter", [&] {
-                    boids_scatter_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(st.p, ids.p, n, cell_of.p,
-                                                                                       cursor.p, sorted.p, sids.p);
+                    boids_scatter_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(
+                        st.p, ids.p, n, cell_of.p, cursor.p, sorted.p, sids.p, cnt.p, ncell <= (1 << 16) ? ncell : 0);
                 });
                 check_launch("boids_scatter_kernel");
             }
