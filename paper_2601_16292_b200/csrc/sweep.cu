@@ -49,6 +49,25 @@ struct SweepArgs {
     int64_t col_cap;         // u16 entries reserved in shared memory
 };
 
+// Appends the agents a0 + b for the set bits b of `mask` to the warp's owner
+// queue (lane k holds the k-th queued agent in qid; qc = queued count), and
+// walks 32 of them as soon as 32 are queued.  All 32 lanes call it.
+template <class W>
+__device__ __forceinline__ void enqueue(uint32_t mask, uint32_t a0, uint32_t& qid, uint32_t& qc, W&& walk)
+{
+    const uint32_t lane = threadIdx.x & 31, k = __popc(mask);
+    if (!k) return;
+    if (lane >= qc && lane < qc + k) qid = a0 + __fns(mask, 0, static_cast<int>(lane - qc + 1));
+    if (qc + k < 32) {
+        qc += k;
+        return;
+    }
+    walk(32u);
+    const uint32_t rem = qc + k - 32;
+    if (lane < rem) qid = a0 + __fns(mask, 0, static_cast<int>(32 - qc + lane + 1));
+    qc = rem;
+}
+
 template <bool COL_SMEM>
 __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
 {
@@ -133,49 +152,63 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
                     reinterpret_cast<uchar4*>(y)[q] = make_uchar4(o[0], o[1], o[2], o[3]);
                 }
                 __syncthreads();
-                // warp-cooperative: the infected lanes of each 32-agent chunk walk their
-                // concatenated rows (graph.cuh walk_rows), so all lanes work on arcs
-                for (int64_t a0 = warp * 32; a0 < a.n_pad; a0 += nwarps * 32) {
-                    const int64_t i = a0 + lane;
-                    const bool is_i = i < a.n && x[i] == kI;
-                    const uint32_t own = __ballot_sync(0xffffffffu, is_i);
-                    if (!own) continue;
-                    const int32_t rb = is_i ? static_cast<int32_t>(rp[i]) : 0, re = is_i ? static_cast<int32_t>(rp[i + 1]) : 0;
-                    walk_rows_probe<1>(col_at, own, rb, re,
-                                       [&](uint32_t j) { return static_cast<uint32_t>(x[j] == kS && y[j] == kS); },
-                                       [&](uint32_t j, int32_t, int L) {  // y: already hit this step
-                        const uint32_t ii = static_cast<uint32_t>(a0 + L);
+                // warp-cooperative: the infected agents of the warp's chunks are
+                // queued (one per lane, compacted across chunks) and walk their
+                // concatenated rows 32 owners at a time (graph.cuh walk_rows), so
+                // the walk's lanes are full even when few agents are infected
+                uint32_t qid = 0, qc = 0;  // lane's queued owner; queued count (warp-uniform)
+                auto walk_push = [&](uint32_t nown) {
+                    const bool mine = static_cast<uint32_t>(lane) < nown;
+                    const int32_t rb = mine ? static_cast<int32_t>(rp[qid]) : 0, re = mine ? static_cast<int32_t>(rp[qid + 1]) : 0;
+                    const uint32_t own = nown >= 32 ? 0xffffffffu : ((1u << nown) - 1u);
+                    walk_rows_pay<1>(col_at, own, rb, re, qid,
+                                     [&](uint32_t j) { return static_cast<uint32_t>(x[j] == kS && y[j] == kS); },
+                                     [&](uint32_t j, int32_t, int, uint32_t ii) {  // y: already hit this step
                         const uint4 w = philox(make_uint4(min(ii, j), max(ii, j), static_cast<uint32_t>(t), TAG_SIR_TX), key);
                         if (static_cast<unsigned long long>(w.x) < tb) y[j] = kI;
                         return false;
                     });
+                };
+                for (int64_t a0 = warp * 32; a0 < a.n_pad; a0 += nwarps * 32) {
+                    const int64_t i = a0 + lane;
+                    const uint32_t own = __ballot_sync(0xffffffffu, i < a.n && x[i] == kI);
+                    enqueue(own, static_cast<uint32_t>(a0), qid, qc, walk_push);
                 }
+                if (qc) walk_push(qc);
                 __syncthreads();
                 for (int64_t i = tid; i < a.n; i += nt) {
                     n_inf += y[i] == kI;
                     n_sus += y[i] == kS;
                 }
             } else {
-                // pull, warp-cooperative: the susceptible lanes of each 32-agent chunk walk
-                // their concatenated rows; an owner stops at its first transmitting arc
+                // pull, warp-cooperative: the susceptible agents of the warp's chunks
+                // are queued (compacted across chunks) and walk their concatenated
+                // rows 32 owners at a time; an owner stops at its first transmitting
+                // arc and writes its own next state
+                uint32_t qid = 0, qc = 0;
+                auto walk_pull = [&](uint32_t nown) {
+                    const bool mine = static_cast<uint32_t>(lane) < nown;
+                    const int32_t rb = mine ? static_cast<int32_t>(rp[qid]) : 0, re = mine ? static_cast<int32_t>(rp[qid + 1]) : 0;
+                    const uint32_t own = nown >= 32 ? 0xffffffffu : ((1u << nown) - 1u);
+                    const uint32_t hit = walk_rows_pay<1>(col_at, own, rb, re, qid,
+                                                          [&](uint32_t j) { return static_cast<uint32_t>(x[j] == kI); },
+                                                          [&](uint32_t j, int32_t, int, uint32_t ii) {
+                        const uint4 w = philox(make_uint4(min(ii, j), max(ii, j), static_cast<uint32_t>(t), TAG_SIR_TX), key);
+                        return static_cast<unsigned long long>(w.x) < tb;
+                    });
+                    if (mine) {
+                        const bool h = (hit >> lane) & 1u;
+                        y[qid] = h ? kI : kS;
+                        n_inf += h;
+                        n_sus += !h;
+                    }
+                };
                 for (int64_t a0 = warp * 32; a0 < a.n_pad; a0 += nwarps * 32) {
                     const int64_t i = a0 + lane;
                     const bool real = i < a.n;
                     const uint8_t in = i < a.n_pad ? x[i] : static_cast<uint8_t>(3);  // 3 = padding
                     const uint32_t s_mask = __ballot_sync(0xffffffffu, real && in == kS);
                     const uint32_t i_mask = __ballot_sync(0xffffffffu, real && in == kI);
-                    uint32_t hit = 0;
-                    if (s_mask) {
-                        const bool mine = (s_mask >> lane) & 1u;
-                        const int32_t rb = mine ? static_cast<int32_t>(rp[i]) : 0, re = mine ? static_cast<int32_t>(rp[i + 1]) : 0;
-                        hit = walk_rows_probe<1>(col_at, s_mask, rb, re,
-                                                 [&](uint32_t j) { return static_cast<uint32_t>(x[j] == kI); },
-                                                 [&](uint32_t j, int32_t, int L) {
-                            const uint32_t ii = static_cast<uint32_t>(a0 + L);
-                            const uint4 w = philox(make_uint4(min(ii, j), max(ii, j), static_cast<uint32_t>(t), TAG_SIR_TX), key);
-                            return static_cast<unsigned long long>(w.x) < tb;
-                        });
-                    }
                     // R4 recovery draws: one Philox block per 4 agents, computed by the
                     // group's first lane and shuffled to the other three
                     uint32_t rw = 0;
@@ -189,13 +222,16 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
                         const int k = lane & 3;
                         rw = k == 0 ? r0 : (k == 1 ? r1 : (k == 2 ? r2 : r3));
                     }
-                    uint8_t o = in;
-                    if (real && in == kS && ((hit >> lane) & 1u)) o = kI;
-                    else if (real && in == kI && static_cast<unsigned long long>(rw) < a.t_gamma) o = kR;
-                    if (i < a.n_pad) y[i] = o;
-                    n_inf += real && o == kI;
-                    n_sus += real && o == kS;
+                    // susceptible agents are written by their walk
+                    if (!((s_mask >> lane) & 1u)) {
+                        uint8_t o = in;
+                        if (real && in == kI && static_cast<unsigned long long>(rw) < a.t_gamma) o = kR;
+                        if (i < a.n_pad) y[i] = o;
+                        n_inf += real && o == kI;
+                    }
+                    enqueue(s_mask, static_cast<uint32_t>(a0), qid, qc, walk_pull);
                 }
+                if (qc) walk_pull(qc);
             }
             n_inf = __reduce_add_sync(0xffffffffu, n_inf);
             n_sus = __reduce_add_sync(0xffffffffu, n_sus);
