@@ -129,6 +129,54 @@ def cpu_baseline_wealth(n_total, seed, budget_s=12.0):
                       f"single thread, {dt:.1f}s"}
 
 
+def run_reference_small(args, oracle, np):
+    """--impl reference --workload c1|c2|c3|c5: the oracle on the host, the
+    inputs built by the oracle itself (graphs, initial states), one JSON line
+    with the same unit as the GPU arm's line for that workload."""
+    from paper_2601_16292_b200 import workloads as W
+    w = args.workload
+    model, ncpu = host_info()
+    keys = ("L", "R", "rs", "wc", "wa", "ws", "vmax", "dt")
+    if w == "c1":
+        c = W.C1_WEALTH_SMALL
+        fn, units, sample = (lambda: oracle.wealth_run(np.ones(c["n"], np.int32), c["seed"], 0, c["steps"]),
+                             c["n"] * c["steps"], f"wealth N={c['n']} x {c['steps']} steps (the whole config)")
+    elif w == "c2":
+        c = W.C2_SIR
+        m_draws, k_inf = W.sir_counts(c)
+        rp, col, _ = oracle.er_graph(c["n"], m_draws, c["seed"])
+        st = oracle.sir_init(c["n"], k_inf, c["seed"])
+        fn, units, sample = (lambda: oracle.sir_run(rp, col, st, c["seed"], c["beta"], c["gamma"], 0, c["steps"]),
+                             c["n"] * c["steps"], f"SIR N={c['n']} x {c['steps']} steps (the whole config)")
+    elif w == "c3":
+        c = W.C3_BOIDS
+        P = oracle.boids_params(**{k: c[k] for k in keys})
+        s0 = oracle.boids_init(c["n"], c["L"], c["seed"])
+        fn, units, sample = (lambda: oracle.boids_run(s0, P, 3), c["n"] * 3,
+                             f"Boids N={c['n']}, first 3 of {c['steps']} steps (sparse phase; later steps denser)")
+    elif w == "c5":
+        c = W.C5_SWEEP
+        betas, seeds = W.sweep_replicates(c)
+        pick = np.arange(0, len(betas), 256)
+        fn, units, sample = (lambda: oracle.sir_sweep(c["n"], c["mean_degree"], c["gamma"], c["init_frac"],
+                                                      betas[pick], seeds[pick], c["steps"]),
+                             c["n"] * c["steps"] * len(pick),
+                             f"{len(pick)} of {len(betas)} replicates spanning all betas, nominal updates")
+    else:
+        print(json.dumps({"impl": "reference", "workload": w, "unavailable": "no oracle leg for this workload"}))
+        return 0
+    for _ in range(min(args.warmup, 1)):
+        fn()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        fn()
+    v = units * args.steps / (time.perf_counter() - t0)
+    print(json.dumps({"impl": "reference", "workload": w, "value": v, "unit": "agent-updates/s",
+                      "cpu_baseline": {"value": v, "unit": "agent-updates/s", "cores": 1, "kind": "oracle",
+                                       "sample": f"{sample}; host {model}, {ncpu} cpus"}}), flush=True)
+    return 0
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle timed on the host cores (bounded sample)."""
     import numpy as np
@@ -137,8 +185,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from paper_2601_16292_b200.workloads import C4_WEALTH_SCALE as cfg
     oracle.build()
+    if args.workload != "c4":
+        return run_reference_small(args, oracle, np)
+    from paper_2601_16292_b200.workloads import C4_WEALTH_SCALE as cfg
     # size the per-step sample so warmup + steps stay within ~2-3 minutes
     n_probe = 2_000_000
     w = np.ones(n_probe, np.int32)

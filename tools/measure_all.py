@@ -1,7 +1,9 @@
 #!/usr/bin/env python
 """Measure every BASELINE config on one B200 through the public API, with the
-CPU oracle timed beside it (single thread, bounded samples), and write one JSON
-object per config to stdout (collected into profiles/rNN_all_configs.jsonl).
+CPU oracle timed beside it by bench.py's reference arm (`bench.py --impl
+reference --workload cX`: single thread, bounded samples; this script never
+imports oracle/), and write one JSON object per config to stdout (collected
+into profiles/rNN_all_configs.jsonl).
 
 GPU timing: CUDA events on the model stream around amber_step(K) after a
 warm-up call; per-kernel device time from the library's event profiler.
@@ -13,15 +15,13 @@ import sys
 # load every kernel at context creation: lazy module loading inside a timed
 # region would be counted as step time
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
-import time
 
-import numpy as np
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-import oracle  # noqa: E402  (tests/bench-only dependency: the CPU baseline)
+import subprocess  # noqa: E402
 from paper_2601_16292_b200 import Model, boids_params, sir_params, sweep, wealth_params  # noqa: E402
 from paper_2601_16292_b200 import workloads as W  # noqa: E402
 
@@ -44,10 +44,12 @@ def timed(m, k):
     return ms, prof
 
 
-def cpu_rate(fn, units):
-    t0 = time.perf_counter()
-    fn()
-    return units / (time.perf_counter() - t0)
+def cpu_rate(workload):
+    """The oracle's rate for a workload from bench.py's reference arm (one timed run)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", workload,
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, cwd=ROOT)
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    return json.loads(line)["value"]
 
 
 def main():
@@ -56,8 +58,7 @@ def main():
     c = W.C1_WEALTH_SMALL
     m = Model("wealth", c["n"], wealth_params(), c["seed"])
     ms, prof = timed(m, c["steps"])
-    cpu = cpu_rate(lambda: oracle.wealth_run(np.ones(c["n"], np.int32), c["seed"], 0, c["steps"]),
-                   c["n"] * c["steps"])
+    cpu = cpu_rate("c1")
     out.append(dict(config="C1 wealth N=1e3 x100", us_per_step=ms / c["steps"] * 1e3,
                     agent_updates_per_s=c["n"] * c["steps"] / ms * 1e3, kernels=prof,
                     bound="launch/latency (single-CTA, all steps one launch)", cpu_oracle_per_s=cpu))
@@ -65,14 +66,8 @@ def main():
     # C2
     c = W.C2_SIR
     m = Model("sir", c["n"], sir_params(c["mean_degree"], c["beta"], c["gamma"], c["init_frac"]), c["seed"])
-    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
-    m.close()
-    m = Model("sir", c["n"], sir_params(c["mean_degree"], c["beta"], c["gamma"], c["init_frac"]), c["seed"])
     ms, prof = timed(m, c["steps"])
-    _, k_inf = W.sir_counts(c)
-    st = oracle.sir_init(c["n"], k_inf, c["seed"])
-    cpu = cpu_rate(lambda: oracle.sir_run(rp, col, st, c["seed"], c["beta"], c["gamma"], 0, c["steps"]),
-                   c["n"] * c["steps"])
+    cpu = cpu_rate("c2")
     out.append(dict(config="C2 SIR G(1e5,5e5) x200", us_per_step=ms / c["steps"] * 1e3,
                     agent_updates_per_s=c["n"] * c["steps"] / ms * 1e3, kernels=prof,
                     bound="latency (L2-resident 4.6 MB; grid barrier per step)", cpu_oracle_per_s=cpu))
@@ -82,9 +77,7 @@ def main():
     bp = boids_params(*[c[k] for k in ("L", "R", "rs", "wc", "wa", "ws", "vmax", "dt")])
     m = Model("boids", c["n"], bp, c["seed"])
     ms, prof = timed(m, c["steps"])
-    P = oracle.boids_params(**{k: c[k] for k in ("L", "R", "rs", "wc", "wa", "ws", "vmax", "dt")})
-    s0 = oracle.boids_init(c["n"], c["L"], c["seed"])
-    cpu = cpu_rate(lambda: oracle.boids_run(s0, P, 3), c["n"] * 3)
+    cpu = cpu_rate("c3")
     out.append(dict(config="C3 Boids N=1e5 x100", us_per_step=ms / c["steps"] * 1e3,
                     agent_updates_per_s=c["n"] * c["steps"] / ms * 1e3, kernels=prof,
                     bound="issue/latency (fp32+int64 stencil, L1-resident)",
@@ -108,9 +101,7 @@ def main():
     betas, seeds = W.sweep_replicates(c)
     res, stt = sweep(c["n"], sir_params(c["mean_degree"], 0.0, c["gamma"], c["init_frac"]), betas, seeds,
                      c["steps"], with_stats=True)
-    pick = np.arange(0, 4096, 256)
-    cpu = cpu_rate(lambda: oracle.sir_sweep(c["n"], c["mean_degree"], c["gamma"], c["init_frac"], betas[pick],
-                                            seeds[pick], c["steps"]), c["n"] * c["steps"] * len(pick))
+    cpu = cpu_rate("c5")
     out.append(dict(config="C5 sweep 4096 x N=1e4 x300", step_ms=stt["step_ms"], build_ms=stt["build_ms"],
                     agent_updates_per_s=stt["agent_updates"] / stt["step_ms"] * 1e3,
                     active_updates_per_s=stt["active_updates"] / stt["step_ms"] * 1e3,
