@@ -281,7 +281,9 @@ int amber_digest(amber_model* m, const char* name, uint64_t* out);
  * 0 = one launch per step, pull only for SIR), SIR "direction" (0 = choose
  * per step, push when 4I < 3S; 1 = always pull; 2 = push whenever the previous
  * counts are known -- identical results, for tests and probes; 1 or 2 also
- * run a single step through the cooperative kernel); Boids: "lanes" (1/4/8/16 lanes
+ * run a single step through the cooperative kernel), SIR "apl" (agents per
+ * lane of the step kernels: 0 = auto (4 above 2^22 agents, else 1), 1, 2 or
+ * 4 -- identical results); Boids: "lanes" (1/4/8/16 lanes
  * per agent in the stencil), "tiled", "fused" (measured alternatives).
  * Read-only (amber_get_option): wealth "replays" (exact-replay count, after
  * the overflow check), "counter_bits", "scatter" (0 bins, 1 packed-counter
