@@ -277,8 +277,13 @@ __global__ void __launch_bounds__(1024, 1) wealth_small_kernel(const SmallArgs a
     extern __shared__ __align__(16) int32_t sw[];
     uint32_t* cnt0 = reinterpret_cast<uint32_t*>(sw + kSmallMax);
     uint32_t* cnt1 = cnt0 + kSmallMax;
-    __shared__ unsigned long long acc[3][5];  // {total, active, digest, sent, got}
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+    // per-warp partial sums of the step records {total, active, digest, sent, got},
+    // three rotating sets (step t's set is next written by step t + 3); plain
+    // stores by each warp's lane 0 and one 32-way sum per field after the
+    // step's barrier (shared 64-bit atomics are CAS loops: 16 contending warps
+    // cost ~1 us per step)
+    __shared__ unsigned long long part[3][32][5];
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = (nt + 31) >> 5;
     const uint32_t n = static_cast<uint32_t>(a.n);
     const unsigned long long m = a.n - (a.exclude_self ? 1 : 0);
     for (uint32_t i = tid; i < n; i += nt) {
@@ -286,12 +291,8 @@ __global__ void __launch_bounds__(1024, 1) wealth_small_kernel(const SmallArgs a
         cnt0[i] = 0u;
         cnt1[i] = 0u;
     }
-    if (tid < 15) (&acc[0][0])[tid] = 0ull;
+    for (int k = tid; k < 3 * 32 * 5; k += nt) (&part[0][0][0])[k] = 0ull;
     __syncthreads();
-    auto warp_add = [&](unsigned long long v, unsigned long long* dst) {
-        v = warp_sum_u64(v);
-        if (lane == 0 && v) atomicAdd(dst, v);
-    };
     // scatter of step t from the pair (i0, i0 + 1) with wealth (v0, v1)
     auto scatter = [&](uint32_t p, int32_t v0, int32_t v1, uint32_t t, uint32_t* cnt) -> unsigned long long {
         const uint32_t i0 = 2 * p;
@@ -318,7 +319,8 @@ __global__ void __launch_bounds__(1024, 1) wealth_small_kernel(const SmallArgs a
         unsigned long long sent = 0;
         for (uint32_t p = tid; p < npairs; p += nt)
             sent += scatter(p, sw[2 * p], 2 * p + 1 < n ? sw[2 * p + 1] : 0, a.t0, (a.t0 & 1) ? cnt1 : cnt0);
-        warp_add(sent, &acc[a.t0 % 3][3]);
+        const unsigned sw0 = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(sent));
+        if (lane == 0) part[a.t0 % 3][warp][3] = sw0;
     }
     __syncthreads();
     for (int64_t k = 0; k < a.steps; ++k) {
@@ -352,18 +354,20 @@ __global__ void __launch_bounds__(1024, 1) wealth_small_kernel(const SmallArgs a
         const unsigned aw = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(act));
         const unsigned gw = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(got));
         const unsigned sw_ = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(sent));
+        if (a.digest) dig = warp_sum_u64(dig);
         if (lane == 0) {
-            if (tw) atomicAdd(&acc[t % 3][0], static_cast<unsigned long long>(static_cast<long long>(tw)));
-            if (aw) atomicAdd(&acc[t % 3][1], static_cast<unsigned long long>(aw));
-            if (gw) atomicAdd(&acc[t % 3][4], static_cast<unsigned long long>(gw));
-            if (sw_) atomicAdd(&acc[(t + 1) % 3][3], static_cast<unsigned long long>(sw_));
+            unsigned long long* x = part[t % 3][warp];
+            x[0] = static_cast<unsigned long long>(static_cast<long long>(tw));
+            x[1] = aw;
+            x[2] = dig;
+            x[4] = gw;
+            part[(t + 1) % 3][warp][3] = sw_;
         }
-        if (a.digest) warp_add(dig, &acc[t % 3][2]);
         __syncthreads();
-        if (tid < 5) {  // step t's record is complete; its accumulator set is next used by step t + 3
-            unsigned long long* x = acc[t % 3];
-            (&a.ring[slot_idx].total)[tid] = x[tid];
-            x[tid] = 0ull;
+        if (tid < 5) {  // step t's record is complete
+            unsigned long long v = 0;
+            for (int w = 0; w < nwarps; ++w) v += part[t % 3][w][tid];
+            (&a.ring[slot_idx].total)[tid] = v;
         }
         if (++slot_idx == ring_cap) slot_idx = 0;
     }
