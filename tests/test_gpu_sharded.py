@@ -137,8 +137,10 @@ def sharded_sir(world, cfg):
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
-def test_sharded_sir_equals_oracle(orc, world):
-    # NEXT-3: id-range shards, pull against the all-gathered I bitmap every step
+@pytest.mark.parametrize("apl", [0, 4])
+def test_sharded_sir_equals_oracle(orc, world, apl):
+    # NEXT-3: id-range shards, pull against the all-gathered I bitmap every step;
+    # apl 4: 128-agent chunks that reach past a shard's end (masked)
     cfg = dict(n=50_003, mean_degree=10.0, beta=0.05, gamma=0.1, init_frac=0.01, seed=7)
     steps = 40
     ref_m = Model("sir", cfg["n"], sir_params(cfg["mean_degree"], cfg["beta"], cfg["gamma"], cfg["init_frac"]),
@@ -154,6 +156,7 @@ def test_sharded_sir_equals_oracle(orc, world):
         assert a[2] + a[3] == b[2] and a[3] % 32 == 0  # contiguous, 32-aligned slices
     for m in ms:
         m.set_option("digest", 1)
+        m.set_option("apl", apl)
     par(ms, lambda m: (m.step(1), m.step(steps - 1)))
     x = np.concatenate(par(ms, lambda m: m.read_column("state")))
     assert np.array_equal(x, ref)
@@ -238,6 +241,7 @@ def test_sharded_boids_equals_oracle(orc, world):
     assert sum(own0) == cfg["n"]
     for m in ms:
         m.set_option("digest", 1)
+        m.set_option("apl", apl)
     par(ms, lambda m: (m.step(1), m.step(steps - 1)))
     got = boids_state(ms)
     want = ref[0]
