@@ -49,25 +49,6 @@ struct SweepArgs {
     int64_t col_cap;         // u16 entries reserved in shared memory
 };
 
-// Appends the agents a0 + b for the set bits b of `mask` to the warp's owner
-// queue (lane k holds the k-th queued agent in qid; qc = queued count), and
-// walks 32 of them as soon as 32 are queued.  All 32 lanes call it.
-template <class W>
-__device__ __forceinline__ void enqueue(uint32_t mask, uint32_t a0, uint32_t& qid, uint32_t& qc, W&& walk)
-{
-    const uint32_t lane = threadIdx.x & 31, k = __popc(mask);
-    if (!k) return;
-    if (lane >= qc && lane < qc + k) qid = a0 + __fns(mask, 0, static_cast<int>(lane - qc + 1));
-    if (qc + k < 32) {
-        qc += k;
-        return;
-    }
-    walk(32u);
-    const uint32_t rem = qc + k - 32;
-    if (lane < rem) qid = a0 + __fns(mask, 0, static_cast<int>(32 - qc + lane + 1));
-    qc = rem;
-}
-
 template <bool COL_SMEM>
 __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
 {
