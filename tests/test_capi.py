@@ -63,3 +63,34 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert not re.search(r"^\s*(import|from)\s+oracle", txt, re.M), f
                 assert "amber_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_only_allowed_places_import_oracle():
+    # oracle/ is test infrastructure: besides tests/, only bench.py's reference /
+    # cpu_baseline legs, __graft_entry__ (build + smoke) and the golden-file
+    # writer (a script that calls nothing but oracle/) may import it
+    allowed = {"bench.py", "__graft_entry__.py", os.path.join("tools", "make_oracle_goldens.py")}
+    for dirpath, dirs, files in os.walk(ROOT):
+        rel = os.path.relpath(dirpath, ROOT)
+        if rel.split(os.sep)[0] in ("tests", "oracle", ".git", "baseline", "gpurun_out"):
+            continue
+        for f in files:
+            if not f.endswith(".py"):
+                continue
+            path = os.path.normpath(os.path.join(rel, f))
+            txt = open(os.path.join(dirpath, f), errors="ignore").read()
+            if re.search(r"^\s*(import|from)\s+oracle\b", txt, re.M):
+                assert path in allowed, path
+
+
+@pytest.mark.parametrize("workload", ["c1", "c2"])
+def test_bench_reference_arm_small_workloads(workload):
+    import json
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", workload,
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, cwd=ROOT, timeout=300)
+    assert r.returncode == 0, r.stderr
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["impl"] == "reference" and line["workload"] == workload
+    assert line["value"] > 0 and line["cpu_baseline"]["kind"] == "oracle"
