@@ -30,15 +30,20 @@ HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if o
 
 
 def timed(m, k):
+    """Step time of k steps, unprofiled (per-kernel events between the launches
+    of a multi-kernel step would count as step time), then the per-kernel split
+    from the next k steps with the profiler on."""
     m.step(2)
     m.synchronize()
-    m.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(m.stream)
     m.step(k)
     e1.record(m.stream)
     m.synchronize()
     ms = e0.elapsed_time(e1)
+    m.profile(True)
+    m.step(k)
+    m.synchronize()
     prof = m.profile_results()
     m.profile(False)
     return ms, prof
