@@ -79,15 +79,39 @@ struct BoidsSlot {
     unsigned long long digest;
 };
 
+// Runs of equal keys in consecutive lanes (key < 0: no item, never merged):
+// the lane of the run's head, the lane's rank in its run and the run length.
+// The state is in the previous step's cell order, so consecutive agents mostly
+// share their new cell: one atomic per run instead of one per agent.  All 32
+// lanes call it.
+__device__ __forceinline__ void lane_runs(int key, int& head, int& rank, int& len)
+{
+    const uint32_t lane = threadIdx.x & 31;
+    const int prev = __shfl_up_sync(0xffffffffu, key, 1);
+    const uint32_t heads = __ballot_sync(0xffffffffu, lane == 0 || key < 0 || prev != key);
+    const uint32_t le = 0xffffffffu >> (31 - lane);  // lanes <= this one
+    head = 31 - __clz(heads & le);
+    rank = static_cast<int>(lane) - head;
+    const uint32_t above = heads & ~le;
+    len = (above ? __ffs(above) - 1 : 32) - head;
+}
+
 __global__ void boids_count_kernel(const float4* __restrict__ st, int64_t n, BoidsArgs a, int* __restrict__ cnt,
                                    int* __restrict__ cell_of, BoidsSlot* slot_zero)
 {
     if (slot_zero && blockIdx.x == 0 && threadIdx.x == 0) *slot_zero = BoidsSlot{0.0, 0.0, 0.0, 0ull};  // this step's record
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-        const float4 s = st[p];
-        const int c = cell_coord(s.y, a) * a.nc + cell_coord(s.x, a);
-        cell_of[p] = c;
-        atomicAdd(cnt + c, 1);
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x, rounds = (n + nt - 1) / nt;
+    for (int64_t r = 0; r < rounds; ++r) {  // uniform trip count: the lanes cooperate
+        const int64_t p = r * nt + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        int c = -1;
+        if (p < n) {
+            const float4 s = st[p];
+            c = cell_coord(s.y, a) * a.nc + cell_coord(s.x, a);
+            cell_of[p] = c;
+        }
+        int head, rank, len;
+        lane_runs(c, head, rank, len);
+        if (c >= 0 && rank == 0) atomicAdd(cnt + c, len);
     }
 }
 
@@ -157,10 +181,19 @@ __global__ void boids_scatter_kernel(const float4* __restrict__ st, const int32_
 {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
     for (int64_t c = tid; c < ncell_zero; c += nt) cnt[c] = 0;
-    for (int64_t p = tid; p < n; p += nt) {
-        const int q = atomicAdd(cursor + cell_of[p], 1);
-        sorted[q] = st[p];
-        sorted_ids[q] = ids[p];
+    const int64_t rounds = (n + nt - 1) / nt;
+    for (int64_t r = 0; r < rounds; ++r) {  // uniform trip count: the lanes cooperate
+        const int64_t p = r * nt + tid;
+        const int c = p < n ? cell_of[p] : -1;
+        int head, rank, len;
+        lane_runs(c, head, rank, len);
+        int q = 0;
+        if (c >= 0 && rank == 0) q = atomicAdd(cursor + c, len);  // one cursor claim per run
+        q = __shfl_sync(0xffffffffu, q, head) + rank;
+        if (c >= 0) {
+            sorted[q] = st[p];
+            sorted_ids[q] = ids[p];
+        }
     }
 }
 
