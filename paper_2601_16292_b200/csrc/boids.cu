@@ -1153,7 +1153,11 @@ public:
     int64_t m_first = 0;
     int ncell = 0;
     int64_t tiled = 0;  // 1: shared-memory tiled stencil kernel (slower once flocks cluster)
-    int64_t lanes = 8;  // lanes per agent in the stencil scan (1 = one-lane kernel; 4, 8, 16)
+    // lanes per agent in the stencil scan (1 = one-lane kernel; 4, 8, 16): 4 measured
+    // best for both the clustered C3 (54 vs 58 us at 8) and the uniform V3 (22.6
+    // vs 32.7 ms): two shuffle levels for the seven int64 sums instead of three,
+    // and eight agents per warp (tools/boids_lanes_probe.py)
+    int64_t lanes = 4;
     int64_t fused = 0;  // 1: all phases of all steps in one cooperative launch (measured slower, r01)
     bool counted = false;  // cnt / cell_of hold the cell counts of the current state (from the last group step)
 
@@ -1639,12 +1643,12 @@ public:
             AMBER_CUDA(cudaMemcpyAsync(&own_rng[1], start.p + (w + 1) * ba.nc, 4, cudaMemcpyDeviceToHost, rt.stream));
             AMBER_CUDA(cudaStreamSynchronize(rt.stream));
             AMBER_REQUIRE(own_rng[1] - own_rng[0] == n_own, "sharded Boids: own agents outside the slab columns");
-            const int gsteps = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_own * 8, 256),
+            const int gsteps = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_own * 4, 256),
                                                                                         rt.num_sms * 8)));
             BoidsSlot* sl = ring.p + (t % metrics_cap);
             const int dg = digest_on ? 1 : 0;
             prof.launch(rt.stream, "boids_slab_step", [&] {
-                slab_step_kernel<8><<<gsteps, 256, 0, rt.stream>>>(sorted.p, sids.p, start.p, own_rng[0], own_rng[1], g,
+                slab_step_kernel<4><<<gsteps, 256, 0, rt.stream>>>(sorted.p, sids.p, start.p, own_rng[0], own_rng[1], g,
                                                                     st.p, ids.p, sl, dg);
             });
             check_launch("slab_step_kernel");

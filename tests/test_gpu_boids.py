@@ -132,11 +132,12 @@ def test_geometry_invariance_and_io(orc, monkeypatch):
         assert np.array_equal(x, y)
     # write/read round trip through the permuted internal order
     e = make(cfg)
+    e.set_option("lanes", 8)  # the cooperative all-phases kernel runs 8 lanes per agent
     e.set_option("fused", 1)  # one cooperative launch for all phases and steps
     e.step(10)
     for x, y in zip(state(a), state(e)):
         assert np.array_equal(x, y)
-    for lanes in (1, 4, 16):
+    for lanes in (1, 8, 16):
         d = make(cfg)
         d.set_option("lanes", lanes)
         d.step(10)
@@ -188,7 +189,7 @@ def test_fused_counts_across_calls_options_and_writes(orc):
     P = oparams(orc, cfg)
     st = state(m)
     plan = [(2, {}), (1, {"lanes": 4}), (2, {"lanes": 8}), (1, {"tiled": 1}), (2, {"tiled": 0}),
-            (2, {"fused": 1}), (1, {"fused": 0}), ("write", None), (3, {})]
+            (2, {"fused": 1, "lanes": 8}), (1, {"fused": 0}), ("write", None), (3, {"lanes": 4})]
     for k, opts in plan:
         if k == "write":
             vx = (st[2] * np.float32(0.75)).astype(np.float32)

@@ -241,7 +241,6 @@ def test_sharded_boids_equals_oracle(orc, world):
     assert sum(own0) == cfg["n"]
     for m in ms:
         m.set_option("digest", 1)
-        m.set_option("apl", apl)
     par(ms, lambda m: (m.step(1), m.step(steps - 1)))
     got = boids_state(ms)
     want = ref[0]
