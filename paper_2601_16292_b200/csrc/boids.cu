@@ -31,6 +31,12 @@ namespace amber {
 namespace {
 
 constexpr float kFix = 16777216.0f;  // 2^24 (B3)
+#ifndef AMBER_BOIDS_INFLIGHT
+#define AMBER_BOIDS_INFLIGHT 2  // candidate loads in flight per lane in interior row runs
+#endif
+#ifndef AMBER_BOIDS_MINB
+#define AMBER_BOIDS_MINB 4  // resident 256-thread blocks per SM for the stencil kernel (register cap 64)
+#endif
 constexpr int kTileCap = 3072;        // staged halo agents per tile (48 KB)
 
 struct BoidsArgs {
@@ -590,6 +596,15 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
             // two cells < L/2 per coordinate): no minimum image, rows as runs
             auto run_in = [&](int b, int e) {
                 int q = b + sub;
+#if AMBER_BOIDS_INFLIGHT == 4
+                for (; q + 3 * G < e; q += 4 * G) {  // four candidate loads in flight per lane
+                    const float4 o0 = sorted[q], o1 = sorted[q + G], o2 = sorted[q + 2 * G], o3 = sorted[q + 3 * G];
+                    boid_accumulate<false>(o0, me, L, halfL, R2, rs2, acc);
+                    boid_accumulate<false>(o1, me, L, halfL, R2, rs2, acc);
+                    boid_accumulate<false>(o2, me, L, halfL, R2, rs2, acc);
+                    boid_accumulate<false>(o3, me, L, halfL, R2, rs2, acc);
+                }
+#endif
                 for (; q + G < e; q += 2 * G) {  // two candidate loads in flight per lane
                     const float4 o0 = sorted[q], o1 = sorted[q + G];
                     boid_accumulate<false>(o0, me, L, halfL, R2, rs2, acc);
@@ -727,7 +742,7 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
 }
 
 template <int G>
-__global__ void __launch_bounds__(256, 4) boids_group_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ sids,
+__global__ void __launch_bounds__(256, AMBER_BOIDS_MINB) boids_group_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ sids,
                                                           const int* __restrict__ start, int64_t n, BoidsArgs a,
                                                           float4* __restrict__ out, int32_t* __restrict__ out_ids,
                                                           BoidsSlot* slot, int digest, int* __restrict__ next_cnt,
