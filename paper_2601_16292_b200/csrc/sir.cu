@@ -271,6 +271,7 @@ struct SirStepArgs {
     int64_t n_steps;         // steps in this launch (persistent) or 1
     int cur;                 // index of the buffers holding the state at t0
     int prev_ok;             // ring slot t0 - 1 holds the counts of the state at t0
+    const SirSlot* prev0;    // else (if set) the counts of the state at t0 are here
     SirSlot* ring;
     int64_t ring_cap;
     int digest;
@@ -749,8 +750,8 @@ __global__ void __launch_bounds__(kSirPT, kSirMinB) sir_persistent_kernel(const 
         if (a.queue && blockIdx.x == 0 && threadIdx.x < 2 * kRegions) a.queue[((t + 1) & 1u) * 2 * kRegions + threadIdx.x] = 0u;
         bool push = false;
         unsigned long long prev_s = 0, prev_i = 0, prev_r = 0;
-        if (k > 0 || a.prev_ok) {
-            const SirSlot* pv = a.ring + ((t + a.ring_cap - 1) % a.ring_cap);
+        if (k > 0 || a.prev_ok || a.prev0) {
+            const SirSlot* pv = k == 0 && a.prev0 ? a.prev0 : a.ring + ((t + a.ring_cap - 1) % a.ring_cap);
             prev_s = pv->S;
             prev_i = pv->I;
             prev_r = pv->R;
@@ -790,6 +791,24 @@ __global__ void sir_rebase_kernel(const int32_t* __restrict__ rp, int64_t cnt, i
         out[k] = rp[k] - base;
 }
 
+// S / I / R counts of a state from its bitmaps (after a column write or a step
+// reset), accumulated into a zeroed ring slot: the next step's direction choice.
+__global__ void sir_count_bits_kernel(const uint32_t* __restrict__ ib, const uint32_t* __restrict__ sb, int64_t n,
+                                      SirSlot* slot)
+{
+    unsigned long long v[3] = {0, 0, 0};
+    const int64_t words = (n + 31) / 32;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t left = n - 32 * w;
+        const uint32_t real = left >= 32 ? 0xffffffffu : ((1u << left) - 1u);
+        v[0] += __popc(sb[w] & real);
+        v[1] += __popc(ib[w] & real);
+        v[2] += __popc(~(sb[w] | ib[w]) & real);
+    }
+    unsigned long long* const outs[3] = {&slot->S, &slot->I, &slot->R};
+    block_sum_atomic<3>(v, outs);
+}
+
 __global__ void sir_zero_slots(SirSlot* ring, int64_t cap, int64_t s0, int64_t count)
 {
     for (int64_t k = threadIdx.x; k < count && k < cap; k += blockDim.x) ring[(s0 + k) % cap] = SirSlot{0, 0, 0, 0};
@@ -813,6 +832,8 @@ public:
     int64_t m_first = 0;
     bool prev_ok = false;  // ring slot t-1 holds the counts of the current state
     int dir = 0;           // "direction" option (SirStepArgs::dir)
+    DevBuf<SirSlot> cnt0;  // counts of the current state after a column write / step reset
+    bool cnt0_ok = false;  // cnt0 is valid (and prev_ok is not): the next launch reads it
     int apl = 0;           // "apl" option: agents per lane of the step kernels (0 = auto, 1, 2, 4)
     // sharded (world > 1, NEXT-3): this rank owns agents [lo, lo + nl) (shard =
     // multiple of 32 agents so bitmap words never straddle ranks), its CSR rows
@@ -967,6 +988,7 @@ public:
             a.sb[c] = sb[c].p;
         }
         a.prev_ok = prev_ok ? 1 : 0;
+        a.prev0 = !prev_ok && cnt0_ok ? cnt0.p : nullptr;
         a.n = nl;
         a.n_pad = npl;
         a.gid0 = static_cast<unsigned long long>(lo);
@@ -1038,6 +1060,7 @@ public:
                 t += chunk;
                 if (chunk & 1) cur ^= 1;
                 prev_ok = true;
+                cnt0_ok = false;
             } else {
                 for (int64_t k = 0; k < chunk; ++k) {
                     SirStepArgs a = args(1);
@@ -1049,6 +1072,7 @@ public:
                     ++t;
                 }
                 prev_ok = true;
+                cnt0_ok = false;
             }
             done += chunk;
         }
@@ -1130,7 +1154,23 @@ public:
         if (bytes < static_cast<size_t>(nl)) fail(AMBER_E_BUFFER_TOO_SMALL, "src smaller than state column");
         copy_in(rt, x[cur].p, src, nl, on_dev);
         build_bits();
-        prev_ok = false;  // the next step pulls (and records the counts again)
+        recount();
+    }
+
+    // Counts of the current state (into cnt0, not the ring: slot t-1 keeps the
+    // record of step t-1), so the next step chooses its direction -- a pull
+    // from a state with few infected agents costs ~15x a push at V2.  Sharded
+    // steps always pull: nothing to do.
+    void recount()
+    {
+        prev_ok = false;
+        cnt0_ok = false;
+        if (sc) return;
+        if (!cnt0.p) cnt0.allocate(&rt, 1);
+        AMBER_CUDA(cudaMemsetAsync(cnt0.p, 0, sizeof(SirSlot), rt.stream));
+        sir_count_bits_kernel<<<rt.num_sms * 4, 256, 0, rt.stream>>>(ib[cur].p, sb[cur].p, nl, cnt0.p);
+        check_launch("sir_count_bits_kernel");
+        cnt0_ok = true;
     }
 
     void read_metrics(const char* name, void* dst, size_t bytes, int64_t* n_out) override
@@ -1176,7 +1216,7 @@ public:
         AMBER_CUDA(cudaStreamSynchronize(rt.stream));
         t = s;
         m_first = s;
-        prev_ok = false;
+        recount();
     }
 
     bool set_option(const char* key, int64_t v) override

@@ -259,3 +259,35 @@ def test_forced_direction_every_step_ragged(orc, n, direction, apl):
     assert [int(m.metrics(k)[-1]) for k in "SIR"] == counts.tolist()
     assert m.digest("state") == orc.digest(x)
     assert int(m.metrics("digest")[-1]) == orc.digest(x)
+
+
+def test_column_write_recounts_and_keeps_history(orc):
+    # after a state write the model counts the new state (so the next step may
+    # push); the records of the steps before the write are unchanged
+    cfg = dict(n=30_011, mean_degree=8.0, beta=0.15, gamma=0.1, init_frac=0.02, seed=5)
+    m = make(cfg)
+    m.set_option("digest", 1)
+    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
+    x = orc.sir_init(cfg["n"], sir_counts(cfg)[1], cfg["seed"])
+    m.step(4)
+    hist = [m.metrics(k).copy() for k in "SIR"]
+    for t in range(4):
+        x = orc.sir_step(rp, col, x, cfg["seed"], t, cfg["beta"], cfg["gamma"])
+    # a mostly susceptible state with few infected agents: the next step should push
+    w = np.where(x == 1, 0, x).astype(np.uint8)
+    w[::997] = 1
+    m.write_column("state", w)
+    for k, h in zip("SIR", hist):
+        assert np.array_equal(m.metrics(k)[:4], h)
+    m.step(3)
+    x = w
+    for t in range(4, 7):
+        x = orc.sir_step(rp, col, x, cfg["seed"], t, cfg["beta"], cfg["gamma"])
+    assert np.array_equal(m.read_column("state"), x)
+    counts = [int((x == s).sum()) for s in range(3)]
+    assert [int(m.metrics(k)[-1]) for k in "SIR"] == counts
+    assert int(m.metrics("digest")[-1]) == orc.digest(x)
+    m.set_step(2)  # a step reset recounts as well
+    m.step(1)
+    y = orc.sir_step(rp, col, x, cfg["seed"], 2, cfg["beta"], cfg["gamma"])
+    assert np.array_equal(m.read_column("state"), y)
