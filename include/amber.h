@@ -282,8 +282,8 @@ int amber_digest(amber_model* m, const char* name, uint64_t* out);
  * per step, push when 4I < 3S; 1 = always pull; 2 = push whenever the previous
  * counts are known -- identical results, for tests and probes; 1 or 2 also
  * run a single step through the cooperative kernel), SIR "apl" (agents per
- * lane of the step kernels: 0 = auto (4 above 2^22 agents, else 1), 1, 2 or
- * 4 -- identical results); Boids: "lanes" (1/4/8/16 lanes per agent in the
+ * lane of the step kernels: 0 = auto (8 above 2^22 agents, else 1), 1, 2, 4
+ * or 8 -- identical results); Boids: "lanes" (1/4/8/16 lanes per agent in the
  * stencil, default 4; "fused" runs only at 8), "tiled", "fused" (measured
  * alternatives, identical results).
  * Read-only (amber_get_option): wealth "replays" (exact-replay count, after

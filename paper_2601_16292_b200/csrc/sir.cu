@@ -306,7 +306,7 @@ constexpr int kSirMinB = AMBER_SIR_MINB;  // min resident blocks per SM (registe
 // very different amounts per chunk, and static striding left most warps
 // waiting at the step barrier (r01 ncu: 43% of stall samples).  Per-step
 // launch: one chunk per warp, the block scheduler balances.
-constexpr int kChunkMax = 128;
+constexpr int kChunkMax = 256;
 constexpr int kQCap = 32 + kChunkMax;  // owner queue per warp: < 32 carried + one chunk
 
 struct SirSmem {
@@ -364,17 +364,10 @@ __device__ __forceinline__ bool bit_of(const uint32_t* bits, uint32_t j)
 
 // The lane's APL state bytes (agents i0 .. i0+APL-1) as one word.
 template <int APL>
-__device__ __forceinline__ uint32_t load_states(const uint8_t* x, int64_t i0)
+__device__ __forceinline__ void store_states(uint8_t* y, int64_t i0, unsigned long long v)
 {
-    if constexpr (APL == 4) return *reinterpret_cast<const uint32_t*>(x + i0);
-    else if constexpr (APL == 2) return *reinterpret_cast<const uint16_t*>(x + i0);
-    else return x[i0];
-}
-
-template <int APL>
-__device__ __forceinline__ void store_states(uint8_t* y, int64_t i0, uint32_t v)
-{
-    if constexpr (APL == 4) *reinterpret_cast<uint32_t*>(y + i0) = v;
+    if constexpr (APL == 8) *reinterpret_cast<unsigned long long*>(y + i0) = v;
+    else if constexpr (APL == 4) *reinterpret_cast<uint32_t*>(y + i0) = static_cast<uint32_t>(v);
     else if constexpr (APL == 2) *reinterpret_cast<uint16_t*>(y + i0) = static_cast<uint16_t>(v);
     else y[i0] = static_cast<uint8_t>(v);
 }
@@ -398,20 +391,25 @@ __device__ __forceinline__ uint32_t lane_real(int64_t i0, int64_t n)
 }
 
 // Recovery draws of the lane's agents i0 .. i0+APL-1 (global ids; i0 is a
-// multiple of APL): lane i & 3 of Philox block i / 4 (R4) -- one block for the
-// whole lane when APL = 4.  Bit k set iff agent i0 + k is in `inf` and recovers.
+// multiple of APL): lane i & 3 of Philox block i / 4 (R4) -- one block per
+// four agents of the lane when APL >= 4.  Bit k set iff agent i0 + k is in `inf`
+// and recovers.
 template <int APL>
 __device__ __forceinline__ uint32_t recover_nib(const SirStepArgs& a, unsigned long long i0, uint32_t t, uint32_t inf)
 {
-    if (!inf) return 0u;
-    const uint4 r = stream_block(a.key, TAG_SIR_REC, i0 >> 2, t);
-    const uint32_t d[4] = {r.x, r.y, r.z, r.w};
     uint32_t out = 0;
 #pragma unroll
-    for (int k = 0; k < APL; ++k) {
-        const uint32_t q = static_cast<uint32_t>((i0 + k) & 3u);
-        const uint32_t v = q == 0 ? d[0] : (q == 1 ? d[1] : (q == 2 ? d[2] : d[3]));
-        if (((inf >> k) & 1u) && v < a.t_gamma) out |= 1u << k;
+    for (int b = 0; b < (APL + 3) / 4; ++b) {
+        const uint32_t part = (inf >> (4 * b)) & 0xfu;
+        if (!part) continue;
+        const uint4 r = stream_block(a.key, TAG_SIR_REC, (i0 >> 2) + b, t);
+        const uint32_t d[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int k = 4 * b; k < APL && k < 4 * b + 4; ++k) {
+            const uint32_t q = static_cast<uint32_t>((i0 + k) & 3u);
+            const uint32_t v = q == 0 ? d[0] : (q == 1 ? d[1] : (q == 2 ? d[2] : d[3]));
+            if (((inf >> k) & 1u) && v < a.t_gamma) out |= 1u << k;
+        }
     }
     return out;
 }
@@ -554,10 +552,10 @@ __device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0,
     }
     const uint32_t recnib = recover_nib<APL>(a, a.gid0 + static_cast<unsigned long long>(i0), t, nib_i);
     const uint32_t s2 = nib_s & ~hitnib, i2 = (nib_s & hitnib) | (nib_i & ~recnib), r2 = real & ~s2 & ~i2;
-    uint32_t yw = 0;
+    unsigned long long yw = 0;
 #pragma unroll
     for (int k = 0; k < APL; ++k) {
-        const uint32_t st = (s2 >> k) & 1u ? kS : ((i2 >> k) & 1u ? kI : ((r2 >> k) & 1u ? kR : kPad));
+        const unsigned long long st = (s2 >> k) & 1u ? kS : ((i2 >> k) & 1u ? kI : ((r2 >> k) & 1u ? kR : kPad));
         yw |= st << (8 * k);
     }
     store_states<APL>(y, i0, yw);
@@ -693,18 +691,25 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
         const uint32_t recnib = recover_nib<APL>(a, static_cast<unsigned long long>(i0), t, nib_i);
         rec += __popc(recnib);
         if (nons) {
-            // the lane's bytes sit in one 32-bit word (i0 is a multiple of APL)
-            const uint32_t sh0 = static_cast<uint32_t>(i0 & 3) * 8u;
-            uint32_t delta = 0;
+            // the lane's bytes sit in one 32-bit word (64-bit for APL 8; i0 is a
+            // multiple of APL)
+            unsigned long long delta = 0;
 #pragma unroll
             for (int k = 0; k < APL; ++k)
                 if ((nons >> k) & 1u) {
-                    const uint32_t nw = ((nib_i & ~recnib) >> k) & 1u ? kI : kR;
-                    const uint32_t old = (b_s >> k) & 1u ? kS : ((b_i >> k) & 1u ? kI : kR);
-                    delta += (nw - old) << (8 * k);  // mod 2^32: bytes stay in 0..3
-                    if (a.digest) dig += digest_term(static_cast<unsigned long long>(i0 + k), nw);
+                    const unsigned long long nw = ((nib_i & ~recnib) >> k) & 1u ? kI : kR;
+                    const unsigned long long old = (b_s >> k) & 1u ? kS : ((b_i >> k) & 1u ? kI : kR);
+                    delta += (nw - old) << (8 * k);  // mod 2^64: bytes stay in 0..3
+                    if (a.digest) dig += digest_term(static_cast<unsigned long long>(i0 + k), static_cast<uint32_t>(nw));
                 }
-            if (delta) atomicAdd(yw + (i0 >> 2), delta << sh0);
+            if (delta) {
+                if constexpr (APL == 8) {
+                    atomicAdd(reinterpret_cast<unsigned long long*>(y) + (i0 >> 3), delta);
+                } else {
+                    const uint32_t sh0 = static_cast<uint32_t>(i0 & 3) * 8u;
+                    atomicAdd(yw + (i0 >> 2), static_cast<uint32_t>(delta) << sh0);
+                }
+            }
         }
         const uint32_t wsurv = word_of<APL>(nib_i & ~recnib), wnons = word_of<APL>(nons);
         // B's bits of the non-S agents -> survivors / cleared S (B's words
@@ -873,7 +878,7 @@ public:
             sir_shard_range(n, rt.world, rt.rank, &lo, &nl, &shard);
             npl = shard;
         }
-        nq = sir_chunks(npl, 4) * kChunkMax;  // the step kernels work on chunks of up to 128 agents
+        nq = sir_chunks(npl, kChunkMax / 32) * kChunkMax;  // the step kernels work on chunks of up to 256 agents
         for (auto& b : x) {
             b.allocate(&rt, nq);
             AMBER_CUDA(cudaMemsetAsync(b.p, kPad, nq, rt.stream));
@@ -1004,13 +1009,14 @@ public:
         return a;
     }
 
-    // agents per lane of the step kernels ("apl" option; auto: 4 for large
+    // agents per lane of the step kernels ("apl" option; auto: 8 for large
     // populations, 1 where the step is latency-bound -- shorter warp tasks)
-    int lanes_apl() const { return apl ? apl : (npl > (1ll << 22) ? 4 : 1); }
+    int lanes_apl() const { return apl ? apl : (npl > (1ll << 22) ? 8 : 1); }
 
     void launch_step(int L, int blocks, int threads, const SirStepArgs& a)
     {
-        if (L == 4) sir_step_kernel<4><<<blocks, threads, 0, rt.stream>>>(a);
+        if (L == 8) sir_step_kernel<8><<<blocks, threads, 0, rt.stream>>>(a);
+        else if (L == 4) sir_step_kernel<4><<<blocks, threads, 0, rt.stream>>>(a);
         else if (L == 2) sir_step_kernel<2><<<blocks, threads, 0, rt.stream>>>(a);
         else sir_step_kernel<1><<<blocks, threads, 0, rt.stream>>>(a);
     }
@@ -1033,7 +1039,8 @@ public:
             const int L = lanes_apl();
             if (persistent && (chunk > 1 || dir != 0)) {
                 const int pthreads = block ? threads : kSirPT;
-                const void* fn = L == 4 ? reinterpret_cast<const void*>(sir_persistent_kernel<4>)
+                const void* fn = L == 8 ? reinterpret_cast<const void*>(sir_persistent_kernel<8>)
+                               : L == 4 ? reinterpret_cast<const void*>(sir_persistent_kernel<4>)
                                : L == 2 ? reinterpret_cast<const void*>(sir_persistent_kernel<2>)
                                         : reinterpret_cast<const void*>(sir_persistent_kernel<1>);
                 int per_sm = 0;
@@ -1234,7 +1241,7 @@ public:
         }
         if (k == "block") AMBER_REQUIRE(v <= 256, "SIR kernels are built for <= 256 threads per block");
         if (k == "apl") {
-            AMBER_REQUIRE(v == 0 || v == 1 || v == 2 || v == 4, "apl must be 0 (auto), 1, 2 or 4");
+            AMBER_REQUIRE(v == 0 || v == 1 || v == 2 || v == 4 || v == 8, "apl must be 0 (auto), 1, 2, 4 or 8");
             apl = static_cast<int>(v);
             return true;
         }

@@ -137,7 +137,7 @@ def sharded_sir(world, cfg):
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
-@pytest.mark.parametrize("apl", [0, 4])
+@pytest.mark.parametrize("apl", [0, 4, 8])
 def test_sharded_sir_equals_oracle(orc, world, apl):
     # NEXT-3: id-range shards, pull against the all-gathered I bitmap every step;
     # apl 4: 128-agent chunks that reach past a shard's end (masked)

@@ -235,7 +235,7 @@ def test_sweep_full_c5_all_replicates_vs_oracle_golden():
 
 @pytest.mark.parametrize("n", [37, 129, 4_097, 100_003])
 @pytest.mark.parametrize("direction", [1, 2])
-@pytest.mark.parametrize("apl", [1, 2, 4])
+@pytest.mark.parametrize("apl", [1, 2, 4, 8])
 def test_forced_direction_every_step_ragged(orc, n, direction, apl):
     # "direction" 1 = pull only, 2 = push whenever possible; both are the same
     # S3 draws, so each step must equal the oracle (128-agent chunks with a

@@ -35,7 +35,7 @@ def run(c, apl, reps):
 res = {}
 for name, c, reps in (("c2", W.C2_SIR, 5), ("v2", W.V2_SIR_SCALE, 1)):
     digs = set()
-    for apl in (1, 2, 4):
+    for apl in (1, 2, 4, 8):
         ms, d = run(c, apl, reps)
         digs.add(d)
         res[f"{name}_apl{apl}_ms"] = ms
