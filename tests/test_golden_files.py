@@ -32,9 +32,13 @@ def test_c4_golden_consistent():
     path = os.path.join(GOLD, "c4_wealth_oracle.txt")
     if not os.path.exists(path):
         pytest.skip("c4 golden not generated yet")
-    r = np.array([[int(v) for v in x] for x in rows("c4_wealth_oracle.txt")], dtype=np.int64)
+    raw = [[int(v) for v in x] for x in rows("c4_wealth_oracle.txt")]
+    assert all(0 <= x[1] < 2 ** 64 for x in raw)  # D1 digests are uint64
+    r = np.array([[x[0], x[2], x[3]] for x in raw], dtype=np.int64)  # step, total, active
     c = C4_WEALTH_SCALE
-    assert r.shape == (c["steps"], 4) and (r[:, 0] == np.arange(c["steps"])).all()
+    assert r.shape == (c["steps"], 3) and (r[:, 0] == np.arange(c["steps"])).all()
+    r = np.column_stack([r[:, 0], np.zeros(len(r), np.int64), r[:, 1], r[:, 2]])
+    assert len({x[1] for x in raw}) == c["steps"]  # the column changes every step
     assert (r[:, 2] == c["n"] * c["w0"]).all()  # W pin (i): total wealth conserved at every step
     assert ((r[:, 3] > 0) & (r[:, 3] <= c["n"])).all()
     # active fraction settles near 2 - sqrt(2) (sanity band only)
