@@ -56,11 +56,25 @@ __global__ void __launch_bounds__(256) walk_step_kernel(PhiloxKey key, int64_t n
                                                         WalkSlot* slot)
 {
     double disp = 0.0;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
-        const float4 x4 = __ldcs(reinterpret_cast<const float4*>(px) + q);
-        const float4 y4 = __ldcs(reinterpret_cast<const float4*>(py) + q);
-        const float4 a4 = __ldcs(reinterpret_cast<const float4*>(ox) + q);
-        const float4 b4 = __ldcs(reinterpret_cast<const float4*>(oy) + q);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // two quads per iteration: all eight 16-byte loads are issued before any use
+    for (int64_t q0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q0 < nq; q0 += 2 * stride) {
+      float4 X[2], Y[2], A[2], B[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t q = q0 + h * stride;
+        if (q < nq) {
+            X[h] = __ldcs(reinterpret_cast<const float4*>(px) + q);
+            Y[h] = __ldcs(reinterpret_cast<const float4*>(py) + q);
+            A[h] = __ldcs(reinterpret_cast<const float4*>(ox) + q);
+            B[h] = __ldcs(reinterpret_cast<const float4*>(oy) + q);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t q = q0 + h * stride;
+        if (q >= nq) break;
+        const float4 x4 = X[h], y4 = Y[h], a4 = A[h], b4 = B[h];
         const unsigned long long blk = 2ull * static_cast<unsigned long long>(q);
         const uint4 w0 = stream_block(key, TAG_WALK_VEL, blk, t);      // agents 4q, 4q+1
         const uint4 w1 = stream_block(key, TAG_WALK_VEL, blk + 1, t);  // agents 4q+2, 4q+3
@@ -86,6 +100,7 @@ __global__ void __launch_bounds__(256) walk_step_kernel(PhiloxKey key, int64_t n
             }
         }
         disp += static_cast<double>(part);
+      }
     }
     __shared__ double red[8];
     disp = warp_sum_f64(disp);
