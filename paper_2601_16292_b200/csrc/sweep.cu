@@ -161,9 +161,11 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
                 }
                 if (qc) walk_push(qc);
                 __syncthreads();
-                for (int64_t i = tid; i < a.n; i += nt) {
-                    n_inf += y[i] == kI;
-                    n_sus += y[i] == kS;
+                // counts of the pushed state, four bytes per load (padding bytes are 3)
+                for (int64_t q = tid; q < nq; q += nt) {
+                    const uint32_t v = reinterpret_cast<const uint32_t*>(y)[q];
+                    n_inf += __popc(__vcmpeq4(v, 0x01010101u)) >> 3;
+                    n_sus += __popc(__vcmpeq4(v, 0x00000000u)) >> 3;
                 }
             } else {
                 // pull, warp-cooperative: the susceptible agents of the warp's chunks
