@@ -268,7 +268,10 @@ int amber_read_metrics(amber_model* m, const char* name, void* dst, size_t dst_b
 int amber_reset_metrics(amber_model* m);
 
 /* D1 digest of a column's current value: sum_i mix64((i << 32) ^ bits32(v_i))
- * mod 2^64 over all agents (global when sharded).  Synchronising. */
+ * mod 2^64 over all agents (global when sharded).  Synchronising.  SIR models
+ * also accept "row_ptr" and "col_idx": the same sum over the int32 CSR arrays
+ * with the array index as i (the local rows of a shard, not all-reduced) --
+ * lets tests compare a full-size graph with an oracle-written golden digest. */
 int amber_digest(amber_model* m, const char* name, uint64_t* out);
 
 /* Model options (int64 values): "digest" (0/1: record a per-step digest of the

@@ -103,6 +103,8 @@ def lib():
             "orc_boids_step_brute_f64": (None, [C.c_int64, C.POINTER(BoidsParams)] + [f64p] * 8),
             "orc_sirs_init": (C.c_int, [C.c_int64, C.c_float, C.c_int64, C.c_uint64, f32p, f32p, u8p]),
             "orc_sirs_contacts": (C.c_int64, [C.c_int64, f32p, f32p, C.c_float, i32p, i32p, C.c_int64]),
+            "orc_sirs_contacts_grid": (C.c_int64, [C.c_int64, f32p, f32p, C.c_float, C.c_float, i32p, i32p,
+                                                   C.c_int64]),
             "orc_sirs_step": (None, [C.c_int64, i32p, i32p, C.c_uint64, C.c_uint32, C.c_uint64,
                                      C.c_uint64, u8p, u8p]),
             "orc_sirs_run": (C.c_int, [C.c_int64, i32p, i32p, C.c_uint64, C.c_double, C.c_double,
@@ -374,6 +376,18 @@ def sirs_contacts(px, py, r, cap=None):
     col = np.zeros(cap, np.int32)
     a = _check(int(lib().orc_sirs_contacts(n, _p(px, C.c_float), _p(py, C.c_float), r, _p(rp, C.c_int32),
                                            _p(col, C.c_int32), cap)))
+    return rp, col[:a].copy()
+
+
+def sirs_contacts_grid(px, py, L, r, cap=None):
+    """Same lists as sirs_contacts, found through a uniform grid (large n)."""
+    px, py = _f32(px), _f32(py)
+    n = px.size
+    cap = cap or max(64 * n, 1)
+    rp = np.zeros(n + 1, np.int32)
+    col = np.zeros(cap, np.int32)
+    a = _check(int(lib().orc_sirs_contacts_grid(n, _p(px, C.c_float), _p(py, C.c_float), L, r, _p(rp, C.c_int32),
+                                                _p(col, C.c_int32), cap)))
     return rp, col[:a].copy()
 
 

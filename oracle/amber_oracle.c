@@ -804,6 +804,86 @@ int64_t orc_sirs_contacts(int64_t n, const float* px, const float* py, float r, 
     return a;
 }
 
+/* C2 at scale: the same contact lists as orc_sirs_contacts (same float test,
+ * same ascending rows) found through a uniform grid instead of all pairs:
+ * nc = max(1, floor(L / (1.001 r))) cells per side of width L / nc >= r, so
+ * every pair within r lies in the same or an adjacent (clipped, no wrap)
+ * cell.  Plain counting sort of the agents by cell, then per agent the 3x3
+ * clipped stencil, the float test, and a sort of the row.  Pinned against
+ * orc_sirs_contacts (brute force) in tests/test_oracle_sirs.py. */
+int64_t orc_sirs_contacts_grid(int64_t n, const float* px, const float* py, float L, float r, int32_t* row_ptr,
+                               int32_t* col, int64_t cap)
+{
+    const float r2 = r * r;
+    int64_t nc = (int64_t)floor((double)L / (1.001 * (double)r));
+    if (nc < 1) nc = 1;
+    if (nc > 65536) nc = 65536;
+    const double cs = (double)L / (double)nc;
+    int64_t ncell = nc * nc;
+    int64_t* start = (int64_t*)calloc((size_t)ncell + 1, sizeof(int64_t));
+    int64_t* cell = (int64_t*)malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
+    int32_t* list = (int32_t*)malloc((size_t)(n > 0 ? n : 1) * sizeof(int32_t));
+    int32_t* row = NULL;
+    int64_t row_cap = 0;
+    if (!start || !cell || !list) { free(start); free(cell); free(list); return ORC_E_OOM; }
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t cx = (int64_t)((double)px[i] / cs), cy = (int64_t)((double)py[i] / cs);
+        if (cx < 0) cx = 0;
+        if (cx >= nc) cx = nc - 1;
+        if (cy < 0) cy = 0;
+        if (cy >= nc) cy = nc - 1;
+        cell[i] = cy * nc + cx;
+        start[cell[i] + 1] += 1;
+    }
+    for (int64_t c = 0; c < ncell; ++c) start[c + 1] += start[c];
+    {
+        int64_t* fill = (int64_t*)malloc((size_t)ncell * sizeof(int64_t));
+        if (!fill) { free(start); free(cell); free(list); return ORC_E_OOM; }
+        memcpy(fill, start, (size_t)ncell * sizeof(int64_t));
+        for (int64_t i = 0; i < n; ++i) list[fill[cell[i]]++] = (int32_t)i;  /* id order within a cell */
+        free(fill);
+    }
+    /* cell-ordered copies of the positions (the same float values) */
+    float* sx = (float*)malloc((size_t)(n > 0 ? n : 1) * sizeof(float));
+    float* sy = (float*)malloc((size_t)(n > 0 ? n : 1) * sizeof(float));
+    if (!sx || !sy) { free(sx); free(sy); free(start); free(cell); free(list); return ORC_E_OOM; }
+    for (int64_t q = 0; q < n; ++q) { sx[q] = px[list[q]]; sy[q] = py[list[q]]; }
+    int64_t a = 0;
+    row_ptr[0] = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t cx = cell[i] % nc, cy = cell[i] / nc, k = 0;
+        for (int64_t y = cy - 1; y <= cy + 1; ++y) {
+            if (y < 0 || y >= nc) continue;
+            for (int64_t x = cx - 1; x <= cx + 1; ++x) {
+                if (x < 0 || x >= nc) continue;
+                int64_t c = y * nc + x;
+                for (int64_t q = start[c]; q < start[c + 1]; ++q) {
+                    int64_t j = list[q];
+                    if (j == i) continue;
+                    float dx = sx[q] - px[i], dy = sy[q] - py[i];
+                    if (dx * dx + dy * dy <= r2) {
+                        if (k >= row_cap) {
+                            row_cap = row_cap ? 2 * row_cap : 64;
+                            int32_t* nr = (int32_t*)realloc(row, (size_t)row_cap * sizeof(int32_t));
+                            if (!nr) { free(row); free(sx); free(sy); free(start); free(cell); free(list); return ORC_E_OOM; }
+                            row = nr;
+                        }
+                        row[k++] = (int32_t)j;
+                    }
+                }
+            }
+        }
+        qsort(row, (size_t)k, sizeof(int32_t), cmp_i32);
+        if (a + k > cap) { free(row); free(sx); free(sy); free(start); free(cell); free(list); return ORC_E_INVALID; }
+        memcpy(col + a, row, (size_t)k * sizeof(int32_t));
+        a += k;
+        if (a > 2147483647) { free(row); free(sx); free(sy); free(start); free(cell); free(list); return ORC_E_INVALID; }
+        row_ptr[i + 1] = (int32_t)a;
+    }
+    free(row); free(sx); free(sy); free(start); free(cell); free(list);
+    return a;
+}
+
 /* C3: one synchronous step: a susceptible with at least one infected contact
  * takes ONE draw, lane32(0x41, i, t) < T(p_infect) (Listing 2); an infected
  * agent recovers iff lane32(0x43, i, t) < T(p_recover); R stays R. */

@@ -98,6 +98,8 @@ int orc_walk_run(int64_t n, float L, float vmax, uint64_t seed, uint32_t t0, int
 int orc_sirs_init(int64_t n, float L, int64_t k, uint64_t seed, float* px, float* py, uint8_t* state);
 int64_t orc_sirs_contacts(int64_t n, const float* px, const float* py, float r, int32_t* row_ptr, int32_t* col,
                           int64_t cap);
+int64_t orc_sirs_contacts_grid(int64_t n, const float* px, const float* py, float L, float r, int32_t* row_ptr,
+                               int32_t* col, int64_t cap);
 void orc_sirs_step(int64_t n, const int32_t* row_ptr, const int32_t* col, uint64_t seed, uint32_t t,
                    uint64_t t_inf, uint64_t t_rec, const uint8_t* x, uint8_t* x_next);
 int orc_sirs_run(int64_t n, const int32_t* row_ptr, const int32_t* col, uint64_t seed, double p_inf,

@@ -233,6 +233,8 @@ void destroy_wealth_exchange(WealthExchange* x)
 
 // Ship bucketed receivers to their owner ranks.  d_recv_total receives the
 // number of ids written contiguously into d_recv_ids.
+bool wealth_exchange_any(WealthExchange* x, Runtime& rt, bool local_flag);
+
 void wealth_exchange_run(WealthExchange* x, Runtime& rt, const unsigned int* d_send_counts,
                          const uint32_t* d_send_ids, uint64_t send_cap, uint32_t* d_recv_ids,
                          unsigned long long* d_recv_total)
@@ -276,13 +278,19 @@ void wealth_exchange_run(WealthExchange* x, Runtime& rt, const unsigned int* d_s
     AMBER_CUDA(cudaMemcpyAsync(x->h_recv.data(), x->recv_counts.p, W * sizeof(unsigned), cudaMemcpyDeviceToHost,
                                rt.stream));
     AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    // overflow is agreed on by every rank BEFORE any payload send/recv is
+    // posted, so no rank throws with a group open while its peers block in
+    // their matching grouped calls
+    bool over = false;
+    for (int p = 0; p < W; ++p)
+        if (p != me && (x->h_send[p] > send_cap || x->h_recv[p] > send_cap)) over = true;
+    if (wealth_exchange_any(x, rt, over)) fail(AMBER_E_CUDA, "wealth exchange: send bucket overflow (some rank)");
     // 2) payload: grouped point-to-point, received contiguously in peer order
     unsigned long long total = 0;
     nccl_check(api.GroupStart(), "ncclGroupStart");
     for (int p = 0; p < W; ++p) {
         if (p == me) continue;
-        const unsigned long long ns = std::min<unsigned long long>(x->h_send[p], send_cap);
-        if (x->h_send[p] > send_cap) fail(AMBER_E_CUDA, "wealth exchange: send bucket overflow");
+        const unsigned long long ns = x->h_send[p];
         if (ns) nccl_check(api.Send(d_send_ids + p * send_cap, ns, ncclUint32, p, x->comm->comm, rt.stream), "ncclSend");
         if (x->h_recv[p])
             nccl_check(api.Recv(d_recv_ids + total, x->h_recv[p], ncclUint32, p, x->comm->comm, rt.stream), "ncclRecv");

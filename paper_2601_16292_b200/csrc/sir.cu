@@ -691,24 +691,27 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
         const uint32_t recnib = recover_nib<APL>(a, static_cast<unsigned long long>(i0), t, nib_i);
         rec += __popc(recnib);
         if (nons) {
-            // the lane's bytes sit in one 32-bit word (64-bit for APL 8; i0 is a
-            // multiple of APL)
-            unsigned long long delta = 0;
+            // the lane's bytes sit in one 32-bit word (two for APL 8; i0 is a
+            // multiple of APL).  One signed delta per 32-bit word, applied with a
+            // 32-bit atomicAdd: exact mod 2^32 because every byte starts and ends
+            // in 0..3, and the same access size as the pushers' atomicOr on
+            // these words (no partially overlapping atomics).
+            constexpr int kW = APL == 8 ? 2 : 1;
+            uint32_t delta[kW] = {};
 #pragma unroll
             for (int k = 0; k < APL; ++k)
                 if ((nons >> k) & 1u) {
-                    const unsigned long long nw = ((nib_i & ~recnib) >> k) & 1u ? kI : kR;
-                    const unsigned long long old = (b_s >> k) & 1u ? kS : ((b_i >> k) & 1u ? kI : kR);
-                    delta += (nw - old) << (8 * k);  // mod 2^64: bytes stay in 0..3
-                    if (a.digest) dig += digest_term(static_cast<unsigned long long>(i0 + k), static_cast<uint32_t>(nw));
+                    const uint32_t nw = ((nib_i & ~recnib) >> k) & 1u ? kI : kR;
+                    const uint32_t old = (b_s >> k) & 1u ? kS : ((b_i >> k) & 1u ? kI : kR);
+                    delta[k >> 2] += (nw - old) << (8 * (k & 3));
+                    if (a.digest) dig += digest_term(static_cast<unsigned long long>(i0 + k), nw);
                 }
-            if (delta) {
-                if constexpr (APL == 8) {
-                    atomicAdd(reinterpret_cast<unsigned long long*>(y) + (i0 >> 3), delta);
-                } else {
-                    const uint32_t sh0 = static_cast<uint32_t>(i0 & 3) * 8u;
-                    atomicAdd(yw + (i0 >> 2), static_cast<uint32_t>(delta) << sh0);
-                }
+            if constexpr (APL == 8) {
+                if (delta[0]) atomicAdd(yw + (i0 >> 2), delta[0]);
+                if (delta[1]) atomicAdd(yw + (i0 >> 2) + 1, delta[1]);
+            } else if (delta[0]) {
+                const uint32_t sh0 = static_cast<uint32_t>(i0 & 3) * 8u;
+                atomicAdd(yw + (i0 >> 2), delta[0] << sh0);
             }
         }
         const uint32_t wsurv = word_of<APL>(nib_i & ~recnib), wnons = word_of<APL>(nons);
@@ -1211,7 +1214,14 @@ public:
 
     uint64_t digest(const char* name) override
     {
-        if (std::string(name) != "state") fail(AMBER_E_UNKNOWN_NAME, std::string("no column ") + name);
+        const std::string k(name);
+        // graph columns: D1 over the int32 bits with the array index as id (the
+        // local rows of a shard; no all-reduce -- test hook for full-size graphs)
+        if (k == "row_ptr")
+            return device_digest_u32(rt, reinterpret_cast<const uint32_t*>(g.row_ptr.p), nl + 1, 0);
+        if (k == "col_idx")
+            return device_digest_u32(rt, reinterpret_cast<const uint32_t*>(g.col.p), g.arcs, 0);
+        if (k != "state") fail(AMBER_E_UNKNOWN_NAME, std::string("no column ") + name);
         unsigned long long d = device_digest_u8(rt, x[cur].p, nl, lo);
         global_sum(&d, 1);
         return d;

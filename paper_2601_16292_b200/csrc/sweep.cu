@@ -53,6 +53,18 @@ struct SweepArgs {
     int64_t col_cap;         // u16 entries reserved in shared memory
 };
 
+// max over replicates k of row_ptr[(k+1) n] - row_ptr[k n] (arcs per replicate)
+__global__ void sweep_max_arcs_kernel(const int32_t* __restrict__ row_ptr, int64_t R, int64_t n,
+                                      unsigned int* __restrict__ out)
+{
+    unsigned int m = 0;
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < R;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        m = max(m, static_cast<unsigned int>(row_ptr[(k + 1) * n] - row_ptr[k * n]));
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
 template <bool COL_SMEM>
 __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
 {
@@ -313,12 +325,18 @@ void run_sweep(int64_t n, const amber_sir_params& base, const amber_replicate* r
         AMBER_CUDA(cudaMemcpyAsync(d_order.p, order.data(), B * sizeof(int), cudaMemcpyHostToDevice, rt.stream));
         d_next.zero_async(rt.stream);
         d_active.zero_async(rt.stream);
-        // max arcs of any replicate in the batch (for the shared-memory column stage)
-        std::vector<int32_t> h_rp(B * n + 1);
-        AMBER_CUDA(cudaMemcpyAsync(h_rp.data(), g.row_ptr.p, (B * n + 1) * 4, cudaMemcpyDeviceToHost, rt.stream));
+        // max arcs of any replicate in the batch (for the shared-memory column
+        // stage), reduced on the device: 4 bytes back instead of the row offsets
+        DevBuf<unsigned int> d_max;
+        d_max.allocate(&rt, 1);
+        d_max.zero_async(rt.stream);
+        sweep_max_arcs_kernel<<<static_cast<int>(std::min<int64_t>(ceil_div(B, 256), 1024)), 256, 0, rt.stream>>>(
+            g.row_ptr.p, B, n, d_max.p);
+        check_launch("sweep_max_arcs_kernel");
+        unsigned int h_max = 0;
+        AMBER_CUDA(cudaMemcpyAsync(&h_max, d_max.p, 4, cudaMemcpyDeviceToHost, rt.stream));
         AMBER_CUDA(cudaStreamSynchronize(rt.stream));
-        int64_t max_arcs = 0;
-        for (int64_t k = 0; k < B; ++k) max_arcs = std::max<int64_t>(max_arcs, h_rp[(k + 1) * n] - h_rp[k * n]);
+        const int64_t max_arcs = h_max;
         AMBER_CUDA(cudaEventRecord(e1, rt.stream));
         SweepArgs a{};
         a.row_ptr = g.row_ptr.p;

@@ -53,7 +53,8 @@ __device__ __forceinline__ float walk_comp(float p, uint32_t u, float vmax, floa
 __global__ void __launch_bounds__(256) walk_step_kernel(PhiloxKey key, int64_t n, int64_t nq, float vmax, float hi,
                                                         uint32_t t, float* __restrict__ px, float* __restrict__ py,
                                                         const float* __restrict__ ox, const float* __restrict__ oy,
-                                                        WalkSlot* slot)
+                                                        WalkSlot* slot, double* __restrict__ part,
+                                                        unsigned int* __restrict__ done)
 {
     double disp = 0.0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -102,14 +103,35 @@ __global__ void __launch_bounds__(256) walk_step_kernel(PhiloxKey key, int64_t n
         disp += static_cast<double>(part);
       }
     }
+    // Deterministic reduction (no floating-point atomics): each block writes its
+    // partial; the last block to finish sums the partials in a fixed order, so
+    // the metric is bit-reproducible from run to run for a given launch geometry.
     __shared__ double red[8];
+    __shared__ bool last;
     disp = warp_sum_f64(disp);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = disp;
     __syncthreads();
     if (threadIdx.x == 0) {
         double s = 0;
         for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += red[w];
-        atomicAdd(&slot->disp, s);
+        part[blockIdx.x] = s;
+        __threadfence();
+        last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double s = 0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) s += __ldcg(part + b);
+    s = warp_sum_f64(s);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += red[w];
+        slot->disp = tot;
+        *done = 0u;  // ready for the next launch (stream-ordered)
     }
 }
 
@@ -127,6 +149,8 @@ public:
     PhiloxKey key{};
     DevBuf<float> col[4];  // pos_x, pos_y, origin_x, origin_y
     DevBuf<WalkSlot> ring;
+    DevBuf<double> part;       // per-block partials of the step's displacement sum
+    DevBuf<unsigned int> done; // blocks finished (last-block reduction)
     int64_t m_first = 0;
 
     WalkModel(int64_t n_, const amber_walk_params& p_, uint64_t seed, const amber_runtime* r)
@@ -141,6 +165,8 @@ public:
         for (auto& c : col) c.allocate(&rt, n_pad);
         ring.allocate(&rt, metrics_cap);
         ring.zero_async(rt.stream);
+        done.allocate(&rt, 1);
+        done.zero_async(rt.stream);
         walk_init_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(key, n, n_pad, p.L, col[0].p, col[1].p, col[2].p,
                                                                col[3].p);
         check_launch("walk_init_kernel");
@@ -152,6 +178,8 @@ public:
         if (rt.stream) cudaStreamSynchronize(rt.stream);
         for (auto& c : col) c.reset();
         ring.reset();
+        part.reset();
+        done.reset();
         rt.destroy();
     }
 
@@ -164,21 +192,22 @@ public:
         const int g = grid ? static_cast<int>(grid)
                            : static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nq, threads),
                                                                                      rt.num_sms * 8)));
-        int64_t done = 0;
-        while (done < nsteps) {
-            const int64_t chunk = std::min<int64_t>(nsteps - done, metrics_cap);
+        if (part.n < static_cast<size_t>(g)) part.allocate(&rt, g);
+        int64_t ndone = 0;
+        while (ndone < nsteps) {
+            const int64_t chunk = std::min<int64_t>(nsteps - ndone, metrics_cap);
             walk_zero_slots<<<1, 256, 0, rt.stream>>>(ring.p, metrics_cap, t, chunk);
             check_launch("walk_zero_slots");
             for (int64_t k = 0; k < chunk; ++k) {
                 prof.launch(rt.stream, "walk_step", [&] {
                     walk_step_kernel<<<g, threads, 0, rt.stream>>>(key, n, nq, p.vmax, hi, static_cast<uint32_t>(t),
                                                                    col[0].p, col[1].p, col[2].p, col[3].p,
-                                                                   ring.p + (t % metrics_cap));
+                                                                   ring.p + (t % metrics_cap), part.p, done.p);
                 });
                 check_launch("walk_step_kernel");
                 ++t;
             }
-            done += chunk;
+            ndone += chunk;
         }
     }
 

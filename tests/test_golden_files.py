@@ -43,3 +43,18 @@ def test_c4_golden_consistent():
     assert ((r[:, 3] > 0) & (r[:, 3] <= c["n"])).all()
     # active fraction settles near 2 - sqrt(2) (sanity band only)
     assert abs(r[-100:, 3].mean() / c["n"] - (2 - np.sqrt(2))) < 0.02
+
+
+def test_v2_golden_consistent():
+    from paper_2601_16292_b200.workloads import V2_SIR_SCALE as c
+    lines = rows("v2_sir_oracle.txt")
+    g = dict(zip(lines[0][0::2], (int(v) for v in lines[0][1::2])))
+    m = int(np.floor(c["n"] * c["mean_degree"] / 2 + 0.5))
+    assert g["arcs"] == 2 * g["edges"]
+    dup = m - g["edges"]  # G4: expected duplicates M(M-1)/(N(N-1)) ~ 25
+    assert 0 < dup < 80
+    r = np.array([[int(v) for v in x] for x in lines[1:]], dtype=np.int64)
+    assert r.shape == (c["steps"], 5) and (r[:, 0] == np.arange(c["steps"])).all()
+    assert (r[:, 1:4].sum(1) == c["n"]).all()  # S pin (i)
+    assert (np.diff(r[:, 1]) <= 0).all() and (np.diff(r[:, 3]) >= 0).all()
+    assert len(set(r[:, 4].tolist())) == c["steps"]

@@ -21,6 +21,15 @@ def state(m):
     return tuple(m.read_column(c) for c in ("pos_x", "pos_y", "vel_x", "vel_y"))
 
 
+def oinit(orc, cfg, m):
+    """The ORACLE's initial state (B1) for cfg, after checking the device's is
+    bit-identical; the oracle is never stepped from device-produced state."""
+    ref = orc.boids_init(cfg["n"], cfg["L"], cfg["seed"])
+    for a, b in zip(state(m), ref):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    return ref
+
+
 def oparams(orc, cfg):
     return orc.boids_params(**{k: cfg[k] for k in KEYS})
 
@@ -36,7 +45,7 @@ def test_init_bit_exact(orc):
 def test_c3_one_step_tolerance_and_exact(orc):
     cfg = C3_BOIDS
     m = make(cfg)
-    st0 = state(m)
+    st0 = oinit(orc, cfg, m)
     m.step(1)
     got = state(m)
     ref = orc.boids_step(st0, oparams(orc, cfg))
@@ -55,7 +64,7 @@ def test_c3_one_step_brute_force_sample(orc):
     # full N, bench configuration: 300 agents checked against the O(N) brute-force scan
     cfg = C3_BOIDS
     m = make(cfg)
-    st0 = state(m)
+    st0 = oinit(orc, cfg, m)
     m.step(1)
     got = state(m)
     ids = np.random.default_rng(1).choice(cfg["n"], 300, replace=False)
@@ -68,7 +77,7 @@ def test_c3_one_step_brute_force_sample(orc):
 def test_c3_hundred_steps_ensemble(orc):
     cfg = C3_BOIDS
     m = make(cfg)
-    st0 = state(m)
+    st0 = oinit(orc, cfg, m)
     m.step(cfg["steps"])
     ms_g, po_g = m.metrics("mean_speed"), m.metrics("polarisation")
     ref, ms_o, po_o = orc.boids_run(st0, oparams(orc, cfg), cfg["steps"])
@@ -89,7 +98,7 @@ def test_dense_flock_tile_overflow_path(orc, monkeypatch, span):
     m = make(cfg)
     assert m.get_option("stencil_span") == int(span)
     m.set_option("tiled", 1)
-    st = state(m)
+    st = oinit(orc, cfg, m)
     P = oparams(orc, cfg)
     m.step(40)
     for _ in range(40):
@@ -103,7 +112,7 @@ def test_dense_flock_tile_overflow_path(orc, monkeypatch, span):
 def test_small_boxes_and_params(orc, kw):
     cfg = dict(C3_BOIDS, n=1500, seed=5, **kw)
     m = make(cfg)
-    st = state(m)
+    st = oinit(orc, cfg, m)
     m.step(15)
     P = oparams(orc, cfg)
     for _ in range(15):
@@ -145,7 +154,9 @@ def test_geometry_invariance_and_io(orc, monkeypatch):
             assert np.array_equal(x, y)
     c = make(cfg)
     c.step(3)
-    s = state(c)
+    s = orc.boids_run(oinit(orc, cfg, make(cfg)), oparams(orc, cfg), 3)[0]
+    for x, y in zip(state(c), s):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
     c.write_column("vel_x", s[2] * 0.5)
     assert np.array_equal(c.read_column("vel_x"), (s[2] * 0.5).astype(np.float32))
     assert c.digest("pos_x") == orc.digest(s[0])
@@ -156,7 +167,7 @@ def test_tiny_populations(orc, n):
     # degenerate cases: a single agent (no neighbours: straight line with wrap), pairs
     cfg = dict(C3_BOIDS, n=n, L=40.0, seed=13)
     m = make(cfg)
-    st = state(m)
+    st = oinit(orc, cfg, m)
     m.step(30)
     P = oparams(orc, cfg)
     for _ in range(30):
@@ -171,7 +182,7 @@ def test_large_grid_device_scan_and_edges(orc):
     cfg = dict(C3_BOIDS, n=30_000, L=3000.0, seed=17)
     m = make(cfg)
     assert m.get_option("cells_per_side") ** 2 > (1 << 16)
-    st = state(m)
+    st = oinit(orc, cfg, m)
     m.step(12)
     P = oparams(orc, cfg)
     for _ in range(12):
@@ -187,7 +198,7 @@ def test_fused_counts_across_calls_options_and_writes(orc):
     cfg = dict(C3_BOIDS, n=6_001, L=250.0, seed=29)
     m = make(cfg)
     P = oparams(orc, cfg)
-    st = state(m)
+    st = oinit(orc, cfg, m)
     plan = [(2, {}), (1, {"lanes": 4}), (2, {"lanes": 8}), (1, {"tiled": 1}), (2, {"tiled": 0}),
             (2, {"fused": 1, "lanes": 8}), (1, {"fused": 0}), ("write", None), (3, {"lanes": 4})]
     for k, opts in plan:

@@ -16,6 +16,15 @@ from paper_2601_16292_b200 import Model, boids_params, loopback_id, shard_range,
 from paper_2601_16292_b200.workloads import C5_SWEEP, sweep_replicates
 
 
+def oracle_graph(orc, cfg, m=None):
+    """The ORACLE's G(n, M) (orc_er_graph); when a one-GPU model is given, its
+    CSR must equal it.  The oracle is never stepped on a device-built graph."""
+    rp, col, _ = orc.er_graph(cfg["n"], orc.round_count(cfg["n"] * cfg["mean_degree"] / 2.0), cfg["seed"])
+    if m is not None:
+        assert np.array_equal(m.read_column("row_ptr"), rp) and np.array_equal(m.read_column("col_idx"), col)
+    return rp, col
+
+
 def par(items, fn):
     out = [None] * len(items)
     err = []
@@ -145,7 +154,7 @@ def test_sharded_sir_equals_oracle(orc, world, apl):
     steps = 40
     ref_m = Model("sir", cfg["n"], sir_params(cfg["mean_degree"], cfg["beta"], cfg["gamma"], cfg["init_frac"]),
                   cfg["seed"])
-    rp, col = ref_m.read_column("row_ptr"), ref_m.read_column("col_idx")
+    rp, col = oracle_graph(orc, cfg, ref_m)
     ref_m.close()
     st = orc.sir_init(cfg["n"], 500, cfg["seed"])
     ref, counts, dig = orc.sir_run(rp, col, st, cfg["seed"], cfg["beta"], cfg["gamma"], 0, steps, digests=True)
@@ -172,9 +181,11 @@ def test_sharded_sir_local_rows_and_column_write(orc):
     cfg = dict(n=20_000, mean_degree=6.0, beta=0.1, gamma=0.2, init_frac=0.005, seed=11)
     full = Model("sir", cfg["n"], sir_params(cfg["mean_degree"], cfg["beta"], cfg["gamma"], cfg["init_frac"]),
                  cfg["seed"])
-    rp, col = full.read_column("row_ptr"), full.read_column("col_idx")
+    rp, col = oracle_graph(orc, cfg, full)
     full.step(8)
-    mid = full.read_column("state")
+    mid = orc.sir_run(rp, col, orc.sir_init(cfg["n"], orc.round_count(cfg["init_frac"] * cfg["n"]), cfg["seed"]),
+                      cfg["seed"], cfg["beta"], cfg["gamma"], 0, 8)[0]
+    assert np.array_equal(full.read_column("state"), mid)
     ms = sharded_sir(2, cfg)
     for m in ms:  # local rows: offsets from 0, global neighbour ids
         _, _, lo, ln = m.column_info("state")
@@ -200,7 +211,7 @@ def test_sir_nccl_plumbing_single_rank(orc, monkeypatch):
     cfg = dict(n=30_001, mean_degree=8.0, beta=0.06, gamma=0.1, init_frac=0.01, seed=3)
     m = Model("sir", cfg["n"], sir_params(cfg["mean_degree"], cfg["beta"], cfg["gamma"], cfg["init_frac"]),
               cfg["seed"], unique_id=nccl_unique_id())
-    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
+    rp, col = oracle_graph(orc, cfg, m)
     m.step(25)
     st = orc.sir_init(cfg["n"], 300, cfg["seed"])
     ref, counts, _ = orc.sir_run(rp, col, st, cfg["seed"], cfg["beta"], cfg["gamma"], 0, 25)

@@ -5,7 +5,24 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 from paper_2601_16292_b200 import Model, sir_params, sweep
-from paper_2601_16292_b200.workloads import C2_SIR, C5_SWEEP, sir_counts, sweep_replicates
+from paper_2601_16292_b200.workloads import C2_SIR, C5_SWEEP, sweep_replicates
+
+
+def sir_counts(cfg):
+    """G1/S1 sizes by the oracle's own rounding (orc_round_count)."""
+    import oracle
+    return (oracle.round_count(cfg["n"] * cfg["mean_degree"] / 2.0),
+            oracle.round_count(cfg["init_frac"] * cfg["n"]))
+
+
+def oracle_graph(orc, m, cfg):
+    """The ORACLE's G(n, M) for cfg (orc_er_graph, never the device's CSR),
+    after checking that the device built exactly that graph; the oracle is
+    then stepped on its own graph."""
+    rp, col, mu = orc.er_graph(cfg["n"], sir_counts(cfg)[0], cfg["seed"])
+    assert np.array_equal(m.read_column("row_ptr"), rp)
+    assert np.array_equal(m.read_column("col_idx"), col)
+    return rp, col
 
 
 def make(cfg, **kw):
@@ -32,8 +49,7 @@ def test_c2_every_step_bit_exact(orc, persistent, digest):
     m = make(cfg)
     m.set_option("persistent", persistent)
     m.set_option("digest", digest)
-    rp = m.read_column("row_ptr")
-    col = m.read_column("col_idx")
+    rp, col = oracle_graph(orc, m, cfg)
     st = orc.sir_init(cfg["n"], sir_counts(cfg)[1], cfg["seed"])
     st_ref, counts, dig = orc.sir_run(rp, col, st, cfg["seed"], cfg["beta"], cfg["gamma"], 0,
                                       cfg["steps"], digests=True)
@@ -59,7 +75,7 @@ def test_special_cases(orc, beta, gamma):
     cfg = dict(n=3000, mean_degree=5.0, beta=beta, gamma=gamma, init_frac=0.003, seed=21)
     m = make(cfg)
     m.step(12)
-    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
+    rp, col = oracle_graph(orc, m, cfg)
     st = orc.sir_init(3000, 9, 21)
     ref, _, _ = orc.sir_run(rp, col, st, 21, beta, gamma, 0, 12)
     assert np.array_equal(m.read_column("state"), ref)
@@ -158,7 +174,7 @@ def test_large_population_dynamic_chunks(orc, digest):
     m.set_option("digest", digest)
     m.step(1)      # first call: push allowed from the seeded counts
     m.step(29)
-    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
+    rp, col = oracle_graph(orc, m, cfg)
     st = orc.sir_init(cfg["n"], 10_000, cfg["seed"])
     ref, counts, dig = orc.sir_run(rp, col, st, cfg["seed"], cfg["beta"], cfg["gamma"], 0, 30, digests=True)
     assert np.array_equal(m.read_column("state"), ref)
@@ -180,9 +196,12 @@ def test_mixed_launch_modes_and_column_write(orc):
     # a column write mid-epidemic, then push steps from the written state
     c = make(cfg)
     c.step(10)
-    mid = c.read_column("state")
+    crp, ccol = oracle_graph(orc, c, cfg)
+    mid = orc.sir_run(crp, ccol, orc.sir_init(cfg["n"], sir_counts(cfg)[1], cfg["seed"]), cfg["seed"],
+                      cfg["beta"], cfg["gamma"], 0, 10)[0]
+    assert np.array_equal(c.read_column("state"), mid)
     d = make(dict(cfg, seed=99))  # another graph: only the state matters after the write
-    rp, col = d.read_column("row_ptr"), d.read_column("col_idx")
+    rp, col = oracle_graph(orc, d, dict(cfg, seed=99))
     d.write_column("state", mid)
     d.set_step(10)
     d.step(15)
@@ -195,7 +214,7 @@ def test_full_occupancy_path_bit_exact(orc):
     cfg = dict(n=5_000_000, mean_degree=10.0, beta=0.05, gamma=0.1, init_frac=0.002, seed=29, steps=14)
     m = make(cfg)
     m.step(cfg["steps"])
-    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
+    rp, col = oracle_graph(orc, m, cfg)
     st = orc.sir_init(cfg["n"], 10_000, cfg["seed"])
     ref, counts, _ = orc.sir_run(rp, col, st, cfg["seed"], cfg["beta"], cfg["gamma"], 0, cfg["steps"])
     assert np.array_equal(m.read_column("state"), ref)
@@ -210,7 +229,7 @@ def test_small_metrics_ring_wraps(orc):
     m.set_option("metrics_capacity", 16)
     m.step(33)
     m.step(37)
-    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
+    rp, col = oracle_graph(orc, m, cfg)
     st = orc.sir_init(cfg["n"], 500, cfg["seed"])
     ref, counts, _ = orc.sir_run(rp, col, st, cfg["seed"], cfg["beta"], cfg["gamma"], 0, cfg["steps"])
     assert np.array_equal(m.read_column("state"), ref)
@@ -246,7 +265,7 @@ def test_forced_direction_every_step_ragged(orc, n, direction, apl):
     m.set_option("apl", apl)  # agents per lane of the step kernels
     assert m.get_option("apl") == apl
     m.set_option("digest", 1)
-    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
+    rp, col = oracle_graph(orc, m, cfg)
     x = orc.sir_init(n, sir_counts(cfg)[1], cfg["seed"])
     t = 0
     for chunk in (1, 1, 3, 1, 5, 2):
@@ -267,7 +286,7 @@ def test_column_write_recounts_and_keeps_history(orc):
     cfg = dict(n=30_011, mean_degree=8.0, beta=0.15, gamma=0.1, init_frac=0.02, seed=5)
     m = make(cfg)
     m.set_option("digest", 1)
-    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
+    rp, col = oracle_graph(orc, m, cfg)
     x = orc.sir_init(cfg["n"], sir_counts(cfg)[1], cfg["seed"])
     m.step(4)
     hist = [m.metrics(k).copy() for k in "SIR"]
@@ -291,3 +310,32 @@ def test_column_write_recounts_and_keeps_history(orc):
     m.step(1)
     y = orc.sir_step(rp, col, x, cfg["seed"], 2, cfg["beta"], cfg["gamma"])
     assert np.array_equal(m.read_column("state"), y)
+
+
+def _v2_golden():
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "v2_sir_oracle.txt")
+    lines = [ln.split() for ln in open(path) if not ln.startswith("#")]
+    g = dict(zip(lines[0][0::2], (int(v) for v in lines[0][1::2])))
+    steps = np.array([[int(v) for v in ln] for ln in lines[1:]], dtype=np.uint64)
+    return g, steps
+
+
+def test_v2_full_size_vs_oracle_golden():
+    # the SURVEY 8(d) roofline variant V2 at its full size (N = 1e8, 1e9 arcs), in
+    # the configuration the bench times (persistent, direction-optimizing, digest
+    # off): the device CSR against the oracle's row_ptr / col digests, the
+    # per-step S, I, R against the oracle's, and the final state's D1 digest --
+    # all from tests/golden/v2_sir_oracle.txt (written by tools/make_oracle_goldens.py
+    # v2, which calls only oracle/)
+    from paper_2601_16292_b200.workloads import V2_SIR_SCALE as cfg
+    g, want = _v2_golden()
+    m = make(cfg)
+    assert m.get_option("edges") == g["edges"]
+    assert m.digest("row_ptr") == g["row_ptr_digest"]
+    assert m.digest("col_idx") == g["col_digest"]
+    m.step(1)
+    m.step(cfg["steps"] - 1)
+    for k, name in enumerate("SIR"):
+        assert np.array_equal(m.metrics(name).astype(np.uint64), want[:, 1 + k]), name
+    assert m.digest("state") == int(want[-1, 4])

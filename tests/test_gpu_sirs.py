@@ -16,7 +16,8 @@ def make(cfg, **kw):
 
 
 def k_inf(cfg):
-    return int(np.floor(cfg["init_frac"] * cfg["n"] + 0.5))
+    import oracle
+    return oracle.round_count(cfg["init_frac"] * cfg["n"])
 
 
 def test_paper_size_bit_exact(orc):
@@ -47,23 +48,20 @@ def test_sizes_and_radii(orc, n, L, r):
     assert np.array_equal(m.read_column("state"), ref)
 
 
-def test_scale_contacts_sampled_and_steps(orc):
-    # N = 1e7 at the paper's density: contact rows of 200 sampled agents checked
-    # against a brute-force float32 scan; then 20 steps against the oracle on the
-    # (validated) contact graph
+def test_scale_contacts_all_rows_and_steps(orc):
+    # N = 1e7 at the paper's density: the oracle builds positions, initial state
+    # and the whole contact graph itself (its grid search, pinned against the
+    # all-pairs definition on CPU); the device's columns must equal them
+    # entirely; then 20 steps of the oracle on ITS graph vs the device
     cfg = SIRS_SCALE
     m = make(cfg)
-    px, py = m.read_column("pos_x"), m.read_column("pos_y")
-    rp, col = m.read_column("row_ptr"), m.read_column("col_idx")
-    r2 = np.float32(cfg["r"]) * np.float32(cfg["r"])
-    for i in np.random.default_rng(0).choice(cfg["n"], 200, replace=False):
-        dx = px - px[i]
-        dy = py - py[i]
-        d2 = dx * dx + dy * dy
-        want = np.nonzero(d2 <= r2)[0]
-        want = want[want != i]
-        assert np.array_equal(col[rp[i]:rp[i + 1]], want)
-    st = m.read_column("state")
-    ref, _ = orc.sirs_run(rp, col, st, cfg["seed"], cfg["p_infect"], cfg["p_recover"], 0, 20)
+    px, py, st = orc.sirs_init(cfg["n"], cfg["L"], k_inf(cfg), cfg["seed"])
+    assert np.array_equal(m.read_column("pos_x"), px) and np.array_equal(m.read_column("pos_y"), py)
+    assert np.array_equal(m.read_column("state"), st)
+    rp, col = orc.sirs_contacts_grid(px, py, cfg["L"], cfg["r"])
+    assert np.array_equal(m.read_column("row_ptr"), rp)
+    assert np.array_equal(m.read_column("col_idx"), col)
+    ref, counts = orc.sirs_run(rp, col, st, cfg["seed"], cfg["p_infect"], cfg["p_recover"], 0, 20)
     m.step(20)
     assert np.array_equal(m.read_column("state"), ref)
+    assert np.array_equal(m.metrics("I")[-20:], counts[:, 1])

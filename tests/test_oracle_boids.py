@@ -157,3 +157,35 @@ def test_c3_short_run_statistics(orc):
     st = orc.boids_init(cfg["n"], cfg["L"], cfg["seed"])
     _, ms, po = orc.boids_run(st, P, 2)
     assert 0.5 < ms[-1] <= 2.0 and po[-1] < 0.05
+
+
+def test_init_equals_curand_reformulation(orc, curand_host):
+    # B1 bit for bit: positions from 32-bit lanes 2i, 2i+1 of tag 0x20 (R4, R8);
+    # velocity by rejection in the unit disc with counter (lo32 i, hi32 i,
+    # attempt, 0x21), words 0 and 1; every draw from cuRAND's Philox routine,
+    # every float op a numpy float32 op (IEEE single rounding, no FMA)
+    n, L = 20_000, np.float32(1000.0)
+    for seed in (3, (7 << 32) | 3):
+        px, py, vx, vy = orc.boids_init(n, float(L), seed)
+        i = np.arange(n, dtype=np.uint64)
+        u01 = lambda w: (np.asarray(w, np.uint32) >> np.uint32(8)).astype(np.float32) * np.float32(2.0 ** -24)
+        assert np.array_equal(px, L * u01(curand_host.lane32(seed, 0x20, 2 * i, 0)))
+        assert np.array_equal(py, L * u01(curand_host.lane32(seed, 0x20, 2 * i + 1, 0)))
+        wx, wy = np.full(n, np.nan, np.float32), np.full(n, np.nan, np.float32)
+        todo, attempt, retried = np.arange(n, dtype=np.uint64), 0, 0
+        key = [[seed & 0xFFFFFFFF, seed >> 32]]
+        while todo.size:
+            ctr = np.stack([(todo & np.uint64(0xFFFFFFFF)).astype(np.uint32), (todo >> np.uint64(32)).astype(np.uint32),
+                            np.full(todo.size, attempt, np.uint32), np.full(todo.size, 0x21, np.uint32)], 1)
+            w = curand_host.blocks(ctr, key)
+            a = np.float32(2.0) * u01(w[:, 0]) - np.float32(1.0)
+            b = np.float32(2.0) * u01(w[:, 1]) - np.float32(1.0)
+            s2 = a * a + b * b
+            ok = (s2 > 0) & (s2 <= 1)
+            s = np.sqrt(s2[ok])
+            wx[todo[ok]], wy[todo[ok]] = a[ok] / s, b[ok] / s
+            todo, attempt = todo[~ok], attempt + 1
+            retried += int(todo.size)
+        assert retried > 0.15 * n  # about 1 - pi/4 of the agents need a second attempt
+        assert np.array_equal(vx.view(np.uint32), wx.view(np.uint32))
+        assert np.array_equal(vy.view(np.uint32), wy.view(np.uint32))

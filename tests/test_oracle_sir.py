@@ -203,3 +203,74 @@ def test_final_size_sanity(orc):
     lo = orc.sir_replicate(n, 8.0, 0.01, 0.1, 0.01, 1, 300) / n
     hi = orc.sir_replicate(n, 8.0, 0.2, 0.1, 0.01, 1, 300) / n
     assert lo < 0.2 and hi > 0.95
+
+
+# ---------------------------------------------------------------------------
+# Bit-level pin of the step's draw keying (S2/S3, R3-R5, R7): an independent
+# columnar re-formulation over the arc list whose every draw comes from
+# cuRAND's Philox routine (tests/pins) with explicitly composed counters, and
+# whose thresholds are exact rationals.  An off-by-one step index, a swapped
+# tag, a lane64/lane32 mix-up, a (max, min) pair order or a dropped key word
+# changes some state within a few steps and fails here.
+# ---------------------------------------------------------------------------
+def t_exact(p):
+    """R7 by exact rational arithmetic: ceil(p * 2^32); p >= 1 -> 2^32."""
+    import math
+    from fractions import Fraction
+    if p >= 1:
+        return 1 << 32
+    return math.ceil(Fraction(p) * (1 << 32))
+
+
+def numpy_sir_step(rp, col, x, seed, t, beta, gamma, curand_host):
+    """S2 over the arc list: s in S becomes I iff some arc (s, i) with x[i] = I has
+    word0(Philox(key = seed, ctr = (min, max, t, 0x10))) < T(beta); i in I
+    becomes R iff lane32(0x11, i, t) < T(gamma); R stays R."""
+    n = x.size
+    src = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
+    dst = col.astype(np.int64)
+    si = (x[src] == 0) & (x[dst] == 1)
+    s, i = src[si], dst[si]
+    lo, hi = np.minimum(s, i), np.maximum(s, i)
+    infected = np.zeros(n, bool)
+    if lo.size:
+        ctr = np.stack([lo.astype(np.uint32), hi.astype(np.uint32),
+                        np.full(lo.size, t, np.uint32), np.full(lo.size, TAG_TX, np.uint32)], 1)
+        w0 = curand_host.blocks(ctr, [[seed & 0xFFFFFFFF, seed >> 32]])[:, 0].astype(np.uint64)
+        infected[s[w0 < np.uint64(t_exact(beta))]] = True
+    rec = curand_host.lane32(seed, TAG_REC, np.arange(n, dtype=np.uint64), t).astype(np.uint64)
+    y = x.copy()
+    y[(x == 0) & infected] = 1
+    y[(x == 1) & (rec < np.uint64(t_exact(gamma)))] = 2
+    return y
+
+
+def test_t_exact_matches_survey_values(orc):
+    # R7 printed values (SURVEY 8(c) R7), exact
+    for p, want in [(0.05, 214_748_365), (0.1, 429_496_730), (0.01, 42_949_673), (0.2, 858_993_460)]:
+        assert t_exact(p) == want == orc.bernoulli_threshold(p)
+
+
+@pytest.mark.parametrize("seed,beta,gamma,t0", [(7, 0.05, 0.1, 0), ((5 << 32) | 7, 0.05, 0.1, 3),
+                                                (11, 0.3, 0.25, 17)])
+def test_sir_step_equals_curand_reformulation(orc, curand_host, seed, beta, gamma, t0):
+    # >= 20 steps at the BJ rates (and a fast epidemic), from step index t0,
+    # on a cuRAND/scipy-built graph and argsort-chosen initial infected
+    n, m, k = 3000, 15_000, 30
+    rp, col, _ = indep_graph(n, m, seed, curand_host)
+    keys = curand_host.lane64(seed, TAG_INIT, np.arange(n, dtype=np.uint64), 0)
+    x = np.zeros(n, np.uint8)
+    x[np.argsort(keys, kind="stable")[:k]] = 1
+    assert np.array_equal(orc.sir_init(n, k, seed), x)
+    ref = x.copy()
+    run_state, counts, _ = orc.sir_run(rp, col, x, seed, beta, gamma, t0, 24)
+    changed = 0
+    for j in range(24):
+        nxt = numpy_sir_step(rp, col, ref, seed, t0 + j, beta, gamma, curand_host)
+        got = orc.sir_step(rp, col, ref, seed, t0 + j, beta, gamma)
+        assert np.array_equal(got, nxt), f"step {t0 + j}"
+        assert counts[j].tolist() == [int((nxt == s).sum()) for s in range(3)]
+        changed += int((nxt != ref).sum())
+        ref = nxt
+    assert np.array_equal(run_state, ref)
+    assert changed > 200  # the epidemic actually moves (both transitions exercised)

@@ -8,7 +8,12 @@ calls nothing but oracle/):
   tests/golden/c5_sweep_oracle.txt    BASELINE config 5: the final R fraction of
       all 4,096 replicates as exact ratios R/N (~1-2 min, one process per core)
 
-python tools/make_oracle_goldens.py [c4] [c5]
+  tests/golden/v2_sir_oracle.txt      SURVEY 8(d) variant V2 (SIR on G(1e8, 5e8),
+      seed 7): the D1 digests of the oracle's CSR row_ptr / col arrays (array
+      index as id), then S, I, R and the state digest after each of the 20
+      steps (~10 min, ~20 GB of host memory)
+
+python tools/make_oracle_goldens.py [c4] [c5] [v2]
 """
 import multiprocessing as mp
 import os
@@ -73,7 +78,30 @@ def c5():
     print("wrote", path)
 
 
+def v2():
+    c = W.V2_SIR_SCALE
+    t0 = time.time()
+    n = c["n"]
+    m = oracle.round_count(n * c["mean_degree"] / 2.0)
+    k = oracle.round_count(c["init_frac"] * n)
+    rp, col, mu = oracle.er_graph(n, m, c["seed"])
+    d_rp = oracle.digest(rp.view(np.uint32))
+    d_col = oracle.digest(col.view(np.uint32))
+    st = oracle.sir_init(n, k, c["seed"])
+    _, counts, dig = oracle.sir_run(rp, col, st, c["seed"], c["beta"], c["gamma"], 0, c["steps"], digests=True)
+    path = os.path.join(ROOT, "tests", "golden", "v2_sir_oracle.txt")
+    with open(path, "w") as f:
+        f.write(f"# SURVEY 8(d) variant V2 (SIR on G(n={n}, M={m}), seed {c['seed']}, beta {c['beta']}, gamma "
+                f"{c['gamma']}, K={k} initially infected, {c['steps']} steps) by oracle/ "
+                f"(tools/make_oracle_goldens.py, repo {git_rev()}, {time.time() - t0:.0f} s)\n")
+        f.write(f"graph edges {mu} arcs {col.size} row_ptr_digest {d_rp} col_digest {d_col}\n")
+        f.write("# step S I R state_digest\n")
+        for t in range(c["steps"]):
+            f.write(f"{t} {int(counts[t, 0])} {int(counts[t, 1])} {int(counts[t, 2])} {int(dig[t])}\n")
+    print("wrote", path)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["c5", "c4"]
     for w in which:
-        {"c4": c4, "c5": c5}[w]()
+        {"c4": c4, "c5": c5, "v2": v2}[w]()
