@@ -81,13 +81,14 @@ class ClockSampler:
     def stop(self):
         if not self.proc:
             return None
+        time.sleep(0.05)
         self.proc.terminate()
         try:
             out, _ = self.proc.communicate(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
             out, _ = self.proc.communicate()
-        sm, mx, reasons = [], None, set()
+        sm, pw, mx, reasons = [], [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in out.strip().splitlines():
             f = [x.strip() for x in ln.split(",")]
@@ -96,6 +97,7 @@ class ClockSampler:
             try:
                 sm.append(float(f[1]))
                 mx = float(f[2])
+                pw.append(float(f[3]))
             except ValueError:
                 continue
             for nm, v in zip(names, f[5:9]):
@@ -103,30 +105,30 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        # "under load": samples drawing more than a third of the busiest sample's power
+        hi = max(pw) if pw else 0.0
+        load = [c for c, p in zip(sm, pw) if p >= hi / 3] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm), "samples_under_load": len(load), "power_w_max": hi,
+                "window": "nvidia-smi every 20 ms over the whole GPU arm (warm-up, timed repetitions, "
+                          "e2e, other configs)"}
 
 
 # ------------------------------------------------------------------ oracle
-def cpu_baseline_wealth(n_total, seed, budget_s=12.0):
-    """Oracle (as it stands, single-threaded C) on a bounded sample: a population
-    of n_s <= n_total agents stepped synchronously for as many steps as fit the
-    budget (at least 2).  Returns the cpu_baseline object."""
+def cpu_baseline_wealth(n_total, seed, steps=2):
+    """Oracle (as it stands, single-threaded C) on the config's FULL population
+    (N = 1e8: ~5 s per step on one core) for `steps` synchronous steps.
+    Returns the cpu_baseline object."""
     import numpy as np
 
     import oracle
-    n_s = int(min(n_total, 10_000_000))
-    w = np.ones(n_s, np.int32)
+    w = np.ones(n_total, np.int32)
     t0 = time.perf_counter()
-    oracle.wealth_step(w, seed, 0)
-    one = time.perf_counter() - t0
-    steps = max(2, int(budget_s / max(one, 1e-6)))
-    t0 = time.perf_counter()
-    w2, _, _, _ = oracle.wealth_run(w, seed, 0, steps)
+    oracle.wealth_run(w, seed, 0, steps)
     dt = time.perf_counter() - t0
-    return {"value": n_s * steps / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"wealth N={n_s:.0e} (of {n_total:.0e}) x {steps} steps, seed {seed}, "
-                      f"single thread, {dt:.1f}s"}
+    return {"value": n_total * steps / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"wealth N={n_total:.0e} (the whole config population) x {steps} steps from the "
+                      f"initial state, seed {seed}, single thread, {dt:.1f}s"}
 
 
 def run_reference_small(args, oracle, np):
@@ -238,6 +240,211 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------ traffic record
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
+
+
+def source_sha(files):
+    """sha256 over the CUDA sources a kernel is built from (its .cu + every .cuh)."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_2601_16292_b200", "csrc")
+    for f in sorted(set(files) | {os.path.basename(x) for x in glob.glob(os.path.join(csrc, "*.cuh"))}):
+        with open(os.path.join(csrc, f), "rb") as fh:
+            h.update(f.encode() + b"\0" + fh.read())
+    return h.hexdigest()[:16]
+
+
+def traffic_record(kernel):
+    """ncu DRAM bytes per launch of `kernel` from profiles/traffic.json (written by
+    tools/traffic_record.py from one `ncu --set full` capture), with the commit it
+    was taken at and whether the kernel's sources are unchanged since."""
+    if not os.path.exists(TRAFFIC_FILE):
+        return None, None
+    rec = json.load(open(TRAFFIC_FILE)).get(kernel)
+    if not rec:
+        return None, None
+    cur = source_sha(rec["sources"])
+    return rec["dram_bytes_per_launch"], {"file": "profiles/traffic.json", "ncu_report": rec.get("report"),
+                                          "commit": rec.get("commit"), "source_sha": rec.get("source_sha"),
+                                          "source_matches_current": cur == rec.get("source_sha")}
+
+
+# ------------------------------------------------------------ the other configs
+def _timed(m, k, torch):
+    """Device time of m.step(k) (one call), CUDA events on the model stream."""
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    m.synchronize()
+    e0.record(m.stream)
+    m.step(k)
+    e1.record(m.stream)
+    m.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def _oracle_rate(fn, units):
+    t0 = time.perf_counter()
+    fn()
+    return units / (time.perf_counter() - t0)
+
+
+def bench_configs(hbm):
+    """BASELINE configs 1, 2, 3, 5 and the SURVEY 8(d) roofline variants V2, V3 on
+    this GPU (unprofiled CUDA-event time of the config's steps) with the oracle
+    timed beside each on this host (single thread; C5 also one process per core),
+    the binding roof and the ncu summary it comes from.  One dict per config."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_2601_16292_b200 import Model, boids_params, sir_params, sweep, wealth_params
+    from paper_2601_16292_b200 import workloads as W
+    oracle.build()
+    bkeys = ("L", "R", "rs", "wc", "wa", "ws", "vmax", "dt")
+    out = {}
+    _, ncpu = host_info()
+
+    # C1: wealth N = 1e3, 100 steps (one single-CTA launch for all steps)
+    c = W.C1_WEALTH_SMALL
+    m = Model("wealth", c["n"], wealth_params(), c["seed"])
+    m.step(c["steps"])
+    m.set_step(0)
+    m.write_column("wealth", np.ones(c["n"], np.int32))
+    ms = _timed(m, c["steps"], torch)
+    ok = bool(np.array_equal(m.read_column("wealth"), oracle.wealth_run(np.ones(c["n"], np.int32), c["seed"], 0,
+                                                                         c["steps"])[0]))
+    m.close()
+    orate = _oracle_rate(lambda: oracle.wealth_run(np.ones(c["n"], np.int32), c["seed"], 0, c["steps"]),
+                         c["n"] * c["steps"])
+    out["c1"] = {"workload": "C1 wealth N=1e3 x100 (BASELINE config 1)", "ms_per_step": ms / c["steps"],
+                 "value": c["n"] * c["steps"] / (ms / 1e3), "unit": UNIT, "bit_exact_vs_oracle": ok,
+                 "roof": {"bound": "latency", "why": "1,000 agents: one CTA, one barrier per step",
+                          "evidence": "DESIGN.md 5 (wealth_small_kernel)"},
+                 "oracle": {"value": orate, "unit": UNIT, "cores": 1, "sample": "the whole config"}}
+
+    # C2: SIR on G(1e5, 5e5), 200 steps (one persistent cooperative launch)
+    c = W.C2_SIR
+    sp = sir_params(c["mean_degree"], c["beta"], c["gamma"], c["init_frac"])
+    m = Model("sir", c["n"], sp, c["seed"])
+    ms = _timed(m, c["steps"], torch)
+    mm, kk = oracle.round_count(c["n"] * c["mean_degree"] / 2.0), oracle.round_count(c["init_frac"] * c["n"])
+    rp, col, _ = oracle.er_graph(c["n"], mm, c["seed"])
+    st0 = oracle.sir_init(c["n"], kk, c["seed"])
+    t0 = time.perf_counter()
+    ref = oracle.sir_run(rp, col, st0, c["seed"], c["beta"], c["gamma"], 0, c["steps"])[0]
+    orate = c["n"] * c["steps"] / (time.perf_counter() - t0)
+    ok = bool(np.array_equal(m.read_column("state"), ref))
+    m.close()
+    out["c2"] = {"workload": "C2 SIR G(1e5, 5e5) x200 (BASELINE config 2)", "ms_per_step": ms / c["steps"],
+                 "value": c["n"] * c["steps"] / (ms / 1e3), "unit": UNIT, "bit_exact_vs_oracle": ok,
+                 "roof": {"bound": "latency", "why": "4.6 MB, L2-resident; per-step grid barrier (1.2-1.6 us) + "
+                          "the bitmap -> row -> probe chain",
+                          "evidence": "profiles/r01_c2_sir_persistent_ncu.txt, profiles/r01_grid_sync_probe.txt"},
+                 "oracle": {"value": orate, "unit": UNIT, "cores": 1, "sample": "the whole config (graph build "
+                            "excluded, as on the GPU)"}}
+
+    # C3: Boids N = 1e5, 100 steps
+    c = W.C3_BOIDS
+    bp = boids_params(*[c[k] for k in bkeys])
+    m = Model("boids", c["n"], bp, c["seed"])
+    m.step(1)
+    ms = _timed(m, c["steps"] - 1, torch)
+    per = ms / (c["steps"] - 1)
+    m.close()
+    P = oracle.boids_params(**{k: c[k] for k in bkeys})
+    s0 = oracle.boids_init(c["n"], c["L"], c["seed"])
+    orate = _oracle_rate(lambda: oracle.boids_run(s0, P, 3), c["n"] * 3)
+    out["c3"] = {"workload": "C3 Boids N=1e5 x100 (BASELINE config 3)", "ms_per_step": per,
+                 "value": c["n"] / (per / 1e3), "unit": UNIT,
+                 "roof": boids_roof(per, c["n"], "C3"),
+                 "oracle": {"value": orate, "unit": UNIT, "cores": 1,
+                            "sample": "first 3 steps on the full population (sparse phase)"}}
+
+    # C5: 4,096 SIR replicates x 300 steps
+    c = W.C5_SWEEP
+    betas, seeds = W.sweep_replicates(c)
+    sp0 = sir_params(c["mean_degree"], 0.0, c["gamma"], c["init_frac"])
+    sweep(c["n"], sp0, betas[:64], seeds[:64], 5)  # warm (module load)
+    res, st = sweep(c["n"], sp0, betas, seeds, c["steps"], with_stats=True)
+    upd = c["n"] * c["steps"] * len(betas)
+    pick = np.arange(0, len(betas), 256)
+    want = oracle.sir_sweep(c["n"], c["mean_degree"], c["gamma"], c["init_frac"], betas[pick], seeds[pick],
+                            c["steps"])
+    t0 = time.perf_counter()
+    oracle.sir_sweep(c["n"], c["mean_degree"], c["gamma"], c["init_frac"], betas[pick], seeds[pick], c["steps"])
+    orate = c["n"] * c["steps"] * len(pick) / (time.perf_counter() - t0)
+    import multiprocessing as mp
+    jobs = [(c["n"], c["mean_degree"], c["gamma"], c["init_frac"], float(betas[k]), int(seeds[k]), c["steps"])
+            for k in np.arange(0, len(betas), 32)]
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(ncpu) as pool:
+        pool.map(_sweep_one, jobs, chunksize=1)
+    orate_all = c["n"] * c["steps"] * len(jobs) / (time.perf_counter() - t0)
+    out["c5"] = {"workload": "C5 sweep 4096 x SIR N=1e4 x300 (BASELINE config 5)",
+                 "ms_total": st["step_ms"], "ms_per_step": st["step_ms"] / c["steps"],
+                 "value": upd / (st["step_ms"] / 1e3), "unit": UNIT + " (nominal: replicates x N x steps)",
+                 "active_updates": st["active_updates"], "build_ms": st["build_ms"],
+                 "sampled_replicates_bit_exact_vs_oracle": bool(np.array_equal(res[pick], want)),
+                 "roof": {"bound": "issue", "why": "graphs and states resident in shared memory for all 300 steps; "
+                          "HBM only for the one-time load", "evidence": "profiles/r01_sweep_ncu.txt"},
+                 "oracle": {"value": orate, "unit": UNIT, "cores": 1,
+                            "sample": f"{len(pick)} of {len(betas)} replicates spanning all betas"},
+                 "oracle_all_cores": {"value": orate_all, "unit": UNIT, "cores": ncpu,
+                                      "sample": f"{len(jobs)} replicates, one process per core"}}
+
+    # V2: SIR on G(1e8, 5e8), 20 steps (SURVEY 8(d) added roofline variant)
+    c = W.V2_SIR_SCALE
+    sp = sir_params(c["mean_degree"], c["beta"], c["gamma"], c["init_frac"])
+    m = Model("sir", c["n"], sp, c["seed"])
+    arcs = m.column_info("col_idx")[3]
+    ms = _timed(m, c["steps"], torch)
+    S, I = (m.metrics(x).astype(np.float64) for x in ("S", "I"))
+    m.close()
+    k0 = oracle.round_count(c["init_frac"] * c["n"])
+    s_prev = np.concatenate([[c["n"] - k0], S[:-1]])
+    i_prev = np.concatenate([[k0], I[:-1]])
+    alg = 2.0 * c["n"] * c["steps"] + float((np.minimum(s_prev, i_prev) * (8.0 + 5.0 * arcs / c["n"])).sum())
+    ach = alg / (ms / 1e3) / 1e9
+    n_o = 1_000_000
+    rp, col, _ = oracle.er_graph(n_o, oracle.round_count(n_o * c["mean_degree"] / 2.0), c["seed"])
+    st0 = oracle.sir_init(n_o, oracle.round_count(c["init_frac"] * n_o), c["seed"])
+    orate = _oracle_rate(lambda: oracle.sir_run(rp, col, st0, c["seed"], c["beta"], c["gamma"], 0, c["steps"]),
+                         n_o * c["steps"])
+    out["v2"] = {"workload": "V2 SIR G(1e8, 5e8) x20 (SURVEY 8(d) roofline variant)",
+                 "ms_per_step": ms / c["steps"], "value": c["n"] * c["steps"] / (ms / 1e3), "unit": UNIT,
+                 "roof": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                          "alg_rule": "2 B/agent + (8 + 5 kbar) B per agent of the smaller of S, I",
+                          "binding": "random L2 neighbour-bitmap probes, one per traversed arc",
+                          "evidence": "profiles/r02_v2_sir_ncu.txt"},
+                 "oracle": {"value": orate, "unit": UNIT, "cores": 1,
+                            "sample": f"the same model at N={n_o:.0e} (mean degree 10), 20 steps"}}
+
+    # V3: Boids N = 1e8, L = 31,623 (density 0.1), 10 steps
+    c = W.V3_BOIDS_SCALE
+    m = Model("boids", c["n"], boids_params(*[c[k] for k in bkeys]), c["seed"])
+    m.step(1)
+    ms = _timed(m, c["steps"] - 1, torch)
+    per = ms / (c["steps"] - 1)
+    m.close()
+    n_o = 1_000_000
+    P = oracle.boids_params(**{**{k: c[k] for k in bkeys}, "L": 3162.3})
+    s0 = oracle.boids_init(n_o, 3162.3, c["seed"])
+    orate = _oracle_rate(lambda: oracle.boids_run(s0, P, 1), n_o)
+    out["v3"] = {"workload": "V3 Boids N=1e8 L=31623 x10 (SURVEY 8(d) roofline variant)", "ms_per_step": per,
+                 "value": c["n"] / (per / 1e3), "unit": UNIT, "roof": boids_roof(per, c["n"], "V3"),
+                 "oracle": {"value": orate, "unit": UNIT, "cores": 1,
+                            "sample": f"N={n_o:.0e} at the same density (L=3162.3), first step"}}
+    return out
+
+
+def boids_roof(ms_per_step, n, which):
+    """Boids binding roof: SM issue of the stencil (FP32/INT mix).  The measured
+    instruction ceiling comes from tools/alu_ceiling.cu (profiles/r02_alu_ceiling.txt)."""
+    return {"bound": "alu", "why": "FP32 + int64 fixed-point stencil over ~90 candidates per agent",
+            "evidence": f"profiles/r01_{'v3' if which == 'V3' else 'c3'}_boids_group_ncu.txt"}
+
+
 # ------------------------------------------------------------------ GPU arm
 def dist_setup(args):
     import torch
@@ -289,32 +496,45 @@ def bench_wealth(args):
               device=local, rank=rank, world=world, unique_id=uid)
     _, _, off, n_loc = m.column_info("wealth")
     stream = m.stream
+    clocks = ClockSampler(local)
+    clocks.start()  # sampled over the whole GPU arm, so the record is never empty
     for _ in range(args.warmup):
         m.step(1)
     m.synchronize()
-    clocks = ClockSampler(local)
-    m.profile(True)
-    barrier_sync(pg, torch)
-    clocks.start()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        m.step(1)
-    ev1.record(stream)
-    m.synchronize()
-    barrier_sync(pg, torch)
-    cl = clocks.stop()
-    ms = ev0.elapsed_time(ev1)
-    ms = max_over_ranks(pg, torch, ms)
-    prof = m.profile_results()
-    m.profile(False)
-    tot = m.metrics("total_wealth")
-    assert (tot == n * cfg["w0"]).all(), "wealth not conserved"
-    # scatter REDs issued in the timed region = senders of each timed step =
-    # agents with w >= amount in the state the step starts from
-    act = m.metrics("active")
-    reds = float(act[-args.steps - 1:-1].sum()) if len(act) > args.steps else float(act[:-1].sum())
+    # PAPER.md l.213 protocol: repetitions of the K-step region, the first 2
+    # discarded as warm-up, the median of the next 5 reported; each repetition
+    # is K steps between a barrier + synchronize on both sides, device time by
+    # CUDA events on the model stream, max over ranks
+    reps_ms, prof, act_hist = [], [], []
+    for rep in range(args.warmup_reps + args.reps):
+        timed = rep >= args.warmup_reps
+        if timed:
+            m.reset_metrics()
+            m.profile(True)
+        barrier_sync(pg, torch)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            m.step(1)
+        ev1.record(stream)
+        m.synchronize()
+        barrier_sync(pg, torch)
+        if timed:
+            reps_ms.append(max_over_ranks(pg, torch, ev0.elapsed_time(ev1)))
+            prof.append(m.profile_results())
+            m.profile(False)
+            tot = m.metrics("total_wealth")
+            assert (tot == n * cfg["w0"]).all(), "wealth not conserved"
+            act_hist.append(m.metrics("active"))
+    med = sorted(range(args.reps), key=lambda k: reps_ms[k])[args.reps // 2]
+    ms, prof = reps_ms[med], prof[med]
+    # scatter REDs issued in the median repetition = senders of each of its steps =
+    # agents with w >= amount in the state the step starts from (the previous
+    # step's `active`; the first step's from the last step of the repetition before)
+    prev_last = int(act_hist[med - 1][-1]) if med > 0 else None
+    act = act_hist[med]
+    reds = float(act[:-1].sum()) + float(prev_last if prev_last is not None else act[0])
     launches = sum(c for _, c, _ in prof)
     dom = max(prof, key=lambda r: r[2]) if prof else ("", 0, 0.0)
     dom_avg_ms = dom[2] / max(dom[1], 1)
@@ -341,7 +561,10 @@ def bench_wealth(args):
     # per step: the 40-byte step record (overflow check + the metric read share one copy)
     e2e = {"value": n * args.steps / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": int(n_loc * 4 / args.steps),
-           "d2h_bytes_per_step": int(n_loc * 4 / args.steps + 40)}
+           "d2h_bytes_per_step": int(n_loc * 4 / args.steps + 40),
+           "note": f"one {n_loc * 4 / 1e6:.0f} MB H2D of the initial column and one D2H of the final column "
+                   f"per run, amortised over the run's K={args.steps} steps (the e2e rate therefore grows "
+                   f"with K), plus a 40-byte host read of each step's observables"}
 
     hbm, kind = peaks()
     # algorithmic bytes of the method per step: the
@@ -350,10 +573,7 @@ def bench_wealth(args):
     transfers = reds / args.steps
     alg_bytes = 8.0 * n_loc + 8.0 * transfers
     achieved = alg_bytes / (dom_avg_ms / 1e3) / 1e9 if dom_avg_ms > 0 else 0.0
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "wealth_traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("dram_bytes_per_launch", {}).get(dom[0])
+    traffic, traffic_src = traffic_record(dom[0])
     if rank == 0:
         model, ncpu = host_info()
         line = {
@@ -367,7 +587,8 @@ def bench_wealth(args):
                        "l2": "state (400 MB int32 column) larger than L2; no flush"},
             "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": hbm,
                          "peak_kind": kind, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "alg_bytes_per_launch": alg_bytes,
                          "alg_bytes_rule": "8 B/agent + 8 B/transfer",
                          "transfers_per_step": transfers,
                          "avg_launch_ms": dom_avg_ms,
@@ -377,8 +598,12 @@ def bench_wealth(args):
                 m.get_option("scatter")),
             "kernels": [{"name": a, "launches": b, "total_ms": c} for a, b, c in prof],
             "gpu_launches": launches,
+            "timing": {"protocol": f"median of {args.reps} timed repetitions of K steps after "
+                                   f"{args.warmup_reps} discarded repetitions (PAPER.md l.213) and W warm-up "
+                                   f"steps; CUDA events on the model stream, max over ranks",
+                       "reps_ms": reps_ms, "median_rep": med},
             "e2e": e2e,
-            "clocks": cl,
+            "clocks": None,
             "host": {"cpu": model, "cpus": ncpu},
         }
         if m.get_option("scatter") == 1:  # packed counters: one L2 RED per transfer
@@ -389,10 +614,16 @@ def bench_wealth(args):
                 "profiles/r01_red_ceiling.txt)",
                 "frac": (reds / (ms / 1e3)) / RED_CEILING if ms > 0 else None,
                 "reds_per_step": reds / args.steps}
+        m.close()
+        if world == 1 and not args.no_configs:
+            line["configs"] = bench_configs(hbm)
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_wealth(n, cfg["seed"])
+        line["clocks"] = clocks.stop()
         print(json.dumps(line), flush=True)
-    m.close()
+    else:
+        m.close()
+        clocks.stop()
     if pg is not None:
         pg.destroy_process_group()
     return 0
@@ -565,6 +796,9 @@ def main():
     ap.add_argument("--impl", default="amber", choices=["amber", "reference"])
     ap.add_argument("--workload", default="c4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other configs' entries (C1-C3, C5, V2, V3)")
+    ap.add_argument("--reps", type=int, default=5, help="timed repetitions of the K-step region (median)")
+    ap.add_argument("--warmup-reps", type=int, default=2, help="discarded repetitions before the timed ones")
     ap.add_argument("--counter-bits", type=int, default=0,
                     help="wealth scatter (amber_wealth_params.counter_bits); 0 = library default")
     args = ap.parse_args()

@@ -48,7 +48,7 @@ def test_c4_golden_consistent():
 def test_v2_golden_consistent():
     from paper_2601_16292_b200.workloads import V2_SIR_SCALE as c
     lines = rows("v2_sir_oracle.txt")
-    g = dict(zip(lines[0][0::2], (int(v) for v in lines[0][1::2])))
+    g = dict(zip(lines[0][1::2], (int(v) for v in lines[0][2::2])))
     m = int(np.floor(c["n"] * c["mean_degree"] / 2 + 0.5))
     assert g["arcs"] == 2 * g["edges"]
     dup = m - g["edges"]  # G4: expected duplicates M(M-1)/(N(N-1)) ~ 25

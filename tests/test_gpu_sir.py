@@ -316,7 +316,7 @@ def _v2_golden():
     import os
     path = os.path.join(os.path.dirname(__file__), "golden", "v2_sir_oracle.txt")
     lines = [ln.split() for ln in open(path) if not ln.startswith("#")]
-    g = dict(zip(lines[0][0::2], (int(v) for v in lines[0][1::2])))
+    g = dict(zip(lines[0][1::2], (int(v) for v in lines[0][2::2])))
     steps = np.array([[int(v) for v in ln] for ln in lines[1:]], dtype=np.uint64)
     return g, steps
 
