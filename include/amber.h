@@ -112,10 +112,8 @@ typedef struct {
     int32_t counter_bits; /* scatter of the transfers: {0 (default = 4), 2, 4, 8, 16, 32} =
                              per-receiver counter width for L2 atomics (narrow counters stay
                              L2-resident; an overflow is detected exactly and the step window
-                             is replayed with 32-bit counters); -1 = range-partitioned
-                             counting sort through shared memory (single GPU, N <= 2^28);
-                             -2 = fused range-binned step (single GPU, 1024..4096 ranges of
-                             2^16 agents; otherwise falls back to 4-bit counters) */
+                             is replayed with 32-bit counters); any other value is
+                             AMBER_E_INVALID_ARG */
 } amber_wealth_params;
 
 /* SIR on G(n, M) (Sec. 5.1.1, Listing 2;
@@ -286,12 +284,11 @@ int amber_digest(amber_model* m, const char* name, uint64_t* out);
  * counts are known -- identical results, for tests and probes; 1 or 2 also
  * run a single step through the cooperative kernel), SIR "apl" (agents per
  * lane of the step kernels: 0 = auto (8 above 2^22 agents, else 1), 1, 2, 4
- * or 8 -- identical results); Boids: "lanes" (1/4/8/16 lanes per agent in the
- * stencil, default 4; "fused" runs only at 8), "tiled", "fused" (measured
- * alternatives, identical results).
+ * or 8 -- identical results); Boids: "lanes" (4/8/16 lanes per agent in the
+ * stencil, default 4 -- identical results).
  * Read-only (amber_get_option): wealth "replays" (exact-replay count, after
- * the overflow check), "counter_bits", "scatter" (0 bins, 1 packed-counter
- * atomics, 2 fused bins, 3 segmented bins), "exchange" (sharded: 0 none,
+ * the overflow check), "counter_bits", "scatter" (1: packed-counter L2
+ * atomics, the one shipped scatter), "exchange" (sharded: 0 none,
  * 1 NCCL send/recv, 2 P2P peer-mapped buckets; set at the first step); SIR
  * "edges"; Boids "cells_per_side", sharded Boids "own_agents" and
  * "slab_columns". */

@@ -37,7 +37,6 @@ constexpr float kFix = 16777216.0f;  // 2^24 (B3)
 #ifndef AMBER_BOIDS_MINB
 #define AMBER_BOIDS_MINB 4  // resident 256-thread blocks per SM for the stencil kernel (register cap 64)
 #endif
-constexpr int kTileCap = 3072;        // staged halo agents per tile (48 KB)
 
 struct BoidsArgs {
     float L, R, rs, wc, wa, ws, vmax, dt;
@@ -217,131 +216,6 @@ __device__ __forceinline__ float min_image(float d, float L, float halfL)
 }
 
 
-// B2-B6 for every agent (sorted order in, sorted order out).
-__global__ void __launch_bounds__(256) boids_step_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ sids,
-                                                         const int* __restrict__ start, int64_t n, BoidsArgs a,
-                                                         float4* __restrict__ out, int32_t* __restrict__ out_ids,
-                                                         BoidsSlot* slot, int digest)
-{
-    const float L = a.L, halfL = __fmul_rn(0.5f, a.L), R2 = __fmul_rn(a.R, a.R), rs2 = __fmul_rn(a.rs, a.rs);
-    double sp_sum = 0.0, ux_sum = 0.0, uy_sum = 0.0;
-    unsigned long long dig = 0;
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-        const float4 me = sorted[p];
-        const int cx = cell_coord(me.x, a), cy = cell_coord(me.y, a);
-        Acc acc{0, 0, 0, 0, 0, 0, 0};
-        const int span = a.nc >= 3 ? a.span : 0;  // nc == 1: the single cell is visited once
-#pragma unroll 1
-        for (int dyc = -span; dyc <= span; ++dyc) {
-            int yy = cy + dyc;
-            yy = yy < 0 ? yy + a.nc : (yy >= a.nc ? yy - a.nc : yy);
-#pragma unroll 1
-            for (int dxc = -span; dxc <= span; ++dxc) {
-                int xx = cx + dxc;
-                xx = xx < 0 ? xx + a.nc : (xx >= a.nc ? xx - a.nc : xx);
-                const int c = yy * a.nc + xx;
-                const int b = start[c], e = start[c + 1];
-                for (int q = b; q < e; ++q) {
-                    if (q == p) continue;
-                    const float4 o = sorted[q];
-                    const float dx = min_image(__fsub_rn(o.x, me.x), L, halfL);
-                    const float dy = min_image(__fsub_rn(o.y, me.y), L, halfL);
-                    const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-                    if (d2 <= R2) {
-                        const long long qx = q24(dx), qy = q24(dy);
-                        acc.n += 1;
-                        acc.sdx += qx;
-                        acc.sdy += qy;
-                        acc.svx += q24(o.z);
-                        acc.svy += q24(o.w);
-                        if (d2 <= rs2) {
-                            acc.ssx += qx;
-                            acc.ssy += qy;
-                        }
-                    }
-                }
-            }
-        }
-        float ux = me.z, uy = me.w;
-        if (acc.n > 0) {
-            const double nd = static_cast<double>(acc.n);
-            const double fix = 16777216.0;
-            const float cohx = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.sdx), fix), nd));
-            const float cohy = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.sdy), fix), nd));
-            const float avx = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.svx), fix), nd));
-            const float avy = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.svy), fix), nd));
-            const float sepx = __double2float_rn(__ddiv_rn(static_cast<double>(acc.ssx), fix));
-            const float sepy = __double2float_rn(__ddiv_rn(static_cast<double>(acc.ssy), fix));
-            ux = __fsub_rn(__fadd_rn(__fadd_rn(me.z, __fmul_rn(a.wc, cohx)), __fmul_rn(a.wa, __fsub_rn(avx, me.z))),
-                           __fmul_rn(a.ws, sepx));
-            uy = __fsub_rn(__fadd_rn(__fadd_rn(me.w, __fmul_rn(a.wc, cohy)), __fmul_rn(a.wa, __fsub_rn(avy, me.w))),
-                           __fmul_rn(a.ws, sepy));
-        }
-        const float s2 = __fadd_rn(__fmul_rn(ux, ux), __fmul_rn(uy, uy));
-        if (s2 > __fmul_rn(a.vmax, a.vmax)) {
-            const float f = __fdiv_rn(a.vmax, __fsqrt_rn(s2));
-            ux = __fmul_rn(ux, f);
-            uy = __fmul_rn(uy, f);
-        }
-        float x = __fadd_rn(me.x, __fmul_rn(ux, a.dt));
-        float y = __fadd_rn(me.y, __fmul_rn(uy, a.dt));
-        if (x < 0.0f) x = __fadd_rn(x, L);
-        if (x >= L) x = __fsub_rn(x, L);
-        if (y < 0.0f) y = __fadd_rn(y, L);
-        if (y >= L) y = __fsub_rn(y, L);
-        out[p] = make_float4(x, y, ux, uy);
-        const int32_t id = sids[p];
-        out_ids[p] = id;
-        // observables (B8), in double
-        const double dvx = static_cast<double>(ux), dvy = static_cast<double>(uy);
-        const double sp = __dsqrt_rn(__dadd_rn(__dmul_rn(dvx, dvx), __dmul_rn(dvy, dvy)));
-        sp_sum += sp;
-        if (sp > 0.0) {
-            ux_sum += __ddiv_rn(dvx, sp);
-            uy_sum += __ddiv_rn(dvy, sp);
-        }
-        if (digest) dig += digest_term(static_cast<unsigned long long>(id), __float_as_uint(x));
-    }
-    // block reduction of the observables
-    __shared__ double red[3][32];
-    __shared__ unsigned long long dred[32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    sp_sum = warp_sum_f64(sp_sum);
-    ux_sum = warp_sum_f64(ux_sum);
-    uy_sum = warp_sum_f64(uy_sum);
-    dig = warp_sum_u64(dig);
-    if (lane == 0) {
-        red[0][wid] = sp_sum;
-        red[1][wid] = ux_sum;
-        red[2][wid] = uy_sum;
-        dred[wid] = dig;
-    }
-    __syncthreads();
-    if (wid == 0) {
-        double s0 = lane < nw ? red[0][lane] : 0.0, s1 = lane < nw ? red[1][lane] : 0.0, s2v = lane < nw ? red[2][lane] : 0.0;
-        unsigned long long d = lane < nw ? dred[lane] : 0ull;
-        s0 = warp_sum_f64(s0);
-        s1 = warp_sum_f64(s1);
-        s2v = warp_sum_f64(s2v);
-        d = warp_sum_u64(d);
-        if (lane == 0) {
-            atomicAdd(&slot->mean_speed, s0);
-            atomicAdd(&slot->polar_x, s1);
-            atomicAdd(&slot->polar_y, s2v);
-            if (digest) atomicAdd(&slot->digest, d);
-        }
-    }
-}
-
-// ---------------------------------------------------------------- tiled step
-// CTA per tile of kT x kT cells.  The (kT+2)^2 halo cells' agents are staged
-// in shared memory (float4 each, contiguous cell runs of the sorted array);
-// each thread then handles inner agents and scans their 3x3 stencil from
-// shared memory.  Tiles whose halo exceeds the staging capacity (dense
-// flocks) read the candidates from global memory instead.  Identical
-// arithmetic to boids_step_kernel (B2-B6), so identical results.
-constexpr int kT = 4, kW = kT + 2, kHalo = kW * kW;
-
 // WRAP = false: the caller guarantees |o - me| <= L/2 per coordinate (both
 // agents in interior cells), where the minimum image is the identity.
 template <bool WRAP = true>
@@ -396,166 +270,6 @@ __device__ __forceinline__ float4 boid_update_means(const float4 me, const Acc& 
     if (y < 0.0f) y = __fadd_rn(y, L);
     if (y >= L) y = __fsub_rn(y, L);
     return make_float4(x, y, ux, uy);
-}
-
-__device__ __forceinline__ float4 boid_update(const float4 me, const Acc& acc, const BoidsArgs& a)
-{
-    const float L = a.L;
-    float ux = me.z, uy = me.w;
-    if (acc.n > 0) {
-        const double nd = static_cast<double>(acc.n);
-        const double fix = 16777216.0;
-        const float cohx = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.sdx), fix), nd));
-        const float cohy = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.sdy), fix), nd));
-        const float avx = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.svx), fix), nd));
-        const float avy = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc.svy), fix), nd));
-        const float sepx = __double2float_rn(__ddiv_rn(static_cast<double>(acc.ssx), fix));
-        const float sepy = __double2float_rn(__ddiv_rn(static_cast<double>(acc.ssy), fix));
-        ux = __fsub_rn(__fadd_rn(__fadd_rn(me.z, __fmul_rn(a.wc, cohx)), __fmul_rn(a.wa, __fsub_rn(avx, me.z))),
-                       __fmul_rn(a.ws, sepx));
-        uy = __fsub_rn(__fadd_rn(__fadd_rn(me.w, __fmul_rn(a.wc, cohy)), __fmul_rn(a.wa, __fsub_rn(avy, me.w))),
-                       __fmul_rn(a.ws, sepy));
-    }
-    const float s2 = __fadd_rn(__fmul_rn(ux, ux), __fmul_rn(uy, uy));
-    if (s2 > __fmul_rn(a.vmax, a.vmax)) {
-        const float f = __fdiv_rn(a.vmax, __fsqrt_rn(s2));
-        ux = __fmul_rn(ux, f);
-        uy = __fmul_rn(uy, f);
-    }
-    float x = __fadd_rn(me.x, __fmul_rn(ux, a.dt));
-    float y = __fadd_rn(me.y, __fmul_rn(uy, a.dt));
-    if (x < 0.0f) x = __fadd_rn(x, L);
-    if (x >= L) x = __fsub_rn(x, L);
-    if (y < 0.0f) y = __fadd_rn(y, L);
-    if (y >= L) y = __fsub_rn(y, L);
-    return make_float4(x, y, ux, uy);
-}
-
-__global__ void __launch_bounds__(256) boids_tile_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ sids,
-                                                         const int* __restrict__ start, BoidsArgs a, int tiles_per_side,
-                                                         int cap, float4* __restrict__ out, int32_t* __restrict__ out_ids,
-                                                         BoidsSlot* slot, int digest)
-{
-    extern __shared__ __align__(16) float4 sa[];
-    __shared__ int hstart[kHalo + 1], hglob[kHalo], hcnt[kHalo];
-    __shared__ int istart[kT * kT + 1], ihalo[kT * kT];
-    const int tid = threadIdx.x;
-    const int tx0 = (blockIdx.x % tiles_per_side) * kT, ty0 = (blockIdx.x / tiles_per_side) * kT;
-    const int nc = a.nc;
-    if (tid < kHalo) {
-        const int hx = tid % kW, hy = tid / kW;
-        int cx = tx0 + hx - 1, cy = ty0 + hy - 1;
-        cx = cx < 0 ? cx + nc : (cx >= nc ? cx - nc : cx);
-        cy = cy < 0 ? cy + nc : (cy >= nc ? cy - nc : cy);
-        const int c = cy * nc + cx;
-        hglob[tid] = start[c];
-        hcnt[tid] = start[c + 1] - start[c];
-    }
-    __syncthreads();
-    if (tid == 0) {
-        int acc = 0;
-        for (int h = 0; h < kHalo; ++h) {
-            hstart[h] = acc;
-            acc += hcnt[h];
-        }
-        hstart[kHalo] = acc;
-        int ia = 0, j = 0;
-        for (int iy = 1; iy <= kT; ++iy)
-            for (int ix = 1; ix <= kT; ++ix) {
-                const bool real = tx0 + ix - 1 < nc && ty0 + iy - 1 < nc;
-                const int h = iy * kW + ix;
-                istart[j] = ia;
-                ihalo[j] = h;
-                ia += real ? hcnt[h] : 0;
-                ++j;
-            }
-        istart[kT * kT] = ia;
-    }
-    __syncthreads();
-    const int total = hstart[kHalo];
-    const bool staged = total <= cap;
-    if (staged) {
-        for (int k = tid; k < total; k += blockDim.x) {
-            int lo = 0, hi = kHalo - 1;  // halo cell of staged entry k
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (hstart[mid] <= k) lo = mid;
-                else hi = mid - 1;
-            }
-            sa[k] = sorted[hglob[lo] + (k - hstart[lo])];
-        }
-    }
-    __syncthreads();
-    const float L = a.L, halfL = __fmul_rn(0.5f, a.L), R2 = __fmul_rn(a.R, a.R), rs2 = __fmul_rn(a.rs, a.rs);
-    const float4* base = staged ? sa : sorted;
-    double sp_sum = 0.0, ux_sum = 0.0, uy_sum = 0.0;
-    unsigned long long dig = 0;
-    const int n_inner = istart[kT * kT];
-    for (int k = tid; k < n_inner; k += blockDim.x) {
-        int lo = 0, hi = kT * kT - 1;  // inner cell of inner agent k
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (istart[mid] <= k) lo = mid;
-            else hi = mid - 1;
-        }
-        const int h = ihalo[lo];
-        const int off = k - istart[lo];
-        const int p = hglob[h] + off;                          // global sorted index
-        const int me_i = staged ? hstart[h] + off : p;         // index in `base`
-        const float4 me = base[me_i];
-        Acc acc{0, 0, 0, 0, 0, 0, 0};
-        const int hx = h % kW, hy = h / kW;
-#pragma unroll 1
-        for (int dyc = -1; dyc <= 1; ++dyc)
-#pragma unroll 1
-            for (int dxc = -1; dxc <= 1; ++dxc) {
-                const int h2 = (hy + dyc) * kW + hx + dxc;
-                const int b = staged ? hstart[h2] : hglob[h2];
-                const int e = b + hcnt[h2];
-                for (int q = b; q < e; ++q)
-                    if (q != me_i) boid_accumulate(base[q], me, L, halfL, R2, rs2, acc);
-            }
-        const float4 nx = boid_update(me, acc, a);
-        out[p] = nx;
-        const int32_t id = sids[p];
-        out_ids[p] = id;
-        const double dvx = static_cast<double>(nx.z), dvy = static_cast<double>(nx.w);
-        const double sp = __dsqrt_rn(__dadd_rn(__dmul_rn(dvx, dvx), __dmul_rn(dvy, dvy)));
-        sp_sum += sp;
-        if (sp > 0.0) {
-            ux_sum += __ddiv_rn(dvx, sp);
-            uy_sum += __ddiv_rn(dvy, sp);
-        }
-        if (digest) dig += digest_term(static_cast<unsigned long long>(id), __float_as_uint(nx.x));
-    }
-    __shared__ double red[3][8];
-    __shared__ unsigned long long dred[8];
-    const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-    sp_sum = warp_sum_f64(sp_sum);
-    ux_sum = warp_sum_f64(ux_sum);
-    uy_sum = warp_sum_f64(uy_sum);
-    dig = warp_sum_u64(dig);
-    if (lane == 0) {
-        red[0][wid] = sp_sum;
-        red[1][wid] = ux_sum;
-        red[2][wid] = uy_sum;
-        dred[wid] = dig;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        double s0 = 0, s1 = 0, s2v = 0;
-        unsigned long long d = 0;
-        for (int w = 0; w < nw; ++w) {
-            s0 += red[0][w];
-            s1 += red[1][w];
-            s2v += red[2][w];
-            d += dred[w];
-        }
-        atomicAdd(&slot->mean_speed, s0);
-        atomicAdd(&slot->polar_x, s1);
-        atomicAdd(&slot->polar_y, s2v);
-        if (digest) atomicAdd(&slot->digest, d);
-    }
 }
 
 // ---------------------------------------------------------------- grouped step
@@ -749,95 +463,6 @@ __global__ void __launch_bounds__(256, AMBER_BOIDS_MINB) boids_group_kernel(cons
                                                           int* __restrict__ next_cell)
 {
     boids_group_body<G>(sorted, sids, start, n, a, out, out_ids, slot, digest, next_cnt, next_cell);
-}
-
-// All steps of a call in ONE cooperative launch: per step, bin counts ->
-// grid barrier -> block 0 scans -> barrier -> counting-sort scatter -> barrier
-// -> grouped stencil step (writes the next state in the new order) -> barrier.
-struct BoidsPersistArgs {
-    float4* st;          // current state (current order), overwritten each step
-    int32_t* ids;
-    float4* sorted;      // scratch: cell-sorted copy
-    int32_t* sids;
-    int *cnt, *start, *cursor, *cell_of, *block_sums;
-    int64_t n;
-    int ncell;
-    BoidsArgs a;
-    BoidsSlot* ring;
-    int64_t ring_cap, t0, steps;
-    int digest;
-};
-
-__global__ void __launch_bounds__(256, 4) boids_persistent_kernel(const BoidsPersistArgs P)
-{
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
-    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t nthr = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    using Scan = cub::BlockScan<int, 256>;
-    using BlockSum = cub::BlockReduce<int, 256>;
-    __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ typename BlockSum::TempStorage sum_tmp;
-    __shared__ int carry;
-    for (int64_t k = 0; k < P.steps; ++k) {
-        // 1) cell of every agent + counts
-        for (int64_t p = tid; p < P.n; p += nthr) {
-            const float4 s = P.st[p];
-            const int c = cell_coord(s.y, P.a) * P.a.nc + cell_coord(s.x, P.a);
-            P.cell_of[p] = c;
-            atomicAdd(P.cnt + c, 1);
-        }
-        grid.sync();
-        // 2) exclusive scan of the counts, spread over all blocks: block b owns
-        //    cells [b*C, (b+1)*C); (a) chunk totals, barrier, (b) offset = sum of
-        //    the preceding totals, chunk scan, write start/cursor, re-zero counts
-        {
-            const int C = (P.ncell + gridDim.x - 1) / gridDim.x;
-            const int c0 = blockIdx.x * C, c1 = min(c0 + C, P.ncell);
-            int s = 0;
-            for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) s += P.cnt[c];
-            const int tot = BlockSum(sum_tmp).Sum(s);
-            if (threadIdx.x == 0) P.block_sums[blockIdx.x] = tot;
-        }
-        grid.sync();
-        {
-            const int C = (P.ncell + gridDim.x - 1) / gridDim.x;
-            const int c0 = blockIdx.x * C, c1 = min(c0 + C, P.ncell);
-            int pre = 0;
-            for (int j = threadIdx.x; j < static_cast<int>(blockIdx.x); j += blockDim.x) pre += P.block_sums[j];
-            __syncthreads();
-            pre = BlockSum(sum_tmp).Sum(pre);
-            if (threadIdx.x == 0) carry = pre;
-            __syncthreads();
-            for (int base = c0; base < c1; base += blockDim.x) {
-                const int c = base + threadIdx.x;
-                const int v = c < c1 ? P.cnt[c] : 0;
-                int ex, agg;
-                Scan(scan_tmp).ExclusiveSum(v, ex, agg);
-                if (c < c1) {
-                    P.start[c] = carry + ex;
-                    P.cursor[c] = carry + ex;
-                    P.cnt[c] = 0;
-                }
-                __syncthreads();
-                if (threadIdx.x == 0) carry += agg;
-                __syncthreads();
-            }
-            if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) P.start[P.ncell] = static_cast<int>(P.n);
-        }
-        grid.sync();
-        // 3) counting-sort placement
-        for (int64_t p = tid; p < P.n; p += nthr) {
-            const int q = atomicAdd(P.cursor + P.cell_of[p], 1);
-            P.sorted[q] = P.st[p];
-            P.sids[q] = P.ids[p];
-        }
-        grid.sync();
-        // 4) the step (next state in sorted order, which becomes the current order)
-        const int64_t t = P.t0 + k;
-        boids_group_body<8>(P.sorted, P.sids, P.start, P.n, P.a, P.st, P.ids, P.ring + (t % P.ring_cap), P.digest);
-        grid.sync();
-    }
 }
 
 // Un-permute: column k of the state (0 x, 1 y, 2 vx, 3 vy) into id order.
@@ -1167,13 +792,11 @@ public:
     DevBuf<BoidsSlot> ring;
     int64_t m_first = 0;
     int ncell = 0;
-    int64_t tiled = 0;  // 1: shared-memory tiled stencil kernel (slower once flocks cluster)
     // lanes per agent in the stencil scan (1 = one-lane kernel; 4, 8, 16): 4 measured
     // best for both the clustered C3 (54 vs 58 us at 8) and the uniform V3 (22.6
     // vs 32.7 ms): two shuffle levels for the seven int64 sums instead of three,
     // and eight agents per warp (tools/boids_lanes_probe.py)
     int64_t lanes = 4;
-    int64_t fused = 0;  // 1: all phases of all steps in one cooperative launch (measured slower, r01)
     bool counted = false;  // cnt / cell_of hold the cell counts of the current state (from the last group step)
 
     BoidsModel(int64_t n_, const amber_boids_params& p_, uint64_t seed_, const amber_runtime* r)
@@ -1187,24 +810,17 @@ public:
                       "Boids params out of range (need L, R, vmax > 0, 0 <= rs <= R, dt >= 0)");
         AMBER_REQUIRE(p.R < 0.5f * p.L && p.vmax * p.dt < 0.5f * p.L, "Boids needs R < L/2 and vmax*dt < L/2");
         ba = BoidsArgs{p.L, p.R, p.rs, p.wc, p.wa, p.ws, p.vmax, p.dt, 0, 0.f, 1};
-        // Cells of side >= R*(1+1e-3) with a 3x3 stencil (default), or >= R/2*(1+1e-3)
-        // with a 5x5 stencil (AMBER_BOIDS_SPAN=2: 25 (R/2)^2 vs 9 R^2, about 30% fewer
-        // candidates, but five short row runs per agent instead of three: measured
-        // slower, C3 99 vs 83 us/step, V3 34.9 vs 32.1 ms/step).  The margin means float
+        // Cells of side >= R*(1+1e-3) with a 3x3 stencil.  The margin means float
         // rounding of the cell index can never hide a neighbour outside the
         // stencil.  The stencil needs >= 3 distinct cells per side; boxes with
         // fewer use one cell holding every agent (each agent then scans all
         // others, i.e. the brute-force definition).  Any covering stencil gives
-        // the same result (exact fixed-point sums, B3).
+        // the same result (exact fixed-point sums, B3).  (A 5x5 stencil of R/2
+        // cells has ~30% fewer candidates but five short row runs per agent:
+        // measured slower, C3 99 vs 83 us, V3 34.9 vs 32.1 ms; not shipped.)
         const double nc1 = std::min(std::floor(static_cast<double>(p.L) / (static_cast<double>(p.R) * 1.001)), 4096.0);
-        const double nc2 = std::min(std::floor(static_cast<double>(p.L) / (static_cast<double>(p.R) * 0.5005)), 8192.0);
-        const double area1 = 9.0 * std::pow(p.L / std::max(nc1, 1.0), 2), area2 = 25.0 * std::pow(p.L / std::max(nc2, 1.0), 2);
-        const char* hc = getenv("AMBER_BOIDS_SPAN");
-        const bool half = nc2 >= 7 && hc && hc[0] == '2';
-        (void)area1;
-        (void)area2;
-        ba.nc = half ? static_cast<int>(nc2) : static_cast<int>(nc1 >= 3 ? nc1 : 1);
-        ba.span = half ? 2 : 1;
+        ba.nc = static_cast<int>(nc1 >= 3 ? nc1 : 1);
+        ba.span = 1;
         ba.inv_cs = static_cast<float>(ba.nc / static_cast<double>(p.L));
         ncell = ba.nc * ba.nc;
         st.allocate(&rt, n);
@@ -1220,8 +836,6 @@ public:
         scan_tmp.allocate(&rt, scan_bytes + 16);
         ring.allocate(&rt, metrics_cap);
         ring.zero_async(rt.stream);
-        AMBER_CUDA(cudaFuncSetAttribute(boids_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(kTileCap * sizeof(float4))));
         boids_init_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(philox_key(seed), n, p.L, st.p, ids.p);
         check_launch("boids_init_kernel");
         AMBER_CUDA(cudaStreamSynchronize(rt.stream));
@@ -1244,34 +858,6 @@ public:
     void step(int64_t nsteps) override
     {
         AMBER_REQUIRE(nsteps >= 0, "n_steps must be >= 0");
-        if (fused && ba.nc >= 3 && !tiled && lanes == 8 && nsteps > 0) {
-            // the cooperative kernel counts from zeroed counters
-            if (counted) AMBER_CUDA(cudaMemsetAsync(cnt.p, 0, static_cast<size_t>(ncell) * sizeof(int), rt.stream));
-            int64_t done = 0;
-            while (done < nsteps) {
-                const int64_t chunk = std::min<int64_t>(nsteps - done, metrics_cap);
-                boids_zero_slots<<<1, 256, 0, rt.stream>>>(ring.p, metrics_cap, t, chunk);
-                check_launch("boids_zero_slots");
-                int per_sm = 0;
-                AMBER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, boids_persistent_kernel, 256, 0));
-                int blocks = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(per_sm) * rt.num_sms,
-                                                                std::max<int64_t>(1, ceil_div(n * 8, 256))));
-                if (grid) blocks = static_cast<int>(std::min<int64_t>(grid, static_cast<int64_t>(per_sm) * rt.num_sms));
-                if (static_cast<int64_t>(block_sums.n) < blocks) block_sums.allocate(&rt, blocks);
-                BoidsPersistArgs P{st.p, ids.p, sorted.p, sids.p, cnt.p, start.p, cursor.p, cell_of.p, block_sums.p, n, ncell, ba,
-                                   ring.p, metrics_cap, t, chunk, digest_on ? 1 : 0};
-                void* kargs[] = {&P};
-                prof.launch(rt.stream, "boids_persistent", [&] {
-                    AMBER_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(boids_persistent_kernel), blocks, 256,
-                                                           kargs, 0, rt.stream));
-                });
-                check_launch("boids_persistent_kernel");
-                t += chunk;
-                done += chunk;
-            }
-            counted = false;
-            return;
-        }
         const int threads = block ? static_cast<int>(std::min<int64_t>(block, 256)) : 256;
         for (int64_t k = 0; k < nsteps; ++k) {
             if (k % metrics_cap == 0) {  // this call's records, a ring's worth at a time
@@ -1318,23 +904,7 @@ public:
                 check_launch("boids_scatter_kernel");
             }
             const BoidsArgs a = ba;
-            if (ba.nc >= 3 && tiled && ba.span == 1) {  // the tiled stencil is 3x3 only
-                const int tps = (ba.nc + kT - 1) / kT;
-                prof.launch(rt.stream, "boids_step", [&] {
-                    boids_tile_kernel<<<tps * tps, 256, kTileCap * sizeof(float4), rt.stream>>>(
-                        sorted.p, sids.p, start.p, a, tps, kTileCap, st.p, ids.p, ring.p + (t % metrics_cap),
-                        digest_on ? 1 : 0);
-                });
-                check_launch("boids_tile_kernel");
-            } else if (lanes == 1) {
-                prof.launch(rt.stream, "boids_step", [&] {
-                    boids_step_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a,
-                                                                                    st.p, ids.p,
-                                                                                    ring.p + (t % metrics_cap),
-                                                                                    digest_on ? 1 : 0);
-                });
-                check_launch("boids_step_kernel");
-            } else {
+            {
                 const int g = grid ? static_cast<int>(grid)
                                    : static_cast<int>(std::max<int64_t>(
                                          1, std::min<int64_t>(ceil_div(n * lanes, threads), rt.num_sms * 8)));
@@ -1467,16 +1037,8 @@ public:
             return true;
         }
         if (k == "block") AMBER_REQUIRE(v <= 256, "Boids kernels are built for <= 256 threads per block");
-        if (k == "tiled") {
-            tiled = v ? 1 : 0;
-            return true;
-        }
-        if (k == "fused") {
-            fused = v ? 1 : 0;
-            return true;
-        }
         if (k == "lanes") {
-            AMBER_REQUIRE(v == 1 || v == 4 || v == 8 || v == 16, "lanes must be 1, 4, 8 or 16");
+            AMBER_REQUIRE(v == 4 || v == 8 || v == 16, "lanes must be 4, 8 or 16");
             lanes = v;
             return true;
         }
@@ -1487,14 +1049,6 @@ public:
     {
         if (std::string(key) == "cells_per_side") {
             *v = ba.nc;
-            return true;
-        }
-        if (std::string(key) == "stencil_span") {
-            *v = ba.span;
-            return true;
-        }
-        if (std::string(key) == "tiled") {
-            *v = tiled;
             return true;
         }
         if (std::string(key) == "lanes") {

@@ -461,20 +461,6 @@ public:
     int64_t h_ring_cap = 0;
     int64_t h_lo = 0, h_hi = 0;  // slots [h_lo, h_hi) of the mirror are current
     int64_t m_first = 0, replays = 0;
-    // range-partitioned scatter (default on one GPU, wealth_bins.cu)
-    bool bins = false;
-    bool slot_ready = false;  // slot(t) is zero and the bins work queues are reset
-    BinPlan plan;
-    BinBuffers bb;
-    // fused range-binned step (wealth_fb.cu)
-    bool fb = false;
-    FbPlan fplan;
-    FbBuffers fbb;
-    int fb_launches = 0;
-    // segmented-bin step (wealth_seg.cu)
-    bool seg = false;
-    SegPlan splan;
-    SegBuffers sgb;
     // cross-shard exchange (world > 1)
     WealthExchange* xch = nullptr;
     DevBuf<uint32_t> send_ids, recv_ids;
@@ -495,15 +481,11 @@ public:
         p = p_;
         seed = seed_;
         key = philox_key(seed);
-        // counter_bits -1: range-partitioned scatter (wealth_bins.cu, single GPU);
-        // 0: default = 4-bit packed counters with L2 atomics (measured faster)
-        const bool want_bins = p.counter_bits == -1 && (r == nullptr || r->world <= 1) &&
-                               !(getenv("AMBER_TEST_FORCE_EXCHANGE") && r && r->nccl_unique_id);
-        const bool want_fb = p.counter_bits == -2 && (r == nullptr || r->world <= 1);
-        const bool want_seg = p.counter_bits == -3 && (r == nullptr || r->world <= 1);
-        if (p.counter_bits <= 0) p.counter_bits = 4;
+        // 0: default = 4-bit packed counters with L2 atomics (the three atomic-free
+        // scatters measured slower live in tools/experiments/)
+        if (p.counter_bits == 0) p.counter_bits = 4;
         B = p.counter_bits;
-        AMBER_REQUIRE(B == 2 || B == 4 || B == 8 || B == 16 || B == 32, "counter_bits must be -3,-2,-1,0,2,4,8,16,32");
+        AMBER_REQUIRE(B == 2 || B == 4 || B == 8 || B == 16 || B == 32, "counter_bits must be 0, 2, 4, 8, 16 or 32");
         AMBER_REQUIRE(p.amount >= 1, "amount must be >= 1");
         AMBER_REQUIRE(p.w0 >= 0, "w0 must be >= 0");
         AMBER_REQUIRE(!p.exclude_self || n >= 2, "exclude_self needs n_agents >= 2");
@@ -514,34 +496,10 @@ public:
         shard_range(n, rt.world, rt.rank, &lo, &hi);
         n_loc = hi - lo;
         n_pad = std::max<int64_t>(ceil_div(std::max<int64_t>(n_loc, 1), kChunkAgents) * kChunkAgents, kChunkAgents);
-        if (want_bins) {
-            const int64_t np = ceil_div(std::max<int64_t>(n_loc, 1), kBinRange) * kBinRange;
-            if (bins_plan(rt, n, lo, np, plan)) {
-                bins = true;
-                n_pad = np;
-            }
-        }
-        if (want_fb) {
-            const int64_t np = ceil_div(std::max<int64_t>(n_loc, 1), kBinRange) * kBinRange;
-            if (fb_plan(rt, n, lo, np, fplan)) {
-                fb = true;
-                n_pad = np;
-            }
-        }
-        if (want_seg && seg_plan(rt, n, n_loc, splan)) {
-            seg = true;
-            n_pad = splan.R * splan.K;
-        }
         fast32 = n < (1ll << 32) - 1 && lo + n_pad < (1ll << 32);
         AMBER_REQUIRE(fast32 || rt.world == 1, "sharded wealth needs ids < 2^32");
         for (auto& b : wb) b.allocate(&rt, n_pad);
-        if (seg) {
-            seg_allocate(rt, splan, sgb);
-        } else if (fb) {
-            fb_allocate(rt, fplan, fbb);
-        } else if (bins) {
-            bins_allocate(rt, plan, bb);
-        } else {
+        {
             const int64_t inc_words = ceil_div(n_pad * B, 32) + 4;
             for (auto& b : inc) {
                 b.allocate(&rt, inc_words);
@@ -614,16 +572,6 @@ public:
         for (auto& b : wb) b.reset();
         for (auto& b : inc) b.reset();
         for (auto& b : inc32) b.reset();
-        for (auto& b : bb.data) b.reset();
-        for (auto& b : bb.cnt) b.reset();
-        bb.queue.reset();
-        for (auto& b : fbb.data) b.reset();
-        for (auto& b : fbb.lo) b.reset();
-        for (auto& b : fbb.hi) b.reset();
-        fbb.queue.reset();
-        for (auto* v : {&sgb.data[0], &sgb.data[1], &sgb.cnt[0], &sgb.cnt[1], &sgb.tail[0], &sgb.tail[1],
-                        &sgb.tcnt[0], &sgb.tcnt[1]})
-            v->reset();
         ring.reset();
         if (h_ring) cudaFreeHost(h_ring);
         send_ids.reset();
@@ -781,7 +729,7 @@ public:
         check_launch("zero_slots_kernel");
     }
 
-    bool small_path() const { return rt.world == 1 && !xch && n <= kSmallMax && !bins && !fb && !seg && persistent; }
+    bool small_path() const { return rt.world == 1 && !xch && n <= kSmallMax && persistent; }
 
     void step(int64_t nsteps) override
     {
@@ -810,73 +758,6 @@ public:
                 cur = other(cur, -1);
                 t += chunk;
                 done += chunk;
-            }
-            return;
-        }
-        if (seg) {
-            WealthStepCfg c{key, n_loc, n_pad, static_cast<unsigned long long>(lo), static_cast<unsigned long long>(n),
-                            p.amount, p.exclude_self, digest_on ? 1 : 0};
-            for (int64_t k = 0; k < nsteps; ++k) {
-                if (win_start >= 0 && t - win_start >= metrics_cap - 4) verify();
-                if (win_start < 0) {
-                    win_start = t;
-                    pinned = cur;
-                }
-                if (!pending) {
-                    zero_slots(t, 2);
-                    seg_launch(rt, prof, splan, sgb, c, false, static_cast<uint32_t>(t), static_cast<uint32_t>(t),
-                               wb[cur].p, nullptr, nullptr, slot(t), nullptr);
-                }
-                const int dst = other(cur, pinned == cur ? -1 : pinned);
-                seg_launch(rt, prof, splan, sgb, c, true, static_cast<uint32_t>(t), static_cast<uint32_t>(t + 1),
-                           wb[cur].p, wb[dst].p, slot(t), slot(t + 1), slot(t + 2));
-                cur = dst;
-                ++t;
-                pending = true;
-            }
-            return;
-        }
-        if (fb) {
-            WealthStepCfg c{key, n_loc, n_pad, static_cast<unsigned long long>(lo), static_cast<unsigned long long>(n),
-                            p.amount, p.exclude_self, digest_on ? 1 : 0};
-            for (int64_t k = 0; k < nsteps; ++k) {
-                if (win_start >= 0 && t - win_start >= metrics_cap - 4) verify();
-                if (win_start < 0) {
-                    win_start = t;
-                    pinned = cur;
-                }
-                if (!pending) {
-                    zero_slots(t, 2);
-                    fb_launch(rt, prof, fplan, fbb, c, false, static_cast<uint32_t>(t), static_cast<uint32_t>(t),
-                              wb[cur].p, nullptr, nullptr, slot(t), nullptr, fb_launches++);
-                }
-                const int dst = other(cur, pinned == cur ? -1 : pinned);
-                fb_launch(rt, prof, fplan, fbb, c, true, static_cast<uint32_t>(t), static_cast<uint32_t>(t + 1), wb[cur].p,
-                          wb[dst].p, slot(t), slot(t + 1), slot(t + 2), fb_launches++);
-                cur = dst;
-                ++t;
-                pending = true;
-            }
-            return;
-        }
-        if (bins) {
-            WealthStepCfg c{key, n_loc, n_pad, static_cast<unsigned long long>(lo), static_cast<unsigned long long>(n),
-                            p.amount, p.exclude_self, digest_on ? 1 : 0};
-            for (int64_t k = 0; k < nsteps; ++k) {
-                if (win_start >= 0 && t - win_start >= metrics_cap - 4) verify();
-                if (win_start < 0) {
-                    win_start = t;
-                    pinned = cur;
-                }
-                if (!slot_ready) {
-                    zero_slots(t, 1);
-                    bb.queue.zero_async(rt.stream);
-                }
-                const int dst = other(cur, pinned == cur ? -1 : pinned);
-                bins_step(rt, prof, plan, bb, c, static_cast<uint32_t>(t), wb[cur].p, wb[dst].p, slot(t), slot(t + 1));
-                slot_ready = true;
-                cur = dst;
-                ++t;
             }
             return;
         }
@@ -948,23 +829,10 @@ public:
         pinned = -1;
     }
 
-    void reset_fb()
-    {
-        if (seg) seg_reset(rt, sgb);
-        if (!fb) return;
-        for (auto& b : fbb.lo) b.zero_async(rt.stream);
-        for (auto& b : fbb.hi) b.zero_async(rt.stream);
-        fbb.queue.zero_async(rt.stream);
-        fb_launches = 0;
-    }
-
     void replay(int64_t s0, int64_t s1)
     {
         ++replays;
         h_hi = h_lo;
-        slot_ready = false;
-        reset_fb();
-        for (auto& b : bb.cnt) b.zero_async(rt.stream);
         cur = pinned;
         for (auto& b : inc) b.zero_async(rt.stream);
         for (auto& b : inc32) {
@@ -993,10 +861,8 @@ public:
 
     void invalidate_pending()
     {
-        slot_ready = false;
         if (pending) {
-            if (fb || seg) reset_fb();
-            else if (inc[t & 1].p) inc[t & 1].zero_async(rt.stream);
+            if (inc[t & 1].p) inc[t & 1].zero_async(rt.stream);
             pending = false;
         }
     }
@@ -1102,34 +968,6 @@ public:
             m_first = t;
             return true;
         }
-        if (k == "bin_capacity" && seg) {  // test hook: shrink the segments to force drops and the exact replay
-            AMBER_REQUIRE(v >= 4 && v <= 0x7fffffff, "bin_capacity must be >= 4");
-            verify();
-            invalidate_pending();
-            splan.cap = static_cast<uint32_t>(v) & ~3u;
-            splan.tcap = static_cast<uint32_t>(std::min<int64_t>(v, 4096));
-            seg_allocate(rt, splan, sgb);
-            return true;
-        }
-        if (k == "bin_capacity" && fb) {  // test hook: shrink the bins to force drops and the exact replay
-            AMBER_REQUIRE(v >= 8 && v <= 0x7fffffff, "bin_capacity must be >= 8");
-            verify();
-            invalidate_pending();
-            fplan.cap_lo = static_cast<uint32_t>(v) & ~7u;
-            fplan.cap_hi = static_cast<uint32_t>(std::min<int64_t>(v, 8192));
-            fb_allocate(rt, fplan, fbb);
-            fb_launches = 0;
-            return true;
-        }
-        if (k == "bin_capacity") {  // test hook: shrink the per-range bins to force the exact replay
-            AMBER_REQUIRE(bins, "bin_capacity applies to the range-partitioned scatter only");
-            AMBER_REQUIRE(v >= 8 && v <= 0x7fffffff, "bin_capacity must be >= 8");
-            verify();
-            invalidate_pending();
-            plan.cap = static_cast<uint32_t>((v + 7) & ~7ll);
-            bins_allocate(rt, plan, bb);
-            return true;
-        }
         if (k == "block") AMBER_REQUIRE(v <= 256, "wealth kernels are built for <= 256 threads per block");
         if (k == "digest" || k == "block" || k == "grid") verify();
         return Model::set_option(key, v);
@@ -1151,8 +989,8 @@ public:
             *v = xch ? (p2p ? 2 : 1) : 0;
             return true;
         }
-        if (k == "scatter") {  // 0: range-partitioned bins, 1: packed-counter atomics, 2: fused binned, 3: segmented bins
-            *v = seg ? 3 : (fb ? 2 : (bins ? 0 : 1));
+        if (k == "scatter") {  // 1: packed-counter L2 atomics (the one shipped scatter)
+            *v = 1;
             return true;
         }
         return Model::get_option(key, v);

@@ -50,54 +50,6 @@ def test_counter_widths_and_ragged_sizes(orc, bits, n):
         assert m.get_option("replays") > 0
 
 
-def test_range_partitioned_scatter_replays_exactly(orc):
-    n, seed = 300_000, 5
-    m = make(n, seed, bits=-1)
-    assert m.get_option("scatter") == 0
-    m.set_option("bin_capacity", 64)  # far below ~3e4 entries per range: every step overflows
-    m.step(6)
-    w, tot, _, _ = orc.wealth_run(np.full(n, 1, np.int32), seed, 0, 6)
-    assert np.array_equal(m.read_column("wealth"), w)
-    assert m.get_option("replays") >= 1
-    assert np.array_equal(m.metrics("total_wealth"), tot)
-    m.step(4)  # back on the fast path after the replay
-    w = orc.wealth_run(w, seed, 6, 4)[0]
-    assert np.array_equal(m.read_column("wealth"), w)
-
-
-def test_fused_binned_scatter_bit_exact(orc):
-    # needs >= 1024 ranges of 2^16 agents (smaller populations fall back to the counters)
-    n, seed = 70_000_003, 19
-    m = make(n, seed, bits=-2)
-    assert m.get_option("scatter") == 2
-    m.step(1)
-    m.step(1)
-    w, tot, act, _ = orc.wealth_run(np.full(n, 1, np.int32), seed, 0, 2)
-    assert np.array_equal(m.read_column("wealth"), w)
-    assert np.array_equal(m.metrics("total_wealth"), tot) and np.array_equal(m.metrics("active"), act)
-    assert m.get_option("replays") == 0
-
-
-def test_fused_binned_overflow_replays_exactly(orc):
-    n, seed = 70_000_000, 4
-    m = make(n, seed, bits=-2)
-    m.set_option("bin_capacity", 4096)
-    m.step(2)
-    w = orc.wealth_run(np.full(n, 1, np.int32), seed, 0, 2)[0]
-    assert np.array_equal(m.read_column("wealth"), w)
-    assert m.get_option("replays") >= 1
-
-
-def test_atomic_and_binned_scatter_agree(orc):
-    n, seed = 200_003, 8
-    a = make(n, seed, bits=-1)
-    b = make(n, seed)
-    assert a.get_option("scatter") == 0 and b.get_option("scatter") == 1
-    a.step(20)
-    b.step(20)
-    assert np.array_equal(a.read_column("wealth"), b.read_column("wealth"))
-
-
 @pytest.mark.parametrize("n", [1, 2, 1000, 16384])
 def test_small_single_cta_path_equals_counter_path(orc, n):
     a = make(n, 42)  # n <= 16384: one CTA runs all steps in shared memory
@@ -202,58 +154,6 @@ def test_errors_are_reported():
         m.read_column("nope")
     with pytest.raises(AmberError):
         m.read_column("wealth", np.zeros(3, np.int32))
-
-
-@pytest.mark.parametrize("n,steps", [(40_000, 25), (5_000_003, 6)])
-def test_segmented_bins_bit_exact(orc, n, steps):
-    # wealth_seg.cu: per-(destination, producer) bin segments + 4-bit shared-memory histograms
-    m = make(n, 31, bits=-3)
-    assert m.get_option("scatter") == 3
-    m.set_option("digest", 1)
-    m.step(1)
-    m.step(steps - 1)
-    w, tot, act, dig = orc.wealth_run(np.full(n, 1, np.int32), 31, 0, steps, digests=True)
-    assert np.array_equal(m.read_column("wealth"), w)
-    assert np.array_equal(m.metrics("total_wealth"), tot) and np.array_equal(m.metrics("active"), act)
-    assert np.array_equal(m.metrics("digest"), dig.astype(np.uint64))
-    assert m.get_option("replays") == 0
-
-
-@pytest.mark.parametrize("kw", [dict(exclude_self=1), dict(w0=3, amount=2)])
-def test_segmented_bins_variants(orc, kw):
-    n, seed = 1_000_001, 12
-    m = make(n, seed, bits=-3, **kw)
-    assert m.get_option("scatter") == 3
-    m.step(5)
-    w0 = kw.get("w0", 1)
-    w = orc.wealth_run(np.full(n, w0, np.int32), seed, 0, 5, amount=kw.get("amount", 1),
-                       exclude_self=kw.get("exclude_self", 0))[0]
-    assert np.array_equal(m.read_column("wealth"), w)
-    assert m.get_option("replays") == 0
-
-
-def test_segmented_bins_overflow_replays_exactly(orc):
-    n, seed = 2_000_000, 6
-    m = make(n, seed, bits=-3)
-    m.set_option("bin_capacity", 8)  # segments and tails far too small: entries dropped every step
-    m.step(3)
-    w = orc.wealth_run(np.full(n, 1, np.int32), seed, 0, 3)[0]
-    assert np.array_equal(m.read_column("wealth"), w)
-    assert m.get_option("replays") >= 1
-    m.step(2)
-    w = orc.wealth_run(w, seed, 3, 2)[0]
-    assert np.array_equal(m.read_column("wealth"), w)
-
-
-def test_segmented_bins_full_size_first_steps(orc):
-    # BASELINE config 4 size (N = 1e8) in the launch configuration bench.py times
-    cfg = C4_WEALTH_SCALE
-    m = make(cfg["n"], cfg["seed"], bits=-3)
-    assert m.get_option("scatter") == 3
-    m.step(2)
-    w = orc.wealth_run(np.full(cfg["n"], 1, np.int32), cfg["seed"], 0, 2)[0]
-    assert np.array_equal(m.read_column("wealth"), w)
-    assert m.get_option("replays") == 0
 
 
 def test_small_metrics_ring_and_per_step_reads(orc):

@@ -23,7 +23,7 @@
 #include <algorithm>
 #include <cub/block/block_scan.cuh>
 
-#include "wealth.cuh"
+#include "wealth_experiments.cuh"
 
 namespace amber {
 

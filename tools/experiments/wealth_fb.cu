@@ -24,7 +24,7 @@
 // the model then replays the window with exact 32-bit counters (wealth.cu).
 #include <algorithm>
 
-#include "wealth.cuh"
+#include "wealth_experiments.cuh"
 
 namespace amber {
 

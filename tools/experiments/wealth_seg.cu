@@ -39,7 +39,7 @@
 #include <algorithm>
 #include <cmath>
 
-#include "wealth.cuh"
+#include "wealth_experiments.cuh"
 
 namespace amber {
 
