@@ -37,6 +37,11 @@ UNIT = "agent-updates/s"
 # random 32-bit L2 atomics, any target set that fits L2 (measured on this pool's B200,
 # tools/red_ceiling.cu -> profiles/r01_red_ceiling.txt): the scatter's binding roof
 RED_CEILING = 1.85e11
+# the Boids stencil's own instruction sequence over shared-memory-staged candidates
+# (memory latency hidden) at full residency, candidate visits per second
+# (tools/alu_ceiling.cu -> profiles/r02_alu_ceiling.txt): pre-quantised-velocity
+# form (the default, option qv) and float-velocity form
+STENCIL_CEILING = {1: 9.337e11, 0: 7.928e11}
 
 
 def peaks():
@@ -351,13 +356,14 @@ def bench_configs(hbm):
     m.step(1)
     ms = _timed(m, c["steps"] - 1, torch)
     per = ms / (c["steps"] - 1)
+    roof3 = boids_roof(m, per, "C3")
     m.close()
     P = oracle.boids_params(**{k: c[k] for k in bkeys})
     s0 = oracle.boids_init(c["n"], c["L"], c["seed"])
     orate = _oracle_rate(lambda: oracle.boids_run(s0, P, 3), c["n"] * 3)
     out["c3"] = {"workload": "C3 Boids N=1e5 x100 (BASELINE config 3)", "ms_per_step": per,
                  "value": c["n"] / (per / 1e3), "unit": UNIT,
-                 "roof": boids_roof(per, c["n"], "C3"),
+                 "roof": roof3,
                  "oracle": {"value": orate, "unit": UNIT, "cores": 1,
                             "sample": "first 3 steps on the full population (sparse phase)"}}
 
@@ -426,23 +432,41 @@ def bench_configs(hbm):
     m.step(1)
     ms = _timed(m, c["steps"] - 1, torch)
     per = ms / (c["steps"] - 1)
+    roofv3 = boids_roof(m, per, "V3")
     m.close()
     n_o = 1_000_000
     P = oracle.boids_params(**{**{k: c[k] for k in bkeys}, "L": 3162.3})
     s0 = oracle.boids_init(n_o, 3162.3, c["seed"])
     orate = _oracle_rate(lambda: oracle.boids_run(s0, P, 1), n_o)
     out["v3"] = {"workload": "V3 Boids N=1e8 L=31623 x10 (SURVEY 8(d) roofline variant)", "ms_per_step": per,
-                 "value": c["n"] / (per / 1e3), "unit": UNIT, "roof": boids_roof(per, c["n"], "V3"),
+                 "value": c["n"] / (per / 1e3), "unit": UNIT, "roof": roofv3,
                  "oracle": {"value": orate, "unit": UNIT, "cores": 1,
                             "sample": f"N={n_o:.0e} at the same density (L=3162.3), first step"}}
     return out
 
 
-def boids_roof(ms_per_step, n, which):
-    """Boids binding roof: SM issue of the stencil (FP32/INT mix).  The measured
-    instruction ceiling comes from tools/alu_ceiling.cu (profiles/r02_alu_ceiling.txt)."""
-    return {"bound": "alu", "why": "FP32 + int64 fixed-point stencil over ~90 candidates per agent",
-            "evidence": f"profiles/r01_{'v3' if which == 'V3' else 'c3'}_boids_group_ncu.txt"}
+def boids_roof(m, ms_per_step, which):
+    """Boids binding roof: the stencil kernel's ALU/issue ceiling.  One more
+    (profiled) step gives the stencil kernel's device time and the candidate
+    visits of its pass (option stencil_candidates); achieved = visits / time,
+    peak = the measured ceiling of the same instruction sequence."""
+    qv = m.get_option("qv")
+    m.profile(True)
+    m.step(1)
+    m.synchronize()
+    prof = {k: t / n for k, n, t in m.profile_results()}
+    m.profile(False)
+    cand = m.get_option("stencil_candidates")
+    st_ms = prof.get("boids_step", 0.0)
+    ach = cand / (st_ms / 1e3) if st_ms > 0 else 0.0
+    peak = STENCIL_CEILING[qv]
+    return {"bound": "alu", "kernel": "boids_group_kernel", "achieved": ach, "peak": peak,
+            "unit": "candidate-visits/s", "frac": ach / peak, "candidates_per_step": cand,
+            "stencil_ms": st_ms, "stencil_share_of_step": st_ms / ms_per_step if ms_per_step > 0 else None,
+            "kernel_ms": prof, "peak_source": "profiles/r02_alu_ceiling.txt (tools/alu_ceiling.cu, "
+                                               f"{'pre-quantised' if qv else 'float'}-velocity stencil)",
+            "why": "FP32 + int64 fixed-point stencil; memory latency hidden in the ceiling",
+            "evidence": f"profiles/r0{'2' if which == 'V3' else '1'}_{which.lower()}_boids_group_ncu.txt"}
 
 
 # ------------------------------------------------------------------ GPU arm

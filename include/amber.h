@@ -94,7 +94,20 @@ typedef struct {
     int rank;                   /* this process's rank in [0, world) */
     int world;                  /* number of processes (one GPU each); 0 or 1 = single */
     const void* nccl_unique_id; /* 128-byte id from amber_nccl_unique_id() on rank 0,
-                                   broadcast to all ranks; required iff world > 1 */
+                                   broadcast to all ranks; required iff world > 1, unless
+                                   host collectives are given (below) */
+    /* Optional host collectives of the caller's own transport (e.g. a gloo or MPI
+     * process group).  Used only when world > 1 and nccl_unique_id is NULL, and
+     * only by the sharded wealth model: its peer-memory (P2P) exchange then maps
+     * the peers' bucket blocks through CUDA IPC handles all-gathered with
+     * host_allgather, and orders every step with host_barrier after the stream
+     * drains (no kernel ever waits on another process's kernel).  Both are
+     * collective over all ranks and return 0 on success; a non-zero return fails
+     * the call with AMBER_E_NCCL.  host_allgather gathers `bytes` from every rank
+     * into recv (world * bytes, rank order). */
+    int (*host_allgather)(const void* send, void* recv, size_t bytes, void* ctx);
+    int (*host_barrier)(void* ctx);
+    void* host_ctx;
 } amber_runtime;
 
 /* ---- model parameters (POD, passed as pointer + sizeof for ABI growth) ---- */

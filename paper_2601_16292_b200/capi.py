@@ -35,13 +35,17 @@ SYMBOLS = ["amber_version", "amber_last_error", "amber_model_create", "amber_mod
            "amber_population_update_paths"]
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+HOST_ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+HOST_BARRIER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p)
 FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 
 
 class amber_runtime(C.Structure):
     _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("alloc", ALLOC_FN),
                 ("free", FREE_FN), ("alloc_ctx", C.c_void_p), ("rank", C.c_int),
-                ("world", C.c_int), ("nccl_unique_id", C.c_void_p)]
+                ("world", C.c_int), ("nccl_unique_id", C.c_void_p),
+                ("host_allgather", HOST_ALLGATHER_FN), ("host_barrier", HOST_BARRIER_FN),
+                ("host_ctx", C.c_void_p)]
 
 
 class amber_wealth_params(C.Structure):

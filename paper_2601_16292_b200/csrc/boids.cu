@@ -35,7 +35,11 @@ constexpr float kFix = 16777216.0f;  // 2^24 (B3)
 #define AMBER_BOIDS_INFLIGHT 2  // candidate loads in flight per lane in interior row runs
 #endif
 #ifndef AMBER_BOIDS_MINB
-#define AMBER_BOIDS_MINB 4  // resident 256-thread blocks per SM for the stencil kernel (register cap 64)
+// resident 256-thread blocks per SM for the stencil kernel: 4 (register cap 64)
+// for small populations, 6 (cap 40) for large ones -- V3 stencil 18.3 -> 17.5 ms
+// (more warps to hide the candidate loads), C3 slightly slower (60.9 -> 63.9 us)
+#define AMBER_BOIDS_MINB 4
+#define AMBER_BOIDS_MINB_LARGE 6
 #endif
 
 struct BoidsArgs {
@@ -178,11 +182,98 @@ __global__ void __launch_bounds__(1024) boids_scan_kernel(const int* __restrict_
     }
 }
 
+// Exclusive scan of the ncell + 1 counts for large grids (> 2^16 cells), by
+// hand in two launches (no library scan on the step path): (1) each 1024-thread
+// block sums a chunk of kScanChunk cells; (2) each block adds the totals of the
+// chunks before it (L2-resident, ~2.4K of them at V3's 10^7 cells), scans its
+// chunk (four cells per thread, warp shuffles + one shared-memory pass over the
+// 32 warp totals), writes start / cursor and re-zeroes the counts.
+constexpr int kScanChunk = 4096;
+
+__device__ __forceinline__ int block_sum_1024(int v, int* red)
+{
+    v = __reduce_add_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int t = threadIdx.x < 32 ? red[threadIdx.x] : 0;
+    if (threadIdx.x < 32) t = __reduce_add_sync(0xffffffffu, t);
+    __syncthreads();
+    return t;  // valid in warp 0
+}
+
+__global__ void __launch_bounds__(1024) boids_chunk_sums_kernel(const int* __restrict__ cnt, int ncell1,
+                                                                int* __restrict__ sums)
+{
+    __shared__ int red[32];
+    const int c0 = blockIdx.x * kScanChunk + threadIdx.x * 4;
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s += c0 + k < ncell1 ? cnt[c0 + k] : 0;
+    s = block_sum_1024(s, red);
+    if (threadIdx.x == 0) sums[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(1024) boids_chunk_scan_kernel(int* __restrict__ cnt, const int* __restrict__ sums,
+                                                                int ncell, int* __restrict__ start,
+                                                                int* __restrict__ cursor)
+{
+    __shared__ int red[32], wex[32];
+    int pre = 0;
+    for (int j = threadIdx.x; j < static_cast<int>(blockIdx.x); j += 1024) pre += sums[j];
+    pre = block_sum_1024(pre, red);
+    if (threadIdx.x == 0) red[0] = pre;
+    __syncthreads();
+    const int carry = red[0];
+    const int c0 = blockIdx.x * kScanChunk + threadIdx.x * 4;
+    int v[4], tsum = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[k] = c0 + k <= ncell ? cnt[c0 + k] : 0;
+        tsum += v[k];
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int incl = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) wex[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        const int x = wex[lane];
+        int xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += u;
+        }
+        wex[lane] = xi - x;
+    }
+    __syncthreads();
+    int run = carry + wex[w] + incl - tsum;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int c = c0 + k;
+        if (c <= ncell) {
+            start[c] = run;
+            if (c < ncell) {
+                cursor[c] = run;
+                cnt[c] = 0;
+            }
+        }
+        run += v[k];
+    }
+}
+
 // Counting-sort scatter; also zeroes the cell counts for the next count pass
 // (ncell_zero cells; 0 when the counts were cleared otherwise).
+// QV (svel != nullptr): the sorted record carries q24(v) as int32 bits in z, w
+// (the stencil's candidates) and svel the float velocity (the agent's own update).
 __global__ void boids_scatter_kernel(const float4* __restrict__ st, const int32_t* __restrict__ ids, int64_t n,
                                      const int* __restrict__ cell_of, int* __restrict__ cursor, float4* __restrict__ sorted,
-                                     int32_t* __restrict__ sorted_ids, int* __restrict__ cnt, int ncell_zero)
+                                     int32_t* __restrict__ sorted_ids, int* __restrict__ cnt, int ncell_zero,
+                                     float2* __restrict__ svel)
 {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
     for (int64_t c = tid; c < ncell_zero; c += nt) cnt[c] = 0;
@@ -196,7 +287,15 @@ __global__ void boids_scatter_kernel(const float4* __restrict__ st, const int32_
         if (c >= 0 && rank == 0) q = atomicAdd(cursor + c, len);  // one cursor claim per run
         q = __shfl_sync(0xffffffffu, q, head) + rank;
         if (c >= 0) {
-            sorted[q] = st[p];
+            AMBER_DCHECK(q >= 0 && q < n, "Boids scatter: sorted slot out of range");
+            const float4 v = st[p];
+            if (svel) {
+                sorted[q] = make_float4(v.x, v.y, __int_as_float(__float2int_rn(__fmul_rn(v.z, kFix))),
+                                        __int_as_float(__float2int_rn(__fmul_rn(v.w, kFix))));
+                svel[q] = make_float2(v.z, v.w);
+            } else {
+                sorted[q] = v;
+            }
             sorted_ids[q] = ids[p];
         }
     }
@@ -218,7 +317,13 @@ __device__ __forceinline__ float min_image(float d, float L, float halfL)
 
 // WRAP = false: the caller guarantees |o - me| <= L/2 per coordinate (both
 // agents in interior cells), where the minimum image is the identity.
-template <bool WRAP = true>
+// QV: the candidate record carries its velocity pre-quantised (o.z, o.w hold
+// q24(v) as int32 bits, written once per agent by the scatter pass), and the
+// displacement converts with a 32-bit F2I: |dx| <= R < 100 so |q24(dx)| < 2^31.
+// Same integers as the float path (B3), two F2I.S64 fewer per neighbour
+// (tools/alu_ceiling.cu: the stencil's ALU ceiling 7.9e11 -> 9.3e11 candidate
+// visits/s, profiles/r02_alu_ceiling.txt).
+template <bool WRAP = true, bool QV = false>
 __device__ __forceinline__ void boid_accumulate(const float4 o, const float4 me, float L, float halfL, float R2,
                                                 float rs2, Acc& acc)
 {
@@ -230,15 +335,28 @@ __device__ __forceinline__ void boid_accumulate(const float4 o, const float4 me,
     }
     const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
     if (d2 <= R2) {
-        const long long qx = q24(dx), qy = q24(dy);
-        acc.n += 1;
-        acc.sdx += qx;
-        acc.sdy += qy;
-        acc.svx += q24(o.z);
-        acc.svy += q24(o.w);
-        if (d2 <= rs2) {
-            acc.ssx += qx;
-            acc.ssy += qy;
+        if constexpr (QV) {
+            const int qx = __float2int_rn(__fmul_rn(dx, kFix)), qy = __float2int_rn(__fmul_rn(dy, kFix));
+            acc.n += 1;
+            acc.sdx += qx;
+            acc.sdy += qy;
+            acc.svx += __float_as_int(o.z);
+            acc.svy += __float_as_int(o.w);
+            if (d2 <= rs2) {
+                acc.ssx += qx;
+                acc.ssy += qy;
+            }
+        } else {
+            const long long qx = q24(dx), qy = q24(dy);
+            acc.n += 1;
+            acc.sdx += qx;
+            acc.sdy += qy;
+            acc.svx += q24(o.z);
+            acc.svy += q24(o.w);
+            if (d2 <= rs2) {
+                acc.ssx += qx;
+                acc.ssy += qy;
+            }
         }
     }
 }
@@ -280,51 +398,66 @@ __device__ __forceinline__ float4 boid_update_means(const float4 me, const Acc& 
 // bit).  G times more threads than agents hide the L1 latency of the candidate
 // loop that bounds the one-lane kernel once flocks cluster (r01 ncu: 15K
 // instructions per agent at step 90, 30% warp occupancy).
-template <int G>
+template <int G, bool QV>
 __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sorted, const int32_t* __restrict__ sids,
                                                  const int* __restrict__ start, int64_t n, const BoidsArgs& a,
                                                  float4* __restrict__ out, int32_t* __restrict__ out_ids, BoidsSlot* slot,
-                                                 int digest, int* __restrict__ next_cnt = nullptr,
-                                                 int* __restrict__ next_cell = nullptr)
+                                                 int digest, int* __restrict__ next_cnt,
+                                                 int* __restrict__ next_cell, const float2* __restrict__ svel)
 {
     static_assert(G >= 4, "the update spreads four divisions over the group's lanes");
     const float L = a.L, halfL = __fmul_rn(0.5f, a.L), R2 = __fmul_rn(a.R, a.R), rs2 = __fmul_rn(a.rs, a.rs);
     const int sub = threadIdx.x & (G - 1);
-    const int64_t gid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / G;
-    const int64_t ng = (static_cast<int64_t>(gridDim.x) * blockDim.x) / G;
+    // each block owns one contiguous range of the cell-sorted agents (blockDim/G
+    // agents per round): consecutive rounds slide along the same cell rows, so
+    // the stencil's rows stay in this SM's L1 instead of being fetched by a
+    // different SM every round
+    const int64_t apb = blockDim.x / G;  // agents per block per round
+    const int64_t ng = apb * gridDim.x;
     const int64_t rounds = (n + ng - 1) / ng;  // uniform: every lane runs every round (shuffles)
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * rounds * apb + threadIdx.x / G;
     double sp_sum = 0.0, ux_sum = 0.0, uy_sum = 0.0;
     unsigned long long dig = 0;
     for (int64_t r = 0; r < rounds; ++r) {
-        const int64_t p = r * ng + gid;
+        const int64_t p = base + r * apb;
         const bool active = p < n;
         Acc acc{0, 0, 0, 0, 0, 0, 0};
         float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
+        int qself_x = 0, qself_y = 0;  // QV: the agent's own quantised velocity
         if (active) {
             me = sorted[p];
+            if constexpr (QV) {
+                qself_x = __float_as_int(me.z);
+                qself_y = __float_as_int(me.w);
+                const float2 v = svel[p];
+                me.z = v.x;
+                me.w = v.y;
+            }
             auto run = [&](int b, int e) {
+                AMBER_DCHECK(b >= 0 && b <= e && e <= n, "Boids stencil: cell run out of range");
                 for (int q = b + sub; q < e; q += G)
-                    boid_accumulate<true>(sorted[q], me, L, halfL, R2, rs2, acc);
+                    boid_accumulate<true, QV>(sorted[q], me, L, halfL, R2, rs2, acc);
             };
             // interior agents (stencil inside the box, so every candidate is within
             // two cells < L/2 per coordinate): no minimum image, rows as runs
             auto run_in = [&](int b, int e) {
+                AMBER_DCHECK(b >= 0 && b <= e && e <= n, "Boids stencil: cell run out of range");
                 int q = b + sub;
 #if AMBER_BOIDS_INFLIGHT == 4
                 for (; q + 3 * G < e; q += 4 * G) {  // four candidate loads in flight per lane
                     const float4 o0 = sorted[q], o1 = sorted[q + G], o2 = sorted[q + 2 * G], o3 = sorted[q + 3 * G];
-                    boid_accumulate<false>(o0, me, L, halfL, R2, rs2, acc);
-                    boid_accumulate<false>(o1, me, L, halfL, R2, rs2, acc);
-                    boid_accumulate<false>(o2, me, L, halfL, R2, rs2, acc);
-                    boid_accumulate<false>(o3, me, L, halfL, R2, rs2, acc);
+                    boid_accumulate<false, QV>(o0, me, L, halfL, R2, rs2, acc);
+                    boid_accumulate<false, QV>(o1, me, L, halfL, R2, rs2, acc);
+                    boid_accumulate<false, QV>(o2, me, L, halfL, R2, rs2, acc);
+                    boid_accumulate<false, QV>(o3, me, L, halfL, R2, rs2, acc);
                 }
 #endif
                 for (; q + G < e; q += 2 * G) {  // two candidate loads in flight per lane
                     const float4 o0 = sorted[q], o1 = sorted[q + G];
-                    boid_accumulate<false>(o0, me, L, halfL, R2, rs2, acc);
-                    boid_accumulate<false>(o1, me, L, halfL, R2, rs2, acc);
+                    boid_accumulate<false, QV>(o0, me, L, halfL, R2, rs2, acc);
+                    boid_accumulate<false, QV>(o1, me, L, halfL, R2, rs2, acc);
                 }
-                if (q < e) boid_accumulate<false>(sorted[q], me, L, halfL, R2, rs2, acc);
+                if (q < e) boid_accumulate<false, QV>(sorted[q], me, L, halfL, R2, rs2, acc);
             };
             const int sp = a.span;
             const int cx0 = a.nc >= 3 ? cell_coord(me.x, a) : 0, cy0 = a.nc >= 3 ? cell_coord(me.y, a) : 0;
@@ -370,8 +503,8 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
         }
         if (active) {  // the agent itself was accumulated once (d = 0, inside both radii): take it out
             acc.n -= 1;
-            acc.svx -= q24(me.z);
-            acc.svy -= q24(me.w);
+            acc.svx -= QV ? static_cast<long long>(qself_x) : q24(me.z);
+            acc.svy -= QV ? static_cast<long long>(qself_y) : q24(me.w);
         }
         // B4's four mean divisions in parallel on lanes 0..3 of the group
         // (x / 2^24 is exact, so it is a multiplication), gathered by shuffles
@@ -455,14 +588,48 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
     __syncthreads();
 }
 
-template <int G>
-__global__ void __launch_bounds__(256, AMBER_BOIDS_MINB) boids_group_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ sids,
+template <int G, bool QV, int MINB = AMBER_BOIDS_MINB>
+__global__ void __launch_bounds__(256, MINB) boids_group_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ sids,
                                                           const int* __restrict__ start, int64_t n, BoidsArgs a,
                                                           float4* __restrict__ out, int32_t* __restrict__ out_ids,
                                                           BoidsSlot* slot, int digest, int* __restrict__ next_cnt,
-                                                          int* __restrict__ next_cell)
+                                                          int* __restrict__ next_cell, const float2* __restrict__ svel)
 {
-    boids_group_body<G>(sorted, sids, start, n, a, out, out_ids, slot, digest, next_cnt, next_cell);
+    boids_group_body<G, QV>(sorted, sids, start, n, a, out, out_ids, slot, digest, next_cnt, next_cell, svel);
+}
+
+// Candidate visits of one stencil pass over the current binning (the 3x3 cell
+// neighbourhood's agent count, summed over the agents; the roofline's unit of
+// work): sum over cells c of count(c) * sum of the counts of c's 3x3 stencil.
+__global__ void boids_candidates_kernel(const int* __restrict__ start, int nc, unsigned long long* out)
+{
+    unsigned long long s = 0;
+    const int64_t ncell = static_cast<int64_t>(nc) * nc;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncell; c += (int64_t)gridDim.x * blockDim.x) {
+        const int cx = static_cast<int>(c % nc), cy = static_cast<int>(c / nc);
+        const long long own = start[c + 1] - start[c];
+        if (!own) continue;
+        long long nb = 0;
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int x = (cx + dx + nc) % nc, y = (cy + dy + nc) % nc;
+                const int64_t k = static_cast<int64_t>(y) * nc + x;
+                nb += start[k + 1] - start[k];
+            }
+        s += static_cast<unsigned long long>(own * nb);
+    }
+    if (s) atomicAdd(out, s);
+}
+
+// 1 in *big if any |velocity| >= 127 or is not finite (the QV stencil's int32 range)
+__global__ void boids_big_velocity_kernel(const float4* __restrict__ st, int64_t n, unsigned int* big)
+{
+    bool b = false;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const float4 s = st[p];
+        b |= !(fabsf(s.z) < 127.0f) || !(fabsf(s.w) < 127.0f);
+    }
+    if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(big, 1u);
 }
 
 // Un-permute: column k of the state (0 x, 1 y, 2 vx, 3 vy) into id order.
@@ -787,8 +954,9 @@ public:
     DevBuf<int32_t> ids, sids;
     DevBuf<int> cnt, start, cursor, cell_of, block_sums;
     DevBuf<float> col_tmp;
-    DevBuf<char> scan_tmp;  // CUB device-scan temporary storage
-    size_t scan_bytes = 0;
+    DevBuf<int> chunk_sums;  // large-grid scan: one total per kScanChunk cells
+    DevBuf<float2> svel;     // QV: float velocities in cell-sorted order
+    bool vel_small = true;   // every |velocity| < 127 (true at init; re-checked on velocity writes)
     DevBuf<BoidsSlot> ring;
     int64_t m_first = 0;
     int ncell = 0;
@@ -832,8 +1000,8 @@ public:
         start.allocate(&rt, ncell + 1);
         cursor.allocate(&rt, ncell + 1);
         cell_of.allocate(&rt, n);
-        AMBER_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, cnt.p, start.p, ncell + 1, rt.stream));
-        scan_tmp.allocate(&rt, scan_bytes + 16);
+        chunk_sums.allocate(&rt, ceil_div(ncell + 1, kScanChunk));
+        svel.allocate(&rt, n);
         ring.allocate(&rt, metrics_cap);
         ring.zero_async(rt.stream);
         boids_init_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(philox_key(seed), n, p.L, st.p, ids.p);
@@ -845,9 +1013,18 @@ public:
     {
         if (rt.stream) cudaStreamSynchronize(rt.stream);
         st.reset(); sorted.reset(); ids.reset(); sids.reset(); cnt.reset(); start.reset(); cursor.reset();
-        cell_of.reset(); col_tmp.reset(); ring.reset(); block_sums.reset(); scan_tmp.reset();
+        cell_of.reset(); col_tmp.reset(); ring.reset(); block_sums.reset(); chunk_sums.reset(); svel.reset();
         rt.destroy();
     }
+
+    // The pre-quantised-velocity stencil (QV) needs |q24(dx)| and |q24(v)| to fit
+    // int32: R < 100, vmax < 64 (so every stepped velocity is small) and the
+    // current velocities small (false after a write of a large velocity, until
+    // the next step has clamped them); the degenerate one-cell box copies the
+    // state without the scatter pass and keeps the float records.
+    bool qv_ok() const { return p.R < 100.0f && p.vmax < 64.0f && ba.nc > 1; }
+    bool qv_now() const { return qv_ok() && vel_small && !no_qv; }
+    int64_t no_qv = 0;  // option "qv" = 0: force the float-velocity stencil (tests)
 
     int grid_for(int threads) const
     {
@@ -889,25 +1066,31 @@ public:
                     if (ncell <= (1 << 16)) {  // one launch: scan, cursors, re-zeroed counts
                         boids_scan_kernel<<<1, 1024, 0, rt.stream>>>(cnt.p, start.p, cursor.p, ncell);
                     } else {
-                        AMBER_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp.p, scan_bytes, cnt.p, start.p, ncell + 1,
-                                                                 rt.stream));
-                        AMBER_CUDA(cudaMemcpyAsync(cursor.p, start.p, static_cast<size_t>(ncell) * sizeof(int),
-                                                   cudaMemcpyDeviceToDevice, rt.stream));
-                        AMBER_CUDA(cudaMemsetAsync(cnt.p, 0, static_cast<size_t>(ncell) * sizeof(int), rt.stream));
+                        const int nch = static_cast<int>(ceil_div(ncell + 1, kScanChunk));
+                        boids_chunk_sums_kernel<<<nch, 1024, 0, rt.stream>>>(cnt.p, ncell + 1, chunk_sums.p);
+                        check_launch("boids_chunk_sums_kernel");
+                        boids_chunk_scan_kernel<<<nch, 1024, 0, rt.stream>>>(cnt.p, chunk_sums.p, ncell, start.p,
+                                                                              cursor.p);
                     }
                 });
                 check_launch("boids_scan");
                 prof.launch(rt.stream, "boids_scatter", [&] {
                     boids_scatter_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(
-                        st.p, ids.p, n, cell_of.p, cursor.p, sorted.p, sids.p, cnt.p, ncell <= (1 << 16) ? ncell : 0);
+                        st.p, ids.p, n, cell_of.p, cursor.p, sorted.p, sids.p, cnt.p, ncell <= (1 << 16) ? ncell : 0,
+                        qv_now() ? svel.p : nullptr);
                 });
                 check_launch("boids_scatter_kernel");
             }
             const BoidsArgs a = ba;
             {
+                // each block steps a contiguous range of the sorted agents: at least
+                // 8 blocks per SM, and at most 64 rounds per block for large N (many
+                // short ranges keep the blocks balanced once flocks cluster)
+                const int64_t apb = threads / lanes;
                 const int g = grid ? static_cast<int>(grid)
                                    : static_cast<int>(std::max<int64_t>(
-                                         1, std::min<int64_t>(ceil_div(n * lanes, threads), rt.num_sms * 8)));
+                                         {1, std::min<int64_t>(ceil_div(n * lanes, threads), rt.num_sms * 8),
+                                          ceil_div(n, apb * 64)}));
                 BoidsSlot* sl = ring.p + (t % metrics_cap);
                 const int dg = digest_on ? 1 : 0;
                 prof.launch(rt.stream, "boids_step", [&] {
@@ -916,20 +1099,28 @@ public:
                     // the streaming count pass (the stencil kernel is issue-bound there:
                     // fused, V3 32.8 -> 33.7 ms)
                     int* nc_cnt = ba.nc > 1 && n <= (1ll << 22) ? cnt.p : nullptr;
-                    if (lanes == 4)
-                        boids_group_kernel<4><<<g, threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a, st.p, ids.p,
-                                                                            sl, dg, nc_cnt, cell_of.p);
-                    else if (lanes == 16)
-                        boids_group_kernel<16><<<g, threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a, st.p, ids.p,
-                                                                             sl, dg, nc_cnt, cell_of.p);
-                    else
-                        boids_group_kernel<8><<<g, threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a, st.p, ids.p,
-                                                                            sl, dg, nc_cnt, cell_of.p);
+                    const bool qv = qv_now();
+#define AMBER_BOIDS_GROUP(G_, QV_, MB_)                                                                          \
+    boids_group_kernel<G_, QV_, MB_><<<g, threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a, st.p, ids.p, sl, \
+                                                                   dg, nc_cnt, cell_of.p, svel.p)
+#define AMBER_BOIDS_GROUP4(QV_)                                                  \
+    if (n > (1ll << 22)) AMBER_BOIDS_GROUP(4, QV_, AMBER_BOIDS_MINB_LARGE); \
+    else AMBER_BOIDS_GROUP(4, QV_, AMBER_BOIDS_MINB)
+                    if (lanes == 4) {
+                        if (qv) { AMBER_BOIDS_GROUP4(true); } else { AMBER_BOIDS_GROUP4(false); }
+                    } else if (lanes == 16) {
+                        if (qv) AMBER_BOIDS_GROUP(16, true, AMBER_BOIDS_MINB); else AMBER_BOIDS_GROUP(16, false, AMBER_BOIDS_MINB);
+                    } else {
+                        if (qv) AMBER_BOIDS_GROUP(8, true, AMBER_BOIDS_MINB); else AMBER_BOIDS_GROUP(8, false, AMBER_BOIDS_MINB);
+                    }
+#undef AMBER_BOIDS_GROUP4
+#undef AMBER_BOIDS_GROUP
                 });
                 check_launch("boids_group_kernel");
                 counted = ba.nc > 1 && n <= (1ll << 22);
             }
             ++t;
+            if (p.vmax < 64.0f) vel_small = true;  // the step clamped every velocity to vmax < 64
         }
     }
 
@@ -972,6 +1163,17 @@ public:
         copy_in(rt, col_tmp.p, src, n * 4, on_dev);
         boids_put_column<<<grid_for(256), 256, 0, rt.stream>>>(st.p, ids.p, n, k, col_tmp.p);
         check_launch("boids_put_column");
+        if (k >= 2) {  // a velocity column: are all velocities still small enough for the QV stencil?
+            DevBuf<unsigned int> big;
+            big.allocate(&rt, 1);
+            big.zero_async(rt.stream);
+            boids_big_velocity_kernel<<<grid_for(256), 256, 0, rt.stream>>>(st.p, n, big.p);
+            check_launch("boids_big_velocity_kernel");
+            unsigned int h = 0;
+            AMBER_CUDA(cudaMemcpyAsync(&h, big.p, 4, cudaMemcpyDeviceToHost, rt.stream));
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            vel_small = h == 0;
+        }
         // positions changed: drop the counts the last group step left (the next
         // step counts again from zero)
         if (counted) AMBER_CUDA(cudaMemsetAsync(cnt.p, 0, static_cast<size_t>(ncell) * sizeof(int), rt.stream));
@@ -1037,6 +1239,10 @@ public:
             return true;
         }
         if (k == "block") AMBER_REQUIRE(v <= 256, "Boids kernels are built for <= 256 threads per block");
+        if (k == "qv") {
+            no_qv = v ? 0 : 1;
+            return true;
+        }
         if (k == "lanes") {
             AMBER_REQUIRE(v == 4 || v == 8 || v == 16, "lanes must be 4, 8 or 16");
             lanes = v;
@@ -1053,6 +1259,23 @@ public:
         }
         if (std::string(key) == "lanes") {
             *v = lanes;
+            return true;
+        }
+        if (std::string(key) == "stencil_candidates") {  // candidate visits of the last step's stencil pass
+            AMBER_REQUIRE(ba.nc >= 3, "stencil_candidates needs >= 3 cells per side");
+            DevBuf<unsigned long long> d;
+            d.allocate(&rt, 1);
+            d.zero_async(rt.stream);
+            boids_candidates_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(start.p, ba.nc, d.p);
+            check_launch("boids_candidates_kernel");
+            unsigned long long h = 0;
+            AMBER_CUDA(cudaMemcpyAsync(&h, d.p, 8, cudaMemcpyDeviceToHost, rt.stream));
+            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            *v = static_cast<int64_t>(h);
+            return true;
+        }
+        if (std::string(key) == "qv") {  // 1: the next step runs the pre-quantised-velocity stencil
+            *v = qv_now() ? 1 : 0;
             return true;
         }
         return Model::get_option(key, v);
@@ -1076,8 +1299,7 @@ public:
     DevBuf<BoidAgent> send, recv;
     DevBuf<uint32_t> counts, keep_n;
     DevBuf<int> cnt, start, cursor;
-    DevBuf<char> scan_tmp;
-    size_t scan_bytes = 0;
+    DevBuf<int> chunk_sums;  // hand-written chunked scan (kScanChunk cells per total)
     int ncell_loc = 0;
     DevBuf<BoidsSlot> ring;
     int64_t m_first = 0;
@@ -1119,8 +1341,7 @@ public:
         cnt.zero_async(rt.stream);
         start.allocate(&rt, ncell_loc + 1);
         cursor.allocate(&rt, ncell_loc + 1);
-        AMBER_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, cnt.p, start.p, ncell_loc + 1, rt.stream));
-        scan_tmp.allocate(&rt, scan_bytes + 16);
+        chunk_sums.allocate(&rt, ceil_div(ncell_loc + 1, kScanChunk));
         ring.allocate(&rt, metrics_cap);
         ring.zero_async(rt.stream);
         // every rank draws the full seeded population (B1) and keeps its slab
@@ -1137,7 +1358,7 @@ public:
         for (auto* b : {&st, &st2, &sorted}) b->reset();
         for (auto* b : {&ids, &ids2, &sids, &cell_of}) b->reset();
         send.reset(); recv.reset(); counts.reset(); keep_n.reset(); cnt.reset(); start.reset(); cursor.reset();
-        scan_tmp.reset(); ring.reset(); d_col0.reset();
+        chunk_sums.reset(); ring.reset(); d_col0.reset();
         if (sc) destroy_shard_comm(sc);
         rt.destroy();
     }
@@ -1181,6 +1402,7 @@ public:
             AMBER_CUDA(cudaStreamSynchronize(rt.stream));
             if (got)
                 slab_unpack_kernel<<<grid_for(got), 256, 0, rt.stream>>>(recv.p, got, st2.p, ids2.p, kept);
+            check_launch("slab_unpack_kernel");
             n_own = kept + static_cast<int64_t>(got);
             std::swap(st.p, st2.p);
             std::swap(ids.p, ids2.p);
@@ -1197,11 +1419,14 @@ public:
             prof.launch(rt.stream, "boids_slab_bin", [&] {
                 slab_count_kernel<<<grid_for(tot), 256, 0, rt.stream>>>(st.p, n_own, recv.p, n_halo, g, cnt.p,
                                                                          cell_of.p);
-                AMBER_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp.p, scan_bytes, cnt.p, start.p, ncell_loc + 1,
-                                                         rt.stream));
-                AMBER_CUDA(cudaMemcpyAsync(cursor.p, start.p, static_cast<size_t>(ncell_loc) * sizeof(int),
-                                           cudaMemcpyDeviceToDevice, rt.stream));
-                AMBER_CUDA(cudaMemsetAsync(cnt.p, 0, static_cast<size_t>(ncell_loc) * sizeof(int), rt.stream));
+                check_launch("slab_count_kernel");
+                const int nch = static_cast<int>(ceil_div(ncell_loc + 1, kScanChunk));
+                boids_chunk_sums_kernel<<<nch, 1024, 0, rt.stream>>>(cnt.p, static_cast<int>(ncell_loc + 1),
+                                                                      chunk_sums.p);
+                check_launch("boids_chunk_sums_kernel");
+                boids_chunk_scan_kernel<<<nch, 1024, 0, rt.stream>>>(cnt.p, chunk_sums.p, static_cast<int>(ncell_loc),
+                                                                      start.p, cursor.p);
+                check_launch("boids_chunk_scan_kernel");
                 slab_scatter_kernel<<<grid_for(tot), 256, 0, rt.stream>>>(st.p, ids.p, n_own, recv.p, n_halo,
                                                                            cell_of.p, cursor.p, sorted.p, sids.p);
             });

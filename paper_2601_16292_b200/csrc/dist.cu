@@ -188,10 +188,31 @@ bool loopback_allgather_f64(const amber_runtime* r, const std::vector<double>& m
     return true;
 }
 
+// ---------------------------------------------------------------- host collectives
+// The caller's own host transport (amber_runtime.host_allgather / host_barrier,
+// e.g. a gloo process group): used by the sharded wealth model's P2P exchange
+// when no NCCL id is given -- IPC handles all-gathered on the host, one host
+// barrier per step after the stream drains.
+struct HostColl {
+    int (*allgather)(const void*, void*, size_t, void*) = nullptr;
+    int (*barrier)(void*) = nullptr;
+    void* ctx = nullptr;
+    bool on() const { return allgather && barrier; }
+    void gather(const void* send, void* recv, size_t bytes) const
+    {
+        if (allgather(send, recv, bytes, ctx) != 0) fail(AMBER_E_NCCL, "host_allgather failed");
+    }
+    void sync() const
+    {
+        if (barrier(ctx) != 0) fail(AMBER_E_NCCL, "host_barrier failed");
+    }
+};
+
 // ---------------------------------------------------------------- wealth exchange
 struct WealthExchange {
     Comm* comm = nullptr;                 // NCCL transport
     std::shared_ptr<LoopbackHub> hub;     // or the loopback transport
+    HostColl hc;                          // or the caller's host collectives (P2P exchange only)
     int rank = 0, world = 1;
     DevBuf<unsigned int> send_counts_copy, recv_counts;
     std::vector<unsigned int> h_send, h_recv;
@@ -203,11 +224,19 @@ WealthExchange* make_wealth_exchange_rt(Runtime& rt, const amber_runtime* r)
     auto* x = new WealthExchange;
     x->rank = rt.rank;
     x->world = rt.world;
-    AMBER_REQUIRE(r && r->nccl_unique_id, "world > 1 needs amber_runtime.nccl_unique_id");
-    if (std::memcmp(r->nccl_unique_id, kLoopbackMagic, sizeof(kLoopbackMagic)) == 0) {
-        x->hub = loopback_hub(static_cast<const char*>(r->nccl_unique_id), rt.world);
+    if (r && !r->nccl_unique_id && r->host_allgather && r->host_barrier) {
+        x->hc.allgather = r->host_allgather;
+        x->hc.barrier = r->host_barrier;
+        x->hc.ctx = r->host_ctx;
     } else {
-        x->comm = make_comm(r);
+        if (!(r && r->nccl_unique_id)) {
+            delete x;
+            fail(AMBER_E_INVALID_ARG, "world > 1 needs amber_runtime.nccl_unique_id (or host collectives)");
+        }
+        if (std::memcmp(r->nccl_unique_id, kLoopbackMagic, sizeof(kLoopbackMagic)) == 0)
+            x->hub = loopback_hub(static_cast<const char*>(r->nccl_unique_id), rt.world);
+        else
+            x->comm = make_comm(r);
     }
     x->send_counts_copy.allocate(&rt, rt.world);
     x->recv_counts.allocate(&rt, rt.world);
@@ -264,6 +293,8 @@ void wealth_exchange_run(WealthExchange* x, Runtime& rt, const unsigned int* d_s
         h.barrier();  // peers may now reuse their send buckets
         return;
     }
+    if (x->hc.on()) fail(AMBER_E_UNSUPPORTED, "host collectives carry the P2P wealth exchange only "
+                                             "(AMBER_WEALTH_EXCHANGE=nccl needs an NCCL id)");
     NcclApi& api = nccl();
     const int W = x->comm->world, me = x->comm->rank;
     // 1) sizes: one count to each peer
@@ -337,6 +368,37 @@ bool wealth_p2p_open(WealthExchange* x, Runtime& rt, void* my_base, std::vector<
         h.barrier();
         for (int p = 0; p < W; ++p) map->peers[p] = const_cast<uint32_t*>(h.send_ids[p]);
         h.barrier();
+    } else if (x->hc.on()) {
+        // cross-process mapping: CUDA IPC handles all-gathered over the host transport
+        bool ok = true;
+        cudaIpcMemHandle_t mine;
+        std::memset(&mine, 0, sizeof(mine));
+        if (cudaIpcGetMemHandle(&mine, my_base) != cudaSuccess) ok = false;
+        cudaGetLastError();
+        std::vector<cudaIpcMemHandle_t> hs(W);
+        x->hc.gather(&mine, hs.data(), sizeof(mine));
+        map->peers[me] = my_base;
+        for (int p = 0; p < W && ok; ++p) {
+            if (p == me) continue;
+            void* ptr = nullptr;
+            if (cudaIpcOpenMemHandle(&ptr, hs[p], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                ok = false;
+                break;
+            }
+            map->peers[p] = ptr;
+            map->opened[p] = true;
+        }
+        const int bad = ok ? 0 : 1;
+        std::vector<int> all(W);
+        x->hc.gather(&bad, all.data(), sizeof(int));  // every rank takes the same path
+        for (int v : all)
+            if (v) ok = false;
+        if (!ok) {
+            for (int p = 0; p < W; ++p)
+                if (map->opened[p]) cudaIpcCloseMemHandle(map->peers[p]);
+            fail(AMBER_E_CUDA, "host-collective P2P exchange: a rank could not map its peers' buckets");
+        }
     } else {
         bool ok = true;
         cudaIpcMemHandle_t mine;
@@ -405,6 +467,11 @@ void wealth_p2p_barrier(WealthExchange* x, Runtime& rt)
         x->hub->barrier();
         return;
     }
+    if (x->hc.on()) {
+        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        x->hc.sync();
+        return;
+    }
     P2PMap* mp;
     {
         std::lock_guard<std::mutex> g(p2p_mu);
@@ -428,9 +495,20 @@ static std::vector<unsigned long long> loopback_sum(WealthExchange* x, const std
     return out;
 }
 
+// host-collective all-reduce (sum) of n host values
+static std::vector<unsigned long long> host_sum(WealthExchange* x, const std::vector<unsigned long long>& mine)
+{
+    std::vector<unsigned long long> all(mine.size() * x->world), out(mine.size(), 0ull);
+    x->hc.gather(mine.data(), all.data(), mine.size() * 8);
+    for (int p = 0; p < x->world; ++p)
+        for (size_t k = 0; k < out.size(); ++k) out[k] += all[p * mine.size() + k];
+    return out;
+}
+
 bool wealth_exchange_any(WealthExchange* x, Runtime& rt, bool local_flag)
 {
     if (x->hub) return loopback_sum(x, {local_flag ? 1ull : 0ull})[0] != 0;
+    if (x->hc.on()) return host_sum(x, {local_flag ? 1ull : 0ull})[0] != 0;
     unsigned long long v = local_flag ? 1ull : 0ull;
     AMBER_CUDA(cudaMemcpyAsync(x->flag.p, &v, 8, cudaMemcpyHostToDevice, rt.stream));
     comm_allreduce_u64(x->comm, rt.stream, x->flag.p, 1);
@@ -441,11 +519,11 @@ bool wealth_exchange_any(WealthExchange* x, Runtime& rt, bool local_flag)
 
 void wealth_exchange_allreduce_u64(WealthExchange* x, Runtime& rt, unsigned long long* d_vals, int n)
 {
-    if (x->hub) {
+    if (x->hub || x->hc.on()) {
         std::vector<unsigned long long> h(n);
         AMBER_CUDA(cudaMemcpyAsync(h.data(), d_vals, n * 8, cudaMemcpyDeviceToHost, rt.stream));
         AMBER_CUDA(cudaStreamSynchronize(rt.stream));
-        h = loopback_sum(x, h);
+        h = x->hub ? loopback_sum(x, h) : host_sum(x, h);
         AMBER_CUDA(cudaMemcpyAsync(d_vals, h.data(), n * 8, cudaMemcpyHostToDevice, rt.stream));
         AMBER_CUDA(cudaStreamSynchronize(rt.stream));
         return;

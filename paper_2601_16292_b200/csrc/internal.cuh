@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <cstring>
 #include <map>
@@ -40,12 +42,49 @@ struct Error {
         if (!(cond)) ::amber::fail(AMBER_E_INVALID_ARG, std::string(msg));        \
     } while (0)
 
-// Check the last launch (launch-config errors surface here, faults later).
+// AMBER_SYNC_DEBUG=1 (environment, read once): every checked launch is followed
+// by a device synchronize, so an asynchronous fault (out-of-bounds access, a
+// failed AMBER_DCHECK) is reported against the kernel that caused it.
+inline bool sync_debug()
+{
+    static const bool on = [] {
+        const char* v = std::getenv("AMBER_SYNC_DEBUG");
+        return v && v[0] && v[0] != '0';
+    }();
+    return on;
+}
+
+// Check the last launch (launch-config errors surface here, faults later --
+// or here, under AMBER_SYNC_DEBUG).
 inline void check_launch(const char* what)
 {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(AMBER_E_CUDA, std::string("launch ") + what + ": " + cudaGetErrorString(e));
+    if (sync_debug()) {
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess)
+            fail(AMBER_E_CUDA, std::string("AMBER_SYNC_DEBUG: ") + what + " -> " + cudaGetErrorString(e));
+    }
 }
+
+// Device-side index checks, compiled in by the bounds build (-DAMBER_BOUNDS:
+// paper_2601_16292_b200/libamber_bounds.so, `python -m paper_2601_16292_b200.build
+// --bounds`); the product library compiles them out.  A failed check prints the
+// site and traps (the launch fails with an unspecified-launch-failure error).
+#ifdef AMBER_BOUNDS
+#define AMBER_DCHECK(cond, what)                                                                    \
+    do {                                                                                            \
+        if (!(cond)) {                                                                              \
+            printf("AMBER_BOUNDS %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, what,       \
+                   static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                    \
+            __trap();                                                                               \
+        }                                                                                           \
+    } while (0)
+#else
+#define AMBER_DCHECK(cond, what) \
+    do {                         \
+    } while (0)
+#endif
 
 // ---------------------------------------------------------------- runtime
 struct Runtime {

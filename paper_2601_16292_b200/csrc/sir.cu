@@ -538,7 +538,10 @@ __device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0,
             const uint32_t own = nown >= 32 ? 0xffffffffu : ((1u << nown) - 1u);
             const uint32_t sid = static_cast<uint32_t>(a.gid0 + static_cast<unsigned long long>(a0 + lid));
             const uint32_t hit = walk_rows_pay<kWalkU>(
-                [&](int32_t e) { return static_cast<uint32_t>(__ldcs(a.col + e)); }, own, rb, re, sid,
+                [&](int32_t e) {
+                    AMBER_DCHECK(e >= 0 && e < a.row_ptr[a.n], "SIR pull: arc index out of the CSR");
+                    return static_cast<uint32_t>(__ldcs(a.col + e));
+                }, own, rb, re, sid,
                 [&](uint32_t j) { return static_cast<uint32_t>(bit_of(ib, j)); },  // j: global id (global bitmap)
                 [&](uint32_t j, int32_t, int, uint32_t s) {
                     const uint4 w = philox(make_uint4(min(s, j), max(s, j), t, TAG_SIR_TX), a.key);
@@ -652,8 +655,14 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
         const uint32_t id = mine ? static_cast<uint32_t>(sm.id[wq][g0 + lane]) : 0u;
         const int32_t rb = mine ? a.row_ptr[id] : 0, re = mine ? a.row_ptr[id + 1] : 0;
         const uint32_t own = nown >= 32 ? 0xffffffffu : ((1u << nown) - 1u);
-        walk_rows_pay<kWalkU>([&](int32_t e) { return static_cast<uint32_t>(__ldcs(a.col + e)); }, own, rb, re, id,
-                              [&](uint32_t j) { return static_cast<uint32_t>(bit_of(sb, j)); },
+        walk_rows_pay<kWalkU>([&](int32_t e) {
+                                  AMBER_DCHECK(e >= 0 && e < a.row_ptr[a.n], "SIR push: arc index out of the CSR");
+                                  return static_cast<uint32_t>(__ldcs(a.col + e));
+                              }, own, rb, re, id,
+                              [&](uint32_t j) {
+                                  AMBER_DCHECK(j < static_cast<uint64_t>(a.n), "SIR push: neighbour id >= n");
+                                  return static_cast<uint32_t>(bit_of(sb, j));
+                              },
                               [&](uint32_t j, int32_t, int, uint32_t s) {
             const uint4 wd = philox(make_uint4(min(s, j), max(s, j), t, TAG_SIR_TX), a.key);
             if (static_cast<unsigned long long>(wd.x) < a.t_beta) {

@@ -170,7 +170,10 @@ __global__ void __launch_bounds__(256) sirs_persistent_kernel(const SirsArgs a)
                 const bool mine = (s_mask >> lane) & 1u;
                 const int32_t rb = mine ? a.row_ptr[u] : 0, re = mine ? a.row_ptr[u + 1] : 0;
                 exposed = walk_rows_probe<4>([&](int32_t e) { return static_cast<uint32_t>(__ldg(a.col + e)); }, s_mask,
-                                             rb, re, [&](uint32_t j) { return static_cast<uint32_t>(x[j] == kI); },
+                                             rb, re, [&](uint32_t j) {
+                                                 AMBER_DCHECK(j < static_cast<uint64_t>(a.n), "SIR-space: contact id >= n");
+                                                 return static_cast<uint32_t>(x[j] == kI);
+                                             },
                                              [](uint32_t, int32_t, int) { return true; });
             }
             uint8_t o = st;

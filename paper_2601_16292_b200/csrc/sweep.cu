@@ -99,7 +99,10 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
         __syncthreads();
         const PhiloxKey key = philox_key(a.seeds[r]);
         auto col_at = [&](int32_t e) {
-            return COL_SMEM ? static_cast<uint32_t>(cs[e]) : static_cast<uint32_t>(gcol[e]);
+            AMBER_DCHECK(e >= 0 && (!COL_SMEM || e < a.col_cap), "sweep: arc index out of the staged columns");
+            const uint32_t j = COL_SMEM ? static_cast<uint32_t>(cs[e]) : static_cast<uint32_t>(gcol[e]);
+            AMBER_DCHECK(j < static_cast<uint64_t>(a.n), "sweep: neighbour id >= n");
+            return j;
         };
         const unsigned long long tb = a.t_beta[r];
         int cur = 0;

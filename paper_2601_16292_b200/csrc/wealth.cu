@@ -112,8 +112,9 @@ __device__ __forceinline__ void red_add_hint(uint32_t* addr, uint32_t v, unsigne
 }
 
 template <int B, class Id>
-__device__ __forceinline__ void add_count(uint32_t* inc, Id rl, unsigned long long pol)
+__device__ __forceinline__ void add_count(uint32_t* inc, Id rl, unsigned long long pol, unsigned long long lim)
 {
+    AMBER_DCHECK(static_cast<unsigned long long>(rl) < lim, "wealth: receiver counter index out of the shard");
     if constexpr (B == 32) {
         red_add_hint(inc + rl, 1u, pol);
     } else {
@@ -142,6 +143,7 @@ __device__ __forceinline__ void remote_append(const WealthArgs& a, bool flag, un
     if (!flag) return;
     unsigned long long d = r / a.shard_size;
     const unsigned dest = static_cast<unsigned>(d < static_cast<unsigned long long>(a.world) ? d : a.world - 1);
+    AMBER_DCHECK(r < a.n_glob, "wealth: remote receiver id >= N");
     const unsigned peers = __match_any_sync(mask, dest);
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(peers) - 1;
@@ -223,9 +225,9 @@ __global__ void __launch_bounds__(256, AMBER_WEALTH_MINB) wealth_step_kernel(con
                         bool local = s;
                         if constexpr (REMOTE) local = s && rl < n_loc;
 #ifndef AMBER_EXPERIMENT_NO_RED
-                        if (local) add_count<B>(a.inc_next, rl, pol);
+                        if (local) add_count<B>(a.inc_next, rl, pol, n_loc);
 #else
-                        if (local && rl == ~Id(0)) add_count<B>(a.inc_next, rl, pol);  // never: cost without REDs
+                        if (local && rl == ~Id(0)) add_count<B>(a.inc_next, rl, pol, n_loc);  // never: cost without REDs
 #endif
                         sent += local;
                         if constexpr (REMOTE) remote_append(a, s && !local, r);
@@ -305,6 +307,7 @@ __global__ void __launch_bounds__(1024, 1) wealth_small_kernel(const SmallArgs a
                 if (h ? s1 : s0) {
                     unsigned long long r = mulhi64(lane64_of(x, h), m);
                     if (a.exclude_self) r += (r >= i0 + h);
+                    AMBER_DCHECK(r < n, "wealth (small): receiver >= n");
                     atomicAdd(cnt + r, 1u);
                     ++sent;
                 }
@@ -377,13 +380,13 @@ __global__ void __launch_bounds__(1024, 1) wealth_small_kernel(const SmallArgs a
 // Received cross-shard receivers -> local counters of the scattered step.
 template <int B>
 __global__ void wealth_recv_kernel(const uint32_t* __restrict__ ids, const unsigned long long* __restrict__ n_ids,
-                                   unsigned long long lo, uint32_t* inc, Slot* slot)
+                                   unsigned long long lo, unsigned long long n_loc, uint32_t* inc, Slot* slot)
 {
     const unsigned long long n = *n_ids;
     unsigned long long cnt = 0;
     for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < n;
          k += (unsigned long long)gridDim.x * blockDim.x) {
-        add_count<B>(inc, static_cast<unsigned long long>(ids[k]) - lo, policy_evict_last());
+        add_count<B>(inc, static_cast<unsigned long long>(ids[k]) - lo, policy_evict_last(), n_loc);
         cnt += 1;
     }
     unsigned long long vals[1] = {cnt};
@@ -398,7 +401,7 @@ __global__ void wealth_recv_kernel(const uint32_t* __restrict__ ids, const unsig
 template <int B>
 __global__ void wealth_recv_p2p_kernel(const unsigned long long* __restrict__ peer_base, int world, int me,
                                        size_t cnt_off, size_t ids_off, unsigned long long cap, unsigned long long lo,
-                                       uint32_t* inc, Slot* slot)
+                                       unsigned long long n_loc, uint32_t* inc, Slot* slot)
 {
     const int p = blockIdx.y;
     unsigned long long got = 0;
@@ -409,7 +412,7 @@ __global__ void wealth_recv_p2p_kernel(const unsigned long long* __restrict__ pe
         const uint32_t* ids = reinterpret_cast<const uint32_t*>(base + ids_off) + static_cast<unsigned long long>(me) * cap;
         for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < m;
              k += (unsigned long long)gridDim.x * blockDim.x) {
-            add_count<B>(inc, static_cast<unsigned long long>(__ldcs(ids + k)) - lo, policy_evict_last());
+            add_count<B>(inc, static_cast<unsigned long long>(__ldcs(ids + k)) - lo, policy_evict_last(), n_loc);
             got += 1;
         }
     }
@@ -693,7 +696,8 @@ public:
                 prof.launch(rt.stream, "wealth_recv_p2p", [&] {
                     kern<<<g, 256, 0, rt.stream>>>(p2p_peers.p, rt.world, rt.rank, p2p_cnt_off[ts & 1],
                                                    p2p_ids_off[ts & 1], static_cast<unsigned long long>(send_cap),
-                                                   static_cast<unsigned long long>(lo), ib[ts & 1].p, slot(ts));
+                                                   static_cast<unsigned long long>(lo),
+                                                   static_cast<unsigned long long>(n_loc), ib[ts & 1].p, slot(ts));
                 });
                 check_launch("wealth_recv_p2p_kernel");
             };
@@ -710,7 +714,9 @@ public:
         auto launch_recv = [&](auto kern) {
             prof.launch(rt.stream, "wealth_recv_apply", [&] {
                 kern<<<rt.num_sms * 4, 256, 0, rt.stream>>>(recv_ids.p, recv_total.p,
-                                                          static_cast<unsigned long long>(lo), ib[ts & 1].p, slot(ts));
+                                                          static_cast<unsigned long long>(lo),
+                                                          static_cast<unsigned long long>(n_loc), ib[ts & 1].p,
+                                                          slot(ts));
             });
             check_launch("wealth_recv_kernel");
         };

@@ -48,8 +48,43 @@ class TorchAllocator:
         self.free = capi.FREE_FN(_free)
 
 
-def make_runtime(device=0, stream=None, torch_alloc=True, rank=0, world=1, unique_id=None):
-    """Build an amber_runtime; keeps ctypes callbacks/buffers alive on the struct."""
+class HostCollectives:
+    """amber_runtime.host_allgather / host_barrier over a torch.distributed
+    process group of any backend (e.g. gloo): the caller's own host transport
+    for the sharded wealth model's peer-memory exchange (argument marshalling
+    only; the exchange itself is the library's CUDA IPC mapping + kernels)."""
+
+    def __init__(self, group=None):
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        self.world = dist.get_world_size(group)
+
+        def _allgather(send, recv, nbytes, ctx):
+            try:
+                src = torch.from_numpy(np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(send)).copy())
+                outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(self.world)]
+                dist.all_gather(outs, src, group=group)
+                C.memmove(recv, torch.cat(outs).numpy().ctypes.data, nbytes * self.world)
+                return 0
+            except Exception:  # reported by the library as AMBER_E_NCCL
+                return 1
+
+        def _barrier(ctx):
+            try:
+                dist.barrier(group=group)
+                return 0
+            except Exception:
+                return 1
+
+        self.allgather = capi.HOST_ALLGATHER_FN(_allgather)
+        self.barrier = capi.HOST_BARRIER_FN(_barrier)
+
+
+def make_runtime(device=0, stream=None, torch_alloc=True, rank=0, world=1, unique_id=None, host_group=None):
+    """Build an amber_runtime; keeps ctypes callbacks/buffers alive on the struct.
+    host_group: a torch.distributed process group whose host collectives carry the
+    sharded wealth exchange instead of NCCL (unique_id must then be None)."""
     rt = capi.amber_runtime()
     rt.device = device
     keep = []
@@ -65,7 +100,13 @@ def make_runtime(device=0, stream=None, torch_alloc=True, rank=0, world=1, uniqu
         rt.alloc, rt.free = ta.alloc, ta.free
         keep.append(ta)
     rt.rank, rt.world = rank, world
-    if world > 1 or unique_id is not None:
+    if host_group is not None:
+        if unique_id is not None:
+            raise ValueError("give either unique_id or host_group")
+        hc = HostCollectives(host_group)
+        rt.host_allgather, rt.host_barrier = hc.allgather, hc.barrier
+        keep.append(hc)
+    elif world > 1 or unique_id is not None:
         if unique_id is None or len(unique_id) < 128:
             raise ValueError("world > 1 needs the 128-byte NCCL unique id")
         buf = C.create_string_buffer(bytes(unique_id), 128)
@@ -116,10 +157,10 @@ class Model:
              "walk": capi.AMBER_WALK, "sir_space": capi.AMBER_SIR_SPACE}
 
     def __init__(self, kind: str, n_agents: int, params, seed: int, *, device=0, stream=None,
-                 torch_alloc=True, rank=0, world=1, unique_id=None):
+                 torch_alloc=True, rank=0, world=1, unique_id=None, host_group=None):
         self.kind = kind
         self.lib = capi.lib()
-        self.rt = make_runtime(device, stream, torch_alloc, rank, world, unique_id)
+        self.rt = make_runtime(device, stream, torch_alloc, rank, world, unique_id, host_group)
         self.stream = self.rt._keep[0]  # torch.cuda.Stream (or the caller's stream handle)
         self.params = params
         h = C.c_void_p()

@@ -94,3 +94,16 @@ def test_bench_reference_arm_small_workloads(workload):
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["impl"] == "reference" and line["workload"] == workload
     assert line["value"] > 0 and line["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_bounds_build_carries_device_checks():
+    # the AMBER_BOUNDS library (built by __graft_entry__.build) contains the
+    # device-side check messages; the product library does not
+    import os
+    pkg = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2601_16292_b200")
+    prod, bnd = os.path.join(pkg, "libamber.so"), os.path.join(pkg, "libamber_bounds.so")
+    if not os.path.exists(bnd):
+        import pytest
+        pytest.skip("bounds build not present (run __graft_entry__.build())")
+    assert b"AMBER_BOUNDS" in open(bnd, "rb").read()
+    assert b"AMBER_BOUNDS" not in open(prod, "rb").read()

@@ -196,3 +196,37 @@ def test_fused_counts_across_calls_options_and_writes(orc):
         for a, b in zip(state(m), st):
             assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
     assert m.metrics("mean_speed").shape[0] >= 1
+
+
+def test_quantised_velocity_stencil_paths(orc):
+    # the pre-quantised-velocity stencil (QV: q24(v) carried as int32 in the
+    # sorted records) and the float-velocity stencil give the same integers (B3)
+    cfg = dict(C3_BOIDS, n=20_000, L=450.0)
+    a = make(cfg)
+    assert a.get_option("qv") == 1
+    a.step(10)
+    b = make(cfg)
+    b.set_option("qv", 0)
+    assert b.get_option("qv") == 0
+    b.step(10)
+    for x, y in zip(state(a), state(b)):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    # a written velocity beyond the int32 range of q24 (|v| >= 128): the next step
+    # runs the float stencil, the clamp brings every velocity back below vmax, and
+    # the steps after it run QV again -- each step equal to the oracle
+    c = make(cfg)
+    st = oinit(orc, cfg, c)
+    vx = (st[2] * np.float32(300.0)).astype(np.float32)
+    c.write_column("vel_x", vx)
+    st = (st[0], st[1], vx, st[3])
+    assert c.get_option("qv") == 0
+    P = oparams(orc, cfg)
+    for k in range(4):
+        c.step(1)
+        st = orc.boids_step(st, P)
+        for x, y in zip(state(c), st):
+            assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), k
+        assert c.get_option("qv") == 1
+    # vmax >= 64: velocities may leave the QV range, the float stencil always runs
+    d = make(dict(cfg, vmax=80.0, L=2000.0))
+    assert d.get_option("qv") == 0

@@ -1,0 +1,37 @@
+"""Cross-process peer-memory exchange on one B200: two
+processes, one GPU, gloo host collectives.  The sharded wealth step's P2P path
+-- cudaIpcGetMemHandle / cudaIpcOpenMemHandle of the bucket blocks and
+wealth_recv_p2p_kernel reading the OTHER process's buckets -- must equal the
+unsharded oracle bit for bit (column, all-reduced total / active / digest),
+including the collective overflow replay with 2-bit counters."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("n,steps,bits", [(200_003, 12, 4), (90_001, 10, 2)])
+def test_two_process_ipc_exchange_bit_exact(tmp_path, n, steps, bits):
+    out = tmp_path / "res.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+           os.path.join(ROOT, "tests", "mp_wealth_ipc_worker.py"), str(out), str(n), "77", str(steps), str(bits)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.load(open(out))
+    assert res["exchange"] == 2, res  # the P2P (IPC-mapped) exchange ran
+    assert res["column_equal"] and res["total_equal"] and res["active_equal"] and res["digest_equal"], res
+    if bits == 2:
+        assert res["replays"] > 0, res  # overflow detected and replayed on both ranks together
