@@ -1006,7 +1006,7 @@ public:
         ring.zero_async(rt.stream);
         boids_init_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(philox_key(seed), n, p.L, st.p, ids.p);
         check_launch("boids_init_kernel");
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
     }
 
     ~BoidsModel() override
@@ -1171,13 +1171,13 @@ public:
             check_launch("boids_big_velocity_kernel");
             unsigned int h = 0;
             AMBER_CUDA(cudaMemcpyAsync(&h, big.p, 4, cudaMemcpyDeviceToHost, rt.stream));
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
             vel_small = h == 0;
         }
         // positions changed: drop the counts the last group step left (the next
         // step counts again from zero)
         if (counted) AMBER_CUDA(cudaMemsetAsync(cnt.p, 0, static_cast<size_t>(ncell) * sizeof(int), rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         counted = false;
     }
 
@@ -1188,7 +1188,7 @@ public:
             fail(AMBER_E_UNKNOWN_NAME, "no metric " + k);
         std::vector<BoidsSlot> h(metrics_cap);
         AMBER_CUDA(cudaMemcpyAsync(h.data(), ring.p, metrics_cap * sizeof(BoidsSlot), cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         const int64_t first = std::max(m_first, t - metrics_cap + 1);
         const int64_t cnt_ = std::max<int64_t>(t - first, 0);
         if (bytes < static_cast<size_t>(cnt_) * 8) fail(AMBER_E_BUFFER_TOO_SMALL, "metrics dst too small");
@@ -1204,7 +1204,7 @@ public:
 
     void reset_metrics() override
     {
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         m_first = t;
     }
 
@@ -1221,7 +1221,7 @@ public:
     void set_step(int64_t s) override
     {
         AMBER_REQUIRE(s >= 0, "step out of range");
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         t = s;
         m_first = s;
     }
@@ -1231,7 +1231,7 @@ public:
         std::string k(key);
         if (k == "metrics_capacity") {
             AMBER_REQUIRE(v >= 16, "metrics_capacity must be >= 16");
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
             metrics_cap = v;
             ring.allocate(&rt, metrics_cap);
             ring.zero_async(rt.stream);
@@ -1270,7 +1270,7 @@ public:
             check_launch("boids_candidates_kernel");
             unsigned long long h = 0;
             AMBER_CUDA(cudaMemcpyAsync(&h, d.p, 8, cudaMemcpyDeviceToHost, rt.stream));
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
             *v = static_cast<int64_t>(h);
             return true;
         }
@@ -1349,7 +1349,7 @@ public:
         check_launch("boids_init_kernel");
         pick(st2.p, ids2.p);
         sc = make_shard_comm(rt, r);
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
     }
 
     ~BoidsShardModel() override
@@ -1377,7 +1377,7 @@ public:
         check_launch("slab_pick_kernel");
         uint32_t h = 0;
         AMBER_CUDA(cudaMemcpyAsync(&h, keep_n.p, 4, cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         n_own = h;
     }
 
@@ -1399,7 +1399,7 @@ public:
             const uint64_t got = shard_alltoallv(sc, rt, send.p, counts.p, cap, sizeof(BoidAgent), recv.p, n);
             uint32_t kept = 0;
             AMBER_CUDA(cudaMemcpyAsync(&kept, keep_n.p, 4, cudaMemcpyDeviceToHost, rt.stream));
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
             if (got)
                 slab_unpack_kernel<<<grid_for(got), 256, 0, rt.stream>>>(recv.p, got, st2.p, ids2.p, kept);
             check_launch("slab_unpack_kernel");
@@ -1435,7 +1435,7 @@ public:
             int own_rng[2] = {0, 0};
             AMBER_CUDA(cudaMemcpyAsync(&own_rng[0], start.p + ba.nc, 4, cudaMemcpyDeviceToHost, rt.stream));
             AMBER_CUDA(cudaMemcpyAsync(&own_rng[1], start.p + (w + 1) * ba.nc, 4, cudaMemcpyDeviceToHost, rt.stream));
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
             AMBER_REQUIRE(own_rng[1] - own_rng[0] == n_own, "sharded Boids: own agents outside the slab columns");
             const int gsteps = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_own * 4, 256),
                                                                                         rt.num_sms * 8)));
@@ -1506,7 +1506,7 @@ public:
         copy_in(rt, f.p, src, n * 4, on_dev);
         boids_put_column<<<grid_for(n_own), 256, 0, rt.stream>>>(st.p, ids.p, n_own, k, f.p);
         check_launch("boids_put_column");
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
     }
 
     void read_metrics(const char* name, void* dst, size_t bytes, int64_t* n_out) override
@@ -1516,7 +1516,7 @@ public:
             fail(AMBER_E_UNKNOWN_NAME, "no metric " + k);
         std::vector<BoidsSlot> h(metrics_cap);
         AMBER_CUDA(cudaMemcpyAsync(h.data(), ring.p, metrics_cap * sizeof(BoidsSlot), cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         const int64_t first = std::max(m_first, t - metrics_cap + 1);
         const int64_t cnt_ = std::max<int64_t>(t - first, 0);
         if (bytes < static_cast<size_t>(cnt_) * 8) fail(AMBER_E_BUFFER_TOO_SMALL, "metrics dst too small");
@@ -1537,7 +1537,7 @@ public:
                                 8 * cnt_);
             all.resize(4 * cnt_ * rt.world);
             AMBER_CUDA(cudaMemcpyAsync(all.data(), d.p, all.size() * 8, cudaMemcpyDeviceToHost, rt.stream));
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
         }
         for (int64_t s = 0; s < cnt_; ++s) {
             double sp = 0, px = 0, py = 0;
@@ -1560,7 +1560,7 @@ public:
 
     void reset_metrics() override
     {
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         m_first = t;
     }
 
@@ -1581,7 +1581,7 @@ public:
     void set_step(int64_t s) override
     {
         AMBER_REQUIRE(s >= 0, "step out of range");
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         t = s;
         m_first = s;
     }
@@ -1591,7 +1591,7 @@ public:
         std::string k(key);
         if (k == "metrics_capacity") {
             AMBER_REQUIRE(v >= 16, "metrics_capacity must be >= 16");
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
             metrics_cap = v;
             ring.allocate(&rt, metrics_cap);
             ring.zero_async(rt.stream);

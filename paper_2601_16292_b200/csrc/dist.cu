@@ -18,6 +18,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <set>
 
 #include "internal.cuh"
 #include "nccl.h"
@@ -38,8 +39,22 @@ struct NcclApi {
     decltype(&ncclRecv) Recv = nullptr;
     decltype(&ncclGroupStart) GroupStart = nullptr;
     decltype(&ncclGroupEnd) GroupEnd = nullptr;
+    decltype(&ncclCommGetAsyncError) CommGetAsyncError = nullptr;
+    decltype(&ncclCommAbort) CommAbort = nullptr;
     std::string error;
 };
+
+// communicators aborted by Runtime::sync (never ncclCommDestroy'd afterwards)
+std::mutex& aborted_mu()
+{
+    static std::mutex m;
+    return m;
+}
+std::set<void*>& aborted()
+{
+    static std::set<void*> s;
+    return s;
+}
 
 NcclApi& nccl()
 {
@@ -65,7 +80,24 @@ NcclApi& nccl()
         AMBER_SYM(Recv, ncclRecv)
         AMBER_SYM(GroupStart, ncclGroupStart)
         AMBER_SYM(GroupEnd, ncclGroupEnd)
+        AMBER_SYM(CommGetAsyncError, ncclCommGetAsyncError)
+        AMBER_SYM(CommAbort, ncclCommAbort)
 #undef AMBER_SYM
+        if (api.error.empty()) {
+            // Runtime::sync polls these while it waits on a stream with collectives
+            g_nccl_async_error = [](void* comm, std::string* msg) -> int {
+                ncclResult_t e = ncclSuccess;
+                if (api.CommGetAsyncError(static_cast<ncclComm_t>(comm), &e) != ncclSuccess) return 0;
+                if (e == ncclSuccess || e == ncclInProgress) return 0;
+                if (msg) *msg = api.GetErrorString(e);
+                return 1;
+            };
+            g_nccl_abort = [](void* comm) {
+                api.CommAbort(static_cast<ncclComm_t>(comm));
+                std::lock_guard<std::mutex> g(aborted_mu());
+                aborted().insert(comm);
+            };
+        }
     });
     if (!api.error.empty()) fail(AMBER_E_NCCL, api.error);
     return api;
@@ -106,7 +138,12 @@ Comm* make_comm(const amber_runtime* r)
 void destroy_comm(Comm* c)
 {
     if (!c) return;
-    if (c->comm) nccl().CommDestroy(c->comm);
+    bool was_aborted = false;
+    {
+        std::lock_guard<std::mutex> g(aborted_mu());
+        was_aborted = aborted().erase(c->comm) > 0;
+    }
+    if (c->comm && !was_aborted) nccl().CommDestroy(c->comm);
     delete c;
 }
 
@@ -235,8 +272,10 @@ WealthExchange* make_wealth_exchange_rt(Runtime& rt, const amber_runtime* r)
         }
         if (std::memcmp(r->nccl_unique_id, kLoopbackMagic, sizeof(kLoopbackMagic)) == 0)
             x->hub = loopback_hub(static_cast<const char*>(r->nccl_unique_id), rt.world);
-        else
+        else {
             x->comm = make_comm(r);
+            rt.nccl_comms.push_back(x->comm->comm);
+        }
     }
     x->send_counts_copy.allocate(&rt, rt.world);
     x->recv_counts.allocate(&rt, rt.world);
@@ -273,7 +312,7 @@ void wealth_exchange_run(WealthExchange* x, Runtime& rt, const unsigned int* d_s
         const int W = x->world, me = x->rank;
         AMBER_CUDA(cudaMemcpyAsync(x->h_send.data(), d_send_counts, W * sizeof(unsigned), cudaMemcpyDeviceToHost,
                                    rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));  // send buckets complete
+        rt.sync();  // send buckets complete
         h.counts[me].assign(x->h_send.begin(), x->h_send.end());
         h.send_ids[me] = d_send_ids;
         h.send_cap[me] = send_cap;
@@ -289,7 +328,7 @@ void wealth_exchange_run(WealthExchange* x, Runtime& rt, const unsigned int* d_s
             total += c;
         }
         AMBER_CUDA(cudaMemcpyAsync(d_recv_total, &total, sizeof(total), cudaMemcpyHostToDevice, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         h.barrier();  // peers may now reuse their send buckets
         return;
     }
@@ -308,7 +347,7 @@ void wealth_exchange_run(WealthExchange* x, Runtime& rt, const unsigned int* d_s
                                rt.stream));
     AMBER_CUDA(cudaMemcpyAsync(x->h_recv.data(), x->recv_counts.p, W * sizeof(unsigned), cudaMemcpyDeviceToHost,
                                rt.stream));
-    AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    rt.sync();
     // overflow is agreed on by every rank BEFORE any payload send/recv is
     // posted, so no rank throws with a group open while its peers block in
     // their matching grouped calls
@@ -329,7 +368,7 @@ void wealth_exchange_run(WealthExchange* x, Runtime& rt, const unsigned int* d_s
     }
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
     AMBER_CUDA(cudaMemcpyAsync(d_recv_total, &total, sizeof(total), cudaMemcpyHostToDevice, rt.stream));
-    AMBER_CUDA(cudaStreamSynchronize(rt.stream));  // `total` lives on this host stack frame
+    rt.sync();  // `total` lives on this host stack frame
 }
 
 // ---------------------------------------------------------------- wealth P2P exchange
@@ -371,9 +410,14 @@ bool wealth_p2p_open(WealthExchange* x, Runtime& rt, void* my_base, std::vector<
     } else if (x->hc.on()) {
         // cross-process mapping: CUDA IPC handles all-gathered over the host transport
         bool ok = true;
+        std::string why;
         cudaIpcMemHandle_t mine;
         std::memset(&mine, 0, sizeof(mine));
-        if (cudaIpcGetMemHandle(&mine, my_base) != cudaSuccess) ok = false;
+        cudaError_t e = cudaIpcGetMemHandle(&mine, my_base);
+        if (e != cudaSuccess) {
+            ok = false;
+            why = std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e);
+        }
         cudaGetLastError();
         std::vector<cudaIpcMemHandle_t> hs(W);
         x->hc.gather(&mine, hs.data(), sizeof(mine));
@@ -381,9 +425,11 @@ bool wealth_p2p_open(WealthExchange* x, Runtime& rt, void* my_base, std::vector<
         for (int p = 0; p < W && ok; ++p) {
             if (p == me) continue;
             void* ptr = nullptr;
-            if (cudaIpcOpenMemHandle(&ptr, hs[p], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            e = cudaIpcOpenMemHandle(&ptr, hs[p], cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) {
                 cudaGetLastError();
                 ok = false;
+                why = std::string("cudaIpcOpenMemHandle(rank ") + std::to_string(p) + "): " + cudaGetErrorString(e);
                 break;
             }
             map->peers[p] = ptr;
@@ -397,7 +443,8 @@ bool wealth_p2p_open(WealthExchange* x, Runtime& rt, void* my_base, std::vector<
         if (!ok) {
             for (int p = 0; p < W; ++p)
                 if (map->opened[p]) cudaIpcCloseMemHandle(map->peers[p]);
-            fail(AMBER_E_CUDA, "host-collective P2P exchange: a rank could not map its peers' buckets");
+            fail(AMBER_E_CUDA, "host-collective P2P exchange: a rank could not map its peers' buckets" +
+                                   (why.empty() ? std::string(" (another rank failed)") : ": " + why));
         }
     } else {
         bool ok = true;
@@ -412,7 +459,7 @@ bool wealth_p2p_open(WealthExchange* x, Runtime& rt, void* my_base, std::vector<
         nccl_check(nccl().AllGather(one.p, all.p, sizeof(mine), ncclChar, x->comm->comm, rt.stream), "ncclAllGather(ipc)");
         std::vector<cudaIpcMemHandle_t> hs(W);
         AMBER_CUDA(cudaMemcpyAsync(hs.data(), all.p, W * sizeof(mine), cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         map->peers[me] = my_base;
         for (int p = 0; p < W && ok; ++p) {
             if (p == me) continue;
@@ -432,7 +479,7 @@ bool wealth_p2p_open(WealthExchange* x, Runtime& rt, void* my_base, std::vector<
         AMBER_CUDA(cudaMemcpyAsync(flag.p, &bad, 8, cudaMemcpyHostToDevice, rt.stream));
         comm_allreduce_u64(x->comm, rt.stream, flag.p, 1);
         AMBER_CUDA(cudaMemcpyAsync(&bad, flag.p, 8, cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         if (bad) {
             for (int p = 0; p < W; ++p)
                 if (map->opened[p]) cudaIpcCloseMemHandle(map->peers[p]);
@@ -463,12 +510,12 @@ void wealth_p2p_close(WealthExchange* x)
 void wealth_p2p_barrier(WealthExchange* x, Runtime& rt)
 {
     if (x->hub) {
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         x->hub->barrier();
         return;
     }
     if (x->hc.on()) {
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         x->hc.sync();
         return;
     }
@@ -513,7 +560,7 @@ bool wealth_exchange_any(WealthExchange* x, Runtime& rt, bool local_flag)
     AMBER_CUDA(cudaMemcpyAsync(x->flag.p, &v, 8, cudaMemcpyHostToDevice, rt.stream));
     comm_allreduce_u64(x->comm, rt.stream, x->flag.p, 1);
     AMBER_CUDA(cudaMemcpyAsync(&v, x->flag.p, 8, cudaMemcpyDeviceToHost, rt.stream));
-    AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    rt.sync();
     return v != 0;
 }
 
@@ -522,10 +569,10 @@ void wealth_exchange_allreduce_u64(WealthExchange* x, Runtime& rt, unsigned long
     if (x->hub || x->hc.on()) {
         std::vector<unsigned long long> h(n);
         AMBER_CUDA(cudaMemcpyAsync(h.data(), d_vals, n * 8, cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         h = x->hub ? loopback_sum(x, h) : host_sum(x, h);
         AMBER_CUDA(cudaMemcpyAsync(d_vals, h.data(), n * 8, cudaMemcpyHostToDevice, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         return;
     }
     comm_allreduce_u64(x->comm, rt.stream, d_vals, static_cast<size_t>(n));
@@ -549,8 +596,10 @@ ShardComm* make_shard_comm(Runtime& rt, const amber_runtime* r)
     c->world = rt.world;
     if (std::memcmp(r->nccl_unique_id, kLoopbackMagic, sizeof(kLoopbackMagic)) == 0)
         c->hub = loopback_hub(static_cast<const char*>(r->nccl_unique_id), rt.world);
-    else
+    else {
         c->comm = make_comm(r);
+        rt.nccl_comms.push_back(c->comm->comm);
+    }
     return c;
 }
 
@@ -567,7 +616,7 @@ void shard_allgather_u32(ShardComm* c, Runtime& rt, const uint32_t* send, uint32
 {
     if (c->hub) {
         LoopbackHub& h = *c->hub;
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));  // my send block is complete
+        rt.sync();  // my send block is complete
         {
             std::lock_guard<std::mutex> g(h.mu);
             if (h.vals[c->rank].size() < 1) h.vals[c->rank].resize(1);
@@ -579,7 +628,7 @@ void shard_allgather_u32(ShardComm* c, Runtime& rt, const uint32_t* send, uint32
             AMBER_CUDA(cudaMemcpyAsync(recv + p * count, src, count * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
                                        rt.stream));
         }
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         h.barrier();  // peers may now overwrite their send blocks
         return;
     }
@@ -596,7 +645,7 @@ uint64_t shard_alltoallv(ShardComm* c, Runtime& rt, const void* send, const uint
     const int W = c->world, me = c->rank;
     std::vector<uint32_t> hs(W);
     AMBER_CUDA(cudaMemcpyAsync(hs.data(), d_counts, W * sizeof(uint32_t), cudaMemcpyDeviceToHost, rt.stream));
-    AMBER_CUDA(cudaStreamSynchronize(rt.stream));  // counts and send blocks complete
+    rt.sync();  // counts and send blocks complete
     for (int p = 0; p < W; ++p)
         if (hs[p] > cap) fail(AMBER_E_CUDA, "shard exchange: send bucket overflow (capacity " + std::to_string(cap) + ")");
     const char* sb = static_cast<const char*>(send);
@@ -617,7 +666,7 @@ uint64_t shard_alltoallv(ShardComm* c, Runtime& rt, const void* send, const uint
                                            k * elem, cudaMemcpyDeviceToDevice, rt.stream));
             total += k;
         }
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         h.barrier();  // peers may now reuse their send blocks
         return total;
     }
@@ -632,7 +681,7 @@ uint64_t shard_alltoallv(ShardComm* c, Runtime& rt, const void* send, const uint
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
     std::vector<uint32_t> hr(W);
     AMBER_CUDA(cudaMemcpyAsync(hr.data(), rc.p, W * sizeof(uint32_t), cudaMemcpyDeviceToHost, rt.stream));
-    AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    rt.sync();
     uint64_t total = 0;
     for (int p = 0; p < W; ++p) total += hr[p];
     if (total > recv_cap) fail(AMBER_E_CUDA, "shard exchange: receive buffer overflow");
@@ -646,7 +695,7 @@ uint64_t shard_alltoallv(ShardComm* c, Runtime& rt, const void* send, const uint
         off += hr[p];
     }
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
-    AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    rt.sync();
     return total;
 }
 
@@ -657,7 +706,7 @@ void shard_allreduce_u64(ShardComm* c, Runtime& rt, unsigned long long* d, size_
         LoopbackHub& h = *c->hub;
         std::vector<unsigned long long> mine(n);
         AMBER_CUDA(cudaMemcpyAsync(mine.data(), d, n * 8, cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         h.vals[c->rank] = mine;
         h.barrier();
         std::vector<unsigned long long> out(n, 0ull);
@@ -665,7 +714,7 @@ void shard_allreduce_u64(ShardComm* c, Runtime& rt, unsigned long long* d, size_
             for (size_t k = 0; k < n; ++k) out[k] += h.vals[p][k];
         h.barrier();
         AMBER_CUDA(cudaMemcpyAsync(d, out.data(), n * 8, cudaMemcpyHostToDevice, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         return;
     }
     comm_allreduce_u64(c->comm, rt.stream, d, n);

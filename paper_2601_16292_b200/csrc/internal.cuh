@@ -97,11 +97,23 @@ struct Runtime {
     int rank = 0, world = 1;
     int num_sms = 148;
 
+    std::vector<void*> nccl_comms;  // communicators this runtime's stream runs collectives on
+
     void init(const amber_runtime* rt);
     void destroy();
     void* alloc_bytes(size_t bytes);
     void free_bytes(void* p, size_t bytes);
+    // Host wait for the stream.  With NCCL communicators attached, a polling
+    // wait: ncclCommGetAsyncError on each, and a host timeout
+    // (AMBER_NCCL_TIMEOUT_S, default 600 s); on an asynchronous NCCL error or
+    // the timeout the communicators are aborted and the call fails with
+    // AMBER_E_NCCL, so one dead rank cannot hang the others forever.
+    void sync();
 };
+
+// NCCL hooks for Runtime::sync (defined in dist.cu): 0 = fine, else the message.
+extern int (*g_nccl_async_error)(void* comm, std::string* msg);
+extern void (*g_nccl_abort)(void* comm);
 
 // RAII device buffer allocated through the runtime's allocator.
 template <class T>

@@ -876,7 +876,7 @@ struct Population {
         std::swap(alive.p, na.p);
         std::swap(alive.n, na.n);
         alive.rt = &rt;
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         cap = nc;
     }
 
@@ -910,7 +910,7 @@ struct Population {
             }
             pop_new_rows_kernel<<<grid_for(n), 256, 0, rt.stream>>>(ids.p, alive.p, rows, rows + n, next_id);
             check_launch("pop_new_rows_kernel");
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
         }
         rows += n;
         live += n;
@@ -932,7 +932,7 @@ struct Population {
         check_launch("pop_find_kernel");
         int hb = 0;
         AMBER_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         if (hb) fail(AMBER_E_INVALID_ARG, "unknown or dead agent id");
     }
 
@@ -946,7 +946,7 @@ struct Population {
         find_rows(u.data(), n, d_rows);
         pop_kill_kernel<<<grid_for(n), 256, 0, rt.stream>>>(alive.p, d_rows.p, n, nullptr);
         check_launch("pop_kill_kernel");
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         live -= n;
     }
 
@@ -965,18 +965,18 @@ struct Population {
                 DevBuf<char> t;
                 t.allocate(&rt, tmp + 16);
                 AMBER_CUDA(cub::DeviceSelect::Flagged(t.p, tmp, in, alive.p, o, n_sel.p, rows, rt.stream));
-                AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+                rt.sync();
             };
             if (esz == 1) run(static_cast<uint8_t*>(data), reinterpret_cast<uint8_t*>(out.p));
             else if (esz == 4) run(static_cast<uint32_t*>(data), reinterpret_cast<uint32_t*>(out.p));
             else run(static_cast<unsigned long long*>(data), reinterpret_cast<unsigned long long*>(out.p));
             AMBER_CUDA(cudaMemcpyAsync(data, out.p, live * esz, cudaMemcpyDeviceToDevice, rt.stream));
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
         };
         for (auto& c : cols) select(c->data.p, dtype_size(c->dtype));
         select(ids.p, 8);
         AMBER_CUDA(cudaMemsetAsync(alive.p, 1, live, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         rows = live;
     }
 
@@ -1104,7 +1104,7 @@ struct Population {
         if (!want_count) return -1;  // asynchronous: nothing to wait for
         unsigned long long h = 0;
         AMBER_CUDA(cudaMemcpyAsync(&h, cnt.p, 8, cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         return static_cast<int64_t>(h);
     }
 
@@ -1136,14 +1136,14 @@ struct Population {
             AMBER_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(jk), dim3(g), dim3(256), kargs, 0, rt.stream));
             check_launch("amber_jit_aggregate");
             AMBER_CUDA(cudaMemcpyAsync(h.data(), part.p, h.size() * 8, cudaMemcpyDeviceToHost, rt.stream));
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
         } else if (rows) {
             ++n_interp;
             pop_aggregate_kernel<<<g, kThreads, smem, rt.stream>>>(pe, pw, views(), ids.p, alive.p, rows,
                                                            static_cast<uint32_t>(step), key, part.p);
             check_launch("pop_aggregate_kernel");
             AMBER_CUDA(cudaMemcpyAsync(h.data(), part.p, h.size() * 8, cudaMemcpyDeviceToHost, rt.stream));
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
         } else {
             for (int b = 0; b < g; ++b) {
                 h[4 * b + 1] = INFINITY;
@@ -1189,7 +1189,7 @@ struct Population {
             DevBuf<char> t;
             t.allocate(&rt, tmp + 16);
             AMBER_CUDA(cub::DeviceSelect::Flagged(t.p, tmp, in, alive.p, o, n_sel.p, rows, rt.stream));
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
         };
         if (esz == 1) run(static_cast<uint8_t*>(data), reinterpret_cast<uint8_t*>(out.p));
         else if (esz == 4) run(static_cast<uint32_t*>(data), reinterpret_cast<uint32_t*>(out.p));
@@ -1219,7 +1219,7 @@ struct Population {
         pop_scatter_kernel<<<grid_for(v.size()), 256, 0, rt.stream>>>(ColView{cols[k]->data.p, cols[k]->dtype}, d_rows.p,
                                                                       d_vals.p, static_cast<int64_t>(v.size()));
         check_launch("pop_scatter_kernel");
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
     }
 };
 

@@ -1,5 +1,9 @@
 // runtime.cu -- runtime binding, allocator hooks, profiler, column/metric
 // copies and the generic digest reduction (product path).
+#include <chrono>
+#include <cstdlib>
+#include <thread>
+
 #include "internal.cuh"
 
 namespace amber {
@@ -25,6 +29,41 @@ void Runtime::init(const amber_runtime* r)
     world = (r && r->world > 1) ? r->world : 1;
     AMBER_REQUIRE(rank >= 0 && rank < world, "amber_runtime.rank out of [0, world)");
     AMBER_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
+}
+
+int (*g_nccl_async_error)(void* comm, std::string* msg) = nullptr;
+void (*g_nccl_abort)(void* comm) = nullptr;
+
+void Runtime::sync()
+{
+    if (nccl_comms.empty() || !g_nccl_async_error) {
+        AMBER_CUDA(cudaStreamSynchronize(stream));
+        return;
+    }
+    static const double limit = [] {
+        const char* v = std::getenv("AMBER_NCCL_TIMEOUT_S");
+        return v && *v ? std::atof(v) : 600.0;
+    }();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (long it = 0;; ++it) {
+        const cudaError_t q = cudaStreamQuery(stream);
+        if (q == cudaSuccess) return;
+        if (q != cudaErrorNotReady) AMBER_CUDA(q);
+        std::string msg;
+        for (void* c : nccl_comms)
+            if (g_nccl_async_error(c, &msg)) {
+                for (void* d : nccl_comms) g_nccl_abort(d);
+                nccl_comms.clear();
+                fail(AMBER_E_NCCL, "NCCL asynchronous error: " + msg);
+            }
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (el > limit) {
+            for (void* d : nccl_comms) g_nccl_abort(d);
+            nccl_comms.clear();
+            fail(AMBER_E_NCCL, "NCCL wait exceeded AMBER_NCCL_TIMEOUT_S (a peer rank stopped?); communicators aborted");
+        }
+        if (it > 2000) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
 }
 
 void Runtime::destroy()
@@ -142,7 +181,7 @@ void copy_out(Runtime& rt, void* dst, const void* src, size_t bytes, bool dst_on
     if (!bytes) return;
     AMBER_CUDA(cudaMemcpyAsync(dst, src, bytes, dst_on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                                rt.stream));
-    AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    rt.sync();
 }
 
 void copy_in(Runtime& rt, void* dst, const void* src, size_t bytes, bool src_on_dev)
@@ -150,7 +189,7 @@ void copy_in(Runtime& rt, void* dst, const void* src, size_t bytes, bool src_on_
     if (!bytes) return;
     AMBER_CUDA(cudaMemcpyAsync(dst, src, bytes, src_on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                                rt.stream));
-    AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    rt.sync();
 }
 
 template <class T>
@@ -163,7 +202,7 @@ void read_ring(Runtime& rt, const T* ring, int64_t cap, int64_t first, int64_t e
         fail(AMBER_E_BUFFER_TOO_SMALL, "metrics buffer too small: need " + std::to_string(n * sizeof(T)) + " bytes");
     std::vector<T> host(cap);
     AMBER_CUDA(cudaMemcpyAsync(host.data(), ring, cap * sizeof(T), cudaMemcpyDeviceToHost, rt.stream));
-    AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    rt.sync();
     T* out = static_cast<T*>(dst);
     for (int64_t s = lo; s < end; ++s) out[s - lo] = host[s % cap];
     if (n_out) *n_out = n;
@@ -201,7 +240,7 @@ static uint64_t device_digest(Runtime& rt, const T* col, int64_t n, int64_t id0)
     check_launch("digest_kernel");
     unsigned long long h = 0;
     AMBER_CUDA(cudaMemcpyAsync(&h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, rt.stream));
-    AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+    rt.sync();
     return h;
 }
 

@@ -910,7 +910,7 @@ public:
             slice_graph();
             ib_glob.allocate(&rt, static_cast<size_t>(rt.world) * (shard / 32) + kChunkMax / 32);  // + one chunk of slack
             sc = make_shard_comm(rt, r);
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
         } else {
             build_init_state(rt, seeds, n, n_pad, k_inf, x[0].p);
         }
@@ -919,7 +919,7 @@ public:
         ring.allocate(&rt, metrics_cap);
         ring.zero_async(rt.stream);
         seed_counts(static_cast<unsigned long long>(n - k_inf), static_cast<unsigned long long>(k_inf), 0ull);
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
     }
 
     // Bitmaps of the current state; the back buffers become a copy of it (the
@@ -941,7 +941,7 @@ public:
         std::vector<int32_t> ends(2);
         AMBER_CUDA(cudaMemcpyAsync(&ends[0], g.row_ptr.p + lo, 4, cudaMemcpyDeviceToHost, rt.stream));
         AMBER_CUDA(cudaMemcpyAsync(&ends[1], g.row_ptr.p + lo + nl, 4, cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         const int64_t arcs = ends[1] - ends[0];
         DevBuf<int32_t> rp, col;
         rp.allocate(&rt, nl + 1);
@@ -950,7 +950,7 @@ public:
         check_launch("sir_rebase_kernel");
         if (arcs)
             AMBER_CUDA(cudaMemcpyAsync(col.p, g.col.p + ends[0], arcs * 4, cudaMemcpyDeviceToDevice, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         std::swap(g.row_ptr.p, rp.p);
         std::swap(g.row_ptr.n, rp.n);
         std::swap(g.col.p, col.p);
@@ -971,7 +971,7 @@ public:
         const SirSlot v{S, I, R, 0};
         AMBER_CUDA(cudaMemcpyAsync(ring.p + (t + metrics_cap - 1) % metrics_cap, &v, sizeof(v),
                                    cudaMemcpyHostToDevice, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         prev_ok = true;
     }
 
@@ -1131,7 +1131,7 @@ public:
         AMBER_CUDA(cudaMemcpyAsync(d.p, h, cnt * 8, cudaMemcpyHostToDevice, rt.stream));
         shard_allreduce_u64(sc, rt, d.p, cnt);
         AMBER_CUDA(cudaMemcpyAsync(h, d.p, cnt * 8, cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
     }
 
     // Sharded: "state" is this rank's slice [lo, lo + nl) of the global column;
@@ -1203,7 +1203,7 @@ public:
         else fail(AMBER_E_UNKNOWN_NAME, "no metric " + k);
         std::vector<SirSlot> h(metrics_cap);
         AMBER_CUDA(cudaMemcpyAsync(h.data(), ring.p, metrics_cap * sizeof(SirSlot), cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         const int64_t first = std::max(m_first, t - metrics_cap);
         const int64_t cnt = std::max<int64_t>(t - first, 0);
         if (bytes < static_cast<size_t>(cnt) * 8) fail(AMBER_E_BUFFER_TOO_SMALL, "metrics dst too small");
@@ -1217,7 +1217,7 @@ public:
 
     void reset_metrics() override
     {
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         m_first = t;
     }
 
@@ -1239,7 +1239,7 @@ public:
     void set_step(int64_t s) override
     {
         AMBER_REQUIRE(s >= 0 && s < (1ll << 32), "step out of range");
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         t = s;
         m_first = s;
         recount();
@@ -1250,7 +1250,7 @@ public:
         std::string k(key);
         if (k == "metrics_capacity") {
             AMBER_REQUIRE(v >= 16, "metrics_capacity must be >= 16");
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
             metrics_cap = v;
             ring.allocate(&rt, metrics_cap);
             ring.zero_async(rt.stream);

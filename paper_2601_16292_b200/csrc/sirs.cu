@@ -361,7 +361,7 @@ public:
         DevBuf<char> t;
         t.allocate(&rt, tmp + 16);
         AMBER_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, count, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
     }
 
     ~SirSpaceModel() override
@@ -442,7 +442,7 @@ public:
         copy_in(rt, tmp.p, src, n, on_dev);
         sirs_to_internal<<<rt.num_sms * 8, 256, 0, rt.stream>>>(tmp.p, sid.p, n, x[cur].p);
         check_launch("sirs_to_internal");
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
     }
 
     // the current state in id order (staging buffer)
@@ -464,7 +464,7 @@ public:
         else fail(AMBER_E_UNKNOWN_NAME, "no metric " + k);
         std::vector<SirsSlot> h(metrics_cap);
         AMBER_CUDA(cudaMemcpyAsync(h.data(), ring.p, metrics_cap * sizeof(SirsSlot), cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         const int64_t first = std::max(m_first, t - metrics_cap);
         const int64_t cnt = std::max<int64_t>(t - first, 0);
         if (bytes < static_cast<size_t>(cnt) * 8) fail(AMBER_E_BUFFER_TOO_SMALL, "metrics dst too small");
@@ -475,7 +475,7 @@ public:
 
     void reset_metrics() override
     {
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         m_first = t;
     }
 
@@ -488,7 +488,7 @@ public:
     void set_step(int64_t s) override
     {
         AMBER_REQUIRE(s >= 0 && s < (1ll << 32), "step out of range");
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         t = s;
         m_first = s;
     }

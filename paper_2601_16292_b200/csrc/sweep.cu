@@ -338,7 +338,7 @@ void run_sweep(int64_t n, const amber_sir_params& base, const amber_replicate* r
         check_launch("sweep_max_arcs_kernel");
         unsigned int h_max = 0;
         AMBER_CUDA(cudaMemcpyAsync(&h_max, d_max.p, 4, cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         const int64_t max_arcs = h_max;
         AMBER_CUDA(cudaEventRecord(e1, rt.stream));
         SweepArgs a{};
@@ -378,7 +378,7 @@ void run_sweep(int64_t n, const amber_sir_params& base, const amber_replicate* r
         AMBER_CUDA(cudaMemcpyAsync(local.data() + b0, d_out.p, B * 8, cudaMemcpyDeviceToHost, rt.stream));
         unsigned long long act = 0;
         AMBER_CUDA(cudaMemcpyAsync(&act, d_active.p, 8, cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         float f1 = 0, f2 = 0;
         AMBER_CUDA(cudaEventElapsedTime(&f1, e0, e1));
         AMBER_CUDA(cudaEventElapsedTime(&f2, e1, e2));
@@ -401,7 +401,7 @@ void run_sweep(int64_t n, const amber_sir_params& base, const amber_replicate* r
         comm_allgather_f64(c, rt.stream, d_loc.p, d_all.p, per);
         std::vector<double> all(per * W);
         AMBER_CUDA(cudaMemcpyAsync(all.data(), d_all.p, per * W * 8, cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         destroy_comm(c);
         for (int64_t k = 0; k < n_reps; ++k) out[k] = all[k];  // rank g's block starts at g*per
     } else {

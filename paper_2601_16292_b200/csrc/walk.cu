@@ -170,7 +170,7 @@ public:
         walk_init_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(key, n, n_pad, p.L, col[0].p, col[1].p, col[2].p,
                                                                col[3].p);
         check_launch("walk_init_kernel");
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
     }
 
     ~WalkModel() override
@@ -251,7 +251,7 @@ public:
         if (std::string(name) != "mean_displacement") fail(AMBER_E_UNKNOWN_NAME, std::string("no metric ") + name);
         std::vector<WalkSlot> h(metrics_cap);
         AMBER_CUDA(cudaMemcpyAsync(h.data(), ring.p, metrics_cap * sizeof(WalkSlot), cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         const int64_t first = std::max(m_first, t - metrics_cap + 1);
         const int64_t cnt = std::max<int64_t>(t - first, 0);
         if (bytes < static_cast<size_t>(cnt) * 8) fail(AMBER_E_BUFFER_TOO_SMALL, "metrics dst too small");
@@ -262,7 +262,7 @@ public:
 
     void reset_metrics() override
     {
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         m_first = t;
     }
 
@@ -276,7 +276,7 @@ public:
     void set_step(int64_t s) override
     {
         AMBER_REQUIRE(s >= 0 && s < (1ll << 32), "step out of range");
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         t = s;
         m_first = s;
     }

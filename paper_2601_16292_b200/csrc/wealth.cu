@@ -529,7 +529,7 @@ public:
             p2p_wanted = !(mode && std::string(mode) == "nccl");  // mapped at the first exchange (collective)
             recv_total.allocate(&rt, 1);
         }
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
     }
 
     // Bucket block [counts par 0 | counts par 1 | ids par 0 | ids par 1] mapped into
@@ -548,14 +548,14 @@ public:
             p2p_block = nullptr;
         }
         AMBER_CUDA(cudaMemsetAsync(p2p_block, 0, 2 * cbytes, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         std::vector<void*> peers;
         if (p2p_block && wealth_p2p_open(xch, rt, p2p_block, peers)) {
             std::vector<unsigned long long> h(peers.size());
             for (size_t k = 0; k < peers.size(); ++k) h[k] = reinterpret_cast<unsigned long long>(peers[k]);
             p2p_peers.allocate(&rt, h.size());
             AMBER_CUDA(cudaMemcpyAsync(p2p_peers.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, rt.stream));
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
             p2p = true;
         } else if (p2p_block) {
             cudaFree(p2p_block);
@@ -810,7 +810,7 @@ public:
                 }
             }
         }
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         h_lo = s0;
         h_hi = s1;
         return h_ring;
@@ -820,7 +820,7 @@ public:
     void verify()
     {
         if (win_start < 0) {
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
             return;
         }
         const Slot* h = fetch_slots(win_start, t);
@@ -858,7 +858,7 @@ public:
         pending = false;
         std::vector<Slot> h(metrics_cap);
         AMBER_CUDA(cudaMemcpyAsync(h.data(), ring.p, metrics_cap * sizeof(Slot), cudaMemcpyDeviceToHost, rt.stream));
-        AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+        rt.sync();
         for (int64_t s = s0; s < s1; ++s)
             if (h[s % metrics_cap].sent != h[s % metrics_cap].got)
                 fail(AMBER_E_CUDA, "wealth replay: increment count mismatch with 32-bit counters");
@@ -924,7 +924,7 @@ public:
             AMBER_CUDA(cudaMemcpyAsync(d.p, vals.data(), cnt * 8, cudaMemcpyHostToDevice, rt.stream));
             wealth_exchange_allreduce_u64(xch, rt, d.p, static_cast<int>(cnt));
             AMBER_CUDA(cudaMemcpyAsync(vals.data(), d.p, cnt * 8, cudaMemcpyDeviceToHost, rt.stream));
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
         }
         std::memcpy(dst, vals.data(), cnt * 8);
         if (n_out) *n_out = cnt;
@@ -947,7 +947,7 @@ public:
             AMBER_CUDA(cudaMemcpyAsync(b.p, &d, 8, cudaMemcpyHostToDevice, rt.stream));
             wealth_exchange_allreduce_u64(xch, rt, b.p, 1);
             AMBER_CUDA(cudaMemcpyAsync(&d, b.p, 8, cudaMemcpyDeviceToHost, rt.stream));
-            AMBER_CUDA(cudaStreamSynchronize(rt.stream));
+            rt.sync();
         }
         return d;
     }

@@ -65,7 +65,8 @@ class HostCollectives:
                 src = torch.from_numpy(np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(send)).copy())
                 outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(self.world)]
                 dist.all_gather(outs, src, group=group)
-                C.memmove(recv, torch.cat(outs).numpy().ctypes.data, nbytes * self.world)
+                buf = torch.cat(outs).numpy()  # keep alive across the copy
+                C.memmove(recv, buf.ctypes.data, nbytes * self.world)
                 return 0
             except Exception:  # reported by the library as AMBER_E_NCCL
                 return 1

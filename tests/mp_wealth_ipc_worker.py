@@ -33,8 +33,10 @@ def main():
     w = torch.from_numpy(m.read_column("wealth").astype(np.int32))
     sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
     dist.all_gather(sizes, torch.tensor([ln], dtype=torch.int64))
-    parts = [torch.zeros(int(s.item()), dtype=torch.int32) for s in sizes]
-    dist.all_gather(parts, w)
+    mx = max(int(s.item()) for s in sizes)  # gloo all_gather needs equal sizes: pad
+    parts = [torch.zeros(mx, dtype=torch.int32) for _ in sizes]
+    dist.all_gather(parts, torch.cat([w, torch.zeros(mx - ln, dtype=torch.int32)]))
+    parts = [p_[:int(s.item())] for p_, s in zip(parts, sizes)]
     tot, act, dig = m.metrics("total_wealth"), m.metrics("active"), m.metrics("digest")
     m.close()
     if rank == 0:

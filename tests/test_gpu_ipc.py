@@ -29,7 +29,8 @@ def test_two_process_ipc_exchange_bit_exact(tmp_path, n, steps, bits):
            "--master-addr=127.0.0.1", f"--master-port={free_port()}",
            os.path.join(ROOT, "tests", "mp_wealth_ipc_worker.py"), str(out), str(n), "77", str(steps), str(bits)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    errs = [ln for ln in (r.stdout + r.stderr).splitlines() if "AmberError" in ln or "Error:" in ln]
+    assert r.returncode == 0, "\n".join(errs[:10]) + "\n" + r.stderr[-2000:]
     res = json.load(open(out))
     assert res["exchange"] == 2, res  # the P2P (IPC-mapped) exchange ran
     assert res["column_equal"] and res["total_equal"] and res["active_equal"] and res["digest_equal"], res
