@@ -37,6 +37,11 @@ UNIT = "agent-updates/s"
 # random 32-bit L2 atomics, any target set that fits L2 (measured on this pool's B200,
 # tools/red_ceiling.cu -> profiles/r01_red_ceiling.txt): the scatter's binding roof
 RED_CEILING = 1.85e11
+# the fused roof of the C4 step: the same 800 MB column stream and 0.587*N random
+# REDs into 4-bit packed L2-resident counters in ONE kernel, with a hash in
+# place of Philox and no apply (tools/red_stream_ceiling.cu ->
+# profiles/r02_red_stream_ceiling.txt, best grid): ms per N = 1e8 step
+STREAM_RED_ROOF_MS = 0.3855
 # the Boids stencil's own instruction sequence over shared-memory-staged candidates
 # (memory latency hidden) at full residency, candidate visits per second
 # (tools/alu_ceiling.cu -> profiles/r02_alu_ceiling.txt): pre-quantised-velocity
@@ -628,6 +633,13 @@ def bench_wealth(args):
             "clocks": None,
             "host": {"cpu": model, "cpus": ncpu},
         }
+        line["stream_red_roof"] = {
+            "bound": "l2_red+hbm", "kernel": dom[0], "achieved_ms": dom_avg_ms,
+            "roof_ms": STREAM_RED_ROOF_MS * n_loc / 1e8, "frac": STREAM_RED_ROOF_MS * n_loc / 1e8 / dom_avg_ms
+            if dom_avg_ms > 0 else None,
+            "roof_source": "tools/red_stream_ceiling.cu (profiles/r02_red_stream_ceiling.txt): 800 MB column "
+                           "stream + 0.587 N random REDs into packed 4-bit counters in one kernel, hash instead "
+                           "of Philox, no apply -- the floor of any one-RED-per-transfer step"}
         if True:  # packed counters: one L2 RED per transfer
             line["l2_atomic_roof"] = {
                 "bound": "l2_atomics", "kernel": dom[0],
