@@ -412,14 +412,19 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
     // agents per round): consecutive rounds slide along the same cell rows, so
     // the stencil's rows stay in this SM's L1 instead of being fetched by a
     // different SM every round
+    // (large populations only: at C3's 1e5 agents -- two rounds per block -- the
+    // grid-strided order measured faster, 54 vs 58 us)
     const int64_t apb = blockDim.x / G;  // agents per block per round
     const int64_t ng = apb * gridDim.x;
     const int64_t rounds = (n + ng - 1) / ng;  // uniform: every lane runs every round (shuffles)
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * rounds * apb + threadIdx.x / G;
+    const bool contig = n > (1ll << 22);
+    const int64_t base = contig ? static_cast<int64_t>(blockIdx.x) * rounds * apb + threadIdx.x / G
+                                : static_cast<int64_t>(blockIdx.x) * apb + threadIdx.x / G;
+    const int64_t rstride = contig ? apb : ng;
     double sp_sum = 0.0, ux_sum = 0.0, uy_sum = 0.0;
     unsigned long long dig = 0;
     for (int64_t r = 0; r < rounds; ++r) {
-        const int64_t p = base + r * apb;
+        const int64_t p = base + r * rstride;
         const bool active = p < n;
         Acc acc{0, 0, 0, 0, 0, 0, 0};
         float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
