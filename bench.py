@@ -155,7 +155,7 @@ def run_reference_small(args, oracle, np):
                              c["n"] * c["steps"], f"wealth N={c['n']} x {c['steps']} steps (the whole config)")
     elif w == "c2":
         c = W.C2_SIR
-        m_draws, k_inf = W.sir_counts(c)
+        m_draws, k_inf = oracle.round_count(c["n"] * c["mean_degree"] / 2.0), oracle.round_count(c["init_frac"] * c["n"])
         rp, col, _ = oracle.er_graph(c["n"], m_draws, c["seed"])
         st = oracle.sir_init(c["n"], k_inf, c["seed"])
         fn, units, sample = (lambda: oracle.sir_run(rp, col, st, c["seed"], c["beta"], c["gamma"], 0, c["steps"]),

@@ -90,12 +90,52 @@ class PopulationRef:
         assert len(st) == 1
         return st[0]
 
+    def eval_tree(self, t):
+        """The plain definition of an expression given as a tuple tree,
+        independent of the product's Expr lowering: ("col", name), ("const", v),
+        ("id",), ("step",), ("rand", tag), (unary, a) for neg / abs / floor /
+        sqrt / not, ("select", c, a, b), (binary, a, b) for add / sub / mul / div
+        / min / max / lt / le / gt / ge / eq / ne / and / or -- every value a
+        float64 column, comparisons 1.0 / 0.0, min / max ignoring NaN (fmin /
+        fmax), as SPEC's float64 evaluation."""
+        n = self.ids.size
+        k = t[0]
+        if k == "col":
+            return self.cols[t[1]].astype(np.float64)
+        if k == "const":
+            return np.full(n, float(t[1]))
+        if k == "id":
+            return self.ids.astype(np.float64)
+        if k == "step":
+            return np.full(n, float(self.step))
+        if k == "rand":
+            return np.array([((lane32(self.seed, t[1], int(i), self.step) >> 8) * 2.0 ** -24) for i in self.ids],
+                            np.float64)
+        with np.errstate(all="ignore"):
+            if k == "select":
+                c, a, b = (self.eval_tree(x) for x in t[1:])
+                return np.where(c != 0, a, b)
+            if len(t) == 2:
+                a = self.eval_tree(t[1])
+                return {"neg": lambda x: -x, "abs": np.abs, "floor": np.floor, "sqrt": np.sqrt,
+                        "not": lambda x: (x == 0).astype(np.float64)}[k](a)
+            a, b = self.eval_tree(t[1]), self.eval_tree(t[2])
+            f = {"add": np.add, "sub": np.subtract, "mul": np.multiply, "div": np.divide, "min": np.fmin,
+                 "max": np.fmax, "lt": np.less, "le": np.less_equal, "gt": np.greater, "ge": np.greater_equal,
+                 "eq": np.equal, "ne": np.not_equal, "and": lambda x, y: (x != 0) & (y != 0),
+                 "or": lambda x, y: (x != 0) | (y != 0)}[k]
+            return np.asarray(f(a, b), np.float64)
+
+    def _value(self, e):
+        return self.eval_tree(e) if isinstance(e, tuple) else self.eval(e)
+
     def update(self, target, prog, where=None):
+        """prog / where: a postfix program (list) or an expression tree (tuple)."""
         sel = self.alive.copy()
         if where:
-            sel &= self.eval(where) != 0
+            sel &= self._value(where) != 0
         with np.errstate(all="ignore"):
-            v = self.eval(prog)
+            v = self._value(prog)
         self.cols[target] = self.cols[target].copy()
         self.cols[target][sel] = v[sel].astype(self.dt[target])
         return int(sel.sum())
@@ -103,10 +143,10 @@ class PopulationRef:
     def aggregate(self, kind, prog=None, where=None):
         sel = self.alive.copy()
         if where:
-            sel &= self.eval(where) != 0
+            sel &= self._value(where) != 0
         if kind == "count":
             return float(sel.sum())
-        v = self.eval(prog)[sel]
+        v = self._value(prog)[sel]
         if kind == "sum":
             return float(v.sum())
         if v.size == 0:

@@ -66,11 +66,3 @@ def sweep_replicates(cfg=C5_SWEEP):
     betas = np.repeat(betas_grid, cfg["n_seed"]).astype(np.float64)
     seeds = np.arange(cfg["n_beta"] * cfg["n_seed"], dtype=np.uint64)
     return betas, seeds
-
-
-def sir_counts(cfg):
-    """G1/S1 integer sizes: M = round(N*kbar/2), K = round(init_frac*N) (round half up)."""
-    n = cfg["n"]
-    m = int(np.floor(n * cfg["mean_degree"] / 2.0 + 0.5))
-    k = int(np.floor(cfg["init_frac"] * n + 0.5))
-    return m, k

@@ -41,23 +41,43 @@ def test_spec_examples():
         q.aggregate("mean", col("w"))
 
 
-def random_expr(rng, depth=3):
+def random_tree(rng, depth=3):
+    """A random expression as a plain tuple tree: the reference evaluates the
+    tree itself (PopulationRef.eval_tree), the device gets it through the
+    product's Expr API (to_expr), so a lowering bug cannot hide on both sides."""
     if depth == 0 or rng.random() < 0.25:
         k = rng.integers(0, 4)
         if k == 0:
-            return col(list(SCHEMA)[rng.integers(0, 5)])
+            return ("col", list(SCHEMA)[rng.integers(0, 5)])
         if k == 1:
-            return float(rng.integers(-5, 6)) / 2
-        if k == 2:
-            return agent_id()
-        return step_index()
-    a, b = random_expr(rng, depth - 1), random_expr(rng, depth - 1)
-    from paper_2601_16292_b200.population import Expr
-    a = Expr.of(a)
+            return ("const", float(rng.integers(-5, 6)) / 2)
+        return ("id",) if k == 2 else ("step",)
+    a, b = random_tree(rng, depth - 1), random_tree(rng, depth - 1)
     op = rng.integers(0, 12)
-    return [lambda: a + b, lambda: a - b, lambda: a * b, lambda: a.min(b), lambda: a.max(b),
-            lambda: a < b, lambda: a >= b, lambda: a == b, lambda: (a > b).where(a, b),
-            lambda: a.abs(), lambda: a.floor(), lambda: a / (Expr.of(b).abs() + 1)][op]()
+    return [("add", a, b), ("sub", a, b), ("mul", a, b), ("min", a, b), ("max", a, b), ("lt", a, b), ("ge", a, b),
+            ("eq", a, b), ("select", ("gt", a, b), a, b), ("abs", a), ("floor", a),
+            ("div", a, ("add", ("abs", b), ("const", 1.0)))][op]
+
+
+def to_expr(t):
+    from paper_2601_16292_b200.population import Expr
+    k = t[0]
+    if k == "col":
+        return col(t[1])
+    if k == "const":
+        return Expr.of(t[1])
+    if k == "id":
+        return agent_id()
+    if k == "step":
+        return step_index()
+    if k == "select":
+        return to_expr(t[1]).where(to_expr(t[2]), to_expr(t[3]))
+    if k in ("abs", "floor"):
+        return getattr(to_expr(t[1]), k)()
+    a, b = to_expr(t[1]), to_expr(t[2])
+    return {"add": lambda: a + b, "sub": lambda: a - b, "mul": lambda: a * b, "div": lambda: a / b,
+            "min": lambda: a.min(b), "max": lambda: a.max(b), "lt": lambda: a < b, "ge": lambda: a >= b,
+            "eq": lambda: a == b, "gt": lambda: a > b, "ne": lambda: a != b}[k]()
 
 
 @pytest.mark.parametrize("jit", ["1", "0"])
@@ -81,23 +101,21 @@ def test_random_programs_match_reference(seed, jit, monkeypatch):
     r.remove_agents(dead.tolist())
     for it in range(12):
         tgt = list(SCHEMA)[rng.integers(0, 5)]
-        e = random_expr(rng)
-        e = e if not isinstance(e, float) else col("y") + e
-        w = (col("s") != 1) if it % 3 else None
+        t = random_tree(rng)
+        w = ("ne", ("col", "s"), ("const", 1.0)) if it % 3 else None
         if tgt in ("a", "b", "s"):  # keep integer targets in range (C conversion semantics)
-            e = col("y").abs().min(100.0) if tgt == "s" else (e if isinstance(e, float) else e).max(-1e6).min(1e6)
-        from paper_2601_16292_b200.population import Expr
-        e = Expr.of(e)
+            t = (("min", ("abs", ("col", "y")), ("const", 100.0)) if tgt == "s"
+                 else ("min", ("max", t, ("const", -1e6)), ("const", 1e6)))
         p.set_step(it)
         r.step = it
-        n1 = p.update(tgt, e, where=w)
-        n2 = r.update(tgt, e.prog, w.prog if w is not None else None)
+        n1 = p.update(tgt, to_expr(t), where=to_expr(w) if w else None)
+        n2 = r.update(tgt, t, w)
         assert n1 == n2
         for k in SCHEMA:
             assert np.array_equal(p.column(k), r.column(k), equal_nan=True), (it, k)
         for kind in ("sum", "min", "max", "count"):
             try:
-                h = r.aggregate(kind, col("y").prog, (col("a") > 0).prog)
+                h = r.aggregate(kind, ("col", "y"), ("gt", ("col", "a"), ("const", 0.0)))
             except ValueError:  # empty selection: the device must refuse too
                 with pytest.raises(Exception):
                     p.aggregate(kind, col("y"), where=col("a") > 0)
@@ -129,8 +147,11 @@ def test_fast_binop_path_matches_reference(op):
     r.remove_agents(dead.tolist())
     f = {"+": lambda a, b: a + b, "-": lambda a, b: a - b, "*": lambda a, b: a * b, "/": lambda a, b: a / b,
          "min": lambda a, b: a.min(b), "max": lambda a, b: a.max(b)}[op]
-    for tgt, e in (("x", f(col("x"), 2.5)), ("y", f(col("y"), col("x"))), ("a", f(col("a"), 3.0))):
-        assert p.update(tgt, e) == r.update(tgt, e.prog)
+    tree = {"+": "add", "-": "sub", "*": "mul", "/": "div", "min": "min", "max": "max"}[op]
+    for tgt, e, t in (("x", f(col("x"), 2.5), (tree, ("col", "x"), ("const", 2.5))),
+                      ("y", f(col("y"), col("x")), (tree, ("col", "y"), ("col", "x"))),
+                      ("a", f(col("a"), 3.0), (tree, ("col", "a"), ("const", 3.0)))):
+        assert p.update(tgt, e) == r.update(tgt, t)
         assert np.array_equal(p.column(tgt), r.column(tgt))
 
 
@@ -141,7 +162,7 @@ def test_rand_is_counter_based(orc):
     p.set_step(5)
     r.step = 5
     p.update("u", rand(0x50))
-    r.update("u", rand(0x50).prog)
+    r.update("u", ("rand", 0x50))
     assert np.array_equal(p.column("u"), r.column("u"))
     assert 0.45 < p.aggregate("mean", col("u")) < 0.55
 

@@ -5,13 +5,30 @@ import numpy as np
 import pytest
 
 from oracle.population import PopulationRef
-from paper_2601_16292_b200.population import col
+
+
+# expressions as plain tuple trees (oracle.population.eval_tree): the pins do
+# not go through the product's Expr lowering
+def col(name):
+    return ("col", name)
+
+
+def add(a, v):
+    return ("add", a, ("const", v))
+
+
+def sub(a, v):
+    return ("sub", a, ("const", v))
+
+
+def cmp(op, a, v):
+    return (op, a, ("const", v))
 
 
 def test_listing1_increment():
     p = PopulationRef({"wealth": "i64"})
     assert p.add_agents(3, wealth=1).tolist() == [0, 1, 2]  # SPEC add_agents example
-    p.update("wealth", (col("wealth") + 10).prog)  # PAPER.md Listing 1
+    p.update("wealth", add(col("wealth"), 10))  # PAPER.md Listing 1
     assert p.column("wealth").tolist() == [11, 11, 11]
 
 
@@ -19,16 +36,16 @@ def test_update_where_example():
     p = PopulationRef({"wealth": "i64"})
     p.add_agents(3)
     p.cols["wealth"][:] = [0, 5, 9]
-    n = p.update("wealth", (col("wealth") - 5).prog, (col("wealth") >= 5).prog)
+    n = p.update("wealth", sub(col("wealth"), 5), cmp("ge", col("wealth"), 5))
     assert p.column("wealth").tolist() == [0, 0, 4] and n == 2
-    assert p.update("wealth", (col("wealth") + 1).prog, (col("wealth") > 100).prog) == 0
+    assert p.update("wealth", add(col("wealth"), 1), cmp("gt", col("wealth"), 100)) == 0
 
 
 def test_aggregate_examples():
     p = PopulationRef({"wealth": "i64"})
     p.add_agents(3)
     p.cols["wealth"][:] = [1, 2, 3]
-    w = col("wealth").prog
+    w = col("wealth")
     assert (p.aggregate("sum", w), p.aggregate("mean", w), p.aggregate("min", w), p.aggregate("max", w)) == \
         (6, 2.0, 1, 3)
     p.remove_agents([1])
@@ -38,9 +55,9 @@ def test_aggregate_examples():
     q.remove_agents([0, 3])
     assert q.aggregate("count") == 3
     q.remove_agents([1, 2, 4])
-    assert q.aggregate("sum", col("x").prog) == 0.0
+    assert q.aggregate("sum", col("x")) == 0.0
     with pytest.raises(ValueError):
-        q.aggregate("mean", col("x").prog)
+        q.aggregate("mean", col("x"))
 
 
 def test_ids_never_reused_and_compact():
@@ -69,7 +86,7 @@ def test_batch_atomic_last_wins():
 def test_dtype_conversion_rules():
     p = PopulationRef({"i": "i32", "f": "f32"})
     p.add_agents(2)
-    p.update("i", (col("i") - 2.7).prog)  # truncation toward zero
-    p.update("f", (col("f") + 0.1).prog)  # round to nearest float32
+    p.update("i", sub(col("i"), 2.7))  # truncation toward zero
+    p.update("f", add(col("f"), 0.1))  # round to nearest float32
     assert p.column("i").tolist() == [-2, -2]
     assert p.column("f")[0] == np.float32(0.1)

@@ -11,7 +11,7 @@ import scipy.sparse as sp
 from scipy.sparse.csgraph import breadth_first_order, shortest_path
 
 from conftest import mulhi64_bigint
-from paper_2601_16292_b200.workloads import C2_SIR, C5_SWEEP, sir_counts, sweep_replicates
+from paper_2601_16292_b200.workloads import C2_SIR, C5_SWEEP, sweep_replicates
 
 TAG_GRAPH, TAG_INIT, TAG_TX, TAG_REC = 0x13, 0x12, 0x10, 0x11
 
@@ -56,7 +56,7 @@ def test_graph_invariants(orc):
 
 def test_graph_duplicate_count_sanity(orc):
     # G4 sanity: expected duplicates M(M-1)/(N(N-1)) ~ 25 for C2
-    m, _ = sir_counts(C2_SIR)
+    m = orc.round_count(C2_SIR["n"] * C2_SIR["mean_degree"] / 2.0)
     _, _, mu = orc.er_graph(C2_SIR["n"], m, C2_SIR["seed"])
     dup = m - mu
     assert 5 < dup < 60
