@@ -44,15 +44,29 @@ constexpr float kFix = 16777216.0f;  // 2^24 (B3)
 
 struct BoidsArgs {
     float L, R, rs, wc, wa, ws, vmax, dt;
-    int nc;       // cells per side
+    int nc;       // cells per side (y; and x for the sharded slabs)
     float inv_cs; // nc / L
     int span = 1; // stencil half-width in cells: 1 (cells >= R) or 2 (cells >= R/2)
+    // one-GPU grid: rows of nc cells of height cs >= R in y, each split into
+    // ncx = sx * nc columns of width cs / sx in x; the stencil of an agent in
+    // column hx covers columns hx - sx .. hx + sx of three rows (one contiguous
+    // run per row, (2 + 1/sx) cs wide instead of 3 cs)
+    int ncx = 0;
+    float inv_csx = 0.f;  // ncx / L
+    int sx = 1;
 };
 
 __device__ __forceinline__ int cell_coord(float x, const BoidsArgs& a)
 {
     int c = static_cast<int>(__fmul_rn(x, a.inv_cs));
     return c < 0 ? 0 : (c >= a.nc ? a.nc - 1 : c);
+}
+
+// x column of the one-GPU grid (width cs / sx)
+__device__ __forceinline__ int cell_x(float x, const BoidsArgs& a)
+{
+    int c = static_cast<int>(__fmul_rn(x, a.inv_csx));
+    return c < 0 ? 0 : (c >= a.ncx ? a.ncx - 1 : c);
 }
 
 // B1: initial positions and rejection-sampled unit velocities (id order).
@@ -115,7 +129,7 @@ __global__ void boids_count_kernel(const float4* __restrict__ st, int64_t n, Boi
         int c = -1;
         if (p < n) {
             const float4 s = st[p];
-            c = cell_coord(s.y, a) * a.nc + cell_coord(s.x, a);
+            c = cell_coord(s.y, a) * a.ncx + cell_x(s.x, a);
             cell_of[p] = c;
         }
         int head, rank, len;
@@ -183,11 +197,11 @@ __global__ void __launch_bounds__(1024) boids_scan_kernel(const int* __restrict_
 }
 
 // Exclusive scan of the ncell + 1 counts for large grids (> 2^16 cells), by
-// hand in two launches (no library scan on the step path): (1) each 1024-thread
-// block sums a chunk of kScanChunk cells; (2) each block adds the totals of the
-// chunks before it (L2-resident, ~2.4K of them at V3's 10^7 cells), scans its
-// chunk (four cells per thread, warp shuffles + one shared-memory pass over the
-// 32 warp totals), writes start / cursor and re-zeroes the counts.
+// hand in three launches (no library scan on the step path): (1) each
+// 1024-thread block sums a chunk of kScanChunk cells; (1b) one CTA scans the
+// chunk totals into offsets; (2) each block scans its chunk from its offset
+// (four cells per thread, warp shuffles + one shared-memory pass over the 32
+// warp totals), writes start / cursor and re-zeroes the counts.
 constexpr int kScanChunk = 4096;
 
 __device__ __forceinline__ int block_sum_1024(int v, int* red)
@@ -207,29 +221,75 @@ __global__ void __launch_bounds__(1024) boids_chunk_sums_kernel(const int* __res
     __shared__ int red[32];
     const int c0 = blockIdx.x * kScanChunk + threadIdx.x * 4;
     int s = 0;
+    if (c0 + 4 <= ncell1) {  // one 16-byte load (cnt is 256-byte aligned, c0 a multiple of 4)
+        const int4 v = *reinterpret_cast<const int4*>(cnt + c0);
+        s = v.x + v.y + v.z + v.w;
+    } else {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) s += c0 + k < ncell1 ? cnt[c0 + k] : 0;
+        for (int k = 0; k < 4; ++k) s += c0 + k < ncell1 ? cnt[c0 + k] : 0;
+    }
     s = block_sum_1024(s, red);
     if (threadIdx.x == 0) sums[blockIdx.x] = s;
 }
 
-__global__ void __launch_bounds__(1024) boids_chunk_scan_kernel(int* __restrict__ cnt, const int* __restrict__ sums,
+// (1b) one CTA turns the chunk totals into exclusive chunk offsets, in place
+// (1024 totals per pass: warp shuffles + the 32 warp totals + a running carry)
+__global__ void __launch_bounds__(1024) boids_chunk_offsets_kernel(int* __restrict__ sums, int nch)
+{
+    __shared__ int wex[32];
+    __shared__ int carry_s;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    for (int base = 0; base < nch; base += 1024) {
+        const int c = base + threadIdx.x;
+        const int v = c < nch ? sums[c] : 0;
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        if (lane == 31) wex[w] = incl;
+        __syncthreads();
+        if (w == 0) {
+            const int x = wex[lane];
+            int xi = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, xi, o);
+                if (lane >= o) xi += u;
+            }
+            wex[lane] = xi - x;
+        }
+        __syncthreads();
+        const int carry = carry_s;
+        if (c < nch) sums[c] = carry + wex[w] + incl - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry_s = carry + wex[31] + incl;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(1024) boids_chunk_scan_kernel(int* __restrict__ cnt, const int* __restrict__ offs,
                                                                 int ncell, int* __restrict__ start,
                                                                 int* __restrict__ cursor)
 {
-    __shared__ int red[32], wex[32];
-    int pre = 0;
-    for (int j = threadIdx.x; j < static_cast<int>(blockIdx.x); j += 1024) pre += sums[j];
-    pre = block_sum_1024(pre, red);
-    if (threadIdx.x == 0) red[0] = pre;
-    __syncthreads();
-    const int carry = red[0];
+    __shared__ int wex[32];
+    const int carry = offs[blockIdx.x];
     const int c0 = blockIdx.x * kScanChunk + threadIdx.x * 4;
     int v[4], tsum = 0;
+    const bool full = c0 + 4 <= ncell;  // all four cells real (and not the terminal entry)
+    if (full) {
+        const int4 q = *reinterpret_cast<const int4*>(cnt + c0);
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+        tsum = q.x + q.y + q.z + q.w;
+    } else {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        v[k] = c0 + k <= ncell ? cnt[c0 + k] : 0;
-        tsum += v[k];
+        for (int k = 0; k < 4; ++k) {
+            v[k] = c0 + k <= ncell ? cnt[c0 + k] : 0;
+            tsum += v[k];
+        }
     }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int incl = tsum;
@@ -252,6 +312,13 @@ __global__ void __launch_bounds__(1024) boids_chunk_scan_kernel(int* __restrict_
     }
     __syncthreads();
     int run = carry + wex[w] + incl - tsum;
+    if (full) {  // 16-byte stores
+        const int4 o = make_int4(run, run + v[0], run + v[0] + v[1], run + v[0] + v[1] + v[2]);
+        *reinterpret_cast<int4*>(start + c0) = o;
+        *reinterpret_cast<int4*>(cursor + c0) = o;
+        *reinterpret_cast<int4*>(cnt + c0) = make_int4(0, 0, 0, 0);
+        return;  // (the terminal entry start[ncell] belongs to a partial quad)
+    }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int c = c0 + k;
@@ -464,30 +531,30 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
                 }
                 if (q < e) boid_accumulate<false, QV>(sorted[q], me, L, halfL, R2, rs2, acc);
             };
-            const int sp = a.span;
-            const int cx0 = a.nc >= 3 ? cell_coord(me.x, a) : 0, cy0 = a.nc >= 3 ? cell_coord(me.y, a) : 0;
-            // interior: the whole stencil inside the box and (sp + 1) cells <= L/2
-            if (a.nc >= 2 * sp + 3 && cx0 >= sp && cx0 + sp < a.nc && cy0 >= sp && cy0 + sp < a.nc) {
+            const int sx = a.sx, ncx = a.ncx;
+            const int cx0 = a.nc >= 3 ? cell_x(me.x, a) : 0, cy0 = a.nc >= 3 ? cell_coord(me.y, a) : 0;
+            // interior: the whole stencil inside the box and within 2 cells < L/2 (nc >= 5)
+            if (a.nc >= 5 && cx0 >= sx && cx0 + sx < ncx && cy0 >= 1 && cy0 + 1 < a.nc) {
 #pragma unroll 1
-                for (int dyc = -sp; dyc <= sp; ++dyc) {
-                    const int row = (cy0 + dyc) * a.nc;
-                    run_in(start[row + cx0 - sp], start[row + cx0 + sp + 1]);
+                for (int dyc = -1; dyc <= 1; ++dyc) {
+                    const int row = (cy0 + dyc) * ncx;
+                    run_in(start[row + cx0 - sx], start[row + cx0 + sx + 1]);
                 }
             } else if (a.nc >= 3) {
                 const int cx = cx0, cy = cy0;
 #pragma unroll 1
-                for (int dyc = -sp; dyc <= sp; ++dyc) {
+                for (int dyc = -1; dyc <= 1; ++dyc) {
                     int yy = cy + dyc;
                     yy = yy < 0 ? yy + a.nc : (yy >= a.nc ? yy - a.nc : yy);
-                    const int row = yy * a.nc;
-                    if (cx >= sp && cx + sp < a.nc) {
-                        // cells cx-sp .. cx+sp of a row are contiguous in the sorted array
-                        run(start[row + cx - sp], start[row + cx + sp + 1]);
+                    const int row = yy * ncx;
+                    if (cx >= sx && cx + sx < ncx) {
+                        // columns cx-sx .. cx+sx of a row are contiguous in the sorted array
+                        run(start[row + cx - sx], start[row + cx + sx + 1]);
                     } else {
 #pragma unroll 1
-                        for (int dxc = -sp; dxc <= sp; ++dxc) {
+                        for (int dxc = -sx; dxc <= sx; ++dxc) {
                             int xx = cx + dxc;
-                            xx = xx < 0 ? xx + a.nc : (xx >= a.nc ? xx - a.nc : xx);
+                            xx = xx < 0 ? xx + ncx : (xx >= ncx ? xx - ncx : xx);
                             run(start[row + xx], start[row + xx + 1]);
                         }
                     }
@@ -530,7 +597,7 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
                 out_ids[p] = id;
                 if (digest) dig += digest_term(static_cast<unsigned long long>(id), __float_as_uint(nx.x));
                 if (next_cnt) {
-                    ncell_of = cell_coord(nx.y, a) * a.nc + cell_coord(nx.x, a);
+                    ncell_of = cell_coord(nx.y, a) * a.ncx + cell_x(nx.x, a);
                     next_cell[p] = ncell_of;
                 }
             }
@@ -606,19 +673,20 @@ __global__ void __launch_bounds__(256, MINB) boids_group_kernel(const float4* __
 // Candidate visits of one stencil pass over the current binning (the 3x3 cell
 // neighbourhood's agent count, summed over the agents; the roofline's unit of
 // work): sum over cells c of count(c) * sum of the counts of c's 3x3 stencil.
-__global__ void boids_candidates_kernel(const int* __restrict__ start, int nc, unsigned long long* out)
+__global__ void boids_candidates_kernel(const int* __restrict__ start, int nc, int ncx, int sx,
+                                        unsigned long long* out)
 {
     unsigned long long s = 0;
-    const int64_t ncell = static_cast<int64_t>(nc) * nc;
+    const int64_t ncell = static_cast<int64_t>(nc) * ncx;
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncell; c += (int64_t)gridDim.x * blockDim.x) {
-        const int cx = static_cast<int>(c % nc), cy = static_cast<int>(c / nc);
+        const int cx = static_cast<int>(c % ncx), cy = static_cast<int>(c / ncx);
         const long long own = start[c + 1] - start[c];
         if (!own) continue;
         long long nb = 0;
         for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int x = (cx + dx + nc) % nc, y = (cy + dy + nc) % nc;
-                const int64_t k = static_cast<int64_t>(y) * nc + x;
+            for (int dx = -sx; dx <= sx; ++dx) {
+                const int x = (cx + dx + ncx) % ncx, y = (cy + dy + nc) % nc;
+                const int64_t k = static_cast<int64_t>(y) * ncx + x;
                 nb += start[k + 1] - start[k];
             }
         s += static_cast<unsigned long long>(own * nb);
@@ -995,7 +1063,17 @@ public:
         ba.nc = static_cast<int>(nc1 >= 3 ? nc1 : 1);
         ba.span = 1;
         ba.inv_cs = static_cast<float>(ba.nc / static_cast<double>(p.L));
-        ncell = ba.nc * ba.nc;
+        // x columns of width cs / sx (AMBER_BOIDS_SX): the stencil row runs shrink
+        // from 3 cs to (2 + 1/sx) cs -- 25% fewer candidates at sx 4
+        // (measured, tools/boids_qv_probe.py: V3 stencil 17.3 -> 15.4 ms at sx 4; C3,
+        // whose small grid is L1-resident, gains nothing and keeps sx 1)
+        const char* sxe = getenv("AMBER_BOIDS_SX");
+        const int sx_default = n > (1ll << 22) ? 4 : 1;
+        ba.sx = ba.nc >= 3 ? std::max(1, std::min(16, sxe && *sxe ? std::atoi(sxe) : sx_default)) : 1;
+        while (ba.sx > 1 && static_cast<int64_t>(ba.nc) * ba.nc * ba.sx > (1ll << 30)) --ba.sx;
+        ba.ncx = ba.nc * ba.sx;
+        ba.inv_csx = static_cast<float>(ba.ncx / static_cast<double>(p.L));
+        ncell = ba.nc * ba.ncx;
         st.allocate(&rt, n);
         sorted.allocate(&rt, n);
         ids.allocate(&rt, n);
@@ -1074,6 +1152,8 @@ public:
                         const int nch = static_cast<int>(ceil_div(ncell + 1, kScanChunk));
                         boids_chunk_sums_kernel<<<nch, 1024, 0, rt.stream>>>(cnt.p, ncell + 1, chunk_sums.p);
                         check_launch("boids_chunk_sums_kernel");
+                        boids_chunk_offsets_kernel<<<1, 1024, 0, rt.stream>>>(chunk_sums.p, nch);
+                        check_launch("boids_chunk_offsets_kernel");
                         boids_chunk_scan_kernel<<<nch, 1024, 0, rt.stream>>>(cnt.p, chunk_sums.p, ncell, start.p,
                                                                               cursor.p);
                     }
@@ -1262,6 +1342,10 @@ public:
             *v = ba.nc;
             return true;
         }
+        if (std::string(key) == "x_subdivision") {  // columns per cell width in x
+            *v = ba.sx;
+            return true;
+        }
         if (std::string(key) == "lanes") {
             *v = lanes;
             return true;
@@ -1271,7 +1355,7 @@ public:
             DevBuf<unsigned long long> d;
             d.allocate(&rt, 1);
             d.zero_async(rt.stream);
-            boids_candidates_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(start.p, ba.nc, d.p);
+            boids_candidates_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(start.p, ba.nc, ba.ncx, ba.sx, d.p);
             check_launch("boids_candidates_kernel");
             unsigned long long h = 0;
             AMBER_CUDA(cudaMemcpyAsync(&h, d.p, 8, cudaMemcpyDeviceToHost, rt.stream));
@@ -1324,6 +1408,9 @@ public:
         AMBER_REQUIRE(nc >= 3 && nc >= rt.world, "sharded Boids needs >= 3 cells per side and >= 1 cell column per rank");
         ba.nc = static_cast<int>(nc);
         ba.inv_cs = static_cast<float>(ba.nc / static_cast<double>(p.L));
+        ba.ncx = ba.nc;  // the slabs keep square cells (column-major local grid)
+        ba.inv_csx = ba.inv_cs;
+        ba.sx = 1;
         col0.resize(rt.world + 1);
         for (int q = 0; q <= rt.world; ++q) col0[q] = static_cast<int>(static_cast<int64_t>(q) * ba.nc / rt.world);
         c_lo = col0[rt.rank];
@@ -1429,6 +1516,8 @@ public:
                 boids_chunk_sums_kernel<<<nch, 1024, 0, rt.stream>>>(cnt.p, static_cast<int>(ncell_loc + 1),
                                                                       chunk_sums.p);
                 check_launch("boids_chunk_sums_kernel");
+                boids_chunk_offsets_kernel<<<1, 1024, 0, rt.stream>>>(chunk_sums.p, nch);
+                check_launch("boids_chunk_offsets_kernel");
                 boids_chunk_scan_kernel<<<nch, 1024, 0, rt.stream>>>(cnt.p, chunk_sums.p, static_cast<int>(ncell_loc),
                                                                       start.p, cursor.p);
                 check_launch("boids_chunk_scan_kernel");

@@ -157,10 +157,13 @@ def test_tiny_populations(orc, n):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
 
 
-def test_large_grid_device_scan_and_edges(orc):
-    # > 2^16 cells: the device-wide cell scan; sparse agents, so most stencils touch
-    # the box edges' wrapped rows/columns as well as interior runs
-    cfg = dict(C3_BOIDS, n=30_000, L=3000.0, seed=17)
+@pytest.mark.parametrize("L,sx", [(3000.0, "1"), (30_000.0, "1"), (3000.0, "4")])
+def test_large_grid_device_scan_and_edges(orc, monkeypatch, L, sx):
+    # > 2^16 cells: the hand-written chunked cell scan (at L = 30,000: 9e6 cells,
+    # > 1,024 chunks, so the chunk-offset pass loops); sparse agents, so most
+    # stencils touch the box edges' wrapped rows/columns as well as interior runs
+    monkeypatch.setenv("AMBER_BOIDS_SX", sx)
+    cfg = dict(C3_BOIDS, n=30_000, L=L, seed=17)
     m = make(cfg)
     assert m.get_option("cells_per_side") ** 2 > (1 << 16)
     st = oinit(orc, cfg, m)
@@ -230,3 +233,21 @@ def test_quantised_velocity_stencil_paths(orc):
     # vmax >= 64: velocities may leave the QV range, the float stencil always runs
     d = make(dict(cfg, vmax=80.0, L=2000.0))
     assert d.get_option("qv") == 0
+
+
+@pytest.mark.parametrize("sx", ["1", "2", "3", "4", "8"])
+def test_x_subdivided_cells(orc, monkeypatch, sx):
+    # rows of R-high cells split into sx columns in x (stencil runs (2 + 1/sx) cs
+    # wide): the same bits for every sx, and the oracle's, incl. the wrapped edges
+    monkeypatch.setenv("AMBER_BOIDS_SX", sx)
+    for kw in (dict(n=20_000, L=450.0), dict(n=6000, L=100.0, rs=0.5, wc=0.5, wa=0.5, ws=0.0), dict(n=3000, L=50.0)):
+        cfg = dict(C3_BOIDS, seed=21, **kw)
+        m = make(cfg)
+        assert m.get_option("x_subdivision") == int(sx)
+        st = oinit(orc, cfg, m)
+        m.step(8)
+        P = oparams(orc, cfg)
+        for _ in range(8):
+            st = orc.boids_step(st, P)
+        for x, z in zip(state(m), st):
+            assert np.array_equal(x.view(np.uint32), z.view(np.uint32))

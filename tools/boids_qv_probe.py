@@ -34,6 +34,6 @@ for name, c, steps in (("c3", W.C3_BOIDS, 100), ("v3", W.V3_BOIDS_SCALE, 10)):
             m.step(2)
             m.synchronize()
             prof = {k: round(t / n, 4) for k, n, t in m.profile_results()}
-            print(json.dumps({"lib": os.environ.get("AMBER_LIB_PATH", "default"), "config": name, "qv": qv, "lanes": lanes, "ms_per_step": round(ms, 4),
+            print(json.dumps({"lib": os.environ.get("AMBER_LIB_PATH", "default"), "sx": m.get_option("x_subdivision"), "config": name, "qv": qv, "lanes": lanes, "ms_per_step": round(ms, 4),
                               "kernel_ms": prof}), flush=True)
             m.close()
