@@ -251,3 +251,33 @@ def test_x_subdivided_cells(orc, monkeypatch, sx):
             st = orc.boids_step(st, P)
         for x, z in zip(state(m), st):
             assert np.array_equal(x.view(np.uint32), z.view(np.uint32))
+
+
+def test_v3_full_size_region_vs_oracle(orc):
+    # the SURVEY 8(d) variant V3 at its full size (N = 1e8, L = 31,623) in the
+    # bench's launch configuration (QV records, x-subdivided rows, 40-register
+    # stencil): the oracle builds the whole initial population itself (B1),
+    # the device's must equal it; then 3 steps of the oracle on the agents of a
+    # 304 x 304 window around (10000, 10000) -- a 200 x 200 core plus a margin
+    # 3 (R + 2 vmax) + R wider than any dependency of the core's agents -- and
+    # every core agent's state after 3 device steps must equal the oracle's
+    from paper_2601_16292_b200.workloads import V3_BOIDS_SCALE as cfg
+    m = make(cfg)
+    ref0 = orc.boids_init(cfg["n"], cfg["L"], cfg["seed"])
+    for a, b in zip(state(m), ref0):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    K, x0, W = 3, 10_000.0, 200.0
+    M = K * (cfg["R"] + 2 * cfg["vmax"] * cfg["dt"]) + cfg["R"]
+    px, py = ref0[0], ref0[1]
+    win = np.nonzero((px >= x0 - M) & (px < x0 + W + M) & (py >= x0 - M) & (py < x0 + W + M))[0]
+    core = (px[win] >= x0) & (px[win] < x0 + W) & (py[win] >= x0) & (py[win] < x0 + W)
+    assert core.sum() > 3000
+    sub = tuple(c[win] for c in ref0)
+    P = oparams(orc, cfg)
+    for _ in range(K):
+        sub = orc.boids_step(sub, P)
+    m.step(1)
+    m.step(K - 1)
+    got = state(m)
+    for g, o in zip(got, sub):
+        assert np.array_equal(g[win[core]].view(np.uint32), o[core].view(np.uint32))
