@@ -130,7 +130,7 @@ __global__ void boids_count_kernel(const float4* __restrict__ st, int64_t n, Boi
         if (p < n) {
             const float4 s = st[p];
             c = cell_coord(s.y, a) * a.ncx + cell_x(s.x, a);
-            cell_of[p] = c;
+            if (cell_of) cell_of[p] = c;
         }
         int head, rank, len;
         lane_runs(c, head, rank, len);
@@ -337,17 +337,24 @@ __global__ void __launch_bounds__(1024) boids_chunk_scan_kernel(int* __restrict_
 // (ncell_zero cells; 0 when the counts were cleared otherwise).
 // QV (svel != nullptr): the sorted record carries q24(v) as int32 bits in z, w
 // (the stencil's candidates) and svel the float velocity (the agent's own update).
+// cell_of == nullptr: the cell is recomputed from the state (which the pass
+// reads anyway) instead of read -- 8 B/agent less traffic between the passes.
 __global__ void boids_scatter_kernel(const float4* __restrict__ st, const int32_t* __restrict__ ids, int64_t n,
                                      const int* __restrict__ cell_of, int* __restrict__ cursor, float4* __restrict__ sorted,
                                      int32_t* __restrict__ sorted_ids, int* __restrict__ cnt, int ncell_zero,
-                                     float2* __restrict__ svel)
+                                     float2* __restrict__ svel, BoidsArgs a)
 {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
     for (int64_t c = tid; c < ncell_zero; c += nt) cnt[c] = 0;
     const int64_t rounds = (n + nt - 1) / nt;
     for (int64_t r = 0; r < rounds; ++r) {  // uniform trip count: the lanes cooperate
         const int64_t p = r * nt + tid;
-        const int c = p < n ? cell_of[p] : -1;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        int c = -1;
+        if (p < n) {
+            v = st[p];
+            c = cell_of ? cell_of[p] : cell_coord(v.y, a) * a.ncx + cell_x(v.x, a);
+        }
         int head, rank, len;
         lane_runs(c, head, rank, len);
         int q = 0;
@@ -355,7 +362,6 @@ __global__ void boids_scatter_kernel(const float4* __restrict__ st, const int32_
         q = __shfl_sync(0xffffffffu, q, head) + rank;
         if (c >= 0) {
             AMBER_DCHECK(q >= 0 && q < n, "Boids scatter: sorted slot out of range");
-            const float4 v = st[p];
             if (svel) {
                 sorted[q] = make_float4(v.x, v.y, __int_as_float(__float2int_rn(__fmul_rn(v.z, kFix))),
                                         __int_as_float(__float2int_rn(__fmul_rn(v.w, kFix))));
@@ -598,7 +604,7 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
                 if (digest) dig += digest_term(static_cast<unsigned long long>(id), __float_as_uint(nx.x));
                 if (next_cnt) {
                     ncell_of = cell_coord(nx.y, a) * a.ncx + cell_x(nx.x, a);
-                    next_cell[p] = ncell_of;
+                    if (next_cell) next_cell[p] = ncell_of;
                 }
             }
             // observables (B8) in double, one per lane
@@ -1039,6 +1045,12 @@ public:
     // and eight agents per warp (tools/boids_lanes_probe.py)
     int64_t lanes = 4;
     bool counted = false;  // cnt / cell_of hold the cell counts of the current state (from the last group step)
+    // populations up to this size count the next step's cells inside the stencil
+    // kernel (one launch less); larger ones run the streaming count pass
+    int64_t fused_count_max = [] {
+        const char* v = getenv("AMBER_BOIDS_FUSED_COUNT_MAX");
+        return v && *v ? std::atoll(v) : (1ll << 22);
+    }();
 
     BoidsModel(int64_t n_, const amber_boids_params& p_, uint64_t seed_, const amber_runtime* r)
     {
@@ -1135,7 +1147,7 @@ public:
                 // the cell counts: from the previous group step (fused), else a count pass
                 if (!counted) {
                     prof.launch(rt.stream, "boids_bin", [&] {
-                        boids_count_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(st.p, n, ba, cnt.p, cell_of.p,
+                        boids_count_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(st.p, n, ba, cnt.p, nullptr,
                                                                                          nullptr);
                     });
                     check_launch("boids_count_kernel");
@@ -1161,8 +1173,9 @@ public:
                 check_launch("boids_scan");
                 prof.launch(rt.stream, "boids_scatter", [&] {
                     boids_scatter_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(
-                        st.p, ids.p, n, cell_of.p, cursor.p, sorted.p, sids.p, cnt.p, ncell <= (1 << 16) ? ncell : 0,
-                        qv_now() ? svel.p : nullptr);
+                        st.p, ids.p, n, nullptr, cursor.p, sorted.p, sids.p, cnt.p,
+                        ncell <= (1 << 16) ? ncell : 0,
+                        qv_now() ? svel.p : nullptr, ba);
                 });
                 check_launch("boids_scatter_kernel");
             }
@@ -1183,11 +1196,11 @@ public:
                     // cells (one launch less per step: C3 83 -> 75 us); large ones keep
                     // the streaming count pass (the stencil kernel is issue-bound there:
                     // fused, V3 32.8 -> 33.7 ms)
-                    int* nc_cnt = ba.nc > 1 && n <= (1ll << 22) ? cnt.p : nullptr;
+                    int* nc_cnt = ba.nc > 1 && n <= fused_count_max ? cnt.p : nullptr;
                     const bool qv = qv_now();
 #define AMBER_BOIDS_GROUP(G_, QV_, MB_)                                                                          \
     boids_group_kernel<G_, QV_, MB_><<<g, threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a, st.p, ids.p, sl, \
-                                                                   dg, nc_cnt, cell_of.p, svel.p)
+                                                                   dg, nc_cnt, nullptr, svel.p)
 #define AMBER_BOIDS_GROUP4(QV_)                                                  \
     if (n > (1ll << 22)) AMBER_BOIDS_GROUP(4, QV_, AMBER_BOIDS_MINB_LARGE); \
     else AMBER_BOIDS_GROUP(4, QV_, AMBER_BOIDS_MINB)
@@ -1202,7 +1215,7 @@ public:
 #undef AMBER_BOIDS_GROUP
                 });
                 check_launch("boids_group_kernel");
-                counted = ba.nc > 1 && n <= (1ll << 22);
+                counted = ba.nc > 1 && n <= fused_count_max;
             }
             ++t;
             if (p.vmax < 64.0f) vel_small = true;  // the step clamped every velocity to vmax < 64

@@ -18,7 +18,7 @@ res = {}
 for name, c, first, k in (("c3", W.C3_BOIDS, 0, 100), ("v3", W.V3_BOIDS_SCALE, 1, 9)):
     bp = boids_params(*[c[x] for x in ("L", "R", "rs", "wc", "wa", "ws", "vmax", "dt")])
     digs = set()
-    for lanes in (1, 4, 8, 16):
+    for lanes in (4, 8, 16):
         m = Model("boids", c["n"], bp, c["seed"])
         m.set_option("lanes", lanes)
         if first:
