@@ -299,6 +299,9 @@ int amber_digest(amber_model* m, const char* name, uint64_t* out);
  * lane of the step kernels: 0 = auto (8 above 2^22 agents, else 1), 1, 2, 4
  * or 8 -- identical results); Boids: "lanes" (4/8/16 lanes per agent in the
  * stencil, default 4 -- identical results).
+ * Test hook: wealth "inject_counter_fault" = local agent k adds one count to
+ * k's pending receiver counter (fault injection: the exact overflow check must
+ * catch it and the replay repair it).
  * Read-only (amber_get_option): wealth "replays" (exact-replay count, after
  * the overflow check), "counter_bits", "scatter" (1: packed-counter L2
  * atomics, the one shipped scatter), "exchange" (sharded: 0 none,

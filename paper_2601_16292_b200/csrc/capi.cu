@@ -56,6 +56,7 @@ int amber_model_create(amber_kind kind, int64_t n_agents, const void* params, si
                        const amber_runtime* rt, amber_model** out)
 {
     return guarded([&] {
+        amber::NvtxRange nv("amber_model_create");
         need(out, "out");
         *out = nullptr;
         need(params, "params");
@@ -107,6 +108,7 @@ int amber_model_destroy(amber_model* m)
 int amber_step(amber_model* m, int64_t n_steps)
 {
     return guarded([&] {
+        amber::NvtxRange nv("amber_step");
         impl(m)->step(n_steps);
         return 0;
     });
@@ -151,6 +153,7 @@ int amber_column_info(amber_model* m, const char* name, amber_dtype* dtype, int6
 int amber_read_column(amber_model* m, const char* name, void* dst, size_t dst_bytes, int dst_on_device)
 {
     return guarded([&] {
+        amber::NvtxRange nv("amber_read_column");
         need(name, "name");
         need(dst, "dst");
         impl(m)->read_column(name, dst, dst_bytes, dst_on_device != 0);
@@ -161,6 +164,7 @@ int amber_read_column(amber_model* m, const char* name, void* dst, size_t dst_by
 int amber_write_column(amber_model* m, const char* name, const void* src, size_t src_bytes, int src_on_device)
 {
     return guarded([&] {
+        amber::NvtxRange nv("amber_write_column");
         need(name, "name");
         need(src, "src");
         impl(m)->write_column(name, src, src_bytes, src_on_device != 0);
@@ -246,6 +250,7 @@ int amber_sweep(amber_kind kind, int64_t n_agents, const void* base_params, size
                 double* out_final_r_frac, amber_sweep_stats* stats)
 {
     return guarded([&] {
+        amber::NvtxRange nv("amber_sweep");
         if (kind != AMBER_SIR_GRAPH) amber::fail(AMBER_E_UNKNOWN_KIND, "amber_sweep supports AMBER_SIR_GRAPH only");
         need(base_params, "base_params");
         AMBER_REQUIRE(params_size >= sizeof(amber_sir_params), "params_size < sizeof(amber_sir_params)");

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <cstdio>
@@ -149,6 +150,15 @@ struct DevBuf {
 // Records a CUDA event pair around every launch of a named kernel while
 // enabled (on the launching stream), so per-kernel device time can be read
 // back without an external profiler.
+// NVTX range for the host side of a phase (amber_* entry points and every
+// named kernel launch); header-only NVTX 3, free when no tool is attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct Profiler {
     bool on = false;
     struct Kernel {
@@ -164,6 +174,7 @@ struct Profiler {
     template <class F>
     void launch(cudaStream_t s, const char* name, F&& f)
     {
+        NvtxRange nv(name);
         if (!on) {
             f();
             return;

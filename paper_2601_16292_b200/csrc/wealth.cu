@@ -421,6 +421,15 @@ __global__ void wealth_recv_p2p_kernel(const unsigned long long* __restrict__ pe
     block_sum_atomic<1>(vals, outs);
 }
 
+// Fault injection (test hook, option "inject_counter_fault"): one extra count
+// in the pending counters of local agent k -- a corrupted counter the exact
+// overflow check (sent != got) must catch and the replay must repair.
+__global__ void wealth_inject_kernel(uint32_t* inc, int64_t k, int B)
+{
+    const int per = 32 / B;
+    atomicAdd(inc + k / per, 1u << (static_cast<uint32_t>(k % per) * B));
+}
+
 __global__ void wealth_fill_kernel(int32_t* w, int64_t n_loc, int64_t n_pad, int32_t w0)
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pad; i += (int64_t)gridDim.x * blockDim.x)
@@ -964,6 +973,12 @@ public:
     bool set_option(const char* key, int64_t v) override
     {
         std::string k(key);
+        if (k == "inject_counter_fault") {  // test hook: corrupt one pending counter (fault injection)
+            AMBER_REQUIRE(pending && v >= 0 && v < n_loc, "inject_counter_fault needs a pending scatter and 0 <= v < n_loc");
+            wealth_inject_kernel<<<1, 1, 0, rt.stream>>>(inc[t & 1].p, v, B);
+            check_launch("wealth_inject_kernel");
+            return true;
+        }
         if (k == "metrics_capacity") {
             AMBER_REQUIRE(v >= 16, "metrics_capacity must be >= 16");
             verify();
