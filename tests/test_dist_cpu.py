@@ -248,3 +248,32 @@ def test_sharded_wealth_step_equals_oracle(world, orc):
     w = np.concatenate([np.array(x, np.int32) for _, x in sorted(parts)])
     ref = orc.wealth_run(np.ones(1003, np.int32), 17, 0, 6)[0]
     assert np.array_equal(w, ref)
+
+
+def _host_collectives(rank, world):
+    # the binding's amber_runtime.host_allgather / host_barrier callbacks over a
+    # gloo group, called through their C function pointers exactly as the
+    # library calls them (send / recv raw addresses, bytes per rank)
+    import ctypes as C
+
+    from paper_2601_16292_b200.model import HostCollectives
+    hc = HostCollectives(dist.group.WORLD)
+    out = []
+    for nbytes in (4, 64, 1000):
+        send = (C.c_uint8 * nbytes)(*[(rank * 31 + k) % 256 for k in range(nbytes)])
+        recv = (C.c_uint8 * (nbytes * world))()
+        rc = hc.allgather(C.addressof(send), C.addressof(recv), nbytes, None)
+        out.append((rc, bytes(recv)))
+    out.append((hc.barrier(None), b""))
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_collectives_marshalling(world):
+    res = run_world(world, _host_collectives)
+    for rank_out in res:
+        for (rc, got), nbytes in zip(rank_out[:3], (4, 64, 1000)):
+            assert rc == 0
+            want = b"".join(bytes((r * 31 + k) % 256 for k in range(nbytes)) for r in range(world))
+            assert got == want
+        assert rank_out[3][0] == 0
