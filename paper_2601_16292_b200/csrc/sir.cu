@@ -293,6 +293,13 @@ constexpr int kSirPT = AMBER_SIR_PT;  // threads per block of the persistent ker
 #define AMBER_SIR_MINB (1024 / AMBER_SIR_PT)
 #endif
 constexpr int kSirMinB = AMBER_SIR_MINB;  // min resident blocks per SM (register cap 64 at 256 threads)
+// 8 agents per lane (large populations): 5 blocks per SM (48 registers, a few
+// spills) -- more warps to cover the random neighbour probes: V2 1.53 -> 1.42
+// ms/step (6 blocks, 40 registers: 1.41 with 4x the spills)
+#ifndef AMBER_SIR_MINB_LARGE
+#define AMBER_SIR_MINB_LARGE 5
+#endif
+constexpr int kSirMinBLarge = AMBER_SIR_MINB_LARGE;
 
 // Warp chunks of 32 * APL agents: lane L holds agents APL*L .. APL*L+APL-1 of
 // the chunk (one load of its state bytes; for APL = 4 one Philox block serves
@@ -755,7 +762,7 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
 // slot, so every block takes the same decision), otherwise it pulls.  Both
 // directions give identical results (S3); the tests check it.
 template <int APL>
-__global__ void __launch_bounds__(kSirPT, kSirMinB) sir_persistent_kernel(const SirStepArgs a)
+__global__ void __launch_bounds__(kSirPT, APL == 8 ? kSirMinBLarge : kSirMinB) sir_persistent_kernel(const SirStepArgs a)
 {
     __shared__ SirSmem sm;
     cg::grid_group grid = cg::this_grid();
