@@ -22,7 +22,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "amber_oracle.c")
 HDR = os.path.join(HERE, "amber_oracle.h")
-LIB = os.path.join(HERE, "liboracle.so")
+LIB = os.environ.get("AMBER_ORACLE_LIB") or os.path.join(HERE, "liboracle.so")  # (sanitizer builds: tests)
 
 TAG_WEALTH_RECV = 0x01
 TAG_SIR_TX = 0x10
