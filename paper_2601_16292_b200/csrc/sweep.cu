@@ -65,6 +65,29 @@ __global__ void sweep_max_arcs_kernel(const int32_t* __restrict__ row_ptr, int64
     if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
 
+// enqueue (graph.cuh) with the queue in shared memory: the owners of `mask`
+// (agents a0 + b) are appended at slots qc + rank; at 32 queued, lane l's
+// owner is slot l and the walk runs; the remainder moves to the front.
+template <class W>
+__device__ __forceinline__ void enqueue_sq(uint32_t mask, uint32_t a0, uint16_t* sq, uint32_t& qid, uint32_t& qc,
+                                           W&& walk)
+{
+    const uint32_t lane = threadIdx.x & 31, k = __popc(mask);
+    if (!k) return;
+    if ((mask >> lane) & 1u) sq[qc + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(a0 + lane);
+    __syncwarp();
+    qc += k;
+    if (qc < 32) return;
+    qid = sq[lane];
+    walk(32u);
+    const uint32_t rem = qc - 32;
+    const uint16_t v = lane < rem ? sq[32 + lane] : 0;
+    __syncwarp();
+    if (lane < rem) sq[lane] = v;
+    __syncwarp();
+    qc = rem;
+}
+
 template <bool COL_SMEM>
 __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
 {
@@ -72,6 +95,12 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
     uint32_t* rp = reinterpret_cast<uint32_t*>(smem);                  // n + 1
     uint16_t* cs = reinterpret_cast<uint16_t*>(rp + ((a.n + 4) & ~3ll));  // col_cap (COL_SMEM)
     uint8_t* xs = reinterpret_cast<uint8_t*>(cs + (COL_SMEM ? ((a.col_cap + 7) & ~7ll) : 0));
+    // COL_SMEM (n <= 65536): each warp's owner queue as 64 u16 slots in shared
+    // memory -- queued by rank (popc of the lower set bits), one STS per owner,
+    // instead of a register queue filled with __fns (r02 ncu: __fns and its
+    // enqueue were 16% of the sweep's instructions)
+    uint16_t* sq = COL_SMEM ? reinterpret_cast<uint16_t*>(xs + ((2 * a.n_pad + 15) & ~15ll)) + (threadIdx.x >> 5) * 64
+                            : nullptr;
     __shared__ int rep_s;
     __shared__ int cnt_s[2][2];  // [parity][I, S]
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -172,9 +201,13 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
                 for (int64_t a0 = warp * 32; a0 < a.n_pad; a0 += nwarps * 32) {
                     const int64_t i = a0 + lane;
                     const uint32_t own = __ballot_sync(0xffffffffu, i < a.n && x[i] == kI);
-                    enqueue(own, static_cast<uint32_t>(a0), qid, qc, walk_push);
+                    if constexpr (COL_SMEM) enqueue_sq(own, static_cast<uint32_t>(a0), sq, qid, qc, walk_push);
+                    else enqueue(own, static_cast<uint32_t>(a0), qid, qc, walk_push);
                 }
-                if (qc) walk_push(qc);
+                if (qc) {
+                    if constexpr (COL_SMEM) qid = static_cast<uint32_t>(lane) < qc ? sq[lane] : 0u;
+                    walk_push(qc);
+                }
                 __syncthreads();
                 // counts of the pushed state, four bytes per load (padding bytes are 3)
                 for (int64_t q = tid; q < nq; q += nt) {
@@ -231,9 +264,13 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
                         if (i < a.n_pad) y[i] = o;
                         n_inf += real && o == kI;
                     }
-                    enqueue(s_mask, static_cast<uint32_t>(a0), qid, qc, walk_pull);
+                    if constexpr (COL_SMEM) enqueue_sq(s_mask, static_cast<uint32_t>(a0), sq, qid, qc, walk_pull);
+                    else enqueue(s_mask, static_cast<uint32_t>(a0), qid, qc, walk_pull);
                 }
-                if (qc) walk_pull(qc);
+                if (qc) {
+                    if constexpr (COL_SMEM) qid = static_cast<uint32_t>(lane) < qc ? sq[lane] : 0u;
+                    walk_pull(qc);
+                }
             }
             n_inf = __reduce_add_sync(0xffffffffu, n_inf);
             n_sus = __reduce_add_sync(0xffffffffu, n_sus);
@@ -360,10 +397,12 @@ void run_sweep(int64_t n, const amber_sir_params& base, const amber_replicate* r
         AMBER_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, rt.device));
         const size_t rp_bytes = ((n + 4) & ~3ll) * 4, st_bytes = 2 * n_pad;
         const size_t col_bytes = ((max_arcs + 7) & ~7ll) * 2;
-        const bool col_smem = n <= 65536 && rp_bytes + col_bytes + st_bytes + 64 <= static_cast<size_t>(smem_max);
+        const size_t sq_bytes = 32 * 64 * 2 + 16;  // the warps' owner queues (COL_SMEM), 16-byte aligned
+        const bool col_smem =
+            n <= 65536 && rp_bytes + col_bytes + st_bytes + sq_bytes + 64 <= static_cast<size_t>(smem_max);
         a.col_smem = col_smem;
         a.col_cap = col_smem ? max_arcs : 0;
-        size_t smem = rp_bytes + (col_smem ? col_bytes : 0) + st_bytes;
+        size_t smem = rp_bytes + (col_smem ? col_bytes + sq_bytes : 0) + st_bytes;
         AMBER_REQUIRE(smem + 64 <= static_cast<size_t>(smem_max), "sweep: replicate state does not fit shared memory");
         auto kern = col_smem ? sir_sweep_kernel<true> : sir_sweep_kernel<false>;
         AMBER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
