@@ -355,6 +355,16 @@ __device__ __forceinline__ uint32_t* queue_of(const SirStepArgs& a, uint32_t t, 
     return a.queue ? a.queue + ((t & 1u) * 2 + phase) * kRegions : nullptr;
 }
 
+// Relaxed (no-return) bitwise reductions: red.global.or / .and.
+__device__ __forceinline__ void red_or(uint32_t* p, uint32_t v)
+{
+    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_and(uint32_t* p, uint32_t v)
+{
+    asm volatile("red.relaxed.gpu.global.and.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // Plain (coherent) load: the bitmaps are rewritten by earlier steps of the same
 // persistent launch, so the read-only (.nc) path must not be used.
 // The lookups are random over the whole bitmap (12.5 MB at N = 1e8), so they
@@ -674,12 +684,24 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
             const uint4 wd = philox(make_uint4(min(s, j), max(s, j), t, TAG_SIR_TX), a.key);
             if (static_cast<unsigned long long>(wd.x) < a.t_beta) {
                 const uint32_t bit = 1u << (j & 31u);
-                const uint32_t prev = atomicOr(ib_next + (j >> 5), bit);
-                if (!(prev & bit)) {
-                    atomicAnd(sb_next + (j >> 5), ~bit);
-                    atomicOr(yw + (j >> 2), static_cast<uint32_t>(kI) << ((j & 3u) * 8u));
-                    ++inf;
-                    if (a.digest) dig += digest_term(j, kI) - digest_term(j, kS);
+                if (a.digest || APL != 8) {  // the old word dedups the digest delta and the count
+                    const uint32_t prev = atomicOr(ib_next + (j >> 5), bit);
+                    if (!(prev & bit)) {
+                        atomicAnd(sb_next + (j >> 5), ~bit);
+                        atomicOr(yw + (j >> 2), static_cast<uint32_t>(kI) << ((j & 3u) * 8u));
+                        ++inf;
+                        dig += digest_term(j, kI) - digest_term(j, kS);
+                    }
+                } else {
+                    // large populations: three idempotent REDs, no returned word to
+                    // wait for (r02 ncu: the returning atomicOr held 10% of the V2
+                    // stall samples); the new infections are counted after the step
+                    // (sir_count_new: one bitmap pass + one grid barrier, V2 1.42 ->
+                    // 1.35 ms/step).  Small ones keep the inline count: at C2 the
+                    // extra barrier per push step costs more (4.98 -> 6.8 us/step).
+                    red_or(ib_next + (j >> 5), bit);
+                    red_and(sb_next + (j >> 5), ~bit);
+                    red_or(yw + (j >> 2), static_cast<uint32_t>(kI) << ((j & 3u) * 8u));
                 }
             }
             return false;  // an infected agent tries every susceptible neighbour
@@ -756,6 +778,22 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
     if (qn) walk(0, qn);
 }
 
+// New infections of a push step that did not count them (no digest): agents S
+// before it (back buffer sb) and I after it (current ib), summed over the grid
+// into that step's ring slot (S -= new, I += new).  After a grid barrier.
+__device__ __forceinline__ void sir_count_new(const SirStepArgs& a, int cur, SirSlot* slot)
+{
+    const uint32_t* sb_prev = a.sb[cur ^ 1];
+    const uint32_t* ib_now = a.ib[cur];
+    const int64_t words = a.n_pad / 32;
+    unsigned long long c = 0;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x)
+        c += __popc(__ldcg(sb_prev + w) & __ldcg(ib_now + w));
+    unsigned long long v[2] = {0ull - c, c};
+    unsigned long long* const outs[2] = {&slot->S, &slot->I};
+    block_sum_atomic<2>(v, outs);
+}
+
 // All n_steps steps in one cooperative launch (grid barrier between steps).
 // Direction-optimizing: step k pushes from the infected agents when they are
 // fewer than 3/4 of the susceptible ones (counts of the previous step from its ring
@@ -767,9 +805,14 @@ __global__ void __launch_bounds__(kSirPT, APL == 8 ? kSirMinBLarge : kSirMinB) s
     __shared__ SirSmem sm;
     cg::grid_group grid = cg::this_grid();
     int cur = a.cur;
+    bool uncounted = false;  // the previous step of this launch pushed without counting its new infections
     for (int64_t k = 0; k < a.n_steps; ++k) {
         const uint32_t t = a.t0 + static_cast<uint32_t>(k);
         SirSlot* sl = a.ring + (t % a.ring_cap);
+        if (uncounted) {  // complete slot t-1 before anyone reads it
+            sir_count_new(a, cur, a.ring + ((t + a.ring_cap - 1) % a.ring_cap));
+            grid.sync();
+        }
         // the counters of step t+1 were last used by step t-1 (finished at the previous barrier)
         if (a.queue && blockIdx.x == 0 && threadIdx.x < 2 * kRegions) a.queue[((t + 1) & 1u) * 2 * kRegions + threadIdx.x] = 0u;
         bool push = false;
@@ -803,9 +846,11 @@ __global__ void __launch_bounds__(kSirPT, APL == 8 ? kSirMinBLarge : kSirMinB) s
             unsigned long long* const outs[4] = {&sl->S, &sl->I, &sl->R, a.digest ? &sl->digest : nullptr};
             block_sum_atomic<4>(cnt, outs);
         }
+        uncounted = push && !a.digest && APL == 8;
         cur ^= 1;
         grid.sync();
     }
+    if (uncounted) sir_count_new(a, cur, a.ring + ((static_cast<int64_t>(a.t0) + a.n_steps - 1) % a.ring_cap));
 }
 
 // Sharded graph slice: row offsets rebased to the shard's first arc.

@@ -339,3 +339,25 @@ def test_v2_full_size_vs_oracle_golden():
     for k, name in enumerate("SIR"):
         assert np.array_equal(m.metrics(name).astype(np.uint64), want[:, 1 + k]), name
     assert m.digest("state") == int(want[-1, 4])
+
+
+@pytest.mark.parametrize("direction", [0, 2])
+def test_apl8_push_counts_deferred(orc, direction):
+    # 8 agents per lane, digest off: pushers set the next bits with no-return
+    # REDs and the new infections are counted after the step (sir_count_new);
+    # the per-step S/I/R must still equal the oracle's, including the last step
+    # of every call and across calls
+    cfg = dict(n=100_003, mean_degree=8.0, beta=0.2, gamma=0.15, init_frac=0.01, seed=13)
+    m = make(cfg)
+    m.set_option("apl", 8)
+    m.set_option("direction", direction)
+    rp, col = oracle_graph(orc, m, cfg)
+    x = orc.sir_init(cfg["n"], sir_counts(cfg)[1], cfg["seed"])
+    t = 0
+    for chunk in (1, 4, 2, 7):
+        m.step(chunk)
+        x, counts, _ = orc.sir_run(rp, col, x, cfg["seed"], cfg["beta"], cfg["gamma"], t, chunk)
+        t += chunk
+        assert np.array_equal(m.read_column("state"), x), f"step {t}"
+        for k, name in enumerate("SIR"):
+            assert np.array_equal(m.metrics(name)[-chunk:], counts[:, k]), (name, t)
