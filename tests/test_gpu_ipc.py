@@ -1,5 +1,5 @@
 """Cross-process peer-memory exchange on one B200: two
-processes, one GPU, gloo host collectives.  The sharded wealth step's P2P path
+or three processes, one GPU, gloo host collectives.  The sharded wealth step's P2P path
 -- cudaIpcGetMemHandle / cudaIpcOpenMemHandle of the bucket blocks and
 wealth_recv_p2p_kernel reading the OTHER process's buckets -- must equal the
 unsharded oracle bit for bit (column, all-reduced total / active / digest),
@@ -22,10 +22,10 @@ def free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("n,steps,bits", [(200_003, 12, 4), (90_001, 10, 2)])
-def test_two_process_ipc_exchange_bit_exact(tmp_path, n, steps, bits):
+@pytest.mark.parametrize("world,n,steps,bits", [(2, 200_003, 12, 4), (2, 90_001, 10, 2), (3, 150_001, 9, 4)])
+def test_multi_process_ipc_exchange_bit_exact(tmp_path, world, n, steps, bits):
     out = tmp_path / "res.json"
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={free_port()}",
            os.path.join(ROOT, "tests", "mp_wealth_ipc_worker.py"), str(out), str(n), "77", str(steps), str(bits)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
