@@ -138,61 +138,84 @@ __global__ void boids_count_kernel(const float4* __restrict__ st, int64_t n, Boi
     }
 }
 
-// Exclusive scan of the cell counts by one CTA (ncell <= 2^16): warp w owns a
-// contiguous segment of cells, read 32 at a time (coalesced).  Pass 1 sums each
-// segment, warp 0 scans the 32 segment totals, pass 2 re-walks each segment
-// with warp inclusive scans plus a running carry, its loads issued eight
-// batches at a time (restrict pointers: nothing aliases the counts, which the
-// scatter kernel zeroes afterwards), and writes start / cursor.
-__global__ void __launch_bounds__(1024) boids_scan_kernel(const int* __restrict__ cnt, int* __restrict__ start,
-                                                          int* __restrict__ cursor, int ncell)
+// Exclusive scan of the ncell + 1 counts by one CTA (ncell <= 2^16), register
+// resident: each thread loads 16 consecutive counts (four 16-byte loads), one
+// block scan of the thread sums (warp shuffles + the 32 warp totals), then 16
+// starts per thread with 16-byte stores -- one global round trip per 16,384
+// cells (r02: replaced a two-pass segment scan, 8.7 -> 6.5 us cold; grids up
+// to kScanSmemCells now fold the scan into the scatter, below).
+__global__ void __launch_bounds__(1024) boids_scan_reg_kernel(const int* __restrict__ cnt, int* __restrict__ start,
+                                                              int* __restrict__ cursor, int ncell)
 {
-    __shared__ int seg_off[32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int per = ((ncell + 31) / 32 + 31) & ~31;  // cells per warp segment (multiple of 32)
-    const int s0 = warp * per, s1 = min(s0 + per, ncell);
-    int sum = 0;
-#pragma unroll 8
-    for (int c = s0 + lane; c < s1; c += 32) sum += cnt[c];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (lane == 0) seg_off[warp] = sum;
+    __shared__ int wsum[32];
+    __shared__ int carry_s;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry_s = 0;
     __syncthreads();
-    if (warp == 0) {
-        const int v = seg_off[lane];
-        int incl = v;
+    const int total = ncell + 1;  // cnt[ncell] = 0, so start[ncell] = n
+    for (int base = 0; base < total; base += 1024 * 16) {
+        const int c0 = base + threadIdx.x * 16;
+        int v[16];
+        const bool full = c0 + 16 <= total;
+        if (full) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int4 q = reinterpret_cast<const int4*>(cnt + c0)[k];
+                v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] = c0 + k < total ? cnt[c0 + k] : 0;
+        }
+        int sum = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) sum += v[k];
+        int incl = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int u = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += u;
         }
-        seg_off[lane] = incl - v;
-        if (lane == 31) start[ncell] = incl;
-    }
-    __syncthreads();
-    int carry = seg_off[warp];
-    for (int b = s0; b < s1; b += 32 * 8) {
-        int v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int c = b + 32 * j + lane;
-            v[j] = c < s1 ? cnt[c] : 0;
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int c = b + 32 * j + lane;
-            int incl = v[j];
+        if (lane == 31) wsum[w] = incl;
+        __syncthreads();
+        if (w == 0) {
+            const int x = wsum[lane];
+            int xi = x;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const int u = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += u;
+                const int u = __shfl_up_sync(0xffffffffu, xi, o);
+                if (lane >= o) xi += u;
             }
-            if (c < s1) {
-                start[c] = carry + incl - v[j];
-                cursor[c] = carry + incl - v[j];
-            }
-            carry += __shfl_sync(0xffffffffu, incl, 31);
+            wsum[lane] = xi - x;
         }
+        __syncthreads();
+        const int carry = carry_s;
+        int run = carry + wsum[w] + incl - sum;
+        if (full && c0 + 16 <= ncell) {  // 16 real cells: 16-byte stores
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                int4 o;
+                o.x = run; run += v[4 * k];
+                o.y = run; run += v[4 * k + 1];
+                o.z = run; run += v[4 * k + 2];
+                o.w = run; run += v[4 * k + 3];
+                reinterpret_cast<int4*>(start + c0)[k] = o;
+                reinterpret_cast<int4*>(cursor + c0)[k] = o;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const int c = c0 + k;
+                if (c < total) {
+                    start[c] = run;
+                    if (c < ncell) cursor[c] = run;
+                }
+                run += v[k];
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) carry_s = run;  // the pass's running total
+        __syncthreads();
     }
 }
 
@@ -368,6 +391,116 @@ __global__ void boids_scatter_kernel(const float4* __restrict__ st, const int32_
                 svel[q] = make_float2(v.z, v.w);
             } else {
                 sorted[q] = v;
+            }
+            sorted_ids[q] = ids[p];
+        }
+    }
+}
+
+// Small grids (<= kScanSmemCells cells): the cell scan folded into the scatter
+// pass.  Every block (1024 threads, one per SM) scans the whole count array
+// itself -- 16 counts per thread by 16-byte loads, one block scan, the starts
+// kept in shared memory -- instead of a one-CTA scan launch before the scatter
+// (C3: 10^4 cells, a 40 KB read per block from L2); block 0 also writes the
+// global starts the stencil reads.  Counts and placement counters are
+// double-buffered by step parity (row stride cs, a multiple of 16, padding
+// zero): this pass reads cnt and claims slots in fill (zero), and zeroes the
+// other parity's cnt (counted by the next stencil) and fill (the next step's
+// placement).
+constexpr int kScanSmemCells = 12000;  // ss: 48 KB static shared memory
+
+__global__ void __launch_bounds__(1024) boids_scatter_scan_kernel(
+    const float4* __restrict__ st, const int32_t* __restrict__ ids, int64_t n, const int* __restrict__ cnt,
+    int* __restrict__ cnt_zero, int* __restrict__ fill, int* __restrict__ fill_zero, int ncell, int cs,
+    int* __restrict__ start, float4* __restrict__ sorted, int32_t* __restrict__ sorted_ids,
+    float2* __restrict__ svel, BoidsArgs a)
+{
+    __shared__ __align__(16) int ss[(kScanSmemCells + 16) & ~15];
+    __shared__ int wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int total = ncell + 1;  // cnt[ncell] = 0, so start[ncell] = n
+    const int c0 = tid * 16;
+    int v[16];
+    if (c0 < total) {  // cs >= c0 + 16: the padded row
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int4 q = __ldcg(reinterpret_cast<const int4*>(cnt + c0) + k);
+            v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = 0;
+    }
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) sum += v[k];
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        const int x = wsum[lane];
+        int xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += u;
+        }
+        wsum[lane] = xi - x;
+    }
+    __syncthreads();
+    if (c0 < total) {
+        int run = wsum[w] + incl - sum;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            int4 o;
+            o.x = run; run += v[4 * k];
+            o.y = run; run += v[4 * k + 1];
+            o.z = run; run += v[4 * k + 2];
+            o.w = run; run += v[4 * k + 3];
+            reinterpret_cast<int4*>(ss + c0)[k] = o;  // c0 + 16 <= 12016
+            if (blockIdx.x == 0) {
+                if (c0 + 4 * k + 4 <= total) {
+                    reinterpret_cast<int4*>(start + c0)[k] = o;
+                } else {
+                    const int e[4] = {o.x, o.y, o.z, o.w};
+                    for (int j = 0; j < 4 && c0 + 4 * k + j < total; ++j) start[c0 + 4 * k + j] = e[j];
+                }
+            }
+        }
+    }
+    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + tid, nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t c = gt; c < cs / 4; c += nt) {
+        reinterpret_cast<int4*>(cnt_zero)[c] = make_int4(0, 0, 0, 0);
+        reinterpret_cast<int4*>(fill_zero)[c] = make_int4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    const int64_t rounds = (n + nt - 1) / nt;
+    for (int64_t r = 0; r < rounds; ++r) {  // uniform trip count: the lanes cooperate
+        const int64_t p = r * nt + gt;
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        int c = -1;
+        if (p < n) {
+            x = st[p];
+            c = cell_coord(x.y, a) * a.ncx + cell_x(x.x, a);
+        }
+        int head, rank, len;
+        lane_runs(c, head, rank, len);
+        int q = 0;
+        if (c >= 0 && rank == 0) q = ss[c] + atomicAdd(fill + c, len);  // one slot claim per run
+        q = __shfl_sync(0xffffffffu, q, head) + rank;
+        if (c >= 0) {
+            AMBER_DCHECK(q >= 0 && q < n, "Boids scatter: sorted slot out of range");
+            if (svel) {
+                sorted[q] = make_float4(x.x, x.y, __int_as_float(__float2int_rn(__fmul_rn(x.z, kFix))),
+                                        __int_as_float(__float2int_rn(__fmul_rn(x.w, kFix))));
+                svel[q] = make_float2(x.z, x.w);
+            } else {
+                sorted[q] = x;
             }
             sorted_ids[q] = ids[p];
         }
@@ -1045,6 +1178,13 @@ public:
     // and eight agents per warp (tools/boids_lanes_probe.py)
     int64_t lanes = 4;
     bool counted = false;  // cnt / cell_of hold the cell counts of the current state (from the last group step)
+    // small grids: counts and placement counters double-buffered by step parity
+    // (boids_scatter_scan_kernel); spar flips every step, independent of t
+    bool fused_scan = false;
+    int spar = 0;
+    DevBuf<int> fill;
+    int cs = 0;  // count row stride (fused_scan: a multiple of 16)
+    int* cnt_of(int par) { return cnt.p + static_cast<int64_t>(par) * cs; }
     // populations up to this size count the next step's cells inside the stencil
     // kernel (one launch less); larger ones run the streaming count pass
     int64_t fused_count_max = [] {
@@ -1090,8 +1230,14 @@ public:
         sorted.allocate(&rt, n);
         ids.allocate(&rt, n);
         sids.allocate(&rt, n);
-        cnt.allocate(&rt, ncell + 1);
+        fused_scan = ba.nc > 1 && ncell <= kScanSmemCells;
+        cs = fused_scan ? (ncell + 16) & ~15 : 0;
+        cnt.allocate(&rt, fused_scan ? 2 * static_cast<int64_t>(cs) : ncell + 1);
         cnt.zero_async(rt.stream);
+        if (fused_scan) {
+            fill.allocate(&rt, 2 * static_cast<int64_t>(cs));
+            fill.zero_async(rt.stream);
+        }
         start.allocate(&rt, ncell + 1);
         cursor.allocate(&rt, ncell + 1);
         cell_of.allocate(&rt, n);
@@ -1107,7 +1253,7 @@ public:
     ~BoidsModel() override
     {
         if (rt.stream) cudaStreamSynchronize(rt.stream);
-        st.reset(); sorted.reset(); ids.reset(); sids.reset(); cnt.reset(); start.reset(); cursor.reset();
+        st.reset(); sorted.reset(); ids.reset(); sids.reset(); cnt.reset(); start.reset(); cursor.reset(); fill.reset();
         cell_of.reset(); col_tmp.reset(); ring.reset(); block_sums.reset(); chunk_sums.reset(); svel.reset();
         rt.destroy();
     }
@@ -1147,8 +1293,8 @@ public:
                 // the cell counts: from the previous group step (fused), else a count pass
                 if (!counted) {
                     prof.launch(rt.stream, "boids_bin", [&] {
-                        boids_count_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(st.p, n, ba, cnt.p, nullptr,
-                                                                                         nullptr);
+                        boids_count_kernel<<<grid_for(threads), threads, 0, rt.stream>>>(st.p, n, ba, cnt_of(spar),
+                                                                                         nullptr, nullptr);
                     });
                     check_launch("boids_count_kernel");
                 }
@@ -1157,9 +1303,21 @@ public:
                 // cursors = starts, counts re-zeroed for the next step: one CTA for small
                 // grids, a device-wide scan for large ones (the one-CTA scan took 20 ms at
                 // V3's 10^7 cells, r01)
+                if (fused_scan) {
+                    prof.launch(rt.stream, "boids_scatter", [&] {
+                        const int gs = grid ? static_cast<int>(grid)
+                                            : static_cast<int>(std::max<int64_t>(
+                                                  1, std::min<int64_t>(ceil_div(n, 1024), rt.num_sms)));
+                        boids_scatter_scan_kernel<<<gs, 1024, 0, rt.stream>>>(
+                            st.p, ids.p, n, cnt_of(spar), cnt_of(spar ^ 1), fill.p + spar * cs,
+                            fill.p + (spar ^ 1) * cs, ncell, cs, start.p, sorted.p, sids.p,
+                            qv_now() ? svel.p : nullptr, ba);
+                    });
+                    check_launch("boids_scatter_scan_kernel");
+                } else {
                 prof.launch(rt.stream, "boids_scan", [&] {
                     if (ncell <= (1 << 16)) {  // one launch: scan, cursors, re-zeroed counts
-                        boids_scan_kernel<<<1, 1024, 0, rt.stream>>>(cnt.p, start.p, cursor.p, ncell);
+                        boids_scan_reg_kernel<<<1, 1024, 0, rt.stream>>>(cnt.p, start.p, cursor.p, ncell);
                     } else {
                         const int nch = static_cast<int>(ceil_div(ncell + 1, kScanChunk));
                         boids_chunk_sums_kernel<<<nch, 1024, 0, rt.stream>>>(cnt.p, ncell + 1, chunk_sums.p);
@@ -1178,6 +1336,7 @@ public:
                         qv_now() ? svel.p : nullptr, ba);
                 });
                 check_launch("boids_scatter_kernel");
+                }
             }
             const BoidsArgs a = ba;
             {
@@ -1196,7 +1355,7 @@ public:
                     // cells (one launch less per step: C3 83 -> 75 us); large ones keep
                     // the streaming count pass (the stencil kernel is issue-bound there:
                     // fused, V3 32.8 -> 33.7 ms)
-                    int* nc_cnt = ba.nc > 1 && n <= fused_count_max ? cnt.p : nullptr;
+                    int* nc_cnt = ba.nc > 1 && n <= fused_count_max ? cnt_of(spar ^ 1) : nullptr;
                     const bool qv = qv_now();
 #define AMBER_BOIDS_GROUP(G_, QV_, MB_)                                                                          \
     boids_group_kernel<G_, QV_, MB_><<<g, threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a, st.p, ids.p, sl, \
@@ -1217,6 +1376,7 @@ public:
                 check_launch("boids_group_kernel");
                 counted = ba.nc > 1 && n <= fused_count_max;
             }
+            if (fused_scan) spar ^= 1;
             ++t;
             if (p.vmax < 64.0f) vel_small = true;  // the step clamped every velocity to vmax < 64
         }
@@ -1274,7 +1434,7 @@ public:
         }
         // positions changed: drop the counts the last group step left (the next
         // step counts again from zero)
-        if (counted) AMBER_CUDA(cudaMemsetAsync(cnt.p, 0, static_cast<size_t>(ncell) * sizeof(int), rt.stream));
+        if (counted) AMBER_CUDA(cudaMemsetAsync(cnt.p, 0, cnt.bytes(), rt.stream));
         rt.sync();
         counted = false;
     }
