@@ -554,7 +554,7 @@ __device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0,
             const int32_t rb = mine ? sm.rb[wq][g0 + lane] : 0, re = mine ? sm.re[wq][g0 + lane] : 0;
             const uint32_t own = nown >= 32 ? 0xffffffffu : ((1u << nown) - 1u);
             const uint32_t sid = static_cast<uint32_t>(a.gid0 + static_cast<unsigned long long>(a0 + lid));
-            const uint32_t hit = walk_rows_pay<kWalkU>(
+            const uint32_t hit = walk_rows_pay<kWalkU, APL == 8>(
                 [&](int32_t e) {
                     AMBER_DCHECK(e >= 0 && e < a.row_ptr[a.n], "SIR pull: arc index out of the CSR");
                     return static_cast<uint32_t>(__ldcs(a.col + e));
@@ -672,7 +672,7 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
         const uint32_t id = mine ? static_cast<uint32_t>(sm.id[wq][g0 + lane]) : 0u;
         const int32_t rb = mine ? a.row_ptr[id] : 0, re = mine ? a.row_ptr[id + 1] : 0;
         const uint32_t own = nown >= 32 ? 0xffffffffu : ((1u << nown) - 1u);
-        walk_rows_pay<kWalkU>([&](int32_t e) {
+        walk_rows_pay<kWalkU, APL == 8>([&](int32_t e) {
                                   AMBER_DCHECK(e >= 0 && e < a.row_ptr[a.n], "SIR push: arc index out of the CSR");
                                   return static_cast<uint32_t>(__ldcs(a.col + e));
                               }, own, rb, re, id,
