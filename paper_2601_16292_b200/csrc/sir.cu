@@ -431,6 +431,48 @@ __device__ __forceinline__ uint32_t recover_nib(const SirStepArgs& a, unsigned l
     return out;
 }
 
+// recover_nib for APL = 8 with the warp's Philox blocks compacted: the lanes'
+// 4-agent groups holding an infected agent are listed in shared memory (ids /
+// infected nibbles, scratch rb / re of the warp's queue slot, which the push
+// queue does not use) and drawn 32 per round, one block per lane, instead of
+// every lane running both of its blocks whenever any lane of the warp needs
+// one (SIMT).  Same draws (R4: word i & 3 of block i / 4).  Push steps with
+// sparse infected sets: V2 r02 ncu, recovery draws ~1/6 of a push step's
+// instructions.  i0: the lane's first global id (a multiple of 8).
+__device__ __forceinline__ uint32_t recover_nib8_compact(const SirStepArgs& a, unsigned long long i0, uint32_t t,
+                                                         uint32_t inf, int32_t* ids, int32_t* res)
+{
+    const int lane = threadIdx.x & 31;
+    const uint32_t p0 = inf & 0xfu, p1 = (inf >> 4) & 0xfu;
+    const uint32_t m0 = __ballot_sync(0xffffffffu, p0 != 0), m1 = __ballot_sync(0xffffffffu, p1 != 0);
+    const uint32_t c0 = __popc(m0), cnt = c0 + __popc(m1);
+    if (!cnt) return 0u;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t r0 = __popc(m0 & lt), r1 = c0 + __popc(m1 & lt);
+    const int32_t g = static_cast<int32_t>(i0 >> 2);
+    if (p0) { ids[r0] = g; res[r0] = static_cast<int32_t>(p0); }
+    if (p1) { ids[r1] = g + 1; res[r1] = static_cast<int32_t>(p1); }
+    __syncwarp();
+    for (uint32_t k = lane; k < cnt; k += 32) {
+        const uint32_t part = static_cast<uint32_t>(res[k]);
+        const uint4 r = stream_block(a.key, TAG_SIR_REC, static_cast<unsigned long long>(static_cast<uint32_t>(ids[k])), t);
+        uint32_t out = 0;
+        if ((part & 1u) && r.x < a.t_gamma) out |= 1u;
+        if ((part & 2u) && r.y < a.t_gamma) out |= 2u;
+        if ((part & 4u) && r.z < a.t_gamma) out |= 4u;
+        if ((part & 8u) && r.w < a.t_gamma) out |= 8u;
+        res[k] = static_cast<int32_t>(out);
+    }
+    __syncwarp();
+    const uint32_t out = (p0 ? static_cast<uint32_t>(res[r0]) : 0u) | ((p1 ? static_cast<uint32_t>(res[r1]) : 0u) << 4);
+    __syncwarp();  // the scratch is rewritten by the next chunk
+    return out;
+}
+
+// Bit k of m (k < 4) -> byte k (0 or 1) of a 32-bit word.
+static_assert(kS == 0 && kI == 1 && kR == 2, "the byte-parallel state deltas assume these codes");
+__device__ __forceinline__ uint32_t spread4(uint32_t m) { return ((m & 0xfu) * 0x00204081u) & 0x01010101u; }
+
 // Exclusive warp prefix sum; *total = the warp's sum.
 __device__ __forceinline__ uint32_t warp_excl(uint32_t v, uint32_t* total)
 {
@@ -470,9 +512,7 @@ __device__ __forceinline__ uint32_t queue_owners(SirSmem& sm, uint32_t qn, uint3
     uint32_t T;
     uint32_t k = qn + warp_excl(__popc(nib), &T);
     if (!kRows) {
-#pragma unroll
-        for (int q = 0; q < APL; ++q)
-            if ((nib >> q) & 1u) sm.id[wq][k++] = id_base + q;
+        for (uint32_t m = nib; m; m &= m - 1u) sm.id[wq][k++] = id_base + __ffs(static_cast<int>(m)) - 1;
         return T;
     }
     if (nib) {
@@ -726,9 +766,24 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
         }
         if (!__any_sync(0xffffffffu, nons != 0)) return;
         // owners: recoveries and the new state of every non-S agent
-        const uint32_t recnib = recover_nib<APL>(a, static_cast<unsigned long long>(i0), t, nib_i);
+        uint32_t recnib;
+        if constexpr (APL == 8) recnib = recover_nib8_compact(a, static_cast<unsigned long long>(i0), t, nib_i, sm.rb[wq], sm.re[wq]);
+        else recnib = recover_nib<APL>(a, static_cast<unsigned long long>(i0), t, nib_i);
         rec += __popc(recnib);
-        if (nons) {
+        if (APL == 8 && !a.digest) {
+            // the same per-word deltas as below, byte-parallel: bit k of a
+            // nibble -> byte k; codes S 0, I 1, R 2
+            if (nons) {
+                const uint32_t surv = nib_i & ~recnib;
+                const uint32_t oi = nons & ~b_s & b_i, orr = nons & ~b_s & ~b_i;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t nw = spread4((nons & surv) >> (4 * h)) + 2u * spread4((nons & ~surv) >> (4 * h));
+                    const uint32_t old = spread4(oi >> (4 * h)) + 2u * spread4(orr >> (4 * h));
+                    if (nw != old) atomicAdd(yw + (i0 >> 2) + h, nw - old);
+                }
+            }
+        } else if (nons) {
             // the lane's bytes sit in one 32-bit word (two for APL 8; i0 is a
             // multiple of APL).  One signed delta per 32-bit word, applied with a
             // 32-bit atomicAdd: exact mod 2^32 because every byte starts and ends

@@ -365,21 +365,24 @@ def test_apl8_push_counts_deferred(orc, direction):
 
 @pytest.mark.parametrize("kbar", [1.5, 3.0, 24.0])
 @pytest.mark.parametrize("direction", [1, 2])
-def test_apl8_walk_owner_lookup_sparse_and_dense(orc, kbar, direction):
+@pytest.mark.parametrize("digest", [0, 1])
+def test_apl8_walk_owner_lookup_sparse_and_dense(orc, kbar, direction, digest):
     # the 8-agents-per-lane walk looks owners up by row-end bits when the
     # non-empty rows form a lane prefix and falls back to the shuffle search
     # otherwise: sparse graphs (many empty rows, both lookups in one run) and
     # dense ones (rows spanning several 128-arc windows) must both equal the
-    # oracle at every step
+    # oracle at every step.  digest 0 also runs the push chunk pass's
+    # compacted recovery draws and byte-parallel state deltas.
     cfg = dict(n=70_001, mean_degree=kbar, beta=0.3, gamma=0.1, init_frac=0.02, seed=int(kbar * 10) + direction)
     m = make(cfg)
     m.set_option("apl", 8)
     m.set_option("direction", direction)
-    m.set_option("digest", 1)
+    m.set_option("digest", digest)
     rp, col = oracle_graph(orc, m, cfg)
     x = orc.sir_init(cfg["n"], sir_counts(cfg)[1], cfg["seed"])
     for t in range(8):
         m.step(1)
         x = orc.sir_step(rp, col, x, cfg["seed"], t, cfg["beta"], cfg["gamma"])
         assert np.array_equal(m.read_column("state"), x), f"step {t}"
+        assert [int(m.metrics(k)[-1]) for k in "SIR"] == [int((x == v).sum()) for v in range(3)], f"step {t}"
     assert m.digest("state") == orc.digest(x)
