@@ -316,6 +316,11 @@ constexpr int kSirMinBLarge = AMBER_SIR_MINB_LARGE;
 constexpr int kChunkMax = 256;
 constexpr int kQCap = 32 + kChunkMax;  // owner queue per warp: < 32 carried + one chunk
 
+// 29 KB per block: the rest of the SM's 256 KB stays L1, which holds the CSR
+// column sectors a walk revisits across its batches.  Measured (r02, V2): a
+// 42 KB struct (12 KB more per block, L1 92 -> 28 KB at five blocks per SM)
+// 1.31 -> 1.93 ms/step; a 21 KB one (two packed queue words, L1 124 KB) no
+// change.
 struct SirSmem {
     int32_t id[kSirPT / 32][kQCap];  // owner: agent offset (pull: in the chunk; push: local agent id)
     int32_t rb[kSirPT / 32][kQCap];  // owner's row [rb, re)
