@@ -63,7 +63,11 @@ __device__ __forceinline__ uint32_t walk_rows_core(C&& col_at, uint32_t own, int
     // instead of the 5-step shuffle search.  Measured (r02): V2 1.354 -> 1.335
     // ms/step; C2 4.94 -> 5.04 us and SIR-in-space 0.172 -> 0.176 ms slower
     // (short walks: the ballot and check cost more than they save), so only
-    // the large-population SIR walk uses it.
+    // the large-population SIR walk uses it.  Also measured and not kept:
+    // compacting the arcs whose probe passed before the draws (full-warp
+    // Philox instead of SIMT utilisation = hit rate): faster only below ~35%
+    // susceptible neighbours in push steps (V2 steps 15-19, which pull), slower
+    // above (compaction cost > saved draws).
     const uint32_t ne = kFast ? __ballot_sync(0xffffffffu, len > 0) : 0u;
     const bool fast = kFast && (ne & (ne + 1u)) == 0u;
     const uint32_t le = 0xffffffffu >> (31 - lane);  // lanes 0 .. lane
