@@ -333,8 +333,9 @@ __host__ __device__ constexpr int64_t sir_chunks(int64_t n_pad, int apl) { retur
 // f(a0, next): next = the base of the chunk this warp processes after a0 when
 // it is already known (-1 otherwise), so the body can prefetch its inputs.
 template <int APL, class F>
-__device__ __forceinline__ void for_chunks(const SirStepArgs& a, uint32_t* q, F&& f)
+__device__ __forceinline__ void for_chunks(const SirStepArgs& a, uint32_t* q, F&& f, int grab = 0)
 {
+    if (!grab) grab = a.grab;
     const int lane = threadIdx.x & 31;
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -347,10 +348,10 @@ __device__ __forceinline__ void for_chunks(const SirStepArgs& a, uint32_t* q, F&
     const int64_t lo = nchunks * r / kRegions, hi = nchunks * (r + 1) / kRegions;
     for (;;) {
         uint32_t c0 = 0;
-        if (lane == 0) c0 = atomicAdd(q + r, static_cast<uint32_t>(a.grab));
+        if (lane == 0) c0 = atomicAdd(q + r, static_cast<uint32_t>(grab));
         c0 = __shfl_sync(0xffffffffu, c0, 0);
         if (lo + c0 >= hi) break;
-        const int64_t e = lo + c0 + a.grab < hi ? lo + c0 + a.grab : hi;
+        const int64_t e = lo + c0 + grab < hi ? lo + c0 + grab : hi;
         for (int64_t c = lo + c0; c < e; ++c) f(c * 32 * APL, c + 1 < e ? (c + 1) * 32 * APL : -1);
     }
 }
@@ -752,6 +753,114 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
             return false;  // an infected agent tries every susceptible neighbour
         });
     };
+    // moves the queue remainder (< 32) to the front after walking full groups
+    auto drain = [&]() {
+        uint32_t g0 = 0;
+        for (; qn - g0 >= 32; g0 += 32) walk(g0, 32);
+        const uint32_t rem = qn - g0;
+        int32_t vi = 0;
+        if (static_cast<uint32_t>(lane) < rem) vi = sm.id[wq][g0 + lane];
+        __syncwarp();
+        if (static_cast<uint32_t>(lane) < rem) sm.id[wq][lane] = vi;
+        __syncwarp();
+        qn = rem;
+    };
+    if (APL == 8 && !a.digest) {
+        // Large populations: the chunk pass one bitmap word (32 agents) per
+        // lane, 1,024 agents per warp chunk -- the per-chunk warp work (loads,
+        // ballots, scans, queue bookkeeping) amortised over 4x the agents of
+        // the 8-agents-per-lane pass below (r02 ncu, V2 push steps at 1-5%
+        // infected: ~300 warp instructions per 256-agent chunk, 40% of the step).
+        // Same draws and the same state / bitmap updates (tests: forced push
+        // at 8 agents per lane, digest off).
+        const int64_t words = a.n_pad >> 5;
+        for_chunks<32>(a, queue_of(a, t, 1), [&](int64_t a0, int64_t) {
+            const int64_t w = (a0 >> 5) + lane;
+            const bool ok = w < words;
+            const uint32_t Ws = ok ? sb[w] : 0u, Wi = ok ? ib[w] : 0u;
+            const uint32_t Wbs = ok ? sb_next[w] : 0u, Wbi = ok ? ib_next[w] : 0u;
+            const int64_t left = a.n - 32 * w;
+            const uint32_t real = !ok || left <= 0 ? 0u : (left >= 32 ? 0xffffffffu : (1u << left) - 1u);
+            const uint32_t nons = real & ~Ws;
+            if (!__any_sync(0xffffffffu, nons != 0)) return;
+            const uint32_t inf_now = Wi & real;
+            // recoveries (R4: word i & 3 of block i / 4): the 4-agent groups
+            // holding an infected agent, compacted over the warp (queue words
+            // rb / re as scratch), drawn 32 per round
+            uint32_t x = inf_now | (inf_now >> 1);
+            x = (x | (x >> 2)) & 0x11111111u;
+            x = (x | (x >> 3)) & 0x03030303u;
+            x = (x | (x >> 6)) & 0x000f000fu;
+            const uint32_t gm = (x | (x >> 12)) & 0xffu;  // bit g: group g of the word has an infected agent
+            uint32_t T;
+            const uint32_t off = warp_excl(__popc(gm), &T);
+            uint32_t recw = 0;
+            if (T) {
+                uint32_t k = off;
+                for (uint32_t m = gm; m; m &= m - 1u, ++k) {
+                    const int g = __ffs(static_cast<int>(m)) - 1;
+                    sm.rb[wq][k] = static_cast<int32_t>(8 * w + g);
+                    sm.re[wq][k] = static_cast<int32_t>((inf_now >> (4 * g)) & 0xfu);
+                }
+                __syncwarp();
+                for (uint32_t e = lane; e < T; e += 32) {
+                    const uint32_t part = static_cast<uint32_t>(sm.re[wq][e]);
+                    const uint4 r = stream_block(a.key, TAG_SIR_REC,
+                                                 static_cast<unsigned long long>(static_cast<uint32_t>(sm.rb[wq][e])), t);
+                    uint32_t o = 0;
+                    if ((part & 1u) && r.x < a.t_gamma) o |= 1u;
+                    if ((part & 2u) && r.y < a.t_gamma) o |= 2u;
+                    if ((part & 4u) && r.z < a.t_gamma) o |= 4u;
+                    if ((part & 8u) && r.w < a.t_gamma) o |= 8u;
+                    sm.re[wq][e] = static_cast<int32_t>(o);
+                }
+                __syncwarp();
+                k = off;
+                for (uint32_t m = gm; m; m &= m - 1u, ++k)
+                    recw |= static_cast<uint32_t>(sm.re[wq][k]) << (4 * (__ffs(static_cast<int>(m)) - 1));
+                __syncwarp();  // the scratch is rewritten by the next chunk
+            }
+            rec += __popc(recw);
+            const uint32_t surv = inf_now & ~recw;
+            if (ok && nons) {
+                // state bytes of the agents whose next state differs from B's
+                // (new: I survivors and R; B: S, I or R), one delta per 4-agent word
+                const uint32_t chg = nons & (Wbs | (Wbi & ~surv));
+                uint32_t cg = chg | (chg >> 1);
+                cg = (cg | (cg >> 2)) & 0x11111111u;
+                cg = (cg | (cg >> 3)) & 0x03030303u;
+                cg = (cg | (cg >> 6)) & 0x000f000fu;
+                cg = (cg | (cg >> 12)) & 0xffu;
+                const uint32_t oi = ~Wbs & Wbi, orr = ~Wbs & ~Wbi;
+                for (uint32_t m = cg; m; m &= m - 1u) {
+                    const int g = __ffs(static_cast<int>(m)) - 1;
+                    const uint32_t c4 = chg >> (4 * g);
+                    const uint32_t nw = spread4(c4 & (surv >> (4 * g))) + 2u * spread4(c4 & ~(surv >> (4 * g)));
+                    const uint32_t old = spread4(c4 & (oi >> (4 * g))) + 2u * spread4(c4 & (orr >> (4 * g)));
+                    atomicAdd(yw + 8 * w + g, nw - old);
+                }
+                // B's bits of the non-S agents -> survivors / cleared S
+                const uint32_t flip = (Wbi ^ surv) & nons;
+                if (flip) atomicXor(ib_next + w, flip);
+                if (Wbs & nons) atomicAnd(sb_next + w, ~nons);
+            }
+            // pushers: queued in rounds of at most 8 per lane (queue capacity:
+            // < 32 carried + 256), walked whenever 32 are queued
+            uint32_t m = inf_now;
+            while (__any_sync(0xffffffffu, m != 0)) {
+                const uint32_t cnt = min(__popc(m), 8);
+                uint32_t tot;
+                uint32_t k = qn + warp_excl(cnt, &tot);
+                for (uint32_t i = 0; i < cnt; ++i, m &= m - 1u)
+                    sm.id[wq][k++] = static_cast<int32_t>(32 * w + __ffs(static_cast<int>(m)) - 1);
+                qn += tot;
+                __syncwarp();
+                if (qn >= 32) drain();
+            }
+        }, a.grab > 4 ? a.grab / 4 : 1);
+        if (qn) walk(0, qn);
+        return;
+    }
     for_chunks<APL>(a, queue_of(a, t, 1), [&](int64_t a0, int64_t) {
         const int64_t i0 = a0 + APL * lane;
         // current state and back state B from the bitmaps (L2-resident, four
@@ -824,16 +933,7 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
         if (!__any_sync(0xffffffffu, nib_i != 0)) return;
         qn += queue_owners<APL, false>(sm, qn, nib_i, static_cast<int32_t>(i0));
         __syncwarp();
-        if (qn < 32) return;
-        uint32_t g0 = 0;
-        for (; qn - g0 >= 32; g0 += 32) walk(g0, 32);
-        const uint32_t rem = qn - g0;
-        int32_t vi = 0;
-        if (static_cast<uint32_t>(lane) < rem) vi = sm.id[wq][g0 + lane];
-        __syncwarp();
-        if (static_cast<uint32_t>(lane) < rem) sm.id[wq][lane] = vi;
-        __syncwarp();
-        qn = rem;
+        if (qn >= 32) drain();
     });
     if (qn) walk(0, qn);
 }
@@ -884,8 +984,10 @@ __global__ void __launch_bounds__(kSirPT, APL == 8 ? kSirMinBLarge : kSirMinB) s
             prev_r = pv->R;
             // per traversed agent a push costs ~1.35x a pull (every arc of a
             // pusher is walked, with a draw per S neighbour; pullers stop at
-            // their first transmission): V2, tools/v2_steps.py
-            push = a.dir == 0 ? 4 * prev_i < 3 * prev_s : a.dir == 2;
+            // their first transmission): V2, tools/v2_steps.py (r01).  At 8
+            // agents per lane (r02 push chunk pass) ~1.1x: V2 step 15 (I/S =
+            // 0.87) pushes in 2.70 ms vs 2.79 pulling, step 16 (1.09) 2.83 vs 2.40
+            push = a.dir == 0 ? (APL == 8 ? 10 * prev_i < 9 * prev_s : 4 * prev_i < 3 * prev_s) : a.dir == 2;
         }
         if (push) {
             long long rec = 0, inf = 0;
