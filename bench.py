@@ -398,7 +398,7 @@ def bench_configs(hbm):
                  "active_updates": st["active_updates"], "build_ms": st["build_ms"],
                  "sampled_replicates_bit_exact_vs_oracle": bool(np.array_equal(res[pick], want)),
                  "roof": {"bound": "issue", "why": "graphs and states resident in shared memory for all 300 steps; "
-                          "HBM only for the one-time load", "evidence": "profiles/r01_sweep_ncu.txt"},
+                          "HBM only for the one-time load", "evidence": "profiles/r02_sweep_ncu.txt"},
                  "oracle": {"value": orate, "unit": UNIT, "cores": 1,
                             "sample": f"{len(pick)} of {len(betas)} replicates spanning all betas"},
                  "oracle_all_cores": {"value": orate_all, "unit": UNIT, "cores": ncpu,
@@ -427,7 +427,7 @@ def bench_configs(hbm):
                  "roof": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                           "alg_rule": "2 B/agent + (8 + 5 kbar) B per agent of the smaller of S, I",
                           "binding": "random L2 neighbour-bitmap probes, one per traversed arc",
-                          "evidence": "profiles/r02_v2_sir_ncu.txt"},
+                          "evidence": "profiles/r02_v2_sir_ncu.txt, profiles/r02_v2_push_step_ncu.txt, profiles/r02_v2_steps.json"},
                  "oracle": {"value": orate, "unit": UNIT, "cores": 1,
                             "sample": f"the same model at N={n_o:.0e} (mean degree 10), 20 steps"}}
 
@@ -471,7 +471,8 @@ def boids_roof(m, ms_per_step, which):
             "kernel_ms": prof, "peak_source": "profiles/r02_alu_ceiling.txt (tools/alu_ceiling.cu, "
                                                f"{'pre-quantised' if qv else 'float'}-velocity stencil)",
             "why": "FP32 + int64 fixed-point stencil; memory latency hidden in the ceiling",
-            "evidence": f"profiles/r0{'2' if which == 'V3' else '1'}_{which.lower()}_boids_group_ncu.txt"}
+            "evidence": ("profiles/r02_v3_boids_group_final_ncu.txt" if which == "V3"
+                         else "profiles/r01_c3_boids_group_ncu.txt")}
 
 
 # ------------------------------------------------------------------ GPU arm
