@@ -429,8 +429,18 @@ __global__ void __launch_bounds__(1024) boids_scatter_scan_kernel(
 {
     __shared__ __align__(16) int ss[(kScanSmemCells + 16) & ~15];
     __shared__ int wsum[32];
+    pdl_wait();  // launched with launch_pdl: the previous step's stencil must be complete
+    pdl_trigger();
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int total = ncell + 1;  // cnt[ncell] = 0, so start[ncell] = n
+    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + tid, nt = (int64_t)gridDim.x * blockDim.x;
+    // the first round's agent loads are issued before the scan (C3: one round)
+    float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f);
+    int32_t id0 = 0;
+    if (gt < n) {
+        x0 = st[gt];
+        id0 = ids[gt];
+    }
     const int c0 = tid * 16;
     int v[16];
     if (c0 < total) {  // cs >= c0 + 16: the padded row
@@ -485,7 +495,6 @@ __global__ void __launch_bounds__(1024) boids_scatter_scan_kernel(
             }
         }
     }
-    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + tid, nt = (int64_t)gridDim.x * blockDim.x;
     for (int64_t c = gt; c < cs / 4; c += nt) {
         reinterpret_cast<int4*>(cnt_zero)[c] = make_int4(0, 0, 0, 0);
         reinterpret_cast<int4*>(fill_zero)[c] = make_int4(0, 0, 0, 0);
@@ -497,7 +506,7 @@ __global__ void __launch_bounds__(1024) boids_scatter_scan_kernel(
         float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
         int c = -1;
         if (p < n) {
-            x = st[p];
+            x = r == 0 ? x0 : st[p];
             c = cell_coord(x.y, a) * a.ncx + cell_x(x.x, a);
         }
         int head, rank, len;
@@ -514,7 +523,7 @@ __global__ void __launch_bounds__(1024) boids_scatter_scan_kernel(
             } else {
                 sorted[q] = x;
             }
-            sorted_ids[q] = ids[p];
+            sorted_ids[q] = r == 0 ? id0 : ids[p];
         }
     }
 }
@@ -826,6 +835,8 @@ __global__ void __launch_bounds__(256, MINB) boids_group_kernel(const float4* __
                                                           BoidsSlot* slot, int digest, int* __restrict__ next_cnt,
                                                           int* __restrict__ next_cell, const float2* __restrict__ svel)
 {
+    pdl_wait();  // launched with launch_pdl: the binning pass must be complete
+    pdl_trigger();
     boids_group_body<G, QV>(sorted, sids, start, n, a, out, out_ids, slot, digest, next_cnt, next_cell, svel);
 }
 
@@ -1321,10 +1332,9 @@ public:
                         const int gs = grid ? static_cast<int>(grid)
                                             : static_cast<int>(std::max<int64_t>(
                                                   1, std::min<int64_t>(ceil_div(n, 1024), rt.num_sms)));
-                        boids_scatter_scan_kernel<<<gs, 1024, 0, rt.stream>>>(
-                            st.p, ids.p, n, cnt_of(spar), cnt_of(spar ^ 1), fill.p + spar * cs,
-                            fill.p + (spar ^ 1) * cs, ncell, cs, start.p, sorted.p, sids.p,
-                            qv_now() ? svel.p : nullptr, ba);
+                        launch_pdl(boids_scatter_scan_kernel, gs, 1024, 0, rt.stream, st.p, ids.p, n, cnt_of(spar),
+                                   cnt_of(spar ^ 1), fill.p + spar * cs, fill.p + (spar ^ 1) * cs, ncell, cs,
+                                   start.p, sorted.p, sids.p, qv_now() ? svel.p : nullptr, ba);
                     });
                     check_launch("boids_scatter_scan_kernel");
                 } else {
@@ -1371,8 +1381,8 @@ public:
                     int* nc_cnt = ba.nc > 1 && n <= fused_count_max ? cnt_of(spar ^ 1) : nullptr;
                     const bool qv = qv_now();
 #define AMBER_BOIDS_GROUP(G_, QV_, MB_)                                                                          \
-    boids_group_kernel<G_, QV_, MB_><<<g, threads, 0, rt.stream>>>(sorted.p, sids.p, start.p, n, a, st.p, ids.p, sl, \
-                                                                   dg, nc_cnt, nullptr, svel.p)
+    launch_pdl(boids_group_kernel<G_, QV_, MB_>, g, threads, 0, rt.stream, sorted.p, sids.p, start.p, n, a, st.p, \
+               ids.p, sl, dg, nc_cnt, static_cast<int*>(nullptr), svel.p)
 #define AMBER_BOIDS_GROUP4(QV_)                                                  \
     if (n > (1ll << 22)) AMBER_BOIDS_GROUP(4, QV_, AMBER_BOIDS_MINB_LARGE); \
     else AMBER_BOIDS_GROUP(4, QV_, AMBER_BOIDS_MINB)

@@ -55,6 +55,39 @@ inline bool sync_debug()
     return on;
 }
 
+// Programmatic dependent launch (PDL, sm_90+): a kernel launched with
+// launch_pdl may start (be scheduled, run its prologue) while the previous
+// kernel on the stream still runs; pdl_wait() -- griddepcontrol.wait -- blocks
+// until that kernel has completed and its writes are visible, so such kernels
+// call it before their first global memory access, then pdl_trigger() to let
+// their own successor be scheduled.  Without the launch attribute both are
+// no-ops.  AMBER_PDL=0 launches normally (A/B measurements).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+inline bool pdl_on()
+{
+    static const bool on = [] {
+        const char* e = getenv("AMBER_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+template <class... KArgs, class... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s, Args... args)
+{
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_on() ? 1 : 0;
+    AMBER_CUDA(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
+}
+
 // Check the last launch (launch-config errors surface here, faults later --
 // or here, under AMBER_SYNC_DEBUG).
 inline void check_launch(const char* what)
