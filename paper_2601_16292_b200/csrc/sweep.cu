@@ -105,6 +105,10 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
     __shared__ int cnt_s[2][2];  // [parity][I, S]
     const int tid = threadIdx.x, nt = blockDim.x;
     const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+    // (Measured, not kept, r02: the push's owner scan from an infected-agent
+    // bitmap written by the copy pass, one set bit per lane per round over 32
+    // words: C5 28.1 vs 24.3 ms -- a round per owner rank costs more than the
+    // byte load + ballot per 32 agents it replaces.)
     // 32-bit indices inside a replicate (its state lives in shared memory, so
     // n_pad < 2^17; 64-bit loop counters cost two instructions per compare /
     // increment: C5 25.5 -> 24.1 ms)
