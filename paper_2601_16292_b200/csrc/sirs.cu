@@ -153,16 +153,18 @@ __global__ void __launch_bounds__(256) sirs_persistent_kernel(const SirsArgs a)
     cg::grid_group grid = cg::this_grid();
     int cur = a.cur;
     const int lane = threadIdx.x & 31;
-    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    // 32-bit agent indices (n < 2^31: int32 CSR)
+    const int gw = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+    const int n = static_cast<int>(a.n), n_pad = static_cast<int>(a.n_pad);
     for (int64_t k = 0; k < a.steps; ++k) {
         const uint32_t t = a.t0 + static_cast<uint32_t>(k);
         const uint8_t* x = a.x[cur];
         uint8_t* y = a.x[cur ^ 1];
         unsigned long long cnt[4] = {0, 0, 0, 0};
-        for (int64_t a0 = gw * 32; a0 < a.n_pad; a0 += nw * 32) {
-            const int64_t u = a0 + lane;
-            const bool real = u < a.n;
+        for (int a0 = gw * 32; a0 < n_pad; a0 += nw * 32) {
+            const int u = a0 + lane;
+            const bool real = u < n;
             const uint8_t st = x[u];
             const uint32_t s_mask = __ballot_sync(0xffffffffu, real && st == kS);
             uint32_t exposed = 0;
