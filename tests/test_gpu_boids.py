@@ -281,3 +281,36 @@ def test_v3_full_size_region_vs_oracle(orc):
     got = state(m)
     for g, o in zip(got, sub):
         assert np.array_equal(g[win[core]].view(np.uint32), o[core].view(np.uint32))
+
+
+def test_pdl_off_and_on_both_equal_the_oracle(orc, tmp_path):
+    # the scatter-scan and stencil kernels are launched with programmatic
+    # dependent launch and wait on the device for their predecessor; with
+    # AMBER_PDL=0 (fixed per process) they launch normally.  Both must equal the
+    # oracle at every checked step.
+    import os
+    import subprocess
+    import sys
+    cfg = dict(C3_BOIDS, n=20_000, L=450.0, seed=41)
+    steps = 12
+    out = tmp_path / "cols.npz"
+    code = (
+        "import numpy as np, sys\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "from paper_2601_16292_b200 import Model, boids_params\n"
+        f"m = Model('boids', {cfg['n']}, boids_params(*{[cfg[k] for k in KEYS]!r}), {cfg['seed']})\n"
+        f"m.step({steps})\n"
+        f"np.savez({str(out)!r}, *[m.read_column(c) for c in ('pos_x', 'pos_y', 'vel_x', 'vel_y')])\n")
+    env = dict(os.environ, AMBER_PDL="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    m = make(cfg)
+    st = oinit(orc, cfg, m)
+    P = oparams(orc, cfg)
+    m.step(steps)
+    for _ in range(steps):
+        st = orc.boids_step(st, P)
+    off = np.load(out)
+    for k, (a, b) in enumerate(zip(state(m), st)):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), "PDL on"
+        assert np.array_equal(off[f"arr_{k}"].view(np.uint32), b.view(np.uint32)), "PDL off"
