@@ -954,6 +954,31 @@ __device__ __forceinline__ void sir_count_new(const SirStepArgs& a, int cur, Sir
     block_sum_atomic<2>(v, outs);
 }
 
+// The identity steps at the end of an epidemic (sir_persistent_kernel): records
+// of the `rem` remaining steps repeat the current counts; an odd remainder
+// copies the state to the other buffer set.  Out of line, so the step loop's
+// register allocation does not carry it (inlined, it added spills to every
+// variant).
+__device__ __noinline__ void sir_identity_tail(SirSlot* ring, int64_t cap, const SirSlot* pv, uint32_t t, int64_t rem,
+                                               int digest, const uint8_t* x, uint8_t* y, const uint32_t* ib,
+                                               uint32_t* ib_o, const uint32_t* sb, uint32_t* sb_o, int64_t n_pad)
+{
+    const SirSlot v{pv->S, 0ull, pv->R, digest ? pv->digest : 0ull};
+    if (blockIdx.x == 0)  // rem <= ring_cap - 1: slot t - 1 is not overwritten
+        for (int64_t j = threadIdx.x; j < rem; j += blockDim.x) ring[(t + j) % cap] = v;
+    if (rem & 1) {
+        const int64_t g0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
+        const uint32_t* xs = reinterpret_cast<const uint32_t*>(x);
+        uint32_t* xd = reinterpret_cast<uint32_t*>(y);
+        for (int64_t i = g0; i < n_pad / 4; i += gs) xd[i] = xs[i];
+        for (int64_t w = g0; w < n_pad / 32; w += gs) {
+            ib_o[w] = ib[w];
+            sb_o[w] = sb[w];
+        }
+    }
+}
+
 // All n_steps steps in one cooperative launch (grid barrier between steps).
 // Direction-optimizing: step k pushes from the infected agents when they are
 // fewer than 3/4 of the susceptible ones (counts of the previous step from its ring
@@ -988,6 +1013,19 @@ __global__ void __launch_bounds__(kSirPT, APL == 8 ? kSirMinBLarge : kSirMinB) s
             // agents per lane (r02 push chunk pass) ~1.1x: V2 step 15 (I/S =
             // 0.87) pushes in 2.70 ms vs 2.79 pulling, step 16 (1.09) 2.83 vs 2.40
             push = a.dir == 0 ? (APL == 8 ? 10 * prev_i < 9 * prev_s : 4 * prev_i < 3 * prev_s) : a.dir == 2;
+        }
+        if (prev_i == 0 && (k > 0 || a.prev_ok || (a.prev0 && !a.digest))) {
+            // No infected agent: nothing can transmit or recover, so this step and
+            // every later one of the launch is the identity (the epidemic is over;
+            // C2: steps 124-199).  Their records repeat the current counts (and
+            // digest); if an odd number of steps remains, the state is copied to
+            // the other buffer set, where the host expects it after the launch
+            // (both sets then hold it, which keeps the push's back-buffer invariant).
+            // All blocks read the same slot after the last barrier, so all leave here.
+            const SirSlot* pv = k == 0 && a.prev0 ? a.prev0 : a.ring + ((t + a.ring_cap - 1) % a.ring_cap);
+            sir_identity_tail(a.ring, a.ring_cap, pv, t, a.n_steps - k, a.digest, a.x[cur], a.x[cur ^ 1], a.ib[cur],
+                              a.ib[cur ^ 1], a.sb[cur], a.sb[cur ^ 1], a.n_pad);
+            return;
         }
         if (push) {
             long long rec = 0, inf = 0;

@@ -386,3 +386,40 @@ def test_apl8_walk_owner_lookup_sparse_and_dense(orc, kbar, direction, digest):
         assert np.array_equal(m.read_column("state"), x), f"step {t}"
         assert [int(m.metrics(k)[-1]) for k in "SIR"] == [int((x == v).sum()) for v in range(3)], f"step {t}"
     assert m.digest("state") == orc.digest(x)
+
+
+@pytest.mark.parametrize("digest", [0, 1])
+@pytest.mark.parametrize("apl", [1, 8])
+def test_epidemic_end_identity_steps(orc, digest, apl):
+    # once no agent is infected every further step is the identity; the
+    # persistent launch records those steps' counts without a pass and leaves
+    # early (copying the state to the other buffer set when an odd number of
+    # steps remains).  Calls of odd and even lengths across the end of the
+    # epidemic, then a write that re-seeds infections (the push runs on the
+    # back buffers again): every step equals the oracle.
+    cfg = dict(n=20_011, mean_degree=3.0, beta=0.08, gamma=0.45, init_frac=0.01, seed=3)
+    m = make(cfg)
+    m.set_option("apl", apl)
+    m.set_option("digest", digest)
+    rp, col = oracle_graph(orc, m, cfg)
+    x = orc.sir_init(cfg["n"], sir_counts(cfg)[1], cfg["seed"])
+    t = 0
+    saw_zero = False
+    for chunk in (5, 9, 1, 12, 3, 7, "write", 2, 11, 4, 1, 9):
+        if chunk == "write":
+            w = x.copy()
+            w[::1013] = 1  # re-seed: ~20 infected agents
+            m.write_column("state", w)
+            x = w
+            continue
+        m.step(chunk)
+        x, counts, _ = orc.sir_run(rp, col, x, cfg["seed"], cfg["beta"], cfg["gamma"], t, chunk)
+        t += chunk
+        assert np.array_equal(m.read_column("state"), x), f"step {t}"
+        for k, name in enumerate("SIR"):
+            assert np.array_equal(m.metrics(name)[-chunk:], counts[:, k]), (name, t)
+        saw_zero |= bool((counts[:, 1] == 0).any())
+        if digest:
+            assert m.digest("state") == orc.digest(x)
+            assert int(m.metrics("digest")[-1]) == orc.digest(x)
+    assert saw_zero
