@@ -657,7 +657,9 @@ __device__ __forceinline__ void boids_group_body(const float4* __restrict__ sort
     // the stencil's rows stay in this SM's L1 instead of being fetched by a
     // different SM every round
     // (large populations only: at C3's 1e5 agents -- two rounds per block -- the
-    // grid-strided order measured faster, 54 vs 58 us)
+    // grid-strided order measured faster, 54 vs 58 us; dealing the warps' chunks
+    // to the blocks round-robin, so each block samples the whole box, 57 vs 44 us
+    // in r02: the block's warps share L1 lines only when they are neighbours)
     const int64_t apb = blockDim.x / G;  // agents per block per round
     const int64_t ng = apb * gridDim.x;
     const int64_t rounds = (n + ng - 1) / ng;  // uniform: every lane runs every round (shuffles)
