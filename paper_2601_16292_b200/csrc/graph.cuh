@@ -135,11 +135,11 @@ __device__ __forceinline__ uint32_t walk_rows(C&& col_at, uint32_t own, int32_t 
 
 // walk_rows with a neighbour probe (see walk_rows_core): test(j, e, owner)
 // runs only where probe(j) != 0.
-template <int kU, class C, class P, class T>
+template <int kU, bool kFast = false, class C, class P, class T>
 __device__ __forceinline__ uint32_t walk_rows_probe(C&& col_at, uint32_t own, int32_t rb, int32_t re, P&& probe,
                                                     T&& test)
 {
-    return walk_rows_core<kU, false, false>(col_at, own, rb, re, 0u, probe, test);
+    return walk_rows_core<kU, false, kFast>(col_at, own, rb, re, 0u, probe, test);
 }
 
 // walk_rows with a per-owner payload: test(j, e, owner, pay_of_owner).  Used

@@ -151,8 +151,9 @@ __device__ __forceinline__ uint32_t lane32_word(const uint4& w, uint32_t k)
 __global__ void __launch_bounds__(256) sirs_persistent_kernel(const SirsArgs a)
 {
     cg::grid_group grid = cg::this_grid();
+    __shared__ int32_t sq[8][3][32];  // per warp: compacted rows (start, end) and their lanes
     int cur = a.cur;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     // 32-bit agent indices (n < 2^31: int32 CSR)
     const int gw = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
@@ -169,14 +170,31 @@ __global__ void __launch_bounds__(256) sirs_persistent_kernel(const SirsArgs a)
             const uint32_t s_mask = __ballot_sync(0xffffffffu, real && st == kS);
             uint32_t exposed = 0;
             if (s_mask) {
+                // the susceptible lanes' rows compacted to lanes 0 .. k-1 (rank =
+                // popc of the lower S lanes, through shared memory), so the walk
+                // finds arc owners by row-end bits (graph.cuh kFast) instead of
+                // the five-step shuffle search; hits map back to the lanes
                 const bool mine = (s_mask >> lane) & 1u;
-                const int32_t rb = mine ? a.row_ptr[u] : 0, re = mine ? a.row_ptr[u + 1] : 0;
-                exposed = walk_rows_probe<4>([&](int32_t e) { return static_cast<uint32_t>(__ldg(a.col + e)); }, s_mask,
-                                             rb, re, [&](uint32_t j) {
-                                                 AMBER_DCHECK(j < static_cast<uint64_t>(a.n), "SIR-space: contact id >= n");
-                                                 return static_cast<uint32_t>(x[j] == kI);
-                                             },
-                                             [](uint32_t, int32_t, int) { return true; });
+                const int rank = __popc(s_mask & ((1u << lane) - 1u)), cnt = __popc(s_mask);
+                if (mine) {
+                    sq[wq][0][rank] = a.row_ptr[u];
+                    sq[wq][1][rank] = a.row_ptr[u + 1];
+                    sq[wq][2][rank] = lane;
+                }
+                __syncwarp();
+                const bool oc = lane < cnt;
+                const int32_t rb = oc ? sq[wq][0][lane] : 0, re = oc ? sq[wq][1][lane] : 0;
+                const int src = oc ? sq[wq][2][lane] : 0;
+                __syncwarp();  // the next chunk rewrites sq
+                const uint32_t own = cnt == 32 ? 0xffffffffu : (1u << cnt) - 1u;
+                const uint32_t hit = walk_rows_probe<4, true>(
+                    [&](int32_t e) { return static_cast<uint32_t>(__ldg(a.col + e)); }, own, rb, re,
+                    [&](uint32_t j) {
+                        AMBER_DCHECK(j < static_cast<uint64_t>(a.n), "SIR-space: contact id >= n");
+                        return static_cast<uint32_t>(x[j] == kI);
+                    },
+                    [](uint32_t, int32_t, int) { return true; });
+                exposed = __reduce_or_sync(0xffffffffu, ((hit >> lane) & 1u) ? 1u << src : 0u);
             }
             uint8_t o = st;
             if (real && (st == kI || ((exposed >> lane) & 1u))) {
