@@ -61,9 +61,10 @@ __device__ __forceinline__ uint32_t walk_rows_core(C&& col_at, uint32_t own, int
     // q = (#lanes with incl <= q0 - 1) + (#row ends in [q0, q]) -- one OR-reduce
     // of the row-end bits of the 32-position window and a popc per batch,
     // instead of the 5-step shuffle search.  Measured (r02): V2 1.354 -> 1.335
-    // ms/step; C2 4.94 -> 5.04 us and SIR-in-space 0.172 -> 0.176 ms slower
-    // (short walks: the ballot and check cost more than they save), so only
-    // the large-population SIR walk uses it.  Also measured and not kept:
+    // ms/step, C5 24.09 -> 23.90 ms, SIR in space (rows compacted to a lane
+    // prefix first) 0.171 -> 0.166 ms; C2 4.94 -> 5.04 us slower (short walks at
+    // one agent per lane: the ballot and check cost more than they save), so
+    // the small-population SIR walk keeps the search.  Also measured and not kept:
     // compacting the arcs whose probe passed before the draws (full-warp
     // Philox instead of SIMT utilisation = hit rate): faster only below ~35%
     // susceptible neighbours in push steps (V2 steps 15-19, which pull), slower

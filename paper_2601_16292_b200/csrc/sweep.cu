@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
                     const bool mine = static_cast<uint32_t>(lane) < nown;
                     const int32_t rb = mine ? static_cast<int32_t>(rp[qid]) : 0, re = mine ? static_cast<int32_t>(rp[qid + 1]) : 0;
                     const uint32_t own = nown >= 32 ? 0xffffffffu : ((1u << nown) - 1u);
-                    walk_rows_pay<kSweepU>(col_at, own, rb, re, qid,
+                    walk_rows_pay<kSweepU, true>(col_at, own, rb, re, qid,
                                      [&](uint32_t j) { return static_cast<uint32_t>(x[j] == kS && y[j] == kS); },
                                      [&](uint32_t j, int32_t, int, uint32_t ii) {  // y: already hit this step
                         const uint4 w = philox(make_uint4(min(ii, j), max(ii, j), static_cast<uint32_t>(t), TAG_SIR_TX), key);
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(1024, 1) sir_sweep_kernel(const SweepArgs a)
                     const bool mine = static_cast<uint32_t>(lane) < nown;
                     const int32_t rb = mine ? static_cast<int32_t>(rp[qid]) : 0, re = mine ? static_cast<int32_t>(rp[qid + 1]) : 0;
                     const uint32_t own = nown >= 32 ? 0xffffffffu : ((1u << nown) - 1u);
-                    const uint32_t hit = walk_rows_pay<kSweepU>(col_at, own, rb, re, qid,
+                    const uint32_t hit = walk_rows_pay<kSweepU, true>(col_at, own, rb, re, qid,
                                                           [&](uint32_t j) { return static_cast<uint32_t>(x[j] == kI); },
                                                           [&](uint32_t j, int32_t, int, uint32_t ii) {
                         const uint4 w = philox(make_uint4(min(ii, j), max(ii, j), static_cast<uint32_t>(t), TAG_SIR_TX), key);
