@@ -423,3 +423,22 @@ def test_epidemic_end_identity_steps(orc, digest, apl):
             assert m.digest("state") == orc.digest(x)
             assert int(m.metrics("digest")[-1]) == orc.digest(x)
     assert saw_zero
+
+
+def test_identity_steps_with_small_ring(orc):
+    # identity steps across several persistent launches of one call (metrics
+    # capacity 16: 15 steps per launch), the records of the last 16 steps checked
+    cfg = dict(n=20_011, mean_degree=3.0, beta=0.08, gamma=0.45, init_frac=0.01, seed=3)
+    m = make(cfg)
+    m.set_option("metrics_capacity", 16)
+    m.set_option("digest", 1)
+    rp, col = oracle_graph(orc, m, cfg)
+    x = orc.sir_init(cfg["n"], sir_counts(cfg)[1], cfg["seed"])
+    m.step(47)
+    x, counts, _ = orc.sir_run(rp, col, x, cfg["seed"], cfg["beta"], cfg["gamma"], 0, 47)
+    assert counts[-1, 1] == 0
+    assert np.array_equal(m.read_column("state"), x)
+    for k, name in enumerate("SIR"):
+        assert np.array_equal(m.metrics(name), counts[-16:, k]), name
+    assert m.digest("state") == orc.digest(x)
+    assert int(m.metrics("digest")[-1]) == orc.digest(x)
