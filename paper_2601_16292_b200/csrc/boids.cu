@@ -385,9 +385,11 @@ __global__ void boids_scatter_kernel(const float4* __restrict__ st, const int32_
     for (int64_t r = 0; r < rounds; ++r) {  // uniform trip count: the lanes cooperate
         const int64_t p = r * nt + tid;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        int32_t id = 0;
         int c = -1;
         if (p < n) {
             v = st[p];
+            id = ids[p];  // issued with the record, not after the cursor claim
             c = cell_of ? cell_of[p] : cell_coord(v.y, a) * a.ncx + cell_x(v.x, a);
         }
         int head, rank, len;
@@ -404,7 +406,7 @@ __global__ void boids_scatter_kernel(const float4* __restrict__ st, const int32_
             } else {
                 sorted[q] = v;
             }
-            sorted_ids[q] = ids[p];
+            sorted_ids[q] = id;
         }
     }
 }
