@@ -75,6 +75,24 @@ __global__ void red_local(unsigned* pool, const int* die_of_sm, const int* pages
     }
 }
 
+// random L2 loads from precomputed lists, 8 independent loads in flight per thread
+__global__ void ld_list(const unsigned* pool, const unsigned* idx0, const unsigned* idx1, const int* die_of_sm,
+                        size_t per_thread_stride, int iters, unsigned* sink)
+{
+    const int d = die_of_sm ? die_of_sm[smid()] : 0;
+    const unsigned* idx = d ? idx1 : idx0;
+    const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    unsigned acc = 0;
+    for (int i = 0; i + 8 <= iters; i += 8) {
+        unsigned v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(pool + idx[(i + u) * per_thread_stride + tid]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    if (acc == 0xDEADBEEFu) sink[0] = acc;
+}
+
 int main()
 {
     const size_t pool_bytes = 64ull << 20;     // 64 MB (32768 pages)
@@ -176,6 +194,18 @@ int main()
         cudaEventRecord(a); red_list<<<grid, thr>>>(pool, d_i0, d_i1, d_die, stride, iters); cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&m2, a, b);
         cudaEventRecord(a); red_list<<<grid, thr>>>(pool, d_i1, d_i0, d_die, stride, iters); cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&m3, a, b);
         printf("list REDs: any %.3f ms  die-local %.3f ms  die-remote %.3f ms\n", m1, m2, m3);
+    }
+    // random 4-byte L2 loads (the SIR walk's neighbour-bitmap probes): does a
+    // die-local replica of a read-only L2-resident array pay?
+    unsigned* d_sink;
+    CK(cudaMalloc(&d_sink, 4));
+    for (int rep = 0; rep < 3; ++rep) {
+        float m1, m2, m3;
+        cudaEventRecord(a); ld_list<<<grid, thr>>>(pool, d_ia, d_ia, nullptr, stride, iters, d_sink); cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&m1, a, b);
+        cudaEventRecord(a); ld_list<<<grid, thr>>>(pool, d_i0, d_i1, d_die, stride, iters, d_sink); cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&m2, a, b);
+        cudaEventRecord(a); ld_list<<<grid, thr>>>(pool, d_i1, d_i0, d_die, stride, iters, d_sink); cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&m3, a, b);
+        printf("list loads %.0f: any %.3f ms (%.2e/s)  die-local %.3f ms (%.2e/s)  die-remote %.3f ms (%.2e/s)\n",
+               (double)total, m1, total / m1 * 1e3, m2, total / m2 * 1e3, m3, total / m3 * 1e3);
     }
     CK(cudaGetLastError());
     return 0;
