@@ -208,6 +208,9 @@ def _sweep_one(job):
     return oracle.sir_sweep(n, kbar, gamma, init_frac, np.array([beta]), np.array([seed], np.uint64), steps)[0]
 
 
+C4_L2 = "state (400 MB int32 column) larger than L2; no flush"
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle timed on the host cores (bounded sample)."""
     import numpy as np
@@ -241,7 +244,7 @@ def run_reference(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": "C4 wealth transfer (BASELINE config 4)", "n_agents": cfg["n"],
-                       "sample_agents": n_s, "seed": cfg["seed"]},
+                       "seed": cfg["seed"], "l2": C4_L2},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"wealth N={n_s} x {args.steps} steps per timed region "
                                        f"(of N={cfg['n']}); host {model}, {ncpu} cpus"},
@@ -636,10 +639,11 @@ def bench_wealth(args):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (seeded Philox population, BASELINE config 4)",
+            # config: the workload only (the reference arm prints the same dict);
+            # how this arm runs it is in parallelism / counter_bits
             "config": {"workload": "C4 wealth transfer (BASELINE config 4)", "n_agents": n,
-                       "seed": cfg["seed"], "parallelism": f"id-sharded x{world}",
-                       "counter_bits": m.get_option("counter_bits"),
-                       "l2": "state (400 MB int32 column) larger than L2; no flush"},
+                       "seed": cfg["seed"], "l2": C4_L2},
+            "parallelism": f"id-sharded x{world}", "counter_bits": m.get_option("counter_bits"),
             "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": hbm,
                          "peak_kind": kind, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": traffic, "traffic_source": traffic_src,
