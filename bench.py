@@ -439,6 +439,16 @@ def bench_configs(hbm):
     i_prev = np.concatenate([[k0], I[:-1]])
     alg = 2.0 * c["n"] * c["steps"] + float((np.minimum(s_prev, i_prev) * (8.0 + 5.0 * arcs / c["n"])).sum())
     ach = alg / (ms / 1e3) / 1e9
+    # the binding roof: one random L2 probe per traversed arc.  Traversed arcs
+    # per step estimated from the previous step's counts and the kernel's
+    # direction rule at 8 agents per lane (push iff 10 I < 9 S: the I agents'
+    # rows, else the S agents'), ignoring the pull's early exits (so the floor
+    # is an upper estimate of the probe work); rate = random 4-byte loads from
+    # an L2-resident array (tools/scatter_probe.cu, profiles/r01_scatter_probe.txt)
+    kbar = arcs / c["n"]
+    walked = np.where(10.0 * i_prev < 9.0 * s_prev, i_prev, s_prev) * kbar
+    probe_rate = 2.776e11
+    floor_ms = float(walked.sum()) / probe_rate * 1e3
     n_o = 1_000_000
     rp, col, _ = oracle.er_graph(n_o, oracle.round_count(n_o * c["mean_degree"] / 2.0), c["seed"])
     st0 = oracle.sir_init(n_o, oracle.round_count(c["init_frac"] * n_o), c["seed"])
@@ -450,6 +460,11 @@ def bench_configs(hbm):
                           "alg_rule": "2 B/agent + (8 + 5 kbar) B per agent of the smaller of S, I",
                           "binding": "random L2 neighbour-bitmap probes, one per traversed arc",
                           "evidence": "profiles/r02_v2_sir_ncu.txt, profiles/r02_v2_push_step_ncu.txt, profiles/r02_v2_steps.json"},
+                 "probe_roof": {"bound": "l2_random_loads", "arcs_walked_per_step_est": float(walked.sum()) / c["steps"],
+                                "peak_loads_per_s": probe_rate, "floor_ms_per_step": floor_ms / c["steps"],
+                                "frac": floor_ms / ms if ms > 0 else None,
+                                "peak_source": "tools/scatter_probe.cu ldg_rand (profiles/r01_scatter_probe.txt)",
+                                "note": "arcs walked estimated from the per-step S/I counts and the direction rule"},
                  "oracle": {"value": orate, "unit": UNIT, "cores": 1,
                             "sample": f"the same model at N={n_o:.0e} (mean degree 10), 20 steps"}}
 
