@@ -23,6 +23,16 @@ namespace {
 #ifndef AMBER_WEALTH_QPT
 #define AMBER_WEALTH_QPT 8
 #endif
+// Sharded-step tunables (r02 ncu launch lists, tools/shard_phase_probe.py, fused
+// step per rank at G = 8 / G = 2): ranks taken when staging 87.3 / 292.7 us vs
+// in a flush pass 90.0 / 301.2; three blocks per SM (80 registers, spills)
+// 85.7-86.2 / 301.6-302.3 -- kept at two (no spills).
+#ifndef AMBER_WEALTH_STAGE_RANK
+#define AMBER_WEALTH_STAGE_RANK 1  // destination ranks taken when staging (shared atomic per append)
+#endif
+#ifndef AMBER_WEALTH_MINB_REMOTE
+#define AMBER_WEALTH_MINB_REMOTE 2
+#endif
 #ifndef AMBER_WEALTH_MINB
 #define AMBER_WEALTH_MINB 1
 #endif
@@ -31,6 +41,14 @@ namespace {
 #endif
 constexpr int kQPT = AMBER_WEALTH_QPT;   // quads (4 agents) per thread per chunk
 constexpr int kChunkAgents = 4 * kQPT * 32;  // agents per warp chunk (512)
+// Remote-bucket slices per destination and the cursor spacing (words).  One
+// cursor per destination took one same-address atomic per warp call and
+// destination: every warp of the grid serialised on world - 1 addresses (r02,
+// tools/shard_phase_probe.py under the ncu launch list: the G = 8 fused step
+// 389 us per rank for 1.25e7 agents, G = 2 1,418 us for 5e7 -- ~0.9 ns per
+// atomic per address).  64 slices on separate 128-byte lines spread them.
+constexpr int kRemoteSlices = 64;
+constexpr int kCountStride = 32;
 
 using Slot = WealthSlot;
 
@@ -50,12 +68,15 @@ struct WealthArgs {
     Slot* slot_apply;    // record of the applied step
     Slot* slot_scatter;  // record receiving the scattered step's increment count
     Slot* slot_zero;     // slot zeroed at kernel start (two steps ahead), may be null
-    // cross-shard receivers (REMOTE): bucket per destination rank
+    // cross-shard receivers (REMOTE): per destination rank, kRemoteSlices
+    // slices (warp chunk c appends to slice c % kRemoteSlices), each with its
+    // own cursor on its own 128-byte line -- see remote_append
     int world;
     unsigned long long shard_size;
-    uint32_t* remote_ids;             // [world][remote_cap] global receiver ids
-    unsigned int* remote_count;       // [world]
-    unsigned long long remote_cap;
+    uint32_t shard_magic;             // 0xFFFFFFFF / shard_size (dest_of: no 64-bit division)
+    uint32_t* remote_ids;             // [world][kRemoteSlices][remote_cap] global receiver ids
+    unsigned int* remote_count;       // [world][kRemoteSlices] cursors, kCountStride words apart
+    unsigned long long remote_cap;    // ids per slice
 };
 
 // ---- packed counters: 4 agents (a quad) own 4*B contiguous bits ----
@@ -135,24 +156,109 @@ __device__ __forceinline__ unsigned long long receiver(unsigned long long x, uns
     return r;
 }
 
-// Warp-aggregated append of a cross-shard receiver into its destination bucket.
-// Must be reached by all 32 lanes (flag selects the participating ones).
-__device__ __forceinline__ void remote_append(const WealthArgs& a, bool flag, unsigned long long r)
+// Owning rank of global id r (sharded runs have ids < 2^32): q = umulhi(r, m)
+// with m = floor((2^32 - 1) / s) is floor(r / s) or one less, fixed by one
+// compare -- the 64-bit division it replaces was 17% of the sharded fused
+// step's instructions (r02 ncu, G = 8).
+__device__ __forceinline__ unsigned dest_of(const WealthArgs& a, unsigned long long r)
+{
+    const uint32_t r32 = static_cast<uint32_t>(r), s32 = static_cast<uint32_t>(a.shard_size);
+    uint32_t q = __umulhi(r32, a.shard_magic);
+    if (r32 - q * s32 >= s32) ++q;
+    return q < static_cast<uint32_t>(a.world) ? q : static_cast<uint32_t>(a.world - 1);
+}
+
+// Warp-aggregated append of a cross-shard receiver into its destination
+// bucket's slice `sl` (the warp chunk's index mod kRemoteSlices; a slice's
+// capacity covers every agent of its chunks, so it cannot overflow).  Must be
+// reached by all 32 lanes (flag selects the participating ones).
+__device__ __forceinline__ void remote_append(const WealthArgs& a, bool flag, unsigned long long r, unsigned sl)
 {
     const unsigned mask = __ballot_sync(0xffffffffu, flag);
     if (!flag) return;
-    unsigned long long d = r / a.shard_size;
-    const unsigned dest = static_cast<unsigned>(d < static_cast<unsigned long long>(a.world) ? d : a.world - 1);
     AMBER_DCHECK(r < a.n_glob, "wealth: remote receiver id >= N");
+    const unsigned dest = dest_of(a, r);
     const unsigned peers = __match_any_sync(mask, dest);
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(peers) - 1;
     const unsigned rank = __popc(peers & ((1u << lane) - 1u));
     unsigned base = 0;
-    if (lane == leader) base = atomicAdd(a.remote_count + dest, static_cast<unsigned>(__popc(peers)));
+    const unsigned long long bucket = static_cast<unsigned long long>(dest) * kRemoteSlices + sl;
+    if (lane == leader) base = atomicAdd(a.remote_count + bucket * kCountStride, static_cast<unsigned>(__popc(peers)));
     base = __shfl_sync(peers, base, leader);
     const unsigned long long pos = base + rank;
-    if (pos < a.remote_cap) a.remote_ids[dest * a.remote_cap + pos] = static_cast<uint32_t>(r);
+    AMBER_DCHECK(pos < a.remote_cap, "wealth: remote bucket slice overflow");
+    if (pos < a.remote_cap) a.remote_ids[bucket * a.remote_cap + pos] = static_cast<uint32_t>(r);
+}
+
+// Warp-staged remote appends (world <= 32): the receivers a warp sends off-shard
+// are queued in shared memory (no global atomic per append) and flushed every
+// kFlushQuads quad rows: per destination ONE cursor atomic for the whole batch
+// (issued by all destination lanes together, so a flush exposes one L2 round
+// trip), then the ids are stored behind it.  The direct warp-aggregated
+// append (remote_append) waited on a returning cursor atomic in every call --
+// ~32 round trips per warp chunk (r02 launch list, G = 8: the fused step 182
+// us per rank with sliced cursors, vs ~49 us of the unsharded kernel's work).
+constexpr int kFlushQuads = 4;                      // quad rows between flushes
+constexpr int kStageCap = kFlushQuads * 4 * 32;     // receivers staged per warp (<= 1 per agent)
+struct RemoteStage {
+    uint32_t id[8][kStageCap];      // receiver ids, arrival order (8 warps per 256-thread block)
+    uint16_t meta[8][kStageCap];    // destination << 10 | rank within the destination
+    unsigned cnt[8][32];            // per-destination counts of the batch
+    unsigned base[8][32];           // per-destination cursor bases
+};
+static_assert(kStageCap <= 1024, "meta packs the rank in 10 bits");
+
+__device__ __forceinline__ void remote_stage(const WealthArgs& a, RemoteStage& st, int wq, unsigned& qn, bool flag,
+                                             unsigned long long r)
+{
+    const unsigned mask = __ballot_sync(0xffffffffu, flag);
+    const int lane = threadIdx.x & 31;
+    if (flag) {
+        AMBER_DCHECK(r < a.n_glob, "wealth: remote receiver id >= N");
+        const unsigned dest = dest_of(a, r);
+        const unsigned pos = qn + __popc(mask & ((1u << lane) - 1u));
+        st.id[wq][pos] = static_cast<uint32_t>(r);
+#if AMBER_WEALTH_STAGE_RANK
+        const unsigned rank = atomicAdd(&st.cnt[wq][dest], 1u);  // shared-memory atomic: rank within the destination
+        st.meta[wq][pos] = static_cast<uint16_t>((dest << 10) | rank);
+#else
+        st.meta[wq][pos] = static_cast<uint16_t>(dest << 10);
+#endif
+    }
+    qn += __popc(mask);
+}
+
+__device__ __forceinline__ void remote_flush(const WealthArgs& a, RemoteStage& st, int wq, unsigned& qn, unsigned sl)
+{
+    const int lane = threadIdx.x & 31;
+    if (qn == 0) return;  // warp-uniform
+#if !AMBER_WEALTH_STAGE_RANK
+    st.cnt[wq][lane] = 0u;
+    __syncwarp();
+    for (unsigned e = lane; e < qn; e += 32) {
+        const unsigned d = st.meta[wq][e] >> 10;
+        const unsigned rank = atomicAdd(&st.cnt[wq][d], 1u);  // shared-memory atomic
+        st.meta[wq][e] = static_cast<uint16_t>((d << 10) | rank);
+    }
+#endif
+    __syncwarp();
+    const unsigned c = st.cnt[wq][lane];
+#if AMBER_WEALTH_STAGE_RANK
+    st.cnt[wq][lane] = 0u;  // the next batch ranks from zero (read above, before the stores below)
+#endif
+    if (c) st.base[wq][lane] = atomicAdd(a.remote_count + (static_cast<unsigned long long>(lane) * kRemoteSlices + sl) *
+                                                             kCountStride, c);
+    __syncwarp();
+    for (unsigned e = lane; e < qn; e += 32) {
+        const unsigned mt = st.meta[wq][e], d = mt >> 10;
+        const unsigned long long pos = static_cast<unsigned long long>(st.base[wq][d]) + (mt & 1023u);
+        AMBER_DCHECK(pos < a.remote_cap, "wealth: remote bucket slice overflow");
+        if (pos < a.remote_cap)
+            a.remote_ids[(static_cast<unsigned long long>(d) * kRemoteSlices + sl) * a.remote_cap + pos] = st.id[wq][e];
+    }
+    __syncwarp();  // the stage is rewritten by the next batch
+    qn = 0;
 }
 
 // One launch of the step pipeline.  Thread layout: a warp owns a chunk of
@@ -162,7 +268,7 @@ __device__ __forceinline__ void remote_append(const WealthArgs& a, bool flag, un
 // index arithmetic); REMOTE: receivers outside this shard are bucketed for
 // the exchange instead of counted locally.
 template <int B, bool APPLY, bool SCATTER, bool DIGEST, bool REMOTE, bool FAST32>
-__global__ void __launch_bounds__(256, AMBER_WEALTH_MINB) wealth_step_kernel(const WealthArgs a)
+__global__ void __launch_bounds__(256, REMOTE ? AMBER_WEALTH_MINB_REMOTE : AMBER_WEALTH_MINB) wealth_step_kernel(const WealthArgs a)
 {
     using Id = typename std::conditional<FAST32, uint32_t, unsigned long long>::type;
     if (a.slot_zero && blockIdx.x == 0 && threadIdx.x == 0) *a.slot_zero = Slot{0, 0, 0, 0, 0};
@@ -175,8 +281,21 @@ __global__ void __launch_bounds__(256, AMBER_WEALTH_MINB) wealth_step_kernel(con
     const unsigned long long m = a.n_glob - (a.exclude_self ? 1 : 0);
     unsigned long long tot = 0, dig = 0;
     uint32_t act = 0, sent = 0, got = 0;
+    RemoteStage* stg = nullptr;
+    if constexpr (REMOTE) {
+        __shared__ RemoteStage st_;
+        stg = &st_;
+    }
+    const int wq = threadIdx.x >> 5;
+    const bool staged = REMOTE && a.world <= 32 && blockDim.x <= 256;
+    unsigned qn = 0;  // staged remote receivers of this warp (warp-uniform)
+    if constexpr (REMOTE) {
+        if (staged) stg->cnt[wq][lane] = 0u;
+        __syncwarp();
+    }
 
     for (int64_t chunk = warp; chunk < a.nchunks; chunk += nwarps) {
+        const unsigned sl = REMOTE ? static_cast<unsigned>(chunk % kRemoteSlices) : 0u;
         int4 w[kQPT];
         uint32_t c[kQPT][4];
 #pragma unroll
@@ -230,9 +349,14 @@ __global__ void __launch_bounds__(256, AMBER_WEALTH_MINB) wealth_step_kernel(con
                         if (local && rl == ~Id(0)) add_count<B>(a.inc_next, rl, pol, n_loc);  // never: cost without REDs
 #endif
                         sent += local;
-                        if constexpr (REMOTE) remote_append(a, s && !local, r);
+                        if constexpr (REMOTE) {
+                            if (staged) remote_stage(a, *stg, wq, qn, s && !local, r);
+                            else remote_append(a, s && !local, r, sl);
+                        }
                     }
                 }
+                if constexpr (REMOTE)
+                    if (staged && ((j % kFlushQuads) == kFlushQuads - 1 || j == kQPT - 1)) remote_flush(a, *stg, wq, qn, sl);
             }
         }
         // per-chunk partial in 32 bits (at most 16 agents' wealth), then widen
@@ -398,6 +522,8 @@ __global__ void wealth_recv_kernel(const uint32_t* __restrict__ ids, const unsig
 // filled for this rank in the scattered step's parity is read straight from
 // p's memory (mapped over NVLink; __ldcv/__ldcs: never a stale cached copy)
 // and applied to the local counters.
+// gridDim.x is a multiple of kRemoteSlices: block x reads slice x %
+// kRemoteSlices of the bucket, striding with the other x / kRemoteSlices blocks.
 template <int B>
 __global__ void wealth_recv_p2p_kernel(const unsigned long long* __restrict__ peer_base, int world, int me,
                                        size_t cnt_off, size_t ids_off, unsigned long long cap, unsigned long long lo,
@@ -407,11 +533,13 @@ __global__ void wealth_recv_p2p_kernel(const unsigned long long* __restrict__ pe
     unsigned long long got = 0;
     if (p != me) {
         const unsigned char* base = reinterpret_cast<const unsigned char*>(peer_base[p]);
-        const unsigned int n = __ldcv(reinterpret_cast<const unsigned int*>(base + cnt_off) + me);
+        const unsigned sl = blockIdx.x % kRemoteSlices;
+        const unsigned long long sub = blockIdx.x / kRemoteSlices, nsub = gridDim.x / kRemoteSlices;
+        const unsigned long long bucket = static_cast<unsigned long long>(me) * kRemoteSlices + sl;
+        const unsigned int n = __ldcv(reinterpret_cast<const unsigned int*>(base + cnt_off) + bucket * kCountStride);
         const unsigned long long m = n < cap ? n : cap;
-        const uint32_t* ids = reinterpret_cast<const uint32_t*>(base + ids_off) + static_cast<unsigned long long>(me) * cap;
-        for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < m;
-             k += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint32_t* ids = reinterpret_cast<const uint32_t*>(base + ids_off) + bucket * cap;
+        for (unsigned long long k = sub * blockDim.x + threadIdx.x; k < m; k += nsub * blockDim.x) {
             add_count<B>(inc, static_cast<unsigned long long>(__ldcs(ids + k)) - lo, policy_evict_last(), n_loc);
             got += 1;
         }
@@ -419,6 +547,35 @@ __global__ void wealth_recv_p2p_kernel(const unsigned long long* __restrict__ pe
     unsigned long long vals[1] = {got};
     unsigned long long* const outs[1] = {&slot->sent};
     block_sum_atomic<1>(vals, outs);
+}
+
+// Sliced buckets -> contiguous per-destination blocks for the transports that
+// ship one block per destination (NCCL send/recv, loopback and host-collective
+// copies): block (x, p) copies slice x of destination p behind the slices
+// before it; block 0 of each destination writes its total.
+__global__ void wealth_compact_kernel(const uint32_t* __restrict__ ids, const unsigned int* __restrict__ cnt,
+                                      unsigned long long cap, uint32_t* __restrict__ out,
+                                      unsigned int* __restrict__ out_cnt, unsigned long long out_cap)
+{
+    const unsigned long long p = blockIdx.y;
+    const int sl = blockIdx.x;
+    __shared__ unsigned long long off_s, tot_s;
+    if (threadIdx.x == 0) {
+        unsigned long long off = 0, tot = 0;
+        for (int k = 0; k < kRemoteSlices; ++k) {
+            const unsigned long long c = cnt[(p * kRemoteSlices + k) * kCountStride];
+            if (k < sl) off += c;
+            tot += c;
+        }
+        off_s = off;
+        tot_s = tot;
+    }
+    __syncthreads();
+    const unsigned long long n = cnt[(p * kRemoteSlices + sl) * kCountStride];
+    const uint32_t* src = ids + (p * kRemoteSlices + sl) * cap;
+    uint32_t* dst = out + p * out_cap + off_s;
+    for (unsigned long long k = threadIdx.x; k < n; k += blockDim.x) dst[k] = src[k];
+    if (sl == 0 && threadIdx.x == 0) out_cnt[p] = static_cast<unsigned int>(tot_s);
 }
 
 // Fault injection (test hook, option "inject_counter_fault"): one extra count
@@ -484,7 +641,10 @@ public:
     size_t p2p_cnt_off[2] = {0, 0}, p2p_ids_off[2] = {0, 0};
     DevBuf<unsigned long long> p2p_peers;
     DevBuf<unsigned long long> recv_total;
-    uint64_t send_cap = 0;
+    uint64_t send_cap = 0;    // ids per destination region (kRemoteSlices slices) and per compacted block
+    uint64_t slice_cap = 0;   // ids per slice: every agent of the slice's warp chunks
+    DevBuf<uint32_t> cmp_ids;          // compacted per-destination blocks (non-P2P transports)
+    DevBuf<unsigned int> cmp_counts;
 
     WealthModel(int64_t n_, const amber_wealth_params& p_, uint64_t seed_, const amber_runtime* r)
     {
@@ -529,10 +689,13 @@ public:
         const bool force_x = force && force[0] == '1' && r && r->nccl_unique_id && rt.world == 1;
         if (rt.world > 1 || force_x) {
             xch = make_wealth_exchange_rt(rt, r);
-            send_cap = static_cast<uint64_t>(std::max<int64_t>(shard, 1));  // same on every rank: peers index each other's buckets
+            // same on every rank (from the common shard size): peers index each other's buckets
+            const int64_t nch_max = ceil_div(std::max<int64_t>(shard, 1), kChunkAgents);
+            slice_cap = static_cast<uint64_t>(ceil_div(nch_max, kRemoteSlices) * kChunkAgents);
+            send_cap = slice_cap * kRemoteSlices;
             send_ids.allocate(&rt, send_cap * rt.world);
             recv_ids.allocate(&rt, static_cast<size_t>(shard) * rt.world + 1);
-            send_counts.allocate(&rt, rt.world);
+            send_counts.allocate(&rt, static_cast<int64_t>(rt.world) * kRemoteSlices * kCountStride);
             send_counts.zero_async(rt.stream);
             const char* mode = getenv("AMBER_WEALTH_EXCHANGE");
             p2p_wanted = !(mode && std::string(mode) == "nccl");  // mapped at the first exchange (collective)
@@ -546,7 +709,7 @@ public:
     // exchange if any rank cannot map its peers.
     void setup_p2p()
     {
-        const size_t cbytes = ((static_cast<size_t>(rt.world) * 4 + 255) / 256) * 256;
+        const size_t cbytes = ((static_cast<size_t>(rt.world) * kRemoteSlices * kCountStride * 4 + 255) / 256) * 256;
         const size_t ibytes = static_cast<size_t>(rt.world) * send_cap * 4;
         p2p_cnt_off[0] = 0;
         p2p_cnt_off[1] = cbytes;
@@ -590,6 +753,8 @@ public:
         recv_ids.reset();
         send_counts.reset();
         recv_total.reset();
+        cmp_ids.reset();
+        cmp_counts.reset();
         rt.destroy();
     }
 
@@ -670,13 +835,16 @@ public:
         if (remote) {
             a.world = rt.world;
             a.shard_size = static_cast<unsigned long long>(shard);
+            a.shard_magic = static_cast<uint32_t>(0xFFFFFFFFull / static_cast<unsigned long long>(shard));
             a.remote_ids = send_ids.p;
             a.remote_count = send_counts.p;
-            a.remote_cap = send_cap;
+            a.remote_cap = slice_cap;
             if (p2p) {  // the scattered step's parity; its previous readers finished (barrier of ts - 1)
                 a.remote_ids = p2p_ids(ts & 1);
                 a.remote_count = p2p_counts(ts & 1);
-                AMBER_CUDA(cudaMemsetAsync(a.remote_count, 0, rt.world * sizeof(unsigned int), rt.stream));
+                AMBER_CUDA(cudaMemsetAsync(a.remote_count, 0,
+                                           static_cast<size_t>(rt.world) * kRemoteSlices * kCountStride * sizeof(unsigned int),
+                                           rt.stream));
             } else {
                 send_counts.zero_async(rt.stream);
             }
@@ -700,11 +868,12 @@ public:
         if (p2p) {
             wealth_p2p_barrier(xch, rt);
             auto launch_p2p = [&](auto kern) {
-                const dim3 g(static_cast<unsigned>(std::max(1, rt.num_sms * 8 / std::max(rt.world - 1, 1))),
-                             static_cast<unsigned>(rt.world));
+                // a multiple of kRemoteSlices blocks per peer (the kernel's slice mapping)
+                const int per = std::max(1, rt.num_sms * 8 / std::max(rt.world - 1, 1) / kRemoteSlices);
+                const dim3 g(static_cast<unsigned>(per * kRemoteSlices), static_cast<unsigned>(rt.world));
                 prof.launch(rt.stream, "wealth_recv_p2p", [&] {
                     kern<<<g, 256, 0, rt.stream>>>(p2p_peers.p, rt.world, rt.rank, p2p_cnt_off[ts & 1],
-                                                   p2p_ids_off[ts & 1], static_cast<unsigned long long>(send_cap),
+                                                   p2p_ids_off[ts & 1], static_cast<unsigned long long>(slice_cap),
                                                    static_cast<unsigned long long>(lo),
                                                    static_cast<unsigned long long>(n_loc), ib[ts & 1].p, slot(ts));
                 });
@@ -719,7 +888,17 @@ public:
             }
             return;
         }
-        wealth_exchange_run(xch, rt, send_counts.p, send_ids.p, send_cap, recv_ids.p, recv_total.p);
+        if (!cmp_ids.p) {
+            cmp_ids.allocate(&rt, send_cap * rt.world);
+            cmp_counts.allocate(&rt, rt.world);
+        }
+        prof.launch(rt.stream, "wealth_compact", [&] {
+            wealth_compact_kernel<<<dim3(kRemoteSlices, rt.world), 256, 0, rt.stream>>>(
+                send_ids.p, send_counts.p, static_cast<unsigned long long>(slice_cap), cmp_ids.p, cmp_counts.p,
+                static_cast<unsigned long long>(send_cap));
+        });
+        check_launch("wealth_compact_kernel");
+        wealth_exchange_run(xch, rt, cmp_counts.p, cmp_ids.p, send_cap, recv_ids.p, recv_total.p);
         auto launch_recv = [&](auto kern) {
             prof.launch(rt.stream, "wealth_recv_apply", [&] {
                 kern<<<rt.num_sms * 4, 256, 0, rt.stream>>>(recv_ids.p, recv_total.p,
