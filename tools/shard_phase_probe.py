@@ -1,6 +1,6 @@
 #!/usr/bin/env python
-"""Per-phase device times of the sharded C4 wealth step at G virtual ranks on
-ONE B200 (loopback transport: each rank's kernels run on this GPU, its own
+"""Per-phase device times of a sharded step (C4 wealth; V2 SIR or V3 Boids with
+a third argument "sir" / "boids") at G virtual ranks on ONE B200 (loopback transport: each rank's kernels run on this GPU, its own
 host thread, host barriers between phases -- no kernel waits on another).
 
 Run it under the ncu launch list so every kernel is timed alone (serialised),
@@ -10,7 +10,7 @@ which is what each rank's kernel costs on its own GPU:
       --log-file gpurun_out/shard_launches.csv python tools/shard_phase_probe.py 8
 
 Without ncu it prints the loopback wall time per step (all ranks' kernels
-sharing one GPU).  python tools/shard_phase_probe.py [G] [steps]"""
+sharing one GPU).  python tools/shard_phase_probe.py [G] [steps] [wealth|sir|boids]"""
 import os
 import sys
 import threading
@@ -18,11 +18,21 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from paper_2601_16292_b200 import Model, loopback_id, wealth_params  # noqa: E402
-from paper_2601_16292_b200.workloads import C4_WEALTH_SCALE as C  # noqa: E402
+from paper_2601_16292_b200 import Model, boids_params, loopback_id, sir_params, wealth_params  # noqa: E402
+from paper_2601_16292_b200 import workloads as W  # noqa: E402
 
 world = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
+kind = sys.argv[3] if len(sys.argv) > 3 else "wealth"
+C = dict({"wealth": W.C4_WEALTH_SCALE, "sir": W.V2_SIR_SCALE, "boids": W.V3_BOIDS_SCALE}[kind])
+if os.environ.get("PROBE_N"):  # smaller population at the same density (G copies of the sharded buffers share one GPU)
+    n2 = int(float(os.environ["PROBE_N"]))
+    if "L" in C:
+        C["L"] = float(C["L"] * (n2 / C["n"]) ** 0.5)
+    C["n"] = n2
+P = {"wealth": lambda: wealth_params(),
+     "sir": lambda: sir_params(C["mean_degree"], C["beta"], C["gamma"], C["init_frac"]),
+     "boids": lambda: boids_params(*[C[k] for k in ("L", "R", "rs", "wc", "wa", "ws", "vmax", "dt")])}[kind]()
 
 
 def par(ms, fn):
@@ -44,13 +54,14 @@ def par(ms, fn):
 
 
 uid = loopback_id()
-ms = [Model("wealth", C["n"], wealth_params(), C["seed"], rank=r, world=world, unique_id=uid) for r in range(world)]
+ms = [Model(kind, C["n"], P, C["seed"], rank=r, world=world, unique_id=uid) for r in range(world)]
 par(ms, lambda m: (m.step(3), m.synchronize()))
 t0 = time.perf_counter()
 par(ms, lambda m: (m.step(steps), m.synchronize()))
 dt = time.perf_counter() - t0
 tots = [None] * world
-par(ms, lambda m: tots.__setitem__(ms.index(m), int(m.metrics("total_wealth")[-1])))
-print(f"G={world} loopback on one GPU: {dt / steps * 1e3:.3f} ms/step wall (all ranks sharing the GPU); "
-      f"total wealth {tots[0]} (expected {C['n']})", flush=True)
+name = {"wealth": "total_wealth", "sir": "I", "boids": "mean_speed"}[kind]
+par(ms, lambda m: tots.__setitem__(ms.index(m), m.metrics(name)[-1]))
+print(f"{kind} G={world} loopback on one GPU: {dt / steps * 1e3:.3f} ms/step wall (all ranks sharing the GPU); "
+      f"last {name} {tots[0]}", flush=True)
 par(ms, lambda m: m.close())
