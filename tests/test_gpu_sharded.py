@@ -71,6 +71,23 @@ def test_sharded_wealth_equals_oracle(orc, world, n):
     assert all(d == orc.digest(ref) for d in dg)
 
 
+@pytest.mark.parametrize("world,n,mode", [(2, 3_000_017, "p2p"), (3, 2_000_003, "nccl"), (33, 50_021, "p2p")])
+def test_sharded_wealth_bucket_slices(orc, monkeypatch, world, n, mode):
+    # many warp chunks per bucket slice (> 64 chunks per rank: slices shared by
+    # several chunks, cursors accumulating), both transports; world > 32 takes the
+    # direct (unstaged) warp-aggregated append
+    if mode == "nccl":
+        monkeypatch.setenv("AMBER_WEALTH_EXCHANGE", "nccl")
+    seed, steps = 19, 6
+    ms = sharded(world, n, seed)
+    par(ms, lambda m: (m.step(2), m.step(4)))
+    w = np.concatenate(par(ms, lambda m: m.read_column("wealth")))
+    ref, tot, _, _ = orc.wealth_run(np.ones(n, np.int32), seed, 0, steps)
+    assert np.array_equal(w, ref)
+    for tt in par(ms, lambda m: m.metrics("total_wealth")):
+        assert np.array_equal(tt, tot)
+
+
 @pytest.mark.parametrize("mode", ["p2p", "nccl"])
 def test_sharded_wealth_exchange_modes(orc, monkeypatch, mode):
     # p2p (default): owners read the peers' buckets in place after a stream-ordered
