@@ -293,9 +293,10 @@ int amber_digest(amber_model* m, const char* name, uint64_t* out);
  * (wealth/SIR: 1 = all steps of a call in one launch (single-CTA kernel for
  * wealth N <= 16384; cooperative direction-optimizing kernel for SIR),
  * 0 = one launch per step, pull only for SIR), SIR "direction" (0 = choose
- * per step, push when 4I < 3S; 1 = always pull; 2 = push whenever the previous
- * counts are known -- identical results, for tests and probes; 1 or 2 also
- * run a single step through the cooperative kernel), SIR "apl" (agents per
+ * per step, push when 4I < 3S (10I < 9S at 8 agents per lane; sharded: from the
+ * global counts of the all-gathered bitmaps); 1 = always pull; 2 = push whenever
+ * the previous counts are known -- identical results, for tests and probes;
+ * 1 or 2 also run a single step through the cooperative kernel), SIR "apl" (agents per
  * lane of the step kernels: 0 = auto (8 above 2^22 agents, else 1), 1, 2, 4
  * or 8 -- identical results); Boids: "lanes" (4/8/16 lanes per agent in the
  * stencil, default 4 -- identical results).

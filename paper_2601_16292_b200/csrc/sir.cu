@@ -278,6 +278,8 @@ struct SirStepArgs {
     uint32_t* queue;         // persistent launch: [2 parities][2 phases][kRegions] chunk counters
     int grab;                // chunks per queue grab
     int dir;                 // 0: direction-optimizing; 1: pull only; 2: push whenever possible (tests, probes)
+    const uint32_t* hits;    // sharded push step: the local words of the step's hit bitmap (S agents a
+                             // pusher infected); the pull kernel then only finalises (no row walk)
 };
 
 constexpr int kRegions = 16;
@@ -589,7 +591,11 @@ __device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0,
     const uint32_t nib_s = (in.ws >> ((APL * lane) & 31)) & kM & real;
     const uint32_t nib_i = (in.wi >> ((APL * lane) & 31)) & kM & real;
     uint32_t hitnib = 0;
-    if (__any_sync(0xffffffffu, nib_s != 0)) {
+    if (a.hits) {
+        // sharded push step: the infections were decided by the pushers (own and
+        // other ranks', all-to-all'd into this shard's words of the hit bitmap)
+        hitnib = (a.hits[(a0 >> 5) + ((APL * lane) >> 5)] >> ((APL * lane) & 31)) & kM & nib_s;
+    } else if (__any_sync(0xffffffffu, nib_s != 0)) {
         if (lane < APL) sm.h[wq][lane] = 0u;
         const uint32_t T = queue_owners<APL>(sm, 0, nib_s, APL * lane, in.r);
         __syncwarp();
@@ -1053,6 +1059,82 @@ __global__ void __launch_bounds__(kSirPT, APL == 8 ? kSirMinBLarge : kSirMinB) s
     if (uncounted) sir_count_new(a, cur, a.ring + ((static_cast<int64_t>(a.t0) + a.n_steps - 1) % a.ring_cap));
 }
 
+// ---- sharded push step (NEXT-3) ----
+// The shard's infected agents (local I words) walk their rows (local offsets,
+// global neighbour ids) against the GLOBAL S bitmap of the current state, with
+// the same pair-keyed draw as every other path (S3); a transmitting arc sets
+// the neighbour's bit in this rank's copy of the global hit bitmap (no-return
+// RED).  The remote parts of that bitmap then go to their owners (fixed-size
+// all-to-all of bitmap blocks) and are OR-ed into the owners' words -- no
+// per-target append, so no cursor atomics (r02: a warp-aggregated id append
+// plus __fns register queues ran 200 us per rank at G = 8, V2 early steps).
+struct ShardPushArgs {
+    PhiloxKey key;
+    const int32_t* row_ptr;    // local rows
+    const int32_t* col;        // global neighbour ids
+    const uint32_t* ib;        // local I words of the current state
+    const uint32_t* sbg;       // global S bitmap of the current state
+    uint32_t* hg;              // this rank's global hit bitmap (zeroed)
+    int64_t nwords;            // local I words (npl / 32)
+    uint32_t lo;
+    unsigned long long t_beta;
+    uint32_t t;
+};
+
+constexpr int kPushQ = 32 + 32 * 32;  // per-warp pusher queue: < 32 carried + one word (32 agents) per lane
+
+__global__ void __launch_bounds__(256) sir_shard_push_kernel(const ShardPushArgs a)
+{
+    __shared__ uint32_t q[8][kPushQ];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    auto walk = [&](uint32_t g0, uint32_t nown) {
+        const bool mine = static_cast<uint32_t>(lane) < nown;
+        const uint32_t id = mine ? q[wq][g0 + lane] : 0u;
+        const int32_t rb = mine ? a.row_ptr[id] : 0, re = mine ? a.row_ptr[id + 1] : 0;
+        const uint32_t own = nown >= 32 ? 0xffffffffu : ((1u << nown) - 1u);
+        walk_rows_pay<4>([&](int32_t e) { return static_cast<uint32_t>(__ldcs(a.col + e)); }, own, rb, re, a.lo + id,
+                         [&](uint32_t j) { return (__ldcg(a.sbg + (j >> 5)) >> (j & 31u)) & 1u; },
+                         [&](uint32_t j, int32_t, int, uint32_t s) {
+            const uint4 w = philox(make_uint4(min(s, j), max(s, j), a.t, TAG_SIR_TX), a.key);
+            if (static_cast<unsigned long long>(w.x) < a.t_beta) red_or(a.hg + (j >> 5), 1u << (j & 31u));
+            return false;  // an infected agent tries every susceptible neighbour
+        });
+    };
+    uint32_t qn = 0;  // queued pushers (warp-uniform, < 32 between words)
+    for (int64_t w0 = warp * 32; w0 < a.nwords; w0 += nwarps * 32) {
+        // one bitmap word (32 agents) per lane; set bits queued at their warp rank
+        const int64_t w = w0 + lane;
+        uint32_t m = w < a.nwords ? a.ib[w] : 0u;
+        uint32_t tot;
+        uint32_t k = qn + warp_excl(__popc(m), &tot);
+        for (; m; m &= m - 1u) q[wq][k++] = static_cast<uint32_t>(32 * w) + (__ffs(static_cast<int>(m)) - 1);
+        qn += tot;
+        __syncwarp();
+        uint32_t g0 = 0;
+        for (; qn - g0 >= 32; g0 += 32) walk(g0, 32);
+        const uint32_t rem = qn - g0;
+        const uint32_t carry = static_cast<uint32_t>(lane) < rem ? q[wq][g0 + lane] : 0u;
+        __syncwarp();
+        if (static_cast<uint32_t>(lane) < rem) q[wq][lane] = carry;
+        __syncwarp();
+        qn = rem;
+    }
+    if (qn) walk(0, qn);
+}
+
+// This shard's hit words |= the blocks the other ranks sent for it (recv holds
+// world blocks of `words` words; the own block is this rank's own region).
+__global__ void sir_shard_or_kernel(const uint32_t* __restrict__ recv, int world, int64_t words, uint32_t* own)
+{
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        for (int p = 0; p < world; ++p) v |= recv[p * words + w];
+        own[w] |= v;
+    }
+}
+
 // Sharded graph slice: row offsets rebased to the shard's first arc.
 __global__ void sir_rebase_kernel(const int32_t* __restrict__ rp, int64_t cnt, int32_t base, int32_t* __restrict__ out)
 {
@@ -1113,7 +1195,12 @@ public:
     int64_t lo = 0, nl = 0, npl = 0, shard = 0;  // local agents / padded (unsharded: n, n_pad)
     int64_t nq = 0;                              // npl rounded up to whole 128-agent chunks
     DevBuf<uint32_t> ib_glob;  // world * shard / 32 words
-    bool glob_ok = false;      // ib_glob holds the current state's bits
+    DevBuf<uint32_t> sb_glob;  // the same for the S bits (probed by the sharded push)
+    bool glob_ok = false;      // ib_glob / sb_glob hold the current state's bits
+    // sharded push step: this rank's global hit bitmap, the blocks received for the
+    // own shard, the (fixed) block sizes of the all-to-all
+    DevBuf<uint32_t> hg, push_cnt, push_recv;
+    DevBuf<SirSlot> gcnt;      // global S / I / R of the current state (direction choice)
 
     SirModel(int64_t n_, const amber_sir_params& p_, uint64_t seed_, const amber_runtime* r)
     {
@@ -1161,6 +1248,9 @@ public:
             if (nl) AMBER_CUDA(cudaMemcpyAsync(x[0].p, full.p + lo, nl, cudaMemcpyDeviceToDevice, rt.stream));
             slice_graph();
             ib_glob.allocate(&rt, static_cast<size_t>(rt.world) * (shard / 32) + kChunkMax / 32);  // + one chunk of slack
+            sb_glob.allocate(&rt, static_cast<size_t>(rt.world) * (shard / 32) + kChunkMax / 32);
+            AMBER_CUDA(cudaMemsetAsync(ib_glob.p, 0, ib_glob.n * 4, rt.stream));
+            AMBER_CUDA(cudaMemsetAsync(sb_glob.p, 0, sb_glob.n * 4, rt.stream));
             sc = make_shard_comm(rt, r);
             rt.sync();
         } else {
@@ -1211,9 +1301,10 @@ public:
     }
 
     // Sharded: all-gather the current state's local I-bitmap words.
-    void gather_bits(const uint32_t* local)
+    void gather_bits(int c)
     {
-        shard_allgather_u32(sc, rt, local, ib_glob.p, static_cast<size_t>(shard / 32));
+        shard_allgather_u32(sc, rt, ib[c].p, ib_glob.p, static_cast<size_t>(shard / 32));
+        shard_allgather_u32(sc, rt, sb[c].p, sb_glob.p, static_cast<size_t>(shard / 32));
         glob_ok = true;
     }
 
@@ -1240,6 +1331,11 @@ public:
         ring.reset();
         queue.reset();
         ib_glob.reset();
+        sb_glob.reset();
+        hg.reset();
+        push_cnt.reset();
+        push_recv.reset();
+        gcnt.reset();
         if (sc) destroy_shard_comm(sc);
         rt.destroy();
     }
@@ -1349,29 +1445,93 @@ public:
         }
     }
 
-    // Sharded steps: per step one pull launch over the local rows (reading the
-    // global I bitmap), then the all-gather of the next bitmap words.  Pull only:
-    // a push would write remote agents.  Identical results for any rank count
-    // (pair-keyed draws, S3).
+    // Sharded steps: per step either one pull launch over the local rows (reading
+    // the global I bitmap) or a push phase (push_phase: the shard's infected
+    // agents mark their targets in a global hit bitmap whose remote blocks go to
+    // their owners) followed by the same launch finalising from the hit bits;
+    // then the all-gather of the next I and S bitmap words.  Identical results
+    // for any rank count and direction (pair-keyed draws, S3).
     void step_sharded(int64_t nsteps)
     {
         const int threads = block ? static_cast<int>(std::min<int64_t>(block, 256)) : 256;
-        if (!glob_ok) gather_bits(ib[cur].p);
+        if (!glob_ok) gather_bits(cur);
         for (int64_t k = 0; k < nsteps; ++k) {
             sir_zero_slots<<<1, 32, 0, rt.stream>>>(ring.p, metrics_cap, t, 1);
             check_launch("sir_zero_slots");
+            const bool push = sharded_push_now();
             SirStepArgs a = args(1);
             a.ib[cur] = ib_glob.p;  // read: global bits of state t; write: local bits of t+1
+            if (push) {
+                push_phase();
+                a.hits = hg.p + lo / 32;  // the step only finalises from the hit bits
+            }
             const int L = lanes_apl();
             int blocks = static_cast<int>(std::max<int64_t>(1, ceil_div(sir_chunks(npl, L), std::max(1, threads / 32))));
             if (grid) blocks = static_cast<int>(grid);
-            prof.launch(rt.stream, "sir_shard_step", [&] { launch_step(L, blocks, threads, a); });
+            prof.launch(rt.stream, push ? "sir_shard_finalize" : "sir_shard_step", [&] { launch_step(L, blocks, threads, a); });
             check_launch("sir_step_kernel");
             cur ^= 1;
             ++t;
-            gather_bits(ib[cur].p);
+            gather_bits(cur);
         }
         prev_ok = false;
+    }
+
+    // Direction of the next sharded step: push when the infected agents are
+    // fewer than 0.9x the susceptible ones (the one-GPU rule at 8 agents per
+    // lane), from the global counts of the current state (popcounts of the
+    // all-gathered bitmaps); option "direction": 1 pull only, 2 push.
+    bool sharded_push_now()
+    {
+        if (dir == 1) return false;
+        if (dir == 2) return true;
+        if (!gcnt.p) gcnt.allocate(&rt, 1);
+        AMBER_CUDA(cudaMemsetAsync(gcnt.p, 0, sizeof(SirSlot), rt.stream));
+        sir_count_bits_kernel<<<rt.num_sms * 2, 256, 0, rt.stream>>>(ib_glob.p, sb_glob.p, n, gcnt.p);
+        check_launch("sir_count_bits_kernel");
+        SirSlot h{};
+        AMBER_CUDA(cudaMemcpyAsync(&h, gcnt.p, sizeof(h), cudaMemcpyDeviceToHost, rt.stream));
+        rt.sync();
+        return 10 * h.I < 9 * h.S;
+    }
+
+    // Sharded push phase of step t: the pushers' walk into this rank's global hit
+    // bitmap, the remote blocks of it to their owners (fixed-size all-to-all),
+    // OR-ed into the own block.
+    void push_phase()
+    {
+        const size_t words = static_cast<size_t>(shard / 32);
+        const size_t gwords = static_cast<size_t>(rt.world) * words + kChunkMax / 32;
+        if (!hg.p) {
+            hg.allocate(&rt, gwords);
+            push_recv.allocate(&rt, static_cast<size_t>(rt.world) * words);
+            push_cnt.allocate(&rt, rt.world);
+            std::vector<uint32_t> c(rt.world, static_cast<uint32_t>(words));
+            AMBER_CUDA(cudaMemcpyAsync(push_cnt.p, c.data(), c.size() * 4, cudaMemcpyHostToDevice, rt.stream));
+            rt.sync();
+        }
+        AMBER_CUDA(cudaMemsetAsync(hg.p, 0, gwords * 4, rt.stream));
+        ShardPushArgs pa{};
+        pa.key = key;
+        pa.row_ptr = g.row_ptr.p;
+        pa.col = g.col.p;
+        pa.ib = ib[cur].p;
+        pa.sbg = sb_glob.p;
+        pa.hg = hg.p;
+        pa.nwords = npl / 32;
+        pa.lo = static_cast<uint32_t>(lo);
+        pa.t_beta = bernoulli_threshold_host(p.beta);
+        pa.t = static_cast<uint32_t>(t);
+        prof.launch(rt.stream, "sir_shard_push", [&] {
+            sir_shard_push_kernel<<<rt.num_sms * 8, 256, 0, rt.stream>>>(pa);
+        });
+        check_launch("sir_shard_push_kernel");
+        shard_alltoallv(sc, rt, hg.p, push_cnt.p, words, 4, push_recv.p, static_cast<size_t>(rt.world) * words);
+        prof.launch(rt.stream, "sir_shard_or", [&] {
+            sir_shard_or_kernel<<<rt.num_sms * 4, 256, 0, rt.stream>>>(push_recv.p, rt.world, static_cast<int64_t>(words),
+                                                                     hg.p + lo / 32);
+        });
+        check_launch("sir_shard_or_kernel");
     }
 
     // Sharded metrics / digests are global: summed over the ranks (collective).
@@ -1518,7 +1678,6 @@ public:
         }
         if (k == "direction") {
             AMBER_REQUIRE(v >= 0 && v <= 2, "direction must be 0 (auto), 1 (pull) or 2 (push)");
-            AMBER_REQUIRE(!sc || v != 2, "sharded SIR steps pull only");
             dir = static_cast<int>(v);
             return true;
         }

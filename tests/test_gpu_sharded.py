@@ -194,6 +194,34 @@ def test_sharded_sir_equals_oracle(orc, world, apl):
     assert all(d == orc.digest(ref) for d in par(ms, lambda m: m.digest("state")))
 
 
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("direction", [0, 2])
+def test_sharded_sir_push_equals_oracle(orc, world, direction):
+    # sharded push steps (direction 2: every step; 0: the global-count rule):
+    # pushers walk their rows against the all-gathered S bitmap, remote targets
+    # are all-to-all'd to their owners, the step finalises from the hit bits
+    cfg = dict(n=50_003, mean_degree=10.0, beta=0.05, gamma=0.1, init_frac=0.01, seed=7)
+    steps = 40
+    ref_m = Model("sir", cfg["n"], sir_params(cfg["mean_degree"], cfg["beta"], cfg["gamma"], cfg["init_frac"]),
+                  cfg["seed"])
+    rp, col = oracle_graph(orc, cfg, ref_m)
+    ref_m.close()
+    st = orc.sir_init(cfg["n"], 500, cfg["seed"])
+    ref, counts, dig = orc.sir_run(rp, col, st, cfg["seed"], cfg["beta"], cfg["gamma"], 0, steps, digests=True)
+    ms = sharded_sir(world, cfg)
+    for m in ms:
+        m.set_option("digest", 1)
+        m.set_option("direction", direction)
+    par(ms, lambda m: (m.step(3), m.step(steps - 3)))
+    x = np.concatenate(par(ms, lambda m: m.read_column("state")))
+    assert np.array_equal(x, ref)
+    for name_k, name in enumerate("SIR"):
+        for v in par(ms, lambda m: m.metrics(name)):
+            assert np.array_equal(v, counts[:, name_k]), name
+    for v in par(ms, lambda m: m.metrics("digest")):
+        assert np.array_equal(v, dig.astype(np.uint64))
+
+
 def test_sharded_sir_local_rows_and_column_write(orc):
     cfg = dict(n=20_000, mean_degree=6.0, beta=0.1, gamma=0.2, init_frac=0.005, seed=11)
     full = Model("sir", cfg["n"], sir_params(cfg["mean_degree"], cfg["beta"], cfg["gamma"], cfg["init_frac"]),

@@ -55,6 +55,9 @@ def par(ms, fn):
 
 uid = loopback_id()
 ms = [Model(kind, C["n"], P, C["seed"], rank=r, world=world, unique_id=uid) for r in range(world)]
+if kind == "sir" and os.environ.get("PROBE_DIR"):  # SIR direction: 0 auto, 1 pull, 2 push
+    for m in ms:
+        m.set_option("direction", int(os.environ["PROBE_DIR"]))
 par(ms, lambda m: (m.step(3), m.synchronize()))
 t0 = time.perf_counter()
 par(ms, lambda m: (m.step(steps), m.synchronize()))
