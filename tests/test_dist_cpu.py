@@ -162,6 +162,60 @@ def _sharded_sir(rank, world):
     return out, ref.tolist()
 
 
+def _sharded_sir_push(rank, world):
+    # the sharded PUSH step (r02): own infected agents walk their rows against the
+    # all-gathered S bitmap, set bits of a global-size hit bitmap; block p of it
+    # goes to rank p (all_to_all), the owner ORs the blocks and finalises
+    import oracle
+    from paper_2601_16292_b200 import sir_shard_range
+    n, kbar, seed, beta, gamma, steps = 2003, 6.0, 5, 0.3, 0.2, 12
+    rp, col, _ = oracle.er_graph(n, int(round(n * kbar / 2)), seed)
+    st0 = oracle.sir_init(n, 20, seed)
+    lo, hi = sir_shard_range(n, world, rank)
+    shard = ((-(-n // world) + 31) // 32) * 32
+    x = st0[lo:hi].copy()
+    T_b, T_g = oracle.bernoulli_threshold(beta), oracle.bernoulli_threshold(gamma)
+
+    def gather(mask):
+        bits = np.zeros(shard, np.uint8)
+        bits[:hi - lo] = mask
+        words = torch.tensor(np.packbits(bits, bitorder="little").view(np.uint32).astype(np.int64))
+        g = [torch.zeros_like(words) for _ in range(world)]
+        dist.all_gather(g, words)
+        return np.concatenate([w.numpy().astype(np.uint32) for w in g])
+
+    for t in range(steps):
+        sg = gather(x == 0)
+        is_s = lambda j: (sg[j >> 5] >> (j & 31)) & 1
+        hit = np.zeros(world * shard, np.uint8)  # this rank's global hit bitmap (one byte per bit here)
+        for k in range(hi - lo):
+            i = lo + k
+            if x[k] != 1:
+                continue
+            for j in col[rp[i]:rp[i + 1]]:
+                j = int(j)
+                if is_s(j) and oracle.sir_tx_word(seed, min(i, j), max(i, j), t) < T_b:
+                    hit[j] = 1
+        # block p of every rank's hit bitmap to rank p (gloo has no all_to_all: an
+        # all-gather of the whole bitmaps, each rank keeping the blocks for it)
+        allh = [torch.zeros(world * shard, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(allh, torch.tensor(hit.astype(np.int64)))
+        mine = np.zeros(shard, np.uint8)
+        for r in allh:
+            mine |= r.numpy()[rank * shard:(rank + 1) * shard].astype(np.uint8)
+        y = x.copy()
+        for k in range(hi - lo):
+            if x[k] == 0 and mine[k]:
+                y[k] = 1
+            elif x[k] == 1 and oracle.lane32(seed, 0x11, lo + k, t) < T_g:
+                y[k] = 2
+        x = y
+    out = [None] * world
+    dist.all_gather_object(out, (lo, x.tolist()))
+    ref = oracle.sir_run(rp, col, st0, seed, beta, gamma, 0, steps)[0]
+    return out, ref.tolist()
+
+
 def _sharded_boids(rank, world):
     import oracle
     L, R, n, seed, steps = 120.0, 10.0, 800, 4, 8
@@ -214,6 +268,13 @@ def test_sharded_boids_slab_halo_equals_oracle(world):
 @pytest.mark.parametrize("world", [2, 4])
 def test_sharded_sir_bitmap_allgather_equals_oracle(world):
     parts, ref = run_world(world, _sharded_sir)[0]
+    x = np.concatenate([np.array(v, np.uint8) for _, v in sorted(parts)])
+    assert np.array_equal(x, np.array(ref, np.uint8))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_sir_push_hit_blocks_equal_oracle(world):
+    parts, ref = run_world(world, _sharded_sir_push)[0]
     x = np.concatenate([np.array(v, np.uint8) for _, v in sorted(parts)])
     assert np.array_equal(x, np.array(ref, np.uint8))
 
