@@ -553,6 +553,7 @@ __device__ __forceinline__ void pull_load(const SirStepArgs& a, int64_t a0, cons
     const int64_t i0 = a0 + APL * lane;
     p.ws = sb[(a0 >> 5) + ((APL * lane) >> 5)];
     p.wi = ib[((a.gid0 + static_cast<unsigned long long>(a0)) >> 5) + ((APL * lane) >> 5)];
+    if (a.hits) return;  // sharded push step: finalise only, no row walk (rows unused)
     if constexpr (APL == 4) {
         if (i0 + 4 <= a.n) {
             const int4 v = *reinterpret_cast<const int4*>(a.row_ptr + i0);
