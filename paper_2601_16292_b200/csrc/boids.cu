@@ -35,10 +35,14 @@ constexpr float kFix = 16777216.0f;  // 2^24 (B3)
 #define AMBER_BOIDS_INFLIGHT 2  // candidate loads in flight per lane in interior row runs
 #endif
 #ifndef AMBER_BOIDS_MINB
-// resident 256-thread blocks per SM for the stencil kernel: 4 (register cap 64)
+// resident 256-thread blocks per SM for the stencil kernel: 3 (register cap 80)
 // for small populations, 6 (cap 40) for large ones -- V3 stencil 18.3 -> 17.5 ms
-// (more warps to hide the candidate loads), C3 slightly slower (60.9 -> 63.9 us)
-#define AMBER_BOIDS_MINB 4
+// (more warps to hide the candidate loads), C3 slightly slower (60.9 -> 63.9 us).
+// r02 C3 A/B (tools/c3_lib_probe.py, same box, alternating runs): 2 / 3 / 4 / 5
+// blocks per SM 42.4 / 42.4 / 43.6 / 42.7 us/step.
+#define AMBER_BOIDS_MINB 3
+#endif
+#ifndef AMBER_BOIDS_MINB_LARGE
 #define AMBER_BOIDS_MINB_LARGE 6
 #endif
 
