@@ -292,6 +292,8 @@ constexpr int kWalkU = AMBER_SIR_WALK_U;  // 32-arc batches in flight per warp (
 #endif
 constexpr int kSirPT = AMBER_SIR_PT;  // threads per block of the persistent kernel
 #ifndef AMBER_SIR_MINB
+// r02 C2 A/B (tools/c2_lib_probe.py): 2 / 3 / 4 / 6 blocks per SM 4.03 / 3.72 /
+// 3.77 / 4.28 us/step -- kept at 4 (the 1% of 3 is within run-to-run spread)
 #define AMBER_SIR_MINB (1024 / AMBER_SIR_PT)
 #endif
 constexpr int kSirMinB = AMBER_SIR_MINB;  // min resident blocks per SM (register cap 64 at 256 threads)
