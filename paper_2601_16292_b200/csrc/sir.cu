@@ -278,8 +278,6 @@ struct SirStepArgs {
     uint32_t* queue;         // persistent launch: [2 parities][2 phases][kRegions] chunk counters
     int grab;                // chunks per queue grab
     int dir;                 // 0: direction-optimizing; 1: pull only; 2: push whenever possible (tests, probes)
-    const uint32_t* hits;    // sharded push step: the local words of the step's hit bitmap (S agents a
-                             // pusher infected); the pull kernel then only finalises (no row walk)
 };
 
 constexpr int kRegions = 16;
@@ -555,7 +553,6 @@ __device__ __forceinline__ void pull_load(const SirStepArgs& a, int64_t a0, cons
     const int64_t i0 = a0 + APL * lane;
     p.ws = sb[(a0 >> 5) + ((APL * lane) >> 5)];
     p.wi = ib[((a.gid0 + static_cast<unsigned long long>(a0)) >> 5) + ((APL * lane) >> 5)];
-    if (a.hits) return;  // sharded push step: finalise only, no row walk (rows unused)
     if constexpr (APL == 4) {
         if (i0 + 4 <= a.n) {
             const int4 v = *reinterpret_cast<const int4*>(a.row_ptr + i0);
@@ -594,11 +591,7 @@ __device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0,
     const uint32_t nib_s = (in.ws >> ((APL * lane) & 31)) & kM & real;
     const uint32_t nib_i = (in.wi >> ((APL * lane) & 31)) & kM & real;
     uint32_t hitnib = 0;
-    if (a.hits) {
-        // sharded push step: the infections were decided by the pushers (own and
-        // other ranks', all-to-all'd into this shard's words of the hit bitmap)
-        hitnib = (a.hits[(a0 >> 5) + ((APL * lane) >> 5)] >> ((APL * lane) & 31)) & kM & nib_s;
-    } else if (__any_sync(0xffffffffu, nib_s != 0)) {
+    if (__any_sync(0xffffffffu, nib_s != 0)) {
         if (lane < APL) sm.h[wq][lane] = 0u;
         const uint32_t T = queue_owners<APL>(sm, 0, nib_s, APL * lane, in.r);
         __syncwarp();
@@ -1138,6 +1131,61 @@ __global__ void sir_shard_or_kernel(const uint32_t* __restrict__ recv, int world
     }
 }
 
+// Finalises a sharded push step from the hit bits, one bitmap word (32 agents)
+// per lane: S agents hit -> I, I agents recover with the same draws as every
+// other path (lane i & 3 of block i / 4 of the recovery stream, R4), R stays R;
+// writes the state bytes (32 per lane), the next I / S words and the step's
+// S / I / R counts (and digest).  Replaces the pull kernel's chunk machinery
+// in hits mode (r02: 47 us per rank at G = 8, V2 early steps).
+__global__ void __launch_bounds__(256) sir_shard_finalize_kernel(const SirStepArgs a, const uint32_t* __restrict__ ibl,
+                                                                 const uint32_t* __restrict__ sbl,
+                                                                 const uint32_t* __restrict__ hits, uint8_t* __restrict__ y,
+                                                                 uint32_t* __restrict__ ib_next,
+                                                                 uint32_t* __restrict__ sb_next, SirSlot* slot)
+{
+    const int64_t words = a.n_pad >> 5;
+    unsigned long long cnt[4] = {0, 0, 0, 0};
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t left = a.n - 32 * w;
+        const uint32_t real = left <= 0 ? 0u : (left >= 32 ? 0xffffffffu : ((1u << left) - 1u));
+        const uint32_t Ws = sbl[w] & real, Wi = ibl[w] & real, H = hits[w] & Ws;
+        const unsigned long long g0 = a.gid0 + 32ull * static_cast<unsigned long long>(w);  // multiple of 32
+        uint32_t rec = 0;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            if (!((Wi >> (4 * g)) & 0xfu)) continue;
+            const uint4 r = stream_block(a.key, TAG_SIR_REC, (g0 >> 2) + g, a.t0);
+            uint32_t o = 0;
+            if (r.x < a.t_gamma) o |= 1u;
+            if (r.y < a.t_gamma) o |= 2u;
+            if (r.z < a.t_gamma) o |= 4u;
+            if (r.w < a.t_gamma) o |= 8u;
+            rec |= (o & (Wi >> (4 * g))) << (4 * g);
+        }
+        const uint32_t s2 = Ws & ~H, i2 = H | (Wi & ~rec), r2 = real & ~s2 & ~i2, pad = ~real;
+        uint32_t b[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+            b[g] = spread4(i2 >> (4 * g)) * kI + spread4(r2 >> (4 * g)) * kR + spread4(pad >> (4 * g)) * kPad;
+        uint4* yv = reinterpret_cast<uint4*>(y + 32 * w);
+        yv[0] = make_uint4(b[0], b[1], b[2], b[3]);
+        yv[1] = make_uint4(b[4], b[5], b[6], b[7]);
+        ib_next[w] = i2;
+        sb_next[w] = s2;
+        cnt[0] += __popc(s2);
+        cnt[1] += __popc(i2);
+        cnt[2] += __popc(r2);
+        if (a.digest) {
+            for (uint32_t m = real; m; m &= m - 1u) {
+                const int k = __ffs(static_cast<int>(m)) - 1;
+                cnt[3] += digest_term(g0 + k, (b[k >> 2] >> (8 * (k & 3))) & 0xffu);
+            }
+        }
+    }
+    unsigned long long* const outs[4] = {&slot->S, &slot->I, &slot->R, a.digest ? &slot->digest : nullptr};
+    block_sum_atomic<4>(cnt, outs);
+}
+
 // Sharded graph slice: row offsets rebased to the shard's first arc.
 __global__ void sir_rebase_kernel(const int32_t* __restrict__ rp, int64_t cnt, int32_t base, int32_t* __restrict__ out)
 {
@@ -1464,15 +1512,23 @@ public:
             const bool push = sharded_push_now();
             SirStepArgs a = args(1);
             a.ib[cur] = ib_glob.p;  // read: global bits of state t; write: local bits of t+1
+            if (push) push_phase();
             if (push) {
-                push_phase();
-                a.hits = hg.p + lo / 32;  // the step only finalises from the hit bits
+                const int fb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(npl / 32, 256),
+                                                                                        rt.num_sms * 8)));
+                prof.launch(rt.stream, "sir_shard_finalize", [&] {
+                    sir_shard_finalize_kernel<<<fb, 256, 0, rt.stream>>>(a, ib[cur].p, sb[cur].p, hg.p + lo / 32,
+                                                                         x[cur ^ 1].p, ib[cur ^ 1].p, sb[cur ^ 1].p,
+                                                                         ring.p + (t % metrics_cap));
+                });
+                check_launch("sir_shard_finalize_kernel");
+            } else {
+                const int L = lanes_apl();
+                int blocks = static_cast<int>(std::max<int64_t>(1, ceil_div(sir_chunks(npl, L), std::max(1, threads / 32))));
+                if (grid) blocks = static_cast<int>(grid);
+                prof.launch(rt.stream, "sir_shard_step", [&] { launch_step(L, blocks, threads, a); });
+                check_launch("sir_step_kernel");
             }
-            const int L = lanes_apl();
-            int blocks = static_cast<int>(std::max<int64_t>(1, ceil_div(sir_chunks(npl, L), std::max(1, threads / 32))));
-            if (grid) blocks = static_cast<int>(grid);
-            prof.launch(rt.stream, push ? "sir_shard_finalize" : "sir_shard_step", [&] { launch_step(L, blocks, threads, a); });
-            check_launch("sir_step_kernel");
             cur ^= 1;
             ++t;
             gather_bits(cur);
