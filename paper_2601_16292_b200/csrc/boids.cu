@@ -1033,9 +1033,13 @@ __global__ void slab_halo_kernel(const float4* __restrict__ st, const int32_t* _
 }
 
 // Local column-major cell of an own agent (local column 1..w) or a halo agent (0 / w + 1).
+// The slab grid is column-major with each cell column split into sub-rows of
+// height cs / sy in y (BoidsArgs sx / ncx / inv_csx carry sy / ny / ny / L here,
+// cell_x of the y coordinate): a stencil run spans (2 + 1 / sy) cs in y
+// instead of 3 cs -- the y counterpart of the one-GPU grid's x-subdivision.
 __device__ __forceinline__ int slab_cell(float4 x, int lcol, const BoidsArgs& a)
 {
-    return lcol * a.nc + cell_coord(x.y, a);
+    return lcol * a.ncx + cell_x(x.y, a);
 }
 
 __global__ void slab_count_kernel(const float4* __restrict__ st, int64_t n_own, const BoidAgent* __restrict__ halo,
@@ -1116,22 +1120,24 @@ __global__ void __launch_bounds__(256, 4) slab_step_kernel(const float4* __restr
                 }
                 if (q < e) boid_accumulate<false>(sorted[q], me, L, halfL, R2, rs2, acc);
             };
-            const int lc = cell_coord(me.x, a) - g.c_lo + 1, cy = cell_coord(me.y, a);
+            const int lc = cell_coord(me.x, a) - g.c_lo + 1;
+            const int sy = a.sx, ny = a.ncx, hy = cell_x(me.y, a);  // y sub-row (slab_cell)
             const int w = g.c_hi - g.c_lo;
             const bool xwrap = (g.c_lo == 0 && lc <= 1) || (g.c_hi == a.nc && lc >= w);
-            const bool inner = a.nc >= 5 && !xwrap && cy >= 1 && cy + 1 < a.nc;
+            const bool yin = hy >= sy && hy + sy < ny;
+            const bool inner = a.nc >= 5 && !xwrap && yin;
 #pragma unroll 1
             for (int dc = -1; dc <= 1; ++dc) {
-                const int colb = (lc + dc) * a.nc;
+                const int colb = (lc + dc) * ny;
                 if (inner) {
-                    run_in(start[colb + cy - 1], start[colb + cy + 2]);
-                } else if (cy >= 1 && cy + 1 < a.nc) {
-                    run(start[colb + cy - 1], start[colb + cy + 2]);
+                    run_in(start[colb + hy - sy], start[colb + hy + sy + 1]);
+                } else if (yin) {
+                    run(start[colb + hy - sy], start[colb + hy + sy + 1]);
                 } else {
 #pragma unroll 1
-                    for (int dy = -1; dy <= 1; ++dy) {
-                        int yy = cy + dy;
-                        yy = yy < 0 ? yy + a.nc : (yy >= a.nc ? yy - a.nc : yy);
+                    for (int dy = -sy; dy <= sy; ++dy) {
+                        int yy = hy + dy;
+                        yy = yy < 0 ? yy + ny : (yy >= ny ? yy - ny : yy);
                         run(start[colb + yy], start[colb + yy + 1]);
                     }
                 }
@@ -1660,16 +1666,21 @@ public:
         AMBER_REQUIRE(nc >= 3 && nc >= rt.world, "sharded Boids needs >= 3 cells per side and >= 1 cell column per rank");
         ba.nc = static_cast<int>(nc);
         ba.inv_cs = static_cast<float>(ba.nc / static_cast<double>(p.L));
-        ba.ncx = ba.nc;  // the slabs keep square cells (column-major local grid)
-        ba.inv_csx = ba.inv_cs;
-        ba.sx = 1;
+        // sub-rows in y (slab_cell): sy = AMBER_BOIDS_SX, default 4 above 2^22
+        // agents (as the one-GPU grid's x columns), 1 below
+        const char* sye = getenv("AMBER_BOIDS_SX");
+        int sy = n > (1ll << 22) ? 4 : 1;
+        if (sye && *sye) sy = std::max(1, std::min(16, std::atoi(sye)));
+        ba.sx = sy;
+        ba.ncx = ba.nc * sy;
+        ba.inv_csx = static_cast<float>(ba.ncx / static_cast<double>(p.L));
         boids_derived(ba);
         col0.resize(rt.world + 1);
         for (int q = 0; q <= rt.world; ++q) col0[q] = static_cast<int>(static_cast<int64_t>(q) * ba.nc / rt.world);
         c_lo = col0[rt.rank];
         c_hi = col0[rt.rank + 1];
         w = c_hi - c_lo;
-        ncell_loc = (w + 2) * ba.nc;
+        ncell_loc = (w + 2) * ba.ncx;
         d_col0.allocate(&rt, rt.world + 1);
         AMBER_CUDA(cudaMemcpyAsync(d_col0.p, col0.data(), col0.size() * sizeof(int), cudaMemcpyHostToDevice, rt.stream));
         cap = n;  // per-destination send capacity: any distribution of the agents fits
@@ -1780,8 +1791,8 @@ public:
             check_launch("slab_scatter_kernel");
             // 4) the step of the own agents: sorted[start[nc], start[(w + 1) nc])
             int own_rng[2] = {0, 0};
-            AMBER_CUDA(cudaMemcpyAsync(&own_rng[0], start.p + ba.nc, 4, cudaMemcpyDeviceToHost, rt.stream));
-            AMBER_CUDA(cudaMemcpyAsync(&own_rng[1], start.p + (w + 1) * ba.nc, 4, cudaMemcpyDeviceToHost, rt.stream));
+            AMBER_CUDA(cudaMemcpyAsync(&own_rng[0], start.p + ba.ncx, 4, cudaMemcpyDeviceToHost, rt.stream));
+            AMBER_CUDA(cudaMemcpyAsync(&own_rng[1], start.p + (w + 1) * ba.ncx, 4, cudaMemcpyDeviceToHost, rt.stream));
             rt.sync();
             AMBER_REQUIRE(own_rng[1] - own_rng[0] == n_own, "sharded Boids: own agents outside the slab columns");
             const int gsteps = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_own * 4, 256),

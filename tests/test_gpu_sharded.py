@@ -315,6 +315,22 @@ def test_sharded_boids_equals_oracle(orc, world):
     assert all(d == one.digest("pos_x") for d in dg)
 
 
+@pytest.mark.parametrize("world,sy", [(2, 4), (3, 3), (5, 2)])
+def test_sharded_boids_y_subrows_equal_oracle(orc, monkeypatch, world, sy):
+    # y sub-rows of the slab grid (AMBER_BOIDS_SX; default 4 above 2^22 agents):
+    # shorter stencil runs, same neighbours -> bit-identical, incl. wrapped rows
+    monkeypatch.setenv("AMBER_BOIDS_SX", str(sy))
+    cfg = dict(n=6000, L=200.0, R=10.0, rs=2.0, wc=0.01, wa=0.125, ws=0.05, vmax=2.0, dt=1.0, seed=3)
+    steps = 20
+    P = orc.boids_params(**{k: cfg[k] for k in BKEYS})
+    ref = orc.boids_run(orc.boids_init(cfg["n"], cfg["L"], cfg["seed"]), P, steps)
+    ms = sharded_boids(world, cfg)
+    par(ms, lambda m: (m.step(3), m.step(steps - 3)))
+    for a, b in zip(boids_state(ms), ref[0]):
+        assert np.array_equal(a.view(np.uint32), np.asarray(b, np.float32).view(np.uint32))
+    assert sum(par(ms, lambda m: m.get_option("own_agents"))) == cfg["n"]
+
+
 def test_sharded_boids_column_write_and_single_rank_nccl(orc, monkeypatch):
     cfg = dict(n=3000, L=150.0, R=10.0, rs=2.0, wc=0.01, wa=0.125, ws=0.05, vmax=2.0, dt=1.0, seed=9)
     one = Model("boids", cfg["n"], boids_params(*[cfg[k] for k in BKEYS]), cfg["seed"])
