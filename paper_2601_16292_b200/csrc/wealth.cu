@@ -247,15 +247,20 @@ __device__ __forceinline__ void remote_flush(const WealthArgs& a, RemoteStage& s
 #if AMBER_WEALTH_STAGE_RANK
     st.cnt[wq][lane] = 0u;  // the next batch ranks from zero (read above, before the stores below)
 #endif
-    if (c) st.base[wq][lane] = atomicAdd(a.remote_count + (static_cast<unsigned long long>(lane) * kRemoteSlices + sl) *
-                                                             kCountStride, c);
+    if (c) {
+        // the batch's first element index in remote_ids (< world * kRemoteSlices *
+        // remote_cap, which is < 2^32 for the sharded id range)
+        const unsigned long long bucket = static_cast<unsigned long long>(lane) * kRemoteSlices + sl;
+        const unsigned b0 = atomicAdd(a.remote_count + bucket * kCountStride, c);
+        AMBER_DCHECK(static_cast<unsigned long long>(b0) + c <= a.remote_cap, "wealth: remote bucket slice overflow");
+        st.base[wq][lane] = static_cast<unsigned long long>(b0) + c <= a.remote_cap
+                                ? static_cast<unsigned>(bucket * a.remote_cap + b0)
+                                : 0xffffffffu;  // impossible by the slice capacity; drop rather than overrun
+    }
     __syncwarp();
     for (unsigned e = lane; e < qn; e += 32) {
-        const unsigned mt = st.meta[wq][e], d = mt >> 10;
-        const unsigned long long pos = static_cast<unsigned long long>(st.base[wq][d]) + (mt & 1023u);
-        AMBER_DCHECK(pos < a.remote_cap, "wealth: remote bucket slice overflow");
-        if (pos < a.remote_cap)
-            a.remote_ids[(static_cast<unsigned long long>(d) * kRemoteSlices + sl) * a.remote_cap + pos] = st.id[wq][e];
+        const unsigned mt = st.meta[wq][e], b = st.base[wq][mt >> 10];
+        if (b != 0xffffffffu) a.remote_ids[b + (mt & 1023u)] = st.id[wq][e];
     }
     __syncwarp();  // the stage is rewritten by the next batch
     qn = 0;
