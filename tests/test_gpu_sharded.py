@@ -88,6 +88,34 @@ def test_sharded_wealth_bucket_slices(orc, monkeypatch, world, n, mode):
         assert np.array_equal(tt, tot)
 
 
+@pytest.mark.parametrize("world,mode", [(8, "p2p"), (2, "nccl")])
+def test_sharded_c4_full_size_vs_oracle_golden(monkeypatch, world, mode):
+    # BASELINE config 4 at full size (N = 1e8) sharded over `world` virtual ranks:
+    # the first 40 steps' global digest / total / active against the oracle-written
+    # golden (tests/golden/c4_wealth_oracle.txt) -- real bucket sizes, slices shared
+    # by ~380 warp chunks each, staged flushes, both transports
+    import os
+    from paper_2601_16292_b200.workloads import C4_WEALTH_SCALE as cfg
+    path = os.path.join(os.path.dirname(__file__), "golden", "c4_wealth_oracle.txt")
+    if not os.path.exists(path):
+        pytest.skip("golden file not generated (tools/make_oracle_goldens.py c4)")
+    rows = [[int(x) for x in ln.split()] for ln in open(path) if not ln.startswith("#")]
+    if mode == "nccl":
+        monkeypatch.setenv("AMBER_WEALTH_EXCHANGE", "nccl")
+    steps = 40
+    ms = sharded(world, cfg["n"], cfg["seed"])
+    for m in ms:
+        m.set_option("digest", 1)
+    par(ms, lambda m: (m.step(7), m.step(steps - 7)))
+    for dg in par(ms, lambda m: m.metrics("digest")):
+        assert [int(x) for x in dg] == [r[1] for r in rows[:steps]]
+    for tt in par(ms, lambda m: m.metrics("total_wealth")):
+        assert [int(x) for x in tt] == [r[2] for r in rows[:steps]]
+    for aa in par(ms, lambda m: m.metrics("active")):
+        assert [int(x) for x in aa] == [r[3] for r in rows[:steps]]
+    par(ms, lambda m: m.close())
+
+
 @pytest.mark.parametrize("mode", ["p2p", "nccl"])
 def test_sharded_wealth_exchange_modes(orc, monkeypatch, mode):
     # p2p (default): owners read the peers' buckets in place after a stream-ordered
