@@ -250,6 +250,27 @@ def test_sharded_sir_push_equals_oracle(orc, world, direction):
         assert np.array_equal(v, dig.astype(np.uint64))
 
 
+def test_sharded_v2_full_size_vs_oracle_golden():
+    # the V2 variant (SIR on G(1e8, 5e8)) sharded over 8 virtual ranks with the
+    # direction rule (push steps through the hit-bitmap exchange, then pull):
+    # per-step global S, I, R and the final state digest against the
+    # oracle-written golden (tests/golden/v2_sir_oracle.txt)
+    import os
+    from paper_2601_16292_b200.workloads import V2_SIR_SCALE as cfg
+    path = os.path.join(os.path.dirname(__file__), "golden", "v2_sir_oracle.txt")
+    if not os.path.exists(path):
+        pytest.skip("golden file not generated (tools/make_oracle_goldens.py v2)")
+    lines = [ln.split() for ln in open(path) if not ln.startswith("#")]
+    want = np.array([[int(v) for v in ln] for ln in lines[1:]], dtype=np.uint64)
+    ms = sharded_sir(8, cfg)
+    par(ms, lambda m: (m.step(3), m.step(cfg["steps"] - 3)))
+    for k, name in enumerate("SIR"):
+        for v in par(ms, lambda m: m.metrics(name)):
+            assert np.array_equal(v.astype(np.uint64), want[:, 1 + k]), name
+    assert all(d == int(want[-1, 4]) for d in par(ms, lambda m: m.digest("state")))
+    par(ms, lambda m: m.close())
+
+
 def test_sharded_sir_local_rows_and_column_write(orc):
     cfg = dict(n=20_000, mean_degree=6.0, beta=0.1, gamma=0.2, init_frac=0.005, seed=11)
     full = Model("sir", cfg["n"], sir_params(cfg["mean_degree"], cfg["beta"], cfg["gamma"], cfg["init_frac"]),
