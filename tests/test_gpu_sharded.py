@@ -380,6 +380,24 @@ def test_sharded_boids_y_subrows_equal_oracle(orc, monkeypatch, world, sy):
     assert sum(par(ms, lambda m: m.get_option("own_agents"))) == cfg["n"]
 
 
+def test_sharded_boids_large_equals_one_gpu(monkeypatch):
+    # 2e6 agents at the V3 density over 4 slabs with y sub-rows against the
+    # one-GPU model with x-subdivided rows (itself bit-exact vs the oracle in
+    # test_gpu_boids.py): every position/velocity bit-identical after 6 steps
+    monkeypatch.setenv("AMBER_BOIDS_SX", "4")
+    n = 2_000_000
+    cfg = dict(n=n, L=float(np.sqrt(n / 0.1)), R=10.0, rs=2.0, wc=0.01, wa=0.125, ws=0.05, vmax=2.0, dt=1.0, seed=9)
+    one = Model("boids", n, boids_params(*[cfg[k] for k in BKEYS]), cfg["seed"])
+    one.step(6)
+    want = [one.read_column(c) for c in ("pos_x", "pos_y", "vel_x", "vel_y")]
+    ms = sharded_boids(4, cfg)
+    par(ms, lambda m: (m.step(2), m.step(4)))
+    for a, b in zip(boids_state(ms), want):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    par(ms, lambda m: m.close())
+    one.close()
+
+
 def test_sharded_boids_column_write_and_single_rank_nccl(orc, monkeypatch):
     cfg = dict(n=3000, L=150.0, R=10.0, rs=2.0, wc=0.01, wa=0.125, ws=0.05, vmax=2.0, dt=1.0, seed=9)
     one = Model("boids", cfg["n"], boids_params(*[cfg[k] for k in BKEYS]), cfg["seed"])
