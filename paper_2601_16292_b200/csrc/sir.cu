@@ -281,6 +281,11 @@ struct SirStepArgs {
 };
 
 constexpr int kRegions = 16;
+#ifndef AMBER_SIR_COL_LD
+// column loads of the step walks: streamed (evict-first).  r02 V2 A/B
+// (tools/v2_run.py): __ldcs 1.268 / __ldg 1.278 / __ldcg 1.277 / __ldca 1.28-1.37 ms/step
+#define AMBER_SIR_COL_LD __ldcs
+#endif
 #ifndef AMBER_SIR_WALK_U
 #define AMBER_SIR_WALK_U 4
 #endif
@@ -605,7 +610,7 @@ __device__ __forceinline__ void sir_pull_chunk(const SirStepArgs& a, int64_t a0,
             const uint32_t hit = walk_rows_pay<kWalkU, APL == 8>(
                 [&](int32_t e) {
                     AMBER_DCHECK(e >= 0 && e < a.row_ptr[a.n], "SIR pull: arc index out of the CSR");
-                    return static_cast<uint32_t>(__ldcs(a.col + e));
+                    return static_cast<uint32_t>(AMBER_SIR_COL_LD(a.col + e));
                 }, own, rb, re, sid,
                 [&](uint32_t j) { return static_cast<uint32_t>(bit_of(ib, j)); },  // j: global id (global bitmap)
                 [&](uint32_t j, int32_t, int, uint32_t s) {
@@ -722,7 +727,7 @@ __device__ __forceinline__ void sir_push_body(const SirStepArgs& a, int c, uint3
         const uint32_t own = nown >= 32 ? 0xffffffffu : ((1u << nown) - 1u);
         walk_rows_pay<kWalkU, APL == 8>([&](int32_t e) {
                                   AMBER_DCHECK(e >= 0 && e < a.row_ptr[a.n], "SIR push: arc index out of the CSR");
-                                  return static_cast<uint32_t>(__ldcs(a.col + e));
+                                  return static_cast<uint32_t>(AMBER_SIR_COL_LD(a.col + e));
                               }, own, rb, re, id,
                               [&](uint32_t j) {
                                   AMBER_DCHECK(j < static_cast<uint64_t>(a.n), "SIR push: neighbour id >= n");
