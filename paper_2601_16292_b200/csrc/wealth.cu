@@ -74,6 +74,8 @@ struct WealthArgs {
     int world;
     unsigned long long shard_size;
     uint32_t shard_magic;             // 0xFFFFFFFF / shard_size (dest_of: no 64-bit division)
+    unsigned long long slo, slim;     // non-REMOTE scatter: counter index = receiver - slo, < slim (the
+                                      // shard: lo / n_loc; the dense exchange: 0 / N, global counters)
     uint32_t* remote_ids;             // [world][kRemoteSlices][remote_cap] global receiver ids
     unsigned int* remote_count;       // [world][kRemoteSlices] cursors, kCountStride words apart
     unsigned long long remote_cap;    // ids per slice
@@ -283,6 +285,8 @@ __global__ void __launch_bounds__(256, REMOTE ? AMBER_WEALTH_MINB_REMOTE : AMBER
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     const unsigned long long pol = policy_evict_last();
     const Id lo = static_cast<Id>(a.lo), n_loc = static_cast<Id>(a.n_loc);
+    const Id slo = REMOTE ? lo : static_cast<Id>(a.slo);
+    const unsigned long long slim = REMOTE ? a.n_loc : a.slim;
     const unsigned long long m = a.n_glob - (a.exclude_self ? 1 : 0);
     unsigned long long tot = 0, dig = 0;
     uint32_t act = 0, sent = 0, got = 0;
@@ -345,13 +349,13 @@ __global__ void __launch_bounds__(256, REMOTE ? AMBER_WEALTH_MINB_REMOTE : AMBER
                         const bool s = v[2 * p + h] >= a.amount;
                         const Id i = i0 + 2 * p + h;
                         const Id r = static_cast<Id>(receiver<FAST32>(lane64_of(x, h), i, m, a.exclude_self));
-                        const Id rl = r - lo;
+                        const Id rl = r - slo;
                         bool local = s;
                         if constexpr (REMOTE) local = s && rl < n_loc;
 #ifndef AMBER_EXPERIMENT_NO_RED
-                        if (local) add_count<B>(a.inc_next, rl, pol, n_loc);
+                        if (local) add_count<B>(a.inc_next, rl, pol, slim);
 #else
-                        if (local && rl == ~Id(0)) add_count<B>(a.inc_next, rl, pol, n_loc);  // never: cost without REDs
+                        if (local && rl == ~Id(0)) add_count<B>(a.inc_next, rl, pol, slim);  // never: cost without REDs
 #endif
                         sent += local;
                         if constexpr (REMOTE) {
@@ -554,6 +558,29 @@ __global__ void wealth_recv_p2p_kernel(const unsigned long long* __restrict__ pe
     block_sum_atomic<1>(vals, outs);
 }
 
+// Dense exchange (AMBER_WEALTH_EXCHANGE=dense): every rank's fused step adds
+// ALL its transfers into its own packed counters over the whole population
+// (global index, no remote staging); after the barrier the owner sums the
+// peers' packed words of its shard (plain 32-bit adds of the packed words: a
+// carry shows up as a lower decoded total, caught by the global sent/got
+// check) into its own counters, and zeroes its own other-parity global
+// counters (last read by the owners before this barrier, next written by the
+// next step).  peer_base[p] + dense_off = rank p's global counters of this parity.
+__global__ void wealth_recv_dense_kernel(const unsigned long long* __restrict__ peer_base, int world,
+                                         size_t dense_off, size_t word0, size_t words, uint32_t* __restrict__ inc_own,
+                                         uint4* __restrict__ zero_own, size_t zero_n)
+{
+    const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+    for (size_t w = tid; w < words; w += nt) {
+        uint32_t v = 0;
+        for (int p = 0; p < world; ++p)
+            v += __ldcg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const unsigned char*>(peer_base[p]) + dense_off) +
+                        word0 + w);
+        inc_own[w] = v;
+    }
+    for (size_t z = tid; z < zero_n; z += nt) zero_own[z] = make_uint4(0u, 0u, 0u, 0u);
+}
+
 // Sliced buckets -> contiguous per-destination blocks for the transports that
 // ship one block per destination (NCCL send/recv, loopback and host-collective
 // copies): block (x, p) copies slice x of destination p behind the slices
@@ -648,6 +675,11 @@ public:
     DevBuf<unsigned long long> recv_total;
     uint64_t send_cap = 0;    // ids per destination region (kRemoteSlices slices) and per compacted block
     uint64_t slice_cap = 0;   // ids per slice: every agent of the slice's warp chunks
+    // dense exchange (AMBER_WEALTH_EXCHANGE=dense, P2P only): global packed counters
+    // per parity inside the peer-mapped block
+    bool dense_mode = false;
+    size_t dense_off[2] = {0, 0}, dense_words = 0;
+    DevBuf<unsigned long long> dsum;   // verify(): global sent / got sums
     DevBuf<uint32_t> cmp_ids;          // compacted per-destination blocks (non-P2P transports)
     DevBuf<unsigned int> cmp_counts;
 
@@ -702,8 +734,13 @@ public:
             recv_ids.allocate(&rt, static_cast<size_t>(shard) * rt.world + 1);
             send_counts.allocate(&rt, static_cast<int64_t>(rt.world) * kRemoteSlices * kCountStride);
             send_counts.zero_async(rt.stream);
+            // AMBER_WEALTH_EXCHANGE: "dense" / "sparse" (P2P), "nccl"; default: P2P, dense
+            // up to 8 ranks (one box; per-rank phases measured on one B200, DESIGN 7),
+            // sparse buckets above (the dense payload does not shrink with the ranks)
             const char* mode = getenv("AMBER_WEALTH_EXCHANGE");
-            p2p_wanted = !(mode && std::string(mode) == "nccl");  // mapped at the first exchange (collective)
+            const std::string ms = mode ? mode : "";
+            p2p_wanted = ms != "nccl";  // mapped at the first exchange (collective)
+            dense_mode = rt.world > 1 && (ms == "dense" || (ms.empty() && rt.world <= 8));
             recv_total.allocate(&rt, 1);
         }
         rt.sync();
@@ -720,11 +757,19 @@ public:
         p2p_cnt_off[1] = cbytes;
         p2p_ids_off[0] = 2 * cbytes;
         p2p_ids_off[1] = 2 * cbytes + ibytes;
-        if (cudaMalloc(&p2p_block, 2 * cbytes + 2 * ibytes) != cudaSuccess) {
+        // dense exchange: global packed counters (all N agents, B bits) per parity
+        dense_words = dense_mode ? static_cast<size_t>(ceil_div(static_cast<int64_t>(rt.world) * shard * B, 32) + 8) : 0;
+        dense_words = (dense_words + 3) / 4 * 4;  // whole uint4s (zeroing)
+        dense_off[0] = 2 * cbytes + 2 * ibytes;
+        dense_off[1] = dense_off[0] + dense_words * 4;
+        const size_t total = 2 * cbytes + 2 * ibytes + 2 * dense_words * 4;
+        if (cudaMalloc(&p2p_block, total) != cudaSuccess) {
             cudaGetLastError();
             p2p_block = nullptr;
         }
-        AMBER_CUDA(cudaMemsetAsync(p2p_block, 0, 2 * cbytes, rt.stream));
+        if (p2p_block) AMBER_CUDA(cudaMemsetAsync(p2p_block, 0, 2 * cbytes, rt.stream));
+        if (p2p_block && dense_words)
+            AMBER_CUDA(cudaMemsetAsync(static_cast<char*>(p2p_block) + dense_off[0], 0, 2 * dense_words * 4, rt.stream));
         rt.sync();
         std::vector<void*> peers;
         if (p2p_block && wealth_p2p_open(xch, rt, p2p_block, peers)) {
@@ -740,6 +785,7 @@ public:
         }
     }
 
+    uint32_t* dense_ctr(int par) { return reinterpret_cast<uint32_t*>(static_cast<char*>(p2p_block) + dense_off[par]); }
     unsigned int* p2p_counts(int par) { return reinterpret_cast<unsigned int*>(static_cast<char*>(p2p_block) + p2p_cnt_off[par]); }
     uint32_t* p2p_ids(int par) { return reinterpret_cast<uint32_t*>(static_cast<char*>(p2p_block) + p2p_ids_off[par]); }
 
@@ -760,6 +806,7 @@ public:
         recv_total.reset();
         cmp_ids.reset();
         cmp_counts.reset();
+        dsum.reset();
         rt.destroy();
     }
 
@@ -832,10 +879,21 @@ public:
         a.slot_apply = apply ? slot(ta) : nullptr;
         a.slot_scatter = scatter ? slot(ts) : nullptr;
         a.slot_zero = (apply && scatter) ? slot(ta + 2) : nullptr;
-        const bool remote = xch != nullptr && scatter;
+        a.slo = static_cast<unsigned long long>(lo);
+        a.slim = static_cast<unsigned long long>(n_loc);
+        bool remote = xch != nullptr && scatter;
         if (remote && p2p_wanted) {  // collective: every rank reaches its first exchange here
             p2p_wanted = false;
             setup_p2p();
+        }
+        const bool dense = remote && p2p && dense_mode && !exact;
+        if (dense) {
+            // all transfers into this rank's global counters of the scattered step's
+            // parity (zeroed by the owner pass of the step before); no remote staging
+            remote = false;
+            a.inc_next = dense_ctr(ts & 1);
+            a.slo = 0;
+            a.slim = static_cast<unsigned long long>(rt.world) * static_cast<unsigned long long>(shard);
         }
         if (remote) {
             a.world = rt.world;
@@ -863,6 +921,24 @@ public:
             default: launch_b<32>(a, apply, scatter, dig, remote); break;
         }
         if (remote) exchange(bits, exact, ts);
+        if (dense) exchange_dense(bits, ts);
+    }
+
+    // Dense exchange of step ts: after the barrier, this rank's counters of ts =
+    // the sum of every rank's global counters over its shard (read in place over
+    // the peer mappings); its own other-parity global counters are zeroed.
+    void exchange_dense(int bits, int64_t ts)
+    {
+        wealth_p2p_barrier(xch, rt);
+        const size_t word0 = static_cast<size_t>(lo) * bits / 32;
+        const size_t words = static_cast<size_t>(ceil_div(n_loc * bits, 32));
+        const int g = rt.num_sms * 4;
+        prof.launch(rt.stream, "wealth_recv_dense", [&] {
+            wealth_recv_dense_kernel<<<g, 256, 0, rt.stream>>>(p2p_peers.p, rt.world, dense_off[ts & 1], word0, words,
+                                                               inc[ts & 1].p, reinterpret_cast<uint4*>(dense_ctr((ts + 1) & 1)),
+                                                               dense_words / 4);
+        });
+        check_launch("wealth_recv_dense_kernel");
     }
 
     // Cross-shard step: ship remote receivers to their owners, add them to the
@@ -1018,11 +1094,27 @@ public:
         }
         const Slot* h = fetch_slots(win_start, t);
         bool bad = false;
-        for (int64_t s = win_start; s < t; ++s) {
-            const Slot& x = h[s % metrics_cap];
-            if (x.sent != x.got) bad = true;
+        if (dense_mode && p2p) {
+            // dense exchange: a rank's increments land on other ranks' agents, so
+            // only the global totals match (a carry lowers the decoded total)
+            unsigned long long v[2] = {0, 0};
+            for (int64_t s = win_start; s < t; ++s) {
+                v[0] += h[s % metrics_cap].sent;
+                v[1] += h[s % metrics_cap].got;
+            }
+            if (!dsum.p) dsum.allocate(&rt, 2);
+            AMBER_CUDA(cudaMemcpyAsync(dsum.p, v, sizeof(v), cudaMemcpyHostToDevice, rt.stream));
+            wealth_exchange_allreduce_u64(xch, rt, dsum.p, 2);
+            AMBER_CUDA(cudaMemcpyAsync(v, dsum.p, sizeof(v), cudaMemcpyDeviceToHost, rt.stream));
+            rt.sync();
+            bad = v[0] != v[1];
+        } else {
+            for (int64_t s = win_start; s < t; ++s) {
+                const Slot& x = h[s % metrics_cap];
+                if (x.sent != x.got) bad = true;
+            }
+            if (xch) bad = wealth_exchange_any(xch, rt, bad);
         }
-        if (xch) bad = wealth_exchange_any(xch, rt, bad);
         if (bad) replay(win_start, t);
         win_start = -1;
         pinned = -1;
@@ -1041,6 +1133,8 @@ public:
         ring.zero_async(rt.stream);
         if (xch) send_counts.zero_async(rt.stream);
         if (p2p) AMBER_CUDA(cudaMemsetAsync(p2p_block, 0, p2p_ids_off[0], rt.stream));
+        if (p2p && dense_words)
+            AMBER_CUDA(cudaMemsetAsync(dense_ctr(0), 0, 2 * dense_words * 4, rt.stream));
         for (int64_t s = s0; s < s1; ++s) {
             if (s == s0) launch(32, true, false, true, s, s, cur, cur);
             const int dst = other(cur, -1);
@@ -1190,8 +1284,8 @@ public:
             *v = B;
             return true;
         }
-        if (k == "exchange") {  // 0: none (one rank), 1: NCCL send/recv, 2: P2P (peer-mapped buckets)
-            *v = xch ? (p2p ? 2 : 1) : 0;
+        if (k == "exchange") {  // 0: none (one rank), 1: NCCL send/recv, 2: P2P (peer-mapped buckets), 3: dense
+            *v = xch ? (p2p ? (dense_mode ? 3 : 2) : 1) : 0;
             return true;
         }
         if (k == "scatter") {  // 1: packed-counter L2 atomics (the one shipped scatter)

@@ -16,6 +16,19 @@ from paper_2601_16292_b200 import Model, boids_params, loopback_id, shard_range,
 from paper_2601_16292_b200.workloads import C5_SWEEP, sweep_replicates
 
 
+@pytest.fixture(autouse=True)
+def _release_device_memory():
+    # the models allocate through torch's caching allocator: return the cached
+    # blocks after each test, so the full-size tests (8 ranks x N = 1e8 wealth,
+    # 8 graph builds of 1e9 arcs) do not meet a fragmented cache
+    yield
+    import gc
+
+    import torch
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
 def oracle_graph(orc, cfg, m=None):
     """The ORACLE's G(n, M) (orc_er_graph); when a one-GPU model is given, its
     CSR must equal it.  The oracle is never stepped on a device-built graph."""
@@ -71,13 +84,12 @@ def test_sharded_wealth_equals_oracle(orc, world, n):
     assert all(d == orc.digest(ref) for d in dg)
 
 
-@pytest.mark.parametrize("world,n,mode", [(2, 3_000_017, "p2p"), (3, 2_000_003, "nccl"), (33, 50_021, "p2p")])
+@pytest.mark.parametrize("world,n,mode", [(2, 3_000_017, "sparse"), (3, 2_000_003, "nccl"), (33, 50_021, "sparse")])
 def test_sharded_wealth_bucket_slices(orc, monkeypatch, world, n, mode):
     # many warp chunks per bucket slice (> 64 chunks per rank: slices shared by
     # several chunks, cursors accumulating), both transports; world > 32 takes the
     # direct (unstaged) warp-aggregated append
-    if mode == "nccl":
-        monkeypatch.setenv("AMBER_WEALTH_EXCHANGE", "nccl")
+    monkeypatch.setenv("AMBER_WEALTH_EXCHANGE", mode)
     seed, steps = 19, 6
     ms = sharded(world, n, seed)
     par(ms, lambda m: (m.step(2), m.step(4)))
@@ -88,7 +100,7 @@ def test_sharded_wealth_bucket_slices(orc, monkeypatch, world, n, mode):
         assert np.array_equal(tt, tot)
 
 
-@pytest.mark.parametrize("world,mode", [(8, "p2p"), (2, "nccl")])
+@pytest.mark.parametrize("world,mode", [(8, "sparse"), (2, "nccl"), (8, "dense"), (3, "dense")])
 def test_sharded_c4_full_size_vs_oracle_golden(monkeypatch, world, mode):
     # BASELINE config 4 at full size (N = 1e8) sharded over `world` virtual ranks:
     # the first 40 steps' global digest / total / active against the oracle-written
@@ -100,8 +112,7 @@ def test_sharded_c4_full_size_vs_oracle_golden(monkeypatch, world, mode):
     if not os.path.exists(path):
         pytest.skip("golden file not generated (tools/make_oracle_goldens.py c4)")
     rows = [[int(x) for x in ln.split()] for ln in open(path) if not ln.startswith("#")]
-    if mode == "nccl":
-        monkeypatch.setenv("AMBER_WEALTH_EXCHANGE", "nccl")
+    monkeypatch.setenv("AMBER_WEALTH_EXCHANGE", mode)
     steps = 40
     ms = sharded(world, cfg["n"], cfg["seed"])
     for m in ms:
@@ -116,16 +127,19 @@ def test_sharded_c4_full_size_vs_oracle_golden(monkeypatch, world, mode):
     par(ms, lambda m: m.close())
 
 
-@pytest.mark.parametrize("mode", ["p2p", "nccl"])
+@pytest.mark.parametrize("mode", ["default", "sparse", "nccl", "dense"])
 def test_sharded_wealth_exchange_modes(orc, monkeypatch, mode):
-    # p2p (default): owners read the peers' buckets in place after a stream-ordered
+    # dense (the default up to 8 ranks): every rank counts all its transfers in
+    # global packed counters, owners sum the peers' words of their shard in place;
+    # sparse: owners read the peers' id buckets in place after a stream-ordered
     # barrier; nccl: counts + payload send/recv through the transport
-    if mode == "nccl":
-        monkeypatch.setenv("AMBER_WEALTH_EXCHANGE", "nccl")
+    if mode != "default":
+        monkeypatch.setenv("AMBER_WEALTH_EXCHANGE", mode)
     world, n, seed, steps = 4, 30_011, 21, 20
     ms = sharded(world, n, seed)
     par(ms, lambda m: (m.step(7), m.step(13)))
-    assert all(m.get_option("exchange") == (2 if mode == "p2p" else 1) for m in ms)  # mapped at the first step
+    assert all(m.get_option("exchange") == {"default": 3, "sparse": 2, "nccl": 1, "dense": 3}[mode]
+               for m in ms)  # mapped at the first step
     w = np.concatenate(par(ms, lambda m: m.read_column("wealth")))
     ref, tot, _, _ = orc.wealth_run(np.ones(n, np.int32), seed, 0, steps)
     assert np.array_equal(w, ref)
@@ -133,8 +147,10 @@ def test_sharded_wealth_exchange_modes(orc, monkeypatch, mode):
         assert np.array_equal(tt, tot)
 
 
-def test_sharded_overflow_replay_is_collective(orc):
+@pytest.mark.parametrize("mode", ["sparse", "dense"])
+def test_sharded_overflow_replay_is_collective(orc, monkeypatch, mode):
     # 2-bit counters overflow on some shard nearly every window: all shards replay
+    monkeypatch.setenv("AMBER_WEALTH_EXCHANGE", mode)
     world, n, seed, steps = 4, 40_000, 5, 12
     ms = sharded(world, n, seed, bits=2)
     par(ms, lambda m: m.step(steps))
