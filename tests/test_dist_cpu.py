@@ -125,6 +125,35 @@ def _sharded_wealth(rank, world):
     return g
 
 
+def _sharded_wealth_dense(rank, world):
+    # the dense exchange (r02 default up to 8 ranks): every rank counts ALL its
+    # transfers in a global per-agent array; each owner sums the ranks' arrays
+    # over its shard (here an all-reduce, then the own slice) and applies them;
+    # the overflow check compares the global totals of issued and decoded counts
+    import oracle
+    from paper_2601_16292_b200 import shard_range
+    n, seed, steps = 1003, 17, 6
+    lo, hi = shard_range(n, world, rank)
+    shard = ((-(-n // world) + 7) // 8) * 8
+    w = np.ones(n, np.int32)[lo:hi].copy()
+    for t in range(steps):
+        glob = np.zeros(world * shard, np.int64)
+        for k, i in enumerate(range(lo, hi)):
+            if w[k] >= 1:
+                glob[oracle.wealth_receiver(seed, n, i, t)] += 1
+        sent = int(glob.sum())
+        g = torch.tensor(glob)
+        dist.all_reduce(g)
+        inc = g.numpy()[lo:hi]
+        tot = torch.tensor([sent, int(inc.sum())], dtype=torch.int64)
+        dist.all_reduce(tot)
+        assert int(tot[0]) == int(tot[1])
+        w = (w - (w >= 1) + inc).astype(np.int32)
+    out = [None] * world
+    dist.all_gather_object(out, (lo, w.tolist()))
+    return out
+
+
 def _sharded_sir(rank, world):
     import oracle
     from paper_2601_16292_b200 import sir_shard_range
@@ -301,6 +330,14 @@ def test_nccl_unique_id_rendezvous(world):
 
 def test_max_over_ranks():
     assert run_world(2, _maxtime) == [3.0, 3.0]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_wealth_dense_exchange_equals_oracle(world, orc):
+    parts = run_world(world, _sharded_wealth_dense)[0]
+    w = np.concatenate([np.array(v, np.int32) for _, v in sorted(parts)])
+    ref = orc.wealth_run(np.ones(1003, np.int32), 17, 0, 6)[0]
+    assert np.array_equal(w, ref)
 
 
 @pytest.mark.parametrize("world", [2, 4])
