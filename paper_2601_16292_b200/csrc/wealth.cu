@@ -571,7 +571,20 @@ __global__ void wealth_recv_dense_kernel(const unsigned long long* __restrict__ 
                                          uint4* __restrict__ zero_own, size_t zero_n)
 {
     const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
-    for (size_t w = tid; w < words; w += nt) {
+    // four words per thread per round: 4 x world independent loads in flight
+    size_t w = tid;
+    for (; w + 3 * nt < words; w += 4 * nt) {
+        uint32_t v[4] = {0u, 0u, 0u, 0u};
+        for (int p = 0; p < world; ++p) {
+            const uint32_t* src =
+                reinterpret_cast<const uint32_t*>(reinterpret_cast<const unsigned char*>(peer_base[p]) + dense_off) + word0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] += __ldcg(src + w + u * nt);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) inc_own[w + u * nt] = v[u];
+    }
+    for (; w < words; w += nt) {
         uint32_t v = 0;
         for (int p = 0; p < world; ++p)
             v += __ldcg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const unsigned char*>(peer_base[p]) + dense_off) +
