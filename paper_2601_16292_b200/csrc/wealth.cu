@@ -753,7 +753,9 @@ public:
             const char* mode = getenv("AMBER_WEALTH_EXCHANGE");
             const std::string ms = mode ? mode : "";
             p2p_wanted = ms != "nccl";  // mapped at the first exchange (collective)
-            dense_mode = rt.world > 1 && (ms == "dense" || (ms.empty() && rt.world <= 8));
+            // (each shard's block of the global packed counters must start on a word:
+            // shard * B a multiple of 32 -- always for B >= 4, shards being multiples of 8)
+            dense_mode = rt.world > 1 && (ms == "dense" || (ms.empty() && rt.world <= 8)) && (shard * B) % 32 == 0;
             recv_total.allocate(&rt, 1);
         }
         rt.sync();

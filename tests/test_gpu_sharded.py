@@ -147,6 +147,18 @@ def test_sharded_wealth_exchange_modes(orc, monkeypatch, mode):
         assert np.array_equal(tt, tot)
 
 
+def test_sharded_dense_falls_back_when_blocks_straddle_words(orc, monkeypatch):
+    # 2-bit counters with shards of 8 x odd agents: a shard's block of the global
+    # packed counters would not start on a word, so the sparse buckets run instead
+    monkeypatch.setenv("AMBER_WEALTH_EXCHANGE", "dense")
+    world, n, seed, steps = 3, 70, 4, 9  # shard = 24 agents: 48 bits
+    ms = sharded(world, n, seed, bits=2)
+    par(ms, lambda m: m.step(steps))
+    assert all(m.get_option("exchange") == 2 for m in ms)
+    w = np.concatenate(par(ms, lambda m: m.read_column("wealth")))
+    assert np.array_equal(w, orc.wealth_run(np.ones(n, np.int32), seed, 0, steps)[0])
+
+
 @pytest.mark.parametrize("mode", ["sparse", "dense"])
 def test_sharded_overflow_replay_is_collective(orc, monkeypatch, mode):
     # 2-bit counters overflow on some shard nearly every window: all shards replay
