@@ -306,7 +306,10 @@ int amber_digest(amber_model* m, const char* name, uint64_t* out);
  * Read-only (amber_get_option): wealth "replays" (exact-replay count, after
  * the overflow check), "counter_bits", "scatter" (1: packed-counter L2
  * atomics, the one shipped scatter), "exchange" (sharded: 0 none,
- * 1 NCCL send/recv, 2 P2P peer-mapped buckets; set at the first step); SIR
+ * 1 NCCL send/recv, 2 P2P peer-mapped id buckets, 3 P2P dense: every rank's
+ * global packed counters summed by the owners in place; set at the first
+ * step; environment AMBER_WEALTH_EXCHANGE = dense | sparse | nccl, default
+ * dense up to 8 ranks when each shard's counter block is word-aligned); SIR
  * "edges"; Boids "cells_per_side", sharded Boids "own_agents" and
  * "slab_columns". */
 int amber_set_option(amber_model* m, const char* key, int64_t value);
